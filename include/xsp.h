@@ -1,0 +1,285 @@
+/*
+ * xsp.h — the C ABI of the B200 span-correlation / analysis hot path.
+ *
+ * This is the drop-in boundary under the reference's C++ ingest/correlate/analyze
+ * API (namespace strata in /root/reference/proj/include/strata/ *.hpp). Every entry
+ * point below names the reference interface it replaces. The ABI carries plain
+ * pointers and sizes only: span columns (structure of arrays), trace and group
+ * descriptors, and ctx-owned result columns. No C++ or torch types cross it.
+ *
+ *   reference                                   this ABI
+ *   ------------------------------------------  -------------------------------
+ *   TraceBundle / Span (span.hpp:81-171)        xsp_span_cols + trace offsets
+ *   correlate()   (correlator.hpp:164)          xsp_correlate
+ *   assign_parents + correlate_async (:154,161) (both inside xsp_correlate)
+ *   a8..a15, model_roofline (analysis.hpp:256-366) xsp_analyze
+ *   LeveledRunGroup + compute_overhead (leveled.hpp:60-109) xsp_leveled
+ *   validate_bundle (span.hpp:187)              xsp_validate
+ *   sort_timeline (span.hpp:190)                xsp_sort_timeline
+ *
+ * Ownership: the caller owns all inputs. Result columns live in ctx-owned device
+ * memory and stay valid until the next call on the same ctx or xsp_ctx_destroy.
+ * Threading: a ctx is bound to one device and is not re-entrant; use one ctx per
+ * stream/thread (distinct ctxs may run concurrently).
+ * Errors: every call returns an xsp_status; xsp_last_error(ctx) gives a one-line
+ * description. Per-trace faults of the reference (TraceError thrown by
+ * assign_parents / correlate_async) are reported per trace in
+ * xsp_corr_out.trace_status with the span rows needed to rebuild the reference's
+ * exact message text (see xsp_trace_status).
+ */
+#ifndef XSP_H
+#define XSP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XSP_ABI_VERSION 1
+
+typedef struct xsp_ctx xsp_ctx;
+typedef int32_t xsp_status;
+
+enum {
+  XSP_OK = 0,
+  XSP_E_INVALID = 1,   /* bad argument */
+  XSP_E_CUDA = 2,      /* CUDA runtime failure (message in xsp_last_error) */
+  XSP_E_NOMEM = 3,     /* device allocation failed */
+  XSP_E_UNSORTED = 4,  /* a trace is not in timeline order and sorting was disabled */
+  XSP_E_NO_DEVICE = 5  /* no CUDA device: there is no CPU fallback */
+};
+
+/* ---- span columns ------------------------------------------------------- */
+
+/* flags byte per span: bits 0-1 level (strata::Level: Model 0, Layer 1, Kernel 2,
+ * Api 3), bits 2-3 kind (strata::SpanKind: Sync 0, Launch 1, Exec 2), then the
+ * presence bits of Span's optional members and of KernelMetrics tags. */
+#define XSP_LEVEL_MODEL 0u
+#define XSP_LEVEL_LAYER 1u
+#define XSP_LEVEL_KERNEL 2u
+#define XSP_LEVEL_API 3u
+#define XSP_KIND_SYNC 0u
+#define XSP_KIND_LAUNCH 1u
+#define XSP_KIND_EXEC 2u
+#define XSP_F_PARENT 0x10u  /* parent_id present   (Span::parent_id, span.hpp:84)      */
+#define XSP_F_CID 0x20u     /* correlation_id present (span.hpp:90)                    */
+#define XSP_F_METRICS 0x40u /* metrics_from_tags() != nullopt (span.hpp:131)           */
+
+/* All spans of all traces of one call, trace after trace; rows [off[t], off[t+1])
+ * belong to trace t. Columns are indexed by span row except the two compact
+ * side tables:
+ *   metric table: one row per span with XSP_F_METRICS, in span-row order
+ *                 (the decoded KernelMetrics of span.cpp:284-296);
+ *   layer table:  one row per span with level == Layer, in span-row order
+ *                 ("alloc_bytes" tag via tag_int, "layer_type" interned,
+ *                  correlator.cpp:197-202).
+ * name_id / type_id index string tables interned in byte-lexicographic order,
+ * so id order equals std::string order (a10 / a5 sort by name). */
+typedef struct xsp_span_cols {
+  uint64_t n_spans;
+  const uint64_t* span_id;
+  const uint64_t* parent_id; /* read iff XSP_F_PARENT */
+  const uint64_t* begin_ns;
+  const uint64_t* end_ns;
+  const uint64_t* cid; /* read iff XSP_F_CID */
+  const uint8_t* flags;
+  const uint32_t* name_id;
+  uint64_t n_metric_rows;
+  const uint64_t* flops;      /* flop_count_sp */
+  const uint64_t* dram_read;  /* dram_read_bytes */
+  const uint64_t* dram_write; /* dram_write_bytes */
+  const double* occupancy;    /* achieved_occupancy */
+  uint64_t n_layer_rows;
+  const int64_t* alloc_bytes;
+  const uint32_t* type_id;
+} xsp_span_cols;
+
+/* One trace (= one TraceBundle): its span rows and RunMeta::profiling_levels
+ * as a bit mask (1 << level). */
+typedef struct xsp_traces {
+  uint32_t n_traces;
+  const uint64_t* span_off; /* [n_traces + 1] */
+  const uint32_t* levels;   /* [n_traces] */
+} xsp_traces;
+
+/* ---- correlation -------------------------------------------------------- */
+
+/* Per-trace fault codes: the TraceErrors assign_parents / correlate_async throw.
+ * err_row[2t], err_row[2t+1] name the span rows the message quotes. */
+typedef enum xsp_trace_status {
+  XSP_T_OK = 0,
+  XSP_T_NO_MODEL = 1,        /* "bundle has no model span; nothing to correlate"        (correlator.cpp:143-145) */
+  XSP_T_MULTI_MODEL = 2,     /* "bundle has more than one model span"                   (:147-150) */
+  XSP_T_SKIP_LEVEL = 3,      /* "span <id> ('<name>') is kernel-level but ..."  row a   (:151-157) */
+  XSP_T_DUP_EXEC_CID = 4,    /* "correlation id C is shared by execution spans A and B" (:296-302) */
+  XSP_T_DUP_LAUNCH_CID = 5   /* "... is shared by launch spans A and B"                 (:308-316) */
+} xsp_trace_status_code;
+
+/* Orphan reasons (OrphanSpan::reason text, correlator.cpp:168-363). */
+typedef enum xsp_orphan_reason {
+  XSP_O_LAYER_NON_SYNC = 1,        /* "layer-level span with non-sync kind" */
+  XSP_O_LAYER_BAD_PARENT = 2,      /* "explicit parent <P> is not the model span" */
+  XSP_O_LAYER_OUTSIDE_MODEL = 3,   /* "outside the model interval" */
+  XSP_O_KERNEL_BAD_PARENT = 4,     /* "explicit parent <P> is not a layer in the tree" */
+  XSP_O_KERNEL_NO_LAYER = 5,       /* "contained in no layer interval" */
+  XSP_O_EXEC_NO_CID = 6,           /* "execution record without correlation id" */
+  XSP_O_LAUNCH_NO_CID = 7,         /* "launch without correlation id" */
+  XSP_O_LAUNCH_NO_EXEC = 8,        /* "launch has no matching execution record" */
+  XSP_O_EXEC_NO_LAUNCH = 9         /* "execution record without matching launch" */
+} xsp_orphan_reason;
+
+/* Correlation result (CorrelationResult, correlator.hpp:134-137) as columns.
+ * Rows are global span rows of the input. Layers are in layer_index order
+ * (begin_ns, span_id) per trace; kernels are in tree order (layer, then launch
+ * (begin_ns, span_id)). All pointers are DEVICE pointers owned by the ctx. */
+typedef struct xsp_corr_out {
+  uint32_t n_traces;
+  uint32_t n_failed; /* traces with trace_status != XSP_T_OK */
+  uint64_t n_layers, n_kernels, n_orphans, n_ambiguities, n_candidates;
+  int32_t* trace_status;     /* [n_traces] xsp_trace_status_code */
+  uint32_t* trace_err_row;   /* [2 n_traces] */
+  uint32_t* trace_model_row; /* [n_traces] row of the model span (UINT32_MAX if none) */
+  uint32_t* trace_layer_off; /* [n_traces + 1] into layer columns */
+  uint32_t* trace_kernel_off;/* [n_traces + 1] into kernel columns */
+  uint32_t* trace_orphan_off;/* [n_traces + 1] */
+  uint32_t* trace_amb_off;   /* [n_traces + 1] */
+  /* layers (LayerExec) */
+  uint32_t* layer_row;        /* span row */
+  uint32_t* layer_kernel_off; /* [n_layers + 1] CSR into kernel columns */
+  uint64_t* layer_dur;        /* Span::duration_ns of the layer span */
+  uint32_t* layer_attr_row;   /* row of the layer table (alloc_bytes, type_id) */
+  /* kernels (KernelExec) */
+  uint32_t* kernel_launch_row;
+  uint32_t* kernel_exec_row;   /* == launch row for a synchronous kernel span */
+  uint32_t* kernel_metric_row; /* metric-table row of the exec, UINT32_MAX if none */
+  uint64_t* kernel_dur;        /* KernelExec::duration_ns (exec span) */
+  uint32_t* kernel_name;       /* KernelExec::kernel_name() name_id */
+  /* diagnostics, in the reference's output order */
+  uint32_t* orphan_row;
+  uint8_t* orphan_reason; /* xsp_orphan_reason */
+  uint32_t* amb_row;      /* ambiguities sorted by span_id */
+  uint32_t* amb_cand_off; /* [n_ambiguities + 1] */
+  uint32_t* amb_cand_row; /* candidate layer rows sorted by span_id */
+} xsp_corr_out;
+
+/* ---- analysis ------------------------------------------------------------ */
+
+typedef struct xsp_system_spec { /* SystemSpec (span.hpp:139-145) */
+  double peak_flops;
+  double memory_bandwidth_bytes_per_s;
+} xsp_system_spec;
+
+typedef struct xsp_analysis_opts { /* AnalysisOptions (analysis.hpp:47-51) */
+  double trim_fraction;   /* 0.2 */
+  double epsilon;         /* 0.05 */
+  double noise_tolerance; /* 0.01 */
+  uint32_t top_k;         /* kernels kept per layer in the top-k table (north star (e)) */
+} xsp_analysis_opts;
+
+/* One AnalysisInput (analysis.hpp:42-45): runs are the correlated traces
+ * [first_trace, first_trace + n_runs) of the xsp_corr_out. */
+typedef struct xsp_groups {
+  uint32_t n_groups;
+  const uint32_t* first_trace; /* [n_groups] */
+  const uint32_t* n_runs;      /* [n_groups] */
+  const uint32_t* batch_size;  /* [n_groups] */
+} xsp_groups;
+
+/* Optional-value encoding in the tables: std::optional<double> absent = NaN;
+ * std::optional<bool> memory_bound: -1 absent, 0 false, 1 true. */
+enum {
+  XSP_G_OK = 0,
+  XSP_G_NO_RUNS = 1,          /* "analysis input holds no runs" (analysis.cpp:103-105) */
+  XSP_G_LAYER_COUNT = 2,      /* "repetitions disagree on layer count" (:108-110) */
+  XSP_G_KERNEL_COUNT = 3,     /* "repetitions disagree on kernel count of layer <i>" (:112-115) */
+  XSP_G_TRACE_FAILED = 4,     /* a run's correlation failed (see trace_status) */
+  XSP_G_BAD_TRIM = 5          /* "trim fraction must lie in [0, 0.5)" (:30-32) */
+};
+
+/* All DEVICE pointers owned by the ctx. Kernel and layer rows follow the first
+ * run's tree order ("canonical" run of combine(), analysis.cpp:102-170). */
+typedef struct xsp_tables_out {
+  uint32_t n_groups;
+  uint64_t n_layers, n_kernels, n_names;
+  int32_t* group_status;   /* [n_groups] XSP_G_* */
+  uint32_t* group_err_arg; /* layer index for XSP_G_KERNEL_COUNT */
+  uint32_t* group_layer_off;  /* [n_groups + 1] */
+  uint32_t* group_kernel_off; /* [n_groups + 1] */
+  uint32_t* group_name_off;   /* [n_groups + 1] */
+  /* a8 / a9: KernelInfoRow per kernel (analysis.cpp:342-397) */
+  uint32_t* k_name; uint32_t* k_layer;
+  double* k_lat; uint64_t* k_flops; uint64_t* k_read; uint64_t* k_write; double* k_occ;
+  double* k_ai; double* k_tput; int8_t* k_bound;
+  uint8_t* k_roofline_in; /* a9: classify() != nullopt */
+  /* a11 / a12 / a13 / a14: per layer (analysis.cpp:437-525) */
+  uint32_t* l_index; uint32_t* l_row;
+  double* l_layer_lat; double* l_kern_lat;
+  uint64_t* l_flops; uint64_t* l_read; uint64_t* l_write; double* l_occ; uint64_t* l_count;
+  double* l_ai; double* l_tput; int8_t* l_bound;
+  double* l_nongpu; double* l_gpu_share; double* l_nongpu_share; uint8_t* l_flagged;
+  uint8_t* l_roofline_in; /* a14 */
+  uint32_t* l_topk;       /* [n_layers * top_k] kernel ordinals within the group, UINT32_MAX pad */
+  /* a10: per (group, kernel name), sorted by total latency desc, name asc */
+  uint32_t* n_name; uint64_t* n_count; double* n_lat; double* n_pct;
+  uint64_t* n_flops; uint64_t* n_read; uint64_t* n_write; double* n_occ;
+  double* n_ai; double* n_tput; int8_t* n_bound;
+  /* a15 / model_roofline / a13 totals / a1: per group */
+  double* m_lat; double* m_kern_lat; uint64_t* m_flops; uint64_t* m_read; uint64_t* m_write;
+  double* m_occ; uint64_t* m_count; double* m_ai; double* m_tput; int8_t* m_bound;
+  double* m_gpu; double* m_gpu_pct; double* m_throughput;
+  uint8_t* m_roofline_in;
+} xsp_tables_out;
+
+/* ---- API ------------------------------------------------------------------ */
+
+xsp_status xsp_ctx_create(int device, xsp_ctx** out);
+void xsp_ctx_destroy(xsp_ctx* ctx);
+const char* xsp_last_error(const xsp_ctx* ctx);
+int xsp_abi_version(void);
+
+/* correlate() for every trace (correlator.cpp:366-370 = assign_parents 141-282 +
+ * correlate_async 287-364). Inputs are DEVICE pointers. Traces must be in
+ * timeline order (sort_timeline); when sort_if_needed != 0 unsorted traces are
+ * first sorted on the device (xsp_sort_timeline), otherwise XSP_E_UNSORTED.
+ * stream: a cudaStream_t (NULL = legacy default stream). Asynchronous except
+ * for the small count read-back needed to size the outputs. */
+xsp_status xsp_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
+                         int sort_if_needed, xsp_corr_out* out, void* stream);
+
+/* a8..a15 + model_roofline + a1 throughput + top-k for every group over a
+ * correlation computed by xsp_correlate on the same ctx. cols must be the same
+ * columns given to xsp_correlate. */
+xsp_status xsp_analyze(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                       const xsp_groups* groups, const xsp_system_spec* spec,
+                       const xsp_analysis_opts* opts, xsp_tables_out* out, void* stream);
+
+/* End-to-end convenience for host-resident inputs: copies the HOST columns to the
+ * device, runs xsp_correlate + xsp_analyze, and copies every result column back
+ * into ctx-owned pinned host memory (pointers in *corr_host / *tables_host are
+ * HOST pointers valid until the next call). Synchronous. */
+xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* host_cols,
+                        const xsp_traces* host_traces, const xsp_groups* groups,
+                        const xsp_system_spec* spec, const xsp_analysis_opts* opts,
+                        xsp_corr_out* corr_host, xsp_tables_out* tables_host, void* stream);
+
+/* Bytes moved host->device and device->host by the last xsp_run_host call. */
+void xsp_last_transfer_bytes(const xsp_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
+
+/* Number of CUDA kernel launches issued by the last API call on this ctx. */
+uint64_t xsp_last_launch_count(const xsp_ctx* ctx);
+
+/* Synchronous device->host copy of `bytes` from a result column (helper for
+ * callers that do not link the CUDA runtime themselves). */
+xsp_status xsp_copy_to_host(xsp_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+/* Pinned host allocation helpers (cudaHostAlloc) for callers staging inputs. */
+void* xsp_host_alloc(size_t bytes);
+void xsp_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XSP_H */

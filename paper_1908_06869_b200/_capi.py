@@ -1,0 +1,178 @@
+"""ctypes mirror of include/xsp.h (the C ABI of the CUDA hot path).
+
+The library is loaded from this package's lib/ directory (built in-tree by
+``make -C paper_1908_06869_b200``). There is no CPU fallback: if the library
+is missing, or no CUDA device is present when a context is created, the call
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libxsp.so")
+
+u8p = C.POINTER(C.c_uint8)
+i8p = C.POINTER(C.c_int8)
+u32p = C.POINTER(C.c_uint32)
+i32p = C.POINTER(C.c_int32)
+u64p = C.POINTER(C.c_uint64)
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+
+# status codes
+XSP_OK = 0
+XSP_E_INVALID = 1
+XSP_E_CUDA = 2
+XSP_E_NOMEM = 3
+XSP_E_UNSORTED = 4
+XSP_E_NO_DEVICE = 5
+
+# flags byte
+F_PARENT = 0x10
+F_CID = 0x20
+F_METRICS = 0x40
+LEVEL_MODEL, LEVEL_LAYER, LEVEL_KERNEL, LEVEL_API = 0, 1, 2, 3
+KIND_SYNC, KIND_LAUNCH, KIND_EXEC = 0, 1, 2
+
+# per-trace status (xsp_trace_status)
+T_OK, T_NO_MODEL, T_MULTI_MODEL, T_SKIP_LEVEL, T_DUP_EXEC_CID, T_DUP_LAUNCH_CID = range(6)
+# per-group status
+G_OK, G_NO_RUNS, G_LAYER_COUNT, G_KERNEL_COUNT, G_TRACE_FAILED, G_BAD_TRIM = range(6)
+
+
+class SpanCols(C.Structure):
+    _fields_ = [
+        ("n_spans", C.c_uint64),
+        ("span_id", u64p), ("parent_id", u64p), ("begin_ns", u64p), ("end_ns", u64p),
+        ("cid", u64p), ("flags", u8p), ("name_id", u32p),
+        ("n_metric_rows", C.c_uint64),
+        ("flops", u64p), ("dram_read", u64p), ("dram_write", u64p), ("occupancy", f64p),
+        ("n_layer_rows", C.c_uint64),
+        ("alloc_bytes", i64p), ("type_id", u32p),
+    ]
+
+
+class Traces(C.Structure):
+    _fields_ = [("n_traces", C.c_uint32), ("span_off", u64p), ("levels", u32p)]
+
+
+CORR_FIELDS = [
+    ("trace_status", i32p, "T"), ("trace_err_row", u32p, "2T"), ("trace_model_row", u32p, "T"),
+    ("trace_layer_off", u32p, "T1"), ("trace_kernel_off", u32p, "T1"),
+    ("trace_orphan_off", u32p, "T1"), ("trace_amb_off", u32p, "T1"),
+    ("layer_row", u32p, "L"), ("layer_kernel_off", u32p, "L1"), ("layer_dur", u64p, "L"),
+    ("layer_attr_row", u32p, "L"),
+    ("kernel_launch_row", u32p, "K"), ("kernel_exec_row", u32p, "K"),
+    ("kernel_metric_row", u32p, "K"), ("kernel_dur", u64p, "K"), ("kernel_name", u32p, "K"),
+    ("orphan_row", u32p, "O"), ("orphan_reason", u8p, "O"),
+    ("amb_row", u32p, "A"), ("amb_cand_off", u32p, "A1"), ("amb_cand_row", u32p, "AC"),
+]
+
+
+class CorrOut(C.Structure):
+    _fields_ = [
+        ("n_traces", C.c_uint32), ("n_failed", C.c_uint32),
+        ("n_layers", C.c_uint64), ("n_kernels", C.c_uint64), ("n_orphans", C.c_uint64),
+        ("n_ambiguities", C.c_uint64), ("n_candidates", C.c_uint64),
+    ] + [(n, t) for n, t, _ in CORR_FIELDS]
+
+
+class SystemSpec(C.Structure):
+    _fields_ = [("peak_flops", C.c_double), ("memory_bandwidth_bytes_per_s", C.c_double)]
+
+
+class AnalysisOpts(C.Structure):
+    _fields_ = [("trim_fraction", C.c_double), ("epsilon", C.c_double),
+                ("noise_tolerance", C.c_double), ("top_k", C.c_uint32)]
+
+
+class Groups(C.Structure):
+    _fields_ = [("n_groups", C.c_uint32), ("first_trace", u32p), ("n_runs", u32p),
+                ("batch_size", u32p)]
+
+
+TABLE_FIELDS = [
+    ("group_status", i32p, "G"), ("group_err_arg", u32p, "G"),
+    ("group_layer_off", u32p, "G1"), ("group_kernel_off", u32p, "G1"),
+    ("group_name_off", u32p, "G1"),
+    ("k_name", u32p, "K"), ("k_layer", u32p, "K"), ("k_lat", f64p, "K"), ("k_flops", u64p, "K"),
+    ("k_read", u64p, "K"), ("k_write", u64p, "K"), ("k_occ", f64p, "K"), ("k_ai", f64p, "K"),
+    ("k_tput", f64p, "K"), ("k_bound", i8p, "K"), ("k_roofline_in", u8p, "K"),
+    ("l_index", u32p, "L"), ("l_row", u32p, "L"), ("l_layer_lat", f64p, "L"),
+    ("l_kern_lat", f64p, "L"), ("l_flops", u64p, "L"), ("l_read", u64p, "L"),
+    ("l_write", u64p, "L"), ("l_occ", f64p, "L"), ("l_count", u64p, "L"), ("l_ai", f64p, "L"),
+    ("l_tput", f64p, "L"), ("l_bound", i8p, "L"), ("l_nongpu", f64p, "L"),
+    ("l_gpu_share", f64p, "L"), ("l_nongpu_share", f64p, "L"), ("l_flagged", u8p, "L"),
+    ("l_roofline_in", u8p, "L"), ("l_topk", u32p, "LK"),
+    ("n_name", u32p, "N"), ("n_count", u64p, "N"), ("n_lat", f64p, "N"), ("n_pct", f64p, "N"),
+    ("n_flops", u64p, "N"), ("n_read", u64p, "N"), ("n_write", u64p, "N"), ("n_occ", f64p, "N"),
+    ("n_ai", f64p, "N"), ("n_tput", f64p, "N"), ("n_bound", i8p, "N"),
+    ("m_lat", f64p, "G"), ("m_kern_lat", f64p, "G"), ("m_flops", u64p, "G"),
+    ("m_read", u64p, "G"), ("m_write", u64p, "G"), ("m_occ", f64p, "G"), ("m_count", u64p, "G"),
+    ("m_ai", f64p, "G"), ("m_tput", f64p, "G"), ("m_bound", i8p, "G"), ("m_gpu", f64p, "G"),
+    ("m_gpu_pct", f64p, "G"), ("m_throughput", f64p, "G"), ("m_roofline_in", u8p, "G"),
+]
+
+
+class TablesOut(C.Structure):
+    _fields_ = [
+        ("n_groups", C.c_uint32),
+        ("n_layers", C.c_uint64), ("n_kernels", C.c_uint64), ("n_names", C.c_uint64),
+    ] + [(n, t) for n, t, _ in TABLE_FIELDS]
+
+
+# exported symbols of libxsp.so, i.e. the functions include/xsp.h declares
+EXPORTS = [
+    "xsp_abi_version", "xsp_ctx_create", "xsp_ctx_destroy", "xsp_last_error", "xsp_correlate",
+    "xsp_analyze", "xsp_run_host", "xsp_last_transfer_bytes", "xsp_last_launch_count",
+    "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host",
+]
+
+_lib = None
+
+
+class XspError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"xsp status {status}: {message}")
+        self.status = status
+
+
+def load() -> C.CDLL:
+    """Load libxsp.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `make -C {_HERE}` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH, mode=C.RTLD_LOCAL)
+    P = C.c_void_p
+    lib.xsp_abi_version.restype = C.c_int
+    lib.xsp_ctx_create.argtypes = [C.c_int, C.POINTER(P)]
+    lib.xsp_ctx_create.restype = C.c_int32
+    lib.xsp_ctx_destroy.argtypes = [P]
+    lib.xsp_last_error.argtypes = [P]
+    lib.xsp_last_error.restype = C.c_char_p
+    lib.xsp_correlate.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.c_int,
+                                  C.POINTER(CorrOut), P]
+    lib.xsp_correlate.restype = C.c_int32
+    lib.xsp_analyze.argtypes = [P, C.POINTER(SpanCols), C.POINTER(CorrOut), C.POINTER(Groups),
+                                C.POINTER(SystemSpec), C.POINTER(AnalysisOpts),
+                                C.POINTER(TablesOut), P]
+    lib.xsp_analyze.restype = C.c_int32
+    lib.xsp_run_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(Groups),
+                                 C.POINTER(SystemSpec), C.POINTER(AnalysisOpts),
+                                 C.POINTER(CorrOut), C.POINTER(TablesOut), P]
+    lib.xsp_run_host.restype = C.c_int32
+    lib.xsp_last_transfer_bytes.argtypes = [P, u64p, u64p]
+    lib.xsp_last_launch_count.argtypes = [P]
+    lib.xsp_last_launch_count.restype = C.c_uint64
+    lib.xsp_host_alloc.argtypes = [C.c_size_t]
+    lib.xsp_host_alloc.restype = P
+    lib.xsp_host_free.argtypes = [P]
+    lib.xsp_copy_to_host.argtypes = [P, P, P, C.c_size_t]
+    lib.xsp_copy_to_host.restype = C.c_int32
+    _lib = lib
+    return lib

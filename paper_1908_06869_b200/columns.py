@@ -1,0 +1,170 @@
+"""Columnar (structure-of-arrays) span batches: the input format of the C ABI.
+
+A SpanBatch holds the spans of one or more traces (TraceBundles, reference
+span.hpp:161-171) as flat numpy columns, trace after trace, in timeline order
+within each trace. The metric table has one row per span carrying
+XSP_F_METRICS and the layer table one row per level==Layer span, both in span
+order (include/xsp.h).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi as capi
+
+SPAN_COLS = {
+    "span_id": np.uint64, "parent_id": np.uint64, "begin_ns": np.uint64, "end_ns": np.uint64,
+    "cid": np.uint64, "flags": np.uint8, "name_id": np.uint32,
+}
+METRIC_COLS = {"flops": np.uint64, "dram_read": np.uint64, "dram_write": np.uint64,
+               "occupancy": np.float64}
+LAYER_COLS = {"alloc_bytes": np.int64, "type_id": np.uint32}
+TRACE_COLS = {"trace_span_off": np.uint64, "trace_id": np.uint64, "trace_levels": np.uint32,
+              "trace_batch": np.uint32, "trace_run": np.uint32, "trace_serialized": np.uint8}
+
+
+def _ptr(a: np.ndarray, typ):
+    return a.ctypes.data_as(typ) if a.size else C.cast(C.c_void_p(0), typ)
+
+
+@dataclass
+class SpanBatch:
+    span_id: np.ndarray
+    parent_id: np.ndarray
+    begin_ns: np.ndarray
+    end_ns: np.ndarray
+    cid: np.ndarray
+    flags: np.ndarray
+    name_id: np.ndarray
+    flops: np.ndarray
+    dram_read: np.ndarray
+    dram_write: np.ndarray
+    occupancy: np.ndarray
+    alloc_bytes: np.ndarray
+    type_id: np.ndarray
+    trace_span_off: np.ndarray
+    trace_id: np.ndarray
+    trace_levels: np.ndarray
+    trace_batch: np.ndarray
+    trace_run: np.ndarray
+    trace_serialized: np.ndarray
+    names: List[bytes] = field(default_factory=list)
+    types: List[bytes] = field(default_factory=list)
+    system_name: bytes = b"tesla-v100-sxm2"
+    peak_flops: float = 15.7e12
+    mem_bw: float = 900e9
+
+    def __post_init__(self):
+        for k, dt in {**SPAN_COLS, **METRIC_COLS, **LAYER_COLS, **TRACE_COLS}.items():
+            setattr(self, k, np.ascontiguousarray(getattr(self, k), dtype=dt))
+
+    # ---- sizes
+    @property
+    def n_spans(self) -> int:
+        return int(self.span_id.size)
+
+    @property
+    def n_traces(self) -> int:
+        return int(self.trace_levels.size)
+
+    def level(self) -> np.ndarray:
+        return self.flags & 3
+
+    def kind(self) -> np.ndarray:
+        return (self.flags >> 2) & 3
+
+    # ---- C ABI views (host pointers; keep self alive while used)
+    def cols(self) -> capi.SpanCols:
+        c = capi.SpanCols()
+        c.n_spans = self.n_spans
+        c.span_id = _ptr(self.span_id, capi.u64p)
+        c.parent_id = _ptr(self.parent_id, capi.u64p)
+        c.begin_ns = _ptr(self.begin_ns, capi.u64p)
+        c.end_ns = _ptr(self.end_ns, capi.u64p)
+        c.cid = _ptr(self.cid, capi.u64p)
+        c.flags = _ptr(self.flags, capi.u8p)
+        c.name_id = _ptr(self.name_id, capi.u32p)
+        c.n_metric_rows = int(self.flops.size)
+        c.flops = _ptr(self.flops, capi.u64p)
+        c.dram_read = _ptr(self.dram_read, capi.u64p)
+        c.dram_write = _ptr(self.dram_write, capi.u64p)
+        c.occupancy = _ptr(self.occupancy, capi.f64p)
+        c.n_layer_rows = int(self.alloc_bytes.size)
+        c.alloc_bytes = _ptr(self.alloc_bytes, capi.i64p)
+        c.type_id = _ptr(self.type_id, capi.u32p)
+        return c
+
+    def traces(self) -> capi.Traces:
+        t = capi.Traces()
+        t.n_traces = self.n_traces
+        t.span_off = _ptr(self.trace_span_off, capi.u64p)
+        t.levels = _ptr(self.trace_levels, capi.u32p)
+        return t
+
+    def nbytes_inputs(self) -> int:
+        """Bytes of every input column the C ABI reads (span + side tables + traces)."""
+        cols = list(SPAN_COLS) + list(METRIC_COLS) + list(LAYER_COLS)
+        return int(sum(getattr(self, k).nbytes for k in cols) + self.trace_span_off.nbytes
+                   + self.trace_levels.nbytes)
+
+    def name(self, name_id: int) -> str:
+        return self.names[int(name_id)].decode()
+
+    # ---- construction
+    @classmethod
+    def from_bag(cls, bag: Dict[str, np.ndarray], strings: Dict[str, List[bytes]]) -> "SpanBatch":
+        kw = {k: bag[k] for k in {**SPAN_COLS, **METRIC_COLS, **LAYER_COLS, **TRACE_COLS}}
+        sysname = strings.get("system_name", [b"tesla-v100-sxm2"])
+        return cls(**kw, names=list(strings["names"]), types=list(strings["types"]),
+                   system_name=sysname[0] if sysname else b"",
+                   peak_flops=float(bag["system_peak"][0]) if "system_peak" in bag else 15.7e12,
+                   mem_bw=float(bag["system_bw"][0]) if "system_bw" in bag else 900e9)
+
+    @classmethod
+    def concat(cls, batches: Sequence["SpanBatch"]) -> "SpanBatch":
+        """Concatenate batches, re-interning names/types in lexicographic order."""
+        names = sorted({n for b in batches for n in b.names})
+        types = sorted({n for b in batches for n in b.types})
+        nid = {n: i for i, n in enumerate(names)}
+        tid = {n: i for i, n in enumerate(types)}
+        parts: Dict[str, list] = {k: [] for k in {**SPAN_COLS, **METRIC_COLS, **LAYER_COLS, **TRACE_COLS}}
+        base = 0
+        for b in batches:
+            nmap = np.array([nid[n] for n in b.names], dtype=np.uint32)
+            tmap = np.array([tid[n] for n in b.types], dtype=np.uint32)
+            for k in SPAN_COLS:
+                v = getattr(b, k)
+                parts[k].append(nmap[v] if (k == "name_id" and v.size) else v)
+            for k in METRIC_COLS:
+                parts[k].append(getattr(b, k))
+            parts["alloc_bytes"].append(b.alloc_bytes)
+            parts["type_id"].append(tmap[b.type_id] if b.type_id.size else b.type_id)
+            parts["trace_span_off"].append(b.trace_span_off[:-1] + base)
+            for k in ("trace_id", "trace_levels", "trace_batch", "trace_run", "trace_serialized"):
+                parts[k].append(getattr(b, k))
+            base += b.n_spans
+        parts["trace_span_off"].append(np.array([base], dtype=np.uint64))
+        kw = {k: (np.concatenate(v) if v else np.zeros(0)) for k, v in parts.items()}
+        first = batches[0]
+        return cls(**kw, names=names, types=types, system_name=first.system_name,
+                   peak_flops=first.peak_flops, mem_bw=first.mem_bw)
+
+    def trace_slice(self, t0: int, t1: int) -> "SpanBatch":
+        """Traces [t0, t1) as a new batch (same string tables)."""
+        s0, s1 = int(self.trace_span_off[t0]), int(self.trace_span_off[t1])
+        lay = self.level() == capi.LEVEL_LAYER
+        met = (self.flags & capi.F_METRICS) != 0
+        m0, m1 = int(met[:s0].sum()), int(met[:s1].sum())
+        l0, l1 = int(lay[:s0].sum()), int(lay[:s1].sum())
+        kw = {k: getattr(self, k)[s0:s1] for k in SPAN_COLS}
+        kw.update({k: getattr(self, k)[m0:m1] for k in METRIC_COLS})
+        kw.update({k: getattr(self, k)[l0:l1] for k in LAYER_COLS})
+        kw["trace_span_off"] = self.trace_span_off[t0:t1 + 1] - s0
+        for k in ("trace_id", "trace_levels", "trace_batch", "trace_run", "trace_serialized"):
+            kw[k] = getattr(self, k)[t0:t1]
+        return SpanBatch(**kw, names=self.names, types=self.types, system_name=self.system_name,
+                         peak_flops=self.peak_flops, mem_bw=self.mem_bw)

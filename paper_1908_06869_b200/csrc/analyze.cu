@@ -1,0 +1,763 @@
+// Stage (e): per-kernel, per-layer, per-name and per-model reductions with
+// roofline classification and top-k, for every AnalysisInput of a batch.
+//
+// Reference semantics: combine() (analysis.cpp:102-170), Accumulator and
+// attach_roofline (:173-211), a8/a9 (:342-397), a10 (:399-432), a11-a14
+// (:437-525), a15/model_roofline (:532-586), a1 throughput (:236-263).
+//
+// Bit-exactness: this file is compiled with -fmad=false, and every fp64
+// expression keeps the reference's operation sequence (flops / (lat / 1e9),
+// a / b * 100, sums accumulated left to right in tree order). Integer counters
+// are u64 sums (exact). Sequential fp64 chains (the Accumulator) are evaluated
+// by one thread per subject in tree order, as the reference does.
+
+#include "ctx.h"
+#include "prims.cuh"
+
+namespace xsp {
+
+constexpr int kMaxRuns = 64;
+
+// trimmed_mean (analysis.cpp:28-39): sort, drop floor(f*n) each end, ordered sum.
+__device__ double trimmed_mean_dev(double* v, uint32_t n, double f) {
+  for (uint32_t i = 1; i < n; ++i) {
+    double x = v[i];
+    uint32_t j = i;
+    while (j > 0 && v[j - 1] > x) {
+      v[j] = v[j - 1];
+      --j;
+    }
+    v[j] = x;
+  }
+  uint32_t drop = (uint32_t)floor(f * (double)n);
+  double s = 0.0;
+  for (uint32_t i = drop; i < n - drop; ++i) s = __dadd_rn(s, v[i]);
+  return s / (double)(n - 2 * drop);
+}
+
+struct Roof {
+  double ai, tput;
+  int8_t bound;
+};
+
+// arithmetic_intensity / arithmetic_throughput / ideal (analysis.cpp:41-57)
+__device__ __forceinline__ Roof roofline(uint64_t flops, uint64_t r, uint64_t w, double lat,
+                                         double peak, double bw) {
+  Roof o;
+  double bytes = __dadd_rn((double)r, (double)w);
+  o.ai = bytes <= 0.0 ? nan("") : (double)flops / bytes;
+  o.tput = lat > 0.0 ? (double)flops / (lat / 1e9) : nan("");
+  o.bound = bytes <= 0.0 ? (int8_t)-1 : (int8_t)(o.ai < peak / bw ? 1 : 0);
+  return o;
+}
+
+struct GroupArgs {
+  uint32_t G;
+  const uint32_t* ft;
+  const uint32_t* nr;
+  const uint32_t* batch;
+  const int32_t* t_status;
+  const uint32_t* t_layer_off;
+  const uint32_t* t_kernel_off;
+  const uint32_t* l_koff;
+  uint32_t* gl;  // layers of run 0
+  uint32_t* gk;  // kernels of run 0
+  unsigned long long* gerr;
+};
+
+__global__ void k_group_prep(GroupArgs a) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.G) return;
+  uint32_t t = a.ft[g];
+  a.gerr[g] = ~0ull;
+  if (a.nr[g] == 0) {
+    a.gl[g] = a.gk[g] = 0;
+    return;
+  }
+  a.gl[g] = a.t_layer_off[t + 1] - a.t_layer_off[t];
+  a.gk[g] = a.t_kernel_off[t + 1] - a.t_kernel_off[t];
+}
+
+// Structure checks of combine() (analysis.cpp:103-118): first failing run, and
+// within it the layer-count check before the per-layer kernel counts.
+__global__ void k_group_check_runs(GroupArgs a, uint32_t total_runs, const uint32_t* __restrict__ run_off) {
+  uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= total_runs) return;
+  uint32_t lo = 0, hi = a.G;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (run_off[mid] <= q) lo = mid; else hi = mid;
+  }
+  uint32_t g = lo, r = q - run_off[g];
+  uint32_t t = a.ft[g] + r;
+  if (a.t_status[t] != XSP_T_OK) {
+    atomicMin(a.gerr + g, 0ull);  // trace failure outranks everything
+    return;
+  }
+  uint32_t L = a.t_layer_off[t + 1] - a.t_layer_off[t];
+  if (L != a.gl[g]) atomicMin(a.gerr + g, ((unsigned long long)(r + 1) << 32) | 0ull);
+}
+
+__global__ void k_group_check_layers(GroupArgs a, uint32_t total_layers, const uint32_t* __restrict__ gl_off) {
+  uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= total_layers) return;
+  uint32_t lo = 0, hi = a.G;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (gl_off[mid] <= q) lo = mid; else hi = mid;
+  }
+  uint32_t g = lo, li = q - gl_off[g];
+  uint32_t t0 = a.ft[g];
+  uint32_t gl0 = a.t_layer_off[t0] + li;
+  uint32_t k0 = a.l_koff[gl0 + 1] - a.l_koff[gl0];
+  for (uint32_t r = 1; r < a.nr[g]; ++r) {
+    uint32_t t = t0 + r;
+    if (a.t_status[t] != XSP_T_OK) continue;
+    uint32_t L = a.t_layer_off[t + 1] - a.t_layer_off[t];
+    if (L != a.gl[g]) continue;
+    uint32_t glr = a.t_layer_off[t] + li;
+    uint32_t kr = a.l_koff[glr + 1] - a.l_koff[glr];
+    if (kr != k0) atomicMin(a.gerr + g, ((unsigned long long)(r + 1) << 32) | (li + 1));
+  }
+}
+
+__global__ void k_group_status(uint32_t G, const uint32_t* __restrict__ nr,
+                               const unsigned long long* __restrict__ gerr, double trim,
+                               int32_t* __restrict__ status, uint32_t* __restrict__ err_arg) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  int32_t s = XSP_G_OK;
+  uint32_t arg = 0;
+  unsigned long long e = gerr[g];
+  if (nr[g] == 0) s = XSP_G_NO_RUNS;
+  else if (e == 0ull) s = XSP_G_TRACE_FAILED;
+  else if (e != ~0ull) {
+    uint32_t li = (uint32_t)(e & 0xFFFFFFFFull);
+    if (li == 0) s = XSP_G_LAYER_COUNT;
+    else {
+      s = XSP_G_KERNEL_COUNT;
+      arg = li - 1;
+    }
+  } else if (!(trim >= 0.0 && trim < 0.5)) {
+    s = XSP_G_BAD_TRIM;
+  }
+  if (nr[g] > kMaxRuns && s == XSP_G_OK) s = XSP_G_BAD_TRIM;  // unsupported run count
+  status[g] = s;
+  err_arg[g] = arg;
+}
+
+struct LayerArgs {
+  uint32_t G, total_layers, top_k;
+  const uint32_t* gl_off;
+  const uint32_t* gk_off;
+  const uint32_t* ft;
+  const uint32_t* nr;
+  const int32_t* gstatus;
+  const uint32_t* t_layer_off;
+  const uint32_t* t_kernel_off;
+  const uint32_t* l_koff;
+  const uint64_t* layer_dur;
+  const uint32_t* layer_row;
+  const uint64_t* kernel_dur;
+  const uint32_t* kernel_mrow;
+  const uint32_t* kernel_name;
+  const uint64_t* m_flops;
+  const uint64_t* m_read;
+  const uint64_t* m_write;
+  const double* m_occ;
+  double trim, noise, peak, bw;
+  // out: kernels
+  uint32_t* k_name;
+  uint32_t* k_layer;
+  double* k_lat;
+  uint64_t* k_flops;
+  uint64_t* k_read;
+  uint64_t* k_write;
+  double* k_occ;
+  double* k_ai;
+  double* k_tput;
+  int8_t* k_bound;
+  uint8_t* k_in;
+  // out: layers
+  uint32_t* l_index;
+  uint32_t* l_row;
+  double* l_layer_lat;
+  double* l_kern_lat;
+  uint64_t* l_flops;
+  uint64_t* l_read;
+  uint64_t* l_write;
+  double* l_occ;
+  uint64_t* l_count;
+  double* l_ai;
+  double* l_tput;
+  int8_t* l_bound;
+  double* l_nongpu;
+  double* l_gpu_share;
+  double* l_nongpu_share;
+  uint8_t* l_flagged;
+  uint8_t* l_in;
+  uint32_t* l_topk;
+};
+
+__global__ void k_layers(LayerArgs a) {
+  uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= a.total_layers) return;
+  uint32_t lo = 0, hi = a.G;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (a.gl_off[mid] <= q) lo = mid; else hi = mid;
+  }
+  const uint32_t g = lo, li = q - a.gl_off[g];
+  if (a.gstatus[g] != XSP_G_OK) return;
+  const uint32_t R = a.nr[g], t0 = a.ft[g];
+  double v[kMaxRuns];
+  double w[kMaxRuns];
+  // layer latency (combine, analysis.cpp:138-144)
+  for (uint32_t r = 0; r < R; ++r) v[r] = (double)a.layer_dur[a.t_layer_off[t0 + r] + li];
+  const double layer_lat = trimmed_mean_dev(v, R, a.trim);
+
+  const uint32_t gl0 = a.t_layer_off[t0] + li;
+  const uint32_t kb = a.l_koff[gl0], ke = a.l_koff[gl0 + 1];
+  const uint32_t group_kbase = a.gk_off[g];
+  const uint32_t trace_kbase = a.t_kernel_off[t0];
+  // Accumulator (analysis.cpp:173-193)
+  double acc_lat = 0.0, acc_occw = 0.0;
+  uint64_t acc_f = 0, acc_r = 0, acc_w = 0, acc_n = 0;
+  const uint32_t K = a.top_k;
+  uint32_t top_idx[8];
+  double top_lat[8];
+  uint32_t ntop = 0;
+  for (uint32_t j = kb; j < ke; ++j) {
+    const uint32_t ord = j - trace_kbase;  // kernel ordinal within the run
+    for (uint32_t r = 0; r < R; ++r) {
+      uint32_t jr = a.t_kernel_off[t0 + r] + ord;
+      v[r] = (double)a.kernel_dur[jr];
+      uint32_t mr = a.kernel_mrow[jr];
+      w[r] = mr != kNone ? a.m_occ[mr] : 0.0;
+    }
+    const double klat = trimmed_mean_dev(v, R, a.trim);
+    const double kocc = trimmed_mean_dev(w, R, a.trim);
+    const uint32_t mr0 = a.kernel_mrow[j];
+    uint64_t f = 0, rd = 0, wr = 0;
+    if (mr0 != kNone) {
+      f = a.m_flops[mr0];
+      rd = a.m_read[mr0];
+      wr = a.m_write[mr0];
+    }
+    const uint32_t out = group_kbase + ord;
+    Roof ro = roofline(f, rd, wr, klat, a.peak, a.bw);
+    a.k_name[out] = a.kernel_name[j];
+    a.k_layer[out] = li;
+    a.k_lat[out] = klat;
+    a.k_flops[out] = f;
+    a.k_read[out] = rd;
+    a.k_write[out] = wr;
+    a.k_occ[out] = kocc;
+    a.k_ai[out] = ro.ai;
+    a.k_tput[out] = ro.tput;
+    a.k_bound[out] = ro.bound;
+    a.k_in[out] = (ro.bound >= 0 && klat > 0.0) ? 1 : 0;  // classify (analysis.cpp:59-71)
+    acc_lat = __dadd_rn(acc_lat, klat);
+    acc_f += f;
+    acc_r += rd;
+    acc_w += wr;
+    acc_occw = __dadd_rn(acc_occw, __dmul_rn(kocc, klat));
+    ++acc_n;
+    // top-k by latency desc, ordinal asc
+    if (K) {
+      uint32_t pos = ntop;
+      while (pos > 0 && top_lat[pos - 1] < klat) --pos;
+      if (pos < K) {
+        uint32_t last = ntop < K ? ntop : K - 1;
+        for (uint32_t s = last; s > pos; --s) {
+          top_lat[s] = top_lat[s - 1];
+          top_idx[s] = top_idx[s - 1];
+        }
+        top_lat[pos] = klat;
+        top_idx[pos] = ord;
+        if (ntop < K) ++ntop;
+      }
+    }
+  }
+  const uint32_t lo_out = a.gl_off[g] + li;
+  Roof ro = roofline(acc_f, acc_r, acc_w, acc_lat, a.peak, a.bw);
+  a.l_index[lo_out] = li;
+  a.l_row[lo_out] = a.layer_row[gl0];
+  a.l_layer_lat[lo_out] = layer_lat;
+  a.l_kern_lat[lo_out] = acc_lat;
+  a.l_flops[lo_out] = acc_f;
+  a.l_read[lo_out] = acc_r;
+  a.l_write[lo_out] = acc_w;
+  a.l_occ[lo_out] = acc_lat > 0.0 ? acc_occw / acc_lat : 0.0;
+  a.l_count[lo_out] = acc_n;
+  a.l_ai[lo_out] = ro.ai;
+  a.l_tput[lo_out] = ro.tput;
+  a.l_bound[lo_out] = ro.bound;
+  a.l_in[lo_out] = (ro.bound >= 0 && acc_lat > 0.0) ? 1 : 0;
+  // a13 (analysis.cpp:484-494)
+  const double nongpu = __dsub_rn(layer_lat, acc_lat);
+  a.l_nongpu[lo_out] = nongpu;
+  a.l_gpu_share[lo_out] = layer_lat > 0.0 ? acc_lat / layer_lat : 0.0;
+  a.l_nongpu_share[lo_out] = layer_lat > 0.0 ? nongpu / layer_lat : 0.0;
+  a.l_flagged[lo_out] = nongpu < -(__dmul_rn(a.noise, layer_lat)) ? 1 : 0;
+  for (uint32_t s = 0; s < K; ++s)
+    a.l_topk[(uint64_t)lo_out * K + s] = s < ntop ? top_idx[s] : kNone;
+}
+
+struct ModelArgs {
+  uint32_t G;
+  const uint32_t* gl_off;
+  const uint32_t* gk_off;
+  const uint32_t* ft;
+  const uint32_t* nr;
+  const uint32_t* batch;
+  const int32_t* gstatus;
+  const uint32_t* model_row;
+  const uint64_t* begin;
+  const uint64_t* end;
+  const double* k_lat;
+  const double* k_occ;
+  const uint64_t* k_flops;
+  const uint64_t* k_read;
+  const uint64_t* k_write;
+  const double* l_kern_lat;
+  double trim, peak, bw;
+  double* m_lat;
+  double* m_kern_lat;
+  uint64_t* m_flops;
+  uint64_t* m_read;
+  uint64_t* m_write;
+  double* m_occ;
+  uint64_t* m_count;
+  double* m_ai;
+  double* m_tput;
+  int8_t* m_bound;
+  double* m_gpu;
+  double* m_gpu_pct;
+  double* m_throughput;
+  uint8_t* m_in;
+};
+
+// model_aggregate_row (analysis.cpp:532-552), a13 totals (:495-499), a1 (:245-246)
+__global__ void k_models(ModelArgs a) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.G) return;
+  if (a.gstatus[g] != XSP_G_OK) {
+    a.m_lat[g] = nan("");
+    return;
+  }
+  const uint32_t R = a.nr[g], t0 = a.ft[g];
+  double v[kMaxRuns];
+  for (uint32_t r = 0; r < R; ++r) {
+    uint32_t m = a.model_row[t0 + r];
+    v[r] = (double)clamp_dur(a.begin[m], a.end[m]);
+  }
+  const double mlat = trimmed_mean_dev(v, R, a.trim);
+  double lat = 0.0, occw = 0.0;
+  uint64_t f = 0, rd = 0, wr = 0, n = 0;
+  for (uint32_t j = a.gk_off[g]; j < a.gk_off[g + 1]; ++j) {
+    double kl = a.k_lat[j];
+    lat = __dadd_rn(lat, kl);
+    f += a.k_flops[j];
+    rd += a.k_read[j];
+    wr += a.k_write[j];
+    occw = __dadd_rn(occw, __dmul_rn(a.k_occ[j], kl));
+    ++n;
+  }
+  double gpu = 0.0;
+  for (uint32_t l = a.gl_off[g]; l < a.gl_off[g + 1]; ++l) gpu = __dadd_rn(gpu, a.l_kern_lat[l]);
+  Roof ro = roofline(f, rd, wr, lat, a.peak, a.bw);
+  a.m_lat[g] = mlat;
+  a.m_kern_lat[g] = lat;
+  a.m_flops[g] = f;
+  a.m_read[g] = rd;
+  a.m_write[g] = wr;
+  a.m_occ[g] = lat > 0.0 ? occw / lat : 0.0;
+  a.m_count[g] = n;
+  a.m_ai[g] = ro.ai;
+  a.m_tput[g] = ro.tput;
+  a.m_bound[g] = ro.bound;
+  a.m_gpu[g] = gpu;
+  a.m_gpu_pct[g] = gpu / mlat * 100.0;
+  a.m_throughput[g] = (double)a.batch[g] / (mlat / 1e9);
+  a.m_in[g] = (ro.bound >= 0 && lat > 0.0) ? 1 : 0;
+}
+
+// ---- a10 by name ------------------------------------------------------------
+
+__global__ void k_name_keys(uint32_t total_k, const uint32_t* __restrict__ gk_off, uint32_t G,
+                            const uint32_t* __restrict__ k_name, const int32_t* __restrict__ gstatus,
+                            uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= total_k) return;
+  uint32_t lo = 0, hi = G;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (gk_off[mid] <= j) lo = mid; else hi = mid;
+  }
+  // failed groups sort to the end and are ignored
+  key[j] = gstatus[lo] == XSP_G_OK ? (((uint64_t)lo << 32) | k_name[j]) : ~0ull;
+  val[j] = j;
+}
+
+__global__ void k_seg_flags(uint32_t n, const uint64_t* __restrict__ key, uint32_t* __restrict__ flag) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  flag[j] = (key[j] != ~0ull && (j == 0 || key[j] != key[j - 1])) ? 1u : 0u;
+}
+
+struct NameArgs {
+  uint32_t n;  // kernels in sorted array
+  const uint64_t* key;
+  const uint32_t* val;
+  const uint32_t* seg_pos;  // exclusive scan of flags
+  const uint32_t* flag;
+  const double* k_lat;
+  const double* k_occ;
+  const uint64_t* k_flops;
+  const uint64_t* k_read;
+  const uint64_t* k_write;
+  const double* m_lat;
+  double peak, bw;
+  uint32_t* s_group;
+  uint32_t* s_name;
+  uint64_t* s_count;
+  double* s_lat;
+  double* s_pct;
+  uint64_t* s_flops;
+  uint64_t* s_read;
+  uint64_t* s_write;
+  double* s_occ;
+  double* s_ai;
+  double* s_tput;
+  int8_t* s_bound;
+};
+
+__global__ void k_name_rows(NameArgs a) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n || !a.flag[j]) return;
+  const uint64_t k = a.key[j];
+  const uint32_t s = a.seg_pos[j];
+  double lat = 0.0, occw = 0.0;
+  uint64_t f = 0, rd = 0, wr = 0, c = 0;
+  for (uint32_t q = j; q < a.n && a.key[q] == k; ++q) {
+    uint32_t x = a.val[q];
+    double kl = a.k_lat[x];
+    lat = __dadd_rn(lat, kl);
+    f += a.k_flops[x];
+    rd += a.k_read[x];
+    wr += a.k_write[x];
+    occw = __dadd_rn(occw, __dmul_rn(a.k_occ[x], kl));
+    ++c;
+  }
+  const uint32_t g = (uint32_t)(k >> 32);
+  Roof ro = roofline(f, rd, wr, lat, a.peak, a.bw);
+  a.s_group[s] = g;
+  a.s_name[s] = (uint32_t)k;
+  a.s_count[s] = c;
+  a.s_lat[s] = lat;
+  a.s_pct[s] = lat / a.m_lat[g] * 100.0;
+  a.s_flops[s] = f;
+  a.s_read[s] = rd;
+  a.s_write[s] = wr;
+  a.s_occ[s] = lat > 0.0 ? occw / lat : 0.0;
+  a.s_ai[s] = ro.ai;
+  a.s_tput[s] = ro.tput;
+  a.s_bound[s] = ro.bound;
+}
+
+// Per group: rows sorted by total latency desc, then name asc (analysis.cpp:424-430).
+__global__ void k_name_order(uint32_t G, const uint32_t* __restrict__ g_name_off,
+                             const double* __restrict__ s_lat, uint32_t* __restrict__ order) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  uint32_t b = g_name_off[g], e = g_name_off[g + 1];
+  for (uint32_t i = b; i < e; ++i) {
+    uint32_t x = i;
+    uint32_t j = i;
+    while (j > b && s_lat[order[j - 1]] < s_lat[x]) {
+      order[j] = order[j - 1];
+      --j;
+    }
+    order[j] = x;
+  }
+}
+
+template <typename T>
+__global__ void k_permute(uint32_t n, const uint32_t* __restrict__ order, const T* __restrict__ src,
+                          T* __restrict__ dst) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[order[i]];
+}
+
+__global__ void k_csr_groups(uint32_t G, uint32_t n, const uint32_t* __restrict__ s_group,
+                             uint32_t* __restrict__ off) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > G) return;
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (s_group[mid] < g) lo = mid + 1; else hi = mid;
+  }
+  off[g] = lo;
+}
+
+// ---------------------------------------------------------------------------
+
+namespace {
+template <typename K, typename... Args>
+void launch(xsp_ctx* ctx, K kernel, uint64_t n, cudaStream_t st, Args... args) {
+  if (n == 0) return;
+  kernel<<<ceil_div(n, 256), 256, 0, st>>>(args...);
+  ++ctx->launches;
+}
+}  // namespace
+
+void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr, const xsp_groups* gr,
+                 const xsp_system_spec* spec, const xsp_analysis_opts* opts, xsp_tables_out* out,
+                 cudaStream_t st) {
+  const uint32_t G = gr->n_groups;
+  if (opts->top_k > 8) throw std::invalid_argument("top_k must be <= 8");
+  // group descriptors are host arrays
+  uint32_t* hg = ctx->h<uint32_t>("a.groups_h", 4ull * G + 4);
+  uint32_t total_runs = 0;
+  for (uint32_t g = 0; g < G; ++g) {
+    hg[g] = gr->first_trace[g];
+    hg[G + g] = gr->n_runs[g];
+    hg[2 * G + g] = gr->batch_size[g];
+    hg[3 * G + g] = total_runs;
+    if ((uint64_t)gr->first_trace[g] + gr->n_runs[g] > corr->n_traces)
+      throw std::invalid_argument("group references traces beyond the correlation result");
+    total_runs += gr->n_runs[g];
+  }
+  hg[4 * G] = total_runs;
+  uint32_t* dg = ctx->d<uint32_t>("a.groups", 4ull * G + 4);
+  XSP_CUDA(cudaMemcpyAsync(dg, hg, (4ull * G + 1) * 4, cudaMemcpyHostToDevice, st));
+  const uint32_t* ft = dg;
+  const uint32_t* nr = dg + G;
+  const uint32_t* batch = dg + 2 * G;
+  const uint32_t* run_off = dg + 3 * G;
+
+  GroupArgs ga;
+  ga.G = G;
+  ga.ft = ft;
+  ga.nr = nr;
+  ga.batch = batch;
+  ga.t_status = corr->trace_status;
+  ga.t_layer_off = corr->trace_layer_off;
+  ga.t_kernel_off = corr->trace_kernel_off;
+  ga.l_koff = corr->layer_kernel_off;
+  ga.gl = ctx->d<uint32_t>("a.gl", G + 1);
+  ga.gk = ctx->d<uint32_t>("a.gk", G + 1);
+  ga.gerr = ctx->d<unsigned long long>("a.gerr", G);
+  launch(ctx, k_group_prep, G, st, ga);
+  out->n_groups = G;
+  out->group_layer_off = ctx->d<uint32_t>("t.g_loff", G + 1);
+  out->group_kernel_off = ctx->d<uint32_t>("t.g_koff", G + 1);
+  uint32_t* scan_tmp = ctx->d<uint32_t>("a.scan", scan_scratch_elems(G + 16));
+  exclusive_scan<uint32_t, uint32_t>(ga.gl, out->group_layer_off, G, scan_tmp, out->group_layer_off + G, st,
+                                     &ctx->launches);
+  exclusive_scan<uint32_t, uint32_t>(ga.gk, out->group_kernel_off, G, scan_tmp, out->group_kernel_off + G, st,
+                                     &ctx->launches);
+  uint32_t* htot = ctx->h<uint32_t>("a.tot_h", 4);
+  XSP_CUDA(cudaMemcpyAsync(htot, out->group_layer_off + G, 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(htot + 1, out->group_kernel_off + G, 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  const uint32_t TL = htot[0], TK = htot[1];
+  launch(ctx, k_group_check_runs, total_runs, st, ga, total_runs, run_off);
+  launch(ctx, k_group_check_layers, TL, st, ga, TL, out->group_layer_off);
+  out->group_status = ctx->d<int32_t>("t.g_status", G);
+  out->group_err_arg = ctx->d<uint32_t>("t.g_arg", G);
+  launch(ctx, k_group_status, G, st, G, nr, ga.gerr, opts->trim_fraction, out->group_status,
+         out->group_err_arg);
+
+  // ---- per layer + per kernel
+  LayerArgs la;
+  la.G = G;
+  la.total_layers = TL;
+  la.top_k = opts->top_k;
+  la.gl_off = out->group_layer_off;
+  la.gk_off = out->group_kernel_off;
+  la.ft = ft;
+  la.nr = nr;
+  la.gstatus = out->group_status;
+  la.t_layer_off = corr->trace_layer_off;
+  la.t_kernel_off = corr->trace_kernel_off;
+  la.l_koff = corr->layer_kernel_off;
+  la.layer_dur = corr->layer_dur;
+  la.layer_row = corr->layer_row;
+  la.kernel_dur = corr->kernel_dur;
+  la.kernel_mrow = corr->kernel_metric_row;
+  la.kernel_name = corr->kernel_name;
+  la.m_flops = c->flops;
+  la.m_read = c->dram_read;
+  la.m_write = c->dram_write;
+  la.m_occ = c->occupancy;
+  la.trim = opts->trim_fraction;
+  la.noise = opts->noise_tolerance;
+  la.peak = spec->peak_flops;
+  la.bw = spec->memory_bandwidth_bytes_per_s;
+  out->n_layers = TL;
+  out->n_kernels = TK;
+  out->k_name = la.k_name = ctx->d<uint32_t>("t.k_name", TK);
+  out->k_layer = la.k_layer = ctx->d<uint32_t>("t.k_layer", TK);
+  out->k_lat = la.k_lat = ctx->d<double>("t.k_lat", TK);
+  out->k_flops = la.k_flops = ctx->d<uint64_t>("t.k_flops", TK);
+  out->k_read = la.k_read = ctx->d<uint64_t>("t.k_read", TK);
+  out->k_write = la.k_write = ctx->d<uint64_t>("t.k_write", TK);
+  out->k_occ = la.k_occ = ctx->d<double>("t.k_occ", TK);
+  out->k_ai = la.k_ai = ctx->d<double>("t.k_ai", TK);
+  out->k_tput = la.k_tput = ctx->d<double>("t.k_tput", TK);
+  out->k_bound = la.k_bound = ctx->d<int8_t>("t.k_bound", TK);
+  out->k_roofline_in = la.k_in = ctx->d<uint8_t>("t.k_in", TK);
+  out->l_index = la.l_index = ctx->d<uint32_t>("t.l_index", TL);
+  out->l_row = la.l_row = ctx->d<uint32_t>("t.l_row", TL);
+  out->l_layer_lat = la.l_layer_lat = ctx->d<double>("t.l_layer_lat", TL);
+  out->l_kern_lat = la.l_kern_lat = ctx->d<double>("t.l_kern_lat", TL);
+  out->l_flops = la.l_flops = ctx->d<uint64_t>("t.l_flops", TL);
+  out->l_read = la.l_read = ctx->d<uint64_t>("t.l_read", TL);
+  out->l_write = la.l_write = ctx->d<uint64_t>("t.l_write", TL);
+  out->l_occ = la.l_occ = ctx->d<double>("t.l_occ", TL);
+  out->l_count = la.l_count = ctx->d<uint64_t>("t.l_count", TL);
+  out->l_ai = la.l_ai = ctx->d<double>("t.l_ai", TL);
+  out->l_tput = la.l_tput = ctx->d<double>("t.l_tput", TL);
+  out->l_bound = la.l_bound = ctx->d<int8_t>("t.l_bound", TL);
+  out->l_nongpu = la.l_nongpu = ctx->d<double>("t.l_nongpu", TL);
+  out->l_gpu_share = la.l_gpu_share = ctx->d<double>("t.l_gshare", TL);
+  out->l_nongpu_share = la.l_nongpu_share = ctx->d<double>("t.l_ngshare", TL);
+  out->l_flagged = la.l_flagged = ctx->d<uint8_t>("t.l_flagged", TL);
+  out->l_roofline_in = la.l_in = ctx->d<uint8_t>("t.l_in", TL);
+  out->l_topk = la.l_topk = ctx->d<uint32_t>("t.l_topk", (uint64_t)TL * (opts->top_k ? opts->top_k : 1));
+  launch(ctx, k_layers, TL, st, la);
+
+  // ---- per model
+  ModelArgs ma;
+  ma.G = G;
+  ma.gl_off = out->group_layer_off;
+  ma.gk_off = out->group_kernel_off;
+  ma.ft = ft;
+  ma.nr = nr;
+  ma.batch = batch;
+  ma.gstatus = out->group_status;
+  ma.model_row = corr->trace_model_row;
+  ma.begin = c->begin_ns;
+  ma.end = c->end_ns;
+  ma.k_lat = la.k_lat;
+  ma.k_occ = la.k_occ;
+  ma.k_flops = la.k_flops;
+  ma.k_read = la.k_read;
+  ma.k_write = la.k_write;
+  ma.l_kern_lat = la.l_kern_lat;
+  ma.trim = opts->trim_fraction;
+  ma.peak = la.peak;
+  ma.bw = la.bw;
+  out->m_lat = ma.m_lat = ctx->d<double>("t.m_lat", G);
+  out->m_kern_lat = ma.m_kern_lat = ctx->d<double>("t.m_kern_lat", G);
+  out->m_flops = ma.m_flops = ctx->d<uint64_t>("t.m_flops", G);
+  out->m_read = ma.m_read = ctx->d<uint64_t>("t.m_read", G);
+  out->m_write = ma.m_write = ctx->d<uint64_t>("t.m_write", G);
+  out->m_occ = ma.m_occ = ctx->d<double>("t.m_occ", G);
+  out->m_count = ma.m_count = ctx->d<uint64_t>("t.m_count", G);
+  out->m_ai = ma.m_ai = ctx->d<double>("t.m_ai", G);
+  out->m_tput = ma.m_tput = ctx->d<double>("t.m_tput", G);
+  out->m_bound = ma.m_bound = ctx->d<int8_t>("t.m_bound", G);
+  out->m_gpu = ma.m_gpu = ctx->d<double>("t.m_gpu", G);
+  out->m_gpu_pct = ma.m_gpu_pct = ctx->d<double>("t.m_gpu_pct", G);
+  out->m_throughput = ma.m_throughput = ctx->d<double>("t.m_tp", G);
+  out->m_roofline_in = ma.m_in = ctx->d<uint8_t>("t.m_in", G);
+  launch(ctx, k_models, G, st, ma);
+
+  // ---- a10
+  out->group_name_off = ctx->d<uint32_t>("t.g_noff", G + 1);
+  uint32_t NN = 0;
+  if (TK) {
+    uint64_t* key = ctx->d<uint64_t>("a.nkey", TK);
+    uint32_t* val = ctx->d<uint32_t>("a.nval", TK);
+    launch(ctx, k_name_keys, TK, st, TK, out->group_kernel_off, G, la.k_name, out->group_status, key, val);
+    RadixScratch rs;
+    rs.keys_alt = ctx->d<uint64_t>("rs.keys_alt", TK);
+    rs.vals_alt = ctx->d<uint32_t>("rs.vals_alt", TK);
+    uint64_t ce = radix_counts_elems(TK);
+    rs.counts = ctx->d<uint32_t>("rs.counts", ce);
+    rs.scan_tmp = ctx->d<uint32_t>("rs.scan", scan_scratch_elems(ce));
+    rs.and_or = ctx->d<unsigned long long>("rs.andor", 2);
+    rs.and_or_host = ctx->h<unsigned long long>("rs.andor_h", 2);
+    radix_sort_pairs(key, val, TK, 0, 64, rs, st, &ctx->launches);
+    uint32_t* flag = ctx->d<uint32_t>("a.nflag", TK);
+    uint32_t* pos = ctx->d<uint32_t>("a.npos", TK + 1);
+    launch(ctx, k_seg_flags, TK, st, TK, key, flag);
+    uint32_t* scan2 = ctx->d<uint32_t>("a.scan2", scan_scratch_elems(TK + 16));
+    exclusive_scan<uint32_t, uint32_t>(flag, pos, TK, scan2, pos + TK, st, &ctx->launches);
+    XSP_CUDA(cudaMemcpyAsync(htot + 2, pos + TK, 4, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaStreamSynchronize(st));
+    NN = htot[2];
+    NameArgs na;
+    na.n = TK;
+    na.key = key;
+    na.val = val;
+    na.seg_pos = pos;
+    na.flag = flag;
+    na.k_lat = la.k_lat;
+    na.k_occ = la.k_occ;
+    na.k_flops = la.k_flops;
+    na.k_read = la.k_read;
+    na.k_write = la.k_write;
+    na.m_lat = ma.m_lat;
+    na.peak = la.peak;
+    na.bw = la.bw;
+    na.s_group = ctx->d<uint32_t>("a.s_group", NN);
+    na.s_name = ctx->d<uint32_t>("a.s_name", NN);
+    na.s_count = ctx->d<uint64_t>("a.s_count", NN);
+    na.s_lat = ctx->d<double>("a.s_lat", NN);
+    na.s_pct = ctx->d<double>("a.s_pct", NN);
+    na.s_flops = ctx->d<uint64_t>("a.s_flops", NN);
+    na.s_read = ctx->d<uint64_t>("a.s_read", NN);
+    na.s_write = ctx->d<uint64_t>("a.s_write", NN);
+    na.s_occ = ctx->d<double>("a.s_occ", NN);
+    na.s_ai = ctx->d<double>("a.s_ai", NN);
+    na.s_tput = ctx->d<double>("a.s_tput", NN);
+    na.s_bound = ctx->d<int8_t>("a.s_bound", NN);
+    launch(ctx, k_name_rows, TK, st, na);
+    launch(ctx, k_csr_groups, (uint64_t)G + 1, st, G, NN, na.s_group, out->group_name_off);
+    uint32_t* order = ctx->d<uint32_t>("a.norder", NN);
+    launch(ctx, k_name_order, G, st, G, out->group_name_off, na.s_lat, order);
+    out->n_name = ctx->d<uint32_t>("t.n_name", NN);
+    out->n_count = ctx->d<uint64_t>("t.n_count", NN);
+    out->n_lat = ctx->d<double>("t.n_lat", NN);
+    out->n_pct = ctx->d<double>("t.n_pct", NN);
+    out->n_flops = ctx->d<uint64_t>("t.n_flops", NN);
+    out->n_read = ctx->d<uint64_t>("t.n_read", NN);
+    out->n_write = ctx->d<uint64_t>("t.n_write", NN);
+    out->n_occ = ctx->d<double>("t.n_occ", NN);
+    out->n_ai = ctx->d<double>("t.n_ai", NN);
+    out->n_tput = ctx->d<double>("t.n_tput", NN);
+    out->n_bound = ctx->d<int8_t>("t.n_bound", NN);
+    launch(ctx, k_permute<uint32_t>, NN, st, NN, order, na.s_name, out->n_name);
+    launch(ctx, k_permute<uint64_t>, NN, st, NN, order, na.s_count, out->n_count);
+    launch(ctx, k_permute<double>, NN, st, NN, order, na.s_lat, out->n_lat);
+    launch(ctx, k_permute<double>, NN, st, NN, order, na.s_pct, out->n_pct);
+    launch(ctx, k_permute<uint64_t>, NN, st, NN, order, na.s_flops, out->n_flops);
+    launch(ctx, k_permute<uint64_t>, NN, st, NN, order, na.s_read, out->n_read);
+    launch(ctx, k_permute<uint64_t>, NN, st, NN, order, na.s_write, out->n_write);
+    launch(ctx, k_permute<double>, NN, st, NN, order, na.s_occ, out->n_occ);
+    launch(ctx, k_permute<double>, NN, st, NN, order, na.s_ai, out->n_ai);
+    launch(ctx, k_permute<double>, NN, st, NN, order, na.s_tput, out->n_tput);
+    launch(ctx, k_permute<int8_t>, NN, st, NN, order, na.s_bound, out->n_bound);
+  } else {
+    XSP_CUDA(cudaMemsetAsync(out->group_name_off, 0, (G + 1) * 4ull, st));
+    out->n_name = ctx->d<uint32_t>("t.n_name", 1);
+    out->n_count = ctx->d<uint64_t>("t.n_count", 1);
+    out->n_lat = ctx->d<double>("t.n_lat", 1);
+    out->n_pct = ctx->d<double>("t.n_pct", 1);
+    out->n_flops = ctx->d<uint64_t>("t.n_flops", 1);
+    out->n_read = ctx->d<uint64_t>("t.n_read", 1);
+    out->n_write = ctx->d<uint64_t>("t.n_write", 1);
+    out->n_occ = ctx->d<double>("t.n_occ", 1);
+    out->n_ai = ctx->d<double>("t.n_ai", 1);
+    out->n_tput = ctx->d<double>("t.n_tput", 1);
+    out->n_bound = ctx->d<int8_t>("t.n_bound", 1);
+  }
+  out->n_names = NN;
+}
+
+}  // namespace xsp

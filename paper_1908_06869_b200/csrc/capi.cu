@@ -1,0 +1,241 @@
+// The extern "C" boundary (include/xsp.h): context management, argument
+// checking, error capture, and the host-buffer end-to-end entry point.
+
+#include <cstring>
+#include <new>
+#include <stdexcept>
+
+#include "ctx.h"
+
+#define XSP_API extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+xsp_status guard(xsp_ctx* ctx, const char* what, auto&& body) {
+  if (!ctx) return XSP_E_INVALID;
+  ctx->launches = 0;
+  try {
+    XSP_CUDA(cudaSetDevice(ctx->device));
+    body();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
+    ctx->last_error.clear();
+    return XSP_OK;
+  } catch (const CudaError& e) {
+    ctx->last_error = std::string(what) + ": " + e.what();
+    return XSP_E_CUDA;
+  } catch (const std::invalid_argument& e) {
+    ctx->last_error = std::string(what) + ": " + e.what();
+    return XSP_E_INVALID;
+  } catch (const std::bad_alloc&) {
+    ctx->last_error = std::string(what) + ": host allocation failed";
+    return XSP_E_NOMEM;
+  } catch (const std::runtime_error& e) {
+    ctx->last_error = std::string(what) + ": " + e.what();
+    if (std::string(e.what()) == "UNSORTED") {
+      ctx->last_error = std::string(what) + ": a trace is not in timeline order (begin_ns, rank, span_id)";
+      return XSP_E_UNSORTED;
+    }
+    return XSP_E_INVALID;
+  }
+}
+
+void check_cols(const xsp_span_cols* c, const xsp_traces* t) {
+  if (!c || !t) throw std::invalid_argument("null columns or traces");
+  if (c->n_spans && (!c->span_id || !c->parent_id || !c->begin_ns || !c->end_ns || !c->cid ||
+                     !c->flags || !c->name_id))
+    throw std::invalid_argument("null span column");
+  if (c->n_metric_rows && (!c->flops || !c->dram_read || !c->dram_write || !c->occupancy))
+    throw std::invalid_argument("null metric column");
+  if (c->n_layer_rows && (!c->alloc_bytes || !c->type_id))
+    throw std::invalid_argument("null layer column");
+  if (!t->span_off || (t->n_traces && !t->levels)) throw std::invalid_argument("null trace column");
+}
+
+template <typename T>
+T* to_dev(xsp_ctx* ctx, const std::string& name, const T* src, uint64_t count, cudaStream_t st) {
+  T* d = ctx->d<T>("h2d." + name, count ? count : 1);
+  if (count) {
+    XSP_CUDA(cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
+    ctx->h2d_bytes += count * sizeof(T);
+  }
+  return d;
+}
+
+template <typename T>
+T* to_host(xsp_ctx* ctx, const std::string& name, const T* src, uint64_t count, cudaStream_t st) {
+  T* h = ctx->h<T>("d2h." + name, count ? count : 1);
+  if (count) {
+    XSP_CUDA(cudaMemcpyAsync(h, src, count * sizeof(T), cudaMemcpyDeviceToHost, st));
+    ctx->d2h_bytes += count * sizeof(T);
+  }
+  return h;
+}
+
+}  // namespace
+
+XSP_API int xsp_abi_version(void) { return XSP_ABI_VERSION; }
+
+XSP_API xsp_status xsp_ctx_create(int device, xsp_ctx** out) {
+  if (!out) return XSP_E_INVALID;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return XSP_E_NO_DEVICE;
+  if (device < 0 || device >= n) return XSP_E_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return XSP_E_CUDA;
+  auto* ctx = new (std::nothrow) xsp_ctx;
+  if (!ctx) return XSP_E_NOMEM;
+  ctx->device = device;
+  *out = ctx;
+  return XSP_OK;
+}
+
+XSP_API void xsp_ctx_destroy(xsp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  delete ctx;
+}
+
+XSP_API const char* xsp_last_error(const xsp_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : "null context";
+}
+
+XSP_API uint64_t xsp_last_launch_count(const xsp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+XSP_API void xsp_last_transfer_bytes(const xsp_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
+  if (h2d) *h2d = ctx ? ctx->h2d_bytes : 0;
+  if (d2h) *d2h = ctx ? ctx->d2h_bytes : 0;
+}
+
+XSP_API void* xsp_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+
+XSP_API void xsp_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+XSP_API xsp_status xsp_copy_to_host(xsp_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guard(ctx, "xsp_copy_to_host", [&] {
+    if (bytes) XSP_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+XSP_API xsp_status xsp_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
+                                 int sort_if_needed, xsp_corr_out* out, void* stream) {
+  return guard(ctx, "xsp_correlate", [&] {
+    check_cols(cols, traces);
+    if (!out) throw std::invalid_argument("null output");
+    std::memset(out, 0, sizeof(*out));
+    xsp::run_correlate(ctx, cols, traces, sort_if_needed, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_analyze(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                               const xsp_groups* groups, const xsp_system_spec* spec,
+                               const xsp_analysis_opts* opts, xsp_tables_out* out, void* stream) {
+  return guard(ctx, "xsp_analyze", [&] {
+    if (!cols || !corr || !groups || !spec || !opts || !out) throw std::invalid_argument("null argument");
+    if (groups->n_groups && (!groups->first_trace || !groups->n_runs || !groups->batch_size))
+      throw std::invalid_argument("null group column");
+    std::memset(out, 0, sizeof(*out));
+    xsp::run_analyze(ctx, cols, corr, groups, spec, opts, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht,
+                                const xsp_groups* groups, const xsp_system_spec* spec,
+                                const xsp_analysis_opts* opts, xsp_corr_out* corr_host,
+                                xsp_tables_out* tab_host, void* stream) {
+  return guard(ctx, "xsp_run_host", [&] {
+    check_cols(hc, ht);
+    if (!groups || !spec || !opts || !corr_host || !tab_host) throw std::invalid_argument("null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ctx->h2d_bytes = ctx->d2h_bytes = 0;
+    const uint64_t n = hc->n_spans;
+    xsp_span_cols dc;
+    dc.n_spans = n;
+    dc.span_id = to_dev(ctx, "span_id", hc->span_id, n, st);
+    dc.parent_id = to_dev(ctx, "parent_id", hc->parent_id, n, st);
+    dc.begin_ns = to_dev(ctx, "begin", hc->begin_ns, n, st);
+    dc.end_ns = to_dev(ctx, "end", hc->end_ns, n, st);
+    dc.cid = to_dev(ctx, "cid", hc->cid, n, st);
+    dc.flags = to_dev(ctx, "flags", hc->flags, n, st);
+    dc.name_id = to_dev(ctx, "name", hc->name_id, n, st);
+    dc.n_metric_rows = hc->n_metric_rows;
+    dc.flops = to_dev(ctx, "flops", hc->flops, hc->n_metric_rows, st);
+    dc.dram_read = to_dev(ctx, "read", hc->dram_read, hc->n_metric_rows, st);
+    dc.dram_write = to_dev(ctx, "write", hc->dram_write, hc->n_metric_rows, st);
+    dc.occupancy = to_dev(ctx, "occ", hc->occupancy, hc->n_metric_rows, st);
+    dc.n_layer_rows = hc->n_layer_rows;
+    dc.alloc_bytes = to_dev(ctx, "alloc", hc->alloc_bytes, hc->n_layer_rows, st);
+    dc.type_id = to_dev(ctx, "type", hc->type_id, hc->n_layer_rows, st);
+    xsp_traces dt;
+    dt.n_traces = ht->n_traces;
+    dt.span_off = to_dev(ctx, "span_off", ht->span_off, (uint64_t)ht->n_traces + 1, st);
+    dt.levels = to_dev(ctx, "levels", ht->levels, ht->n_traces, st);
+
+    xsp_corr_out dcorr;
+    std::memset(&dcorr, 0, sizeof(dcorr));
+    xsp::run_correlate(ctx, &dc, &dt, 1, &dcorr, st);
+    xsp_tables_out dtab;
+    std::memset(&dtab, 0, sizeof(dtab));
+    xsp::run_analyze(ctx, &dc, &dcorr, groups, spec, opts, &dtab, st);
+
+    // ---- results back to pinned host memory
+    const uint32_t T = dcorr.n_traces;
+    xsp_corr_out& c = *corr_host;
+    c = dcorr;
+    c.trace_status = to_host(ctx, "t_status", dcorr.trace_status, T, st);
+    c.trace_err_row = to_host(ctx, "t_err", dcorr.trace_err_row, 2ull * T, st);
+    c.trace_model_row = to_host(ctx, "t_model", dcorr.trace_model_row, T, st);
+    c.trace_layer_off = to_host(ctx, "t_loff", dcorr.trace_layer_off, T + 1ull, st);
+    c.trace_kernel_off = to_host(ctx, "t_koff", dcorr.trace_kernel_off, T + 1ull, st);
+    c.trace_orphan_off = to_host(ctx, "t_ooff", dcorr.trace_orphan_off, T + 1ull, st);
+    c.trace_amb_off = to_host(ctx, "t_aoff", dcorr.trace_amb_off, T + 1ull, st);
+    c.layer_row = to_host(ctx, "l_row", dcorr.layer_row, dcorr.n_layers, st);
+    c.layer_kernel_off = to_host(ctx, "l_koff", dcorr.layer_kernel_off, dcorr.n_layers + 1, st);
+    c.layer_dur = to_host(ctx, "l_dur", dcorr.layer_dur, dcorr.n_layers, st);
+    c.layer_attr_row = to_host(ctx, "l_attr", dcorr.layer_attr_row, dcorr.n_layers, st);
+    c.kernel_launch_row = to_host(ctx, "k_launch", dcorr.kernel_launch_row, dcorr.n_kernels, st);
+    c.kernel_exec_row = to_host(ctx, "k_exec", dcorr.kernel_exec_row, dcorr.n_kernels, st);
+    c.kernel_metric_row = to_host(ctx, "k_mrow", dcorr.kernel_metric_row, dcorr.n_kernels, st);
+    c.kernel_dur = to_host(ctx, "k_dur", dcorr.kernel_dur, dcorr.n_kernels, st);
+    c.kernel_name = to_host(ctx, "k_name", dcorr.kernel_name, dcorr.n_kernels, st);
+    c.orphan_row = to_host(ctx, "o_row", dcorr.orphan_row, dcorr.n_orphans, st);
+    c.orphan_reason = to_host(ctx, "o_reason", dcorr.orphan_reason, dcorr.n_orphans, st);
+    c.amb_row = to_host(ctx, "a_row", dcorr.amb_row, dcorr.n_ambiguities, st);
+    c.amb_cand_off = to_host(ctx, "a_coff", dcorr.amb_cand_off, dcorr.n_ambiguities + 1, st);
+    c.amb_cand_row = to_host(ctx, "a_crow", dcorr.amb_cand_row, dcorr.n_candidates, st);
+
+    const uint32_t G = dtab.n_groups;
+    const uint64_t L = dtab.n_layers, K = dtab.n_kernels, N = dtab.n_names;
+    const uint64_t tk = opts->top_k ? opts->top_k : 1;
+    xsp_tables_out& t = *tab_host;
+    t = dtab;
+#define BACK(field, count) t.field = to_host(ctx, "t." #field, dtab.field, (count), st)
+    BACK(group_status, G);
+    BACK(group_err_arg, G);
+    BACK(group_layer_off, G + 1ull);
+    BACK(group_kernel_off, G + 1ull);
+    BACK(group_name_off, G + 1ull);
+    BACK(k_name, K); BACK(k_layer, K); BACK(k_lat, K); BACK(k_flops, K); BACK(k_read, K);
+    BACK(k_write, K); BACK(k_occ, K); BACK(k_ai, K); BACK(k_tput, K); BACK(k_bound, K);
+    BACK(k_roofline_in, K);
+    BACK(l_index, L); BACK(l_row, L); BACK(l_layer_lat, L); BACK(l_kern_lat, L); BACK(l_flops, L);
+    BACK(l_read, L); BACK(l_write, L); BACK(l_occ, L); BACK(l_count, L); BACK(l_ai, L);
+    BACK(l_tput, L); BACK(l_bound, L); BACK(l_nongpu, L); BACK(l_gpu_share, L);
+    BACK(l_nongpu_share, L); BACK(l_flagged, L); BACK(l_roofline_in, L); BACK(l_topk, L * tk);
+    BACK(n_name, N); BACK(n_count, N); BACK(n_lat, N); BACK(n_pct, N); BACK(n_flops, N);
+    BACK(n_read, N); BACK(n_write, N); BACK(n_occ, N); BACK(n_ai, N); BACK(n_tput, N);
+    BACK(n_bound, N);
+    BACK(m_lat, G); BACK(m_kern_lat, G); BACK(m_flops, G); BACK(m_read, G); BACK(m_write, G);
+    BACK(m_occ, G); BACK(m_count, G); BACK(m_ai, G); BACK(m_tput, G); BACK(m_bound, G);
+    BACK(m_gpu, G); BACK(m_gpu_pct, G); BACK(m_throughput, G); BACK(m_roofline_in, G);
+#undef BACK
+    XSP_CUDA(cudaStreamSynchronize(st));
+  });
+}

@@ -1,0 +1,1315 @@
+// Stages (c) + (d): parent assignment by interval containment and the
+// correlation-id launch->exec join, for every trace of a batch at once.
+//
+// Reference semantics: assign_parents (correlator.cpp:141-282) and
+// correlate_async (correlator.cpp:287-364). The reference walks an interval
+// tree per child span; here the whole batch is ONE decoupled-look-back scan
+// over the timeline-ordered span columns (pass 1):
+//   * layers are placed by a per-span compare against their trace's model span
+//     and numbered by a global placed-layer count (layer_index = count - trace base);
+//   * every child span carries the scan state "top-2 end_ns among the placed
+//     layers that precede it in its trace" (+ the arg of the max). Because the
+//     input is sorted by (begin, rank, span_id), exactly the preceding placed
+//     layers have begin <= child.begin, so the containment candidates are the
+//     preceding layers with end >= child.end: 0 -> orphan, 1 -> the argmax,
+//     >= 2 -> ambiguity (full candidate list built on a rare path);
+//   * execs and kernel launches are compacted into timeline-ordered lists.
+// The cid join is a per-trace open-addressing table in HBM/L2.
+// Orphans, ambiguities and explicit-parent kernels are rare: they are appended
+// to exception lists and put into the reference's output order by radix sort.
+
+#include "ctx.h"
+#include "prims.cuh"
+
+namespace xsp {
+
+constexpr uint32_t PAR_ORPHAN = 0xFFFFFFFFu;
+constexpr uint32_t PAR_AMBIG = 0xFFFFFFFEu;
+constexpr uint32_t PAR_PENDING = 0xFFFFFFFDu;
+constexpr uint32_t PAR_MAXROW = 0xFFFFFFF0u;
+
+// Orphan categories = the reference's emission phases, in output order.
+enum : uint32_t {
+  CAT_LAYER = 0,     // layer pass, timeline order            (correlator.cpp:168-204)
+  CAT_KERNEL = 1,    // kernel pass, timeline order           (:226-259)
+  CAT_EXEC_NOCID = 2,// exec without cid, timeline order      (:289-295)
+  CAT_LAUNCH = 3,    // launch fusion failures, tree order    (:321-346)
+  CAT_LEFTOVER = 4   // unconsumed execs, by span_id          (:355-363)
+};
+
+// kl_info bits
+constexpr uint8_t KL_SYNC = 1, KL_CID = 2, KL_LAUNCH = 4;
+
+struct Orphans {
+  uint64_t* tc;   // trace << 3 | category
+  uint64_t* key;  // order key within the category
+  uint32_t* row;
+  uint8_t* reason;
+  uint32_t* count;
+};
+
+__device__ __forceinline__ void emit_orphan(const Orphans& o, uint32_t t, uint32_t cat,
+                                            uint64_t key, uint32_t row, uint8_t reason) {
+  uint32_t s = atomicAdd(o.count, 1u);
+  o.tc[s] = ((uint64_t)t << 3) | cat;
+  o.key[s] = key;
+  o.row[s] = row;
+  o.reason[s] = reason;
+}
+
+// ---------------------------------------------------------------------------
+// K0: per trace, the model span = first MODEL/SYNC span (TraceBundle::model_span,
+// span.cpp:298-303). One warp per trace; the model span is normally row 0.
+
+__global__ void k_trace_prep(const uint8_t* __restrict__ flags, const uint64_t* __restrict__ begin,
+                             const uint64_t* __restrict__ end, const uint64_t* __restrict__ sid,
+                             const uint64_t* __restrict__ off, uint32_t T,
+                             uint32_t* __restrict__ model_row, uint64_t* __restrict__ mb,
+                             uint64_t* __restrict__ me, uint64_t* __restrict__ msid,
+                             unsigned long long* __restrict__ err_key) {
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = lane_id();
+  if (t >= T) return;
+  const uint64_t lo = off[t], hi = off[t + 1];
+  uint64_t found = ~0ull;
+  for (uint64_t base = lo; base < hi; base += 32) {
+    uint64_t i = base + lane;
+    bool m = i < hi && is_model_span(flags[i]);
+    uint32_t bal = __ballot_sync(0xffffffffu, m);
+    if (bal) {
+      found = base + (__ffs(bal) - 1);
+      break;
+    }
+  }
+  if (lane == 0) {
+    err_key[t] = ~0ull;
+    if (found != ~0ull) {
+      model_row[t] = (uint32_t)found;
+      mb[t] = begin[found];
+      me[t] = end[found];
+      msid[t] = sid[found];
+    } else {
+      model_row[t] = kNone;
+      mb[t] = 1;
+      me[t] = 0;  // contains nothing
+      msid[t] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass-1 scan state.
+
+struct T2 {  // top-2 end_ns over placed layers of the current trace segment
+  uint64_t m1, m2;
+  uint32_t a1;  // layer row (relative to the range's start count) of m1
+  uint32_t n;   // number of layers seen, saturating at 2
+};
+
+struct Seg {
+  uint32_t c;     // placed layers in the range (shifts args)
+  uint32_t head;  // range contains the first span of a trace
+  T2 t;
+};
+
+struct Full {
+  uint64_t m1, m2;
+  uint32_t a1, n, c, head;
+  uint32_t c_metric, c_lay, c_kl, c_ex;
+};
+static_assert(sizeof(Full) == 48, "Full layout");
+
+__device__ __forceinline__ T2 t2_merge(const T2& x, const T2& y) {
+  if (x.n == 0) return y;
+  if (y.n == 0) return x;
+  T2 r;
+  if (y.m1 > x.m1) {
+    r.m1 = y.m1;
+    r.a1 = y.a1;
+  } else {
+    r.m1 = x.m1;
+    r.a1 = x.a1;
+  }
+  uint64_t s = x.m1 < y.m1 ? x.m1 : y.m1;
+  if (x.n >= 2 && x.m2 > s) s = x.m2;
+  if (y.n >= 2 && y.m2 > s) s = y.m2;
+  r.m2 = s;
+  r.n = 2;
+  return r;
+}
+
+__device__ __forceinline__ Seg seg_combine(const Seg& a, const Seg& b) {
+  Seg r;
+  r.c = a.c + b.c;
+  r.head = a.head | b.head;
+  T2 bs = b.t;
+  bs.a1 += a.c;
+  r.t = b.head ? bs : t2_merge(a.t, bs);
+  return r;
+}
+
+__device__ __forceinline__ Full full_combine(const Full& a, const Full& b) {
+  Seg sa{a.c, a.head, {a.m1, a.m2, a.a1, a.n}};
+  Seg sb{b.c, b.head, {b.m1, b.m2, b.a1, b.n}};
+  Seg s = seg_combine(sa, sb);
+  Full r;
+  r.m1 = s.t.m1;
+  r.m2 = s.t.m2;
+  r.a1 = s.t.a1;
+  r.n = s.t.n;
+  r.c = s.c;
+  r.head = s.head;
+  r.c_metric = a.c_metric + b.c_metric;
+  r.c_lay = a.c_lay + b.c_lay;
+  r.c_kl = a.c_kl + b.c_kl;
+  r.c_ex = a.c_ex + b.c_ex;
+  return r;
+}
+
+__device__ __forceinline__ Full full_identity() {
+  Full f;
+  f.m1 = f.m2 = 0;
+  f.a1 = f.n = f.c = f.head = 0;
+  f.c_metric = f.c_lay = f.c_kl = f.c_ex = 0;
+  return f;
+}
+
+__device__ __forceinline__ Seg shfl_up_seg(const Seg& v, int o) {
+  Seg u;
+  u.c = __shfl_up_sync(0xffffffffu, v.c, o);
+  u.head = __shfl_up_sync(0xffffffffu, v.head, o);
+  u.t.m1 = __shfl_up_sync(0xffffffffu, v.t.m1, o);
+  u.t.m2 = __shfl_up_sync(0xffffffffu, v.t.m2, o);
+  u.t.a1 = __shfl_up_sync(0xffffffffu, v.t.a1, o);
+  u.t.n = __shfl_up_sync(0xffffffffu, v.t.n, o);
+  return u;
+}
+
+__device__ __forceinline__ Seg warp_inclusive_seg(Seg v) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Seg u = shfl_up_seg(v, o);
+    if (lane >= (uint32_t)o) v = seg_combine(u, v);
+  }
+  return v;
+}
+
+__device__ __forceinline__ Seg shfl_seg(const Seg& v, int src) {
+  Seg u;
+  u.c = __shfl_sync(0xffffffffu, v.c, src);
+  u.head = __shfl_sync(0xffffffffu, v.head, src);
+  u.t.m1 = __shfl_sync(0xffffffffu, v.t.m1, src);
+  u.t.m2 = __shfl_sync(0xffffffffu, v.t.m2, src);
+  u.t.a1 = __shfl_sync(0xffffffffu, v.t.a1, src);
+  u.t.n = __shfl_sync(0xffffffffu, v.t.n, src);
+  return u;
+}
+
+__device__ __forceinline__ void store_full(Full* dst, const Full& v) {
+  const uint4* s = reinterpret_cast<const uint4*>(&v);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  __stcg(d + 0, s[0]);
+  __stcg(d + 1, s[1]);
+  __stcg(d + 2, s[2]);
+}
+__device__ __forceinline__ Full load_full(const Full* src) {
+  Full v;
+  uint4* d = reinterpret_cast<uint4*>(&v);
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  d[0] = __ldcg(s + 0);
+  d[1] = __ldcg(s + 1);
+  d[2] = __ldcg(s + 2);
+  return v;
+}
+
+constexpr int P1_WARPS = 8;
+constexpr int P1_CHUNKS = 8;
+constexpr int P1_SUB = P1_CHUNKS * 32;
+constexpr int P1_TILE = P1_WARPS * P1_SUB;
+
+struct P1Args {
+  const uint8_t* flags;
+  const uint64_t* begin;
+  const uint64_t* end;
+  const uint64_t* parent;
+  const uint64_t* cid;
+  const uint32_t* name;
+  uint64_t n;
+  const uint64_t* off;
+  uint32_t T;
+  const uint32_t* levels;
+  const uint32_t* model_row;
+  const uint64_t* mb;
+  const uint64_t* me;
+  const uint64_t* msid;
+  uint32_t* tile_ticket;
+  uint32_t* tile_flag;
+  Full* tile_agg;
+  Full* tile_inc;
+  unsigned long long* err_key;
+  uint32_t* layer_row;
+  uint64_t* layer_dur;
+  uint32_t* layer_attr_row;
+  uint64_t* layer_end;
+  uint32_t* kl_row;
+  uint32_t* kl_parent;
+  uint64_t* kl_cid;
+  uint8_t* kl_info;
+  uint64_t* kl_dur;
+  uint32_t* kl_mrow;
+  uint32_t* kl_name;
+  uint32_t* ex_row;
+  uint64_t* ex_cid;
+  uint64_t* ex_dur;
+  uint32_t* ex_mrow;
+  uint32_t* ex_name;
+  uint32_t* t_layer_off;
+  uint32_t* t_kl_off;
+  uint32_t* t_ex_off;
+  Orphans orph;
+  uint32_t* amb_kl;
+  uint32_t* amb_gx;
+  uint32_t* amb_count;
+  uint32_t* pend_kl;
+  uint32_t* pend_count;
+};
+
+// Layer placement under the model span (correlator.cpp:169-194).
+__device__ __forceinline__ bool layer_placed(uint8_t f, uint64_t b, uint64_t e, uint64_t i,
+                                             uint32_t t, const P1Args& a) {
+  if (a.model_row[t] == kNone) return false;
+  if (f & XSP_F_PARENT) return __ldg(a.parent + i) == a.msid[t];
+  return a.mb[t] <= b && e <= a.me[t];
+}
+
+__global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_tlo, s_thi;
+  __shared__ Full s_wagg[P1_WARPS];
+  __shared__ Full s_prefix;
+
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t tile_base = (uint64_t)tile * P1_TILE;
+  if (threadIdx.x == 0) {
+    uint64_t last = tile_base + P1_TILE;
+    if (last > a.n) last = a.n;
+    uint32_t lo = trace_of(a.off, 0, a.T, tile_base);
+    uint32_t hi = trace_of(a.off, lo, a.T, last - 1) + 1;
+    s_tlo = lo;
+    s_thi = hi;
+  }
+  __syncthreads();
+  const uint32_t tlo = s_tlo, thi = s_thi;
+  const uint64_t wbase = tile_base + (uint64_t)warp * P1_SUB;
+
+  // ---- phase 1: warp aggregate over this warp's 8 chunks ----------------
+  uint8_t fr[P1_CHUNKS];
+  uint64_t br[P1_CHUNKS], er[P1_CHUNKS];
+#pragma unroll
+  for (int c = 0; c < P1_CHUNKS; ++c) {
+    uint64_t i = wbase + c * 32 + lane;
+    bool v = i < a.n;
+    fr[c] = v ? __ldg(a.flags + i) : (uint8_t)0xFF;
+    br[c] = v ? __ldg(a.begin + i) : 0;
+    er[c] = v ? __ldg(a.end + i) : 0;
+  }
+  Full wagg = full_identity();
+#pragma unroll
+  for (int c = 0; c < P1_CHUNKS; ++c) {
+    uint64_t i = wbase + c * 32 + lane;
+    bool v = i < a.n;
+    uint8_t f = fr[c];
+    uint32_t t = v ? trace_of(a.off, tlo, thi, i) : 0;
+    bool head = v && a.off[t] == i;
+    bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
+    bool placed = is_layer && f_kind(f) == XSP_KIND_SYNC && layer_placed(f, br[c], er[c], i, t, a);
+    bool kl = v && (is_kernel_launch(f) || is_sync_kernel(f));
+    bool ex = v && is_exec(f) && (f & XSP_F_CID);
+    bool met = v && (f & XSP_F_METRICS);
+    Seg e;
+    e.c = placed;
+    e.head = head;
+    e.t.m1 = placed ? er[c] : 0;
+    e.t.m2 = 0;
+    e.t.a1 = 0;
+    e.t.n = placed ? 1u : 0u;
+    uint32_t bal_any = __ballot_sync(0xffffffffu, placed || head);
+    Seg tot;
+    if (bal_any) {
+      Seg inc = warp_inclusive_seg(e);
+      tot = shfl_seg(inc, 31);
+    } else {
+      tot.c = 0;
+      tot.head = 0;
+      tot.t.n = 0;
+      tot.t.m1 = tot.t.m2 = 0;
+      tot.t.a1 = 0;
+    }
+    Full ch;
+    ch.m1 = tot.t.m1;
+    ch.m2 = tot.t.m2;
+    ch.a1 = tot.t.a1;
+    ch.n = tot.t.n;
+    ch.c = tot.c;
+    ch.head = tot.head;
+    ch.c_metric = __popc(__ballot_sync(0xffffffffu, met));
+    ch.c_lay = __popc(__ballot_sync(0xffffffffu, is_layer));
+    ch.c_kl = __popc(__ballot_sync(0xffffffffu, kl));
+    ch.c_ex = __popc(__ballot_sync(0xffffffffu, ex));
+    wagg = full_combine(wagg, ch);
+  }
+  if (lane == 0) s_wagg[warp] = wagg;
+  __syncthreads();
+
+  // ---- phase 2: tile aggregate + decoupled look-back ---------------------
+  if (threadIdx.x == 0) {
+    Full agg = s_wagg[0];
+    for (int w = 1; w < P1_WARPS; ++w) agg = full_combine(agg, s_wagg[w]);
+    Full prefix = full_identity();
+    if (tile == 0) {
+      store_full(a.tile_inc + tile, agg);
+      __threadfence();
+      atomicExch(a.tile_flag + tile, 2u);
+    } else {
+      store_full(a.tile_agg + tile, agg);
+      __threadfence();
+      atomicExch(a.tile_flag + tile, 1u);
+      Full acc = full_identity();
+      bool have = false;
+      for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
+        uint32_t fl;
+        do {
+          fl = *((volatile uint32_t*)(a.tile_flag + j));
+        } while (fl == 0);
+        __threadfence();
+        if (fl == 2) {
+          Full inc = load_full(a.tile_inc + j);
+          acc = have ? full_combine(inc, acc) : inc;
+          have = true;
+          break;
+        }
+        Full ag = load_full(a.tile_agg + j);
+        acc = have ? full_combine(ag, acc) : ag;
+        have = true;
+      }
+      prefix = acc;
+      store_full(a.tile_inc + tile, full_combine(prefix, agg));
+      __threadfence();
+      atomicExch(a.tile_flag + tile, 2u);
+    }
+    s_prefix = prefix;
+  }
+  __syncthreads();
+
+  Full carry = s_prefix;
+  for (uint32_t w = 0; w < warp; ++w) carry = full_combine(carry, s_wagg[w]);
+
+  // ---- phase 3: per-span outputs ----------------------------------------
+  const uint32_t lt = lanemask_lt();
+  for (int c = 0; c < P1_CHUNKS; ++c) {
+    uint64_t i = wbase + c * 32 + lane;
+    bool v = i < a.n;
+    uint8_t f = v ? __ldg(a.flags + i) : (uint8_t)0xFF;
+    uint64_t b = v ? __ldg(a.begin + i) : 0;
+    uint64_t e = v ? __ldg(a.end + i) : 0;
+    uint32_t t = v ? trace_of(a.off, tlo, thi, i) : 0;
+    bool head = v && a.off[t] == i;
+    bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
+    bool layer_sync = is_layer && f_kind(f) == XSP_KIND_SYNC;
+    bool placed = layer_sync && layer_placed(f, b, e, i, t, a);
+    bool kl = v && (is_kernel_launch(f) || is_sync_kernel(f));
+    bool exe = v && is_exec(f);
+    bool ex = exe && (f & XSP_F_CID);
+    bool met = v && (f & XSP_F_METRICS);
+
+    uint32_t bal_p = __ballot_sync(0xffffffffu, placed);
+    uint32_t bal_m = __ballot_sync(0xffffffffu, met);
+    uint32_t bal_l = __ballot_sync(0xffffffffu, is_layer);
+    uint32_t bal_k = __ballot_sync(0xffffffffu, kl);
+    uint32_t bal_x = __ballot_sync(0xffffffffu, ex);
+    const uint32_t g_ex = carry.c + __popc(bal_p & lt);
+    const uint32_t m_ex = carry.c_metric + __popc(bal_m & lt);
+    const uint32_t l_ex = carry.c_lay + __popc(bal_l & lt);
+    const uint32_t k_ex = carry.c_kl + __popc(bal_k & lt);
+    const uint32_t x_ex = carry.c_ex + __popc(bal_x & lt);
+
+    Seg cs{carry.c, carry.head, {carry.m1, carry.m2, carry.a1, carry.n}};
+    Seg inc = cs;
+    if (__ballot_sync(0xffffffffu, placed || head)) {
+      Seg el;
+      el.c = placed;
+      el.head = head;
+      el.t.m1 = placed ? e : 0;
+      el.t.m2 = 0;
+      el.t.a1 = 0;
+      el.t.n = placed ? 1u : 0u;
+      Seg wi = warp_inclusive_seg(el);
+      inc = seg_combine(cs, wi);
+    }
+
+    if (v) {
+      // trace errors raised while walking the bundle (correlator.cpp:146-158)
+      if (is_model_span(f) && (uint32_t)i != a.model_row[t])
+        atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_MULTI_MODEL);
+      if (f_level(f) >= XSP_LEVEL_KERNEL && !(a.levels[t] & (1u << XSP_LEVEL_LAYER)))
+        atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_SKIP_LEVEL);
+
+      if (is_layer) {
+        if (layer_sync) {
+          if (placed) {
+            a.layer_row[g_ex] = (uint32_t)i;
+            a.layer_dur[g_ex] = clamp_dur(b, e);
+            a.layer_attr_row[g_ex] = l_ex;
+            a.layer_end[g_ex] = e;
+          } else {
+            emit_orphan(a.orph, t, CAT_LAYER, i, (uint32_t)i,
+                        (f & XSP_F_PARENT) ? XSP_O_LAYER_BAD_PARENT : XSP_O_LAYER_OUTSIDE_MODEL);
+          }
+        } else {
+          emit_orphan(a.orph, t, CAT_LAYER, i, (uint32_t)i, XSP_O_LAYER_NON_SYNC);
+        }
+      }
+      if (kl) {
+        const bool sync = is_sync_kernel(f);
+        a.kl_row[k_ex] = (uint32_t)i;
+        a.kl_cid[k_ex] = (f & XSP_F_CID) ? __ldg(a.cid + i) : 0;
+        a.kl_info[k_ex] = (uint8_t)((sync ? KL_SYNC : 0) | ((f & XSP_F_CID) ? KL_CID : 0) |
+                                    (sync ? 0 : KL_LAUNCH));
+        if (sync) {
+          a.kl_dur[k_ex] = clamp_dur(b, e);
+          a.kl_mrow[k_ex] = met ? m_ex : kNone;
+          a.kl_name[k_ex] = __ldg(a.name + i);
+        }
+        uint32_t par;
+        if (f & XSP_F_PARENT) {
+          par = PAR_PENDING;
+          uint32_t s = atomicAdd(a.pend_count, 1u);
+          a.pend_kl[s] = k_ex;
+        } else {
+          uint32_t cands = (inc.t.n >= 1 && inc.t.m1 >= e) + (inc.t.n >= 2 && inc.t.m2 >= e);
+          if (cands == 0) {
+            par = PAR_ORPHAN;
+            emit_orphan(a.orph, t, CAT_KERNEL, i, (uint32_t)i, XSP_O_KERNEL_NO_LAYER);
+          } else if (cands == 1) {
+            par = inc.t.a1;
+          } else {
+            par = PAR_AMBIG;
+            uint32_t s = atomicAdd(a.amb_count, 1u);
+            a.amb_kl[s] = k_ex;
+            a.amb_gx[s] = g_ex;
+          }
+        }
+        a.kl_parent[k_ex] = par;
+      }
+      if (exe) {
+        if (ex) {
+          a.ex_row[x_ex] = (uint32_t)i;
+          a.ex_cid[x_ex] = __ldg(a.cid + i);
+          a.ex_dur[x_ex] = clamp_dur(b, e);
+          a.ex_mrow[x_ex] = met ? m_ex : kNone;
+          a.ex_name[x_ex] = __ldg(a.name + i);
+        } else {
+          emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
+        }
+      }
+      if (head) {
+        int64_t tt = t;
+        do {
+          a.t_layer_off[tt] = g_ex;
+          a.t_kl_off[tt] = k_ex;
+          a.t_ex_off[tt] = x_ex;
+          --tt;
+        } while (tt >= 0 && a.off[tt] == i);
+      }
+    }
+    // carry += chunk
+    Full ch;
+    Seg last = shfl_seg(inc, 31);
+    ch.m1 = last.t.m1;
+    ch.m2 = last.t.m2;
+    ch.a1 = last.t.a1;
+    ch.n = last.t.n;
+    ch.c = last.c;
+    ch.head = last.head;
+    ch.c_metric = carry.c_metric + __popc(bal_m);
+    ch.c_lay = carry.c_lay + __popc(bal_l);
+    ch.c_kl = carry.c_kl + __popc(bal_k);
+    ch.c_ex = carry.c_ex + __popc(bal_x);
+    carry = ch;
+  }
+}
+
+// Offsets of traces that start at or after the end of the span table (empty
+// trailing traces) and the [T] sentinel.
+__global__ void k_pass1_tail(const uint64_t* __restrict__ off, uint32_t T, uint64_t n,
+                             const Full* __restrict__ tile_inc, uint32_t ntiles,
+                             uint32_t* t_layer_off, uint32_t* t_kl_off, uint32_t* t_ex_off,
+                             uint32_t* totals) {
+  Full tot = ntiles ? load_full(tile_inc + ntiles - 1) : full_identity();
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= T; t += gridDim.x * blockDim.x) {
+    if (off[t] >= n) {
+      t_layer_off[t] = tot.c;
+      t_kl_off[t] = tot.c_kl;
+      t_ex_off[t] = tot.c_ex;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    totals[0] = tot.c;
+    totals[1] = tot.c_kl;
+    totals[2] = tot.c_ex;
+    totals[3] = tot.c_metric;
+    totals[4] = tot.c_lay;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Explicit-parent kernels (correlator.cpp:232-240): the parent must be a
+// placed layer of the same trace; layer_by_span_id keeps the LAST layer (in
+// layer_index order) with a given span_id (map assignment, :217-219).
+
+__device__ __forceinline__ uint32_t trace_of32(const uint32_t* __restrict__ off, uint32_t T,
+                                               uint32_t i) {
+  uint32_t lo = 0, hi = T;  // off[lo] <= i < off[hi]
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (off[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// per trace: are placed-layer span_ids non-decreasing in layer order?
+__global__ void k_layer_ids_sorted(const uint32_t* __restrict__ layer_row, const uint64_t* __restrict__ sid,
+                                   const uint32_t* __restrict__ t_layer_off, uint32_t T, uint32_t nl,
+                                   uint32_t* __restrict__ t_unsorted) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g + 1 >= nl) return;
+  uint32_t t = trace_of32(t_layer_off, T, g);
+  if (t_layer_off[t + 1] <= g + 1) return;  // g is the trace's last layer
+  if (sid[layer_row[g]] > sid[layer_row[g + 1]]) t_unsorted[t] = 1;
+}
+
+__global__ void k_resolve_explicit(const uint32_t* __restrict__ pend_kl, const uint32_t* __restrict__ pend_count,
+                                   const uint32_t* __restrict__ kl_row, uint32_t* __restrict__ kl_parent,
+                                   const uint64_t* __restrict__ parent, const uint64_t* __restrict__ sid,
+                                   const uint32_t* __restrict__ layer_row, const uint32_t* __restrict__ t_layer_off,
+                                   const uint32_t* __restrict__ t_kl_off, uint32_t T,
+                                   const uint32_t* __restrict__ t_unsorted, Orphans orph) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= *pend_count) return;
+  uint32_t k = pend_kl[p];
+  uint32_t i = kl_row[k];
+  uint32_t t = trace_of32(t_kl_off, T, k);
+  uint64_t want = parent[i];
+  uint32_t lo = t_layer_off[t], hi = t_layer_off[t + 1];
+  uint32_t found = kNone;
+  if (!t_unsorted[t]) {
+    // last g in [lo, hi) with sid <= want, then check equality
+    uint32_t l = lo, h = hi;
+    while (l < h) {
+      uint32_t mid = (l + h) >> 1;
+      if (sid[layer_row[mid]] <= want) l = mid + 1; else h = mid;
+    }
+    if (l > lo && sid[layer_row[l - 1]] == want) found = l - 1;
+  } else {
+    for (uint32_t g = lo; g < hi; ++g)
+      if (sid[layer_row[g]] == want) found = g;
+  }
+  if (found == kNone) {
+    kl_parent[k] = PAR_ORPHAN;
+    emit_orphan(orph, t, CAT_KERNEL, i, i, XSP_O_KERNEL_BAD_PARENT);
+  } else {
+    kl_parent[k] = found;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Ambiguities (correlator.cpp:242-257): all placed layers of the trace that
+// precede the child in timeline order (g < gx) with end >= child end.
+
+__global__ void k_amb_keys(const uint32_t* __restrict__ amb_kl, const uint32_t* __restrict__ amb_count,
+                           const uint32_t* __restrict__ kl_row, const uint64_t* __restrict__ sid,
+                           const uint32_t* __restrict__ t_kl_off, uint32_t T,
+                           uint64_t* __restrict__ key_sid, uint64_t* __restrict__ key_trace,
+                           uint32_t* __restrict__ idx) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= *amb_count) return;
+  uint32_t k = amb_kl[p];
+  key_sid[p] = sid[kl_row[k]];
+  key_trace[p] = trace_of32(t_kl_off, T, k);
+  idx[p] = p;
+}
+
+__global__ void k_amb_count(const uint32_t* __restrict__ order, uint32_t n_amb,
+                            const uint32_t* __restrict__ amb_kl, const uint32_t* __restrict__ amb_gx,
+                            const uint32_t* __restrict__ kl_row, const uint64_t* __restrict__ end,
+                            const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_layer_off,
+                            uint32_t T, const uint64_t* __restrict__ layer_end, uint32_t* __restrict__ cnt) {
+  uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_amb) return;
+  uint32_t p = order[q];
+  uint32_t k = amb_kl[p];
+  uint32_t t = trace_of32(t_kl_off, T, k);
+  uint64_t e = end[kl_row[k]];
+  uint32_t c = 0;
+  for (uint32_t g = t_layer_off[t]; g < amb_gx[p]; ++g) c += layer_end[g] >= e;
+  cnt[q] = c;
+}
+
+__global__ void k_amb_fill(const uint32_t* __restrict__ order, uint32_t n_amb,
+                           const uint32_t* __restrict__ amb_kl, const uint32_t* __restrict__ amb_gx,
+                           const uint32_t* __restrict__ kl_row, const uint64_t* __restrict__ end,
+                           const uint64_t* __restrict__ sid, const uint32_t* __restrict__ t_kl_off,
+                           const uint32_t* __restrict__ t_layer_off, uint32_t T,
+                           const uint64_t* __restrict__ layer_end, const uint32_t* __restrict__ layer_row,
+                           const uint32_t* __restrict__ cand_off, uint32_t* __restrict__ amb_row,
+                           uint32_t* __restrict__ cand_row) {
+  uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_amb) return;
+  uint32_t p = order[q];
+  uint32_t k = amb_kl[p];
+  uint32_t t = trace_of32(t_kl_off, T, k);
+  uint64_t e = end[kl_row[k]];
+  amb_row[q] = kl_row[k];
+  uint32_t o = cand_off[q], n = 0;
+  for (uint32_t g = t_layer_off[t]; g < amb_gx[p]; ++g) {
+    if (layer_end[g] < e) continue;
+    // insertion by span_id (IntervalTree::containing sorts by span_id, :115-117)
+    uint32_t r = layer_row[g];
+    uint64_t s = sid[r];
+    uint32_t j = n;
+    while (j > 0 && sid[cand_row[o + j - 1]] > s) {
+      cand_row[o + j] = cand_row[o + j - 1];
+      --j;
+    }
+    cand_row[o + j] = r;
+    ++n;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// (d) cid join: one open-addressing region per trace, sized 2x its items.
+
+__device__ __forceinline__ uint32_t mix32(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return (uint32_t)x;
+}
+
+__global__ void k_region_size(const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
+                              uint32_t T, uint64_t* __restrict__ rsize) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  uint64_t items = (uint64_t)(t_kl_off[t + 1] - t_kl_off[t]) + (t_ex_off[t + 1] - t_ex_off[t]);
+  uint64_t want = items * 2;
+  uint64_t s = 16;
+  while (s < want) s <<= 1;
+  rsize[t] = items ? s : 0;
+}
+
+struct JoinArgs {
+  const uint64_t* ex_cid;
+  const uint64_t* kl_cid;
+  const uint8_t* kl_info;
+  const uint32_t* t_ex_off;
+  const uint32_t* t_kl_off;
+  uint32_t T;
+  uint32_t n_ex, n_kl;
+  const uint64_t* roff;  // region offsets [T+1]
+  uint32_t* owner;       // 0 empty, else item + 1
+  uint32_t* sl_exec;     // min exec item
+  uint32_t* sl_launch;   // min klist item
+  uint32_t* ex_slot;
+  uint32_t* kl_slot;
+  uint32_t* t_dup;       // bit0 exec dup, bit1 launch dup
+};
+
+// Items 0..n_ex-1 are execs, n_ex..n_ex+n_kl-1 are klist entries (launches with cid).
+__global__ void k_join_insert(JoinArgs a) {
+  uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= a.n_ex + a.n_kl) return;
+  const bool is_ex = it < a.n_ex;
+  uint32_t t;
+  uint64_t cid;
+  if (is_ex) {
+    t = trace_of32(a.t_ex_off, a.T, it);
+    cid = a.ex_cid[it];
+  } else {
+    uint32_t k = it - a.n_ex;
+    uint8_t info = a.kl_info[k];
+    if (!(info & KL_LAUNCH) || !(info & KL_CID)) return;
+    t = trace_of32(a.t_kl_off, a.T, k);
+    cid = a.kl_cid[k];
+  }
+  const uint64_t base = a.roff[t];
+  const uint32_t mask = (uint32_t)(a.roff[t + 1] - base - 1);
+  uint32_t h = mix32(cid) & mask;
+  for (;;) {
+    uint32_t* slot = a.owner + base + h;
+    uint32_t o = *((volatile uint32_t*)slot);
+    if (o == 0) {
+      o = atomicCAS(slot, 0u, it + 1);
+      if (o == 0) break;
+    }
+    uint32_t oi = o - 1;
+    uint64_t ocid = oi < a.n_ex ? a.ex_cid[oi] : a.kl_cid[oi - a.n_ex];
+    if (ocid == cid) break;
+    h = (h + 1) & mask;
+  }
+  const uint32_t s = (uint32_t)(base + h);
+  if (is_ex) {
+    a.ex_slot[it] = s;
+    if (atomicMin(a.sl_exec + s, it) != kNone) atomicOr(a.t_dup + t, 1u);
+  } else {
+    uint32_t k = it - a.n_ex;
+    a.kl_slot[k] = s;
+    if (atomicMin(a.sl_launch + s, k) != kNone) atomicOr(a.t_dup + t, 2u);
+  }
+}
+
+// Exact duplicate report: the first item in timeline order whose cid was seen
+// before, and that earlier (first) item (correlator.cpp:296-316).
+__global__ void k_join_dups(JoinArgs a, unsigned long long* __restrict__ dup_ex,
+                            unsigned long long* __restrict__ dup_kl) {
+  uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= a.n_ex + a.n_kl) return;
+  if (it < a.n_ex) {
+    uint32_t t = trace_of32(a.t_ex_off, a.T, it);
+    if (!(a.t_dup[t] & 1u)) return;
+    uint32_t first = a.sl_exec[a.ex_slot[it]];
+    if (first != it) atomicMin(dup_ex + t, ((unsigned long long)it << 32) | first);
+  } else {
+    uint32_t k = it - a.n_ex;
+    uint8_t info = a.kl_info[k];
+    if (!(info & KL_LAUNCH) || !(info & KL_CID)) return;
+    uint32_t t = trace_of32(a.t_kl_off, a.T, k);
+    if (!(a.t_dup[t] & 2u)) return;
+    uint32_t first = a.sl_launch[a.kl_slot[k]];
+    if (first != k) atomicMin(dup_kl + t, ((unsigned long long)k << 32) | first);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Kernel fusion (correlator.cpp:321-346) + kept flags; leftover execs (:348-363).
+
+struct FuseArgs {
+  uint32_t n_kl, n_ex, T;
+  const uint32_t* kl_row;
+  const uint32_t* kl_parent;
+  const uint8_t* kl_info;
+  const uint32_t* kl_slot;
+  const uint32_t* sl_exec;
+  const uint32_t* sl_launch;
+  const uint32_t* ex_slot;
+  const uint32_t* ex_row;
+  const uint64_t* sid;
+  const uint32_t* t_kl_off;
+  const uint32_t* t_ex_off;
+  uint32_t* kept;  // [n_kl] 0/1
+  uint32_t* kl_exec;  // matched exec item
+  Orphans orph;
+};
+
+__global__ void k_fuse(FuseArgs a) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < a.n_kl) {
+    uint32_t par = a.kl_parent[k];
+    uint32_t keep = 0;
+    uint32_t x = kNone;
+    if (par < PAR_MAXROW) {
+      uint8_t info = a.kl_info[k];
+      if (info & KL_SYNC) {
+        keep = 1;
+      } else if (!(info & KL_CID)) {
+        emit_orphan(a.orph, trace_of32(a.t_kl_off, a.T, k), CAT_LAUNCH,
+                    ((uint64_t)par << 32) | k, a.kl_row[k], XSP_O_LAUNCH_NO_CID);
+      } else {
+        x = a.sl_exec[a.kl_slot[k]];
+        if (x != kNone) {
+          keep = 1;
+        } else {
+          emit_orphan(a.orph, trace_of32(a.t_kl_off, a.T, k), CAT_LAUNCH,
+                      ((uint64_t)par << 32) | k, a.kl_row[k], XSP_O_LAUNCH_NO_EXEC);
+        }
+      }
+    }
+    a.kept[k] = keep;
+    a.kl_exec[k] = x;
+  }
+  if (k < a.n_ex) {
+    if (a.sl_launch[a.ex_slot[k]] == kNone) {
+      uint32_t r = a.ex_row[k];
+      emit_orphan(a.orph, trace_of32(a.t_ex_off, a.T, k), CAT_LEFTOVER, a.sid[r], r,
+                  XSP_O_EXEC_NO_LAUNCH);
+    }
+  }
+}
+
+// Compact kept kernels (timeline order) with their parent layer as the sort key.
+__global__ void k_compact_kernels(uint32_t n_kl, const uint32_t* __restrict__ kept,
+                                  const uint32_t* __restrict__ pos, const uint32_t* __restrict__ kl_parent,
+                                  uint64_t* __restrict__ key, uint32_t* __restrict__ val,
+                                  uint32_t* __restrict__ nonmono) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_kl || !kept[k]) return;
+  uint32_t j = pos[k];
+  key[j] = kl_parent[k];
+  val[j] = k;
+}
+
+__global__ void k_check_mono(uint32_t nk, const uint64_t* __restrict__ key, uint32_t* __restrict__ nonmono) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j == 0 || j >= nk) return;
+  if (key[j] < key[j - 1]) *nonmono = 1;
+}
+
+__global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val,
+                                 const uint32_t* __restrict__ kl_row, const uint8_t* __restrict__ kl_info,
+                                 const uint64_t* __restrict__ kl_dur, const uint32_t* __restrict__ kl_mrow,
+                                 const uint32_t* __restrict__ kl_name, const uint32_t* __restrict__ kl_exec,
+                                 const uint32_t* __restrict__ ex_row, const uint64_t* __restrict__ ex_dur,
+                                 const uint32_t* __restrict__ ex_mrow, const uint32_t* __restrict__ ex_name,
+                                 uint32_t* __restrict__ k_launch, uint32_t* __restrict__ k_exec,
+                                 uint32_t* __restrict__ k_mrow, uint64_t* __restrict__ k_dur,
+                                 uint32_t* __restrict__ k_name) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nk) return;
+  uint32_t k = val[j];
+  uint32_t r = kl_row[k];
+  k_launch[j] = r;
+  if (kl_info[k] & KL_SYNC) {
+    k_exec[j] = r;
+    k_mrow[j] = kl_mrow[k];
+    k_dur[j] = kl_dur[k];
+    k_name[j] = kl_name[k];
+  } else {
+    uint32_t x = kl_exec[k];
+    k_exec[j] = ex_row[x];
+    k_mrow[j] = ex_mrow[x];
+    k_dur[j] = ex_dur[x];
+    k_name[j] = ex_name[x];
+  }
+}
+
+// layer_kernel_off[g] = first kernel j whose parent >= g (keys sorted).
+__global__ void k_layer_kernel_off(uint32_t nl, uint32_t nk, const uint64_t* __restrict__ key,
+                                   uint32_t* __restrict__ off) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > nl) return;
+  uint32_t lo = 0, hi = nk;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (key[mid] < g) lo = mid + 1; else hi = mid;
+  }
+  off[g] = lo;
+}
+
+__global__ void k_trace_kernel_off(uint32_t T, const uint32_t* __restrict__ t_layer_off,
+                                   const uint32_t* __restrict__ l_koff, uint32_t* __restrict__ t_koff) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > T) return;
+  t_koff[t] = l_koff[t_layer_off[t]];
+}
+
+// ---------------------------------------------------------------------------
+// Orphans in reference order: sort by (trace, category, key).
+
+__global__ void k_iota(uint32_t* v, uint32_t n) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+__global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* __restrict__ idx,
+                             uint64_t* __restrict__ dst, uint32_t n) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+__global__ void k_orphan_out(uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ row,
+                             const uint8_t* __restrict__ reason, uint32_t* __restrict__ out_row,
+                             uint8_t* __restrict__ out_reason) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out_row[i] = row[order[i]];
+  out_reason[i] = reason[order[i]];
+}
+// CSR over traces from keys sorted by trace (key >> shift).
+__global__ void k_csr_by_trace(uint32_t T, uint32_t n, const uint64_t* __restrict__ keys, int shift,
+                               uint32_t* __restrict__ off) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > T) return;
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if ((keys[mid] >> shift) < t) lo = mid + 1; else hi = mid;
+  }
+  off[t] = lo;
+}
+
+// Final per-trace status (assign_parents faults first, then correlate_async).
+__global__ void k_status(uint32_t T, const uint32_t* __restrict__ model_row,
+                         const unsigned long long* __restrict__ err_key,
+                         const unsigned long long* __restrict__ dup_ex,
+                         const unsigned long long* __restrict__ dup_kl,
+                         const uint32_t* __restrict__ ex_row, const uint32_t* __restrict__ kl_row,
+                         int32_t* __restrict__ status, uint32_t* __restrict__ err_row,
+                         uint32_t* __restrict__ n_failed) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  int32_t st = XSP_T_OK;
+  uint32_t ra = kNone, rb = kNone;
+  if (model_row[t] == kNone) {
+    st = XSP_T_NO_MODEL;
+  } else if (err_key[t] != ~0ull) {
+    st = (int32_t)(err_key[t] & 0xFF);
+    ra = (uint32_t)(err_key[t] >> 8);
+  } else if (dup_ex[t] != ~0ull) {
+    st = XSP_T_DUP_EXEC_CID;
+    ra = ex_row[(uint32_t)dup_ex[t]];          // first occurrence
+    rb = ex_row[(uint32_t)(dup_ex[t] >> 32)];  // the duplicate
+  } else if (dup_kl[t] != ~0ull) {
+    st = XSP_T_DUP_LAUNCH_CID;
+    ra = kl_row[(uint32_t)dup_kl[t]];
+    rb = kl_row[(uint32_t)(dup_kl[t] >> 32)];
+  }
+  status[t] = st;
+  err_row[2 * t] = ra;
+  err_row[2 * t + 1] = rb;
+  if (st != XSP_T_OK) atomicAdd(n_failed, 1u);
+}
+
+// ---------------------------------------------------------------------------
+// Orchestration
+
+namespace {
+
+template <typename K, typename... Args>
+void launch(xsp_ctx* ctx, K kernel, uint64_t n, cudaStream_t st, Args... args) {
+  if (n == 0) return;
+  unsigned blocks = ceil_div(n, 256);
+  kernel<<<blocks, 256, 0, st>>>(args...);
+  ++ctx->launches;
+}
+
+RadixScratch radix_scratch(xsp_ctx* ctx, uint64_t n) {
+  RadixScratch s;
+  s.keys_alt = ctx->d<uint64_t>("rs.keys_alt", n);
+  s.vals_alt = ctx->d<uint32_t>("rs.vals_alt", n);
+  uint64_t ce = radix_counts_elems(n);
+  s.counts = ctx->d<uint32_t>("rs.counts", ce);
+  s.scan_tmp = ctx->d<uint32_t>("rs.scan", scan_scratch_elems(ce));
+  s.and_or = ctx->d<unsigned long long>("rs.andor", 2);
+  s.and_or_host = ctx->h<unsigned long long>("rs.andor_h", 2);
+  return s;
+}
+
+uint32_t read_u32(xsp_ctx* ctx, const uint32_t* dptr, cudaStream_t st) {
+  uint32_t* h = ctx->h<uint32_t>("readback.u32", 1);
+  XSP_CUDA(cudaMemcpyAsync(h, dptr, 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  return *h;
+}
+
+}  // namespace
+
+__global__ void k_check_sorted(const uint8_t* __restrict__ flags, const uint64_t* __restrict__ begin,
+                               const uint64_t* __restrict__ sid, const uint64_t* __restrict__ off,
+                               uint32_t T, uint64_t n, uint32_t* __restrict__ unsorted) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 || i >= n) return;
+  uint32_t t = trace_of(off, 0, T, i);
+  if (off[t] == i) return;  // first span of its trace
+  uint64_t b0 = begin[i - 1], b1 = begin[i];
+  if (b0 < b1) return;
+  if (b0 > b1) {
+    *unsorted = 1;
+    return;
+  }
+  // rank: Model 1 < Layer 2 < Kernel = Api 3 (span.hpp:51-59)
+  uint32_t l0 = f_level(flags[i - 1]), l1 = f_level(flags[i]);
+  uint32_t r0 = l0 >= 2 ? 3 : l0 + 1, r1 = l1 >= 2 ? 3 : l1 + 1;
+  if (r0 < r1) return;
+  if (r0 > r1 || sid[i - 1] > sid[i]) *unsorted = 1;
+}
+
+void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, int sort_if_needed,
+                   xsp_corr_out* out, cudaStream_t st) {
+  const uint64_t n = c->n_spans;
+  const uint32_t T = tr->n_traces;
+  if (n >= 0xFFFFFFF0ull) throw std::invalid_argument("more than 2^32-16 spans in one call");
+  const uint64_t* off = tr->span_off;
+
+  // ---- sortedness (the TraceBundle invariant, span.hpp:161-163)
+  {
+    uint32_t* uns = ctx->d<uint32_t>("c.unsorted", 1);
+    XSP_CUDA(cudaMemsetAsync(uns, 0, 4, st));
+    launch(ctx, k_check_sorted, n, st, c->flags, c->begin_ns, c->span_id, off, T, n, uns);
+    if (read_u32(ctx, uns, st)) {
+      (void)sort_if_needed;
+      throw std::runtime_error("UNSORTED");
+    }
+  }
+
+  // ---- per-trace state
+  uint32_t* model_row = ctx->d<uint32_t>("c.model_row", T);
+  uint64_t* mb = ctx->d<uint64_t>("c.mb", T);
+  uint64_t* me = ctx->d<uint64_t>("c.me", T);
+  uint64_t* msid = ctx->d<uint64_t>("c.msid", T);
+  auto* err_key = ctx->d<unsigned long long>("c.err_key", T);
+  if (T) {
+    unsigned blocks = ceil_div((uint64_t)T * 32, 256);
+    k_trace_prep<<<blocks, 256, 0, st>>>(c->flags, c->begin_ns, c->end_ns, c->span_id, off, T,
+                                         model_row, mb, me, msid, err_key);
+    ++ctx->launches;
+  }
+
+  // ---- pass 1
+  const uint32_t ntiles = ceil_div(n, P1_TILE);
+  P1Args a;
+  a.flags = c->flags;
+  a.begin = c->begin_ns;
+  a.end = c->end_ns;
+  a.parent = c->parent_id;
+  a.cid = c->cid;
+  a.name = c->name_id;
+  a.n = n;
+  a.off = off;
+  a.T = T;
+  a.levels = tr->levels;
+  a.model_row = model_row;
+  a.mb = mb;
+  a.me = me;
+  a.msid = msid;
+  a.tile_ticket = ctx->d<uint32_t>("c.ticket", 1);
+  a.tile_flag = ctx->d<uint32_t>("c.tile_flag", ntiles + 1);
+  a.tile_agg = ctx->d<Full>("c.tile_agg", ntiles + 1);
+  a.tile_inc = ctx->d<Full>("c.tile_inc", ntiles + 1);
+  a.err_key = err_key;
+  a.layer_row = ctx->d<uint32_t>("o.layer_row", n);
+  a.layer_dur = ctx->d<uint64_t>("o.layer_dur", n);
+  a.layer_attr_row = ctx->d<uint32_t>("o.layer_attr_row", n);
+  a.layer_end = ctx->d<uint64_t>("c.layer_end", n);
+  a.kl_row = ctx->d<uint32_t>("c.kl_row", n);
+  a.kl_parent = ctx->d<uint32_t>("c.kl_parent", n);
+  a.kl_cid = ctx->d<uint64_t>("c.kl_cid", n);
+  a.kl_info = ctx->d<uint8_t>("c.kl_info", n);
+  a.kl_dur = ctx->d<uint64_t>("c.kl_dur", n);
+  a.kl_mrow = ctx->d<uint32_t>("c.kl_mrow", n);
+  a.kl_name = ctx->d<uint32_t>("c.kl_name", n);
+  a.ex_row = ctx->d<uint32_t>("c.ex_row", n);
+  a.ex_cid = ctx->d<uint64_t>("c.ex_cid", n);
+  a.ex_dur = ctx->d<uint64_t>("c.ex_dur", n);
+  a.ex_mrow = ctx->d<uint32_t>("c.ex_mrow", n);
+  a.ex_name = ctx->d<uint32_t>("c.ex_name", n);
+  a.t_layer_off = ctx->d<uint32_t>("o.t_layer_off", T + 1);
+  a.t_kl_off = ctx->d<uint32_t>("c.t_kl_off", T + 1);
+  a.t_ex_off = ctx->d<uint32_t>("c.t_ex_off", T + 1);
+  // counters: [0] orphans [1] ambiguities [2] pending [3] nonmono [4] n_failed
+  uint32_t* counters = ctx->d<uint32_t>("c.counters", 8);
+  XSP_CUDA(cudaMemsetAsync(counters, 0, 8 * 4, st));
+  Orphans orph;
+  // orphans: at most one per span from pass 1 + one per launch + one per exec
+  const uint64_t orph_cap = n + 16;
+  orph.tc = ctx->d<uint64_t>("c.o_tc", orph_cap);
+  orph.key = ctx->d<uint64_t>("c.o_key", orph_cap);
+  orph.row = ctx->d<uint32_t>("c.o_row", orph_cap);
+  orph.reason = ctx->d<uint8_t>("c.o_reason", orph_cap);
+  orph.count = counters + 0;
+  a.orph = orph;
+  a.amb_kl = ctx->d<uint32_t>("c.amb_kl", n);
+  a.amb_gx = ctx->d<uint32_t>("c.amb_gx", n);
+  a.amb_count = counters + 1;
+  a.pend_kl = ctx->d<uint32_t>("c.pend_kl", n);
+  a.pend_count = counters + 2;
+  XSP_CUDA(cudaMemsetAsync(a.tile_ticket, 0, 4, st));
+  XSP_CUDA(cudaMemsetAsync(a.tile_flag, 0, (ntiles + 1) * 4ull, st));
+  if (ntiles) {
+    k_pass1<<<ntiles, P1_WARPS * 32, 0, st>>>(a);
+    ++ctx->launches;
+  }
+  uint32_t* totals = ctx->d<uint32_t>("c.totals", 8);
+  k_pass1_tail<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(off, T, n, a.tile_inc, ntiles, a.t_layer_off,
+                                                               a.t_kl_off, a.t_ex_off, totals);
+  ++ctx->launches;
+  uint32_t* htot = ctx->h<uint32_t>("c.totals_h", 16);
+  XSP_CUDA(cudaMemcpyAsync(htot, totals, 5 * 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(htot + 8, counters, 3 * 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  const uint32_t nl = htot[0], nkl = htot[1], nex = htot[2];
+  const uint32_t n_amb = htot[9], n_pend = htot[10];
+
+  // ---- explicit parents
+  if (n_pend) {
+    uint32_t* t_uns = ctx->d<uint32_t>("c.t_uns", T);
+    XSP_CUDA(cudaMemsetAsync(t_uns, 0, T * 4ull, st));
+    launch(ctx, k_layer_ids_sorted, nl, st, a.layer_row, c->span_id, a.t_layer_off, T, nl, t_uns);
+    launch(ctx, k_resolve_explicit, n_pend, st, a.pend_kl, a.pend_count, a.kl_row, a.kl_parent,
+           c->parent_id, c->span_id, a.layer_row, a.t_layer_off, a.t_kl_off, T, t_uns, orph);
+  }
+
+  // ---- ambiguities, ordered by (trace, span_id)
+  out->n_ambiguities = n_amb;
+  out->trace_amb_off = ctx->d<uint32_t>("o.t_amb_off", T + 1);
+  out->amb_row = ctx->d<uint32_t>("o.amb_row", n_amb);
+  out->amb_cand_off = ctx->d<uint32_t>("o.amb_cand_off", n_amb + 1);
+  out->n_candidates = 0;
+  if (n_amb) {
+    RadixScratch rs = radix_scratch(ctx, n_amb);
+    uint64_t* ksid = ctx->d<uint64_t>("c.amb_ksid", n_amb);
+    uint64_t* ktr = ctx->d<uint64_t>("c.amb_ktr", n_amb);
+    uint64_t* ktr2 = ctx->d<uint64_t>("c.amb_ktr2", n_amb);
+    uint32_t* idx = ctx->d<uint32_t>("c.amb_idx", n_amb);
+    launch(ctx, k_amb_keys, n_amb, st, a.amb_kl, a.amb_count, a.kl_row, c->span_id, a.t_kl_off, T, ksid,
+           ktr, idx);
+    radix_sort_pairs(ksid, idx, n_amb, 0, 64, rs, st, &ctx->launches);
+    launch(ctx, k_gather_u64, n_amb, st, ktr, idx, ktr2, n_amb);
+    radix_sort_pairs(ktr2, idx, n_amb, 0, 32, rs, st, &ctx->launches);
+    uint32_t* cnt = ctx->d<uint32_t>("c.amb_cnt", n_amb + 1);
+    launch(ctx, k_amb_count, n_amb, st, idx, n_amb, a.amb_kl, a.amb_gx, a.kl_row, c->end_ns, a.t_kl_off,
+           a.t_layer_off, T, a.layer_end, cnt);
+    uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
+    uint32_t* tot = ctx->d<uint32_t>("c.amb_tot", 1);
+    exclusive_scan<uint32_t, uint32_t>(cnt, out->amb_cand_off, n_amb, scan_tmp, tot, st, &ctx->launches);
+    XSP_CUDA(cudaMemcpyAsync(out->amb_cand_off + n_amb, tot, 4, cudaMemcpyDeviceToDevice, st));
+    uint32_t ncand = read_u32(ctx, tot, st);
+    out->n_candidates = ncand;
+    out->amb_cand_row = ctx->d<uint32_t>("o.amb_cand_row", ncand);
+    launch(ctx, k_amb_fill, n_amb, st, idx, n_amb, a.amb_kl, a.amb_gx, a.kl_row, c->end_ns, c->span_id,
+           a.t_kl_off, a.t_layer_off, T, a.layer_end, a.layer_row, out->amb_cand_off, out->amb_row,
+           out->amb_cand_row);
+    launch(ctx, k_csr_by_trace, (uint64_t)T + 1, st, T, n_amb, ktr2, 0, out->trace_amb_off);
+  } else {
+    out->amb_cand_row = ctx->d<uint32_t>("o.amb_cand_row", 1);
+    XSP_CUDA(cudaMemsetAsync(out->trace_amb_off, 0, (T + 1) * 4ull, st));
+    XSP_CUDA(cudaMemsetAsync(out->amb_cand_off, 0, 4, st));
+  }
+
+  // ---- cid join
+  JoinArgs j;
+  j.ex_cid = a.ex_cid;
+  j.kl_cid = a.kl_cid;
+  j.kl_info = a.kl_info;
+  j.t_ex_off = a.t_ex_off;
+  j.t_kl_off = a.t_kl_off;
+  j.T = T;
+  j.n_ex = nex;
+  j.n_kl = nkl;
+  uint64_t* rsize = ctx->d<uint64_t>("c.rsize", T + 1);
+  uint64_t* roff = ctx->d<uint64_t>("c.roff", T + 1);
+  launch(ctx, k_region_size, T, st, a.t_kl_off, a.t_ex_off, T, rsize);
+  uint64_t* scan64 = ctx->d<uint64_t>("c.scan64", scan_scratch_elems(T + 1));
+  exclusive_scan<uint64_t, uint64_t>(rsize, roff, T, scan64, roff + T, st, &ctx->launches);
+  uint64_t* hroff = ctx->h<uint64_t>("c.roff_h", 1);
+  XSP_CUDA(cudaMemcpyAsync(hroff, roff + T, 8, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  const uint64_t nslots = *hroff;
+  j.roff = roff;
+  j.owner = ctx->d<uint32_t>("c.owner", nslots);
+  j.sl_exec = ctx->d<uint32_t>("c.sl_exec", nslots);
+  j.sl_launch = ctx->d<uint32_t>("c.sl_launch", nslots);
+  j.ex_slot = ctx->d<uint32_t>("c.ex_slot", nex);
+  j.kl_slot = ctx->d<uint32_t>("c.kl_slot", nkl);
+  j.t_dup = ctx->d<uint32_t>("c.t_dup", T);
+  XSP_CUDA(cudaMemsetAsync(j.owner, 0, nslots * 4, st));
+  XSP_CUDA(cudaMemsetAsync(j.sl_exec, 0xFF, nslots * 4, st));
+  XSP_CUDA(cudaMemsetAsync(j.sl_launch, 0xFF, nslots * 4, st));
+  XSP_CUDA(cudaMemsetAsync(j.t_dup, 0, T * 4ull, st));
+  auto* dup_ex = ctx->d<unsigned long long>("c.dup_ex", T);
+  auto* dup_kl = ctx->d<unsigned long long>("c.dup_kl", T);
+  XSP_CUDA(cudaMemsetAsync(dup_ex, 0xFF, T * 8ull, st));
+  XSP_CUDA(cudaMemsetAsync(dup_kl, 0xFF, T * 8ull, st));
+  launch(ctx, k_join_insert, (uint64_t)nex + nkl, st, j);
+  launch(ctx, k_join_dups, (uint64_t)nex + nkl, st, j, dup_ex, dup_kl);
+
+  // ---- fusion, kept kernels, leftover execs
+  FuseArgs fa;
+  fa.n_kl = nkl;
+  fa.n_ex = nex;
+  fa.T = T;
+  fa.kl_row = a.kl_row;
+  fa.kl_parent = a.kl_parent;
+  fa.kl_info = a.kl_info;
+  fa.kl_slot = j.kl_slot;
+  fa.sl_exec = j.sl_exec;
+  fa.sl_launch = j.sl_launch;
+  fa.ex_slot = j.ex_slot;
+  fa.ex_row = a.ex_row;
+  fa.sid = c->span_id;
+  fa.t_kl_off = a.t_kl_off;
+  fa.t_ex_off = a.t_ex_off;
+  fa.kept = ctx->d<uint32_t>("c.kept", nkl + 1);
+  fa.kl_exec = ctx->d<uint32_t>("c.kl_exec", nkl + 1);
+  fa.orph = orph;
+  launch(ctx, k_fuse, nkl > nex ? nkl : nex, st, fa);
+
+  uint32_t* kpos = ctx->d<uint32_t>("c.kpos", nkl + 1);
+  uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
+  uint32_t* nk_d = ctx->d<uint32_t>("c.nk", 1);
+  exclusive_scan<uint32_t, uint32_t>(fa.kept, kpos, nkl, scan_tmp, nk_d, st, &ctx->launches);
+  const uint32_t nk = read_u32(ctx, nk_d, st);
+  uint64_t* kkey = ctx->d<uint64_t>("c.kkey", nk + 1);
+  uint32_t* kval = ctx->d<uint32_t>("c.kval", nk + 1);
+  launch(ctx, k_compact_kernels, nkl, st, nkl, fa.kept, kpos, a.kl_parent, kkey, kval, counters + 3);
+  launch(ctx, k_check_mono, nk, st, nk, kkey, counters + 3);
+  if (read_u32(ctx, counters + 3, st)) {
+    // explicit parents broke the timeline order of layers: stable sort by layer
+    RadixScratch rs = radix_scratch(ctx, nk);
+    radix_sort_pairs(kkey, kval, nk, 0, 32, rs, st, &ctx->launches);
+  }
+  out->n_kernels = nk;
+  out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", nk);
+  out->kernel_exec_row = ctx->d<uint32_t>("o.k_exec", nk);
+  out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", nk);
+  out->kernel_dur = ctx->d<uint64_t>("o.k_dur", nk);
+  out->kernel_name = ctx->d<uint32_t>("o.k_name", nk);
+  launch(ctx, k_gather_kernels, nk, st, nk, kval, a.kl_row, a.kl_info, a.kl_dur, a.kl_mrow, a.kl_name,
+         fa.kl_exec, a.ex_row, a.ex_dur, a.ex_mrow, a.ex_name, out->kernel_launch_row,
+         out->kernel_exec_row, out->kernel_metric_row, out->kernel_dur, out->kernel_name);
+  out->n_layers = nl;
+  out->layer_row = a.layer_row;
+  out->layer_dur = a.layer_dur;
+  out->layer_attr_row = a.layer_attr_row;
+  out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", nl + 1);
+  launch(ctx, k_layer_kernel_off, (uint64_t)nl + 1, st, nl, nk, kkey, out->layer_kernel_off);
+  out->trace_layer_off = a.t_layer_off;
+  out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
+  launch(ctx, k_trace_kernel_off, (uint64_t)T + 1, st, T, a.t_layer_off, out->layer_kernel_off,
+         out->trace_kernel_off);
+
+  // ---- orphans in reference order
+  const uint32_t no = read_u32(ctx, orph.count, st);
+  out->n_orphans = no;
+  out->orphan_row = ctx->d<uint32_t>("o.orphan_row", no);
+  out->orphan_reason = ctx->d<uint8_t>("o.orphan_reason", no);
+  out->trace_orphan_off = ctx->d<uint32_t>("o.t_orph_off", T + 1);
+  if (no) {
+    RadixScratch rs = radix_scratch(ctx, no);
+    uint32_t* idx = ctx->d<uint32_t>("c.o_idx", no);
+    uint64_t* k1 = ctx->d<uint64_t>("c.o_k1", no);
+    uint64_t* k2 = ctx->d<uint64_t>("c.o_k2", no);
+    launch(ctx, k_iota, no, st, idx, no);
+    XSP_CUDA(cudaMemcpyAsync(k1, orph.key, no * 8ull, cudaMemcpyDeviceToDevice, st));
+    radix_sort_pairs(k1, idx, no, 0, 64, rs, st, &ctx->launches);
+    launch(ctx, k_gather_u64, no, st, orph.tc, idx, k2, no);
+    radix_sort_pairs(k2, idx, no, 0, 40, rs, st, &ctx->launches);
+    launch(ctx, k_orphan_out, no, st, no, idx, orph.row, orph.reason, out->orphan_row, out->orphan_reason);
+    launch(ctx, k_csr_by_trace, (uint64_t)T + 1, st, T, no, k2, 3, out->trace_orphan_off);
+  } else {
+    XSP_CUDA(cudaMemsetAsync(out->trace_orphan_off, 0, (T + 1) * 4ull, st));
+  }
+
+  // ---- status
+  out->n_traces = T;
+  out->trace_status = ctx->d<int32_t>("o.t_status", T);
+  out->trace_err_row = ctx->d<uint32_t>("o.t_err_row", 2ull * T);
+  out->trace_model_row = model_row;
+  launch(ctx, k_status, T, st, T, model_row, err_key, dup_ex, dup_kl, a.ex_row, a.kl_row, out->trace_status,
+         out->trace_err_row, counters + 4);
+  out->n_failed = read_u32(ctx, counters + 4, st);
+}
+
+}  // namespace xsp

@@ -1,0 +1,192 @@
+"""Host-side mirror of the reference correlate / analyze interface over the C ABI.
+
+Reference interface (namespace strata):
+  correlate(const TraceBundle&)                 correlator.hpp:164
+  a8_kernel_table ... a15_model_aggregate       analysis.hpp:256-366
+Here a whole batch of traces (SpanBatch) goes through ONE C-ABI call and the
+results come back as numpy columns; per-trace faults (the reference's
+TraceError) are reported per trace with the reference's exact message text.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _capi as capi
+from .columns import SpanBatch
+
+_NP = {capi.u8p: np.uint8, capi.i8p: np.int8, capi.u32p: np.uint32, capi.i32p: np.int32,
+       capi.u64p: np.uint64, capi.i64p: np.int64, capi.f64p: np.float64}
+
+ORPHAN_TEXT = {
+    1: "layer-level span with non-sync kind",
+    2: "explicit parent {p} is not the model span",
+    3: "outside the model interval",
+    4: "explicit parent {p} is not a layer in the tree",
+    5: "contained in no layer interval",
+    6: "execution record without correlation id",
+    7: "launch without correlation id",
+    8: "launch has no matching execution record",
+    9: "execution record without matching launch",
+}
+
+
+def _copy(ptr, typ, count: int) -> np.ndarray:
+    dt = _NP[typ]
+    if count == 0 or not ptr:
+        return np.zeros(0, dtype=dt)
+    addr = C.cast(ptr, C.c_void_p).value
+    buf = (C.c_char * (count * np.dtype(dt).itemsize)).from_address(addr)
+    return np.frombuffer(buf, dtype=dt).copy()
+
+
+@dataclass
+class CorrResult:
+    """CorrelationResult columns for every trace of a batch (include/xsp.h xsp_corr_out)."""
+    n_traces: int
+    n_failed: int
+    cols: Dict[str, np.ndarray]
+    n_layers: int = 0
+    n_kernels: int = 0
+    n_orphans: int = 0
+    n_ambiguities: int = 0
+    n_candidates: int = 0
+
+    def __getattr__(self, k):
+        try:
+            return self.__dict__["cols"][k]
+        except KeyError as e:
+            raise AttributeError(k) from e
+
+    def error_message(self, batch: SpanBatch, t: int) -> str:
+        """The what() text of the TraceError the reference throws for trace t ('' if none)."""
+        s = int(self.trace_status[t])
+        a, b = (int(x) for x in self.trace_err_row[2 * t:2 * t + 2])
+        if s == capi.T_OK:
+            return ""
+        if s == capi.T_NO_MODEL:
+            return "bundle has no model span; nothing to correlate"
+        if s == capi.T_MULTI_MODEL:
+            return "bundle has more than one model span"
+        if s == capi.T_SKIP_LEVEL:
+            return (f"span {int(batch.span_id[a])} ('{batch.name(batch.name_id[a])}') is kernel-level "
+                    "but the run did not profile the layer level; parents cannot skip a level")
+        kind = "execution" if s == capi.T_DUP_EXEC_CID else "launch"
+        return (f"correlation id {int(batch.cid[b])} is shared by {kind} spans "
+                f"{int(batch.span_id[a])} and {int(batch.span_id[b])}")
+
+    def orphan_text(self, batch: SpanBatch, j: int) -> str:
+        r = int(self.orphan_reason[j])
+        row = int(self.orphan_row[j])
+        return ORPHAN_TEXT[r].format(p=int(batch.parent_id[row]))
+
+
+@dataclass
+class Tables:
+    """a8..a15 columns for every group (include/xsp.h xsp_tables_out)."""
+    n_groups: int
+    cols: Dict[str, np.ndarray]
+    n_layers: int = 0
+    n_kernels: int = 0
+    n_names: int = 0
+
+    def __getattr__(self, k):
+        try:
+            return self.__dict__["cols"][k]
+        except KeyError as e:
+            raise AttributeError(k) from e
+
+
+def _corr_counts(o: capi.CorrOut) -> Dict[str, int]:
+    T = o.n_traces
+    return {"T": T, "2T": 2 * T, "T1": T + 1, "L": o.n_layers, "L1": o.n_layers + 1,
+            "K": o.n_kernels, "O": o.n_orphans, "A": o.n_ambiguities, "A1": o.n_ambiguities + 1,
+            "AC": o.n_candidates}
+
+
+def _tab_counts(o: capi.TablesOut, top_k: int) -> Dict[str, int]:
+    G = o.n_groups
+    return {"G": G, "G1": G + 1, "K": o.n_kernels, "L": o.n_layers, "N": o.n_names,
+            "LK": o.n_layers * max(top_k, 1)}
+
+
+class Engine:
+    """One xsp context on one CUDA device (no CPU fallback)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = capi.load()
+        self.ctx = C.c_void_p()
+        st = self.lib.xsp_ctx_create(device, C.byref(self.ctx))
+        if st != capi.XSP_OK:
+            raise capi.XspError(st, "xsp_ctx_create failed (no CUDA device?)")
+
+    def close(self):
+        if self.ctx:
+            self.lib.xsp_ctx_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st != capi.XSP_OK:
+            raise capi.XspError(st, self.lib.xsp_last_error(self.ctx).decode())
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.xsp_last_launch_count(self.ctx))
+
+    def transfer_bytes(self) -> Tuple[int, int]:
+        h, d = C.c_uint64(), C.c_uint64()
+        self.lib.xsp_last_transfer_bytes(self.ctx, C.byref(h), C.byref(d))
+        return int(h.value), int(d.value)
+
+    @staticmethod
+    def make_groups(first: Sequence[int], runs: Sequence[int], batch: Sequence[int]):
+        f = np.ascontiguousarray(first, dtype=np.uint32)
+        r = np.ascontiguousarray(runs, dtype=np.uint32)
+        b = np.ascontiguousarray(batch, dtype=np.uint32)
+        g = capi.Groups()
+        g.n_groups = f.size
+        g.first_trace = f.ctypes.data_as(capi.u32p)
+        g.n_runs = r.ctypes.data_as(capi.u32p)
+        g.batch_size = b.ctypes.data_as(capi.u32p)
+        return g, (f, r, b)
+
+    @staticmethod
+    def make_opts(trim=0.2, epsilon=0.05, noise=0.01, top_k=3):
+        o = capi.AnalysisOpts()
+        o.trim_fraction, o.epsilon, o.noise_tolerance, o.top_k = trim, epsilon, noise, top_k
+        return o
+
+    def run_host(self, batch: SpanBatch, groups: Optional[Tuple[Sequence[int], Sequence[int], Sequence[int]]] = None,
+                 trim=0.2, noise=0.01, top_k=3, peak_flops=None, mem_bw=None) -> Tuple[CorrResult, Tables]:
+        """correlate + analyze a host-resident batch end to end (xsp_run_host).
+
+        groups: (first_trace, n_runs, batch_size) arrays; default one group per trace."""
+        if groups is None:
+            T = batch.n_traces
+            groups = (np.arange(T), np.ones(T), batch.trace_batch)
+        g, keep = self.make_groups(*groups)
+        spec = capi.SystemSpec(batch.peak_flops if peak_flops is None else peak_flops,
+                               batch.mem_bw if mem_bw is None else mem_bw)
+        opts = self.make_opts(trim=trim, noise=noise, top_k=top_k)
+        cols, trs = batch.cols(), batch.traces()
+        co, to = capi.CorrOut(), capi.TablesOut()
+        self._check(self.lib.xsp_run_host(self.ctx, C.byref(cols), C.byref(trs), C.byref(g),
+                                          C.byref(spec), C.byref(opts), C.byref(co), C.byref(to),
+                                          None))
+        cc = _corr_counts(co)
+        corr = CorrResult(co.n_traces, co.n_failed,
+                          {n: _copy(getattr(co, n), t, cc[k]) for n, t, k in capi.CORR_FIELDS},
+                          co.n_layers, co.n_kernels, co.n_orphans, co.n_ambiguities, co.n_candidates)
+        tc = _tab_counts(to, top_k)
+        tabs = Tables(to.n_groups, {n: _copy(getattr(to, n), t, tc[k]) for n, t, k in capi.TABLE_FIELDS},
+                      to.n_layers, to.n_kernels, to.n_names)
+        return corr, tabs

@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path (through the C ABI) against the UNMODIFIED reference
+(oracle/_ref/libxsp_ref.so) on the same inputs. Bit-exact for every index,
+count and integer sum; bit-exact for fp64 too (the reference's op order is
+reproduced with -fmad=false)."""
+import numpy as np
+import pytest
+
+import cases
+from builders import API, KERNEL, LAYER, MLG, MODEL, batch_of
+from oracle import ref
+from parity import compare_correlation, compare_tables, topk_oracle
+
+pytestmark = pytest.mark.gpu
+
+FIXTURES = ["minimal", "resnet-like", "mobilenet-like", "overlap", "async-straggler", "overhead-chain"]
+
+
+def run_both(engine, b, groups=None, trim=0.2, noise=0.01, top_k=3):
+    corr, tabs = engine.run_host(b, groups=groups, trim=trim, noise=noise, top_k=top_k)
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+    if groups is None:
+        first, runs = np.arange(b.n_traces), np.ones(b.n_traces)
+    else:
+        first, runs = groups[0], groups[1]
+    aa, ast = ref.analyze(b, first, runs, trim=trim, noise=noise)
+    compare_tables(b, tabs, aa, ast)
+    return corr, tabs
+
+
+@pytest.mark.parametrize("fixture", FIXTURES)
+def test_fixture_pipeline(engine, has_ref, fixture):
+    """Criterion 10 shape (acceptance_main.cpp:315-364): every fixture x batch."""
+    g = ref.Generator()
+    for batch in (1, 2, 4, 8):
+        g.emit(fixture, batch=batch)
+    b = g.batch()
+    corr, tabs = run_both(engine, b)
+    if fixture == "overlap":
+        assert corr.n_ambiguities > 0
+    else:
+        assert corr.n_orphans == 0 and corr.n_ambiguities == 0
+
+
+def test_repetitions_trimmed_mean(engine, has_ref):
+    """C1: resnet-like x 10 jittered iterations in one AnalysisInput."""
+    g = ref.Generator()
+    for r in range(10):
+        g.emit("resnet-like", batch=4, run_index=r, jitter_max=1000, jitter_seed=100 + r)
+    b = g.batch()
+    corr, tabs = run_both(engine, b, groups=([0], [10], [4]))
+    assert tabs.n_kernels == 293 and tabs.n_layers == 234
+
+
+def test_many_groups(engine, has_ref):
+    g = ref.Generator()
+    for m in ("resnet-like", "mobilenet-like", "overhead-chain"):
+        for batch in (1, 2):
+            for r in range(3):
+                g.emit(m, batch=batch, run_index=r, jitter_max=500, jitter_seed=7 * r + batch)
+    b = g.batch()
+    first = np.arange(0, 18, 3)
+    run_both(engine, b, groups=(first, np.full(6, 3), np.array([1, 2] * 3)))
+
+
+def test_structure_mismatch_groups(engine, has_ref):
+    """combine() errors (analysis.cpp:103-118) per group."""
+    g = ref.Generator()
+    g.emit("resnet-like").emit("mobilenet-like")          # layer count differs
+    g.emit("minimal").emit("minimal", levels=0b011)       # kernel count of layer 0 differs
+    b = g.batch()
+    corr, tabs = engine.run_host(b, groups=([0, 2], [2, 2], [1, 1]))
+    aa, ast = ref.analyze(b, [0, 2], [2, 2])
+    compare_tables(b, tabs, aa, ast)
+    assert list(tabs.group_status) == [2, 3]
+
+
+def test_random_nested_acceptance(engine, has_ref):
+    """Criterion 8 (acceptance_main.cpp:181-235): rng 99, 97 sizes in [20,600] + 10k + 3k + 3k."""
+    import random
+    sizes_rng = random.Random(0)
+    g = ref.Generator()
+    # the reference draws sizes from the same mt19937_64 it generates with; here sizes
+    # come from Python and the bundles from the reference generator (seed 99)
+    for _ in range(97):
+        g.random_nested(99, 20 + sizes_rng.randrange(581))
+    for s in (10_000, 3_000, 3_000):
+        g.random_nested(99, s)
+    b = g.batch()
+    corr, _ = engine.run_host(b)
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+    assert corr.n_orphans == 0 and corr.n_ambiguities == 0
+
+
+def test_random_nested_explicit_fractions(engine, has_ref):
+    g = ref.Generator()
+    for frac in (0.0, 0.5, 1.0):
+        for _ in range(5):
+            g.random_nested(2026, 800, frac)
+    b = g.batch()
+    corr, _ = engine.run_host(b)
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+
+
+def test_async_bijection(engine, has_ref):
+    """Criterion 9 (acceptance_main.cpp:237-313): 5000 shuffled pairs."""
+    g = ref.Generator()
+    g.random_async(7, 5_000)
+    g.random_async(15, 500)
+    b = g.batch()
+    corr, tabs = run_both(engine, b)
+    assert corr.n_orphans == 0
+    assert corr.n_kernels == 5_500
+
+
+def test_file_order_independence(engine, has_ref):
+    """test_correlator.cpp:315-327: shuffled + re-sorted input gives the same tree."""
+    g = ref.Generator()
+    g.random_nested(7, 200)
+    g.random_nested(7, 200).shuffle_last(7, resort=True)
+    b = g.batch()
+    corr, _ = engine.run_host(b)
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+
+
+@pytest.mark.parametrize("case", ["nesting", "layer_attrs", "explicit_beats_containment",
+                                  "overlapping_layers", "orphans", "fusion", "unmatched_async",
+                                  "mixed_orphan_order"])
+def test_edge_cases(engine, has_ref, case):
+    b = batch_of([getattr(cases, case)()])
+    run_both(engine, b)
+
+
+def test_trace_errors_in_one_batch(engine, has_ref):
+    """Per-trace TraceErrors with the reference's exact messages, mixed with good traces."""
+    traces = [cases.nesting(), cases.dup_launch_cid(), cases.fusion(), cases.dup_exec_cid(),
+              cases.no_model(), cases.two_models(), cases.skip_level(), cases.orphans()]
+    levels = [MLG] * len(traces)
+    levels[6] = (1 << MODEL) | (1 << KERNEL)
+    b = batch_of(traces, levels=levels)
+    corr, tabs = engine.run_host(b)
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+    assert list(corr.trace_status) == [0, 5, 0, 4, 1, 2, 3, 0]
+
+
+def test_topk(engine, has_ref):
+    g = ref.Generator()
+    for r in range(5):
+        g.emit("resnet-like", batch=2, run_index=r, jitter_max=200_000, jitter_seed=r)
+    b = g.batch()
+    for k in (1, 3, 8):
+        corr, tabs = engine.run_host(b, groups=([0], [5], [2]), top_k=k)
+        want = topk_oracle(tabs.k_lat, tabs.k_layer, k)
+        np.testing.assert_array_equal(tabs.l_topk.reshape(-1, k), want)
+
+
+def test_leveled_chain_correlation(engine, has_ref):
+    """C2 bundles ({M}, {M,L}, {M,L,G}) correlate like the reference."""
+    g = ref.Generator()
+    g.chain("resnet-like", 1, 15_700_000, 0, 2.0)
+    g.chain("overhead-chain", 1, 15_700_000, 0, 2.0)
+    b = g.batch()
+    corr, _ = engine.run_host(b)
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+
+
+def test_empty_and_tiny(engine, has_ref):
+    b = batch_of([[], cases.two_models()[:1], cases.nesting()])
+    corr, tabs = engine.run_host(b)
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+
+
+def test_golden_fixtures(engine):
+    """Committed reference outputs (tests/golden, made by make_golden.py); needs no oracle .so."""
+    import os
+    from golden_io import load_golden
+    gdir = os.path.join(os.path.dirname(__file__), "golden")
+    files = sorted(f for f in os.listdir(gdir) if f.endswith(".npz"))
+    assert files
+    for f in files:
+        b, (ca, cs), (aa, ast), groups = load_golden(os.path.join(gdir, f))
+        corr, tabs = engine.run_host(b, groups=groups)
+        compare_correlation(b, corr, ca, cs)
+        compare_tables(b, tabs, aa, ast)
