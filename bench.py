@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""Benchmark: M spans/s correlated + analysed (BASELINE.json metric) on B200.
+
+Workload (BASELINE.json configs[2], "C3"): 65 synthetic models x 8 batch sizes
+(1..128) x R iterations, ~50M spans at R=20, every span in one xsp_correlate +
+xsp_analyze pass (parent join, cid join, per-kernel/layer/name/model tables,
+roofline classification, top-3 per layer). Inputs (~3 GB) are far larger than
+the 126 MB L2, so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1: one process per GPU (torchrun), each rank correlates its own C3-sized
+corpus (independent traces -> no data-path collective; weak scaling); time is
+the max over ranks. `value` is device-resident throughput; `e2e` goes through
+the host-buffer C-ABI entry (xsp_run_host) with H2D of the inputs and D2H of all
+result columns inside the timed region. `--impl reference` times the reference's
+own CPU implementation (oracle/_ref, unmodified strata sources) with all host
+threads on a bounded sample of the same corpus.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "M spans/sec correlated+analyzed at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "M spans/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            p = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def pass1_bytes(b) -> int:
+    """Algorithmic bytes of one k_pass1 launch: every span's flags,
+    begin, end; parent_id of spans with one; cid of spans with one; name_id of
+    kernel/exec spans; writes: 24 B per placed layer, 17 B per kernel-list entry
+    (+16 B for synchronous kernels), 28 B per execution record, 12 B per trace."""
+    f = b.flags
+    lvl, kind = f & 3, (f >> 2) & 3
+    n = b.n_spans
+    has_p = int(((f & 0x10) != 0).sum())
+    has_c = int(((f & 0x20) != 0).sum())
+    layer = int(((lvl == 1) & (kind == 0)).sum())
+    launch = int(((kind == 1) & (lvl >= 2)).sum())
+    synck = int(((kind == 0) & (lvl == 2)).sum())
+    exe = int((kind == 2).sum())
+    reads = n * 17 + has_p * 8 + has_c * 8 + (launch + synck + exe) * 4
+    writes = layer * 24 + (launch + synck) * 17 + synck * 16 + exe * 28 + b.n_traces * 12
+    return reads + writes
+
+
+def survey_bytes(b) -> float:
+    """SURVEY.md §8(d) algorithmic bytes for the whole pipeline: per layer with K kernels
+    (157 + 162 K) B, plus a 96 B model row per trace."""
+    f = b.flags
+    lvl, kind = f & 3, (f >> 2) & 3
+    layers = int(((lvl == 1) & (kind == 0)).sum())
+    kernels = int(((kind == 1) & (lvl >= 2)).sum()) + int(((kind == 0) & (lvl == 2)).sum())
+    return 157.0 * layers + 162.0 * kernels + 96.0 * b.n_traces
+
+
+def make_workload(args, rank: int):
+    from paper_1908_06869_b200 import synth
+    return synth.c3(runs=args.runs, n_models=args.models, seed=1 + rank)
+
+
+def sample_groups(gf, gr, b, max_spans: int):
+    """First groups of the corpus up to ~max_spans spans (bounded CPU sample)."""
+    off = b.trace_span_off
+    k = 0
+    while k < len(gf):
+        end = int(off[gf[k] + gr[k]])
+        if end > max_spans and k > 0:
+            break
+        k += 1
+    return k, int(off[gf[k - 1] + gr[k - 1]])
+
+
+def cpu_reference(b, gf, gr, max_spans: int, reps: int = 1):
+    from oracle import ref
+    k, spans = sample_groups(gf, gr, b, max_spans)
+    sub = b.trace_slice(0, int(gf[k - 1] + gr[k - 1]))
+    threads = os.cpu_count() or 1
+    secs = ref.time_pipeline(sub, gf[:k], gr[:k], threads, reps)
+    return {"value": spans / secs / 1e6, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"first {k} of {len(gf)} (model,batch) groups = {spans} spans, "
+                      f"correlate + a8..a15 per group, {threads} threads (oracle/_ref, unmodified strata)",
+            "seconds": secs}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libxsp_ref.so not built"}))
+        return
+    from paper_1908_06869_b200 import synth
+    # a bounded sample of the same corpus: the first models of the C3 family
+    models = synth.make_models(args.models, seed=1)[:max(1, args.models // 10)]
+    b, gf, gr, gb = synth.corpus(models, (1, 2, 4, 8, 16, 32, 64, 128), args.runs, seed=1 + 1000)
+    budget = args.ref_sample_spans
+    for _ in range(args.warmup):
+        cpu_reference(b, gf, gr, budget // 4)
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        r = cpu_reference(b, gf, gr, budget)
+        vals.append(r["value"])
+        secs += r["seconds"]
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64",
+            "data": "synthetic", "config": config(args),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["cores"], "kind": "reference",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def config(args):
+    return {"workload": "C3: 65 synthetic models x 8 batch sizes (1..128) x R iterations, correlate + "
+                        "a8..a15 + top-3, one group per (model,batch)",
+            "models": args.models, "batches": [1, 2, 4, 8, 16, 32, 64, 128], "iterations": args.runs,
+            "l2": "inputs (>2 GB/GPU) exceed the 126 MB L2; no flush needed",
+            "parallelism": f"trace-sharded x{args.gpus} (weak)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--runs", type=int, default=20, help="iterations per (model, batch) group")
+    ap.add_argument("--models", type=int, default=65)
+    ap.add_argument("--ref-sample-spans", type=int, default=3_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    from paper_1908_06869_b200.engine import DeviceBatch, Engine
+    b, gf, gr, gb = make_workload(args, rank)
+    groups = (gf, gr, gb)
+    eng = Engine(local)
+    dev = DeviceBatch(b, local)
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def step():
+        co = eng.correlate_device(dev, stream=stream)
+        eng.analyze_device(dev, co, groups, stream=stream)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    eng.set_profiling(True)
+    eng.stage_reset()
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        t0.record()
+        for _ in range(args.steps):
+            step()
+            launches += eng.launches
+        t1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    stages = eng.stage_times()
+    eng.set_profiling(False)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    spans_total = b.n_spans * world
+    value = spans_total / (ms / 1e3) / 1e6
+
+    # ---- end to end through the host-buffer C ABI (pinned inputs, H2D + D2H timed)
+    hb = b.pinned()
+    for _ in range(1):
+        eng.run_host(hb, groups=groups, raw=True)
+    barrier()
+    e_t0 = time.perf_counter()
+    for _ in range(args.steps):
+        eng.run_host(hb, groups=groups, raw=True)
+    torch.cuda.synchronize()
+    e_ms = (time.perf_counter() - e_t0) * 1e3 / args.steps
+    h2d, d2h = eng.transfer_bytes()
+    if dist:
+        t = torch.tensor([e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e = {"value": spans_total / (e_ms / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
+
+    if rank != 0:
+        return
+    peak, peak_kind = hbm_peak()
+    dom = max(stages, key=lambda k: stages[k][0])
+    p1_ms = stages["pass1"][0] / max(stages["pass1"][1], 1)
+    p1_bytes = pass1_bytes(b)
+    achieved = p1_bytes / (p1_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_pass1 (parent join + list compaction, 1 launch/step)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_kind": peak_kind, "traffic": None, "bytes_per_launch": p1_bytes,
+                "ms_per_launch": p1_ms}
+    sv = survey_bytes(b)
+    pipe_gbs = sv * world / (ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic", "config": config(args),
+        "spans_per_gpu": b.n_spans, "e2e": e2e, "gpu_launches": launches,
+        "roofline": roofline,
+        "pipeline_roofline": {"bound": "hbm", "bytes_per_span": sv / b.n_spans, "achieved": pipe_gbs,
+                              "peak": peak, "unit": "GB/s", "frac": pipe_gbs / peak / world,
+                              "definition": "SURVEY.md 8(d): (157+162K) B per layer + 96 B per trace"},
+        "stages_ms": {k: v[0] / max(v[1], 1) for k, v in stages.items()},
+        "dominant_stage": dom,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import ref
+        if ref.available():
+            cb = cpu_reference(b, gf, gr, args.ref_sample_spans)
+            cb.pop("seconds")
+            line["cpu_baseline"] = cb
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

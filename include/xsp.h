@@ -270,6 +270,15 @@ void xsp_last_transfer_bytes(const xsp_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 /* Number of CUDA kernel launches issued by the last API call on this ctx. */
 uint64_t xsp_last_launch_count(const xsp_ctx* ctx);
 
+/* Per-stage device timing: when enabled, every call records CUDA events around
+ * each stage (on the stream the stage's kernels are launched on) and accumulates
+ * the elapsed times until xsp_stage_reset. xsp_stage_times fills up to `max`
+ * entries (stage name, total ms, number of timed executions) and returns the
+ * number of stages. */
+void xsp_set_profiling(xsp_ctx* ctx, int enabled);
+void xsp_stage_reset(xsp_ctx* ctx);
+int xsp_stage_times(xsp_ctx* ctx, int max, const char** names, double* total_ms, uint64_t* count);
+
 /* Synchronous device->host copy of `bytes` from a result column (helper for
  * callers that do not link the CUDA runtime themselves). */
 xsp_status xsp_copy_to_host(xsp_ctx* ctx, void* dst, const void* src, size_t bytes);

@@ -127,7 +127,8 @@ class TablesOut(C.Structure):
 EXPORTS = [
     "xsp_abi_version", "xsp_ctx_create", "xsp_ctx_destroy", "xsp_last_error", "xsp_correlate",
     "xsp_analyze", "xsp_run_host", "xsp_last_transfer_bytes", "xsp_last_launch_count",
-    "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host",
+    "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host", "xsp_set_profiling", "xsp_stage_reset",
+    "xsp_stage_times",
 ]
 
 _lib = None
@@ -174,5 +175,9 @@ def load() -> C.CDLL:
     lib.xsp_host_free.argtypes = [P]
     lib.xsp_copy_to_host.argtypes = [P, P, P, C.c_size_t]
     lib.xsp_copy_to_host.restype = C.c_int32
+    lib.xsp_set_profiling.argtypes = [P, C.c_int]
+    lib.xsp_stage_reset.argtypes = [P]
+    lib.xsp_stage_times.argtypes = [P, C.c_int, C.POINTER(C.c_char_p), f64p, u64p]
+    lib.xsp_stage_times.restype = C.c_int
     _lib = lib
     return lib

@@ -111,6 +111,23 @@ class SpanBatch:
         return int(sum(getattr(self, k).nbytes for k in cols) + self.trace_span_off.nbytes
                    + self.trace_levels.nbytes)
 
+    def pinned(self) -> "SpanBatch":
+        """A copy whose columns live in page-locked host memory (fast H2D/D2H)."""
+        import torch
+        keep = []
+
+        def pin(a):
+            view = {np.uint64: np.int64, np.uint32: np.int32}.get(a.dtype.type, a.dtype.type)
+            t = torch.from_numpy(np.ascontiguousarray(a).view(view)).pin_memory()
+            keep.append(t)
+            return t.numpy().view(a.dtype)
+
+        kw = {k: pin(getattr(self, k)) for k in {**SPAN_COLS, **METRIC_COLS, **LAYER_COLS, **TRACE_COLS}}
+        out = SpanBatch(**kw, names=self.names, types=self.types, system_name=self.system_name,
+                        peak_flops=self.peak_flops, mem_bw=self.mem_bw)
+        out._pinned = keep
+        return out
+
     def name(self, name_id: int) -> str:
         return self.names[int(name_id)].decode()
 

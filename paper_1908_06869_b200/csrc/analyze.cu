@@ -628,7 +628,9 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->l_flagged = la.l_flagged = ctx->d<uint8_t>("t.l_flagged", TL);
   out->l_roofline_in = la.l_in = ctx->d<uint8_t>("t.l_in", TL);
   out->l_topk = la.l_topk = ctx->d<uint32_t>("t.l_topk", (uint64_t)TL * (opts->top_k ? opts->top_k : 1));
+  ctx->stage_begin("layers", st);
   launch(ctx, k_layers, TL, st, la);
+  ctx->stage_end("layers", st);
 
   // ---- per model
   ModelArgs ma;
@@ -665,12 +667,15 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->m_gpu_pct = ma.m_gpu_pct = ctx->d<double>("t.m_gpu_pct", G);
   out->m_throughput = ma.m_throughput = ctx->d<double>("t.m_tp", G);
   out->m_roofline_in = ma.m_in = ctx->d<uint8_t>("t.m_in", G);
+  ctx->stage_begin("models", st);
   launch(ctx, k_models, G, st, ma);
+  ctx->stage_end("models", st);
 
   // ---- a10
   out->group_name_off = ctx->d<uint32_t>("t.g_noff", G + 1);
   uint32_t NN = 0;
   if (TK) {
+    ctx->stage_begin("names", st);
     uint64_t* key = ctx->d<uint64_t>("a.nkey", TK);
     uint32_t* val = ctx->d<uint32_t>("a.nval", TK);
     launch(ctx, k_name_keys, TK, st, TK, out->group_kernel_off, G, la.k_name, out->group_status, key, val);
@@ -743,6 +748,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     launch(ctx, k_permute<double>, NN, st, NN, order, na.s_ai, out->n_ai);
     launch(ctx, k_permute<double>, NN, st, NN, order, na.s_tput, out->n_tput);
     launch(ctx, k_permute<int8_t>, NN, st, NN, order, na.s_bound, out->n_bound);
+    ctx->stage_end("names", st);
   } else {
     XSP_CUDA(cudaMemsetAsync(out->group_name_off, 0, (G + 1) * 4ull, st));
     out->n_name = ctx->d<uint32_t>("t.n_name", 1);

@@ -118,6 +118,31 @@ XSP_API void xsp_host_free(void* p) {
   if (p) cudaFreeHost(p);
 }
 
+XSP_API void xsp_set_profiling(xsp_ctx* ctx, int enabled) {
+  if (ctx) ctx->profiling = enabled != 0;
+}
+
+XSP_API void xsp_stage_reset(xsp_ctx* ctx) {
+  if (!ctx) return;
+  ctx->stage_collect();
+  for (auto& s : ctx->stages) {
+    s.ms = 0.0;
+    s.calls = 0;
+  }
+}
+
+XSP_API int xsp_stage_times(xsp_ctx* ctx, int max, const char** names, double* total_ms, uint64_t* count) {
+  if (!ctx) return 0;
+  ctx->stage_collect();
+  int n = static_cast<int>(ctx->stages.size());
+  for (int i = 0; i < n && i < max; ++i) {
+    if (names) names[i] = ctx->stages[i].name.c_str();
+    if (total_ms) total_ms[i] = ctx->stages[i].ms;
+    if (count) count[i] = ctx->stages[i].calls;
+  }
+  return n;
+}
+
 XSP_API xsp_status xsp_copy_to_host(xsp_ctx* ctx, void* dst, const void* src, size_t bytes) {
   return guard(ctx, "xsp_copy_to_host", [&] {
     if (bytes) XSP_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));

@@ -1047,7 +1047,9 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   {
     uint32_t* uns = ctx->d<uint32_t>("c.unsorted", 1);
     XSP_CUDA(cudaMemsetAsync(uns, 0, 4, st));
+    ctx->stage_begin("check_sorted", st);
     launch(ctx, k_check_sorted, n, st, c->flags, c->begin_ns, c->span_id, off, T, n, uns);
+    ctx->stage_end("check_sorted", st);
     if (read_u32(ctx, uns, st)) {
       (void)sort_if_needed;
       throw std::runtime_error("UNSORTED");
@@ -1061,9 +1063,11 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   uint64_t* msid = ctx->d<uint64_t>("c.msid", T);
   auto* err_key = ctx->d<unsigned long long>("c.err_key", T);
   if (T) {
+    ctx->stage_begin("trace_prep", st);
     unsigned blocks = ceil_div((uint64_t)T * 32, 256);
     k_trace_prep<<<blocks, 256, 0, st>>>(c->flags, c->begin_ns, c->end_ns, c->span_id, off, T,
                                          model_row, mb, me, msid, err_key);
+    ctx->stage_end("trace_prep", st);
     ++ctx->launches;
   }
 
@@ -1128,7 +1132,9 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   XSP_CUDA(cudaMemsetAsync(a.tile_ticket, 0, 4, st));
   XSP_CUDA(cudaMemsetAsync(a.tile_flag, 0, (ntiles + 1) * 4ull, st));
   if (ntiles) {
+    ctx->stage_begin("pass1", st);
     k_pass1<<<ntiles, P1_WARPS * 32, 0, st>>>(a);
+    ctx->stage_end("pass1", st);
     ++ctx->launches;
   }
   uint32_t* totals = ctx->d<uint32_t>("c.totals", 8);
@@ -1222,8 +1228,10 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   auto* dup_kl = ctx->d<unsigned long long>("c.dup_kl", T);
   XSP_CUDA(cudaMemsetAsync(dup_ex, 0xFF, T * 8ull, st));
   XSP_CUDA(cudaMemsetAsync(dup_kl, 0xFF, T * 8ull, st));
+  ctx->stage_begin("join", st);
   launch(ctx, k_join_insert, (uint64_t)nex + nkl, st, j);
   launch(ctx, k_join_dups, (uint64_t)nex + nkl, st, j, dup_ex, dup_kl);
+  ctx->stage_end("join", st);
 
   // ---- fusion, kept kernels, leftover execs
   FuseArgs fa;
@@ -1244,7 +1252,9 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   fa.kept = ctx->d<uint32_t>("c.kept", nkl + 1);
   fa.kl_exec = ctx->d<uint32_t>("c.kl_exec", nkl + 1);
   fa.orph = orph;
+  ctx->stage_begin("fuse", st);
   launch(ctx, k_fuse, nkl > nex ? nkl : nex, st, fa);
+  ctx->stage_end("fuse", st);
 
   uint32_t* kpos = ctx->d<uint32_t>("c.kpos", nkl + 1);
   uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
@@ -1266,6 +1276,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", nk);
   out->kernel_dur = ctx->d<uint64_t>("o.k_dur", nk);
   out->kernel_name = ctx->d<uint32_t>("o.k_name", nk);
+  ctx->stage_begin("gather", st);
   launch(ctx, k_gather_kernels, nk, st, nk, kval, a.kl_row, a.kl_info, a.kl_dur, a.kl_mrow, a.kl_name,
          fa.kl_exec, a.ex_row, a.ex_dur, a.ex_mrow, a.ex_name, out->kernel_launch_row,
          out->kernel_exec_row, out->kernel_metric_row, out->kernel_dur, out->kernel_name);
@@ -1279,6 +1290,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
   launch(ctx, k_trace_kernel_off, (uint64_t)T + 1, st, T, a.t_layer_off, out->layer_kernel_off,
          out->trace_kernel_off);
+  ctx->stage_end("gather", st);
 
   // ---- orphans in reference order
   const uint32_t no = read_u32(ctx, orph.count, st);

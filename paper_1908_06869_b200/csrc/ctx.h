@@ -7,6 +7,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "xsp.h"
 
@@ -33,6 +34,63 @@ struct xsp_ctx {
   };
   std::map<std::string, Buf> dev;
   std::map<std::string, Buf> host;  // pinned
+
+  // ---- optional per-stage timing with CUDA events on the launching stream
+  struct Stage {
+    std::string name;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // pending (begin, end) pairs
+    double ms = 0.0;
+    uint64_t calls = 0;
+  };
+  bool profiling = false;
+  std::vector<Stage> stages;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t take_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) throw CudaError("cudaEventCreate failed");
+    return e;
+  }
+  Stage& stage(const std::string& name) {
+    for (auto& s : stages)
+      if (s.name == name) return s;
+    stages.push_back(Stage{name, {}, 0.0, 0});
+    return stages.back();
+  }
+  // begin/end of a named stage on stream st (no-ops unless profiling)
+  void stage_begin(const std::string& name, cudaStream_t st) {
+    if (!profiling) return;
+    cudaEvent_t b = take_event();
+    cudaEventRecord(b, st);
+    stage(name).ev.push_back({b, nullptr});
+  }
+  void stage_end(const std::string& name, cudaStream_t st) {
+    if (!profiling) return;
+    cudaEvent_t e = take_event();
+    cudaEventRecord(e, st);
+    stage(name).ev.back().second = e;
+  }
+  // resolve pending events into milliseconds
+  void stage_collect() {
+    for (auto& s : stages) {
+      for (auto& [b, e] : s.ev) {
+        float ms = 0.f;
+        if (e) {
+          cudaEventSynchronize(e);
+          cudaEventElapsedTime(&ms, b, e);
+          event_pool.push_back(e);
+        }
+        event_pool.push_back(b);
+        s.ms += ms;
+        ++s.calls;
+      }
+      s.ev.clear();
+    }
+  }
 
   // Grow-only named device buffer with at least `bytes` bytes.
   void* dbuf(const std::string& name, size_t bytes) {
@@ -74,6 +132,8 @@ struct xsp_ctx {
     return static_cast<T*>(hbuf(name, count * sizeof(T)));
   }
   ~xsp_ctx() {
+    stage_collect();
+    for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
     for (auto& [k, b] : dev)
       if (b.ptr) cudaFree(b.ptr);
     for (auto& [k, b] : host)

@@ -113,6 +113,47 @@ def _tab_counts(o: capi.TablesOut, top_k: int) -> Dict[str, int]:
             "LK": o.n_layers * max(top_k, 1)}
 
 
+class DeviceBatch:
+    """A SpanBatch resident in HBM (torch tensors are only the allocator here)."""
+
+    def __init__(self, batch: SpanBatch, device: int = 0):
+        import torch
+        self.batch = batch
+        self.t = {}
+        for k in ("span_id", "parent_id", "begin_ns", "end_ns", "cid", "flags", "name_id", "flops",
+                  "dram_read", "dram_write", "occupancy", "alloc_bytes", "type_id", "trace_span_off",
+                  "trace_levels"):
+            a = getattr(batch, k)
+            view = {np.uint64: np.int64, np.uint32: np.int32}.get(a.dtype.type, a.dtype.type)
+            self.t[k] = torch.from_numpy(np.ascontiguousarray(a).view(view)).to(f"cuda:{device}")
+        self.nbytes = sum(int(x.numel() * x.element_size()) for x in self.t.values())
+
+    def _p(self, k, typ):
+        x = self.t[k]
+        return C.cast(C.c_void_p(x.data_ptr() if x.numel() else 0), typ)
+
+    def cols(self) -> capi.SpanCols:
+        b = self.batch
+        c = capi.SpanCols()
+        c.n_spans = b.n_spans
+        for k, typ in (("span_id", capi.u64p), ("parent_id", capi.u64p), ("begin_ns", capi.u64p),
+                       ("end_ns", capi.u64p), ("cid", capi.u64p), ("flags", capi.u8p),
+                       ("name_id", capi.u32p), ("flops", capi.u64p), ("dram_read", capi.u64p),
+                       ("dram_write", capi.u64p), ("occupancy", capi.f64p),
+                       ("alloc_bytes", capi.i64p), ("type_id", capi.u32p)):
+            setattr(c, k, self._p(k, typ))
+        c.n_metric_rows = int(b.flops.size)
+        c.n_layer_rows = int(b.alloc_bytes.size)
+        return c
+
+    def traces(self) -> capi.Traces:
+        t = capi.Traces()
+        t.n_traces = self.batch.n_traces
+        t.span_off = self._p("trace_span_off", capi.u64p)
+        t.levels = self._p("trace_levels", capi.u32p)
+        return t
+
+
 class Engine:
     """One xsp context on one CUDA device (no CPU fallback)."""
 
@@ -165,11 +206,46 @@ class Engine:
         o.trim_fraction, o.epsilon, o.noise_tolerance, o.top_k = trim, epsilon, noise, top_k
         return o
 
+    # ---- device-resident path (inputs already in HBM; results stay in HBM)
+    def correlate_device(self, dbatch: DeviceBatch, stream=None) -> capi.CorrOut:
+        cols, trs = dbatch.cols(), dbatch.traces()
+        co = capi.CorrOut()
+        self._check(self.lib.xsp_correlate(self.ctx, C.byref(cols), C.byref(trs), 1, C.byref(co),
+                                           C.c_void_p(stream)))
+        return co
+
+    def analyze_device(self, dbatch: DeviceBatch, corr: capi.CorrOut, groups, trim=0.2, noise=0.01,
+                       top_k=3, stream=None) -> capi.TablesOut:
+        g, keep = self.make_groups(*groups)
+        spec = capi.SystemSpec(dbatch.batch.peak_flops, dbatch.batch.mem_bw)
+        opts = self.make_opts(trim=trim, noise=noise, top_k=top_k)
+        cols = dbatch.cols()
+        to = capi.TablesOut()
+        self._check(self.lib.xsp_analyze(self.ctx, C.byref(cols), C.byref(corr), C.byref(g),
+                                         C.byref(spec), C.byref(opts), C.byref(to), C.c_void_p(stream)))
+        return to
+
+    def set_profiling(self, on: bool):
+        self.lib.xsp_set_profiling(self.ctx, int(on))
+
+    def stage_reset(self):
+        self.lib.xsp_stage_reset(self.ctx)
+
+    def stage_times(self) -> Dict[str, Tuple[float, int]]:
+        n = self.lib.xsp_stage_times(self.ctx, 0, None, None, None)
+        names = (C.c_char_p * max(n, 1))()
+        ms = (C.c_double * max(n, 1))()
+        cnt = (C.c_uint64 * max(n, 1))()
+        self.lib.xsp_stage_times(self.ctx, n, names, ms, cnt)
+        return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(n)}
+
     def run_host(self, batch: SpanBatch, groups: Optional[Tuple[Sequence[int], Sequence[int], Sequence[int]]] = None,
-                 trim=0.2, noise=0.01, top_k=3, peak_flops=None, mem_bw=None) -> Tuple[CorrResult, Tables]:
+                 trim=0.2, noise=0.01, top_k=3, peak_flops=None, mem_bw=None,
+                 raw: bool = False) -> Tuple[CorrResult, Tables]:
         """correlate + analyze a host-resident batch end to end (xsp_run_host).
 
-        groups: (first_trace, n_runs, batch_size) arrays; default one group per trace."""
+        groups: (first_trace, n_runs, batch_size) arrays; default one group per trace.
+        raw=True returns the C structs whose columns stay in ctx-owned pinned memory."""
         if groups is None:
             T = batch.n_traces
             groups = (np.arange(T), np.ones(T), batch.trace_batch)
@@ -182,6 +258,8 @@ class Engine:
         self._check(self.lib.xsp_run_host(self.ctx, C.byref(cols), C.byref(trs), C.byref(g),
                                           C.byref(spec), C.byref(opts), C.byref(co), C.byref(to),
                                           None))
+        if raw:
+            return co, to
         cc = _corr_counts(co)
         corr = CorrResult(co.n_traces, co.n_failed,
                           {n: _copy(getattr(co, n), t, cc[k]) for n, t, k in capi.CORR_FIELDS},
