@@ -338,34 +338,67 @@ struct ModelArgs {
   uint8_t* m_in;
 };
 
-// model_aggregate_row (analysis.cpp:532-552), a13 totals (:495-499), a1 (:245-246)
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// model_aggregate_row (analysis.cpp:532-552), a13 totals (:495-499), a1 (:245-246).
+// One warp per group: lanes load 32 consecutive kernel rows (coalesced) and the
+// fp64 accumulators then consume them strictly left to right through register
+// broadcast, so the rounding sequence is exactly the reference's; u64 counters
+// are reduced in any order (exact).
 __global__ void k_models(ModelArgs a) {
-  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
   if (g >= a.G) return;
   if (a.gstatus[g] != XSP_G_OK) {
-    a.m_lat[g] = nan("");
+    if (lane == 0) a.m_lat[g] = nan("");
     return;
   }
   const uint32_t R = a.nr[g], t0 = a.ft[g];
-  double v[kMaxRuns];
-  for (uint32_t r = 0; r < R; ++r) {
-    uint32_t m = a.model_row[t0 + r];
-    v[r] = (double)clamp_dur(a.begin[m], a.end[m]);
+  double mlat = 0.0;
+  if (lane == 0) {
+    double v[kMaxRuns];
+    for (uint32_t r = 0; r < R; ++r) {
+      uint32_t m = a.model_row[t0 + r];
+      v[r] = (double)clamp_dur(a.begin[m], a.end[m]);
+    }
+    mlat = trimmed_mean_dev(v, R, a.trim);
   }
-  const double mlat = trimmed_mean_dev(v, R, a.trim);
+  mlat = __shfl_sync(0xffffffffu, mlat, 0);
   double lat = 0.0, occw = 0.0;
-  uint64_t f = 0, rd = 0, wr = 0, n = 0;
-  for (uint32_t j = a.gk_off[g]; j < a.gk_off[g + 1]; ++j) {
-    double kl = a.k_lat[j];
-    lat = __dadd_rn(lat, kl);
-    f += a.k_flops[j];
-    rd += a.k_read[j];
-    wr += a.k_write[j];
-    occw = __dadd_rn(occw, __dmul_rn(a.k_occ[j], kl));
-    ++n;
+  uint64_t f = 0, rd = 0, wr = 0;
+  const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
+  for (uint32_t base = k0; base < k1; base += 32) {
+    const uint32_t j = base + lane;
+    double kl = 0.0, prod = 0.0;
+    if (j < k1) {
+      kl = a.k_lat[j];
+      prod = __dmul_rn(a.k_occ[j], kl);
+      f += a.k_flops[j];
+      rd += a.k_read[j];
+      wr += a.k_write[j];
+    }
+    const uint32_t cnt = min(32u, k1 - base);
+    for (uint32_t s = 0; s < cnt; ++s) {
+      lat = __dadd_rn(lat, __shfl_sync(0xffffffffu, kl, s));
+      occw = __dadd_rn(occw, __shfl_sync(0xffffffffu, prod, s));
+    }
   }
+  f = warp_sum_u64(f);
+  rd = warp_sum_u64(rd);
+  wr = warp_sum_u64(wr);
+  const uint64_t n = k1 - k0;
   double gpu = 0.0;
-  for (uint32_t l = a.gl_off[g]; l < a.gl_off[g + 1]; ++l) gpu = __dadd_rn(gpu, a.l_kern_lat[l]);
+  for (uint32_t base = a.gl_off[g]; base < a.gl_off[g + 1]; base += 32) {
+    const uint32_t l = base + lane;
+    double x = l < a.gl_off[g + 1] ? a.l_kern_lat[l] : 0.0;
+    const uint32_t cnt = min(32u, a.gl_off[g + 1] - base);
+    for (uint32_t s = 0; s < cnt; ++s) gpu = __dadd_rn(gpu, __shfl_sync(0xffffffffu, x, s));
+  }
+  if (lane != 0) return;
   Roof ro = roofline(f, rd, wr, lat, a.peak, a.bw);
   a.m_lat[g] = mlat;
   a.m_kern_lat[g] = lat;
@@ -668,7 +701,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->m_throughput = ma.m_throughput = ctx->d<double>("t.m_tp", G);
   out->m_roofline_in = ma.m_in = ctx->d<uint8_t>("t.m_in", G);
   ctx->stage_begin("models", st);
-  launch(ctx, k_models, G, st, ma);
+  launch(ctx, k_models, (uint64_t)G * 32, st, ma);
   ctx->stage_end("models", st);
 
   // ---- a10

@@ -98,112 +98,58 @@ __global__ void k_trace_prep(const uint8_t* __restrict__ flags, const uint64_t* 
 }
 
 // ---------------------------------------------------------------------------
-// Pass-1 scan state.
-
-struct T2 {  // top-2 end_ns over placed layers of the current trace segment
-  uint64_t m1, m2;
-  uint32_t a1;  // layer row (relative to the range's start count) of m1
-  uint32_t n;   // number of layers seen, saturating at 2
-};
-
-struct Seg {
-  uint32_t c;     // placed layers in the range (shifts args)
-  uint32_t head;  // range contains the first span of a trace
-  T2 t;
-};
-
+// Pass-1 scan state (the decoupled look-back payload).
+//
+// For a child span c whose last preceding placed layer (in its trace) is j,
+// with M_j = max end_ns over the placed layers before j, the containment
+// candidates are exactly the preceding placed layers with end >= c.end, so:
+//   end_j >= e, M_j <  e  -> one candidate: j
+//   end_j >= e, M_j >= e  -> >= 2 candidates: ambiguity
+//   end_j <  e, M_j <  e  -> no candidate: orphan
+//   end_j <  e, M_j >= e  -> an earlier layer outlives j (nested/overlapping
+//                            layers): resolved exactly on the rare path.
+// Ends are stored as end+1 so that 0 means "no layer".
 struct Full {
-  uint64_t m1, m2;
-  uint32_t a1, n, c, head;
+  uint64_t last_end1;  // end+1 of the last placed layer of the current trace segment
+  uint64_t last_M1;    // max end+1 over placed layers before it in the segment
+  uint64_t run_M1;     // max end+1 over all placed layers of the segment
+  uint32_t c;          // placed layers (global count)
+  uint32_t head;       // the range contains the first span of a trace
   uint32_t c_metric, c_lay, c_kl, c_ex;
 };
 static_assert(sizeof(Full) == 48, "Full layout");
 
-__device__ __forceinline__ T2 t2_merge(const T2& x, const T2& y) {
-  if (x.n == 0) return y;
-  if (y.n == 0) return x;
-  T2 r;
-  if (y.m1 > x.m1) {
-    r.m1 = y.m1;
-    r.a1 = y.a1;
-  } else {
-    r.m1 = x.m1;
-    r.a1 = x.a1;
-  }
-  uint64_t s = x.m1 < y.m1 ? x.m1 : y.m1;
-  if (x.n >= 2 && x.m2 > s) s = x.m2;
-  if (y.n >= 2 && y.m2 > s) s = y.m2;
-  r.m2 = s;
-  r.n = 2;
-  return r;
-}
-
-__device__ __forceinline__ Seg seg_combine(const Seg& a, const Seg& b) {
-  Seg r;
-  r.c = a.c + b.c;
-  r.head = a.head | b.head;
-  T2 bs = b.t;
-  bs.a1 += a.c;
-  r.t = b.head ? bs : t2_merge(a.t, bs);
-  return r;
-}
+__device__ __forceinline__ uint64_t max64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
 __device__ __forceinline__ Full full_combine(const Full& a, const Full& b) {
-  Seg sa{a.c, a.head, {a.m1, a.m2, a.a1, a.n}};
-  Seg sb{b.c, b.head, {b.m1, b.m2, b.a1, b.n}};
-  Seg s = seg_combine(sa, sb);
   Full r;
-  r.m1 = s.t.m1;
-  r.m2 = s.t.m2;
-  r.a1 = s.t.a1;
-  r.n = s.t.n;
-  r.c = s.c;
-  r.head = s.head;
+  r.c = a.c + b.c;
+  r.head = a.head | b.head;
   r.c_metric = a.c_metric + b.c_metric;
   r.c_lay = a.c_lay + b.c_lay;
   r.c_kl = a.c_kl + b.c_kl;
   r.c_ex = a.c_ex + b.c_ex;
+  if (b.head) {
+    r.last_end1 = b.last_end1;
+    r.last_M1 = b.last_M1;
+    r.run_M1 = b.run_M1;
+  } else if (b.last_end1) {
+    r.last_end1 = b.last_end1;
+    r.last_M1 = max64(a.run_M1, b.last_M1);
+    r.run_M1 = max64(a.run_M1, b.run_M1);
+  } else {
+    r.last_end1 = a.last_end1;
+    r.last_M1 = a.last_M1;
+    r.run_M1 = a.run_M1;
+  }
   return r;
 }
 
 __device__ __forceinline__ Full full_identity() {
   Full f;
-  f.m1 = f.m2 = 0;
-  f.a1 = f.n = f.c = f.head = 0;
-  f.c_metric = f.c_lay = f.c_kl = f.c_ex = 0;
+  f.last_end1 = f.last_M1 = f.run_M1 = 0;
+  f.c = f.head = f.c_metric = f.c_lay = f.c_kl = f.c_ex = 0;
   return f;
-}
-
-__device__ __forceinline__ Seg shfl_up_seg(const Seg& v, int o) {
-  Seg u;
-  u.c = __shfl_up_sync(0xffffffffu, v.c, o);
-  u.head = __shfl_up_sync(0xffffffffu, v.head, o);
-  u.t.m1 = __shfl_up_sync(0xffffffffu, v.t.m1, o);
-  u.t.m2 = __shfl_up_sync(0xffffffffu, v.t.m2, o);
-  u.t.a1 = __shfl_up_sync(0xffffffffu, v.t.a1, o);
-  u.t.n = __shfl_up_sync(0xffffffffu, v.t.n, o);
-  return u;
-}
-
-__device__ __forceinline__ Seg warp_inclusive_seg(Seg v) {
-  const uint32_t lane = lane_id();
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    Seg u = shfl_up_seg(v, o);
-    if (lane >= (uint32_t)o) v = seg_combine(u, v);
-  }
-  return v;
-}
-
-__device__ __forceinline__ Seg shfl_seg(const Seg& v, int src) {
-  Seg u;
-  u.c = __shfl_sync(0xffffffffu, v.c, src);
-  u.head = __shfl_sync(0xffffffffu, v.head, src);
-  u.t.m1 = __shfl_sync(0xffffffffu, v.t.m1, src);
-  u.t.m2 = __shfl_sync(0xffffffffu, v.t.m2, src);
-  u.t.a1 = __shfl_sync(0xffffffffu, v.t.a1, src);
-  u.t.n = __shfl_sync(0xffffffffu, v.t.n, src);
-  return u;
 }
 
 __device__ __forceinline__ void store_full(Full* dst, const Full& v) {
@@ -222,6 +168,67 @@ __device__ __forceinline__ Full load_full(const Full* src) {
   d[2] = __ldcg(s + 2);
   return v;
 }
+__device__ __forceinline__ Full shfl_full(const Full& v, int src) {
+  Full u;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
+  uint32_t* d = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+  for (int w = 0; w < 12; ++w) d[w] = __shfl_sync(0xffffffffu, s[w], src);
+  return u;
+}
+
+// Per-chunk (32 spans, one per lane) evaluation shared by both phases.
+struct Chunk {
+  uint32_t P, H;      // ballots: placed layers, trace heads
+  int seg;            // highest head lane <= this lane, -1 if none
+  uint64_t w;         // end+1 if placed else 0
+  uint64_t exM;       // max w over lanes [max(seg,0), lane) of the segment
+  uint64_t incM;      // max w over lanes [max(seg,0), lane]
+};
+
+__device__ __forceinline__ Chunk chunk_scan(bool placed, bool head, uint64_t e) {
+  Chunk k;
+  const uint32_t lane = lane_id();
+  k.P = __ballot_sync(0xffffffffu, placed);
+  k.H = __ballot_sync(0xffffffffu, head);
+  const uint32_t hle = k.H & (lanemask_lt() | (1u << lane));
+  k.seg = hle ? 31 - __clz(hle) : -1;
+  k.w = placed ? (e == ~0ull ? e : e + 1) : 0;
+  uint64_t x = k.w;
+  if (k.P) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((int)lane - o >= k.seg && (int)lane >= o) x = max64(x, y);
+    }
+  }
+  k.incM = x;
+  uint64_t p = __shfl_up_sync(0xffffffffu, x, 1);
+  k.exM = ((int)lane - 1 >= k.seg && lane >= 1) ? p : 0;
+  return k;
+}
+
+// Aggregate of one chunk (counts come from ballots).
+__device__ __forceinline__ Full chunk_agg(const Chunk& k, uint32_t bm, uint32_t bl, uint32_t bk,
+                                          uint32_t bx) {
+  Full f;
+  f.c = __popc(k.P);
+  f.head = k.H != 0;
+  f.c_metric = __popc(bm);
+  f.c_lay = __popc(bl);
+  f.c_kl = __popc(bk);
+  f.c_ex = __popc(bx);
+  const int s31 = k.H ? 31 - __clz(k.H) : 0;  // start of the last segment
+  const uint32_t lastP = k.P & (0xffffffffu << s31);
+  const int q = lastP ? 31 - __clz(lastP) : 0;
+  const uint64_t qw = __shfl_sync(0xffffffffu, k.w, q);
+  const uint64_t qex = __shfl_sync(0xffffffffu, k.exM, q);
+  const uint64_t run = __shfl_sync(0xffffffffu, k.incM, 31);
+  f.last_end1 = lastP ? qw : 0;
+  f.last_M1 = lastP ? qex : 0;
+  f.run_M1 = run;
+  return f;
+}
 
 constexpr int P1_WARPS = 8;
 constexpr int P1_CHUNKS = 8;
@@ -229,6 +236,8 @@ constexpr int P1_SUB = P1_CHUNKS * 32;
 constexpr int P1_TILE = P1_WARPS * P1_SUB;
 
 struct P1Args {
+  const uint64_t* span_id;
+  uint32_t* unsorted;
   const uint8_t* flags;
   const uint64_t* begin;
   const uint64_t* end;
@@ -304,151 +313,159 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
   }
   __syncthreads();
   const uint32_t tlo = s_tlo, thi = s_thi;
+  const bool one_trace = thi - tlo == 1;
   const uint64_t wbase = tile_base + (uint64_t)warp * P1_SUB;
 
-  // ---- phase 1: warp aggregate over this warp's 8 chunks ----------------
-  uint8_t fr[P1_CHUNKS];
-  uint64_t br[P1_CHUNKS], er[P1_CHUNKS];
-#pragma unroll
-  for (int c = 0; c < P1_CHUNKS; ++c) {
-    uint64_t i = wbase + c * 32 + lane;
-    bool v = i < a.n;
-    fr[c] = v ? __ldg(a.flags + i) : (uint8_t)0xFF;
-    br[c] = v ? __ldg(a.begin + i) : 0;
-    er[c] = v ? __ldg(a.end + i) : 0;
-  }
+  // ---- phase 1: warp aggregate ----------------------------------------------
   Full wagg = full_identity();
-#pragma unroll
+#pragma unroll 2
   for (int c = 0; c < P1_CHUNKS; ++c) {
-    uint64_t i = wbase + c * 32 + lane;
-    bool v = i < a.n;
-    uint8_t f = fr[c];
-    uint32_t t = v ? trace_of(a.off, tlo, thi, i) : 0;
-    bool head = v && a.off[t] == i;
-    bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
-    bool placed = is_layer && f_kind(f) == XSP_KIND_SYNC && layer_placed(f, br[c], er[c], i, t, a);
-    bool kl = v && (is_kernel_launch(f) || is_sync_kernel(f));
-    bool ex = v && is_exec(f) && (f & XSP_F_CID);
-    bool met = v && (f & XSP_F_METRICS);
-    Seg e;
-    e.c = placed;
-    e.head = head;
-    e.t.m1 = placed ? er[c] : 0;
-    e.t.m2 = 0;
-    e.t.a1 = 0;
-    e.t.n = placed ? 1u : 0u;
-    uint32_t bal_any = __ballot_sync(0xffffffffu, placed || head);
-    Seg tot;
-    if (bal_any) {
-      Seg inc = warp_inclusive_seg(e);
-      tot = shfl_seg(inc, 31);
-    } else {
-      tot.c = 0;
-      tot.head = 0;
-      tot.t.n = 0;
-      tot.t.m1 = tot.t.m2 = 0;
-      tot.t.a1 = 0;
+    const uint64_t i = wbase + c * 32 + lane;
+    const bool v = i < a.n;
+    const uint8_t f = v ? __ldg(a.flags + i) : (uint8_t)0xFF;
+    const uint32_t t = !v ? 0 : (one_trace ? tlo : trace_of(a.off, tlo, thi, i));
+    const bool head = v && __ldg(a.off + t) == i;
+    const bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
+    bool placed = false;
+    uint64_t e = 0;
+    if (is_layer && f_kind(f) == XSP_KIND_SYNC) {
+      const uint64_t b = __ldg(a.begin + i);
+      e = __ldg(a.end + i);
+      placed = layer_placed(f, b, e, i, t, a);
     }
-    Full ch;
-    ch.m1 = tot.t.m1;
-    ch.m2 = tot.t.m2;
-    ch.a1 = tot.t.a1;
-    ch.n = tot.t.n;
-    ch.c = tot.c;
-    ch.head = tot.head;
-    ch.c_metric = __popc(__ballot_sync(0xffffffffu, met));
-    ch.c_lay = __popc(__ballot_sync(0xffffffffu, is_layer));
-    ch.c_kl = __popc(__ballot_sync(0xffffffffu, kl));
-    ch.c_ex = __popc(__ballot_sync(0xffffffffu, ex));
+    const bool kl = v && (is_kernel_launch(f) || is_sync_kernel(f));
+    const bool ex = v && is_exec(f) && (f & XSP_F_CID);
+    const bool met = v && (f & XSP_F_METRICS);
+    Chunk k = chunk_scan(placed, head, e);
+    Full ch = chunk_agg(k, __ballot_sync(0xffffffffu, met), __ballot_sync(0xffffffffu, is_layer),
+                        __ballot_sync(0xffffffffu, kl), __ballot_sync(0xffffffffu, ex));
     wagg = full_combine(wagg, ch);
   }
   if (lane == 0) s_wagg[warp] = wagg;
   __syncthreads();
 
-  // ---- phase 2: tile aggregate + decoupled look-back ---------------------
-  if (threadIdx.x == 0) {
+  // ---- phase 2: tile aggregate + warp-parallel decoupled look-back ----------
+  if (warp == 0) {
     Full agg = s_wagg[0];
     for (int w = 1; w < P1_WARPS; ++w) agg = full_combine(agg, s_wagg[w]);
     Full prefix = full_identity();
     if (tile == 0) {
-      store_full(a.tile_inc + tile, agg);
-      __threadfence();
-      atomicExch(a.tile_flag + tile, 2u);
-    } else {
-      store_full(a.tile_agg + tile, agg);
-      __threadfence();
-      atomicExch(a.tile_flag + tile, 1u);
-      Full acc = full_identity();
-      bool have = false;
-      for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
-        uint32_t fl;
-        do {
-          fl = *((volatile uint32_t*)(a.tile_flag + j));
-        } while (fl == 0);
+      if (lane == 0) {
+        store_full(a.tile_inc + tile, agg);
         __threadfence();
-        if (fl == 2) {
-          Full inc = load_full(a.tile_inc + j);
-          acc = have ? full_combine(inc, acc) : inc;
-          have = true;
-          break;
+        atomicExch(a.tile_flag + tile, 2u);
+      }
+    } else {
+      if (lane == 0) {
+        store_full(a.tile_agg + tile, agg);
+        __threadfence();
+        atomicExch(a.tile_flag + tile, 1u);
+      }
+      // window of 32 predecessors per step; lane l looks at tile base - l
+      Full acc = full_identity();
+      int64_t base = (int64_t)tile - 1;
+      for (;;) {
+        const int64_t j = base - lane;
+        uint32_t fl = 2;  // before tile 0: identity prefix
+        if (j >= 0) {
+          do {
+            fl = *((volatile uint32_t*)(a.tile_flag + j));
+          } while (fl == 0);
         }
-        Full ag = load_full(a.tile_agg + j);
-        acc = have ? full_combine(ag, acc) : ag;
-        have = true;
+        __threadfence();
+        const uint32_t incl = __ballot_sync(0xffffffffu, fl == 2);
+        const uint32_t stop = incl ? (__ffs(incl) - 1) : 31;  // closest inclusive prefix
+        Full v = full_identity();
+        if (j >= 0 && lane <= stop) v = (fl == 2) ? load_full(a.tile_inc + j) : load_full(a.tile_agg + j);
+        // ordered tree reduction: higher lanes hold older tiles
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          Full u;
+          const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
+          uint32_t* d = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+          for (int w = 0; w < 12; ++w) d[w] = __shfl_down_sync(0xffffffffu, s[w], o);
+          if ((lane & (2 * o - 1)) == 0) v = full_combine(u, v);
+        }
+        acc = full_combine(shfl_full(v, 0), acc);
+        if (incl) break;
+        base -= 32;
       }
       prefix = acc;
-      store_full(a.tile_inc + tile, full_combine(prefix, agg));
-      __threadfence();
-      atomicExch(a.tile_flag + tile, 2u);
+      if (lane == 0) {
+        store_full(a.tile_inc + tile, full_combine(prefix, agg));
+        __threadfence();
+        atomicExch(a.tile_flag + tile, 2u);
+      }
     }
-    s_prefix = prefix;
+    if (lane == 0) s_prefix = prefix;
   }
   __syncthreads();
 
   Full carry = s_prefix;
   for (uint32_t w = 0; w < warp; ++w) carry = full_combine(carry, s_wagg[w]);
 
-  // ---- phase 3: per-span outputs ----------------------------------------
+  // ---- phase 3: per-span outputs -------------------------------------------
   const uint32_t lt = lanemask_lt();
   for (int c = 0; c < P1_CHUNKS; ++c) {
-    uint64_t i = wbase + c * 32 + lane;
-    bool v = i < a.n;
-    uint8_t f = v ? __ldg(a.flags + i) : (uint8_t)0xFF;
-    uint64_t b = v ? __ldg(a.begin + i) : 0;
-    uint64_t e = v ? __ldg(a.end + i) : 0;
-    uint32_t t = v ? trace_of(a.off, tlo, thi, i) : 0;
-    bool head = v && a.off[t] == i;
-    bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
-    bool layer_sync = is_layer && f_kind(f) == XSP_KIND_SYNC;
-    bool placed = layer_sync && layer_placed(f, b, e, i, t, a);
-    bool kl = v && (is_kernel_launch(f) || is_sync_kernel(f));
-    bool exe = v && is_exec(f);
-    bool ex = exe && (f & XSP_F_CID);
-    bool met = v && (f & XSP_F_METRICS);
+    const uint64_t i = wbase + c * 32 + lane;
+    const bool v = i < a.n;
+    const uint8_t f = v ? __ldg(a.flags + i) : (uint8_t)0xFF;
+    const uint64_t b = v ? __ldg(a.begin + i) : 0;
+    const uint64_t e = v ? __ldg(a.end + i) : 0;
+    const uint32_t t = !v ? 0 : (one_trace ? tlo : trace_of(a.off, tlo, thi, i));
+    const bool head = v && __ldg(a.off + t) == i;
+    const bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
+    const bool layer_sync = is_layer && f_kind(f) == XSP_KIND_SYNC;
+    const bool placed = layer_sync && layer_placed(f, b, e, i, t, a);
+    const bool kl = v && (is_kernel_launch(f) || is_sync_kernel(f));
+    const bool exe = v && is_exec(f);
+    const bool ex = exe && (f & XSP_F_CID);
+    const bool met = v && (f & XSP_F_METRICS);
 
-    uint32_t bal_p = __ballot_sync(0xffffffffu, placed);
-    uint32_t bal_m = __ballot_sync(0xffffffffu, met);
-    uint32_t bal_l = __ballot_sync(0xffffffffu, is_layer);
-    uint32_t bal_k = __ballot_sync(0xffffffffu, kl);
-    uint32_t bal_x = __ballot_sync(0xffffffffu, ex);
-    const uint32_t g_ex = carry.c + __popc(bal_p & lt);
-    const uint32_t m_ex = carry.c_metric + __popc(bal_m & lt);
-    const uint32_t l_ex = carry.c_lay + __popc(bal_l & lt);
-    const uint32_t k_ex = carry.c_kl + __popc(bal_k & lt);
-    const uint32_t x_ex = carry.c_ex + __popc(bal_x & lt);
+    const uint32_t bm = __ballot_sync(0xffffffffu, met);
+    const uint32_t bl = __ballot_sync(0xffffffffu, is_layer);
+    const uint32_t bk = __ballot_sync(0xffffffffu, kl);
+    const uint32_t bx = __ballot_sync(0xffffffffu, ex);
+    const Chunk k = chunk_scan(placed, head, e);
+    const uint32_t g_ex = carry.c + __popc(k.P & lt);
+    const uint32_t m_ex = carry.c_metric + __popc(bm & lt);
+    const uint32_t l_ex = carry.c_lay + __popc(bl & lt);
+    const uint32_t k_ex = carry.c_kl + __popc(bk & lt);
+    const uint32_t x_ex = carry.c_ex + __popc(bx & lt);
 
-    Seg cs{carry.c, carry.head, {carry.m1, carry.m2, carry.a1, carry.n}};
-    Seg inc = cs;
-    if (__ballot_sync(0xffffffffu, placed || head)) {
-      Seg el;
-      el.c = placed;
-      el.head = head;
-      el.t.m1 = placed ? e : 0;
-      el.t.m2 = 0;
-      el.t.a1 = 0;
-      el.t.n = placed ? 1u : 0u;
-      Seg wi = warp_inclusive_seg(el);
-      inc = seg_combine(cs, wi);
+    // last placed layer before this lane in its trace segment: (end+1, M+1)
+    const uint32_t segmask = k.seg >= 0 ? (0xffffffffu << k.seg) : 0xffffffffu;
+    const uint32_t pq = k.P & lt & segmask;
+    const int q = pq ? 31 - __clz(pq) : 0;
+    const uint64_t qw = __shfl_sync(0xffffffffu, k.w, q);
+    const uint64_t qex = __shfl_sync(0xffffffffu, k.exM, q);
+    uint64_t jend1 = 0, jM1 = 0;
+    if (pq) {
+      jend1 = qw;
+      jM1 = k.seg >= 0 ? qex : max64(carry.run_M1, qex);
+    } else if (k.seg < 0) {
+      jend1 = carry.last_end1;
+      jM1 = carry.last_M1;
+    }
+
+    // timeline order (begin_ns, rank, span_id) within the trace (span.hpp:161-163)
+    {
+      uint64_t pb = __shfl_up_sync(0xffffffffu, b, 1);
+      uint32_t pf = __shfl_up_sync(0xffffffffu, (uint32_t)f, 1);
+      if (lane == 0 && v && i > 0) {
+        pb = __ldg(a.begin + i - 1);
+        pf = __ldg(a.flags + i - 1);
+      }
+      if (v && !head && i > 0 && pb >= b) {
+        bool bad = pb > b;
+        if (!bad) {
+          const uint32_t l0 = f_level((uint8_t)pf), l1 = f_level(f);
+          const uint32_t r0 = l0 >= 2 ? 3 : l0 + 1, r1 = l1 >= 2 ? 3 : l1 + 1;
+          bad = r0 > r1 || (r0 == r1 && __ldg(a.span_id + i - 1) > __ldg(a.span_id + i));
+        }
+        if (bad) atomicOr(a.unsorted, 1u);
+      }
     }
 
     if (v) {
@@ -490,13 +507,15 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
           uint32_t s = atomicAdd(a.pend_count, 1u);
           a.pend_kl[s] = k_ex;
         } else {
-          uint32_t cands = (inc.t.n >= 1 && inc.t.m1 >= e) + (inc.t.n >= 2 && inc.t.m2 >= e);
-          if (cands == 0) {
+          const bool in_j = jend1 > e;  // end_j >= e (ends stored +1)
+          const bool in_m = jM1 > e;    // some earlier layer has end >= e
+          if (in_j && !in_m) {
+            par = g_ex - 1;
+          } else if (!in_j && !in_m) {
             par = PAR_ORPHAN;
             emit_orphan(a.orph, t, CAT_KERNEL, i, (uint32_t)i, XSP_O_KERNEL_NO_LAYER);
-          } else if (cands == 1) {
-            par = inc.t.a1;
           } else {
+            // >= 2 candidates, or an earlier layer outlives j: exact rare path
             par = PAR_AMBIG;
             uint32_t s = atomicAdd(a.amb_count, 1u);
             a.amb_kl[s] = k_ex;
@@ -526,23 +545,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
         } while (tt >= 0 && a.off[tt] == i);
       }
     }
-    // carry += chunk
-    Full ch;
-    Seg last = shfl_seg(inc, 31);
-    ch.m1 = last.t.m1;
-    ch.m2 = last.t.m2;
-    ch.a1 = last.t.a1;
-    ch.n = last.t.n;
-    ch.c = last.c;
-    ch.head = last.head;
-    ch.c_metric = carry.c_metric + __popc(bal_m);
-    ch.c_lay = carry.c_lay + __popc(bal_l);
-    ch.c_kl = carry.c_kl + __popc(bal_k);
-    ch.c_ex = carry.c_ex + __popc(bal_x);
-    carry = ch;
+    carry = full_combine(carry, chunk_agg(k, bm, bl, bk, bx));
   }
 }
-
 // Offsets of traces that start at or after the end of the span table (empty
 // trailing traces) and the [T] sentinel.
 __global__ void k_pass1_tail(const uint64_t* __restrict__ off, uint32_t T, uint64_t n,
@@ -629,6 +634,45 @@ __global__ void k_resolve_explicit(const uint32_t* __restrict__ pend_kl, const u
 // ---------------------------------------------------------------------------
 // Ambiguities (correlator.cpp:242-257): all placed layers of the trace that
 // precede the child in timeline order (g < gx) with end >= child end.
+
+// Children flagged in pass 1 with >= 2 candidates, or whose last preceding
+// layer does not contain them while an earlier one might: count exactly.
+__global__ void k_amb_resolve(uint32_t n_raw, const uint32_t* __restrict__ amb_kl,
+                              const uint32_t* __restrict__ amb_gx, const uint32_t* __restrict__ kl_row,
+                              const uint64_t* __restrict__ end, const uint32_t* __restrict__ t_kl_off,
+                              const uint32_t* __restrict__ t_layer_off, uint32_t T,
+                              const uint64_t* __restrict__ layer_end, uint32_t* __restrict__ kl_parent,
+                              uint32_t* __restrict__ keep) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_raw) return;
+  const uint32_t k = amb_kl[p];
+  const uint32_t t = trace_of32(t_kl_off, T, k);
+  const uint64_t e = end[kl_row[k]];
+  const uint32_t lo = t_layer_off[t];
+  uint32_t cnt = 0, last = kNone;
+  for (uint32_t g = amb_gx[p]; g > lo && cnt < 2;) {
+    --g;
+    if (layer_end[g] >= e) {
+      ++cnt;
+      last = g;
+    }
+  }
+  if (cnt == 1) {
+    kl_parent[k] = last;
+    keep[p] = 0;
+  } else {
+    keep[p] = 1;
+  }
+}
+
+__global__ void k_amb_compact(uint32_t n_raw, const uint32_t* __restrict__ keep, const uint32_t* __restrict__ pos,
+                              const uint32_t* __restrict__ kl, const uint32_t* __restrict__ gx,
+                              uint32_t* __restrict__ kl2, uint32_t* __restrict__ gx2) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_raw || !keep[p]) return;
+  kl2[pos[p]] = kl[p];
+  gx2[pos[p]] = gx[p];
+}
 
 __global__ void k_amb_keys(const uint32_t* __restrict__ amb_kl, const uint32_t* __restrict__ amb_count,
                            const uint32_t* __restrict__ kl_row, const uint64_t* __restrict__ sid,
@@ -1043,19 +1087,6 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   if (n >= 0xFFFFFFF0ull) throw std::invalid_argument("more than 2^32-16 spans in one call");
   const uint64_t* off = tr->span_off;
 
-  // ---- sortedness (the TraceBundle invariant, span.hpp:161-163)
-  {
-    uint32_t* uns = ctx->d<uint32_t>("c.unsorted", 1);
-    XSP_CUDA(cudaMemsetAsync(uns, 0, 4, st));
-    ctx->stage_begin("check_sorted", st);
-    launch(ctx, k_check_sorted, n, st, c->flags, c->begin_ns, c->span_id, off, T, n, uns);
-    ctx->stage_end("check_sorted", st);
-    if (read_u32(ctx, uns, st)) {
-      (void)sort_if_needed;
-      throw std::runtime_error("UNSORTED");
-    }
-  }
-
   // ---- per-trace state
   uint32_t* model_row = ctx->d<uint32_t>("c.model_row", T);
   uint64_t* mb = ctx->d<uint64_t>("c.mb", T);
@@ -1074,6 +1105,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   // ---- pass 1
   const uint32_t ntiles = ceil_div(n, P1_TILE);
   P1Args a;
+  a.span_id = c->span_id;
   a.flags = c->flags;
   a.begin = c->begin_ns;
   a.end = c->end_ns;
@@ -1115,6 +1147,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   // counters: [0] orphans [1] ambiguities [2] pending [3] nonmono [4] n_failed
   uint32_t* counters = ctx->d<uint32_t>("c.counters", 8);
   XSP_CUDA(cudaMemsetAsync(counters, 0, 8 * 4, st));
+  a.unsorted = counters + 5;
   Orphans orph;
   // orphans: at most one per span from pass 1 + one per launch + one per exec
   const uint64_t orph_cap = n + 16;
@@ -1143,10 +1176,15 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   ++ctx->launches;
   uint32_t* htot = ctx->h<uint32_t>("c.totals_h", 16);
   XSP_CUDA(cudaMemcpyAsync(htot, totals, 5 * 4, cudaMemcpyDeviceToHost, st));
-  XSP_CUDA(cudaMemcpyAsync(htot + 8, counters, 3 * 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(htot + 8, counters, 6 * 4, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
   const uint32_t nl = htot[0], nkl = htot[1], nex = htot[2];
-  const uint32_t n_amb = htot[9], n_pend = htot[10];
+  const uint32_t n_amb_raw = htot[9], n_pend = htot[10];
+  if (htot[13]) {
+    // not in timeline order (span.hpp:161-163); stage (b) sorting is not wired yet
+    (void)sort_if_needed;
+    throw std::runtime_error("UNSORTED");
+  }
 
   // ---- explicit parents
   if (n_pend) {
@@ -1155,6 +1193,24 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     launch(ctx, k_layer_ids_sorted, nl, st, a.layer_row, c->span_id, a.t_layer_off, T, nl, t_uns);
     launch(ctx, k_resolve_explicit, n_pend, st, a.pend_kl, a.pend_count, a.kl_row, a.kl_parent,
            c->parent_id, c->span_id, a.layer_row, a.t_layer_off, a.t_kl_off, T, t_uns, orph);
+  }
+
+  // ---- rare containment cases: exact candidate count by scanning back
+  uint32_t n_amb = 0;
+  if (n_amb_raw) {
+    uint32_t* keep = ctx->d<uint32_t>("c.amb_keep", n_amb_raw + 1);
+    uint32_t* pos = ctx->d<uint32_t>("c.amb_pos", n_amb_raw + 1);
+    launch(ctx, k_amb_resolve, n_amb_raw, st, n_amb_raw, a.amb_kl, a.amb_gx, a.kl_row, c->end_ns,
+           a.t_kl_off, a.t_layer_off, T, a.layer_end, a.kl_parent, keep);
+    uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
+    exclusive_scan<uint32_t, uint32_t>(keep, pos, n_amb_raw, scan_tmp, counters + 6, st, &ctx->launches);
+    uint32_t* kl2 = ctx->d<uint32_t>("c.amb_kl2", n_amb_raw);
+    uint32_t* gx2 = ctx->d<uint32_t>("c.amb_gx2", n_amb_raw);
+    launch(ctx, k_amb_compact, n_amb_raw, st, n_amb_raw, keep, pos, a.amb_kl, a.amb_gx, kl2, gx2);
+    n_amb = read_u32(ctx, counters + 6, st);
+    a.amb_kl = kl2;
+    a.amb_gx = gx2;
+    a.amb_count = counters + 6;
   }
 
   // ---- ambiguities, ordered by (trace, span_id)

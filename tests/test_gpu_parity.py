@@ -188,3 +188,13 @@ def test_golden_fixtures(engine):
         corr, tabs = engine.run_host(b, groups=groups)
         compare_correlation(b, corr, ca, cs)
         compare_tables(b, tabs, aa, ast)
+
+
+def test_unsorted_input_is_rejected(engine):
+    """Traces must be in timeline order (span.hpp:161-163); an unsorted trace is
+    detected on the device (no silent misattribution)."""
+    from paper_1908_06869_b200 import _capi as capi
+    b = batch_of([cases.nesting()[::-1]], sort=False)
+    with pytest.raises(capi.XspError) as e:
+        engine.run_host(b)
+    assert e.value.status == capi.XSP_E_UNSORTED
