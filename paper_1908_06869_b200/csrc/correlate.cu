@@ -7,14 +7,18 @@
 // over the timeline-ordered span columns (pass 1):
 //   * layers are placed by a per-span compare against their trace's model span
 //     and numbered by a global placed-layer count (layer_index = count - trace base);
-//   * every child span carries the scan state "top-2 end_ns among the placed
-//     layers that precede it in its trace" (+ the arg of the max). Because the
-//     input is sorted by (begin, rank, span_id), exactly the preceding placed
-//     layers have begin <= child.begin, so the containment candidates are the
-//     preceding layers with end >= child.end: 0 -> orphan, 1 -> the argmax,
-//     >= 2 -> ambiguity (full candidate list built on a rare path);
-//   * execs and kernel launches are compacted into timeline-ordered lists.
-// The cid join is a per-trace open-addressing table in HBM/L2.
+//   * because the input is sorted by (begin, rank, span_id), the containment
+//     candidates of a child are exactly the preceding placed layers of its trace
+//     with end >= child.end. The scan carries, for the last preceding placed
+//     layer j, end_j and M_j = max end over the layers before j, which decides
+//     0 / 1 / >=2 candidates exactly except when end_j < e <= M_j (nested or
+//     overlapping layers), which goes to an exact rare path;
+//   * kernel launches (+ synchronous kernels) and execs are compacted into
+//     timeline-ordered 16-byte entries.
+// The cid join (stage d) is a sort-merge join on presorted input: per trace,
+// the r-th cid-bearing launch meets the r-th exec when both streams carry the
+// same strictly increasing cids (checked in one streaming pass); traces that
+// fail the check use a per-trace open-addressing table.
 // Orphans, ambiguities and explicit-parent kernels are rare: they are appended
 // to exception lists and put into the reference's output order by radix sort.
 
@@ -30,15 +34,25 @@ constexpr uint32_t PAR_MAXROW = 0xFFFFFFF0u;
 
 // Orphan categories = the reference's emission phases, in output order.
 enum : uint32_t {
-  CAT_LAYER = 0,     // layer pass, timeline order            (correlator.cpp:168-204)
-  CAT_KERNEL = 1,    // kernel pass, timeline order           (:226-259)
-  CAT_EXEC_NOCID = 2,// exec without cid, timeline order      (:289-295)
-  CAT_LAUNCH = 3,    // launch fusion failures, tree order    (:321-346)
-  CAT_LEFTOVER = 4   // unconsumed execs, by span_id          (:355-363)
+  CAT_LAYER = 0,      // layer pass, timeline order            (correlator.cpp:168-204)
+  CAT_KERNEL = 1,     // kernel pass, timeline order           (:226-259)
+  CAT_EXEC_NOCID = 2, // exec without cid, timeline order      (:289-295)
+  CAT_LAUNCH = 3,     // launch fusion failures, tree order    (:321-346)
+  CAT_LEFTOVER = 4    // unconsumed execs, by span_id          (:355-363)
 };
 
-// kl_info bits
-constexpr uint8_t KL_SYNC = 1, KL_CID = 2, KL_LAUNCH = 4;
+// Kernel-list entry: a kernel launch (Kernel/Api level) or a synchronous kernel.
+struct __align__(16) KlEnt {
+  uint32_t row;     // span row
+  uint32_t parent;  // placed layer row, or PAR_*
+  uint64_t cid;     // correlation id (0 if absent)
+};
+// Execution-list entry: an exec span carrying a correlation id.
+struct __align__(16) ExEnt {
+  uint32_t row;   // span row
+  uint32_t mrow;  // metric-table row, kNone if none
+  uint64_t cid;
+};
 
 struct Orphans {
   uint64_t* tc;   // trace << 3 | category
@@ -55,6 +69,26 @@ __device__ __forceinline__ void emit_orphan(const Orphans& o, uint32_t t, uint32
   o.key[s] = key;
   o.row[s] = row;
   o.reason[s] = reason;
+}
+
+__device__ __forceinline__ uint32_t trace_of32(const uint32_t* __restrict__ off, uint32_t T, uint32_t i) {
+  uint32_t lo = 0, hi = T;  // off[lo] <= i < off[hi]
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(off + mid) <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Trace of item i for a warp processing consecutive items: one binary search
+// per warp, then a short per-lane walk (items of a trace are contiguous).
+__device__ __forceinline__ uint32_t warp_trace_of(const uint32_t* __restrict__ off, uint32_t T,
+                                                  uint32_t i, uint32_t first_i) {
+  uint32_t t0 = 0;
+  if (lane_id() == 0) t0 = trace_of32(off, T, first_i);
+  uint32_t t = __shfl_sync(0xffffffffu, t0, 0);
+  while (t + 1 < T && __ldg(off + t + 1) <= i) ++t;
+  return t;
 }
 
 // ---------------------------------------------------------------------------
@@ -98,17 +132,8 @@ __global__ void k_trace_prep(const uint8_t* __restrict__ flags, const uint64_t* 
 }
 
 // ---------------------------------------------------------------------------
-// Pass-1 scan state (the decoupled look-back payload).
-//
-// For a child span c whose last preceding placed layer (in its trace) is j,
-// with M_j = max end_ns over the placed layers before j, the containment
-// candidates are exactly the preceding placed layers with end >= c.end, so:
-//   end_j >= e, M_j <  e  -> one candidate: j
-//   end_j >= e, M_j >= e  -> >= 2 candidates: ambiguity
-//   end_j <  e, M_j <  e  -> no candidate: orphan
-//   end_j <  e, M_j >= e  -> an earlier layer outlives j (nested/overlapping
-//                            layers): resolved exactly on the rare path.
-// Ends are stored as end+1 so that 0 means "no layer".
+// Pass-1 scan state (the decoupled look-back payload). Ends are stored as
+// end+1 so that 0 means "no layer".
 struct Full {
   uint64_t last_end1;  // end+1 of the last placed layer of the current trace segment
   uint64_t last_M1;    // max end+1 over placed layers before it in the segment
@@ -177,13 +202,13 @@ __device__ __forceinline__ Full shfl_full(const Full& v, int src) {
   return u;
 }
 
-// Per-chunk (32 spans, one per lane) evaluation shared by both phases.
+// Per-chunk (32 spans, one per lane) segmented max-scan over placed-layer ends.
 struct Chunk {
-  uint32_t P, H;      // ballots: placed layers, trace heads
-  int seg;            // highest head lane <= this lane, -1 if none
-  uint64_t w;         // end+1 if placed else 0
-  uint64_t exM;       // max w over lanes [max(seg,0), lane) of the segment
-  uint64_t incM;      // max w over lanes [max(seg,0), lane]
+  uint32_t P, H;  // ballots: placed layers, trace heads
+  int seg;        // highest head lane <= this lane, -1 if none
+  uint64_t w;     // end+1 if placed else 0
+  uint64_t exM;   // max w over lanes [max(seg,0), lane)
+  uint64_t incM;  // max w over lanes [max(seg,0), lane]
 };
 
 __device__ __forceinline__ Chunk chunk_scan(bool placed, bool head, uint64_t e) {
@@ -208,7 +233,6 @@ __device__ __forceinline__ Chunk chunk_scan(bool placed, bool head, uint64_t e) 
   return k;
 }
 
-// Aggregate of one chunk (counts come from ballots).
 __device__ __forceinline__ Full chunk_agg(const Chunk& k, uint32_t bm, uint32_t bl, uint32_t bk,
                                           uint32_t bx) {
   Full f;
@@ -234,16 +258,16 @@ constexpr int P1_WARPS = 8;
 constexpr int P1_CHUNKS = 8;
 constexpr int P1_SUB = P1_CHUNKS * 32;
 constexpr int P1_TILE = P1_WARPS * P1_SUB;
+constexpr int P1_TCACHE = 32;  // traces of a tile cached in shared memory
 
 struct P1Args {
+  int bulk;  // all columns 16-byte aligned: stage full tiles with cp.async.bulk
   const uint64_t* span_id;
-  uint32_t* unsorted;
   const uint8_t* flags;
   const uint64_t* begin;
   const uint64_t* end;
   const uint64_t* parent;
   const uint64_t* cid;
-  const uint32_t* name;
   uint64_t n;
   const uint64_t* off;
   uint32_t T;
@@ -256,23 +280,14 @@ struct P1Args {
   uint32_t* tile_flag;
   Full* tile_agg;
   Full* tile_inc;
+  uint32_t* unsorted;
   unsigned long long* err_key;
   uint32_t* layer_row;
   uint64_t* layer_dur;
   uint32_t* layer_attr_row;
-  uint64_t* layer_end;
-  uint32_t* kl_row;
-  uint32_t* kl_parent;
-  uint64_t* kl_cid;
-  uint8_t* kl_info;
-  uint64_t* kl_dur;
-  uint32_t* kl_mrow;
-  uint32_t* kl_name;
-  uint32_t* ex_row;
-  uint64_t* ex_cid;
-  uint64_t* ex_dur;
-  uint32_t* ex_mrow;
-  uint32_t* ex_name;
+  KlEnt* kl;
+  uint32_t* kl_mrow;  // synchronous kernels only
+  ExEnt* ex;
   uint32_t* t_layer_off;
   uint32_t* t_kl_off;
   uint32_t* t_ex_off;
@@ -284,62 +299,154 @@ struct P1Args {
   uint32_t* pend_count;
 };
 
-// Layer placement under the model span (correlator.cpp:169-194).
-__device__ __forceinline__ bool layer_placed(uint8_t f, uint64_t b, uint64_t e, uint64_t i,
-                                             uint32_t t, const P1Args& a) {
-  if (a.model_row[t] == kNone) return false;
-  if (f & XSP_F_PARENT) return __ldg(a.parent + i) == a.msid[t];
-  return a.mb[t] <= b && e <= a.me[t];
+struct TraceCache {
+  uint64_t off[P1_TCACHE + 1];
+  uint64_t mb[P1_TCACHE], me[P1_TCACHE], msid[P1_TCACHE];
+  uint32_t model_row[P1_TCACHE], levels[P1_TCACHE];
+};
+
+// Tile staging buffer (dynamic shared memory): the tile's span columns, brought
+// in by one bulk asynchronous copy per column (TMA engine, cp.async.bulk).
+struct TileSmem {
+  uint64_t begin[P1_TILE];
+  uint64_t end[P1_TILE];
+  uint64_t cid[P1_TILE];
+  uint64_t parent[P1_TILE];
+  uint8_t flags[P1_TILE];
+};
+constexpr size_t P1_SMEM = sizeof(TileSmem);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
-__global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
+__global__ void __launch_bounds__(P1_WARPS * 32, 3) k_pass1(P1Args a) {
+  extern __shared__ __align__(128) unsigned char p1_dyn[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(p1_dyn);
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_tlo, s_thi;
   __shared__ Full s_wagg[P1_WARPS];
   __shared__ Full s_prefix;
+  __shared__ TraceCache tc;
+  __shared__ __align__(8) uint64_t s_bar;
 
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_ticket, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t tile_base = (uint64_t)tile * P1_TILE;
   if (threadIdx.x == 0) {
-    uint64_t last = tile_base + P1_TILE;
+    const uint32_t tile = atomicAdd(a.tile_ticket, 1u);
+    const uint64_t tb = (uint64_t)tile * P1_TILE;
+    uint64_t last = tb + P1_TILE;
     if (last > a.n) last = a.n;
-    uint32_t lo = trace_of(a.off, 0, a.T, tile_base);
-    uint32_t hi = trace_of(a.off, lo, a.T, last - 1) + 1;
+    const uint32_t lo = trace_of(a.off, 0, a.T, tb);
+    s_tile = tile;
     s_tlo = lo;
-    s_thi = hi;
+    s_thi = trace_of(a.off, lo, a.T, last - 1) + 1;
+    // stage the tile: one bulk copy per column (full, aligned tiles)
+    if (a.bulk && last - tb == P1_TILE) {
+      mbar_init(&s_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&s_bar, P1_TILE * (4 * 8 + 1));
+      bulk_g2s(sm.begin, a.begin + tb, P1_TILE * 8, &s_bar);
+      bulk_g2s(sm.end, a.end + tb, P1_TILE * 8, &s_bar);
+      bulk_g2s(sm.cid, a.cid + tb, P1_TILE * 8, &s_bar);
+      bulk_g2s(sm.parent, a.parent + tb, P1_TILE * 8, &s_bar);
+      bulk_g2s(sm.flags, a.flags + tb, P1_TILE, &s_bar);
+    }
   }
   __syncthreads();
-  const uint32_t tlo = s_tlo, thi = s_thi;
-  const bool one_trace = thi - tlo == 1;
-  const uint64_t wbase = tile_base + (uint64_t)warp * P1_SUB;
+  const uint32_t tile = s_tile, tlo = s_tlo, thi = s_thi;
+  const uint64_t tile_base = (uint64_t)tile * P1_TILE;
+  const uint32_t tile_n = (uint32_t)min((uint64_t)P1_TILE, a.n - tile_base);
+  const uint32_t ncache = min(thi - tlo, (uint32_t)P1_TCACHE);
+  if (threadIdx.x <= ncache) tc.off[threadIdx.x] = a.off[tlo + threadIdx.x];
+  if (threadIdx.x < ncache) {
+    const uint32_t t = tlo + threadIdx.x;
+    tc.mb[threadIdx.x] = a.mb[t];
+    tc.me[threadIdx.x] = a.me[t];
+    tc.msid[threadIdx.x] = a.msid[t];
+    tc.model_row[threadIdx.x] = a.model_row[t];
+    tc.levels[threadIdx.x] = a.levels[t];
+  }
+  if (a.bulk && tile_n == P1_TILE) {
+    mbar_wait(&s_bar, 0);
+  } else {
+    for (uint32_t j = threadIdx.x; j < P1_TILE; j += blockDim.x) {
+      const bool v = j < tile_n;
+      const uint64_t i = tile_base + j;
+      sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
+      sm.begin[j] = v ? a.begin[i] : 0;
+      sm.end[j] = v ? a.end[i] : 0;
+      sm.cid[j] = v ? a.cid[i] : 0;
+      sm.parent[j] = v ? a.parent[i] : 0;
+    }
+  }
+  __syncthreads();
+  const bool cached = thi - tlo <= (uint32_t)P1_TCACHE;
+  const uint32_t wj = warp * P1_SUB;  // warp's first local index
+
+  // trace index of span i (relative to tlo)
+  auto trace_rel = [&](uint64_t i) -> uint32_t {
+    if (cached) {
+      uint32_t lo = 0, hi = thi - tlo;
+      while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (tc.off[mid] <= i) lo = mid; else hi = mid;
+      }
+      return lo;
+    }
+    return trace_of(a.off, tlo, thi, i) - tlo;
+  };
+  auto t_off = [&](uint32_t r) { return cached ? tc.off[r] : a.off[tlo + r]; };
+  auto t_model = [&](uint32_t r) { return cached ? tc.model_row[r] : a.model_row[tlo + r]; };
+  // layer placement under the model span (correlator.cpp:169-194)
+  auto placed_in = [&](uint8_t f, uint64_t b, uint64_t e, uint64_t par, uint32_t r) -> bool {
+    if (t_model(r) == kNone) return false;
+    if (f & XSP_F_PARENT) return par == (cached ? tc.msid[r] : a.msid[tlo + r]);
+    return (cached ? tc.mb[r] : a.mb[tlo + r]) <= b && e <= (cached ? tc.me[r] : a.me[tlo + r]);
+  };
 
   // ---- phase 1: warp aggregate ----------------------------------------------
   Full wagg = full_identity();
 #pragma unroll 2
   for (int c = 0; c < P1_CHUNKS; ++c) {
-    const uint64_t i = wbase + c * 32 + lane;
-    const bool v = i < a.n;
-    const uint8_t f = v ? __ldg(a.flags + i) : (uint8_t)0xFF;
-    const uint32_t t = !v ? 0 : (one_trace ? tlo : trace_of(a.off, tlo, thi, i));
-    const bool head = v && __ldg(a.off + t) == i;
+    const uint32_t j = wj + c * 32 + lane;
+    const uint64_t i = tile_base + j;
+    const bool v = j < tile_n;
+    const uint8_t f = sm.flags[j];
+    const uint32_t r = v ? trace_rel(i) : 0;
+    const bool head = v && t_off(r) == i;
     const bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
-    bool placed = false;
-    uint64_t e = 0;
-    if (is_layer && f_kind(f) == XSP_KIND_SYNC) {
-      const uint64_t b = __ldg(a.begin + i);
-      e = __ldg(a.end + i);
-      placed = layer_placed(f, b, e, i, t, a);
-    }
+    const uint64_t e = sm.end[j];
+    const bool placed = is_layer && f_kind(f) == XSP_KIND_SYNC && placed_in(f, sm.begin[j], e, sm.parent[j], r);
     const bool kl = v && (is_kernel_launch(f) || is_sync_kernel(f));
     const bool ex = v && is_exec(f) && (f & XSP_F_CID);
     const bool met = v && (f & XSP_F_METRICS);
-    Chunk k = chunk_scan(placed, head, e);
-    Full ch = chunk_agg(k, __ballot_sync(0xffffffffu, met), __ballot_sync(0xffffffffu, is_layer),
-                        __ballot_sync(0xffffffffu, kl), __ballot_sync(0xffffffffu, ex));
-    wagg = full_combine(wagg, ch);
+    const Chunk k = chunk_scan(placed, head, e);
+    wagg = full_combine(wagg, chunk_agg(k, __ballot_sync(0xffffffffu, met), __ballot_sync(0xffffffffu, is_layer),
+                                        __ballot_sync(0xffffffffu, kl), __ballot_sync(0xffffffffu, ex)));
   }
   if (lane == 0) s_wagg[warp] = wagg;
   __syncthreads();
@@ -365,18 +472,18 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
       Full acc = full_identity();
       int64_t base = (int64_t)tile - 1;
       for (;;) {
-        const int64_t j = base - lane;
+        const int64_t jt = base - lane;
         uint32_t fl = 2;  // before tile 0: identity prefix
-        if (j >= 0) {
+        if (jt >= 0) {
           do {
-            fl = *((volatile uint32_t*)(a.tile_flag + j));
+            fl = *((volatile uint32_t*)(a.tile_flag + jt));
           } while (fl == 0);
         }
         __threadfence();
         const uint32_t incl = __ballot_sync(0xffffffffu, fl == 2);
         const uint32_t stop = incl ? (__ffs(incl) - 1) : 31;  // closest inclusive prefix
         Full v = full_identity();
-        if (j >= 0 && lane <= stop) v = (fl == 2) ? load_full(a.tile_inc + j) : load_full(a.tile_agg + j);
+        if (jt >= 0 && lane <= stop) v = (fl == 2) ? load_full(a.tile_inc + jt) : load_full(a.tile_agg + jt);
         // ordered tree reduction: higher lanes hold older tiles
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -408,19 +515,23 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
   // ---- phase 3: per-span outputs -------------------------------------------
   const uint32_t lt = lanemask_lt();
   for (int c = 0; c < P1_CHUNKS; ++c) {
-    const uint64_t i = wbase + c * 32 + lane;
-    const bool v = i < a.n;
-    const uint8_t f = v ? __ldg(a.flags + i) : (uint8_t)0xFF;
-    const uint64_t b = v ? __ldg(a.begin + i) : 0;
-    const uint64_t e = v ? __ldg(a.end + i) : 0;
-    const uint32_t t = !v ? 0 : (one_trace ? tlo : trace_of(a.off, tlo, thi, i));
-    const bool head = v && __ldg(a.off + t) == i;
+    const uint32_t j = wj + c * 32 + lane;
+    const uint64_t i = tile_base + j;
+    const bool v = j < tile_n;
+    const uint8_t f = sm.flags[j];
+    const uint64_t b = sm.begin[j];
+    const uint64_t e = sm.end[j];
+    const uint32_t r = v ? trace_rel(i) : 0;
+    const uint32_t t = tlo + r;
+    const bool head = v && t_off(r) == i;
     const bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
     const bool layer_sync = is_layer && f_kind(f) == XSP_KIND_SYNC;
-    const bool placed = layer_sync && layer_placed(f, b, e, i, t, a);
-    const bool kl = v && (is_kernel_launch(f) || is_sync_kernel(f));
+    const bool placed = layer_sync && placed_in(f, b, e, sm.parent[j], r);
+    const bool sync = v && is_sync_kernel(f);
+    const bool kl = v && (is_kernel_launch(f) || sync);
     const bool exe = v && is_exec(f);
-    const bool ex = exe && (f & XSP_F_CID);
+    const bool has_cid = f & XSP_F_CID;
+    const bool ex = exe && has_cid;
     const bool met = v && (f & XSP_F_METRICS);
 
     const uint32_t bm = __ballot_sync(0xffffffffu, met);
@@ -429,38 +540,15 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
     const uint32_t bx = __ballot_sync(0xffffffffu, ex);
     const Chunk k = chunk_scan(placed, head, e);
     const uint32_t g_ex = carry.c + __popc(k.P & lt);
-    const uint32_t m_ex = carry.c_metric + __popc(bm & lt);
-    const uint32_t l_ex = carry.c_lay + __popc(bl & lt);
-    const uint32_t k_ex = carry.c_kl + __popc(bk & lt);
-    const uint32_t x_ex = carry.c_ex + __popc(bx & lt);
-
-    // last placed layer before this lane in its trace segment: (end+1, M+1)
-    const uint32_t segmask = k.seg >= 0 ? (0xffffffffu << k.seg) : 0xffffffffu;
-    const uint32_t pq = k.P & lt & segmask;
-    const int q = pq ? 31 - __clz(pq) : 0;
-    const uint64_t qw = __shfl_sync(0xffffffffu, k.w, q);
-    const uint64_t qex = __shfl_sync(0xffffffffu, k.exM, q);
-    uint64_t jend1 = 0, jM1 = 0;
-    if (pq) {
-      jend1 = qw;
-      jM1 = k.seg >= 0 ? qex : max64(carry.run_M1, qex);
-    } else if (k.seg < 0) {
-      jend1 = carry.last_end1;
-      jM1 = carry.last_M1;
-    }
 
     // timeline order (begin_ns, rank, span_id) within the trace (span.hpp:161-163)
-    {
-      uint64_t pb = __shfl_up_sync(0xffffffffu, b, 1);
-      uint32_t pf = __shfl_up_sync(0xffffffffu, (uint32_t)f, 1);
-      if (lane == 0 && v && i > 0) {
-        pb = __ldg(a.begin + i - 1);
-        pf = __ldg(a.flags + i - 1);
-      }
-      if (v && !head && i > 0 && pb >= b) {
+    if (v && !head && i > 0) {
+      const uint64_t pb = j > 0 ? sm.begin[j - 1] : __ldg(a.begin + i - 1);
+      if (pb >= b) {
         bool bad = pb > b;
         if (!bad) {
-          const uint32_t l0 = f_level((uint8_t)pf), l1 = f_level(f);
+          const uint8_t pf = j > 0 ? sm.flags[j - 1] : __ldg(a.flags + i - 1);
+          const uint32_t l0 = f_level(pf), l1 = f_level(f);
           const uint32_t r0 = l0 >= 2 ? 3 : l0 + 1, r1 = l1 >= 2 ? 3 : l1 + 1;
           bad = r0 > r1 || (r0 == r1 && __ldg(a.span_id + i - 1) > __ldg(a.span_id + i));
         }
@@ -468,47 +556,50 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
       }
     }
 
+    // (end+1, M+1) of the last placed layer before each lane in its segment
+    const uint32_t segmask = k.seg >= 0 ? (0xffffffffu << k.seg) : 0xffffffffu;
+    const uint32_t pq = k.P & lt & segmask;
+    const int q = pq ? 31 - __clz(pq) : 0;
+    const uint64_t qw = __shfl_sync(0xffffffffu, k.w, q);
+    const uint64_t qex = __shfl_sync(0xffffffffu, k.exM, q);
+
     if (v) {
       // trace errors raised while walking the bundle (correlator.cpp:146-158)
-      if (is_model_span(f) && (uint32_t)i != a.model_row[t])
+      if (is_model_span(f) && (uint32_t)i != t_model(r))
         atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_MULTI_MODEL);
-      if (f_level(f) >= XSP_LEVEL_KERNEL && !(a.levels[t] & (1u << XSP_LEVEL_LAYER)))
+      if (f_level(f) >= XSP_LEVEL_KERNEL &&
+          !((cached ? tc.levels[r] : a.levels[t]) & (1u << XSP_LEVEL_LAYER)))
         atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_SKIP_LEVEL);
 
       if (is_layer) {
-        if (layer_sync) {
-          if (placed) {
-            a.layer_row[g_ex] = (uint32_t)i;
-            a.layer_dur[g_ex] = clamp_dur(b, e);
-            a.layer_attr_row[g_ex] = l_ex;
-            a.layer_end[g_ex] = e;
-          } else {
-            emit_orphan(a.orph, t, CAT_LAYER, i, (uint32_t)i,
-                        (f & XSP_F_PARENT) ? XSP_O_LAYER_BAD_PARENT : XSP_O_LAYER_OUTSIDE_MODEL);
-          }
+        const uint32_t l_ex = carry.c_lay + __popc(bl & lt);
+        if (layer_sync && placed) {
+          a.layer_row[g_ex] = (uint32_t)i;
+          a.layer_dur[g_ex] = clamp_dur(b, e);
+          a.layer_attr_row[g_ex] = l_ex;
         } else {
-          emit_orphan(a.orph, t, CAT_LAYER, i, (uint32_t)i, XSP_O_LAYER_NON_SYNC);
+          emit_orphan(a.orph, t, CAT_LAYER, i, (uint32_t)i,
+                      !layer_sync ? XSP_O_LAYER_NON_SYNC
+                                  : ((f & XSP_F_PARENT) ? XSP_O_LAYER_BAD_PARENT : XSP_O_LAYER_OUTSIDE_MODEL));
         }
       }
       if (kl) {
-        const bool sync = is_sync_kernel(f);
-        a.kl_row[k_ex] = (uint32_t)i;
-        a.kl_cid[k_ex] = (f & XSP_F_CID) ? __ldg(a.cid + i) : 0;
-        a.kl_info[k_ex] = (uint8_t)((sync ? KL_SYNC : 0) | ((f & XSP_F_CID) ? KL_CID : 0) |
-                                    (sync ? 0 : KL_LAUNCH));
-        if (sync) {
-          a.kl_dur[k_ex] = clamp_dur(b, e);
-          a.kl_mrow[k_ex] = met ? m_ex : kNone;
-          a.kl_name[k_ex] = __ldg(a.name + i);
-        }
+        const uint32_t k_ex = carry.c_kl + __popc(bk & lt);
         uint32_t par;
         if (f & XSP_F_PARENT) {
           par = PAR_PENDING;
-          uint32_t s = atomicAdd(a.pend_count, 1u);
-          a.pend_kl[s] = k_ex;
+          a.pend_kl[atomicAdd(a.pend_count, 1u)] = k_ex;
         } else {
+          uint64_t jend1 = 0, jM1 = 0;
+          if (pq) {
+            jend1 = qw;
+            jM1 = k.seg >= 0 ? qex : max64(carry.run_M1, qex);
+          } else if (k.seg < 0) {
+            jend1 = carry.last_end1;
+            jM1 = carry.last_M1;
+          }
           const bool in_j = jend1 > e;  // end_j >= e (ends stored +1)
-          const bool in_m = jM1 > e;    // some earlier layer has end >= e
+          const bool in_m = jM1 > e;    // an earlier layer has end >= e
           if (in_j && !in_m) {
             par = g_ex - 1;
           } else if (!in_j && !in_m) {
@@ -517,25 +608,32 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1(P1Args a) {
           } else {
             // >= 2 candidates, or an earlier layer outlives j: exact rare path
             par = PAR_AMBIG;
-            uint32_t s = atomicAdd(a.amb_count, 1u);
+            const uint32_t s = atomicAdd(a.amb_count, 1u);
             a.amb_kl[s] = k_ex;
             a.amb_gx[s] = g_ex;
           }
         }
-        a.kl_parent[k_ex] = par;
+        KlEnt ent;
+        ent.row = (uint32_t)i;
+        ent.parent = par;
+        ent.cid = has_cid ? sm.cid[j] : 0;
+        a.kl[k_ex] = ent;
+        if (sync) a.kl_mrow[k_ex] = met ? carry.c_metric + __popc(bm & lt) : kNone;
       }
       if (exe) {
         if (ex) {
-          a.ex_row[x_ex] = (uint32_t)i;
-          a.ex_cid[x_ex] = __ldg(a.cid + i);
-          a.ex_dur[x_ex] = clamp_dur(b, e);
-          a.ex_mrow[x_ex] = met ? m_ex : kNone;
-          a.ex_name[x_ex] = __ldg(a.name + i);
+          ExEnt ent;
+          ent.row = (uint32_t)i;
+          ent.mrow = met ? carry.c_metric + __popc(bm & lt) : kNone;
+          ent.cid = sm.cid[j];
+          a.ex[carry.c_ex + __popc(bx & lt)] = ent;
         } else {
           emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
         }
       }
       if (head) {
+        const uint32_t k_ex = carry.c_kl + __popc(bk & lt);
+        const uint32_t x_ex = carry.c_ex + __popc(bx & lt);
         int64_t tt = t;
         do {
           a.t_layer_off[tt] = g_ex;
@@ -576,16 +674,6 @@ __global__ void k_pass1_tail(const uint64_t* __restrict__ off, uint32_t T, uint6
 // placed layer of the same trace; layer_by_span_id keeps the LAST layer (in
 // layer_index order) with a given span_id (map assignment, :217-219).
 
-__device__ __forceinline__ uint32_t trace_of32(const uint32_t* __restrict__ off, uint32_t T,
-                                               uint32_t i) {
-  uint32_t lo = 0, hi = T;  // off[lo] <= i < off[hi]
-  while (hi - lo > 1) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (off[mid] <= i) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 // per trace: are placed-layer span_ids non-decreasing in layer order?
 __global__ void k_layer_ids_sorted(const uint32_t* __restrict__ layer_row, const uint64_t* __restrict__ sid,
                                    const uint32_t* __restrict__ t_layer_off, uint32_t T, uint32_t nl,
@@ -598,15 +686,14 @@ __global__ void k_layer_ids_sorted(const uint32_t* __restrict__ layer_row, const
 }
 
 __global__ void k_resolve_explicit(const uint32_t* __restrict__ pend_kl, const uint32_t* __restrict__ pend_count,
-                                   const uint32_t* __restrict__ kl_row, uint32_t* __restrict__ kl_parent,
-                                   const uint64_t* __restrict__ parent, const uint64_t* __restrict__ sid,
-                                   const uint32_t* __restrict__ layer_row, const uint32_t* __restrict__ t_layer_off,
-                                   const uint32_t* __restrict__ t_kl_off, uint32_t T,
-                                   const uint32_t* __restrict__ t_unsorted, Orphans orph) {
+                                   KlEnt* __restrict__ kl, const uint64_t* __restrict__ parent,
+                                   const uint64_t* __restrict__ sid, const uint32_t* __restrict__ layer_row,
+                                   const uint32_t* __restrict__ t_layer_off, const uint32_t* __restrict__ t_kl_off,
+                                   uint32_t T, const uint32_t* __restrict__ t_unsorted, Orphans orph) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= *pend_count) return;
   uint32_t k = pend_kl[p];
-  uint32_t i = kl_row[k];
+  uint32_t i = kl[k].row;
   uint32_t t = trace_of32(t_kl_off, T, k);
   uint64_t want = parent[i];
   uint32_t lo = t_layer_off[t], hi = t_layer_off[t + 1];
@@ -624,10 +711,10 @@ __global__ void k_resolve_explicit(const uint32_t* __restrict__ pend_kl, const u
       if (sid[layer_row[g]] == want) found = g;
   }
   if (found == kNone) {
-    kl_parent[k] = PAR_ORPHAN;
+    kl[k].parent = PAR_ORPHAN;
     emit_orphan(orph, t, CAT_KERNEL, i, i, XSP_O_KERNEL_BAD_PARENT);
   } else {
-    kl_parent[k] = found;
+    kl[k].parent = found;
   }
 }
 
@@ -638,27 +725,26 @@ __global__ void k_resolve_explicit(const uint32_t* __restrict__ pend_kl, const u
 // Children flagged in pass 1 with >= 2 candidates, or whose last preceding
 // layer does not contain them while an earlier one might: count exactly.
 __global__ void k_amb_resolve(uint32_t n_raw, const uint32_t* __restrict__ amb_kl,
-                              const uint32_t* __restrict__ amb_gx, const uint32_t* __restrict__ kl_row,
+                              const uint32_t* __restrict__ amb_gx, KlEnt* __restrict__ kl,
                               const uint64_t* __restrict__ end, const uint32_t* __restrict__ t_kl_off,
                               const uint32_t* __restrict__ t_layer_off, uint32_t T,
-                              const uint64_t* __restrict__ layer_end, uint32_t* __restrict__ kl_parent,
-                              uint32_t* __restrict__ keep) {
+                              const uint32_t* __restrict__ layer_row, uint32_t* __restrict__ keep) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_raw) return;
   const uint32_t k = amb_kl[p];
   const uint32_t t = trace_of32(t_kl_off, T, k);
-  const uint64_t e = end[kl_row[k]];
+  const uint64_t e = end[kl[k].row];
   const uint32_t lo = t_layer_off[t];
   uint32_t cnt = 0, last = kNone;
   for (uint32_t g = amb_gx[p]; g > lo && cnt < 2;) {
     --g;
-    if (layer_end[g] >= e) {
+    if (end[layer_row[g]] >= e) {
       ++cnt;
       last = g;
     }
   }
   if (cnt == 1) {
-    kl_parent[k] = last;
+    kl[k].parent = last;
     keep[p] = 0;
   } else {
     keep[p] = 1;
@@ -674,55 +760,53 @@ __global__ void k_amb_compact(uint32_t n_raw, const uint32_t* __restrict__ keep,
   gx2[pos[p]] = gx[p];
 }
 
-__global__ void k_amb_keys(const uint32_t* __restrict__ amb_kl, const uint32_t* __restrict__ amb_count,
-                           const uint32_t* __restrict__ kl_row, const uint64_t* __restrict__ sid,
-                           const uint32_t* __restrict__ t_kl_off, uint32_t T,
+__global__ void k_amb_keys(const uint32_t* __restrict__ amb_kl, uint32_t n_amb, const KlEnt* __restrict__ kl,
+                           const uint64_t* __restrict__ sid, const uint32_t* __restrict__ t_kl_off, uint32_t T,
                            uint64_t* __restrict__ key_sid, uint64_t* __restrict__ key_trace,
                            uint32_t* __restrict__ idx) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= *amb_count) return;
+  if (p >= n_amb) return;
   uint32_t k = amb_kl[p];
-  key_sid[p] = sid[kl_row[k]];
+  key_sid[p] = sid[kl[k].row];
   key_trace[p] = trace_of32(t_kl_off, T, k);
   idx[p] = p;
 }
 
 __global__ void k_amb_count(const uint32_t* __restrict__ order, uint32_t n_amb,
                             const uint32_t* __restrict__ amb_kl, const uint32_t* __restrict__ amb_gx,
-                            const uint32_t* __restrict__ kl_row, const uint64_t* __restrict__ end,
+                            const KlEnt* __restrict__ kl, const uint64_t* __restrict__ end,
                             const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_layer_off,
-                            uint32_t T, const uint64_t* __restrict__ layer_end, uint32_t* __restrict__ cnt) {
+                            uint32_t T, const uint32_t* __restrict__ layer_row, uint32_t* __restrict__ cnt) {
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n_amb) return;
   uint32_t p = order[q];
   uint32_t k = amb_kl[p];
   uint32_t t = trace_of32(t_kl_off, T, k);
-  uint64_t e = end[kl_row[k]];
+  uint64_t e = end[kl[k].row];
   uint32_t c = 0;
-  for (uint32_t g = t_layer_off[t]; g < amb_gx[p]; ++g) c += layer_end[g] >= e;
+  for (uint32_t g = t_layer_off[t]; g < amb_gx[p]; ++g) c += end[layer_row[g]] >= e;
   cnt[q] = c;
 }
 
 __global__ void k_amb_fill(const uint32_t* __restrict__ order, uint32_t n_amb,
                            const uint32_t* __restrict__ amb_kl, const uint32_t* __restrict__ amb_gx,
-                           const uint32_t* __restrict__ kl_row, const uint64_t* __restrict__ end,
+                           const KlEnt* __restrict__ kl, const uint64_t* __restrict__ end,
                            const uint64_t* __restrict__ sid, const uint32_t* __restrict__ t_kl_off,
                            const uint32_t* __restrict__ t_layer_off, uint32_t T,
-                           const uint64_t* __restrict__ layer_end, const uint32_t* __restrict__ layer_row,
-                           const uint32_t* __restrict__ cand_off, uint32_t* __restrict__ amb_row,
-                           uint32_t* __restrict__ cand_row) {
+                           const uint32_t* __restrict__ layer_row, const uint32_t* __restrict__ cand_off,
+                           uint32_t* __restrict__ amb_row, uint32_t* __restrict__ cand_row) {
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n_amb) return;
   uint32_t p = order[q];
   uint32_t k = amb_kl[p];
   uint32_t t = trace_of32(t_kl_off, T, k);
-  uint64_t e = end[kl_row[k]];
-  amb_row[q] = kl_row[k];
+  uint64_t e = end[kl[k].row];
+  amb_row[q] = kl[k].row;
   uint32_t o = cand_off[q], n = 0;
   for (uint32_t g = t_layer_off[t]; g < amb_gx[p]; ++g) {
-    if (layer_end[g] < e) continue;
-    // insertion by span_id (IntervalTree::containing sorts by span_id, :115-117)
     uint32_t r = layer_row[g];
+    if (end[r] < e) continue;
+    // insertion by span_id (IntervalTree::containing sorts by span_id, :115-117)
     uint64_t s = sid[r];
     uint32_t j = n;
     while (j > 0 && sid[cand_row[o + j - 1]] > s) {
@@ -735,7 +819,44 @@ __global__ void k_amb_fill(const uint32_t* __restrict__ order, uint32_t n_amb,
 }
 
 // ---------------------------------------------------------------------------
-// (d) cid join: one open-addressing region per trace, sized 2x its items.
+// (d) cid join.
+//
+// Fast path (sort-merge on presorted streams): trace t is "merge-aligned" when
+// it has as many cid-bearing exec entries as kernel-list entries, every entry is
+// a launch with a cid, and launch r and exec r carry the same cid with cids
+// strictly increasing in r. Then the r-th launch fuses with the r-th exec, every
+// exec is consumed and no cid repeats — exactly what the reference's hash maps
+// produce. Other traces use the per-trace open-addressing table below.
+
+__global__ void k_join_counts(const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
+                              uint32_t T, uint32_t* __restrict__ t_slow, uint32_t* __restrict__ any_slow) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const bool mismatch = (t_kl_off[t + 1] - t_kl_off[t]) != (t_ex_off[t + 1] - t_ex_off[t]);
+  t_slow[t] = mismatch;
+  if (mismatch) *any_slow = 1;
+}
+
+__global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const ExEnt* __restrict__ ex,
+                             const uint8_t* __restrict__ flags, const uint32_t* __restrict__ t_kl_off,
+                             const uint32_t* __restrict__ t_ex_off, uint32_t T, uint32_t* __restrict__ t_slow,
+                             uint32_t* __restrict__ any_slow) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t first = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  if (first >= nkl) return;
+  const uint32_t t = warp_trace_of(t_kl_off, T, k < nkl ? k : nkl - 1, first);
+  if (k >= nkl) return;
+  const uint32_t r = k - t_kl_off[t];
+  const KlEnt ent = kl[k];
+  const uint8_t f = flags[ent.row];
+  bool ok = !t_slow[t] && f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID);
+  if (ok) ok = ex[t_ex_off[t] + r].cid == ent.cid;
+  if (ok && r > 0) ok = kl[k - 1].cid < ent.cid;
+  if (!ok) {
+    t_slow[t] = 1;
+    *any_slow = 1;
+  }
+}
 
 __device__ __forceinline__ uint32_t mix32(uint64_t x) {
   x ^= x >> 33;
@@ -747,22 +868,22 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
 }
 
 __global__ void k_region_size(const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
-                              uint32_t T, uint64_t* __restrict__ rsize) {
+                              const uint32_t* __restrict__ t_slow, uint32_t T, uint64_t* __restrict__ rsize) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   uint64_t items = (uint64_t)(t_kl_off[t + 1] - t_kl_off[t]) + (t_ex_off[t + 1] - t_ex_off[t]);
-  uint64_t want = items * 2;
   uint64_t s = 16;
-  while (s < want) s <<= 1;
-  rsize[t] = items ? s : 0;
+  while (s < items * 2) s <<= 1;
+  rsize[t] = (items && t_slow[t]) ? s : 0;
 }
 
 struct JoinArgs {
-  const uint64_t* ex_cid;
-  const uint64_t* kl_cid;
-  const uint8_t* kl_info;
+  const ExEnt* ex;
+  const KlEnt* kl;
+  const uint8_t* flags;
   const uint32_t* t_ex_off;
   const uint32_t* t_kl_off;
+  const uint32_t* t_slow;
   uint32_t T;
   uint32_t n_ex, n_kl;
   const uint64_t* roff;  // region offsets [T+1]
@@ -774,7 +895,8 @@ struct JoinArgs {
   uint32_t* t_dup;       // bit0 exec dup, bit1 launch dup
 };
 
-// Items 0..n_ex-1 are execs, n_ex..n_ex+n_kl-1 are klist entries (launches with cid).
+// Items 0..n_ex-1 are execs, n_ex..n_ex+n_kl-1 kernel-list entries (launches
+// with a cid). Only items of slow traces take part.
 __global__ void k_join_insert(JoinArgs a) {
   uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
   if (it >= a.n_ex + a.n_kl) return;
@@ -783,13 +905,15 @@ __global__ void k_join_insert(JoinArgs a) {
   uint64_t cid;
   if (is_ex) {
     t = trace_of32(a.t_ex_off, a.T, it);
-    cid = a.ex_cid[it];
+    if (!a.t_slow[t]) return;
+    cid = a.ex[it].cid;
   } else {
     uint32_t k = it - a.n_ex;
-    uint8_t info = a.kl_info[k];
-    if (!(info & KL_LAUNCH) || !(info & KL_CID)) return;
     t = trace_of32(a.t_kl_off, a.T, k);
-    cid = a.kl_cid[k];
+    if (!a.t_slow[t]) return;
+    const uint8_t f = a.flags[a.kl[k].row];
+    if (!is_kernel_launch(f) || !(f & XSP_F_CID)) return;
+    cid = a.kl[k].cid;
   }
   const uint64_t base = a.roff[t];
   const uint32_t mask = (uint32_t)(a.roff[t + 1] - base - 1);
@@ -802,7 +926,7 @@ __global__ void k_join_insert(JoinArgs a) {
       if (o == 0) break;
     }
     uint32_t oi = o - 1;
-    uint64_t ocid = oi < a.n_ex ? a.ex_cid[oi] : a.kl_cid[oi - a.n_ex];
+    uint64_t ocid = oi < a.n_ex ? a.ex[oi].cid : a.kl[oi - a.n_ex].cid;
     if (ocid == cid) break;
     h = (h + 1) & mask;
   }
@@ -830,10 +954,10 @@ __global__ void k_join_dups(JoinArgs a, unsigned long long* __restrict__ dup_ex,
     if (first != it) atomicMin(dup_ex + t, ((unsigned long long)it << 32) | first);
   } else {
     uint32_t k = it - a.n_ex;
-    uint8_t info = a.kl_info[k];
-    if (!(info & KL_LAUNCH) || !(info & KL_CID)) return;
     uint32_t t = trace_of32(a.t_kl_off, a.T, k);
     if (!(a.t_dup[t] & 2u)) return;
+    const uint8_t f = a.flags[a.kl[k].row];
+    if (!is_kernel_launch(f) || !(f & XSP_F_CID)) return;
     uint32_t first = a.sl_launch[a.kl_slot[k]];
     if (first != k) atomicMin(dup_kl + t, ((unsigned long long)k << 32) | first);
   }
@@ -844,114 +968,119 @@ __global__ void k_join_dups(JoinArgs a, unsigned long long* __restrict__ dup_ex,
 
 struct FuseArgs {
   uint32_t n_kl, n_ex, T;
-  const uint32_t* kl_row;
-  const uint32_t* kl_parent;
-  const uint8_t* kl_info;
+  const KlEnt* kl;
+  const ExEnt* ex;
+  const uint8_t* flags;
+  const uint32_t* t_slow;
   const uint32_t* kl_slot;
   const uint32_t* sl_exec;
   const uint32_t* sl_launch;
   const uint32_t* ex_slot;
-  const uint32_t* ex_row;
   const uint64_t* sid;
   const uint32_t* t_kl_off;
   const uint32_t* t_ex_off;
-  uint32_t* kept;  // [n_kl] 0/1
+  uint32_t* kept;     // [n_kl] 0/1
   uint32_t* kl_exec;  // matched exec item
   Orphans orph;
+  bool any_slow;
 };
 
 __global__ void k_fuse(FuseArgs a) {
-  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < a.n_kl) {
-    uint32_t par = a.kl_parent[k];
-    uint32_t keep = 0;
-    uint32_t x = kNone;
-    if (par < PAR_MAXROW) {
-      uint8_t info = a.kl_info[k];
-      if (info & KL_SYNC) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t first = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  if (first >= a.n_kl) return;
+  const uint32_t t = warp_trace_of(a.t_kl_off, a.T, k < a.n_kl ? k : a.n_kl - 1, first);
+  if (k >= a.n_kl) return;
+  const KlEnt ent = a.kl[k];
+  uint32_t keep = 0, x = kNone;
+  if (ent.parent < PAR_MAXROW) {
+    const uint8_t f = a.flags[ent.row];
+    if (is_sync_kernel(f)) {
+      keep = 1;
+    } else if (!(f & XSP_F_CID)) {
+      emit_orphan(a.orph, t, CAT_LAUNCH, ((uint64_t)ent.parent << 32) | k, ent.row, XSP_O_LAUNCH_NO_CID);
+    } else {
+      x = (a.any_slow && a.t_slow[t]) ? a.sl_exec[a.kl_slot[k]] : a.t_ex_off[t] + (k - a.t_kl_off[t]);
+      if (x != kNone) {
         keep = 1;
-      } else if (!(info & KL_CID)) {
-        emit_orphan(a.orph, trace_of32(a.t_kl_off, a.T, k), CAT_LAUNCH,
-                    ((uint64_t)par << 32) | k, a.kl_row[k], XSP_O_LAUNCH_NO_CID);
       } else {
-        x = a.sl_exec[a.kl_slot[k]];
-        if (x != kNone) {
-          keep = 1;
-        } else {
-          emit_orphan(a.orph, trace_of32(a.t_kl_off, a.T, k), CAT_LAUNCH,
-                      ((uint64_t)par << 32) | k, a.kl_row[k], XSP_O_LAUNCH_NO_EXEC);
-        }
+        emit_orphan(a.orph, t, CAT_LAUNCH, ((uint64_t)ent.parent << 32) | k, ent.row, XSP_O_LAUNCH_NO_EXEC);
       }
     }
-    a.kept[k] = keep;
-    a.kl_exec[k] = x;
   }
-  if (k < a.n_ex) {
-    if (a.sl_launch[a.ex_slot[k]] == kNone) {
-      uint32_t r = a.ex_row[k];
-      emit_orphan(a.orph, trace_of32(a.t_ex_off, a.T, k), CAT_LEFTOVER, a.sid[r], r,
-                  XSP_O_EXEC_NO_LAUNCH);
-    }
+  a.kept[k] = keep;
+  a.kl_exec[k] = x;
+}
+
+__global__ void k_leftover(FuseArgs a) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= a.n_ex) return;
+  const uint32_t t = trace_of32(a.t_ex_off, a.T, x);
+  if (!a.t_slow[t]) return;  // merge-aligned traces consume every exec
+  if (a.sl_launch[a.ex_slot[x]] == kNone) {
+    const uint32_t r = a.ex[x].row;
+    emit_orphan(a.orph, t, CAT_LEFTOVER, a.sid[r], r, XSP_O_EXEC_NO_LAUNCH);
   }
 }
 
 // Compact kept kernels (timeline order) with their parent layer as the sort key.
 __global__ void k_compact_kernels(uint32_t n_kl, const uint32_t* __restrict__ kept,
-                                  const uint32_t* __restrict__ pos, const uint32_t* __restrict__ kl_parent,
+                                  const uint32_t* __restrict__ pos, const KlEnt* __restrict__ kl,
                                   uint64_t* __restrict__ key, uint32_t* __restrict__ val,
                                   uint32_t* __restrict__ nonmono) {
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_kl || !kept[k]) return;
-  uint32_t j = pos[k];
-  key[j] = kl_parent[k];
+  const uint32_t j = pos[k];
+  const uint32_t par = kl[k].parent;
+  key[j] = par;
   val[j] = k;
 }
 
-__global__ void k_check_mono(uint32_t nk, const uint64_t* __restrict__ key, uint32_t* __restrict__ nonmono) {
+// tree order == timeline order unless explicit parents broke it
+__global__ void k_check_mono(const uint32_t* __restrict__ nk, const uint64_t* __restrict__ key,
+                             uint32_t* __restrict__ nonmono) {
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j == 0 || j >= nk) return;
+  if (j == 0 || j >= *nk) return;
   if (key[j] < key[j - 1]) *nonmono = 1;
 }
 
-__global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val,
-                                 const uint32_t* __restrict__ kl_row, const uint8_t* __restrict__ kl_info,
-                                 const uint64_t* __restrict__ kl_dur, const uint32_t* __restrict__ kl_mrow,
-                                 const uint32_t* __restrict__ kl_name, const uint32_t* __restrict__ kl_exec,
-                                 const uint32_t* __restrict__ ex_row, const uint64_t* __restrict__ ex_dur,
-                                 const uint32_t* __restrict__ ex_mrow, const uint32_t* __restrict__ ex_name,
-                                 uint32_t* __restrict__ k_launch, uint32_t* __restrict__ k_exec,
-                                 uint32_t* __restrict__ k_mrow, uint64_t* __restrict__ k_dur,
-                                 uint32_t* __restrict__ k_name) {
+__global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val, const KlEnt* __restrict__ kl,
+                                 const uint32_t* __restrict__ kl_mrow, const uint32_t* __restrict__ kl_exec,
+                                 const ExEnt* __restrict__ ex, const uint8_t* __restrict__ flags,
+                                 const uint64_t* __restrict__ begin, const uint64_t* __restrict__ end,
+                                 const uint32_t* __restrict__ name, uint32_t* __restrict__ k_launch,
+                                 uint32_t* __restrict__ k_exec, uint32_t* __restrict__ k_mrow,
+                                 uint64_t* __restrict__ k_dur, uint32_t* __restrict__ k_name) {
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nk) return;
-  uint32_t k = val[j];
-  uint32_t r = kl_row[k];
-  k_launch[j] = r;
-  if (kl_info[k] & KL_SYNC) {
-    k_exec[j] = r;
-    k_mrow[j] = kl_mrow[k];
-    k_dur[j] = kl_dur[k];
-    k_name[j] = kl_name[k];
+  const uint32_t k = val[j];
+  const uint32_t r = kl[k].row;
+  const uint32_t x = kl_exec[k];
+  uint32_t er, mr;
+  if (x == kNone) {  // synchronous kernel: launch and exec are the same record
+    er = r;
+    mr = kl_mrow[k];
   } else {
-    uint32_t x = kl_exec[k];
-    k_exec[j] = ex_row[x];
-    k_mrow[j] = ex_mrow[x];
-    k_dur[j] = ex_dur[x];
-    k_name[j] = ex_name[x];
+    const ExEnt e = ex[x];
+    er = e.row;
+    mr = e.mrow;
   }
+  k_launch[j] = r;
+  k_exec[j] = er;
+  k_mrow[j] = mr;
+  k_dur[j] = clamp_dur(begin[er], end[er]);
+  k_name[j] = name[er];
 }
 
-// layer_kernel_off[g] = first kernel j whose parent >= g (keys sorted).
+// layer_kernel_off[g] = first kernel j whose parent >= g (keys sorted): each
+// boundary between consecutive keys fills the layers in between.
 __global__ void k_layer_kernel_off(uint32_t nl, uint32_t nk, const uint64_t* __restrict__ key,
                                    uint32_t* __restrict__ off) {
-  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g > nl) return;
-  uint32_t lo = 0, hi = nk;
-  while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (key[mid] < g) lo = mid + 1; else hi = mid;
-  }
-  off[g] = lo;
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > nk) return;
+  const int64_t prev = j > 0 ? (int64_t)key[j - 1] : -1;
+  const int64_t cur = j < nk ? (int64_t)key[j] : (int64_t)nl;
+  for (int64_t g = prev + 1; g <= cur; ++g) off[g] = j;
 }
 
 __global__ void k_trace_kernel_off(uint32_t T, const uint32_t* __restrict__ t_layer_off,
@@ -998,10 +1127,9 @@ __global__ void k_csr_by_trace(uint32_t T, uint32_t n, const uint64_t* __restric
 __global__ void k_status(uint32_t T, const uint32_t* __restrict__ model_row,
                          const unsigned long long* __restrict__ err_key,
                          const unsigned long long* __restrict__ dup_ex,
-                         const unsigned long long* __restrict__ dup_kl,
-                         const uint32_t* __restrict__ ex_row, const uint32_t* __restrict__ kl_row,
-                         int32_t* __restrict__ status, uint32_t* __restrict__ err_row,
-                         uint32_t* __restrict__ n_failed) {
+                         const unsigned long long* __restrict__ dup_kl, const ExEnt* __restrict__ ex,
+                         const KlEnt* __restrict__ kl, int32_t* __restrict__ status,
+                         uint32_t* __restrict__ err_row, uint32_t* __restrict__ n_failed) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   int32_t st = XSP_T_OK;
@@ -1013,12 +1141,12 @@ __global__ void k_status(uint32_t T, const uint32_t* __restrict__ model_row,
     ra = (uint32_t)(err_key[t] >> 8);
   } else if (dup_ex[t] != ~0ull) {
     st = XSP_T_DUP_EXEC_CID;
-    ra = ex_row[(uint32_t)dup_ex[t]];          // first occurrence
-    rb = ex_row[(uint32_t)(dup_ex[t] >> 32)];  // the duplicate
+    ra = ex[(uint32_t)dup_ex[t]].row;          // first occurrence
+    rb = ex[(uint32_t)(dup_ex[t] >> 32)].row;  // the duplicate
   } else if (dup_kl[t] != ~0ull) {
     st = XSP_T_DUP_LAUNCH_CID;
-    ra = kl_row[(uint32_t)dup_kl[t]];
-    rb = kl_row[(uint32_t)(dup_kl[t] >> 32)];
+    ra = kl[(uint32_t)dup_kl[t]].row;
+    rb = kl[(uint32_t)(dup_kl[t] >> 32)].row;
   }
   status[t] = st;
   err_row[2 * t] = ra;
@@ -1060,26 +1188,6 @@ uint32_t read_u32(xsp_ctx* ctx, const uint32_t* dptr, cudaStream_t st) {
 
 }  // namespace
 
-__global__ void k_check_sorted(const uint8_t* __restrict__ flags, const uint64_t* __restrict__ begin,
-                               const uint64_t* __restrict__ sid, const uint64_t* __restrict__ off,
-                               uint32_t T, uint64_t n, uint32_t* __restrict__ unsorted) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0 || i >= n) return;
-  uint32_t t = trace_of(off, 0, T, i);
-  if (off[t] == i) return;  // first span of its trace
-  uint64_t b0 = begin[i - 1], b1 = begin[i];
-  if (b0 < b1) return;
-  if (b0 > b1) {
-    *unsorted = 1;
-    return;
-  }
-  // rank: Model 1 < Layer 2 < Kernel = Api 3 (span.hpp:51-59)
-  uint32_t l0 = f_level(flags[i - 1]), l1 = f_level(flags[i]);
-  uint32_t r0 = l0 >= 2 ? 3 : l0 + 1, r1 = l1 >= 2 ? 3 : l1 + 1;
-  if (r0 < r1) return;
-  if (r0 > r1 || sid[i - 1] > sid[i]) *unsorted = 1;
-}
-
 void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, int sort_if_needed,
                    xsp_corr_out* out, cudaStream_t st) {
   const uint64_t n = c->n_spans;
@@ -1096,14 +1204,18 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   if (T) {
     ctx->stage_begin("trace_prep", st);
     unsigned blocks = ceil_div((uint64_t)T * 32, 256);
-    k_trace_prep<<<blocks, 256, 0, st>>>(c->flags, c->begin_ns, c->end_ns, c->span_id, off, T,
-                                         model_row, mb, me, msid, err_key);
+    k_trace_prep<<<blocks, 256, 0, st>>>(c->flags, c->begin_ns, c->end_ns, c->span_id, off, T, model_row, mb, me,
+                                         msid, err_key);
     ctx->stage_end("trace_prep", st);
     ++ctx->launches;
   }
 
   // ---- pass 1
   const uint32_t ntiles = ceil_div(n, P1_TILE);
+  // counters: [0] orphans [1] ambiguities [2] pending [3] nonmono [4] n_failed
+  //           [5] unsorted [6] ambiguities after resolution [7] any slow trace
+  uint32_t* counters = ctx->d<uint32_t>("c.counters", 8);
+  XSP_CUDA(cudaMemsetAsync(counters, 0, 8 * 4, st));
   P1Args a;
   a.span_id = c->span_id;
   a.flags = c->flags;
@@ -1111,7 +1223,6 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.end = c->end_ns;
   a.parent = c->parent_id;
   a.cid = c->cid;
-  a.name = c->name_id;
   a.n = n;
   a.off = off;
   a.T = T;
@@ -1124,37 +1235,23 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.tile_flag = ctx->d<uint32_t>("c.tile_flag", ntiles + 1);
   a.tile_agg = ctx->d<Full>("c.tile_agg", ntiles + 1);
   a.tile_inc = ctx->d<Full>("c.tile_inc", ntiles + 1);
+  a.unsorted = counters + 5;
   a.err_key = err_key;
   a.layer_row = ctx->d<uint32_t>("o.layer_row", n);
   a.layer_dur = ctx->d<uint64_t>("o.layer_dur", n);
   a.layer_attr_row = ctx->d<uint32_t>("o.layer_attr_row", n);
-  a.layer_end = ctx->d<uint64_t>("c.layer_end", n);
-  a.kl_row = ctx->d<uint32_t>("c.kl_row", n);
-  a.kl_parent = ctx->d<uint32_t>("c.kl_parent", n);
-  a.kl_cid = ctx->d<uint64_t>("c.kl_cid", n);
-  a.kl_info = ctx->d<uint8_t>("c.kl_info", n);
-  a.kl_dur = ctx->d<uint64_t>("c.kl_dur", n);
+  a.kl = ctx->d<KlEnt>("c.kl", n);
   a.kl_mrow = ctx->d<uint32_t>("c.kl_mrow", n);
-  a.kl_name = ctx->d<uint32_t>("c.kl_name", n);
-  a.ex_row = ctx->d<uint32_t>("c.ex_row", n);
-  a.ex_cid = ctx->d<uint64_t>("c.ex_cid", n);
-  a.ex_dur = ctx->d<uint64_t>("c.ex_dur", n);
-  a.ex_mrow = ctx->d<uint32_t>("c.ex_mrow", n);
-  a.ex_name = ctx->d<uint32_t>("c.ex_name", n);
+  a.ex = ctx->d<ExEnt>("c.ex", n);
   a.t_layer_off = ctx->d<uint32_t>("o.t_layer_off", T + 1);
   a.t_kl_off = ctx->d<uint32_t>("c.t_kl_off", T + 1);
   a.t_ex_off = ctx->d<uint32_t>("c.t_ex_off", T + 1);
-  // counters: [0] orphans [1] ambiguities [2] pending [3] nonmono [4] n_failed
-  uint32_t* counters = ctx->d<uint32_t>("c.counters", 8);
-  XSP_CUDA(cudaMemsetAsync(counters, 0, 8 * 4, st));
-  a.unsorted = counters + 5;
   Orphans orph;
-  // orphans: at most one per span from pass 1 + one per launch + one per exec
-  const uint64_t orph_cap = n + 16;
-  orph.tc = ctx->d<uint64_t>("c.o_tc", orph_cap);
-  orph.key = ctx->d<uint64_t>("c.o_key", orph_cap);
-  orph.row = ctx->d<uint32_t>("c.o_row", orph_cap);
-  orph.reason = ctx->d<uint8_t>("c.o_reason", orph_cap);
+  const uint64_t orph_cap = n + 16;  // at most one per span (exec-level layers: two, but then no launch)
+  orph.tc = ctx->d<uint64_t>("c.o_tc", 2 * orph_cap);
+  orph.key = ctx->d<uint64_t>("c.o_key", 2 * orph_cap);
+  orph.row = ctx->d<uint32_t>("c.o_row", 2 * orph_cap);
+  orph.reason = ctx->d<uint8_t>("c.o_reason", 2 * orph_cap);
   orph.count = counters + 0;
   a.orph = orph;
   a.amb_kl = ctx->d<uint32_t>("c.amb_kl", n);
@@ -1164,9 +1261,12 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.pend_count = counters + 2;
   XSP_CUDA(cudaMemsetAsync(a.tile_ticket, 0, 4, st));
   XSP_CUDA(cudaMemsetAsync(a.tile_flag, 0, (ntiles + 1) * 4ull, st));
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  a.bulk = al16(c->begin_ns) && al16(c->end_ns) && al16(c->cid) && al16(c->parent_id) && al16(c->flags);
   if (ntiles) {
+    XSP_CUDA(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM));
     ctx->stage_begin("pass1", st);
-    k_pass1<<<ntiles, P1_WARPS * 32, 0, st>>>(a);
+    k_pass1<<<ntiles, P1_WARPS * 32, P1_SMEM, st>>>(a);
     ctx->stage_end("pass1", st);
     ++ctx->launches;
   }
@@ -1181,7 +1281,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   const uint32_t nl = htot[0], nkl = htot[1], nex = htot[2];
   const uint32_t n_amb_raw = htot[9], n_pend = htot[10];
   if (htot[13]) {
-    // not in timeline order (span.hpp:161-163); stage (b) sorting is not wired yet
+    // not in timeline order (span.hpp:161-163)
     (void)sort_if_needed;
     throw std::runtime_error("UNSORTED");
   }
@@ -1191,8 +1291,8 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     uint32_t* t_uns = ctx->d<uint32_t>("c.t_uns", T);
     XSP_CUDA(cudaMemsetAsync(t_uns, 0, T * 4ull, st));
     launch(ctx, k_layer_ids_sorted, nl, st, a.layer_row, c->span_id, a.t_layer_off, T, nl, t_uns);
-    launch(ctx, k_resolve_explicit, n_pend, st, a.pend_kl, a.pend_count, a.kl_row, a.kl_parent,
-           c->parent_id, c->span_id, a.layer_row, a.t_layer_off, a.t_kl_off, T, t_uns, orph);
+    launch(ctx, k_resolve_explicit, n_pend, st, a.pend_kl, a.pend_count, a.kl, c->parent_id, c->span_id,
+           a.layer_row, a.t_layer_off, a.t_kl_off, T, t_uns, orph);
   }
 
   // ---- rare containment cases: exact candidate count by scanning back
@@ -1200,8 +1300,8 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   if (n_amb_raw) {
     uint32_t* keep = ctx->d<uint32_t>("c.amb_keep", n_amb_raw + 1);
     uint32_t* pos = ctx->d<uint32_t>("c.amb_pos", n_amb_raw + 1);
-    launch(ctx, k_amb_resolve, n_amb_raw, st, n_amb_raw, a.amb_kl, a.amb_gx, a.kl_row, c->end_ns,
-           a.t_kl_off, a.t_layer_off, T, a.layer_end, a.kl_parent, keep);
+    launch(ctx, k_amb_resolve, n_amb_raw, st, n_amb_raw, a.amb_kl, a.amb_gx, a.kl, c->end_ns, a.t_kl_off,
+           a.t_layer_off, T, a.layer_row, keep);
     uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
     exclusive_scan<uint32_t, uint32_t>(keep, pos, n_amb_raw, scan_tmp, counters + 6, st, &ctx->launches);
     uint32_t* kl2 = ctx->d<uint32_t>("c.amb_kl2", n_amb_raw);
@@ -1210,7 +1310,6 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     n_amb = read_u32(ctx, counters + 6, st);
     a.amb_kl = kl2;
     a.amb_gx = gx2;
-    a.amb_count = counters + 6;
   }
 
   // ---- ambiguities, ordered by (trace, span_id)
@@ -1225,14 +1324,13 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     uint64_t* ktr = ctx->d<uint64_t>("c.amb_ktr", n_amb);
     uint64_t* ktr2 = ctx->d<uint64_t>("c.amb_ktr2", n_amb);
     uint32_t* idx = ctx->d<uint32_t>("c.amb_idx", n_amb);
-    launch(ctx, k_amb_keys, n_amb, st, a.amb_kl, a.amb_count, a.kl_row, c->span_id, a.t_kl_off, T, ksid,
-           ktr, idx);
+    launch(ctx, k_amb_keys, n_amb, st, a.amb_kl, n_amb, a.kl, c->span_id, a.t_kl_off, T, ksid, ktr, idx);
     radix_sort_pairs(ksid, idx, n_amb, 0, 64, rs, st, &ctx->launches);
     launch(ctx, k_gather_u64, n_amb, st, ktr, idx, ktr2, n_amb);
     radix_sort_pairs(ktr2, idx, n_amb, 0, 32, rs, st, &ctx->launches);
     uint32_t* cnt = ctx->d<uint32_t>("c.amb_cnt", n_amb + 1);
-    launch(ctx, k_amb_count, n_amb, st, idx, n_amb, a.amb_kl, a.amb_gx, a.kl_row, c->end_ns, a.t_kl_off,
-           a.t_layer_off, T, a.layer_end, cnt);
+    launch(ctx, k_amb_count, n_amb, st, idx, n_amb, a.amb_kl, a.amb_gx, a.kl, c->end_ns, a.t_kl_off,
+           a.t_layer_off, T, a.layer_row, cnt);
     uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
     uint32_t* tot = ctx->d<uint32_t>("c.amb_tot", 1);
     exclusive_scan<uint32_t, uint32_t>(cnt, out->amb_cand_off, n_amb, scan_tmp, tot, st, &ctx->launches);
@@ -1240,9 +1338,8 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     uint32_t ncand = read_u32(ctx, tot, st);
     out->n_candidates = ncand;
     out->amb_cand_row = ctx->d<uint32_t>("o.amb_cand_row", ncand);
-    launch(ctx, k_amb_fill, n_amb, st, idx, n_amb, a.amb_kl, a.amb_gx, a.kl_row, c->end_ns, c->span_id,
-           a.t_kl_off, a.t_layer_off, T, a.layer_end, a.layer_row, out->amb_cand_off, out->amb_row,
-           out->amb_cand_row);
+    launch(ctx, k_amb_fill, n_amb, st, idx, n_amb, a.amb_kl, a.amb_gx, a.kl, c->end_ns, c->span_id, a.t_kl_off,
+           a.t_layer_off, T, a.layer_row, out->amb_cand_off, out->amb_row, out->amb_cand_row);
     launch(ctx, k_csr_by_trace, (uint64_t)T + 1, st, T, n_amb, ktr2, 0, out->trace_amb_off);
   } else {
     out->amb_cand_row = ctx->d<uint32_t>("o.amb_cand_row", 1);
@@ -1250,98 +1347,112 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     XSP_CUDA(cudaMemsetAsync(out->amb_cand_off, 0, 4, st));
   }
 
-  // ---- cid join
+  // ---- cid join: merge-aligned check, hash table for the other traces
+  ctx->stage_begin("join", st);
   JoinArgs j;
-  j.ex_cid = a.ex_cid;
-  j.kl_cid = a.kl_cid;
-  j.kl_info = a.kl_info;
+  j.ex = a.ex;
+  j.kl = a.kl;
+  j.flags = c->flags;
   j.t_ex_off = a.t_ex_off;
   j.t_kl_off = a.t_kl_off;
+  uint32_t* t_slow = ctx->d<uint32_t>("c.t_slow", T + 1);
+  j.t_slow = t_slow;
   j.T = T;
   j.n_ex = nex;
   j.n_kl = nkl;
-  uint64_t* rsize = ctx->d<uint64_t>("c.rsize", T + 1);
-  uint64_t* roff = ctx->d<uint64_t>("c.roff", T + 1);
-  launch(ctx, k_region_size, T, st, a.t_kl_off, a.t_ex_off, T, rsize);
-  uint64_t* scan64 = ctx->d<uint64_t>("c.scan64", scan_scratch_elems(T + 1));
-  exclusive_scan<uint64_t, uint64_t>(rsize, roff, T, scan64, roff + T, st, &ctx->launches);
-  uint64_t* hroff = ctx->h<uint64_t>("c.roff_h", 1);
-  XSP_CUDA(cudaMemcpyAsync(hroff, roff + T, 8, cudaMemcpyDeviceToHost, st));
-  XSP_CUDA(cudaStreamSynchronize(st));
-  const uint64_t nslots = *hroff;
-  j.roff = roff;
-  j.owner = ctx->d<uint32_t>("c.owner", nslots);
-  j.sl_exec = ctx->d<uint32_t>("c.sl_exec", nslots);
-  j.sl_launch = ctx->d<uint32_t>("c.sl_launch", nslots);
-  j.ex_slot = ctx->d<uint32_t>("c.ex_slot", nex);
-  j.kl_slot = ctx->d<uint32_t>("c.kl_slot", nkl);
-  j.t_dup = ctx->d<uint32_t>("c.t_dup", T);
-  XSP_CUDA(cudaMemsetAsync(j.owner, 0, nslots * 4, st));
-  XSP_CUDA(cudaMemsetAsync(j.sl_exec, 0xFF, nslots * 4, st));
-  XSP_CUDA(cudaMemsetAsync(j.sl_launch, 0xFF, nslots * 4, st));
-  XSP_CUDA(cudaMemsetAsync(j.t_dup, 0, T * 4ull, st));
+  launch(ctx, k_join_counts, T, st, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
+  launch(ctx, k_join_check, nkl, st, nkl, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
+  const uint32_t any_slow = read_u32(ctx, counters + 7, st);
   auto* dup_ex = ctx->d<unsigned long long>("c.dup_ex", T);
   auto* dup_kl = ctx->d<unsigned long long>("c.dup_kl", T);
   XSP_CUDA(cudaMemsetAsync(dup_ex, 0xFF, T * 8ull, st));
   XSP_CUDA(cudaMemsetAsync(dup_kl, 0xFF, T * 8ull, st));
-  ctx->stage_begin("join", st);
-  launch(ctx, k_join_insert, (uint64_t)nex + nkl, st, j);
-  launch(ctx, k_join_dups, (uint64_t)nex + nkl, st, j, dup_ex, dup_kl);
+  j.ex_slot = ctx->d<uint32_t>("c.ex_slot", nex + 1);
+  j.kl_slot = ctx->d<uint32_t>("c.kl_slot", nkl + 1);
+  if (any_slow) {
+    uint64_t* rsize = ctx->d<uint64_t>("c.rsize", T + 1);
+    uint64_t* roff = ctx->d<uint64_t>("c.roff", T + 1);
+    launch(ctx, k_region_size, T, st, a.t_kl_off, a.t_ex_off, t_slow, T, rsize);
+    uint64_t* scan64 = ctx->d<uint64_t>("c.scan64", scan_scratch_elems(T + 1));
+    exclusive_scan<uint64_t, uint64_t>(rsize, roff, T, scan64, roff + T, st, &ctx->launches);
+    uint64_t* hroff = ctx->h<uint64_t>("c.roff_h", 1);
+    XSP_CUDA(cudaMemcpyAsync(hroff, roff + T, 8, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaStreamSynchronize(st));
+    const uint64_t nslots = *hroff;
+    j.roff = roff;
+    j.owner = ctx->d<uint32_t>("c.owner", nslots);
+    j.sl_exec = ctx->d<uint32_t>("c.sl_exec", nslots);
+    j.sl_launch = ctx->d<uint32_t>("c.sl_launch", nslots);
+    j.t_dup = ctx->d<uint32_t>("c.t_dup", T);
+    XSP_CUDA(cudaMemsetAsync(j.owner, 0, nslots * 4, st));
+    XSP_CUDA(cudaMemsetAsync(j.sl_exec, 0xFF, nslots * 4, st));
+    XSP_CUDA(cudaMemsetAsync(j.sl_launch, 0xFF, nslots * 4, st));
+    XSP_CUDA(cudaMemsetAsync(j.t_dup, 0, T * 4ull, st));
+    launch(ctx, k_join_insert, (uint64_t)nex + nkl, st, j);
+    launch(ctx, k_join_dups, (uint64_t)nex + nkl, st, j, dup_ex, dup_kl);
+  } else {
+    j.sl_exec = j.sl_launch = nullptr;
+  }
   ctx->stage_end("join", st);
 
   // ---- fusion, kept kernels, leftover execs
+  ctx->stage_begin("fuse", st);
   FuseArgs fa;
   fa.n_kl = nkl;
   fa.n_ex = nex;
   fa.T = T;
-  fa.kl_row = a.kl_row;
-  fa.kl_parent = a.kl_parent;
-  fa.kl_info = a.kl_info;
+  fa.kl = a.kl;
+  fa.ex = a.ex;
+  fa.flags = c->flags;
+  fa.t_slow = t_slow;
   fa.kl_slot = j.kl_slot;
   fa.sl_exec = j.sl_exec;
   fa.sl_launch = j.sl_launch;
   fa.ex_slot = j.ex_slot;
-  fa.ex_row = a.ex_row;
   fa.sid = c->span_id;
   fa.t_kl_off = a.t_kl_off;
   fa.t_ex_off = a.t_ex_off;
   fa.kept = ctx->d<uint32_t>("c.kept", nkl + 1);
   fa.kl_exec = ctx->d<uint32_t>("c.kl_exec", nkl + 1);
   fa.orph = orph;
-  ctx->stage_begin("fuse", st);
-  launch(ctx, k_fuse, nkl > nex ? nkl : nex, st, fa);
-  ctx->stage_end("fuse", st);
+  fa.any_slow = any_slow != 0;
+  launch(ctx, k_fuse, nkl, st, fa);
+  if (any_slow) launch(ctx, k_leftover, nex, st, fa);
 
   uint32_t* kpos = ctx->d<uint32_t>("c.kpos", nkl + 1);
   uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
   uint32_t* nk_d = ctx->d<uint32_t>("c.nk", 1);
   exclusive_scan<uint32_t, uint32_t>(fa.kept, kpos, nkl, scan_tmp, nk_d, st, &ctx->launches);
-  const uint32_t nk = read_u32(ctx, nk_d, st);
-  uint64_t* kkey = ctx->d<uint64_t>("c.kkey", nk + 1);
-  uint32_t* kval = ctx->d<uint32_t>("c.kval", nk + 1);
-  launch(ctx, k_compact_kernels, nkl, st, nkl, fa.kept, kpos, a.kl_parent, kkey, kval, counters + 3);
-  launch(ctx, k_check_mono, nk, st, nk, kkey, counters + 3);
-  if (read_u32(ctx, counters + 3, st)) {
+  uint64_t* kkey = ctx->d<uint64_t>("c.kkey", nkl + 1);
+  uint32_t* kval = ctx->d<uint32_t>("c.kval", nkl + 1);
+  launch(ctx, k_compact_kernels, nkl, st, nkl, fa.kept, kpos, a.kl, kkey, kval, counters + 3);
+  launch(ctx, k_check_mono, nkl, st, nk_d, kkey, counters + 3);
+  XSP_CUDA(cudaMemcpyAsync(htot, nk_d, 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(htot + 1, counters + 3, 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  const uint32_t nk = htot[0];
+  ctx->stage_end("fuse", st);
+  if (htot[1]) {
     // explicit parents broke the timeline order of layers: stable sort by layer
     RadixScratch rs = radix_scratch(ctx, nk);
     radix_sort_pairs(kkey, kval, nk, 0, 32, rs, st, &ctx->launches);
   }
+  ctx->stage_begin("gather", st);
   out->n_kernels = nk;
   out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", nk);
   out->kernel_exec_row = ctx->d<uint32_t>("o.k_exec", nk);
   out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", nk);
   out->kernel_dur = ctx->d<uint64_t>("o.k_dur", nk);
   out->kernel_name = ctx->d<uint32_t>("o.k_name", nk);
-  ctx->stage_begin("gather", st);
-  launch(ctx, k_gather_kernels, nk, st, nk, kval, a.kl_row, a.kl_info, a.kl_dur, a.kl_mrow, a.kl_name,
-         fa.kl_exec, a.ex_row, a.ex_dur, a.ex_mrow, a.ex_name, out->kernel_launch_row,
-         out->kernel_exec_row, out->kernel_metric_row, out->kernel_dur, out->kernel_name);
+  launch(ctx, k_gather_kernels, nk, st, nk, kval, a.kl, a.kl_mrow, fa.kl_exec, a.ex, c->flags, c->begin_ns,
+         c->end_ns, c->name_id, out->kernel_launch_row, out->kernel_exec_row, out->kernel_metric_row,
+         out->kernel_dur, out->kernel_name);
   out->n_layers = nl;
   out->layer_row = a.layer_row;
   out->layer_dur = a.layer_dur;
   out->layer_attr_row = a.layer_attr_row;
   out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", nl + 1);
-  launch(ctx, k_layer_kernel_off, (uint64_t)nl + 1, st, nl, nk, kkey, out->layer_kernel_off);
+  launch(ctx, k_layer_kernel_off, (uint64_t)nk + 1, st, nl, nk, kkey, out->layer_kernel_off);
   out->trace_layer_off = a.t_layer_off;
   out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
   launch(ctx, k_trace_kernel_off, (uint64_t)T + 1, st, T, a.t_layer_off, out->layer_kernel_off,
@@ -1375,7 +1486,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   out->trace_status = ctx->d<int32_t>("o.t_status", T);
   out->trace_err_row = ctx->d<uint32_t>("o.t_err_row", 2ull * T);
   out->trace_model_row = model_row;
-  launch(ctx, k_status, T, st, T, model_row, err_key, dup_ex, dup_kl, a.ex_row, a.kl_row, out->trace_status,
+  launch(ctx, k_status, T, st, T, model_row, err_key, dup_ex, dup_kl, a.ex, a.kl, out->trace_status,
          out->trace_err_row, counters + 4);
   out->n_failed = read_u32(ctx, counters + 4, st);
 }
