@@ -199,88 +199,105 @@ struct LayerArgs {
   uint32_t* l_topk;
 };
 
-__global__ void k_layers(LayerArgs a) {
-  uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= a.total_layers) return;
-  uint32_t lo = 0, hi = a.G;
+__device__ __forceinline__ uint32_t group_of(const uint32_t* __restrict__ off, uint32_t G, uint32_t q) {
+  uint32_t lo = 0, hi = G;  // off[lo] <= q < off[hi]
   while (hi - lo > 1) {
     uint32_t mid = (lo + hi) >> 1;
-    if (a.gl_off[mid] <= q) lo = mid; else hi = mid;
+    if (__ldg(off + mid) <= q) lo = mid; else hi = mid;
   }
-  const uint32_t g = lo, li = q - a.gl_off[g];
+  return lo;
+}
+
+// Per (group, kernel ordinal): combine() over repetitions (analysis.cpp:146-167)
+// and the a8 / a9 row (:342-397). One thread per kernel keeps R independent
+// gathers in flight.
+__global__ void k_kernels(LayerArgs a, uint32_t total_kernels) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= total_kernels) return;
+  const uint32_t g = group_of(a.gk_off, a.G, q);
   if (a.gstatus[g] != XSP_G_OK) return;
+  const uint32_t ord = q - a.gk_off[g];
   const uint32_t R = a.nr[g], t0 = a.ft[g];
   double v[kMaxRuns];
   double w[kMaxRuns];
-  // layer latency (combine, analysis.cpp:138-144)
+  for (uint32_t r = 0; r < R; ++r) {
+    const uint32_t jr = a.t_kernel_off[t0 + r] + ord;
+    v[r] = (double)a.kernel_dur[jr];
+    const uint32_t mr = a.kernel_mrow[jr];
+    w[r] = mr != kNone ? a.m_occ[mr] : 0.0;
+  }
+  const double klat = trimmed_mean_dev(v, R, a.trim);
+  const double kocc = trimmed_mean_dev(w, R, a.trim);
+  const uint32_t j = a.t_kernel_off[t0] + ord;
+  const uint32_t mr0 = a.kernel_mrow[j];
+  uint64_t f = 0, rd = 0, wr = 0;
+  if (mr0 != kNone) {  // counters from the first repetition (:162-166)
+    f = a.m_flops[mr0];
+    rd = a.m_read[mr0];
+    wr = a.m_write[mr0];
+  }
+  const Roof ro = roofline(f, rd, wr, klat, a.peak, a.bw);
+  a.k_name[q] = a.kernel_name[j];
+  a.k_lat[q] = klat;
+  a.k_flops[q] = f;
+  a.k_read[q] = rd;
+  a.k_write[q] = wr;
+  a.k_occ[q] = kocc;
+  a.k_ai[q] = ro.ai;
+  a.k_tput[q] = ro.tput;
+  a.k_bound[q] = ro.bound;
+  a.k_in[q] = (ro.bound >= 0 && klat > 0.0) ? 1 : 0;  // classify (analysis.cpp:59-71)
+}
+
+// Per (group, layer): combine() layer latency (:135-144), the Accumulator over
+// the layer's kernels in tree order (:173-211), a11-a14 rows and top-k.
+__global__ void k_layers(LayerArgs a) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= a.total_layers) return;
+  const uint32_t g = group_of(a.gl_off, a.G, q);
+  const uint32_t li = q - a.gl_off[g];
+  if (a.gstatus[g] != XSP_G_OK) return;
+  const uint32_t R = a.nr[g], t0 = a.ft[g];
+  double v[kMaxRuns];
   for (uint32_t r = 0; r < R; ++r) v[r] = (double)a.layer_dur[a.t_layer_off[t0 + r] + li];
   const double layer_lat = trimmed_mean_dev(v, R, a.trim);
 
   const uint32_t gl0 = a.t_layer_off[t0] + li;
-  const uint32_t kb = a.l_koff[gl0], ke = a.l_koff[gl0 + 1];
-  const uint32_t group_kbase = a.gk_off[g];
   const uint32_t trace_kbase = a.t_kernel_off[t0];
-  // Accumulator (analysis.cpp:173-193)
+  const uint32_t kb = a.gk_off[g] + (a.l_koff[gl0] - trace_kbase);
+  const uint32_t ke = a.gk_off[g] + (a.l_koff[gl0 + 1] - trace_kbase);
   double acc_lat = 0.0, acc_occw = 0.0;
-  uint64_t acc_f = 0, acc_r = 0, acc_w = 0, acc_n = 0;
+  uint64_t acc_f = 0, acc_r = 0, acc_w = 0;
   const uint32_t K = a.top_k;
   uint32_t top_idx[8];
   double top_lat[8];
   uint32_t ntop = 0;
-  for (uint32_t j = kb; j < ke; ++j) {
-    const uint32_t ord = j - trace_kbase;  // kernel ordinal within the run
-    for (uint32_t r = 0; r < R; ++r) {
-      uint32_t jr = a.t_kernel_off[t0 + r] + ord;
-      v[r] = (double)a.kernel_dur[jr];
-      uint32_t mr = a.kernel_mrow[jr];
-      w[r] = mr != kNone ? a.m_occ[mr] : 0.0;
-    }
-    const double klat = trimmed_mean_dev(v, R, a.trim);
-    const double kocc = trimmed_mean_dev(w, R, a.trim);
-    const uint32_t mr0 = a.kernel_mrow[j];
-    uint64_t f = 0, rd = 0, wr = 0;
-    if (mr0 != kNone) {
-      f = a.m_flops[mr0];
-      rd = a.m_read[mr0];
-      wr = a.m_write[mr0];
-    }
-    const uint32_t out = group_kbase + ord;
-    Roof ro = roofline(f, rd, wr, klat, a.peak, a.bw);
-    a.k_name[out] = a.kernel_name[j];
-    a.k_layer[out] = li;
-    a.k_lat[out] = klat;
-    a.k_flops[out] = f;
-    a.k_read[out] = rd;
-    a.k_write[out] = wr;
-    a.k_occ[out] = kocc;
-    a.k_ai[out] = ro.ai;
-    a.k_tput[out] = ro.tput;
-    a.k_bound[out] = ro.bound;
-    a.k_in[out] = (ro.bound >= 0 && klat > 0.0) ? 1 : 0;  // classify (analysis.cpp:59-71)
+  for (uint32_t x = kb; x < ke; ++x) {
+    const double klat = a.k_lat[x];
+    a.k_layer[x] = li;
     acc_lat = __dadd_rn(acc_lat, klat);
-    acc_f += f;
-    acc_r += rd;
-    acc_w += wr;
-    acc_occw = __dadd_rn(acc_occw, __dmul_rn(kocc, klat));
-    ++acc_n;
+    acc_f += a.k_flops[x];
+    acc_r += a.k_read[x];
+    acc_w += a.k_write[x];
+    acc_occw = __dadd_rn(acc_occw, __dmul_rn(a.k_occ[x], klat));
     // top-k by latency desc, ordinal asc
     if (K) {
       uint32_t pos = ntop;
       while (pos > 0 && top_lat[pos - 1] < klat) --pos;
       if (pos < K) {
-        uint32_t last = ntop < K ? ntop : K - 1;
+        const uint32_t last = ntop < K ? ntop : K - 1;
         for (uint32_t s = last; s > pos; --s) {
           top_lat[s] = top_lat[s - 1];
           top_idx[s] = top_idx[s - 1];
         }
         top_lat[pos] = klat;
-        top_idx[pos] = ord;
+        top_idx[pos] = x - a.gk_off[g];
         if (ntop < K) ++ntop;
       }
     }
   }
-  const uint32_t lo_out = a.gl_off[g] + li;
-  Roof ro = roofline(acc_f, acc_r, acc_w, acc_lat, a.peak, a.bw);
+  const uint32_t lo_out = q;
+  const Roof ro = roofline(acc_f, acc_r, acc_w, acc_lat, a.peak, a.bw);
   a.l_index[lo_out] = li;
   a.l_row[lo_out] = a.layer_row[gl0];
   a.l_layer_lat[lo_out] = layer_lat;
@@ -289,7 +306,7 @@ __global__ void k_layers(LayerArgs a) {
   a.l_read[lo_out] = acc_r;
   a.l_write[lo_out] = acc_w;
   a.l_occ[lo_out] = acc_lat > 0.0 ? acc_occw / acc_lat : 0.0;
-  a.l_count[lo_out] = acc_n;
+  a.l_count[lo_out] = ke - kb;
   a.l_ai[lo_out] = ro.ai;
   a.l_tput[lo_out] = ro.tput;
   a.l_bound[lo_out] = ro.bound;
@@ -300,8 +317,7 @@ __global__ void k_layers(LayerArgs a) {
   a.l_gpu_share[lo_out] = layer_lat > 0.0 ? acc_lat / layer_lat : 0.0;
   a.l_nongpu_share[lo_out] = layer_lat > 0.0 ? nongpu / layer_lat : 0.0;
   a.l_flagged[lo_out] = nongpu < -(__dmul_rn(a.noise, layer_lat)) ? 1 : 0;
-  for (uint32_t s = 0; s < K; ++s)
-    a.l_topk[(uint64_t)lo_out * K + s] = s < ntop ? top_idx[s] : kNone;
+  for (uint32_t s = 0; s < K; ++s) a.l_topk[(uint64_t)lo_out * K + s] = s < ntop ? top_idx[s] : kNone;
 }
 
 struct ModelArgs {
@@ -417,6 +433,167 @@ __global__ void k_models(ModelArgs a) {
 }
 
 // ---- a10 by name ------------------------------------------------------------
+//
+// Fast path: one warp per group with a shared-memory table keyed by name_id
+// (std::map<std::string, Accumulator> of analysis.cpp:402-407; ids are interned
+// in string order, so sorting by id is sorting by name). u64 counters use shared
+// atomics (order-free, exact); the two fp64 chains per name are applied by lane
+// 0 strictly in tree order. Groups with more than NCAP distinct names fall back
+// to the sort-based path below.
+
+constexpr int NCAP = 128;
+constexpr int NAME_WARPS = 4;
+constexpr uint32_t NEMPTY = 0xFFFFFFFFu;
+
+struct NameTable {
+  uint32_t key[NCAP];
+  double lat[NCAP], occw[NCAP];
+  unsigned long long f[NCAP], r[NCAP], w[NCAP], cnt[NCAP];
+  uint32_t used[NCAP];
+  uint32_t nused;
+};
+
+struct NameFastArgs {
+  uint32_t G;
+  const uint32_t* gk_off;
+  const int32_t* gstatus;
+  const uint32_t* k_name;
+  const double* k_lat;
+  const double* k_occ;
+  const uint64_t* k_flops;
+  const uint64_t* k_read;
+  const uint64_t* k_write;
+  const double* m_lat;
+  double peak, bw;
+  uint32_t* g_count;    // distinct names per group
+  uint32_t* overflow;   // any group exceeded NCAP
+  // rows per group in final order, staged at [g * NCAP, g * NCAP + count)
+  uint32_t* s_name;
+  uint64_t* s_count;
+  double* s_lat;
+  double* s_pct;
+  uint64_t* s_flops;
+  uint64_t* s_read;
+  uint64_t* s_write;
+  double* s_occ;
+  double* s_ai;
+  double* s_tput;
+  int8_t* s_bound;
+};
+
+__global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) {
+  __shared__ NameTable tab[NAME_WARPS];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t g = blockIdx.x * NAME_WARPS + warp;
+  if (g >= a.G) return;
+  NameTable& T = tab[warp];
+  for (uint32_t s = lane; s < NCAP; s += 32) {
+    T.key[s] = NEMPTY;
+    T.lat[s] = T.occw[s] = 0.0;
+    T.f[s] = T.r[s] = T.w[s] = T.cnt[s] = 0;
+  }
+  if (lane == 0) T.nused = 0;
+  __syncwarp();
+  if (a.gstatus[g] != XSP_G_OK) {
+    if (lane == 0) a.g_count[g] = 0;
+    return;
+  }
+  bool over = false;
+  const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
+  for (uint32_t base = k0; base < k1; base += 32) {
+    const uint32_t x = base + lane;
+    const bool v = x < k1;
+    uint32_t slot = 0;
+    double kl = 0.0, prod = 0.0;
+    if (v) {
+      const uint32_t nm = a.k_name[x];
+      kl = a.k_lat[x];
+      prod = __dmul_rn(a.k_occ[x], kl);
+      uint32_t h = (nm * 2654435761u) & (NCAP - 1);
+      uint32_t probes = 0;
+      for (;;) {
+        const uint32_t old = atomicCAS(&T.key[h], NEMPTY, nm);
+        if (old == NEMPTY) {
+          T.used[atomicAdd(&T.nused, 1u)] = h;
+          break;
+        }
+        if (old == nm) break;
+        h = (h + 1) & (NCAP - 1);
+        if (++probes >= NCAP) {
+          over = true;
+          break;
+        }
+      }
+      slot = h;
+      if (!over) {
+        atomicAdd(&T.f[slot], (unsigned long long)a.k_flops[x]);
+        atomicAdd(&T.r[slot], (unsigned long long)a.k_read[x]);
+        atomicAdd(&T.w[slot], (unsigned long long)a.k_write[x]);
+        atomicAdd(&T.cnt[slot], 1ull);
+      }
+    }
+    if (__any_sync(0xffffffffu, over)) break;
+    const uint32_t n = min(32u, k1 - base);
+    for (uint32_t s = 0; s < n; ++s) {  // Accumulator::add in tree order
+      const uint32_t sl = __shfl_sync(0xffffffffu, slot, s);
+      const double l = __shfl_sync(0xffffffffu, kl, s);
+      const double p = __shfl_sync(0xffffffffu, prod, s);
+      if (lane == 0) {
+        T.lat[sl] = __dadd_rn(T.lat[sl], l);
+        T.occw[sl] = __dadd_rn(T.occw[sl], p);
+      }
+    }
+    __syncwarp();
+  }
+  if (__any_sync(0xffffffffu, over)) {
+    if (lane == 0) {
+      a.g_count[g] = 0;
+      atomicOr(a.overflow, 1u);
+    }
+    return;
+  }
+  __syncwarp();
+  const uint32_t nu = T.nused;
+  const double mlat = a.m_lat[g];
+  // rank = position under (total latency desc, name asc) (analysis.cpp:424-430)
+  for (uint32_t u = lane; u < nu; u += 32) {
+    const uint32_t s = T.used[u];
+    const double l = T.lat[s];
+    const uint32_t nm = T.key[s];
+    uint32_t rank = 0;
+    for (uint32_t v2 = 0; v2 < nu; ++v2) {
+      const uint32_t s2 = T.used[v2];
+      const double l2 = T.lat[s2];
+      rank += (l2 > l) || (l2 == l && T.key[s2] < nm);
+    }
+    const uint64_t o = (uint64_t)g * NCAP + rank;
+    const Roof ro = roofline(T.f[s], T.r[s], T.w[s], l, a.peak, a.bw);
+    a.s_name[o] = nm;
+    a.s_count[o] = T.cnt[s];
+    a.s_lat[o] = l;
+    a.s_pct[o] = l / mlat * 100.0;
+    a.s_flops[o] = T.f[s];
+    a.s_read[o] = T.r[s];
+    a.s_write[o] = T.w[s];
+    a.s_occ[o] = l > 0.0 ? T.occw[s] / l : 0.0;
+    a.s_ai[o] = ro.ai;
+    a.s_tput[o] = ro.tput;
+    a.s_bound[o] = ro.bound;
+  }
+  if (lane == 0) a.g_count[g] = nu;
+}
+
+// staged rows [g * NCAP, + count) -> output [off[g], off[g+1])
+template <typename T>
+__global__ void k_names_place(uint32_t G, const uint32_t* __restrict__ off, const T* __restrict__ src,
+                              T* __restrict__ dst) {
+  const uint32_t g = blockIdx.x;
+  if (g >= G) return;
+  const uint32_t n = off[g + 1] - off[g];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[off[g] + i] = src[(uint64_t)g * NCAP + i];
+}
+
+// Sort-based fallback (any number of names per group).
 
 __global__ void k_name_keys(uint32_t total_k, const uint32_t* __restrict__ gk_off, uint32_t G,
                             const uint32_t* __restrict__ k_name, const int32_t* __restrict__ gstatus,
@@ -662,6 +839,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->l_roofline_in = la.l_in = ctx->d<uint8_t>("t.l_in", TL);
   out->l_topk = la.l_topk = ctx->d<uint32_t>("t.l_topk", (uint64_t)TL * (opts->top_k ? opts->top_k : 1));
   ctx->stage_begin("layers", st);
+  launch(ctx, k_kernels, TK, st, la, TK);
   launch(ctx, k_layers, TL, st, la);
   ctx->stage_end("layers", st);
 
@@ -707,7 +885,75 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   // ---- a10
   out->group_name_off = ctx->d<uint32_t>("t.g_noff", G + 1);
   uint32_t NN = 0;
-  if (TK) {
+  bool names_done = false;
+  if (TK && G) {
+    ctx->stage_begin("names", st);
+    NameFastArgs nf;
+    nf.G = G;
+    nf.gk_off = out->group_kernel_off;
+    nf.gstatus = out->group_status;
+    nf.k_name = la.k_name;
+    nf.k_lat = la.k_lat;
+    nf.k_occ = la.k_occ;
+    nf.k_flops = la.k_flops;
+    nf.k_read = la.k_read;
+    nf.k_write = la.k_write;
+    nf.m_lat = ma.m_lat;
+    nf.peak = la.peak;
+    nf.bw = la.bw;
+    nf.g_count = ctx->d<uint32_t>("a.ng_count", G + 1);
+    nf.overflow = ctx->d<uint32_t>("a.n_over", 1);
+    const uint64_t cap = (uint64_t)G * NCAP;
+    nf.s_name = ctx->d<uint32_t>("a.s_name", cap);
+    nf.s_count = ctx->d<uint64_t>("a.s_count", cap);
+    nf.s_lat = ctx->d<double>("a.s_lat", cap);
+    nf.s_pct = ctx->d<double>("a.s_pct", cap);
+    nf.s_flops = ctx->d<uint64_t>("a.s_flops", cap);
+    nf.s_read = ctx->d<uint64_t>("a.s_read", cap);
+    nf.s_write = ctx->d<uint64_t>("a.s_write", cap);
+    nf.s_occ = ctx->d<double>("a.s_occ", cap);
+    nf.s_ai = ctx->d<double>("a.s_ai", cap);
+    nf.s_tput = ctx->d<double>("a.s_tput", cap);
+    nf.s_bound = ctx->d<int8_t>("a.s_bound", cap);
+    XSP_CUDA(cudaMemsetAsync(nf.overflow, 0, 4, st));
+    k_names_fast<<<ceil_div(G, NAME_WARPS), NAME_WARPS * 32, 0, st>>>(nf);
+    ++ctx->launches;
+    exclusive_scan<uint32_t, uint32_t>(nf.g_count, out->group_name_off, G, scan_tmp, out->group_name_off + G, st,
+                                       &ctx->launches);
+    XSP_CUDA(cudaMemcpyAsync(htot + 2, out->group_name_off + G, 4, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaMemcpyAsync(htot + 3, nf.overflow, 4, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaStreamSynchronize(st));
+    if (!htot[3]) {
+      NN = htot[2];
+      out->n_name = ctx->d<uint32_t>("t.n_name", NN);
+      out->n_count = ctx->d<uint64_t>("t.n_count", NN);
+      out->n_lat = ctx->d<double>("t.n_lat", NN);
+      out->n_pct = ctx->d<double>("t.n_pct", NN);
+      out->n_flops = ctx->d<uint64_t>("t.n_flops", NN);
+      out->n_read = ctx->d<uint64_t>("t.n_read", NN);
+      out->n_write = ctx->d<uint64_t>("t.n_write", NN);
+      out->n_occ = ctx->d<double>("t.n_occ", NN);
+      out->n_ai = ctx->d<double>("t.n_ai", NN);
+      out->n_tput = ctx->d<double>("t.n_tput", NN);
+      out->n_bound = ctx->d<int8_t>("t.n_bound", NN);
+      const uint32_t* o = out->group_name_off;
+      k_names_place<uint32_t><<<G, 128, 0, st>>>(G, o, nf.s_name, out->n_name);
+      k_names_place<uint64_t><<<G, 128, 0, st>>>(G, o, nf.s_count, out->n_count);
+      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_lat, out->n_lat);
+      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_pct, out->n_pct);
+      k_names_place<uint64_t><<<G, 128, 0, st>>>(G, o, nf.s_flops, out->n_flops);
+      k_names_place<uint64_t><<<G, 128, 0, st>>>(G, o, nf.s_read, out->n_read);
+      k_names_place<uint64_t><<<G, 128, 0, st>>>(G, o, nf.s_write, out->n_write);
+      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_occ, out->n_occ);
+      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_ai, out->n_ai);
+      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_tput, out->n_tput);
+      k_names_place<int8_t><<<G, 128, 0, st>>>(G, o, nf.s_bound, out->n_bound);
+      ctx->launches += 11;
+      names_done = true;
+    }
+    ctx->stage_end("names", st);
+  }
+  if (TK && !names_done) {
     ctx->stage_begin("names", st);
     uint64_t* key = ctx->d<uint64_t>("a.nkey", TK);
     uint32_t* val = ctx->d<uint32_t>("a.nval", TK);
@@ -782,7 +1028,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     launch(ctx, k_permute<double>, NN, st, NN, order, na.s_tput, out->n_tput);
     launch(ctx, k_permute<int8_t>, NN, st, NN, order, na.s_bound, out->n_bound);
     ctx->stage_end("names", st);
-  } else {
+  } else if (!names_done) {
     XSP_CUDA(cudaMemsetAsync(out->group_name_off, 0, (G + 1) * 4ull, st));
     out->n_name = ctx->d<uint32_t>("t.n_name", 1);
     out->n_count = ctx->d<uint64_t>("t.n_count", 1);
