@@ -156,6 +156,7 @@ typedef struct xsp_corr_out {
   uint32_t* kernel_metric_row; /* metric-table row of the exec, UINT32_MAX if none */
   uint64_t* kernel_dur;        /* KernelExec::duration_ns (exec span) */
   uint32_t* kernel_name;       /* KernelExec::kernel_name() name_id */
+  double* kernel_occ;          /* metrics->achieved_occupancy, 0 without metrics */
   /* diagnostics, in the reference's output order */
   uint32_t* orphan_row;
   uint8_t* orphan_reason; /* xsp_orphan_reason */

@@ -66,6 +66,7 @@ CORR_FIELDS = [
     ("layer_attr_row", u32p, "L"),
     ("kernel_launch_row", u32p, "K"), ("kernel_exec_row", u32p, "K"),
     ("kernel_metric_row", u32p, "K"), ("kernel_dur", u64p, "K"), ("kernel_name", u32p, "K"),
+    ("kernel_occ", f64p, "K"),
     ("orphan_row", u32p, "O"), ("orphan_reason", u8p, "O"),
     ("amb_row", u32p, "A"), ("amb_cand_off", u32p, "A1"), ("amb_cand_row", u32p, "AC"),
 ]

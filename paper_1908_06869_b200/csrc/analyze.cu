@@ -161,6 +161,7 @@ struct LayerArgs {
   const uint64_t* kernel_dur;
   const uint32_t* kernel_mrow;
   const uint32_t* kernel_name;
+  const double* kernel_occ;
   const uint64_t* m_flops;
   const uint64_t* m_read;
   const uint64_t* m_write;
@@ -223,8 +224,7 @@ __global__ void k_kernels(LayerArgs a, uint32_t total_kernels) {
   for (uint32_t r = 0; r < R; ++r) {
     const uint32_t jr = a.t_kernel_off[t0 + r] + ord;
     v[r] = (double)a.kernel_dur[jr];
-    const uint32_t mr = a.kernel_mrow[jr];
-    w[r] = mr != kNone ? a.m_occ[mr] : 0.0;
+    w[r] = a.kernel_occ[jr];
   }
   const double klat = trimmed_mean_dev(v, R, a.trim);
   const double kocc = trimmed_mean_dev(w, R, a.trim);
@@ -450,6 +450,7 @@ struct NameTable {
   double lat[NCAP], occw[NCAP];
   unsigned long long f[NCAP], r[NCAP], w[NCAP], cnt[NCAP];
   uint32_t used[NCAP];
+  uint32_t start[NCAP];
   uint32_t nused;
 };
 
@@ -467,6 +468,9 @@ struct NameFastArgs {
   double peak, bw;
   uint32_t* g_count;    // distinct names per group
   uint32_t* overflow;   // any group exceeded NCAP
+  uint32_t* ks_slot;    // [TK] scratch: name slot of each kernel
+  uint32_t* ks_rank;    // [TK] scratch: rank of the kernel within its name
+  uint32_t* perm;       // [TK] scratch: kernels grouped by name, tree order within
   // rows per group in final order, staged at [g * NCAP, g * NCAP + count)
   uint32_t* s_name;
   uint64_t* s_count;
@@ -500,15 +504,14 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
   }
   bool over = false;
   const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
+  const uint32_t lt = lanemask_lt();
+  // pass A: slot per kernel, u64 counters, stable rank of the kernel within its name
   for (uint32_t base = k0; base < k1; base += 32) {
     const uint32_t x = base + lane;
     const bool v = x < k1;
-    uint32_t slot = 0;
-    double kl = 0.0, prod = 0.0;
+    uint32_t slot = NCAP + lane;  // distinct dummy for idle lanes
     if (v) {
       const uint32_t nm = a.k_name[x];
-      kl = a.k_lat[x];
-      prod = __dmul_rn(a.k_occ[x], kl);
       uint32_t h = (nm * 2654435761u) & (NCAP - 1);
       uint32_t probes = 0;
       for (;;) {
@@ -524,24 +527,22 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
           break;
         }
       }
-      slot = h;
       if (!over) {
+        slot = h;
         atomicAdd(&T.f[slot], (unsigned long long)a.k_flops[x]);
         atomicAdd(&T.r[slot], (unsigned long long)a.k_read[x]);
         atomicAdd(&T.w[slot], (unsigned long long)a.k_write[x]);
-        atomicAdd(&T.cnt[slot], 1ull);
       }
     }
     if (__any_sync(0xffffffffu, over)) break;
-    const uint32_t n = min(32u, k1 - base);
-    for (uint32_t s = 0; s < n; ++s) {  // Accumulator::add in tree order
-      const uint32_t sl = __shfl_sync(0xffffffffu, slot, s);
-      const double l = __shfl_sync(0xffffffffu, kl, s);
-      const double p = __shfl_sync(0xffffffffu, prod, s);
-      if (lane == 0) {
-        T.lat[sl] = __dadd_rn(T.lat[sl], l);
-        T.occw[sl] = __dadd_rn(T.occw[sl], p);
-      }
+    const uint32_t peers = __match_any_sync(0xffffffffu, slot);
+    unsigned long long rank = 0;
+    if (v) rank = T.cnt[slot];
+    __syncwarp();
+    if (v && (peers & lt) == 0) T.cnt[slot] = rank + __popc(peers);
+    if (v) {
+      a.ks_slot[x] = slot;
+      a.ks_rank[x] = (uint32_t)(rank + __popc(peers & lt));
     }
     __syncwarp();
   }
@@ -554,6 +555,47 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
   }
   __syncwarp();
   const uint32_t nu = T.nused;
+  // pass B: start of each name's run = exclusive prefix of counts over slots
+  {
+    unsigned long long c4[NCAP / 32], s = 0;
+#pragma unroll
+    for (int q = 0; q < NCAP / 32; ++q) {
+      c4[q] = T.cnt[lane * (NCAP / 32) + q];
+      s += c4[q];
+    }
+    unsigned long long incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    unsigned long long run = incl - s;
+#pragma unroll
+    for (int q = 0; q < NCAP / 32; ++q) {
+      T.start[lane * (NCAP / 32) + q] = (uint32_t)run;
+      run += c4[q];
+    }
+  }
+  __syncwarp();
+  // pass C: stable scatter of kernel ordinals by name
+  for (uint32_t x = k0 + lane; x < k1; x += 32) a.perm[k0 + T.start[a.ks_slot[x]] + a.ks_rank[x]] = x;
+  __syncwarp();
+  // pass D: one lane per name walks that name's kernels in tree order
+  // (Accumulator::add, analysis.cpp:181-188)
+  for (uint32_t u = lane; u < nu; u += 32) {
+    const uint32_t s = T.used[u];
+    const uint32_t b = k0 + T.start[s], n = (uint32_t)T.cnt[s];
+    double lat = 0.0, occw = 0.0;
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t x = a.perm[b + i];
+      const double l = a.k_lat[x];
+      lat = __dadd_rn(lat, l);
+      occw = __dadd_rn(occw, __dmul_rn(a.k_occ[x], l));
+    }
+    T.lat[s] = lat;
+    T.occw[s] = occw;
+  }
+  __syncwarp();
   const double mlat = a.m_lat[g];
   // rank = position under (total latency desc, name asc) (analysis.cpp:424-430)
   for (uint32_t u = lane; u < nu; u += 32) {
@@ -799,6 +841,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   la.kernel_dur = corr->kernel_dur;
   la.kernel_mrow = corr->kernel_metric_row;
   la.kernel_name = corr->kernel_name;
+  la.kernel_occ = corr->kernel_occ;
   la.m_flops = c->flops;
   la.m_read = c->dram_read;
   la.m_write = c->dram_write;
@@ -903,6 +946,9 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     nf.bw = la.bw;
     nf.g_count = ctx->d<uint32_t>("a.ng_count", G + 1);
     nf.overflow = ctx->d<uint32_t>("a.n_over", 1);
+    nf.ks_slot = ctx->d<uint32_t>("a.ks_slot", TK);
+    nf.ks_rank = ctx->d<uint32_t>("a.ks_rank", TK);
+    nf.perm = ctx->d<uint32_t>("a.perm", TK);
     const uint64_t cap = (uint64_t)G * NCAP;
     nf.s_name = ctx->d<uint32_t>("a.s_name", cap);
     nf.s_count = ctx->d<uint64_t>("a.s_count", cap);

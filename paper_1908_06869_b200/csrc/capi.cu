@@ -230,6 +230,7 @@ XSP_API xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp
     c.kernel_metric_row = to_host(ctx, "k_mrow", dcorr.kernel_metric_row, dcorr.n_kernels, st);
     c.kernel_dur = to_host(ctx, "k_dur", dcorr.kernel_dur, dcorr.n_kernels, st);
     c.kernel_name = to_host(ctx, "k_name", dcorr.kernel_name, dcorr.n_kernels, st);
+    c.kernel_occ = to_host(ctx, "k_occ", dcorr.kernel_occ, dcorr.n_kernels, st);
     c.orphan_row = to_host(ctx, "o_row", dcorr.orphan_row, dcorr.n_orphans, st);
     c.orphan_reason = to_host(ctx, "o_reason", dcorr.orphan_reason, dcorr.n_orphans, st);
     c.amb_row = to_host(ctx, "a_row", dcorr.amb_row, dcorr.n_ambiguities, st);

@@ -1048,9 +1048,10 @@ __global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val, 
                                  const uint32_t* __restrict__ kl_mrow, const uint32_t* __restrict__ kl_exec,
                                  const ExEnt* __restrict__ ex, const uint8_t* __restrict__ flags,
                                  const uint64_t* __restrict__ begin, const uint64_t* __restrict__ end,
-                                 const uint32_t* __restrict__ name, uint32_t* __restrict__ k_launch,
-                                 uint32_t* __restrict__ k_exec, uint32_t* __restrict__ k_mrow,
-                                 uint64_t* __restrict__ k_dur, uint32_t* __restrict__ k_name) {
+                                 const uint32_t* __restrict__ name, const double* __restrict__ occ,
+                                 uint32_t* __restrict__ k_launch, uint32_t* __restrict__ k_exec,
+                                 uint32_t* __restrict__ k_mrow, uint64_t* __restrict__ k_dur,
+                                 uint32_t* __restrict__ k_name, double* __restrict__ k_occ) {
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nk) return;
   const uint32_t k = val[j];
@@ -1070,36 +1071,61 @@ __global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val, 
   k_mrow[j] = mr;
   k_dur[j] = clamp_dur(begin[er], end[er]);
   k_name[j] = name[er];
+  k_occ[j] = mr != kNone ? occ[mr] : 0.0;
 }
 
-// Clean batches (no orphan, ambiguity or explicit parent, every trace
-// merge-aligned): every kernel-list entry is kept, in tree order, and entry r
-// of trace t fuses with exec r of trace t.
-__global__ void k_gather_fast(uint32_t nk, const KlEnt* __restrict__ kl, const ExEnt* __restrict__ ex,
+// Clean batches (no orphan, ambiguity or explicit parent): optimistic fusion.
+// Every kernel-list entry is kept in tree order and entry r of trace t fuses
+// with exec r of trace t, PROVIDED the trace is merge-aligned (same count of
+// launches and execs, every entry a launch with a cid, equal cids at equal
+// rank, strictly increasing). The same pass verifies that; any failure sets
+// *fail and the caller reruns the general join.
+__global__ void k_gather_fast(uint32_t nk, uint32_t nex, const KlEnt* __restrict__ kl,
+                              const ExEnt* __restrict__ ex, const uint8_t* __restrict__ flags,
                               const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
                               uint32_t T, const uint64_t* __restrict__ begin, const uint64_t* __restrict__ end,
-                              const uint32_t* __restrict__ name, uint32_t* __restrict__ k_launch,
-                              uint32_t* __restrict__ k_exec, uint32_t* __restrict__ k_mrow,
-                              uint64_t* __restrict__ k_dur, uint32_t* __restrict__ k_name,
-                              uint32_t* __restrict__ l_koff, uint32_t nl) {
+                              const uint32_t* __restrict__ name, const double* __restrict__ occ,
+                              uint32_t* __restrict__ k_launch, uint32_t* __restrict__ k_exec,
+                              uint32_t* __restrict__ k_mrow, uint64_t* __restrict__ k_dur,
+                              uint32_t* __restrict__ k_name, double* __restrict__ k_occ,
+                              uint32_t* __restrict__ l_koff, uint32_t nl, uint32_t* __restrict__ fail) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t first = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
   if (first > nk) return;
+  uint32_t t = 0;
+  if (nk) t = warp_trace_of(t_kl_off, T, j < nk ? j : nk - 1, first < nk ? first : nk - 1);
   if (j > nk) return;
   // layer CSR boundaries (keys = parents, non-decreasing)
   const int64_t prev = j > 0 ? (int64_t)kl[j - 1].parent : -1;
   const int64_t cur = j < nk ? (int64_t)kl[j].parent : (int64_t)nl;
   for (int64_t g = prev + 1; g <= cur; ++g) l_koff[g] = j;
-  if (j == nk) return;
-  uint32_t t = 0;
-  t = trace_of32(t_kl_off, T, j);
+  if (j == nk) {
+    if (nex != nk) *fail = 1;  // some trace has execs but no launches
+    return;
+  }
   const KlEnt ent = kl[j];
-  const ExEnt e = ex[t_ex_off[t] + (j - t_kl_off[t])];
+  const uint32_t kb = t_kl_off[t], xb = t_ex_off[t];
+  const uint32_t r = j - kb;
+  const uint8_t f = flags[ent.row];
+  bool ok = (t_kl_off[t + 1] - kb) == (t_ex_off[t + 1] - xb) && f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID);
+  ExEnt e;
+  e.row = ent.row;
+  e.mrow = kNone;
+  e.cid = 0;
+  if (ok) {
+    e = ex[xb + r];
+    ok = e.cid == ent.cid && (r == 0 || kl[j - 1].cid < ent.cid);
+  }
+  if (!ok) {
+    *fail = 1;
+    return;
+  }
   k_launch[j] = ent.row;
   k_exec[j] = e.row;
   k_mrow[j] = e.mrow;
   k_dur[j] = clamp_dur(begin[e.row], end[e.row]);
   k_name[j] = name[e.row];
+  k_occ[j] = e.mrow != kNone ? occ[e.mrow] : 0.0;
 }
 
 // layer_kernel_off[g] = first kernel j whose parent >= g (keys sorted): each
@@ -1377,6 +1403,53 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     XSP_CUDA(cudaMemsetAsync(out->amb_cand_off, 0, 4, st));
   }
 
+  // ---- clean batch: optimistic merge-aligned fusion (general path on failure)
+  if (htot[8] == 0 && n_pend == 0 && n_amb_raw == 0) {
+    ctx->stage_begin("gather", st);
+    out->n_kernels = nkl;
+    out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", nkl);
+    out->kernel_exec_row = ctx->d<uint32_t>("o.k_exec", nkl);
+    out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", nkl);
+    out->kernel_dur = ctx->d<uint64_t>("o.k_dur", nkl);
+    out->kernel_name = ctx->d<uint32_t>("o.k_name", nkl);
+    out->kernel_occ = ctx->d<double>("o.k_occ", nkl);
+    out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", nl + 1);
+    uint32_t* fail = counters + 7;
+    launch(ctx, k_gather_fast, (uint64_t)nkl + 1, st, nkl, nex, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T,
+           c->begin_ns, c->end_ns, c->name_id, c->occupancy, out->kernel_launch_row, out->kernel_exec_row,
+           out->kernel_metric_row, out->kernel_dur, out->kernel_name, out->kernel_occ, out->layer_kernel_off, nl,
+           fail);
+    out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
+    launch(ctx, k_trace_kernel_off, (uint64_t)T + 1, st, T, a.t_layer_off, out->layer_kernel_off,
+           out->trace_kernel_off);
+    out->n_traces = T;
+    out->trace_status = ctx->d<int32_t>("o.t_status", T);
+    out->trace_err_row = ctx->d<uint32_t>("o.t_err_row", 2ull * T);
+    out->trace_model_row = model_row;
+    auto* no_dup = ctx->d<unsigned long long>("c.no_dup", T);
+    XSP_CUDA(cudaMemsetAsync(no_dup, 0xFF, T * 8ull, st));
+    launch(ctx, k_status, T, st, T, model_row, err_key, no_dup, no_dup, a.ex, a.kl, out->trace_status,
+           out->trace_err_row, counters + 4);
+    XSP_CUDA(cudaMemcpyAsync(htot, counters + 4, 16, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaStreamSynchronize(st));
+    ctx->stage_end("gather", st);
+    if (!htot[3]) {
+      out->n_failed = htot[0];
+      out->n_layers = nl;
+      out->layer_row = a.layer_row;
+      out->layer_dur = a.layer_dur;
+      out->layer_attr_row = a.layer_attr_row;
+      out->trace_layer_off = a.t_layer_off;
+      out->n_orphans = 0;
+      out->orphan_row = ctx->d<uint32_t>("o.orphan_row", 1);
+      out->orphan_reason = ctx->d<uint8_t>("o.orphan_reason", 1);
+      out->trace_orphan_off = ctx->d<uint32_t>("o.t_orph_off", T + 1);
+      XSP_CUDA(cudaMemsetAsync(out->trace_orphan_off, 0, (T + 1) * 4ull, st));
+      return;
+    }
+    XSP_CUDA(cudaMemsetAsync(counters + 4, 0, 4 * 4, st));  // retry: reset n_failed, flags
+  }
+
   // ---- cid join: merge-aligned check, hash table for the other traces
   ctx->stage_begin("join", st);
   JoinArgs j;
@@ -1424,44 +1497,6 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     j.sl_exec = j.sl_launch = nullptr;
   }
   ctx->stage_end("join", st);
-
-  const uint32_t n_orph_p1 = read_u32(ctx, orph.count, st);
-  if (!any_slow && n_orph_p1 == 0 && n_pend == 0 && n_amb_raw == 0) {
-    // clean batch: identity tree order, rank-aligned fusion
-    ctx->stage_begin("gather", st);
-    out->n_kernels = nkl;
-    out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", nkl);
-    out->kernel_exec_row = ctx->d<uint32_t>("o.k_exec", nkl);
-    out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", nkl);
-    out->kernel_dur = ctx->d<uint64_t>("o.k_dur", nkl);
-    out->kernel_name = ctx->d<uint32_t>("o.k_name", nkl);
-    out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", nl + 1);
-    launch(ctx, k_gather_fast, (uint64_t)nkl + 1, st, nkl, a.kl, a.ex, a.t_kl_off, a.t_ex_off, T, c->begin_ns,
-           c->end_ns, c->name_id, out->kernel_launch_row, out->kernel_exec_row, out->kernel_metric_row,
-           out->kernel_dur, out->kernel_name, out->layer_kernel_off, nl);
-    out->n_layers = nl;
-    out->layer_row = a.layer_row;
-    out->layer_dur = a.layer_dur;
-    out->layer_attr_row = a.layer_attr_row;
-    out->trace_layer_off = a.t_layer_off;
-    out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
-    launch(ctx, k_trace_kernel_off, (uint64_t)T + 1, st, T, a.t_layer_off, out->layer_kernel_off,
-           out->trace_kernel_off);
-    ctx->stage_end("gather", st);
-    out->n_orphans = 0;
-    out->orphan_row = ctx->d<uint32_t>("o.orphan_row", 1);
-    out->orphan_reason = ctx->d<uint8_t>("o.orphan_reason", 1);
-    out->trace_orphan_off = ctx->d<uint32_t>("o.t_orph_off", T + 1);
-    XSP_CUDA(cudaMemsetAsync(out->trace_orphan_off, 0, (T + 1) * 4ull, st));
-    out->n_traces = T;
-    out->trace_status = ctx->d<int32_t>("o.t_status", T);
-    out->trace_err_row = ctx->d<uint32_t>("o.t_err_row", 2ull * T);
-    out->trace_model_row = model_row;
-    launch(ctx, k_status, T, st, T, model_row, err_key, dup_ex, dup_kl, a.ex, a.kl, out->trace_status,
-           out->trace_err_row, counters + 4);
-    out->n_failed = read_u32(ctx, counters + 4, st);
-    return;
-  }
 
   // ---- fusion, kept kernels, leftover execs
   ctx->stage_begin("fuse", st);
@@ -1512,9 +1547,10 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", nk);
   out->kernel_dur = ctx->d<uint64_t>("o.k_dur", nk);
   out->kernel_name = ctx->d<uint32_t>("o.k_name", nk);
+  out->kernel_occ = ctx->d<double>("o.k_occ", nk);
   launch(ctx, k_gather_kernels, nk, st, nk, kval, a.kl, a.kl_mrow, fa.kl_exec, a.ex, c->flags, c->begin_ns,
-         c->end_ns, c->name_id, out->kernel_launch_row, out->kernel_exec_row, out->kernel_metric_row,
-         out->kernel_dur, out->kernel_name);
+         c->end_ns, c->name_id, c->occupancy, out->kernel_launch_row, out->kernel_exec_row,
+         out->kernel_metric_row, out->kernel_dur, out->kernel_name, out->kernel_occ);
   out->n_layers = nl;
   out->layer_row = a.layer_row;
   out->layer_dur = a.layer_dur;
