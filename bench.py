@@ -92,10 +92,12 @@ class ClockSampler:
 
 
 def pass1_bytes(b) -> int:
-    """Algorithmic bytes of one k_pass1 launch: every span's flags,
-    begin, end; parent_id of spans with one; cid of spans with one; name_id of
-    kernel/exec spans; writes: 24 B per placed layer, 17 B per kernel-list entry
-    (+16 B for synchronous kernels), 28 B per execution record, 12 B per trace."""
+    """Algorithmic bytes of one k_pass1 launch: reads every span's
+    flags (1 B), begin and end (16 B), the parent_id of spans that carry one and
+    the cid of spans that carry one (8 B each); writes 16 B per placed layer
+    (row, duration, attribute row), a 16 B entry per kernel launch / synchronous
+    kernel (+4 B metric row for the latter), a 16 B entry per execution record
+    with a cid, and 12 B of offsets per trace."""
     f = b.flags
     lvl, kind = f & 3, (f >> 2) & 3
     n = b.n_spans
@@ -104,10 +106,22 @@ def pass1_bytes(b) -> int:
     layer = int(((lvl == 1) & (kind == 0)).sum())
     launch = int(((kind == 1) & (lvl >= 2)).sum())
     synck = int(((kind == 0) & (lvl == 2)).sum())
-    exe = int((kind == 2).sum())
-    reads = n * 17 + has_p * 8 + has_c * 8 + (launch + synck + exe) * 4
-    writes = layer * 24 + (launch + synck) * 17 + synck * 16 + exe * 28 + b.n_traces * 12
+    exe = int(((kind == 2) & ((f & 0x20) != 0)).sum())
+    reads = n * 17 + has_p * 8 + has_c * 8
+    writes = layer * 16 + (launch + synck) * 16 + synck * 4 + exe * 16 + b.n_traces * 12
     return reads + writes
+
+
+def measured_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed
+    ncu --set full capture summary (profiles/traffic.json), per launch, or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)[kernel]
+        return {"bytes": d["dram_bytes"], "capture": d["capture"], "workload": d["workload"]}
+    except Exception:
+        return None
 
 
 def survey_bytes(b) -> float:
@@ -280,7 +294,7 @@ def main():
     achieved = p1_bytes / (p1_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": "k_pass1 (parent join + list compaction, 1 launch/step)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_kind": peak_kind, "traffic": None, "bytes_per_launch": p1_bytes,
+                "peak_kind": peak_kind, "traffic": measured_traffic("k_pass1"), "bytes_per_launch": p1_bytes,
                 "ms_per_launch": p1_ms}
     sv = survey_bytes(b)
     pipe_gbs = sv * world / (ms / 1e3) / 1e9

@@ -233,6 +233,51 @@ typedef struct xsp_tables_out {
   uint8_t* m_roofline_in;
 } xsp_tables_out;
 
+/* ---- leveled measurement (stage f) ----------------------------------------- */
+
+/* Level sets of one LeveledRunGroup (leveled.hpp:60-71): set s holds the
+ * correlated traces trace_idx[set_off[s] .. set_off[s+1]) of an xsp_corr_out
+ * (its repetitions, in order), captured at profiling levels `levels[s]` (bit
+ * mask). HOST arrays. */
+typedef struct xsp_level_sets {
+  uint32_t n_sets;
+  const uint32_t* set_off;   /* [n_sets + 1] */
+  const uint32_t* trace_idx; /* [set_off[n_sets]] */
+  const uint32_t* levels;    /* [n_sets] */
+} xsp_level_sets;
+
+enum {
+  XSP_L_OK = 0,
+  XSP_L_TOO_FEW = 1,      /* "overhead needs at least two chained level sets; got N" (leveled.cpp:148-151) */
+  XSP_L_NOT_CHAIN = 2,    /* "profiling-level sets A and B do not form an inclusion chain" (:131-138); err_a/err_b = set indices */
+  XSP_L_AMBIGUOUS = 3,    /* a trace has ambiguities (LeveledRunGroup::add, :69-75); err_a = trace */
+  XSP_L_TRACE_FAILED = 4  /* a trace's correlation failed; err_a = trace */
+};
+
+/* Event flags per chain step (leveled.cpp:182-213). */
+#define XSP_EV_IN_NARROW 0x01u   /* event visible in the narrower set of the step */
+#define XSP_EV_IN_WIDE 0x02u     /* event visible in the wider set of the step */
+#define XSP_EV_CLAMPED 0x04u     /* small negative overhead clamped to 0 */
+#define XSP_EV_NEGATIVE 0x08u    /* negative beyond noise tolerance (kept, warning) */
+
+/* compute_overhead (leveled.cpp:145-231) as columns. Events are the union of
+ * the sets' LeveledEventKeys sorted by (rank(level), layer_index, kernel_index);
+ * sets are in chain order (ascending size). DEVICE pointers owned by the ctx. */
+typedef struct xsp_overhead_out {
+  int32_t status;
+  uint32_t err_a, err_b;
+  uint32_t n_sets;        /* chain length */
+  uint32_t n_events;
+  const uint32_t* chain;  /* HOST: chain position -> input set index */
+  uint8_t* ev_level;      /* Level (Model 0, Layer 1, Kernel 2) */
+  uint32_t* ev_layer;
+  uint32_t* ev_kernel;
+  double* lat;            /* [n_sets * n_events] trimmed-mean latency per set, NaN if absent */
+  double* overhead;       /* [(n_sets-1) * n_events] wide - narrow (after clamping), NaN if absent */
+  uint8_t* step_flags;    /* [(n_sets-1) * n_events] XSP_EV_* */
+  double* accurate;       /* [n_events] accurate_latency_ns, NaN if no set qualifies */
+} xsp_overhead_out;
+
 /* ---- API ------------------------------------------------------------------ */
 
 xsp_status xsp_ctx_create(int device, xsp_ctx** out);
@@ -255,6 +300,13 @@ xsp_status xsp_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_trac
 xsp_status xsp_analyze(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
                        const xsp_groups* groups, const xsp_system_spec* spec,
                        const xsp_analysis_opts* opts, xsp_tables_out* out, void* stream);
+
+/* LeveledRunGroup + compute_overhead (leveled.cpp:56-231) over a correlation
+ * computed by xsp_correlate on the same ctx. Uses opts->trim_fraction and
+ * opts->noise_tolerance. Synchronous (the chain order is decided on the host). */
+xsp_status xsp_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                       const xsp_level_sets* sets, const xsp_analysis_opts* opts, xsp_overhead_out* out,
+                       void* stream);
 
 /* End-to-end convenience for host-resident inputs: copies the HOST columns to the
  * device, runs xsp_correlate + xsp_analyze, and copies every result column back

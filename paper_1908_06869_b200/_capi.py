@@ -124,12 +124,26 @@ class TablesOut(C.Structure):
     ] + [(n, t) for n, t, _ in TABLE_FIELDS]
 
 
+class LevelSets(C.Structure):
+    _fields_ = [("n_sets", C.c_uint32), ("set_off", u32p), ("trace_idx", u32p), ("levels", u32p)]
+
+
+class OverheadOut(C.Structure):
+    _fields_ = [("status", C.c_int32), ("err_a", C.c_uint32), ("err_b", C.c_uint32),
+                ("n_sets", C.c_uint32), ("n_events", C.c_uint32), ("chain", u32p),
+                ("ev_level", u8p), ("ev_layer", u32p), ("ev_kernel", u32p), ("lat", f64p),
+                ("overhead", f64p), ("step_flags", u8p), ("accurate", f64p)]
+
+
+L_OK, L_TOO_FEW, L_NOT_CHAIN, L_AMBIGUOUS, L_TRACE_FAILED = range(5)
+EV_IN_NARROW, EV_IN_WIDE, EV_CLAMPED, EV_NEGATIVE = 1, 2, 4, 8
+
 # exported symbols of libxsp.so, i.e. the functions include/xsp.h declares
 EXPORTS = [
     "xsp_abi_version", "xsp_ctx_create", "xsp_ctx_destroy", "xsp_last_error", "xsp_correlate",
     "xsp_analyze", "xsp_run_host", "xsp_last_transfer_bytes", "xsp_last_launch_count",
     "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host", "xsp_set_profiling", "xsp_stage_reset",
-    "xsp_stage_times",
+    "xsp_stage_times", "xsp_leveled",
 ]
 
 _lib = None
@@ -180,5 +194,8 @@ def load() -> C.CDLL:
     lib.xsp_stage_reset.argtypes = [P]
     lib.xsp_stage_times.argtypes = [P, C.c_int, C.POINTER(C.c_char_p), f64p, u64p]
     lib.xsp_stage_times.restype = C.c_int
+    lib.xsp_leveled.argtypes = [P, C.POINTER(SpanCols), C.POINTER(CorrOut), C.POINTER(LevelSets),
+                                C.POINTER(AnalysisOpts), C.POINTER(OverheadOut), P]
+    lib.xsp_leveled.restype = C.c_int32
     _lib = lib
     return lib

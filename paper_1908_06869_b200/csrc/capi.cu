@@ -171,6 +171,18 @@ XSP_API xsp_status xsp_analyze(xsp_ctx* ctx, const xsp_span_cols* cols, const xs
   });
 }
 
+XSP_API xsp_status xsp_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                               const xsp_level_sets* sets, const xsp_analysis_opts* opts,
+                               xsp_overhead_out* out, void* stream) {
+  return guard(ctx, "xsp_leveled", [&] {
+    if (!cols || !corr || !sets || !opts || !out) throw std::invalid_argument("null argument");
+    if (!sets->set_off || (sets->n_sets && (!sets->trace_idx || !sets->levels)))
+      throw std::invalid_argument("null level-set column");
+    std::memset(out, 0, sizeof(*out));
+    xsp::run_leveled(ctx, cols, corr, sets, opts, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
 XSP_API xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht,
                                 const xsp_groups* groups, const xsp_system_spec* spec,
                                 const xsp_analysis_opts* opts, xsp_corr_out* corr_host,

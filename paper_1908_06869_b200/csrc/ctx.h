@@ -147,4 +147,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* tr
 void run_analyze(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
                  const xsp_groups* groups, const xsp_system_spec* spec,
                  const xsp_analysis_opts* opts, xsp_tables_out* out, cudaStream_t st);
+void run_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                 const xsp_level_sets* sets, const xsp_analysis_opts* opts, xsp_overhead_out* out,
+                 cudaStream_t st);
 }  // namespace xsp

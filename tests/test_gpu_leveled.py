@@ -1,0 +1,99 @@
+"""GPU parity for stage (f), the leveled-measurement merge, against the reference's
+LeveledRunGroup::from_bundles + compute_overhead (oracle/_ref)."""
+import numpy as np
+import pytest
+
+from oracle import ref
+from paper_1908_06869_b200.leveled import LeveledError, compute_overhead
+
+pytestmark = pytest.mark.gpu
+
+M, ML, MLG = 0b001, 0b011, 0b111
+
+
+def compare(report, bag):
+    arrays, strings = bag
+    assert int(arrays["status"][0]) == 0, strings["error"]
+    n = len(arrays["o_level"])
+    assert len(report.rows) == n
+    off = arrays["o_ov_off"]
+    for i, row in enumerate(report.rows):
+        assert row.level == int(arrays["o_level"][i])
+        assert row.layer_index == int(arrays["o_layer"][i])
+        assert row.kernel_index == int(arrays["o_kernel"][i])
+        acc = arrays["o_accurate"][i]
+        if np.isnan(acc):
+            assert row.accurate_latency_ns is None
+        else:
+            assert row.accurate_latency_ns == acc
+        assert row.clamped == bool(arrays["o_clamped"][i])
+        want = {int(arrays["o_ov_mask"][j]): float(arrays["o_ov_val"][j]) for j in range(off[i], off[i + 1])}
+        assert row.overhead_by_added_levels == want, (i, row.overhead_by_added_levels, want)
+    want_model = {int(m): float(v) for m, v in zip(arrays["model_ov_mask"], arrays["model_ov_val"])}
+    assert report.model_overhead_by_added_levels == want_model
+    assert report.warnings == [w.decode() for w in strings["warnings"]]
+
+
+def run(engine, gen, **kw):
+    b = gen.batch()
+    return compute_overhead(engine, b, **kw), ref.leveled(b, **{k: v for k, v in kw.items()})
+
+
+def test_overhead_chain_recovers_injected_overhead(engine, has_ref):
+    """Criterion 7 (acceptance_main.cpp:154-179): 157 ms / 58.2 ms / 0.24 ms exactly."""
+    g = ref.Generator().chain("overhead-chain", 1, 15_700_000, 0, 2.0)
+    rep, bag = run(engine, g)
+    compare(rep, bag)
+    assert rep.warnings == []
+    assert rep.model_overhead_by_added_levels[0b010] == 157_000_000.0
+    assert rep.model_overhead_by_added_levels[0b100] == 58_200_000.0
+    layer0 = next(r for r in rep.rows if r.level == 1 and r.layer_index == 0)
+    assert layer0.overhead_by_added_levels[0b100] == 240_000.0
+
+
+@pytest.mark.parametrize("model", ["resnet-like", "mobilenet-like", "minimal", "async-straggler"])
+def test_chain_fixtures(engine, has_ref, model):
+    g = ref.Generator().chain(model, 2, 15_700_000, 1000, 1.5)
+    compare(*run(engine, g))
+
+
+def test_repetitions_with_jitter_and_clamping(engine, has_ref):
+    """Trimmed means over repeated runs per level set; jitter larger than the injected
+    overhead produces clamped and negative-beyond-noise steps (leveled.cpp:190-201)."""
+    g = ref.Generator()
+    for levels in (M, ML, MLG):
+        for r in range(5):
+            g.emit("overhead-chain", 1, levels, 0, 0, 1.0, False, r, 400_000, 31 * r + levels)
+    for noise in (0.01, 0.0, 0.5):
+        rep, bag = run(engine, g, noise=noise)
+        compare(rep, bag)
+
+
+def test_structure_changes_across_the_chain(engine, has_ref):
+    """Events present in one set only produce the 'visible under' warnings."""
+    g = ref.Generator()
+    g.emit("minimal", 1, M).emit("resnet-like", 1, ML).emit("resnet-like", 1, MLG)
+    compare(*run(engine, g))
+
+
+def test_two_sets_and_order_independence(engine, has_ref):
+    g = ref.Generator()
+    g.emit("resnet-like", 1, MLG, 1_000_000).emit("resnet-like", 1, M)
+    compare(*run(engine, g))
+
+
+def test_faults(engine, has_ref):
+    b = ref.Generator().emit("resnet-like", 1, MLG).batch()
+    with pytest.raises(LeveledError, match="at least two chained level sets; got 1"):
+        compute_overhead(engine, b)
+    b = ref.Generator().emit("resnet-like", 1, ML).emit("resnet-like", 1, 0b101).batch()
+    with pytest.raises(LeveledError, match="do not form an inclusion chain"):
+        compute_overhead(engine, b)
+    _, bag = ref.leveled(b)
+    assert "M+L and M+G do not form an inclusion chain" in bag[1]["error"][0].decode()
+    b = ref.Generator().emit("overlap", 1, M).emit("overlap", 1, MLG).batch()
+    with pytest.raises(LeveledError, match="ambiguous span"):
+        compute_overhead(engine, b)
+    b = ref.Generator().emit("minimal", 1, M).emit("minimal", 2, ML).batch()
+    with pytest.raises(LeveledError, match="runs mix batch sizes 1 and 2"):
+        compute_overhead(engine, b)
