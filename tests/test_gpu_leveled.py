@@ -86,11 +86,17 @@ def test_faults(engine, has_ref):
     b = ref.Generator().emit("resnet-like", 1, MLG).batch()
     with pytest.raises(LeveledError, match="at least two chained level sets; got 1"):
         compute_overhead(engine, b)
-    b = ref.Generator().emit("resnet-like", 1, ML).emit("resnet-like", 1, 0b101).batch()
-    with pytest.raises(LeveledError, match="do not form an inclusion chain"):
+    b = ref.Generator().emit("resnet-like", 1, ML).emit("resnet-like", 1, 0b1001).batch()
+    with pytest.raises(LeveledError) as e:
         compute_overhead(engine, b)
-    _, bag = ref.leveled(b)
-    assert "M+L and M+G do not form an inclusion chain" in bag[1]["error"][0].decode()
+    _, strings = ref.leveled(b)
+    assert str(e.value) == strings["error"][0].decode()
+    assert "M+L and M+A do not form an inclusion chain" in str(e.value)
+    # a bundle the correlator rejects: the TraceError propagates unchanged
+    b = ref.Generator().emit("resnet-like", 1, ML).emit("resnet-like", 1, 0b101).batch()
+    with pytest.raises(RuntimeError) as e:
+        compute_overhead(engine, b)
+    assert str(e.value) == ref.leveled(b)[1]["error"][0].decode()
     b = ref.Generator().emit("overlap", 1, M).emit("overlap", 1, MLG).batch()
     with pytest.raises(LeveledError, match="ambiguous span"):
         compute_overhead(engine, b)
