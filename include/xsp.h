@@ -287,12 +287,39 @@ int xsp_abi_version(void);
 
 /* correlate() for every trace (correlator.cpp:366-370 = assign_parents 141-282 +
  * correlate_async 287-364). Inputs are DEVICE pointers. Traces must be in
- * timeline order (sort_timeline); when sort_if_needed != 0 unsorted traces are
- * first sorted on the device (xsp_sort_timeline), otherwise XSP_E_UNSORTED.
+ * timeline order (sort_timeline, span.hpp:161-163), else XSP_E_UNSORTED.
+ * mode: 0, or XSP_CORR_PARENTS_ONLY for assign_parents alone (kernel launches
+ * keep no exec: kernel_exec_row = UINT32_MAX; no fusion orphans or cid faults).
  * stream: a cudaStream_t (NULL = legacy default stream). Asynchronous except
- * for the small count read-back needed to size the outputs. */
-xsp_status xsp_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
-                         int sort_if_needed, xsp_corr_out* out, void* stream);
+ * for the small count read-backs needed to size the outputs. */
+#define XSP_CORR_PARENTS_ONLY 2
+xsp_status xsp_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces, int mode,
+                         xsp_corr_out* out, void* stream);
+
+/* sort_timeline (span.cpp:112-127) for every trace: perm[j] = input row of the
+ * span at position j once each trace [span_off[t], span_off[t+1]) is stably
+ * sorted by (begin_ns, rank(level), span_id). *was_sorted = 1 when the input
+ * already was (perm is then the identity). HOST pointers; synchronous. */
+xsp_status xsp_sort_timeline_host(xsp_ctx* ctx, uint64_t n_spans, const uint64_t* begin_ns,
+                                  const uint8_t* flags, const uint64_t* span_id, uint32_t n_traces,
+                                  const uint64_t* span_off, uint32_t* perm, int* was_sorted);
+
+/* Host-buffer forms used by the C++ drop-in (libstrata_b200): inputs are HOST
+ * pointers, copied to the device; results are copied back into ctx-owned pinned
+ * host memory (pointers valid until the next call on the ctx). Synchronous.
+ * xsp_analyze_host / xsp_leveled_host take a HOST xsp_corr_out (e.g. packed from
+ * existing entity trees); only the columns the analysis reads must be set:
+ * trace_status, trace_model_row, trace_layer_off, trace_kernel_off,
+ * trace_amb_off, layer_row, layer_kernel_off, layer_dur, kernel_metric_row,
+ * kernel_dur, kernel_name, kernel_occ. */
+xsp_status xsp_correlate_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces, int mode,
+                              xsp_corr_out* out);
+xsp_status xsp_analyze_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                            const xsp_groups* groups, const xsp_system_spec* spec,
+                            const xsp_analysis_opts* opts, xsp_tables_out* out);
+xsp_status xsp_leveled_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                            const xsp_level_sets* sets, const xsp_analysis_opts* opts,
+                            xsp_overhead_out* out);
 
 /* a8..a15 + model_roofline + a1 throughput + top-k for every group over a
  * correlation computed by xsp_correlate on the same ctx. cols must be the same

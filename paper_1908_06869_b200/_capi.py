@@ -143,7 +143,8 @@ EXPORTS = [
     "xsp_abi_version", "xsp_ctx_create", "xsp_ctx_destroy", "xsp_last_error", "xsp_correlate",
     "xsp_analyze", "xsp_run_host", "xsp_last_transfer_bytes", "xsp_last_launch_count",
     "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host", "xsp_set_profiling", "xsp_stage_reset",
-    "xsp_stage_times", "xsp_leveled",
+    "xsp_stage_times", "xsp_leveled", "xsp_sort_timeline_host", "xsp_correlate_host",
+    "xsp_analyze_host", "xsp_leveled_host",
 ]
 
 _lib = None
@@ -197,5 +198,10 @@ def load() -> C.CDLL:
     lib.xsp_leveled.argtypes = [P, C.POINTER(SpanCols), C.POINTER(CorrOut), C.POINTER(LevelSets),
                                 C.POINTER(AnalysisOpts), C.POINTER(OverheadOut), P]
     lib.xsp_leveled.restype = C.c_int32
+    lib.xsp_sort_timeline_host.argtypes = [P, C.c_uint64, u64p, u8p, u64p, C.c_uint32, u64p, u32p,
+                                           C.POINTER(C.c_int)]
+    lib.xsp_sort_timeline_host.restype = C.c_int32
+    lib.xsp_correlate_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.c_int, C.POINTER(CorrOut)]
+    lib.xsp_correlate_host.restype = C.c_int32
     _lib = lib
     return lib

@@ -1,5 +1,5 @@
 // The extern "C" boundary (include/xsp.h): context management, argument
-// checking, error capture, and the host-buffer end-to-end entry point.
+// checking, error capture, and the host-buffer entry points.
 
 #include <cstring>
 #include <new>
@@ -8,6 +8,11 @@
 #include "ctx.h"
 
 #define XSP_API extern "C" __attribute__((visibility("default")))
+
+namespace xsp {
+void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const uint8_t* flags, const uint64_t* sid,
+                       uint32_t T, const uint64_t* off, uint32_t* perm, uint32_t* was_sorted, cudaStream_t st);
+}
 
 namespace {
 
@@ -41,15 +46,14 @@ xsp_status guard(xsp_ctx* ctx, const char* what, auto&& body) {
 }
 
 void check_cols(const xsp_span_cols* c, const xsp_traces* t) {
-  if (!c || !t) throw std::invalid_argument("null columns or traces");
-  if (c->n_spans && (!c->span_id || !c->parent_id || !c->begin_ns || !c->end_ns || !c->cid ||
-                     !c->flags || !c->name_id))
+  if (!c) throw std::invalid_argument("null columns");
+  if (c->n_spans && (!c->span_id || !c->parent_id || !c->begin_ns || !c->end_ns || !c->cid || !c->flags ||
+                     !c->name_id))
     throw std::invalid_argument("null span column");
   if (c->n_metric_rows && (!c->flops || !c->dram_read || !c->dram_write || !c->occupancy))
     throw std::invalid_argument("null metric column");
-  if (c->n_layer_rows && (!c->alloc_bytes || !c->type_id))
-    throw std::invalid_argument("null layer column");
-  if (!t->span_off || (t->n_traces && !t->levels)) throw std::invalid_argument("null trace column");
+  if (c->n_layer_rows && (!c->alloc_bytes || !c->type_id)) throw std::invalid_argument("null layer column");
+  if (t && (!t->span_off || (t->n_traces && !t->levels))) throw std::invalid_argument("null trace column");
 }
 
 template <typename T>
@@ -70,6 +74,123 @@ T* to_host(xsp_ctx* ctx, const std::string& name, const T* src, uint64_t count, 
     ctx->d2h_bytes += count * sizeof(T);
   }
   return h;
+}
+
+xsp_span_cols upload_cols(xsp_ctx* ctx, const xsp_span_cols* hc, cudaStream_t st) {
+  const uint64_t n = hc->n_spans;
+  xsp_span_cols dc;
+  dc.n_spans = n;
+  dc.span_id = to_dev(ctx, "span_id", hc->span_id, n, st);
+  dc.parent_id = to_dev(ctx, "parent_id", hc->parent_id, n, st);
+  dc.begin_ns = to_dev(ctx, "begin", hc->begin_ns, n, st);
+  dc.end_ns = to_dev(ctx, "end", hc->end_ns, n, st);
+  dc.cid = to_dev(ctx, "cid", hc->cid, n, st);
+  dc.flags = to_dev(ctx, "flags", hc->flags, n, st);
+  dc.name_id = to_dev(ctx, "name", hc->name_id, n, st);
+  dc.n_metric_rows = hc->n_metric_rows;
+  dc.flops = to_dev(ctx, "flops", hc->flops, hc->n_metric_rows, st);
+  dc.dram_read = to_dev(ctx, "read", hc->dram_read, hc->n_metric_rows, st);
+  dc.dram_write = to_dev(ctx, "write", hc->dram_write, hc->n_metric_rows, st);
+  dc.occupancy = to_dev(ctx, "occ", hc->occupancy, hc->n_metric_rows, st);
+  dc.n_layer_rows = hc->n_layer_rows;
+  dc.alloc_bytes = to_dev(ctx, "alloc", hc->alloc_bytes, hc->n_layer_rows, st);
+  dc.type_id = to_dev(ctx, "type", hc->type_id, hc->n_layer_rows, st);
+  return dc;
+}
+
+xsp_traces upload_traces(xsp_ctx* ctx, const xsp_traces* ht, cudaStream_t st) {
+  xsp_traces dt;
+  dt.n_traces = ht->n_traces;
+  dt.span_off = to_dev(ctx, "span_off", ht->span_off, (uint64_t)ht->n_traces + 1, st);
+  dt.levels = to_dev(ctx, "levels", ht->levels, ht->n_traces, st);
+  return dt;
+}
+
+// the columns analysis / leveling read from a (host) correlation
+xsp_corr_out upload_corr(xsp_ctx* ctx, const xsp_corr_out* h, cudaStream_t st) {
+  xsp_corr_out d = *h;
+  const uint64_t T = h->n_traces, L = h->n_layers, K = h->n_kernels;
+  d.trace_status = to_dev(ctx, "c.t_status", h->trace_status, T, st);
+  d.trace_model_row = to_dev(ctx, "c.t_model", h->trace_model_row, T, st);
+  d.trace_layer_off = to_dev(ctx, "c.t_loff", h->trace_layer_off, T + 1, st);
+  d.trace_kernel_off = to_dev(ctx, "c.t_koff", h->trace_kernel_off, T + 1, st);
+  d.trace_amb_off = to_dev(ctx, "c.t_aoff", h->trace_amb_off, T + 1, st);
+  d.layer_row = to_dev(ctx, "c.l_row", h->layer_row, L, st);
+  d.layer_kernel_off = to_dev(ctx, "c.l_koff", h->layer_kernel_off, L + 1, st);
+  d.layer_dur = to_dev(ctx, "c.l_dur", h->layer_dur, L, st);
+  d.kernel_metric_row = to_dev(ctx, "c.k_mrow", h->kernel_metric_row, K, st);
+  d.kernel_dur = to_dev(ctx, "c.k_dur", h->kernel_dur, K, st);
+  d.kernel_name = to_dev(ctx, "c.k_name", h->kernel_name, K, st);
+  d.kernel_occ = to_dev(ctx, "c.k_occ", h->kernel_occ, K, st);
+  return d;
+}
+
+void download_corr(xsp_ctx* ctx, const xsp_corr_out& dcorr, xsp_corr_out* c, cudaStream_t st) {
+  const uint32_t T = dcorr.n_traces;
+  *c = dcorr;
+  c->trace_status = to_host(ctx, "t_status", dcorr.trace_status, T, st);
+  c->trace_err_row = to_host(ctx, "t_err", dcorr.trace_err_row, 2ull * T, st);
+  c->trace_model_row = to_host(ctx, "t_model", dcorr.trace_model_row, T, st);
+  c->trace_layer_off = to_host(ctx, "t_loff", dcorr.trace_layer_off, T + 1ull, st);
+  c->trace_kernel_off = to_host(ctx, "t_koff", dcorr.trace_kernel_off, T + 1ull, st);
+  c->trace_orphan_off = to_host(ctx, "t_ooff", dcorr.trace_orphan_off, T + 1ull, st);
+  c->trace_amb_off = to_host(ctx, "t_aoff", dcorr.trace_amb_off, T + 1ull, st);
+  c->layer_row = to_host(ctx, "l_row", dcorr.layer_row, dcorr.n_layers, st);
+  c->layer_kernel_off = to_host(ctx, "l_koff", dcorr.layer_kernel_off, dcorr.n_layers + 1, st);
+  c->layer_dur = to_host(ctx, "l_dur", dcorr.layer_dur, dcorr.n_layers, st);
+  c->layer_attr_row = to_host(ctx, "l_attr", dcorr.layer_attr_row, dcorr.n_layers, st);
+  c->kernel_launch_row = to_host(ctx, "k_launch", dcorr.kernel_launch_row, dcorr.n_kernels, st);
+  c->kernel_exec_row = to_host(ctx, "k_exec", dcorr.kernel_exec_row, dcorr.n_kernels, st);
+  c->kernel_metric_row = to_host(ctx, "k_mrow", dcorr.kernel_metric_row, dcorr.n_kernels, st);
+  c->kernel_dur = to_host(ctx, "k_dur", dcorr.kernel_dur, dcorr.n_kernels, st);
+  c->kernel_name = to_host(ctx, "k_name", dcorr.kernel_name, dcorr.n_kernels, st);
+  c->kernel_occ = to_host(ctx, "k_occ", dcorr.kernel_occ, dcorr.n_kernels, st);
+  c->orphan_row = to_host(ctx, "o_row", dcorr.orphan_row, dcorr.n_orphans, st);
+  c->orphan_reason = to_host(ctx, "o_reason", dcorr.orphan_reason, dcorr.n_orphans, st);
+  c->amb_row = to_host(ctx, "a_row", dcorr.amb_row, dcorr.n_ambiguities, st);
+  c->amb_cand_off = to_host(ctx, "a_coff", dcorr.amb_cand_off, dcorr.n_ambiguities + 1, st);
+  c->amb_cand_row = to_host(ctx, "a_crow", dcorr.amb_cand_row, dcorr.n_candidates, st);
+}
+
+void download_tables(xsp_ctx* ctx, const xsp_tables_out& dtab, const xsp_analysis_opts* opts, xsp_tables_out* t,
+                     cudaStream_t st) {
+  const uint32_t G = dtab.n_groups;
+  const uint64_t L = dtab.n_layers, K = dtab.n_kernels, N = dtab.n_names;
+  const uint64_t tk = opts->top_k ? opts->top_k : 1;
+  *t = dtab;
+#define BACK(field, count) t->field = to_host(ctx, "t." #field, dtab.field, (count), st)
+  BACK(group_status, G);
+  BACK(group_err_arg, G);
+  BACK(group_layer_off, G + 1ull);
+  BACK(group_kernel_off, G + 1ull);
+  BACK(group_name_off, G + 1ull);
+  BACK(k_name, K); BACK(k_layer, K); BACK(k_lat, K); BACK(k_flops, K); BACK(k_read, K);
+  BACK(k_write, K); BACK(k_occ, K); BACK(k_ai, K); BACK(k_tput, K); BACK(k_bound, K);
+  BACK(k_roofline_in, K);
+  BACK(l_index, L); BACK(l_row, L); BACK(l_layer_lat, L); BACK(l_kern_lat, L); BACK(l_flops, L);
+  BACK(l_read, L); BACK(l_write, L); BACK(l_occ, L); BACK(l_count, L); BACK(l_ai, L);
+  BACK(l_tput, L); BACK(l_bound, L); BACK(l_nongpu, L); BACK(l_gpu_share, L);
+  BACK(l_nongpu_share, L); BACK(l_flagged, L); BACK(l_roofline_in, L); BACK(l_topk, L * tk);
+  BACK(n_name, N); BACK(n_count, N); BACK(n_lat, N); BACK(n_pct, N); BACK(n_flops, N);
+  BACK(n_read, N); BACK(n_write, N); BACK(n_occ, N); BACK(n_ai, N); BACK(n_tput, N);
+  BACK(n_bound, N);
+  BACK(m_lat, G); BACK(m_kern_lat, G); BACK(m_flops, G); BACK(m_read, G); BACK(m_write, G);
+  BACK(m_occ, G); BACK(m_count, G); BACK(m_ai, G); BACK(m_tput, G); BACK(m_bound, G);
+  BACK(m_gpu, G); BACK(m_gpu_pct, G); BACK(m_throughput, G); BACK(m_roofline_in, G);
+#undef BACK
+}
+
+void download_overhead(xsp_ctx* ctx, const xsp_overhead_out& d, xsp_overhead_out* o, cudaStream_t st) {
+  *o = d;
+  if (d.status != XSP_L_OK) return;
+  const uint64_t E = d.n_events, S = d.n_sets;
+  o->ev_level = to_host(ctx, "l.ev_level", d.ev_level, E, st);
+  o->ev_layer = to_host(ctx, "l.ev_layer", d.ev_layer, E, st);
+  o->ev_kernel = to_host(ctx, "l.ev_kernel", d.ev_kernel, E, st);
+  o->lat = to_host(ctx, "l.lat", d.lat, S * E, st);
+  o->overhead = to_host(ctx, "l.ov", d.overhead, (S - 1) * E, st);
+  o->step_flags = to_host(ctx, "l.flags", d.step_flags, (S - 1) * E, st);
+  o->accurate = to_host(ctx, "l.acc", d.accurate, E, st);
 }
 
 }  // namespace
@@ -97,9 +218,7 @@ XSP_API void xsp_ctx_destroy(xsp_ctx* ctx) {
   delete ctx;
 }
 
-XSP_API const char* xsp_last_error(const xsp_ctx* ctx) {
-  return ctx ? ctx->last_error.c_str() : "null context";
-}
+XSP_API const char* xsp_last_error(const xsp_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
 
 XSP_API uint64_t xsp_last_launch_count(const xsp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
@@ -149,13 +268,13 @@ XSP_API xsp_status xsp_copy_to_host(xsp_ctx* ctx, void* dst, const void* src, si
   });
 }
 
-XSP_API xsp_status xsp_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
-                                 int sort_if_needed, xsp_corr_out* out, void* stream) {
+XSP_API xsp_status xsp_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces, int mode,
+                                 xsp_corr_out* out, void* stream) {
   return guard(ctx, "xsp_correlate", [&] {
     check_cols(cols, traces);
-    if (!out) throw std::invalid_argument("null output");
+    if (!traces || !out) throw std::invalid_argument("null argument");
     std::memset(out, 0, sizeof(*out));
-    xsp::run_correlate(ctx, cols, traces, sort_if_needed, out, static_cast<cudaStream_t>(stream));
+    xsp::run_correlate(ctx, cols, traces, mode, out, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -183,97 +302,96 @@ XSP_API xsp_status xsp_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xs
   });
 }
 
+XSP_API xsp_status xsp_sort_timeline_host(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const uint8_t* flags,
+                                          const uint64_t* span_id, uint32_t n_traces, const uint64_t* span_off,
+                                          uint32_t* perm, int* was_sorted) {
+  return guard(ctx, "xsp_sort_timeline_host", [&] {
+    if (!span_off || !perm || (n && (!begin || !flags || !span_id))) throw std::invalid_argument("null argument");
+    if (n >= 0xFFFFFFF0ull) throw std::invalid_argument("more than 2^32-16 spans in one call");
+    cudaStream_t st = nullptr;
+    const uint64_t* db = to_dev(ctx, "s.begin", begin, n, st);
+    const uint8_t* df = to_dev(ctx, "s.flags", flags, n, st);
+    const uint64_t* ds = to_dev(ctx, "s.sid", span_id, n, st);
+    const uint64_t* doff = to_dev(ctx, "s.off", span_off, (uint64_t)n_traces + 1, st);
+    uint32_t* dperm = ctx->d<uint32_t>("s.perm", n ? n : 1);
+    uint32_t sorted = 0;
+    xsp::run_sort_timeline(ctx, n, db, df, ds, n_traces, doff, dperm, &sorted, st);
+    if (n) XSP_CUDA(cudaMemcpy(perm, dperm, n * 4, cudaMemcpyDeviceToHost));
+    if (was_sorted) *was_sorted = (int)sorted;
+  });
+}
+
+XSP_API xsp_status xsp_correlate_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht, int mode,
+                                      xsp_corr_out* out) {
+  return guard(ctx, "xsp_correlate_host", [&] {
+    check_cols(hc, ht);
+    if (!ht || !out) throw std::invalid_argument("null argument");
+    cudaStream_t st = nullptr;
+    ctx->h2d_bytes = ctx->d2h_bytes = 0;
+    xsp_span_cols dc = upload_cols(ctx, hc, st);
+    xsp_traces dt = upload_traces(ctx, ht, st);
+    xsp_corr_out dcorr;
+    std::memset(&dcorr, 0, sizeof(dcorr));
+    xsp::run_correlate(ctx, &dc, &dt, mode, &dcorr, st);
+    download_corr(ctx, dcorr, out, st);
+    XSP_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+XSP_API xsp_status xsp_analyze_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_corr_out* hcorr,
+                                    const xsp_groups* groups, const xsp_system_spec* spec,
+                                    const xsp_analysis_opts* opts, xsp_tables_out* out) {
+  return guard(ctx, "xsp_analyze_host", [&] {
+    check_cols(hc, nullptr);
+    if (!hcorr || !groups || !spec || !opts || !out) throw std::invalid_argument("null argument");
+    cudaStream_t st = nullptr;
+    ctx->h2d_bytes = ctx->d2h_bytes = 0;
+    xsp_span_cols dc = upload_cols(ctx, hc, st);
+    xsp_corr_out dcorr = upload_corr(ctx, hcorr, st);
+    xsp_tables_out dtab;
+    std::memset(&dtab, 0, sizeof(dtab));
+    xsp::run_analyze(ctx, &dc, &dcorr, groups, spec, opts, &dtab, st);
+    download_tables(ctx, dtab, opts, out, st);
+    XSP_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+XSP_API xsp_status xsp_leveled_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_corr_out* hcorr,
+                                    const xsp_level_sets* sets, const xsp_analysis_opts* opts,
+                                    xsp_overhead_out* out) {
+  return guard(ctx, "xsp_leveled_host", [&] {
+    check_cols(hc, nullptr);
+    if (!hcorr || !sets || !opts || !out) throw std::invalid_argument("null argument");
+    cudaStream_t st = nullptr;
+    xsp_span_cols dc = upload_cols(ctx, hc, st);
+    xsp_corr_out dcorr = upload_corr(ctx, hcorr, st);
+    xsp_overhead_out dov;
+    std::memset(&dov, 0, sizeof(dov));
+    xsp::run_leveled(ctx, &dc, &dcorr, sets, opts, &dov, st);
+    download_overhead(ctx, dov, out, st);
+    XSP_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 XSP_API xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht,
                                 const xsp_groups* groups, const xsp_system_spec* spec,
                                 const xsp_analysis_opts* opts, xsp_corr_out* corr_host,
                                 xsp_tables_out* tab_host, void* stream) {
   return guard(ctx, "xsp_run_host", [&] {
     check_cols(hc, ht);
-    if (!groups || !spec || !opts || !corr_host || !tab_host) throw std::invalid_argument("null argument");
+    if (!ht || !groups || !spec || !opts || !corr_host || !tab_host) throw std::invalid_argument("null argument");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ctx->h2d_bytes = ctx->d2h_bytes = 0;
-    const uint64_t n = hc->n_spans;
-    xsp_span_cols dc;
-    dc.n_spans = n;
-    dc.span_id = to_dev(ctx, "span_id", hc->span_id, n, st);
-    dc.parent_id = to_dev(ctx, "parent_id", hc->parent_id, n, st);
-    dc.begin_ns = to_dev(ctx, "begin", hc->begin_ns, n, st);
-    dc.end_ns = to_dev(ctx, "end", hc->end_ns, n, st);
-    dc.cid = to_dev(ctx, "cid", hc->cid, n, st);
-    dc.flags = to_dev(ctx, "flags", hc->flags, n, st);
-    dc.name_id = to_dev(ctx, "name", hc->name_id, n, st);
-    dc.n_metric_rows = hc->n_metric_rows;
-    dc.flops = to_dev(ctx, "flops", hc->flops, hc->n_metric_rows, st);
-    dc.dram_read = to_dev(ctx, "read", hc->dram_read, hc->n_metric_rows, st);
-    dc.dram_write = to_dev(ctx, "write", hc->dram_write, hc->n_metric_rows, st);
-    dc.occupancy = to_dev(ctx, "occ", hc->occupancy, hc->n_metric_rows, st);
-    dc.n_layer_rows = hc->n_layer_rows;
-    dc.alloc_bytes = to_dev(ctx, "alloc", hc->alloc_bytes, hc->n_layer_rows, st);
-    dc.type_id = to_dev(ctx, "type", hc->type_id, hc->n_layer_rows, st);
-    xsp_traces dt;
-    dt.n_traces = ht->n_traces;
-    dt.span_off = to_dev(ctx, "span_off", ht->span_off, (uint64_t)ht->n_traces + 1, st);
-    dt.levels = to_dev(ctx, "levels", ht->levels, ht->n_traces, st);
-
+    xsp_span_cols dc = upload_cols(ctx, hc, st);
+    xsp_traces dt = upload_traces(ctx, ht, st);
     xsp_corr_out dcorr;
     std::memset(&dcorr, 0, sizeof(dcorr));
-    xsp::run_correlate(ctx, &dc, &dt, 1, &dcorr, st);
+    xsp::run_correlate(ctx, &dc, &dt, 0, &dcorr, st);
     xsp_tables_out dtab;
     std::memset(&dtab, 0, sizeof(dtab));
     xsp::run_analyze(ctx, &dc, &dcorr, groups, spec, opts, &dtab, st);
-
-    // ---- results back to pinned host memory
-    const uint32_t T = dcorr.n_traces;
-    xsp_corr_out& c = *corr_host;
-    c = dcorr;
-    c.trace_status = to_host(ctx, "t_status", dcorr.trace_status, T, st);
-    c.trace_err_row = to_host(ctx, "t_err", dcorr.trace_err_row, 2ull * T, st);
-    c.trace_model_row = to_host(ctx, "t_model", dcorr.trace_model_row, T, st);
-    c.trace_layer_off = to_host(ctx, "t_loff", dcorr.trace_layer_off, T + 1ull, st);
-    c.trace_kernel_off = to_host(ctx, "t_koff", dcorr.trace_kernel_off, T + 1ull, st);
-    c.trace_orphan_off = to_host(ctx, "t_ooff", dcorr.trace_orphan_off, T + 1ull, st);
-    c.trace_amb_off = to_host(ctx, "t_aoff", dcorr.trace_amb_off, T + 1ull, st);
-    c.layer_row = to_host(ctx, "l_row", dcorr.layer_row, dcorr.n_layers, st);
-    c.layer_kernel_off = to_host(ctx, "l_koff", dcorr.layer_kernel_off, dcorr.n_layers + 1, st);
-    c.layer_dur = to_host(ctx, "l_dur", dcorr.layer_dur, dcorr.n_layers, st);
-    c.layer_attr_row = to_host(ctx, "l_attr", dcorr.layer_attr_row, dcorr.n_layers, st);
-    c.kernel_launch_row = to_host(ctx, "k_launch", dcorr.kernel_launch_row, dcorr.n_kernels, st);
-    c.kernel_exec_row = to_host(ctx, "k_exec", dcorr.kernel_exec_row, dcorr.n_kernels, st);
-    c.kernel_metric_row = to_host(ctx, "k_mrow", dcorr.kernel_metric_row, dcorr.n_kernels, st);
-    c.kernel_dur = to_host(ctx, "k_dur", dcorr.kernel_dur, dcorr.n_kernels, st);
-    c.kernel_name = to_host(ctx, "k_name", dcorr.kernel_name, dcorr.n_kernels, st);
-    c.kernel_occ = to_host(ctx, "k_occ", dcorr.kernel_occ, dcorr.n_kernels, st);
-    c.orphan_row = to_host(ctx, "o_row", dcorr.orphan_row, dcorr.n_orphans, st);
-    c.orphan_reason = to_host(ctx, "o_reason", dcorr.orphan_reason, dcorr.n_orphans, st);
-    c.amb_row = to_host(ctx, "a_row", dcorr.amb_row, dcorr.n_ambiguities, st);
-    c.amb_cand_off = to_host(ctx, "a_coff", dcorr.amb_cand_off, dcorr.n_ambiguities + 1, st);
-    c.amb_cand_row = to_host(ctx, "a_crow", dcorr.amb_cand_row, dcorr.n_candidates, st);
-
-    const uint32_t G = dtab.n_groups;
-    const uint64_t L = dtab.n_layers, K = dtab.n_kernels, N = dtab.n_names;
-    const uint64_t tk = opts->top_k ? opts->top_k : 1;
-    xsp_tables_out& t = *tab_host;
-    t = dtab;
-#define BACK(field, count) t.field = to_host(ctx, "t." #field, dtab.field, (count), st)
-    BACK(group_status, G);
-    BACK(group_err_arg, G);
-    BACK(group_layer_off, G + 1ull);
-    BACK(group_kernel_off, G + 1ull);
-    BACK(group_name_off, G + 1ull);
-    BACK(k_name, K); BACK(k_layer, K); BACK(k_lat, K); BACK(k_flops, K); BACK(k_read, K);
-    BACK(k_write, K); BACK(k_occ, K); BACK(k_ai, K); BACK(k_tput, K); BACK(k_bound, K);
-    BACK(k_roofline_in, K);
-    BACK(l_index, L); BACK(l_row, L); BACK(l_layer_lat, L); BACK(l_kern_lat, L); BACK(l_flops, L);
-    BACK(l_read, L); BACK(l_write, L); BACK(l_occ, L); BACK(l_count, L); BACK(l_ai, L);
-    BACK(l_tput, L); BACK(l_bound, L); BACK(l_nongpu, L); BACK(l_gpu_share, L);
-    BACK(l_nongpu_share, L); BACK(l_flagged, L); BACK(l_roofline_in, L); BACK(l_topk, L * tk);
-    BACK(n_name, N); BACK(n_count, N); BACK(n_lat, N); BACK(n_pct, N); BACK(n_flops, N);
-    BACK(n_read, N); BACK(n_write, N); BACK(n_occ, N); BACK(n_ai, N); BACK(n_tput, N);
-    BACK(n_bound, N);
-    BACK(m_lat, G); BACK(m_kern_lat, G); BACK(m_flops, G); BACK(m_read, G); BACK(m_write, G);
-    BACK(m_occ, G); BACK(m_count, G); BACK(m_ai, G); BACK(m_tput, G); BACK(m_bound, G);
-    BACK(m_gpu, G); BACK(m_gpu_pct, G); BACK(m_throughput, G); BACK(m_roofline_in, G);
-#undef BACK
+    download_corr(ctx, dcorr, corr_host, st);
+    download_tables(ctx, dtab, opts, tab_host, st);
     XSP_CUDA(cudaStreamSynchronize(st));
   });
 }

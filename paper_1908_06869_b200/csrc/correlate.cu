@@ -262,6 +262,7 @@ constexpr int P1_TCACHE = 32;  // traces of a tile cached in shared memory
 
 struct P1Args {
   int bulk;  // all columns 16-byte aligned: stage full tiles with cp.async.bulk
+  int parents_only;
   const uint64_t* span_id;
   const uint8_t* flags;
   const uint64_t* begin;
@@ -628,7 +629,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, 3) k_pass1(P1Args a) {
           ent.cid = sm.cid[j];
           a.ex[carry.c_ex + __popc(bx & lt)] = ent;
         } else {
-          emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
+          if (!a.parents_only) emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
         }
       }
       if (head) {
@@ -983,6 +984,7 @@ struct FuseArgs {
   uint32_t* kl_exec;  // matched exec item
   Orphans orph;
   bool any_slow;
+  bool parents_only;  // assign_parents without correlate_async
 };
 
 __global__ void k_fuse(FuseArgs a) {
@@ -995,8 +997,9 @@ __global__ void k_fuse(FuseArgs a) {
   uint32_t keep = 0, x = kNone;
   if (ent.parent < PAR_MAXROW) {
     const uint8_t f = a.flags[ent.row];
-    if (is_sync_kernel(f)) {
+    if (is_sync_kernel(f) || a.parents_only) {
       keep = 1;
+      x = is_sync_kernel(f) ? kNone : kNone - 1;  // kNone-1: launch left unfused
     } else if (!(f & XSP_F_CID)) {
       emit_orphan(a.orph, t, CAT_LAUNCH, ((uint64_t)ent.parent << 32) | k, ent.row, XSP_O_LAUNCH_NO_CID);
     } else {
@@ -1061,6 +1064,14 @@ __global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val, 
   if (x == kNone) {  // synchronous kernel: launch and exec are the same record
     er = r;
     mr = kl_mrow[k];
+  } else if (x == kNone - 1) {  // assign_parents only: launch without its exec
+    k_launch[j] = r;
+    k_exec[j] = kNone;
+    k_mrow[j] = kNone;
+    k_dur[j] = 0;
+    k_name[j] = name[r];
+    k_occ[j] = 0.0;
+    return;
   } else {
     const ExEnt e = ex[x];
     er = e.row;
@@ -1244,8 +1255,10 @@ uint32_t read_u32(xsp_ctx* ctx, const uint32_t* dptr, cudaStream_t st) {
 
 }  // namespace
 
-void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, int sort_if_needed,
+void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, int mode,
                    xsp_corr_out* out, cudaStream_t st) {
+  const int sort_if_needed = mode & 1;
+  const bool parents_only = (mode & XSP_CORR_PARENTS_ONLY) != 0;
   const uint64_t n = c->n_spans;
   const uint32_t T = tr->n_traces;
   if (n >= 0xFFFFFFF0ull) throw std::invalid_argument("more than 2^32-16 spans in one call");
@@ -1310,6 +1323,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   orph.reason = ctx->d<uint8_t>("c.o_reason", 2 * orph_cap);
   orph.count = counters + 0;
   a.orph = orph;
+  a.parents_only = parents_only;
   a.amb_kl = ctx->d<uint32_t>("c.amb_kl", n);
   a.amb_gx = ctx->d<uint32_t>("c.amb_gx", n);
   a.amb_count = counters + 1;
@@ -1404,7 +1418,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   }
 
   // ---- clean batch: optimistic merge-aligned fusion (general path on failure)
-  if (htot[8] == 0 && n_pend == 0 && n_amb_raw == 0) {
+  if (htot[8] == 0 && n_pend == 0 && n_amb_raw == 0 && !parents_only) {
     ctx->stage_begin("gather", st);
     out->n_kernels = nkl;
     out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", nkl);
@@ -1463,9 +1477,13 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   j.T = T;
   j.n_ex = nex;
   j.n_kl = nkl;
-  launch(ctx, k_join_counts, T, st, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
-  launch(ctx, k_join_check, nkl, st, nkl, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
-  const uint32_t any_slow = read_u32(ctx, counters + 7, st);
+  uint32_t any_slow = 0;
+  if (!parents_only) {
+    launch(ctx, k_join_counts, T, st, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
+    launch(ctx, k_join_check, nkl, st, nkl, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, t_slow,
+           counters + 7);
+    any_slow = read_u32(ctx, counters + 7, st);
+  }
   auto* dup_ex = ctx->d<unsigned long long>("c.dup_ex", T);
   auto* dup_kl = ctx->d<unsigned long long>("c.dup_kl", T);
   XSP_CUDA(cudaMemsetAsync(dup_ex, 0xFF, T * 8ull, st));
@@ -1519,6 +1537,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   fa.kl_exec = ctx->d<uint32_t>("c.kl_exec", nkl + 1);
   fa.orph = orph;
   fa.any_slow = any_slow != 0;
+  fa.parents_only = parents_only;
   launch(ctx, k_fuse, nkl, st, fa);
   if (any_slow) launch(ctx, k_leftover, nex, st, fa);
 
