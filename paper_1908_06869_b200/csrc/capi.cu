@@ -182,7 +182,7 @@ void download_tables(xsp_ctx* ctx, const xsp_tables_out& dtab, const xsp_analysi
 
 void download_overhead(xsp_ctx* ctx, const xsp_overhead_out& d, xsp_overhead_out* o, cudaStream_t st) {
   *o = d;
-  if (d.status != XSP_L_OK) return;
+  if (d.status == XSP_L_AMBIGUOUS || d.status == XSP_L_TRACE_FAILED || d.n_sets == 0) return;
   const uint64_t E = d.n_events, S = d.n_sets;
   o->ev_level = to_host(ctx, "l.ev_level", d.ev_level, E, st);
   o->ev_layer = to_host(ctx, "l.ev_layer", d.ev_layer, E, st);

@@ -259,17 +259,19 @@ void run_leveled(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   for (uint32_t i = 1; i < NS; ++i) {
     const uint32_t narrow = sets->levels[order[i - 1]], wide = sets->levels[order[i]];
     if (narrow & ~wide) {
-      out->status = XSP_L_NOT_CHAIN;
-      out->err_a = order[i - 1];
-      out->err_b = order[i];
-      return;
+      // reported, but per-set latencies are still computed (accurate_latency)
+      if (out->status == XSP_L_OK) {
+        out->status = XSP_L_NOT_CHAIN;
+        out->err_a = order[i - 1];
+        out->err_b = order[i];
+      }
     }
   }
-  if (NS < 2) {
+  if (NS < 2 && out->status == XSP_L_OK) {
     out->status = XSP_L_TOO_FEW;
     out->err_a = NS;
-    return;
   }
+  if (NS == 0) return;
   const uint32_t total_runs = sets->set_off[NS];
   uint32_t* hs = ctx->h<uint32_t>("l.sets_h", 2ull * NS + 2 + total_runs);
   uint32_t* htr = hs + 2 * NS + 1;
