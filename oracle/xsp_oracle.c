@@ -134,6 +134,7 @@ typedef struct {
   vu64 l_dur;
   vu32 k_launch, k_exec, k_mrow, k_name;
   vu64 k_dur;
+  vf64 k_occ;
   vu32 o_row;
   vu8 o_reason;
   vu32 a_row, a_coff, a_crow;
@@ -437,6 +438,7 @@ int xspo_correlate(const xsp_span_cols* c, const xsp_traces* tr, xsp_corr_out* o
               vu32_push(&A.k_mrow, mrow[x]);
               vu64_push(&A.k_dur, dur(c->begin_ns[x], c->end_ns[x]));
               vu32_push(&A.k_name, c->name_id[x]);
+              vf64_push(&A.k_occ, mrow[x] != NONE ? c->occupancy[mrow[x]] : 0.0);
             }
             ++q;
           }
@@ -506,6 +508,7 @@ int xspo_correlate(const xsp_span_cols* c, const xsp_traces* tr, xsp_corr_out* o
   out->kernel_metric_row = A.k_mrow.v;
   out->kernel_dur = A.k_dur.v;
   out->kernel_name = A.k_name.v;
+  out->kernel_occ = A.k_occ.v;
   out->orphan_row = A.o_row.v;
   out->orphan_reason = A.o_reason.v;
   out->amb_row = A.a_row.v;
@@ -518,7 +521,7 @@ void xspo_corr_free(xsp_corr_out* o) {
   void* ps[] = {o->trace_status, o->trace_err_row, o->trace_model_row, o->trace_layer_off,
                 o->trace_kernel_off, o->trace_orphan_off, o->trace_amb_off, o->layer_row,
                 o->layer_kernel_off, o->layer_dur, o->layer_attr_row, o->kernel_launch_row,
-                o->kernel_exec_row, o->kernel_metric_row, o->kernel_dur, o->kernel_name,
+                o->kernel_exec_row, o->kernel_metric_row, o->kernel_dur, o->kernel_name, o->kernel_occ,
                 o->orphan_row, o->orphan_reason, o->amb_row, o->amb_cand_off, o->amb_cand_row};
   for (size_t i = 0; i < sizeof(ps) / sizeof(ps[0]); ++i) free(ps[i]);
   memset(o, 0, sizeof(*o));
