@@ -22,6 +22,9 @@
 // Orphans, ambiguities and explicit-parent kernels are rare: they are appended
 // to exception lists and put into the reference's output order by radix sort.
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "ctx.h"
 #include "prims.cuh"
 
@@ -100,11 +103,21 @@ __global__ void k_trace_prep(const uint8_t* __restrict__ flags, const uint64_t* 
                              const uint64_t* __restrict__ off, uint32_t T,
                              uint32_t* __restrict__ model_row, uint64_t* __restrict__ mb,
                              uint64_t* __restrict__ me, uint64_t* __restrict__ msid,
-                             unsigned long long* __restrict__ err_key) {
+                             unsigned long long* __restrict__ err_key, uint64_t n, uint32_t tile_spans,
+                             uint32_t* __restrict__ tile_lo, uint32_t* __restrict__ tile_hi) {
   const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
   if (t >= T) return;
   const uint64_t lo = off[t], hi = off[t + 1];
+  if (lo < hi) {
+    // pass-1 tiles whose first / last span lies in this trace (trace_of semantics:
+    // the containing non-empty trace)
+    for (uint64_t b = (lo + tile_spans - 1) / tile_spans + lane; b * tile_spans < hi; b += 32) tile_lo[b] = t;
+    for (uint64_t b = lo / tile_spans + lane; b * tile_spans < hi; b += 32) {
+      const uint64_t last = min((b + 1) * tile_spans, n) - 1;
+      if (last >= lo && last < hi) tile_hi[b] = t;
+    }
+  }
   uint64_t found = ~0ull;
   for (uint64_t base = lo; base < hi; base += 32) {
     uint64_t i = base + lane;
@@ -177,22 +190,49 @@ __device__ __forceinline__ Full full_identity() {
   return f;
 }
 
-__device__ __forceinline__ void store_full(Full* dst, const Full& v) {
-  const uint4* s = reinterpret_cast<const uint4*>(&v);
-  uint4* d = reinterpret_cast<uint4*>(dst);
-  __stcg(d + 0, s[0]);
-  __stcg(d + 1, s[1]);
-  __stcg(d + 2, s[2]);
+// Look-back tile descriptor: the 12 payload words of a Full in four 16-byte
+// words, each led by a status word (1 = tile aggregate, 2 = inclusive prefix).
+// A reader validates every 16-byte word by its own status, so one relaxed
+// vector-load round trip returns status and value together (no fences); a
+// 16-byte aligned vector access is observed whole. Slot 2t holds tile t's
+// aggregate, slot 2t+1 its inclusive prefix; both are zeroed per call.
+struct __align__(16) TileDesc {
+  uint4 w[4];
+};
+constexpr uint32_t DESC_AGG = 1, DESC_INC = 2;
+
+__device__ __forceinline__ void st_relaxed_v4(uint4* p, uint4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
-__device__ __forceinline__ Full load_full(const Full* src) {
-  Full v;
-  uint4* d = reinterpret_cast<uint4*>(&v);
-  const uint4* s = reinterpret_cast<const uint4*>(src);
-  d[0] = __ldcg(s + 0);
-  d[1] = __ldcg(s + 1);
-  d[2] = __ldcg(s + 2);
+__device__ __forceinline__ uint4 ld_relaxed_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
   return v;
 }
+__device__ __forceinline__ void desc_store(TileDesc* d, const Full& v, uint32_t status) {
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) st_relaxed_v4(d->w + q, make_uint4(status, s[3 * q], s[3 * q + 1], s[3 * q + 2]));
+}
+// true when all four words carry `status`; v is then the published value
+__device__ __forceinline__ bool desc_unpack(const uint4 (&w)[4], uint32_t status, Full& v) {
+  uint32_t* d = reinterpret_cast<uint32_t*>(&v);
+  bool ok = true;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    ok &= w[q].x == status;
+    d[3 * q] = w[q].y;
+    d[3 * q + 1] = w[q].z;
+    d[3 * q + 2] = w[q].w;
+  }
+  return ok;
+}
+
 __device__ __forceinline__ Full shfl_full(const Full& v, int src) {
   Full u;
   const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
@@ -202,66 +242,23 @@ __device__ __forceinline__ Full shfl_full(const Full& v, int src) {
   return u;
 }
 
-// Per-chunk (32 spans, one per lane) segmented max-scan over placed-layer ends.
-struct Chunk {
-  uint32_t P, H;  // ballots: placed layers, trace heads
-  int seg;        // highest head lane <= this lane, -1 if none
-  uint64_t w;     // end+1 if placed else 0
-  uint64_t exM;   // max w over lanes [max(seg,0), lane)
-  uint64_t incM;  // max w over lanes [max(seg,0), lane]
-};
-
-__device__ __forceinline__ Chunk chunk_scan(bool placed, bool head, uint64_t e) {
-  Chunk k;
-  const uint32_t lane = lane_id();
-  k.P = __ballot_sync(0xffffffffu, placed);
-  k.H = __ballot_sync(0xffffffffu, head);
-  const uint32_t hle = k.H & (lanemask_lt() | (1u << lane));
-  k.seg = hle ? 31 - __clz(hle) : -1;
-  k.w = placed ? (e == ~0ull ? e : e + 1) : 0;
-  uint64_t x = k.w;
-  if (k.P) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if ((int)lane - o >= k.seg && (int)lane >= o) x = max64(x, y);
-    }
-  }
-  k.incM = x;
-  uint64_t p = __shfl_up_sync(0xffffffffu, x, 1);
-  k.exM = ((int)lane - 1 >= k.seg && lane >= 1) ? p : 0;
-  return k;
-}
-
-__device__ __forceinline__ Full chunk_agg(const Chunk& k, uint32_t bm, uint32_t bl, uint32_t bk,
-                                          uint32_t bx) {
-  Full f;
-  f.c = __popc(k.P);
-  f.head = k.H != 0;
-  f.c_metric = __popc(bm);
-  f.c_lay = __popc(bl);
-  f.c_kl = __popc(bk);
-  f.c_ex = __popc(bx);
-  const int s31 = k.H ? 31 - __clz(k.H) : 0;  // start of the last segment
-  const uint32_t lastP = k.P & (0xffffffffu << s31);
-  const int q = lastP ? 31 - __clz(lastP) : 0;
-  const uint64_t qw = __shfl_sync(0xffffffffu, k.w, q);
-  const uint64_t qex = __shfl_sync(0xffffffffu, k.exM, q);
-  const uint64_t run = __shfl_sync(0xffffffffu, k.incM, 31);
-  f.last_end1 = lastP ? qw : 0;
-  f.last_M1 = lastP ? qex : 0;
-  f.run_M1 = run;
-  return f;
-}
-
-constexpr int P1_WARPS = 8;
-constexpr int P1_CHUNKS = 8;
-constexpr int P1_SUB = P1_CHUNKS * 32;
-constexpr int P1_TILE = P1_WARPS * P1_SUB;
-constexpr int P1_TCACHE = 32;  // traces of a tile cached in shared memory
+// Pass-1 work decomposition: a tile of 2048 timeline-consecutive spans per CTA,
+// 8 consecutive spans per thread. Each thread folds its spans serially into a
+// `Full` aggregate (phase 1), one warp-level scan of the 32 thread aggregates
+// plus the block's decoupled look-back gives every thread its exclusive prefix,
+// and the thread re-walks its spans with that running state (phase 3) emitting
+// outputs with plain counters.
+constexpr int P1_CWARPS = 7;  // compute warps; warp 7 runs the look-back
+constexpr int P1_THREADS = (P1_CWARPS + 1) * 32;
+constexpr int P1_ITEMS = 8;
+constexpr int P1_SUB = P1_ITEMS * 32;  // spans per compute warp
+constexpr int P1_TILE = P1_CWARPS * P1_SUB;
+constexpr int P1_ROWS = P1_TILE / 16;  // 128-byte rows of 16 u64 per column
+static_assert(P1_TILE % 128 == 0, "swizzled columns need 1024-byte aligned bases");
+constexpr int P1_TCACHE = 32;          // traces of a tile cached in shared memory
 
 struct P1Args {
-  int bulk;  // all columns 16-byte aligned: stage full tiles with cp.async.bulk
+  int bulk;  // full tiles staged by TMA tensor copies (columns 16-byte aligned)
   int parents_only;
   const uint64_t* span_id;
   const uint8_t* flags;
@@ -278,9 +275,10 @@ struct P1Args {
   const uint64_t* me;
   const uint64_t* msid;
   uint32_t* tile_ticket;
-  uint32_t* tile_flag;
-  Full* tile_agg;
-  Full* tile_inc;
+  const uint32_t* tile_lo;  // trace of each tile's first span (k_trace_prep)
+  const uint32_t* tile_hi;  // trace of each tile's last span
+  TileDesc* tile_desc;  // 2 slots per tile (aggregate, inclusive)
+  unsigned long long* dbg;  // optional per-tile timeline (XSP_P1_TRACE)
   uint32_t* unsorted;
   unsigned long long* err_key;
   uint32_t* layer_row;
@@ -300,14 +298,23 @@ struct P1Args {
   uint32_t* pend_count;
 };
 
+// TMA descriptors of the four u64 columns, each viewed as a 2-D tensor of
+// [n/16 rows][16 spans] and copied as 128-row boxes with the 128-byte swizzle.
+struct P1Maps {
+  CUtensorMap begin, end, cid, parent;
+};
+
 struct TraceCache {
   uint64_t off[P1_TCACHE + 1];
   uint64_t mb[P1_TCACHE], me[P1_TCACHE], msid[P1_TCACHE];
   uint32_t model_row[P1_TCACHE], levels[P1_TCACHE];
 };
 
-// Tile staging buffer (dynamic shared memory): the tile's span columns, brought
-// in by one bulk asynchronous copy per column (TMA engine, cp.async.bulk).
+// Tile staging buffer (dynamic shared memory, 1024-byte aligned). The u64
+// columns are stored in the TMA SWIZZLE_128B pattern: span j lives in row j/16,
+// 16-byte chunk ((j/2) % 8) ^ (row % 8). A thread's 8 consecutive spans are four
+// 16-byte chunks whose swizzled addresses fall in distinct banks across every
+// quarter-warp, so the per-thread serial walk reads shared memory conflict-free.
 struct TileSmem {
   uint64_t begin[P1_TILE];
   uint64_t end[P1_TILE];
@@ -315,7 +322,11 @@ struct TileSmem {
   uint64_t parent[P1_TILE];
   uint8_t flags[P1_TILE];
 };
-constexpr size_t P1_SMEM = sizeof(TileSmem);
+constexpr size_t P1_SMEM = sizeof(TileSmem) + 1024;  // + alignment slack
+
+__host__ __device__ __forceinline__ uint32_t sw128(uint32_t j) {
+  return (j & ~15u) | (((((j >> 1) & 7u) ^ ((j >> 4) & 7u))) << 1) | (j & 1u);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -344,147 +355,151 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_g2s_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+// two consecutive spans (j even) of a swizzled column
+__device__ __forceinline__ void ld_pair(const uint64_t* col, uint32_t j, uint64_t& v0, uint64_t& v1) {
+  const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(col + sw128(j));
+  v0 = p.x;
+  v1 = p.y;
+}
 
-__global__ void __launch_bounds__(P1_WARPS * 32, 3) k_pass1(P1Args a) {
-  extern __shared__ __align__(128) unsigned char p1_dyn[];
-  TileSmem& sm = *reinterpret_cast<TileSmem*>(p1_dyn);
+// Per-trace attributes a thread needs while walking its spans.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct TraceAttrs {
+  uint64_t cur, next;  // offsets of the current trace and the one after it
+  uint64_t mb, me, msid;
+  uint32_t model, levels;
+};
+
+__device__ __forceinline__ void bar_sync_compute() {
+  asm volatile("bar.sync 1, %0;" ::"n"(P1_CWARPS * 32) : "memory");
+}
+
+__global__ void __launch_bounds__(P1_THREADS, 3) k_pass1(P1Args a, const __grid_constant__ P1Maps maps) {
+  extern __shared__ unsigned char p1_dyn[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(p1_dyn + ((1024u - (smem_u32(p1_dyn) & 1023u)) & 1023u));
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_tlo, s_thi;
-  __shared__ Full s_wagg[P1_WARPS];
-  __shared__ Full s_prefix;
+  __shared__ Full s_wagg[P1_CWARPS];
+  __shared__ Full s_prefix, s_agg;
   __shared__ TraceCache tc;
   __shared__ __align__(8) uint64_t s_bar;
 
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const bool lbw = warp == P1_CWARPS;  // the look-back warp
+  const uint64_t t_start = a.dbg ? gtimer() : 0;
   if (threadIdx.x == 0) {
     const uint32_t tile = atomicAdd(a.tile_ticket, 1u);
     const uint64_t tb = (uint64_t)tile * P1_TILE;
     uint64_t last = tb + P1_TILE;
     if (last > a.n) last = a.n;
-    const uint32_t lo = trace_of(a.off, 0, a.T, tb);
     s_tile = tile;
-    s_tlo = lo;
-    s_thi = trace_of(a.off, lo, a.T, last - 1) + 1;
-    // stage the tile: one bulk copy per column (full, aligned tiles)
     if (a.bulk && last - tb == P1_TILE) {
       mbar_init(&s_bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       mbar_expect_tx(&s_bar, P1_TILE * (4 * 8 + 1));
-      bulk_g2s(sm.begin, a.begin + tb, P1_TILE * 8, &s_bar);
-      bulk_g2s(sm.end, a.end + tb, P1_TILE * 8, &s_bar);
-      bulk_g2s(sm.cid, a.cid + tb, P1_TILE * 8, &s_bar);
-      bulk_g2s(sm.parent, a.parent + tb, P1_TILE * 8, &s_bar);
+      const int y = (int)(tb / 16);
+      tma_g2s_2d(sm.begin, &maps.begin, 0, y, &s_bar);
+      tma_g2s_2d(sm.end, &maps.end, 0, y, &s_bar);
+      tma_g2s_2d(sm.cid, &maps.cid, 0, y, &s_bar);
+      tma_g2s_2d(sm.parent, &maps.parent, 0, y, &s_bar);
       bulk_g2s(sm.flags, a.flags + tb, P1_TILE, &s_bar);
     }
+    s_tlo = __ldg(a.tile_lo + tile);
+    s_thi = __ldg(a.tile_hi + tile) + 1;
   }
   __syncthreads();
   const uint32_t tile = s_tile, tlo = s_tlo, thi = s_thi;
   const uint64_t tile_base = (uint64_t)tile * P1_TILE;
   const uint32_t tile_n = (uint32_t)min((uint64_t)P1_TILE, a.n - tile_base);
-  const uint32_t ncache = min(thi - tlo, (uint32_t)P1_TCACHE);
-  if (threadIdx.x <= ncache) tc.off[threadIdx.x] = a.off[tlo + threadIdx.x];
-  if (threadIdx.x < ncache) {
-    const uint32_t t = tlo + threadIdx.x;
-    tc.mb[threadIdx.x] = a.mb[t];
-    tc.me[threadIdx.x] = a.me[t];
-    tc.msid[threadIdx.x] = a.msid[t];
-    tc.model_row[threadIdx.x] = a.model_row[t];
-    tc.levels[threadIdx.x] = a.levels[t];
-  }
-  if (a.bulk && tile_n == P1_TILE) {
-    mbar_wait(&s_bar, 0);
-  } else {
-    for (uint32_t j = threadIdx.x; j < P1_TILE; j += blockDim.x) {
-      const bool v = j < tile_n;
-      const uint64_t i = tile_base + j;
-      sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
-      sm.begin[j] = v ? a.begin[i] : 0;
-      sm.end[j] = v ? a.end[i] : 0;
-      sm.cid[j] = v ? a.cid[i] : 0;
-      sm.parent[j] = v ? a.parent[i] : 0;
-    }
-  }
-  __syncthreads();
   const bool cached = thi - tlo <= (uint32_t)P1_TCACHE;
-  const uint32_t wj = warp * P1_SUB;  // warp's first local index
+  const uint32_t j0 = threadIdx.x * P1_ITEMS;  // compute thread's first local index
+  const uint64_t i0 = tile_base + j0;
+  if (a.dbg && threadIdx.x == 0) a.dbg[tile * 16 + 0] = t_start;
 
-  // trace index of span i (relative to tlo)
-  auto trace_rel = [&](uint64_t i) -> uint32_t {
+  auto t_off = [&](uint32_t r) -> uint64_t { return cached ? tc.off[r] : __ldg(a.off + tlo + r); };
+  auto load_attrs = [&](uint32_t r, TraceAttrs& ta) {
+    ta.cur = t_off(r);
+    ta.next = t_off(r + 1);
     if (cached) {
-      uint32_t lo = 0, hi = thi - tlo;
-      while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (tc.off[mid] <= i) lo = mid; else hi = mid;
-      }
-      return lo;
-    }
-    return trace_of(a.off, tlo, thi, i) - tlo;
-  };
-  auto t_off = [&](uint32_t r) { return cached ? tc.off[r] : a.off[tlo + r]; };
-  auto t_model = [&](uint32_t r) { return cached ? tc.model_row[r] : a.model_row[tlo + r]; };
-  // layer placement under the model span (correlator.cpp:169-194)
-  auto placed_in = [&](uint8_t f, uint64_t b, uint64_t e, uint64_t par, uint32_t r) -> bool {
-    if (t_model(r) == kNone) return false;
-    if (f & XSP_F_PARENT) return par == (cached ? tc.msid[r] : a.msid[tlo + r]);
-    return (cached ? tc.mb[r] : a.mb[tlo + r]) <= b && e <= (cached ? tc.me[r] : a.me[tlo + r]);
-  };
-
-  // ---- phase 1: warp aggregate ----------------------------------------------
-  Full wagg = full_identity();
-#pragma unroll 2
-  for (int c = 0; c < P1_CHUNKS; ++c) {
-    const uint32_t j = wj + c * 32 + lane;
-    const uint64_t i = tile_base + j;
-    const bool v = j < tile_n;
-    const uint8_t f = sm.flags[j];
-    const uint32_t r = v ? trace_rel(i) : 0;
-    const bool head = v && t_off(r) == i;
-    const bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
-    const uint64_t e = sm.end[j];
-    const bool placed = is_layer && f_kind(f) == XSP_KIND_SYNC && placed_in(f, sm.begin[j], e, sm.parent[j], r);
-    const bool kl = v && (is_kernel_launch(f) || is_sync_kernel(f));
-    const bool ex = v && is_exec(f) && (f & XSP_F_CID);
-    const bool met = v && (f & XSP_F_METRICS);
-    const Chunk k = chunk_scan(placed, head, e);
-    wagg = full_combine(wagg, chunk_agg(k, __ballot_sync(0xffffffffu, met), __ballot_sync(0xffffffffu, is_layer),
-                                        __ballot_sync(0xffffffffu, kl), __ballot_sync(0xffffffffu, ex)));
-  }
-  if (lane == 0) s_wagg[warp] = wagg;
-  __syncthreads();
-
-  // ---- phase 2: tile aggregate + warp-parallel decoupled look-back ----------
-  if (warp == 0) {
-    Full agg = s_wagg[0];
-    for (int w = 1; w < P1_WARPS; ++w) agg = full_combine(agg, s_wagg[w]);
-    Full prefix = full_identity();
-    if (tile == 0) {
-      if (lane == 0) {
-        store_full(a.tile_inc + tile, agg);
-        __threadfence();
-        atomicExch(a.tile_flag + tile, 2u);
-      }
+      ta.mb = tc.mb[r];
+      ta.me = tc.me[r];
+      ta.msid = tc.msid[r];
+      ta.model = tc.model_row[r];
+      ta.levels = tc.levels[r];
     } else {
-      if (lane == 0) {
-        store_full(a.tile_agg + tile, agg);
-        __threadfence();
-        atomicExch(a.tile_flag + tile, 1u);
-      }
-      // window of 32 predecessors per step; lane l looks at tile base - l
-      Full acc = full_identity();
+      const uint32_t t = tlo + r;
+      ta.mb = __ldg(a.mb + t);
+      ta.me = __ldg(a.me + t);
+      ta.msid = __ldg(a.msid + t);
+      ta.model = __ldg(a.model_row + t);
+      ta.levels = __ldg(a.levels + t);
+    }
+  };
+  // layer placement under the model span (correlator.cpp:169-194)
+  auto placed_in = [](const TraceAttrs& ta, uint8_t f, uint64_t b, uint64_t e, uint64_t par) -> bool {
+    if (ta.model == kNone) return false;
+    if (f & XSP_F_PARENT) return par == ta.msid;
+    return ta.mb <= b && e <= ta.me;
+  };
+
+  uint32_t r0 = 0;
+  uint64_t fl8 = 0;
+  Full lane_ex;  // exclusive prefix of the thread within its warp
+  if (lbw) {
+    // ---- look-back warp: exclusive prefix over the predecessor tiles, polled
+    // while the compute warps run phase 1. Window of 32 predecessors per step;
+    // lane l looks at tile base - l.
+    Full prefix = full_identity();
+    if (tile > 0) {
       int64_t base = (int64_t)tile - 1;
       for (;;) {
         const int64_t jt = base - lane;
-        uint32_t fl = 2;  // before tile 0: identity prefix
-        if (jt >= 0) {
-          do {
-            fl = *((volatile uint32_t*)(a.tile_flag + jt));
-          } while (fl == 0);
-        }
-        __threadfence();
-        const uint32_t incl = __ballot_sync(0xffffffffu, fl == 2);
-        const uint32_t stop = incl ? (__ffs(incl) - 1) : 31;  // closest inclusive prefix
         Full v = full_identity();
-        if (jt >= 0 && lane <= stop) v = (fl == 2) ? load_full(a.tile_inc + jt) : load_full(a.tile_agg + jt);
+        bool is_inc = true;  // before tile 0: identity prefix
+        if (jt >= 0) {
+          const TileDesc* dj = a.tile_desc + 2 * jt;
+          // first attempt reads both slots whole (one round trip when the tile
+          // has published); while spinning, poll only the leading status words
+          uint4 wi[4], wa[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            wi[q] = ld_relaxed_v4(dj[1].w + q);
+            wa[q] = ld_relaxed_v4(dj[0].w + q);
+          }
+          for (;;) {
+            if (desc_unpack(wi, DESC_INC, v)) break;
+            if (desc_unpack(wa, DESC_AGG, v)) {
+              is_inc = false;
+              break;
+            }
+            if (a.dbg) atomicAdd(a.dbg + tile * 16 + 7, 1ull);
+            __nanosleep(128);
+            wi[0] = ld_relaxed_v4(dj[1].w);
+            wa[0] = ld_relaxed_v4(dj[0].w);
+            if (wi[0].x == DESC_INC) {
+#pragma unroll
+              for (int q = 1; q < 4; ++q) wi[q] = ld_relaxed_v4(dj[1].w + q);
+            } else if (wa[0].x == DESC_AGG) {
+#pragma unroll
+              for (int q = 1; q < 4; ++q) wa[q] = ld_relaxed_v4(dj[0].w + q);
+            }
+          }
+        }
+        const uint32_t incl = __ballot_sync(0xffffffffu, is_inc);
+        const uint32_t stop = incl ? (__ffs(incl) - 1) : 31;  // closest inclusive prefix
+        if (lane > stop) v = full_identity();
         // ordered tree reduction: higher lanes hold older tiles
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -495,114 +510,232 @@ __global__ void __launch_bounds__(P1_WARPS * 32, 3) k_pass1(P1Args a) {
           for (int w = 0; w < 12; ++w) d[w] = __shfl_down_sync(0xffffffffu, s[w], o);
           if ((lane & (2 * o - 1)) == 0) v = full_combine(u, v);
         }
-        acc = full_combine(shfl_full(v, 0), acc);
+        prefix = full_combine(shfl_full(v, 0), prefix);
         if (incl) break;
+        if (a.dbg && lane == 0) a.dbg[tile * 16 + 6] += 1;
         base -= 32;
-      }
-      prefix = acc;
-      if (lane == 0) {
-        store_full(a.tile_inc + tile, full_combine(prefix, agg));
-        __threadfence();
-        atomicExch(a.tile_flag + tile, 2u);
       }
     }
     if (lane == 0) s_prefix = prefix;
+    if (a.dbg && lane == 0) a.dbg[tile * 16 + 5] = gtimer();
+  } else {
+    const uint32_t ncache = min(thi - tlo, (uint32_t)P1_TCACHE);
+    if (threadIdx.x <= ncache) tc.off[threadIdx.x] = a.off[tlo + threadIdx.x];
+    if (threadIdx.x < ncache) {
+      const uint32_t t = tlo + threadIdx.x;
+      tc.mb[threadIdx.x] = a.mb[t];
+      tc.me[threadIdx.x] = a.me[t];
+      tc.msid[threadIdx.x] = a.msid[t];
+      tc.model_row[threadIdx.x] = a.model_row[t];
+      tc.levels[threadIdx.x] = a.levels[t];
+    }
+    if (a.bulk && tile_n == P1_TILE) {
+      mbar_wait(&s_bar, 0);
+    } else {
+      for (uint32_t j = threadIdx.x; j < P1_TILE; j += P1_CWARPS * 32) {
+        const bool v = j < tile_n;
+        const uint64_t i = tile_base + j;
+        const uint32_t s = sw128(j);
+        sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
+        sm.begin[s] = v ? a.begin[i] : 0;
+        sm.end[s] = v ? a.end[i] : 0;
+        sm.cid[s] = v ? a.cid[i] : 0;
+        sm.parent[s] = v ? a.parent[i] : 0;
+      }
+    }
+    bar_sync_compute();
+    if (a.dbg && threadIdx.x == 0) a.dbg[tile * 16 + 1] = gtimer();
+    // trace of the thread's first span (relative to tlo); later spans walk forward
+    if (j0 < tile_n) {
+      uint32_t lo = 0, hi = thi - tlo;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (t_off(mid) <= i0) lo = mid; else hi = mid;
+      }
+      r0 = lo;
+    }
+    fl8 = *reinterpret_cast<const uint64_t*>(sm.flags + j0);
+
+    // ---- phase 1: thread aggregate (serial over 8 spans) ----------------------
+    Full th = full_identity();
+    {
+      TraceAttrs ta;
+      uint32_t r = r0;
+      load_attrs(r, ta);
+#pragma unroll
+      for (int p = 0; p < P1_ITEMS / 2; ++p) {
+        uint64_t bb[2], ee[2], pp[2];
+        ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
+        ld_pair(sm.end, j0 + 2 * p, ee[0], ee[1]);
+    ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
+        ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = 2 * p + h;
+          const uint64_t i = i0 + k;
+          const bool v = j0 + k < tile_n;
+          const uint8_t f = (uint8_t)(fl8 >> (8 * k));
+          if (!v) continue;
+          if (i >= ta.next) {
+            do { ++r; } while (t_off(r + 1) <= i);
+            load_attrs(r, ta);
+          }
+          if (ta.cur == i) {  // trace head: new segment
+            th.head = 1;
+            th.last_end1 = th.last_M1 = th.run_M1 = 0;
+          }
+          const bool is_layer = f_level(f) == XSP_LEVEL_LAYER;
+          const uint64_t e = ee[h];
+          if (is_layer && f_kind(f) == XSP_KIND_SYNC && placed_in(ta, f, bb[h], e, pp[h])) {
+            const uint64_t w = e == ~0ull ? e : e + 1;
+            th.last_M1 = th.run_M1;
+            th.last_end1 = w;
+            th.run_M1 = max64(th.run_M1, w);
+            ++th.c;
+          }
+          th.c_lay += is_layer;
+          th.c_metric += (f & XSP_F_METRICS) != 0;
+          th.c_kl += is_kernel_launch(f) || is_sync_kernel(f);
+          th.c_ex += is_exec(f) && (f & XSP_F_CID);
+        }
+      }
+    }
+    // warp-inclusive scan of the thread aggregates (lanes in span order)
+    Full inc = th;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      Full u;
+      const uint32_t* s = reinterpret_cast<const uint32_t*>(&inc);
+      uint32_t* d = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+      for (int w = 0; w < 12; ++w) d[w] = __shfl_up_sync(0xffffffffu, s[w], o);
+      if (lane >= (uint32_t)o) inc = full_combine(u, inc);
+    }
+    if (lane == 31) s_wagg[warp] = inc;
+    {
+      const uint32_t* s = reinterpret_cast<const uint32_t*>(&inc);
+      uint32_t* d = reinterpret_cast<uint32_t*>(&lane_ex);
+#pragma unroll
+      for (int w = 0; w < 12; ++w) d[w] = __shfl_up_sync(0xffffffffu, s[w], 1);
+      if (lane == 0) lane_ex = full_identity();
+    }
+    bar_sync_compute();
+    if (threadIdx.x == 0) {
+      // publish the tile aggregate (tile 0: its inclusive prefix) for the successors
+      Full agg = s_wagg[0];
+      for (int w = 1; w < P1_CWARPS; ++w) agg = full_combine(agg, s_wagg[w]);
+      desc_store(a.tile_desc + 2 * tile + (tile == 0 ? 1 : 0), agg, tile == 0 ? DESC_INC : DESC_AGG);
+      s_agg = agg;
+      if (a.dbg) a.dbg[tile * 16 + 2] = gtimer();
+    }
   }
   __syncthreads();
+  if (lbw) {
+    if (lane == 0 && tile > 0) desc_store(a.tile_desc + 2 * tile + 1, full_combine(s_prefix, s_agg), DESC_INC);
+    return;
+  }
+  if (a.dbg && threadIdx.x == 0) a.dbg[tile * 16 + 3] = gtimer();
 
   Full carry = s_prefix;
   for (uint32_t w = 0; w < warp; ++w) carry = full_combine(carry, s_wagg[w]);
+  carry = full_combine(carry, lane_ex);
 
-  // ---- phase 3: per-span outputs -------------------------------------------
-  const uint32_t lt = lanemask_lt();
-  for (int c = 0; c < P1_CHUNKS; ++c) {
-    const uint32_t j = wj + c * 32 + lane;
-    const uint64_t i = tile_base + j;
-    const bool v = j < tile_n;
-    const uint8_t f = sm.flags[j];
-    const uint64_t b = sm.begin[j];
-    const uint64_t e = sm.end[j];
-    const uint32_t r = v ? trace_rel(i) : 0;
-    const uint32_t t = tlo + r;
-    const bool head = v && t_off(r) == i;
-    const bool is_layer = v && f_level(f) == XSP_LEVEL_LAYER;
-    const bool layer_sync = is_layer && f_kind(f) == XSP_KIND_SYNC;
-    const bool placed = layer_sync && placed_in(f, b, e, sm.parent[j], r);
-    const bool sync = v && is_sync_kernel(f);
-    const bool kl = v && (is_kernel_launch(f) || sync);
-    const bool exe = v && is_exec(f);
-    const bool has_cid = f & XSP_F_CID;
-    const bool ex = exe && has_cid;
-    const bool met = v && (f & XSP_F_METRICS);
-
-    const uint32_t bm = __ballot_sync(0xffffffffu, met);
-    const uint32_t bl = __ballot_sync(0xffffffffu, is_layer);
-    const uint32_t bk = __ballot_sync(0xffffffffu, kl);
-    const uint32_t bx = __ballot_sync(0xffffffffu, ex);
-    const Chunk k = chunk_scan(placed, head, e);
-    const uint32_t g_ex = carry.c + __popc(k.P & lt);
-
-    // timeline order (begin_ns, rank, span_id) within the trace (span.hpp:161-163)
-    if (v && !head && i > 0) {
-      const uint64_t pb = j > 0 ? sm.begin[j - 1] : __ldg(a.begin + i - 1);
-      if (pb >= b) {
+  // ---- phase 3: per-span outputs (serial over the thread's 8 spans) ----------
+  if (j0 >= tile_n) return;
+  TraceAttrs ta;
+  uint32_t r = r0;
+  load_attrs(r, ta);
+  uint32_t g = carry.c, c_metric = carry.c_metric, c_lay = carry.c_lay, c_kl = carry.c_kl, c_ex = carry.c_ex;
+  uint64_t lastE = carry.last_end1, lastM = carry.last_M1, runM = carry.run_M1;
+  // predecessor of the first span, for the timeline-order check
+  uint64_t pb = 0;
+  uint8_t pf = 0;
+  if (i0 > 0) {
+    pb = j0 > 0 ? sm.begin[sw128(j0 - 1)] : __ldg(a.begin + i0 - 1);
+    pf = j0 > 0 ? sm.flags[j0 - 1] : __ldg(a.flags + i0 - 1);
+  }
+#pragma unroll
+  for (int p = 0; p < P1_ITEMS / 2; ++p) {
+    uint64_t bb[2], ee[2], pp[2], cc[2];
+    ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
+    ld_pair(sm.end, j0 + 2 * p, ee[0], ee[1]);
+    ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
+    ld_pair(sm.cid, j0 + 2 * p, cc[0], cc[1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = 2 * p + h;
+      const uint64_t i = i0 + k;
+      if (j0 + k >= tile_n) break;
+      const uint8_t f = (uint8_t)(fl8 >> (8 * k));
+      const uint64_t b = bb[h], e = ee[h];
+      if (i >= ta.next) {
+        do { ++r; } while (t_off(r + 1) <= i);
+        load_attrs(r, ta);
+      }
+      const uint32_t t = tlo + r;
+      const bool head = ta.cur == i;
+      if (head) {
+        lastE = lastM = runM = 0;
+        int64_t tt = t;
+        do {
+          a.t_layer_off[tt] = g;
+          a.t_kl_off[tt] = c_kl;
+          a.t_ex_off[tt] = c_ex;
+          --tt;
+        } while (tt >= 0 && __ldg(a.off + tt) == i);
+      } else if (i > 0 && pb >= b) {
+        // timeline order (begin_ns, rank, span_id) within the trace (span.hpp:161-163)
         bool bad = pb > b;
         if (!bad) {
-          const uint8_t pf = j > 0 ? sm.flags[j - 1] : __ldg(a.flags + i - 1);
           const uint32_t l0 = f_level(pf), l1 = f_level(f);
-          const uint32_t r0 = l0 >= 2 ? 3 : l0 + 1, r1 = l1 >= 2 ? 3 : l1 + 1;
-          bad = r0 > r1 || (r0 == r1 && __ldg(a.span_id + i - 1) > __ldg(a.span_id + i));
+          const uint32_t r0_ = l0 >= 2 ? 3 : l0 + 1, r1_ = l1 >= 2 ? 3 : l1 + 1;
+          bad = r0_ > r1_ || (r0_ == r1_ && __ldg(a.span_id + i - 1) > __ldg(a.span_id + i));
         }
         if (bad) atomicOr(a.unsorted, 1u);
       }
-    }
+      pb = b;
+      pf = f;
 
-    // (end+1, M+1) of the last placed layer before each lane in its segment
-    const uint32_t segmask = k.seg >= 0 ? (0xffffffffu << k.seg) : 0xffffffffu;
-    const uint32_t pq = k.P & lt & segmask;
-    const int q = pq ? 31 - __clz(pq) : 0;
-    const uint64_t qw = __shfl_sync(0xffffffffu, k.w, q);
-    const uint64_t qex = __shfl_sync(0xffffffffu, k.exM, q);
-
-    if (v) {
       // trace errors raised while walking the bundle (correlator.cpp:146-158)
-      if (is_model_span(f) && (uint32_t)i != t_model(r))
+      if (is_model_span(f) && (uint32_t)i != ta.model)
         atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_MULTI_MODEL);
-      if (f_level(f) >= XSP_LEVEL_KERNEL &&
-          !((cached ? tc.levels[r] : a.levels[t]) & (1u << XSP_LEVEL_LAYER)))
+      if (f_level(f) >= XSP_LEVEL_KERNEL && !(ta.levels & (1u << XSP_LEVEL_LAYER)))
         atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_SKIP_LEVEL);
 
-      if (is_layer) {
-        const uint32_t l_ex = carry.c_lay + __popc(bl & lt);
-        if (layer_sync && placed) {
-          a.layer_row[g_ex] = (uint32_t)i;
-          a.layer_dur[g_ex] = clamp_dur(b, e);
-          a.layer_attr_row[g_ex] = l_ex;
+      const bool met = (f & XSP_F_METRICS) != 0;
+      const uint32_t mrow = met ? c_metric : kNone;
+      c_metric += met;
+      if (f_level(f) == XSP_LEVEL_LAYER) {
+        const bool layer_sync = f_kind(f) == XSP_KIND_SYNC;
+        if (layer_sync && placed_in(ta, f, b, e, pp[h])) {
+          a.layer_row[g] = (uint32_t)i;
+          a.layer_dur[g] = clamp_dur(b, e);
+          a.layer_attr_row[g] = c_lay;
+          ++g;
+          const uint64_t w = e == ~0ull ? e : e + 1;
+          lastM = runM;
+          lastE = w;
+          runM = max64(runM, w);
         } else {
           emit_orphan(a.orph, t, CAT_LAYER, i, (uint32_t)i,
                       !layer_sync ? XSP_O_LAYER_NON_SYNC
                                   : ((f & XSP_F_PARENT) ? XSP_O_LAYER_BAD_PARENT : XSP_O_LAYER_OUTSIDE_MODEL));
         }
+        ++c_lay;
       }
-      if (kl) {
-        const uint32_t k_ex = carry.c_kl + __popc(bk & lt);
+      const bool sync = is_sync_kernel(f);
+      const bool has_cid = (f & XSP_F_CID) != 0;
+      if (is_kernel_launch(f) || sync) {
+        const uint32_t k_ex = c_kl++;
         uint32_t par;
         if (f & XSP_F_PARENT) {
           par = PAR_PENDING;
           a.pend_kl[atomicAdd(a.pend_count, 1u)] = k_ex;
         } else {
-          uint64_t jend1 = 0, jM1 = 0;
-          if (pq) {
-            jend1 = qw;
-            jM1 = k.seg >= 0 ? qex : max64(carry.run_M1, qex);
-          } else if (k.seg < 0) {
-            jend1 = carry.last_end1;
-            jM1 = carry.last_M1;
-          }
-          const bool in_j = jend1 > e;  // end_j >= e (ends stored +1)
-          const bool in_m = jM1 > e;    // an earlier layer has end >= e
+          const bool in_j = lastE > e;  // end_j >= e (ends stored +1)
+          const bool in_m = lastM > e;  // an earlier layer has end >= e
           if (in_j && !in_m) {
-            par = g_ex - 1;
+            par = g - 1;
           } else if (!in_j && !in_m) {
             par = PAR_ORPHAN;
             emit_orphan(a.orph, t, CAT_KERNEL, i, (uint32_t)i, XSP_O_KERNEL_NO_LAYER);
@@ -611,49 +744,43 @@ __global__ void __launch_bounds__(P1_WARPS * 32, 3) k_pass1(P1Args a) {
             par = PAR_AMBIG;
             const uint32_t s = atomicAdd(a.amb_count, 1u);
             a.amb_kl[s] = k_ex;
-            a.amb_gx[s] = g_ex;
+            a.amb_gx[s] = g;
           }
         }
         KlEnt ent;
         ent.row = (uint32_t)i;
         ent.parent = par;
-        ent.cid = has_cid ? sm.cid[j] : 0;
+        ent.cid = has_cid ? cc[h] : 0;
         a.kl[k_ex] = ent;
-        if (sync) a.kl_mrow[k_ex] = met ? carry.c_metric + __popc(bm & lt) : kNone;
+        if (sync) a.kl_mrow[k_ex] = mrow;
       }
-      if (exe) {
-        if (ex) {
+      if (is_exec(f)) {
+        if (has_cid) {
           ExEnt ent;
           ent.row = (uint32_t)i;
-          ent.mrow = met ? carry.c_metric + __popc(bm & lt) : kNone;
-          ent.cid = sm.cid[j];
-          a.ex[carry.c_ex + __popc(bx & lt)] = ent;
-        } else {
-          if (!a.parents_only) emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
+          ent.mrow = mrow;
+          ent.cid = cc[h];
+          a.ex[c_ex++] = ent;
+        } else if (!a.parents_only) {
+          emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
         }
       }
-      if (head) {
-        const uint32_t k_ex = carry.c_kl + __popc(bk & lt);
-        const uint32_t x_ex = carry.c_ex + __popc(bx & lt);
-        int64_t tt = t;
-        do {
-          a.t_layer_off[tt] = g_ex;
-          a.t_kl_off[tt] = k_ex;
-          a.t_ex_off[tt] = x_ex;
-          --tt;
-        } while (tt >= 0 && a.off[tt] == i);
-      }
     }
-    carry = full_combine(carry, chunk_agg(k, bm, bl, bk, bx));
   }
+  if (a.dbg && threadIdx.x == 0) a.dbg[tile * 16 + 4] = gtimer();
 }
 // Offsets of traces that start at or after the end of the span table (empty
 // trailing traces) and the [T] sentinel.
 __global__ void k_pass1_tail(const uint64_t* __restrict__ off, uint32_t T, uint64_t n,
-                             const Full* __restrict__ tile_inc, uint32_t ntiles,
+                             const TileDesc* __restrict__ tile_desc, uint32_t ntiles,
                              uint32_t* t_layer_off, uint32_t* t_kl_off, uint32_t* t_ex_off,
                              uint32_t* totals) {
-  Full tot = ntiles ? load_full(tile_inc + ntiles - 1) : full_identity();
+  Full tot = full_identity();
+  if (ntiles) {
+    uint4 w[4];
+    for (int q = 0; q < 4; ++q) w[q] = tile_desc[2 * ntiles - 1].w[q];
+    desc_unpack(w, DESC_INC, tot);
+  }
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= T; t += gridDim.x * blockDim.x) {
     if (off[t] >= n) {
       t_layer_off[t] = tot.c;
@@ -1246,6 +1373,31 @@ RadixScratch radix_scratch(xsp_ctx* ctx, uint64_t n) {
   return s;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    XSP_CUDA(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// A u64 span column as a [n/16][16] tensor, 128-row boxes, 128-byte swizzle.
+void col_tmap(CUtensorMap* m, const uint64_t* col, uint64_t n) {
+  cuuint64_t dims[2] = {16, n / 16};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {16, (cuuint32_t)P1_ROWS};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = tmap_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(col), dims, strides,
+                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
 uint32_t read_u32(xsp_ctx* ctx, const uint32_t* dptr, cudaStream_t st) {
   uint32_t* h = ctx->h<uint32_t>("readback.u32", 1);
   XSP_CUDA(cudaMemcpyAsync(h, dptr, 4, cudaMemcpyDeviceToHost, st));
@@ -1270,17 +1422,19 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   uint64_t* me = ctx->d<uint64_t>("c.me", T);
   uint64_t* msid = ctx->d<uint64_t>("c.msid", T);
   auto* err_key = ctx->d<unsigned long long>("c.err_key", T);
+  const uint32_t ntiles = ceil_div(n, P1_TILE);
+  uint32_t* tile_lo = ctx->d<uint32_t>("c.tile_lo", ntiles + 1);
+  uint32_t* tile_hi = ctx->d<uint32_t>("c.tile_hi", ntiles + 1);
   if (T) {
     ctx->stage_begin("trace_prep", st);
     unsigned blocks = ceil_div((uint64_t)T * 32, 256);
     k_trace_prep<<<blocks, 256, 0, st>>>(c->flags, c->begin_ns, c->end_ns, c->span_id, off, T, model_row, mb, me,
-                                         msid, err_key);
+                                         msid, err_key, n, (uint32_t)P1_TILE, tile_lo, tile_hi);
     ctx->stage_end("trace_prep", st);
     ++ctx->launches;
   }
 
   // ---- pass 1
-  const uint32_t ntiles = ceil_div(n, P1_TILE);
   // counters: [0] orphans [1] ambiguities [2] pending [3] nonmono [4] n_failed
   //           [5] unsorted [6] ambiguities after resolution [7] any slow trace
   uint32_t* counters = ctx->d<uint32_t>("c.counters", 8);
@@ -1301,9 +1455,15 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.me = me;
   a.msid = msid;
   a.tile_ticket = ctx->d<uint32_t>("c.ticket", 1);
-  a.tile_flag = ctx->d<uint32_t>("c.tile_flag", ntiles + 1);
-  a.tile_agg = ctx->d<Full>("c.tile_agg", ntiles + 1);
-  a.tile_inc = ctx->d<Full>("c.tile_inc", ntiles + 1);
+  a.tile_lo = tile_lo;
+  a.tile_hi = tile_hi;
+  a.tile_desc = ctx->d<TileDesc>("c.tile_desc", 2ull * ntiles + 2);
+  a.dbg = nullptr;
+  const char* p1_trace = getenv("XSP_P1_TRACE");
+  if (p1_trace) {
+    a.dbg = ctx->d<unsigned long long>("c.p1dbg", 16ull * ntiles + 16);
+    XSP_CUDA(cudaMemsetAsync(a.dbg, 0, (16ull * ntiles + 16) * 8, st));
+  }
   a.unsorted = counters + 5;
   a.err_key = err_key;
   a.layer_row = ctx->d<uint32_t>("o.layer_row", n);
@@ -1330,18 +1490,36 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.pend_kl = ctx->d<uint32_t>("c.pend_kl", n);
   a.pend_count = counters + 2;
   XSP_CUDA(cudaMemsetAsync(a.tile_ticket, 0, 4, st));
-  XSP_CUDA(cudaMemsetAsync(a.tile_flag, 0, (ntiles + 1) * 4ull, st));
+  XSP_CUDA(cudaMemsetAsync(a.tile_desc, 0, (2ull * ntiles + 2) * sizeof(TileDesc), st));
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  a.bulk = al16(c->begin_ns) && al16(c->end_ns) && al16(c->cid) && al16(c->parent_id) && al16(c->flags);
+  a.bulk = n >= (uint64_t)P1_TILE && al16(c->begin_ns) && al16(c->end_ns) && al16(c->cid) &&
+           al16(c->parent_id) && al16(c->flags);
+  P1Maps maps;
+  memset(&maps, 0, sizeof(maps));
+  if (a.bulk) {
+    col_tmap(&maps.begin, c->begin_ns, n);
+    col_tmap(&maps.end, c->end_ns, n);
+    col_tmap(&maps.cid, c->cid, n);
+    col_tmap(&maps.parent, c->parent_id, n);
+  }
   if (ntiles) {
     XSP_CUDA(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM));
     ctx->stage_begin("pass1", st);
-    k_pass1<<<ntiles, P1_WARPS * 32, P1_SMEM, st>>>(a);
+    k_pass1<<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
     ctx->stage_end("pass1", st);
     ++ctx->launches;
+    if (p1_trace) {
+      std::vector<unsigned long long> h(16ull * ntiles);
+      XSP_CUDA(cudaMemcpyAsync(h.data(), a.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st));
+      XSP_CUDA(cudaStreamSynchronize(st));
+      if (FILE* f = fopen(p1_trace, "wb")) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+      }
+    }
   }
   uint32_t* totals = ctx->d<uint32_t>("c.totals", 8);
-  k_pass1_tail<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(off, T, n, a.tile_inc, ntiles, a.t_layer_off,
+  k_pass1_tail<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(off, T, n, a.tile_desc, ntiles, a.t_layer_off,
                                                                a.t_kl_off, a.t_ex_off, totals);
   ++ctx->launches;
   uint32_t* htot = ctx->h<uint32_t>("c.totals_h", 16);
