@@ -784,7 +784,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   }
   hg[4 * G] = total_runs;
   uint32_t* dg = ctx->d<uint32_t>("a.groups", 4ull * G + 4);
-  XSP_CUDA(cudaMemcpyAsync(dg, hg, (4ull * G + 1) * 4, cudaMemcpyHostToDevice, st));
+  xfer_small(dg, hg, (4ull * G + 1) * 4, st);
   const uint32_t* ft = dg;
   const uint32_t* nr = dg + G;
   const uint32_t* batch = dg + 2 * G;
@@ -812,8 +812,8 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   exclusive_scan<uint32_t, uint32_t>(ga.gk, out->group_kernel_off, G, scan_tmp, out->group_kernel_off + G, st,
                                      &ctx->launches);
   uint32_t* htot = ctx->h<uint32_t>("a.tot_h", 4);
-  XSP_CUDA(cudaMemcpyAsync(htot, out->group_layer_off + G, 4, cudaMemcpyDeviceToHost, st));
-  XSP_CUDA(cudaMemcpyAsync(htot + 1, out->group_kernel_off + G, 4, cudaMemcpyDeviceToHost, st));
+  xfer_small(htot, out->group_layer_off + G, 4, st);
+  xfer_small(htot + 1, out->group_kernel_off + G, 4, st);
   XSP_CUDA(cudaStreamSynchronize(st));
   const uint32_t TL = htot[0], TK = htot[1];
   launch(ctx, k_group_check_runs, total_runs, st, ga, total_runs, run_off);
@@ -966,8 +966,8 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     ++ctx->launches;
     exclusive_scan<uint32_t, uint32_t>(nf.g_count, out->group_name_off, G, scan_tmp, out->group_name_off + G, st,
                                        &ctx->launches);
-    XSP_CUDA(cudaMemcpyAsync(htot + 2, out->group_name_off + G, 4, cudaMemcpyDeviceToHost, st));
-    XSP_CUDA(cudaMemcpyAsync(htot + 3, nf.overflow, 4, cudaMemcpyDeviceToHost, st));
+    xfer_small(htot + 2, out->group_name_off + G, 4, st);
+    xfer_small(htot + 3, nf.overflow, 4, st);
     XSP_CUDA(cudaStreamSynchronize(st));
     if (!htot[3]) {
       NN = htot[2];
@@ -1018,7 +1018,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     launch(ctx, k_seg_flags, TK, st, TK, key, flag);
     uint32_t* scan2 = ctx->d<uint32_t>("a.scan2", scan_scratch_elems(TK + 16));
     exclusive_scan<uint32_t, uint32_t>(flag, pos, TK, scan2, pos + TK, st, &ctx->launches);
-    XSP_CUDA(cudaMemcpyAsync(htot + 2, pos + TK, 4, cudaMemcpyDeviceToHost, st));
+    xfer_small(htot + 2, pos + TK, 4, st);
     XSP_CUDA(cudaStreamSynchronize(st));
     NN = htot[2];
     NameArgs na;

@@ -10,6 +10,9 @@
 #define XSP_API extern "C" __attribute__((visibility("default")))
 
 namespace xsp {
+bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht, const xsp_groups* groups,
+                      const xsp_system_spec* spec, const xsp_analysis_opts* opts, xsp_corr_out* corr_host,
+                      xsp_tables_out* tab_host);
 void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const uint8_t* flags, const uint64_t* sid,
                        uint32_t T, const uint64_t* off, uint32_t* perm, uint32_t* was_sorted, cudaStream_t st);
 }
@@ -382,6 +385,10 @@ XSP_API xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp
     if (!ht || !groups || !spec || !opts || !corr_host || !tab_host) throw std::invalid_argument("null argument");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ctx->h2d_bytes = ctx->d2h_bytes = 0;
+    if (groups->n_groups && (!groups->first_trace || !groups->n_runs || !groups->batch_size))
+      throw std::invalid_argument("null group column");
+    // large batches: chunked pipeline overlapping H2D, compute and D2H (pipeline.cu)
+    if (xsp::run_host_chunked(ctx, hc, ht, groups, spec, opts, corr_host, tab_host)) return;
     xsp_span_cols dc = upload_cols(ctx, hc, st);
     xsp_traces dt = upload_traces(ctx, ht, st);
     xsp_corr_out dcorr;

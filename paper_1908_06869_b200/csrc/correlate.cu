@@ -1400,7 +1400,7 @@ void col_tmap(CUtensorMap* m, const uint64_t* col, uint64_t n) {
 
 uint32_t read_u32(xsp_ctx* ctx, const uint32_t* dptr, cudaStream_t st) {
   uint32_t* h = ctx->h<uint32_t>("readback.u32", 1);
-  XSP_CUDA(cudaMemcpyAsync(h, dptr, 4, cudaMemcpyDeviceToHost, st));
+  xfer_small(h, dptr, 4, st);
   XSP_CUDA(cudaStreamSynchronize(st));
   return *h;
 }
@@ -1523,8 +1523,8 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
                                                                a.t_kl_off, a.t_ex_off, totals);
   ++ctx->launches;
   uint32_t* htot = ctx->h<uint32_t>("c.totals_h", 16);
-  XSP_CUDA(cudaMemcpyAsync(htot, totals, 5 * 4, cudaMemcpyDeviceToHost, st));
-  XSP_CUDA(cudaMemcpyAsync(htot + 8, counters, 6 * 4, cudaMemcpyDeviceToHost, st));
+  xfer_small(htot, totals, 5 * 4, st);
+  xfer_small(htot + 8, counters, 6 * 4, st);
   XSP_CUDA(cudaStreamSynchronize(st));
   const uint32_t nl = htot[0], nkl = htot[1], nex = htot[2];
   const uint32_t n_amb_raw = htot[9], n_pend = htot[10];
@@ -1622,7 +1622,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     XSP_CUDA(cudaMemsetAsync(no_dup, 0xFF, T * 8ull, st));
     launch(ctx, k_status, T, st, T, model_row, err_key, no_dup, no_dup, a.ex, a.kl, out->trace_status,
            out->trace_err_row, counters + 4);
-    XSP_CUDA(cudaMemcpyAsync(htot, counters + 4, 16, cudaMemcpyDeviceToHost, st));
+    xfer_small(htot, counters + 4, 16, st);
     XSP_CUDA(cudaStreamSynchronize(st));
     ctx->stage_end("gather", st);
     if (!htot[3]) {
@@ -1675,7 +1675,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     uint64_t* scan64 = ctx->d<uint64_t>("c.scan64", scan_scratch_elems(T + 1));
     exclusive_scan<uint64_t, uint64_t>(rsize, roff, T, scan64, roff + T, st, &ctx->launches);
     uint64_t* hroff = ctx->h<uint64_t>("c.roff_h", 1);
-    XSP_CUDA(cudaMemcpyAsync(hroff, roff + T, 8, cudaMemcpyDeviceToHost, st));
+    xfer_small(hroff, roff + T, 8, st);
     XSP_CUDA(cudaStreamSynchronize(st));
     const uint64_t nslots = *hroff;
     j.roff = roff;
@@ -1727,8 +1727,8 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   uint32_t* kval = ctx->d<uint32_t>("c.kval", nkl + 1);
   launch(ctx, k_compact_kernels, nkl, st, nkl, fa.kept, kpos, a.kl, kkey, kval, counters + 3);
   launch(ctx, k_check_mono, nkl, st, nk_d, kkey, counters + 3);
-  XSP_CUDA(cudaMemcpyAsync(htot, nk_d, 4, cudaMemcpyDeviceToHost, st));
-  XSP_CUDA(cudaMemcpyAsync(htot + 1, counters + 3, 4, cudaMemcpyDeviceToHost, st));
+  xfer_small(htot, nk_d, 4, st);
+  xfer_small(htot + 1, counters + 3, 4, st);
   XSP_CUDA(cudaStreamSynchronize(st));
   const uint32_t nk = htot[0];
   ctx->stage_end("fuse", st);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -92,10 +93,15 @@ struct xsp_ctx {
     }
   }
 
+  // Suffix appended to every device buffer name while set: the chunked host
+  // pipeline runs consecutive chunks on two disjoint buffer sets, so one
+  // chunk's results can stream out while the next chunk computes.
+  std::string tag;
   // Grow-only named device buffer with at least `bytes` bytes.
-  void* dbuf(const std::string& name, size_t bytes) {
+  void* dbuf(const std::string& name_, size_t bytes) {
     if (bytes == 0) bytes = 16;
-    Buf& b = dev[name];
+    Buf& b = dev[tag.empty() ? name_ : name_ + tag];
+    const std::string& name = name_;
     if (b.bytes < bytes) {
       if (b.ptr) cudaFree(b.ptr);
       b.ptr = nullptr;
@@ -131,8 +137,49 @@ struct xsp_ctx {
   T* h(const std::string& name, uint64_t count) {
     return static_cast<T*>(hbuf(name, count * sizeof(T)));
   }
+  // Pinned buffer with at least `bytes`, preserving its first `keep` bytes when
+  // it has to grow (callers make sure no copy into it is in flight).
+  void* hbuf_keep(const std::string& name, size_t bytes, size_t keep) {
+    Buf& b = host[name];
+    if (b.bytes >= bytes && b.ptr) return b.ptr;
+    size_t want = bytes + bytes / 2 + 4096;
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, want, cudaHostAllocDefault) != cudaSuccess)
+      throw CudaError("cudaHostAlloc of " + std::to_string(want) + " bytes failed");
+    if (b.ptr) {
+      if (keep) std::memcpy(p, b.ptr, keep < b.bytes ? keep : b.bytes);
+      cudaFreeHost(b.ptr);
+    }
+    b.ptr = p;
+    b.bytes = want;
+    return p;
+  }
+  size_t hcap(const std::string& name) {
+    auto it = host.find(name);
+    return it == host.end() ? 0 : it->second.bytes;
+  }
+  // ctx-owned non-blocking streams for the chunked host pipeline
+  cudaStream_t copy_stream = nullptr, work_stream = nullptr, out_stream = nullptr;
+  cudaStream_t stream_copy() {
+    if (!copy_stream && cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+      throw CudaError("cudaStreamCreate failed");
+    return copy_stream;
+  }
+  cudaStream_t stream_out() {
+    if (!out_stream && cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking) != cudaSuccess)
+      throw CudaError("cudaStreamCreate failed");
+    return out_stream;
+  }
+  cudaStream_t stream_work() {
+    if (!work_stream && cudaStreamCreateWithFlags(&work_stream, cudaStreamNonBlocking) != cudaSuccess)
+      throw CudaError("cudaStreamCreate failed");
+    return work_stream;
+  }
   ~xsp_ctx() {
     stage_collect();
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (work_stream) cudaStreamDestroy(work_stream);
+    if (out_stream) cudaStreamDestroy(out_stream);
     for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
     for (auto& [k, b] : dev)
       if (b.ptr) cudaFree(b.ptr);

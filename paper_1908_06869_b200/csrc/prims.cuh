@@ -9,6 +9,21 @@
 namespace xsp {
 
 // ---------------------------------------------------------------------------
+// Small transfers (counts, flags, group descriptors) between device memory and
+// pinned host memory, which is device-addressable under unified virtual
+// addressing: one warp moves the words, so the transfer never waits on a copy
+// engine behind bulk copies that other streams have queued (csrc/pipeline.cu
+// streams the next chunk's columns while the current chunk computes).
+static __global__ void k_xfer_words(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += 32) dst[i] = src[i];
+}
+// bytes: a multiple of 4, both pointers 4-byte aligned
+inline void xfer_small(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  k_xfer_words<<<1, 32, 0, st>>>(static_cast<uint32_t*>(dst), static_cast<const uint32_t*>(src),
+                                 static_cast<uint32_t>(bytes / 4));
+}
+
+// ---------------------------------------------------------------------------
 // Exclusive scan, reduce-then-scan (3 launches per level, recursive on the
 // block sums). `total` (optional, device) receives the sum of all inputs.
 
@@ -212,12 +227,12 @@ inline void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t n, int lo_
   if (n <= 1) return;
   s.and_or_host[0] = ~0ull;
   s.and_or_host[1] = 0ull;
-  cudaMemcpyAsync(s.and_or, s.and_or_host, 16, cudaMemcpyHostToDevice, st);
+  xfer_small(s.and_or, s.and_or_host, 16, st);
   unsigned g = ceil_div(n, 256);
   if (g > 1184) g = 1184;
   k_rs_bits<<<g, 256, 0, st>>>(keys, n, s.and_or);
   ++*launches;
-  cudaMemcpyAsync(s.and_or_host, s.and_or, 16, cudaMemcpyDeviceToHost, st);
+  xfer_small(s.and_or_host, s.and_or, 16, st);
   cudaStreamSynchronize(st);
   const uint64_t varying = s.and_or_host[0] ^ s.and_or_host[1];
   const uint32_t ntiles = ceil_div(n, kRsTile);
