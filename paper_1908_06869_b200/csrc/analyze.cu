@@ -35,6 +35,93 @@ __device__ double trimmed_mean_dev(double* v, uint32_t n, double f) {
   return s / (double)(n - 2 * drop);
 }
 
+// Register-resident bitonic sorting networks (all indices compile-time after
+// unrolling, so the values stay in registers).
+template <int N, typename T>
+__device__ __forceinline__ void bitonic_sort(T (&v)[N]) {
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const T a = v[i], b = v[l];
+          const bool up = (i & k) == 0;
+          const bool sw = up ? (b < a) : (a < b);
+          v[i] = sw ? b : a;
+          v[l] = sw ? a : b;
+        }
+      }
+    }
+  }
+}
+
+// trimmed_mean over n <= N doubles produced by load(r): the n values padded
+// with +inf are sorted (skipped when they already are, e.g. all equal), then the
+// kept middle is summed in ascending order as the reference does.
+template <int N, typename Load>
+__device__ __forceinline__ double trimmed_mean_net(Load load, uint32_t n, double f) {
+  double v[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = (uint32_t)i < n ? load((uint32_t)i) : __longlong_as_double(0x7ff0000000000000ll);
+  bool sorted = true;
+#pragma unroll
+  for (int i = 1; i < N; ++i) sorted &= !(v[i] < v[i - 1]);
+  if (!sorted) bitonic_sort<N>(v);
+  const uint32_t drop = (uint32_t)floor(f * (double)n);
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if ((uint32_t)i >= drop && (uint32_t)i < n - drop) s = __dadd_rn(s, v[i]);
+  return s / (double)(n - 2 * drop);
+}
+
+template <typename Load>
+__device__ __forceinline__ double trimmed_mean_any(Load load, uint32_t n, double f) {
+  if (n <= 8) return trimmed_mean_net<8>(load, n, f);
+  if (n <= 16) return trimmed_mean_net<16>(load, n, f);
+  if (n <= 32) return trimmed_mean_net<32>(load, n, f);
+  double v[kMaxRuns];
+  for (uint32_t r = 0; r < n; ++r) v[r] = load(r);
+  return trimmed_mean_dev(v, n, f);
+}
+
+// Integer samples (durations in ns): when every sample fits in 32 bits they are
+// sorted as u32 and the kept middle is summed exactly in u64. The reference sums
+// the same values as doubles in ascending order; every partial sum is an integer
+// below 2^53, so each of its additions is exact and both give the same double.
+template <int N, typename Load>
+__device__ __forceinline__ bool trimmed_mean_u32(Load load, uint32_t n, double f, double& out) {
+  uint32_t v[N];
+  uint64_t hi = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const uint64_t x = (uint32_t)i < n ? load((uint32_t)i) : 0xFFFFFFFFull;
+    hi |= x >> 32;
+    v[i] = (uint32_t)x;
+  }
+  if (hi) return false;
+  bitonic_sort<N>(v);
+  const uint32_t drop = (uint32_t)floor(f * (double)n);
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if ((uint32_t)i >= drop && (uint32_t)i < n - drop) s += v[i];
+  out = (double)s / (double)(n - 2 * drop);
+  return true;
+}
+
+template <typename Load>  // load(r) -> uint64_t
+__device__ __forceinline__ double trimmed_mean_int(Load load, uint32_t n, double f) {
+  double out;
+  if (n <= 8 && trimmed_mean_u32<8>(load, n, f, out)) return out;
+  if (n > 8 && n <= 16 && trimmed_mean_u32<16>(load, n, f, out)) return out;
+  if (n > 16 && n <= 32 && trimmed_mean_u32<32>(load, n, f, out)) return out;
+  return trimmed_mean_any([&](uint32_t r) { return (double)load(r); }, n, f);
+}
+
 struct Roof {
   double ai, tput;
   int8_t bound;
@@ -219,15 +306,10 @@ __global__ void k_kernels(LayerArgs a, uint32_t total_kernels) {
   if (a.gstatus[g] != XSP_G_OK) return;
   const uint32_t ord = q - a.gk_off[g];
   const uint32_t R = a.nr[g], t0 = a.ft[g];
-  double v[kMaxRuns];
-  double w[kMaxRuns];
-  for (uint32_t r = 0; r < R; ++r) {
-    const uint32_t jr = a.t_kernel_off[t0 + r] + ord;
-    v[r] = (double)a.kernel_dur[jr];
-    w[r] = a.kernel_occ[jr];
-  }
-  const double klat = trimmed_mean_dev(v, R, a.trim);
-  const double kocc = trimmed_mean_dev(w, R, a.trim);
+  const double klat =
+      trimmed_mean_int([&](uint32_t r) { return a.kernel_dur[a.t_kernel_off[t0 + r] + ord]; }, R, a.trim);
+  const double kocc = trimmed_mean_any([&](uint32_t r) { return a.kernel_occ[a.t_kernel_off[t0 + r] + ord]; }, R,
+                                       a.trim);
   const uint32_t j = a.t_kernel_off[t0] + ord;
   const uint32_t mr0 = a.kernel_mrow[j];
   uint64_t f = 0, rd = 0, wr = 0;
@@ -258,9 +340,8 @@ __global__ void k_layers(LayerArgs a) {
   const uint32_t li = q - a.gl_off[g];
   if (a.gstatus[g] != XSP_G_OK) return;
   const uint32_t R = a.nr[g], t0 = a.ft[g];
-  double v[kMaxRuns];
-  for (uint32_t r = 0; r < R; ++r) v[r] = (double)a.layer_dur[a.t_layer_off[t0 + r] + li];
-  const double layer_lat = trimmed_mean_dev(v, R, a.trim);
+  const double layer_lat =
+      trimmed_mean_int([&](uint32_t r) { return a.layer_dur[a.t_layer_off[t0 + r] + li]; }, R, a.trim);
 
   const uint32_t gl0 = a.t_layer_off[t0] + li;
   const uint32_t trace_kbase = a.t_kernel_off[t0];
@@ -376,12 +457,12 @@ __global__ void k_models(ModelArgs a) {
   const uint32_t R = a.nr[g], t0 = a.ft[g];
   double mlat = 0.0;
   if (lane == 0) {
-    double v[kMaxRuns];
-    for (uint32_t r = 0; r < R; ++r) {
-      uint32_t m = a.model_row[t0 + r];
-      v[r] = (double)clamp_dur(a.begin[m], a.end[m]);
-    }
-    mlat = trimmed_mean_dev(v, R, a.trim);
+    mlat = trimmed_mean_int(
+        [&](uint32_t r) {
+          const uint32_t m = a.model_row[t0 + r];
+          return clamp_dur(a.begin[m], a.end[m]);
+        },
+        R, a.trim);
   }
   mlat = __shfl_sync(0xffffffffu, mlat, 0);
   double lat = 0.0, occw = 0.0;
@@ -398,9 +479,17 @@ __global__ void k_models(ModelArgs a) {
       wr += a.k_write[j];
     }
     const uint32_t cnt = min(32u, k1 - base);
-    for (uint32_t s = 0; s < cnt; ++s) {
-      lat = __dadd_rn(lat, __shfl_sync(0xffffffffu, kl, s));
-      occw = __dadd_rn(occw, __shfl_sync(0xffffffffu, prod, s));
+    if (cnt == 32) {
+#pragma unroll
+      for (int s = 0; s < 32; ++s) {
+        lat = __dadd_rn(lat, __shfl_sync(0xffffffffu, kl, s));
+        occw = __dadd_rn(occw, __shfl_sync(0xffffffffu, prod, s));
+      }
+    } else {
+      for (uint32_t s = 0; s < cnt; ++s) {
+        lat = __dadd_rn(lat, __shfl_sync(0xffffffffu, kl, s));
+        occw = __dadd_rn(occw, __shfl_sync(0xffffffffu, prod, s));
+      }
     }
   }
   f = warp_sum_u64(f);
@@ -412,7 +501,12 @@ __global__ void k_models(ModelArgs a) {
     const uint32_t l = base + lane;
     double x = l < a.gl_off[g + 1] ? a.l_kern_lat[l] : 0.0;
     const uint32_t cnt = min(32u, a.gl_off[g + 1] - base);
-    for (uint32_t s = 0; s < cnt; ++s) gpu = __dadd_rn(gpu, __shfl_sync(0xffffffffu, x, s));
+    if (cnt == 32) {
+#pragma unroll
+      for (int s = 0; s < 32; ++s) gpu = __dadd_rn(gpu, __shfl_sync(0xffffffffu, x, s));
+    } else {
+      for (uint32_t s = 0; s < cnt; ++s) gpu = __dadd_rn(gpu, __shfl_sync(0xffffffffu, x, s));
+    }
   }
   if (lane != 0) return;
   Roof ro = roofline(f, rd, wr, lat, a.peak, a.bw);
@@ -586,7 +680,22 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
     const uint32_t s = T.used[u];
     const uint32_t b = k0 + T.start[s], n = (uint32_t)T.cnt[s];
     double lat = 0.0, occw = 0.0;
-    for (uint32_t i = 0; i < n; ++i) {
+    uint32_t i = 0;
+    for (; i + 8 <= n; i += 8) {  // eight independent gathers in flight, then the ordered chain
+      double l8[8], o8[8];
+#pragma unroll
+      for (int u2 = 0; u2 < 8; ++u2) {
+        const uint32_t x = a.perm[b + i + u2];
+        l8[u2] = a.k_lat[x];
+        o8[u2] = a.k_occ[x];
+      }
+#pragma unroll
+      for (int u2 = 0; u2 < 8; ++u2) {
+        lat = __dadd_rn(lat, l8[u2]);
+        occw = __dadd_rn(occw, __dmul_rn(o8[u2], l8[u2]));
+      }
+    }
+    for (; i < n; ++i) {
       const uint32_t x = a.perm[b + i];
       const double l = a.k_lat[x];
       lat = __dadd_rn(lat, l);
