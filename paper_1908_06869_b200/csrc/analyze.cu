@@ -599,13 +599,16 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
   bool over = false;
   const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
   const uint32_t lt = lanemask_lt();
-  // pass A: slot per kernel, u64 counters, stable rank of the kernel within its name
+  // pass A: slot per kernel and its stable rank within its name (the next
+  // chunk's names are loaded while this chunk is hashed)
+  uint32_t nm_next = k0 + lane < k1 ? a.k_name[k0 + lane] : 0;
   for (uint32_t base = k0; base < k1; base += 32) {
     const uint32_t x = base + lane;
     const bool v = x < k1;
+    const uint32_t nm = nm_next;
+    if (base + 32 + lane < k1) nm_next = a.k_name[base + 32 + lane];
     uint32_t slot = NCAP + lane;  // distinct dummy for idle lanes
     if (v) {
-      const uint32_t nm = a.k_name[x];
       uint32_t h = (nm * 2654435761u) & (NCAP - 1);
       uint32_t probes = 0;
       for (;;) {
@@ -621,12 +624,7 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
           break;
         }
       }
-      if (!over) {
-        slot = h;
-        atomicAdd(&T.f[slot], (unsigned long long)a.k_flops[x]);
-        atomicAdd(&T.r[slot], (unsigned long long)a.k_read[x]);
-        atomicAdd(&T.w[slot], (unsigned long long)a.k_write[x]);
-      }
+      if (!over) slot = h;
     }
     if (__any_sync(0xffffffffu, over)) break;
     const uint32_t peers = __match_any_sync(0xffffffffu, slot);
@@ -675,11 +673,12 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
   for (uint32_t x = k0 + lane; x < k1; x += 32) a.perm[k0 + T.start[a.ks_slot[x]] + a.ks_rank[x]] = x;
   __syncwarp();
   // pass D: one lane per name walks that name's kernels in tree order
-  // (Accumulator::add, analysis.cpp:181-188)
+  // (Accumulator::add, analysis.cpp:181-188); the u64 counters ride along (exact)
   for (uint32_t u = lane; u < nu; u += 32) {
     const uint32_t s = T.used[u];
     const uint32_t b = k0 + T.start[s], n = (uint32_t)T.cnt[s];
     double lat = 0.0, occw = 0.0;
+    unsigned long long f = 0, rd = 0, wr = 0;
     uint32_t i = 0;
     for (; i + 8 <= n; i += 8) {  // eight independent gathers in flight, then the ordered chain
       double l8[8], o8[8];
@@ -688,6 +687,9 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
         const uint32_t x = a.perm[b + i + u2];
         l8[u2] = a.k_lat[x];
         o8[u2] = a.k_occ[x];
+        f += a.k_flops[x];
+        rd += a.k_read[x];
+        wr += a.k_write[x];
       }
 #pragma unroll
       for (int u2 = 0; u2 < 8; ++u2) {
@@ -700,9 +702,15 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
       const double l = a.k_lat[x];
       lat = __dadd_rn(lat, l);
       occw = __dadd_rn(occw, __dmul_rn(a.k_occ[x], l));
+      f += a.k_flops[x];
+      rd += a.k_read[x];
+      wr += a.k_write[x];
     }
     T.lat[s] = lat;
     T.occw[s] = occw;
+    T.f[s] = f;
+    T.r[s] = rd;
+    T.w[s] = wr;
   }
   __syncwarp();
   const double mlat = a.m_lat[g];
