@@ -455,28 +455,47 @@ __global__ void k_models(ModelArgs a) {
     return;
   }
   const uint32_t R = a.nr[g], t0 = a.ft[g];
-  double mlat = 0.0;
-  if (lane == 0) {
-    mlat = trimmed_mean_int(
-        [&](uint32_t r) {
-          const uint32_t m = a.model_row[t0 + r];
-          return clamp_dur(a.begin[m], a.end[m]);
-        },
-        R, a.trim);
+  // model latency: lane r loads run r's model span; every lane then runs the
+  // same trimmed mean over the shuffled values (warp-uniform, no idle lanes)
+  uint64_t mdur = 0;
+  if (lane < R) {
+    const uint32_t m = a.model_row[t0 + lane];
+    mdur = clamp_dur(a.begin[m], a.end[m]);
   }
-  mlat = __shfl_sync(0xffffffffu, mlat, 0);
+  uint64_t mdur_hi = 0;  // runs 32..63 (kMaxRuns)
+  if (R > 32 && lane + 32 < R) {
+    const uint32_t m = a.model_row[t0 + 32 + lane];
+    mdur_hi = clamp_dur(a.begin[m], a.end[m]);
+  }
   double lat = 0.0, occw = 0.0;
   uint64_t f = 0, rd = 0, wr = 0;
   const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
+  // lanes load 32 consecutive rows (the next chunk while this one is consumed);
+  // the fp64 chains then take them strictly left to right through register
+  // broadcast, so the rounding sequence is exactly the reference's
+  double kl_n = 0.0, oc_n = 0.0;
+  uint64_t f_n = 0, r_n = 0, w_n = 0;
+  if (k0 + lane < k1) {
+    kl_n = a.k_lat[k0 + lane];
+    oc_n = a.k_occ[k0 + lane];
+    f_n = a.k_flops[k0 + lane];
+    r_n = a.k_read[k0 + lane];
+    w_n = a.k_write[k0 + lane];
+  }
   for (uint32_t base = k0; base < k1; base += 32) {
-    const uint32_t j = base + lane;
-    double kl = 0.0, prod = 0.0;
-    if (j < k1) {
-      kl = a.k_lat[j];
-      prod = __dmul_rn(a.k_occ[j], kl);
-      f += a.k_flops[j];
-      rd += a.k_read[j];
-      wr += a.k_write[j];
+    const double kl = kl_n, prod = __dmul_rn(oc_n, kl_n);
+    f += f_n;
+    rd += r_n;
+    wr += w_n;
+    const uint32_t jn = base + 32 + lane;
+    kl_n = oc_n = 0.0;
+    f_n = r_n = w_n = 0;
+    if (jn < k1) {
+      kl_n = a.k_lat[jn];
+      oc_n = a.k_occ[jn];
+      f_n = a.k_flops[jn];
+      r_n = a.k_read[jn];
+      w_n = a.k_write[jn];
     }
     const uint32_t cnt = min(32u, k1 - base);
     if (cnt == 32) {
@@ -497,10 +516,12 @@ __global__ void k_models(ModelArgs a) {
   wr = warp_sum_u64(wr);
   const uint64_t n = k1 - k0;
   double gpu = 0.0;
-  for (uint32_t base = a.gl_off[g]; base < a.gl_off[g + 1]; base += 32) {
-    const uint32_t l = base + lane;
-    double x = l < a.gl_off[g + 1] ? a.l_kern_lat[l] : 0.0;
-    const uint32_t cnt = min(32u, a.gl_off[g + 1] - base);
+  const uint32_t l0 = a.gl_off[g], l1 = a.gl_off[g + 1];
+  double x_n = l0 + lane < l1 ? a.l_kern_lat[l0 + lane] : 0.0;
+  for (uint32_t base = l0; base < l1; base += 32) {
+    const double x = x_n;
+    x_n = base + 32 + lane < l1 ? a.l_kern_lat[base + 32 + lane] : 0.0;
+    const uint32_t cnt = min(32u, l1 - base);
     if (cnt == 32) {
 #pragma unroll
       for (int s = 0; s < 32; ++s) gpu = __dadd_rn(gpu, __shfl_sync(0xffffffffu, x, s));
@@ -508,6 +529,13 @@ __global__ void k_models(ModelArgs a) {
       for (uint32_t s = 0; s < cnt; ++s) gpu = __dadd_rn(gpu, __shfl_sync(0xffffffffu, x, s));
     }
   }
+  const double mlat = trimmed_mean_int(
+      [&](uint32_t r) {
+        const uint64_t lo = __shfl_sync(0xffffffffu, mdur, r & 31u);
+        const uint64_t hi = __shfl_sync(0xffffffffu, mdur_hi, r & 31u);
+        return r < 32 ? lo : hi;
+      },
+      R, a.trim);
   if (lane != 0) return;
   Roof ro = roofline(f, rd, wr, lat, a.peak, a.bw);
   a.m_lat[g] = mlat;
