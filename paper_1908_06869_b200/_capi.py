@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libxsp.so")
+LIB_PATH = os.environ.get("XSP_LIB") or os.path.join(_HERE, "lib", "libxsp.so")  # XSP_LIB: tuning variants
 
 u8p = C.POINTER(C.c_uint8)
 i8p = C.POINTER(C.c_int8)

@@ -190,49 +190,6 @@ __device__ __forceinline__ Full full_identity() {
   return f;
 }
 
-// Look-back tile descriptor: the 12 payload words of a Full in four 16-byte
-// words, each led by a status word (1 = tile aggregate, 2 = inclusive prefix).
-// A reader validates every 16-byte word by its own status, so one relaxed
-// vector-load round trip returns status and value together (no fences); a
-// 16-byte aligned vector access is observed whole. Slot 2t holds tile t's
-// aggregate, slot 2t+1 its inclusive prefix; both are zeroed per call.
-struct __align__(16) TileDesc {
-  uint4 w[4];
-};
-constexpr uint32_t DESC_AGG = 1, DESC_INC = 2;
-
-__device__ __forceinline__ void st_relaxed_v4(uint4* p, uint4 v) {
-  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ uint4 ld_relaxed_v4(const uint4* p) {
-  uint4 v;
-  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ void desc_store(TileDesc* d, const Full& v, uint32_t status) {
-  const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) st_relaxed_v4(d->w + q, make_uint4(status, s[3 * q], s[3 * q + 1], s[3 * q + 2]));
-}
-// true when all four words carry `status`; v is then the published value
-__device__ __forceinline__ bool desc_unpack(const uint4 (&w)[4], uint32_t status, Full& v) {
-  uint32_t* d = reinterpret_cast<uint32_t*>(&v);
-  bool ok = true;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    ok &= w[q].x == status;
-    d[3 * q] = w[q].y;
-    d[3 * q + 1] = w[q].z;
-    d[3 * q + 2] = w[q].w;
-  }
-  return ok;
-}
-
 __device__ __forceinline__ Full shfl_full(const Full& v, int src) {
   Full u;
   const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
@@ -242,23 +199,35 @@ __device__ __forceinline__ Full shfl_full(const Full& v, int src) {
   return u;
 }
 
-// Pass-1 work decomposition: a tile of 2048 timeline-consecutive spans per CTA,
-// 8 consecutive spans per thread. Each thread folds its spans serially into a
-// `Full` aggregate (phase 1), one warp-level scan of the 32 thread aggregates
-// plus the block's decoupled look-back gives every thread its exclusive prefix,
-// and the thread re-walks its spans with that running state (phase 3) emitting
-// outputs with plain counters.
-constexpr int P1_CWARPS = 7;  // compute warps; warp 7 runs the look-back
-constexpr int P1_THREADS = (P1_CWARPS + 1) * 32;
+// Pass-1 work decomposition: a tile of P1_TILE timeline-consecutive spans per
+// CTA, 8 consecutive spans per thread. Pass 1 is reduce-then-scan (no
+// decoupled look-back: a look-back makes every tile wait for the slowest of its
+// recent predecessors, which measured a third of the kernel's time):
+//   k_p1_reduce  per tile, each thread folds its 8 spans serially into a Full;
+//                a warp scan + block combine gives the tile aggregate (reads
+//                flags, begin, end, parent_id);
+//   k_p1_scan    one CTA: exclusive scan over groups of 32 tile aggregates;
+//   k_pass1      per tile, the tile is staged into shared memory by TMA, the
+//                thread folds are recomputed, and every thread re-walks its
+//                spans from its exclusive prefix emitting outputs with plain
+//                counters.
+#ifndef XSP_P1_WARPS
+#define XSP_P1_WARPS 8
+#endif
+constexpr int P1_WARPS = XSP_P1_WARPS;
+constexpr int P1_THREADS = P1_WARPS * 32;
 constexpr int P1_ITEMS = 8;
-constexpr int P1_SUB = P1_ITEMS * 32;  // spans per compute warp
-constexpr int P1_TILE = P1_CWARPS * P1_SUB;
+constexpr int P1_SUB = P1_ITEMS * 32;  // spans per warp
+constexpr int P1_TILE = P1_WARPS * P1_SUB;
 constexpr int P1_ROWS = P1_TILE / 16;  // 128-byte rows of 16 u64 per column
 static_assert(P1_TILE % 128 == 0, "swizzled columns need 1024-byte aligned bases");
+static_assert(P1_ROWS <= 256, "TMA box rows");
 constexpr int P1_TCACHE = 32;          // traces of a tile cached in shared memory
+constexpr int P1_SCAN_THREADS = 1024;
 
 struct P1Args {
-  int bulk;  // full tiles staged by TMA tensor copies (columns 16-byte aligned)
+  int bulk;     // full tiles staged by TMA tensor copies (columns 16-byte aligned)
+  int aligned;  // begin/end 16-byte and flags 8-byte aligned (vector loads in k_p1_reduce)
   int parents_only;
   const uint64_t* span_id;
   const uint8_t* flags;
@@ -274,11 +243,14 @@ struct P1Args {
   const uint64_t* mb;
   const uint64_t* me;
   const uint64_t* msid;
-  uint32_t* tile_ticket;
   const uint32_t* tile_lo;  // trace of each tile's first span (k_trace_prep)
   const uint32_t* tile_hi;  // trace of each tile's last span
-  TileDesc* tile_desc;  // 2 slots per tile (aggregate, inclusive)
-  unsigned long long* dbg;  // optional per-tile timeline (XSP_P1_TRACE)
+  uint32_t ntiles;
+  Full* tile_agg;           // [ntiles] (k_p1_reduce)
+  Full* group_sum;          // [ngroups] totals of 32-tile groups (k_p1_reduce)
+  uint32_t* group_done;     // [ngroups] finished tiles per group (zeroed per call)
+  Full* tile_prefix;        // [ngroups + 1] exclusive prefixes of 32-tile groups + total (k_p1_scan)
+  Full* tile_excl;          // [ntiles] exclusive prefix of every tile (k_p1_tile_prefix)
   uint32_t* unsorted;
   unsigned long long* err_key;
   uint32_t* layer_row;
@@ -323,6 +295,8 @@ struct TileSmem {
   uint8_t flags[P1_TILE];
 };
 constexpr size_t P1_SMEM = sizeof(TileSmem) + 1024;  // + alignment slack
+// resident CTAs per SM the register budget is sized for (shared memory bound)
+constexpr int P1_MINB = (int)((220u * 1024u) / (P1_SMEM + 2048u)) < 8 ? (int)((220u * 1024u) / (P1_SMEM + 2048u)) : 8;
 
 __host__ __device__ __forceinline__ uint32_t sw128(uint32_t j) {
   return (j & ~15u) | (((((j >> 1) & 7u) ^ ((j >> 4) & 7u))) << 1) | (j & 1u);
@@ -368,70 +342,30 @@ __device__ __forceinline__ void ld_pair(const uint64_t* col, uint32_t j, uint64_
   v0 = p.x;
   v1 = p.y;
 }
-
-// Per-trace attributes a thread needs while walking its spans.
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
+__device__ __forceinline__ ulonglong2 ldg_nc_v2(const uint64_t* p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
 }
 
+// Per-trace attributes a thread needs while walking its spans.
 struct TraceAttrs {
   uint64_t cur, next;  // offsets of the current trace and the one after it
   uint64_t mb, me, msid;
   uint32_t model, levels;
 };
 
-__device__ __forceinline__ void bar_sync_compute() {
-  asm volatile("bar.sync 1, %0;" ::"n"(P1_CWARPS * 32) : "memory");
-}
-
-__global__ void __launch_bounds__(P1_THREADS, 3) k_pass1(P1Args a, const __grid_constant__ P1Maps maps) {
-  extern __shared__ unsigned char p1_dyn[];
-  TileSmem& sm = *reinterpret_cast<TileSmem*>(p1_dyn + ((1024u - (smem_u32(p1_dyn) & 1023u)) & 1023u));
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_tlo, s_thi;
-  __shared__ Full s_wagg[P1_CWARPS];
-  __shared__ Full s_prefix, s_agg;
-  __shared__ TraceCache tc;
-  __shared__ __align__(8) uint64_t s_bar;
-
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const bool lbw = warp == P1_CWARPS;  // the look-back warp
-  const uint64_t t_start = a.dbg ? gtimer() : 0;
-  if (threadIdx.x == 0) {
-    const uint32_t tile = atomicAdd(a.tile_ticket, 1u);
-    const uint64_t tb = (uint64_t)tile * P1_TILE;
-    uint64_t last = tb + P1_TILE;
-    if (last > a.n) last = a.n;
-    s_tile = tile;
-    if (a.bulk && last - tb == P1_TILE) {
-      mbar_init(&s_bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      mbar_expect_tx(&s_bar, P1_TILE * (4 * 8 + 1));
-      const int y = (int)(tb / 16);
-      tma_g2s_2d(sm.begin, &maps.begin, 0, y, &s_bar);
-      tma_g2s_2d(sm.end, &maps.end, 0, y, &s_bar);
-      tma_g2s_2d(sm.cid, &maps.cid, 0, y, &s_bar);
-      tma_g2s_2d(sm.parent, &maps.parent, 0, y, &s_bar);
-      bulk_g2s(sm.flags, a.flags + tb, P1_TILE, &s_bar);
-    }
-    s_tlo = __ldg(a.tile_lo + tile);
-    s_thi = __ldg(a.tile_hi + tile) + 1;
-  }
-  __syncthreads();
-  const uint32_t tile = s_tile, tlo = s_tlo, thi = s_thi;
-  const uint64_t tile_base = (uint64_t)tile * P1_TILE;
-  const uint32_t tile_n = (uint32_t)min((uint64_t)P1_TILE, a.n - tile_base);
-  const bool cached = thi - tlo <= (uint32_t)P1_TCACHE;
-  const uint32_t j0 = threadIdx.x * P1_ITEMS;  // compute thread's first local index
-  const uint64_t i0 = tile_base + j0;
-  if (a.dbg && threadIdx.x == 0) a.dbg[tile * 16 + 0] = t_start;
-
-  auto t_off = [&](uint32_t r) -> uint64_t { return cached ? tc.off[r] : __ldg(a.off + tlo + r); };
-  auto load_attrs = [&](uint32_t r, TraceAttrs& ta) {
-    ta.cur = t_off(r);
-    ta.next = t_off(r + 1);
+// The tile's traces [tlo, thi): attributes of the first P1_TCACHE of them are
+// cached in shared memory; the rest are read from global memory.
+struct TileTraces {
+  const P1Args& a;
+  const TraceCache& tc;
+  uint32_t tlo;
+  bool cached;
+  __device__ __forceinline__ uint64_t off(uint32_t r) const { return cached ? tc.off[r] : __ldg(a.off + tlo + r); }
+  __device__ __forceinline__ void load(uint32_t r, TraceAttrs& ta) const {
+    ta.cur = off(r);
+    ta.next = off(r + 1);
     if (cached) {
       ta.mb = tc.mb[r];
       ta.me = tc.me[r];
@@ -446,196 +380,436 @@ __global__ void __launch_bounds__(P1_THREADS, 3) k_pass1(P1Args a, const __grid_
       ta.model = __ldg(a.model_row + t);
       ta.levels = __ldg(a.levels + t);
     }
-  };
-  // layer placement under the model span (correlator.cpp:169-194)
-  auto placed_in = [](const TraceAttrs& ta, uint8_t f, uint64_t b, uint64_t e, uint64_t par) -> bool {
-    if (ta.model == kNone) return false;
-    if (f & XSP_F_PARENT) return par == ta.msid;
-    return ta.mb <= b && e <= ta.me;
-  };
+  }
+  // trace (relative to tlo) of span i of the tile
+  __device__ __forceinline__ uint32_t find(uint64_t i, uint32_t thi) const {
+    uint32_t lo = 0, hi = thi - tlo;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (off(mid) <= i) lo = mid; else hi = mid;
+    }
+    return lo;
+  }
+};
 
-  uint32_t r0 = 0;
-  uint64_t fl8 = 0;
-  Full lane_ex;  // exclusive prefix of the thread within its warp
-  if (lbw) {
-    // ---- look-back warp: exclusive prefix over the predecessor tiles, polled
-    // while the compute warps run phase 1. Window of 32 predecessors per step;
-    // lane l looks at tile base - l.
-    Full prefix = full_identity();
-    if (tile > 0) {
-      int64_t base = (int64_t)tile - 1;
-      for (;;) {
-        const int64_t jt = base - lane;
-        Full v = full_identity();
-        bool is_inc = true;  // before tile 0: identity prefix
-        if (jt >= 0) {
-          const TileDesc* dj = a.tile_desc + 2 * jt;
-          // first attempt reads both slots whole (one round trip when the tile
-          // has published); while spinning, poll only the leading status words
-          uint4 wi[4], wa[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            wi[q] = ld_relaxed_v4(dj[1].w + q);
-            wa[q] = ld_relaxed_v4(dj[0].w + q);
-          }
-          for (;;) {
-            if (desc_unpack(wi, DESC_INC, v)) break;
-            if (desc_unpack(wa, DESC_AGG, v)) {
-              is_inc = false;
-              break;
-            }
-            if (a.dbg) atomicAdd(a.dbg + tile * 16 + 7, 1ull);
-            __nanosleep(128);
-            wi[0] = ld_relaxed_v4(dj[1].w);
-            wa[0] = ld_relaxed_v4(dj[0].w);
-            if (wi[0].x == DESC_INC) {
-#pragma unroll
-              for (int q = 1; q < 4; ++q) wi[q] = ld_relaxed_v4(dj[1].w + q);
-            } else if (wa[0].x == DESC_AGG) {
-#pragma unroll
-              for (int q = 1; q < 4; ++q) wa[q] = ld_relaxed_v4(dj[0].w + q);
-            }
-          }
-        }
-        const uint32_t incl = __ballot_sync(0xffffffffu, is_inc);
-        const uint32_t stop = incl ? (__ffs(incl) - 1) : 31;  // closest inclusive prefix
-        if (lane > stop) v = full_identity();
-        // ordered tree reduction: higher lanes hold older tiles
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          Full u;
-          const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
-          uint32_t* d = reinterpret_cast<uint32_t*>(&u);
-#pragma unroll
-          for (int w = 0; w < 12; ++w) d[w] = __shfl_down_sync(0xffffffffu, s[w], o);
-          if ((lane & (2 * o - 1)) == 0) v = full_combine(u, v);
-        }
-        prefix = full_combine(shfl_full(v, 0), prefix);
-        if (incl) break;
-        if (a.dbg && lane == 0) a.dbg[tile * 16 + 6] += 1;
-        base -= 32;
-      }
-    }
-    if (lane == 0) s_prefix = prefix;
-    if (a.dbg && lane == 0) a.dbg[tile * 16 + 5] = gtimer();
-  } else {
-    const uint32_t ncache = min(thi - tlo, (uint32_t)P1_TCACHE);
-    if (threadIdx.x <= ncache) tc.off[threadIdx.x] = a.off[tlo + threadIdx.x];
-    if (threadIdx.x < ncache) {
-      const uint32_t t = tlo + threadIdx.x;
-      tc.mb[threadIdx.x] = a.mb[t];
-      tc.me[threadIdx.x] = a.me[t];
-      tc.msid[threadIdx.x] = a.msid[t];
-      tc.model_row[threadIdx.x] = a.model_row[t];
-      tc.levels[threadIdx.x] = a.levels[t];
-    }
-    if (a.bulk && tile_n == P1_TILE) {
-      mbar_wait(&s_bar, 0);
-    } else {
-      for (uint32_t j = threadIdx.x; j < P1_TILE; j += P1_CWARPS * 32) {
-        const bool v = j < tile_n;
-        const uint64_t i = tile_base + j;
-        const uint32_t s = sw128(j);
-        sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
-        sm.begin[s] = v ? a.begin[i] : 0;
-        sm.end[s] = v ? a.end[i] : 0;
-        sm.cid[s] = v ? a.cid[i] : 0;
-        sm.parent[s] = v ? a.parent[i] : 0;
-      }
-    }
-    bar_sync_compute();
-    if (a.dbg && threadIdx.x == 0) a.dbg[tile * 16 + 1] = gtimer();
-    // trace of the thread's first span (relative to tlo); later spans walk forward
-    if (j0 < tile_n) {
-      uint32_t lo = 0, hi = thi - tlo;
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (t_off(mid) <= i0) lo = mid; else hi = mid;
-      }
-      r0 = lo;
-    }
-    fl8 = *reinterpret_cast<const uint64_t*>(sm.flags + j0);
+__device__ __forceinline__ void fill_trace_cache(const P1Args& a, TraceCache& tc, uint32_t tlo, uint32_t thi) {
+  const uint32_t ncache = min(thi - tlo, (uint32_t)P1_TCACHE);
+  if (threadIdx.x <= ncache) tc.off[threadIdx.x] = a.off[tlo + threadIdx.x];
+  if (threadIdx.x < ncache) {
+    const uint32_t t = tlo + threadIdx.x;
+    tc.mb[threadIdx.x] = a.mb[t];
+    tc.me[threadIdx.x] = a.me[t];
+    tc.msid[threadIdx.x] = a.msid[t];
+    tc.model_row[threadIdx.x] = a.model_row[t];
+    tc.levels[threadIdx.x] = a.levels[t];
+  }
+}
 
-    // ---- phase 1: thread aggregate (serial over 8 spans) ----------------------
-    Full th = full_identity();
-    {
-      TraceAttrs ta;
-      uint32_t r = r0;
-      load_attrs(r, ta);
+// layer placement under the model span (correlator.cpp:169-194)
+__device__ __forceinline__ bool placed_in(const TraceAttrs& ta, uint8_t f, uint64_t b, uint64_t e, uint64_t par) {
+  if (ta.model == kNone) return false;
+  if (f & XSP_F_PARENT) return par == ta.msid;
+  return ta.mb <= b && e <= ta.me;
+}
+
+// Phase 1: the Full aggregate of a thread's P1_ITEMS consecutive spans starting
+// at global row i0 (local index j0 of a tile of tile_n spans). ld(p, b[2], e[2],
+// par[2], f0, f1) yields spans 2p and 2p+1; parent_id is only needed (and only
+// read) for spans with XSP_F_PARENT.
+// Byte-parallel (SWAR) role masks of 8 flags bytes: bit k = predicate of span k.
+__device__ __forceinline__ uint32_t byte_mask_eq(uint64_t fl8, uint32_t and_mask, uint32_t value) {
+  const uint32_t lo = __vcmpeq4((uint32_t)fl8 & and_mask, value);
+  const uint32_t hi = __vcmpeq4((uint32_t)(fl8 >> 32) & and_mask, value);
+  const uint64_t m = ((uint64_t)hi << 32 | lo) & 0x0101010101010101ull;
+  return (uint32_t)((m * 0x0102040810204080ull) >> 56);  // gather bit 0 of every byte
+}
+struct RoleMasks {
+  uint32_t layer, layer_sync, metric, kl, ex_cid;
+};
+// Roles (xsp_common.cuh): layer = level 1; layer_sync = layer + kind Sync;
+// kl = is_kernel_launch (kind Launch, level >= Kernel) or is_sync_kernel
+// (kind Sync, level Kernel); ex_cid = is_exec with a correlation id.
+__device__ __forceinline__ RoleMasks role_masks(uint64_t fl8) {
+  RoleMasks m;
+  m.layer = byte_mask_eq(fl8, 0x03030303u, 0x01010101u);
+  m.layer_sync = byte_mask_eq(fl8, 0x0F0F0F0Fu, 0x01010101u);
+  m.metric = byte_mask_eq(fl8, 0x40404040u, 0x40404040u);
+  m.kl = byte_mask_eq(fl8, 0x0E0E0E0Eu, 0x06060606u) | byte_mask_eq(fl8, 0x0F0F0F0Fu, 0x02020202u);
+  m.ex_cid = byte_mask_eq(fl8, 0x2C2C2C2Cu, 0x28282828u);
+  return m;
+}
+
+template <typename Load>
+__device__ __forceinline__ Full fold_thread(const TileTraces& tt, uint32_t r0, uint64_t i0, uint32_t j0,
+                                            uint32_t tile_n, uint64_t fl8, Load ld) {
+  Full th = full_identity();
+  TraceAttrs ta;
+  uint32_t r = r0;
+  tt.load(r, ta);
+  if (j0 + P1_ITEMS <= tile_n && ta.cur < i0 && ta.next >= i0 + P1_ITEMS) {
+    // fast path: 8 spans inside one trace, no trace head among them. Counts
+    // from the flag bytes; only layer/sync spans touch the containment state.
+    const RoleMasks m = role_masks(fl8);
+    th.c_lay = __popc(m.layer);
+    th.c_metric = __popc(m.metric);
+    th.c_kl = __popc(m.kl);
+    th.c_ex = __popc(m.ex_cid);
+    if (m.layer_sync) {
 #pragma unroll
       for (int p = 0; p < P1_ITEMS / 2; ++p) {
+        if (!((m.layer_sync >> (2 * p)) & 3u)) continue;
         uint64_t bb[2], ee[2], pp[2];
-        ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
-        ld_pair(sm.end, j0 + 2 * p, ee[0], ee[1]);
-    ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
-        ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
+        ld(p, bb, ee, pp, (uint8_t)(fl8 >> (16 * p)), (uint8_t)(fl8 >> (16 * p + 8)));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int k = 2 * p + h;
-          const uint64_t i = i0 + k;
-          const bool v = j0 + k < tile_n;
           const uint8_t f = (uint8_t)(fl8 >> (8 * k));
-          if (!v) continue;
-          if (i >= ta.next) {
-            do { ++r; } while (t_off(r + 1) <= i);
-            load_attrs(r, ta);
-          }
-          if (ta.cur == i) {  // trace head: new segment
-            th.head = 1;
-            th.last_end1 = th.last_M1 = th.run_M1 = 0;
-          }
-          const bool is_layer = f_level(f) == XSP_LEVEL_LAYER;
-          const uint64_t e = ee[h];
-          if (is_layer && f_kind(f) == XSP_KIND_SYNC && placed_in(ta, f, bb[h], e, pp[h])) {
+          if (((m.layer_sync >> k) & 1u) && placed_in(ta, f, bb[h], ee[h], pp[h])) {
+            const uint64_t e = ee[h];
             const uint64_t w = e == ~0ull ? e : e + 1;
             th.last_M1 = th.run_M1;
             th.last_end1 = w;
             th.run_M1 = max64(th.run_M1, w);
             ++th.c;
           }
-          th.c_lay += is_layer;
-          th.c_metric += (f & XSP_F_METRICS) != 0;
-          th.c_kl += is_kernel_launch(f) || is_sync_kernel(f);
-          th.c_ex += is_exec(f) && (f & XSP_F_CID);
         }
       }
     }
-    // warp-inclusive scan of the thread aggregates (lanes in span order)
-    Full inc = th;
+    return th;
+  }
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      Full u;
-      const uint32_t* s = reinterpret_cast<const uint32_t*>(&inc);
-      uint32_t* d = reinterpret_cast<uint32_t*>(&u);
+  for (int p = 0; p < P1_ITEMS / 2; ++p) {
+    uint64_t bb[2], ee[2], pp[2];
+    ld(p, bb, ee, pp, (uint8_t)(fl8 >> (16 * p)), (uint8_t)(fl8 >> (16 * p + 8)));
 #pragma unroll
-      for (int w = 0; w < 12; ++w) d[w] = __shfl_up_sync(0xffffffffu, s[w], o);
-      if (lane >= (uint32_t)o) inc = full_combine(u, inc);
+    for (int h = 0; h < 2; ++h) {
+      const int k = 2 * p + h;
+      const uint64_t i = i0 + k;
+      if (j0 + k >= tile_n) continue;
+      const uint8_t f = (uint8_t)(fl8 >> (8 * k));
+      if (i >= ta.next) {
+        do { ++r; } while (tt.off(r + 1) <= i);
+        tt.load(r, ta);
+      }
+      if (ta.cur == i) {  // trace head: new segment
+        th.head = 1;
+        th.last_end1 = th.last_M1 = th.run_M1 = 0;
+      }
+      const bool is_layer = f_level(f) == XSP_LEVEL_LAYER;
+      const uint64_t e = ee[h];
+      if (is_layer && f_kind(f) == XSP_KIND_SYNC && placed_in(ta, f, bb[h], e, pp[h])) {
+        const uint64_t w = e == ~0ull ? e : e + 1;
+        th.last_M1 = th.run_M1;
+        th.last_end1 = w;
+        th.run_M1 = max64(th.run_M1, w);
+        ++th.c;
+      }
+      th.c_lay += is_layer;
+      th.c_metric += (f & XSP_F_METRICS) != 0;
+      th.c_kl += is_kernel_launch(f) || is_sync_kernel(f);
+      th.c_ex += is_exec(f) && (f & XSP_F_CID);
     }
-    if (lane == 31) s_wagg[warp] = inc;
-    {
-      const uint32_t* s = reinterpret_cast<const uint32_t*>(&inc);
-      uint32_t* d = reinterpret_cast<uint32_t*>(&lane_ex);
+  }
+  return th;
+}
+
+__device__ __forceinline__ Full warp_inclusive(const Full& th, uint32_t lane) {
+  Full inc = th;
 #pragma unroll
-      for (int w = 0; w < 12; ++w) d[w] = __shfl_up_sync(0xffffffffu, s[w], 1);
-      if (lane == 0) lane_ex = full_identity();
+  for (int o = 1; o < 32; o <<= 1) {
+    Full u;
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(&inc);
+    uint32_t* d = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int w = 0; w < 12; ++w) d[w] = __shfl_up_sync(0xffffffffu, s[w], o);
+    if (lane >= (uint32_t)o) inc = full_combine(u, inc);
+  }
+  return inc;
+}
+
+// The same inclusive scan for thread folds of one warp (lane = sequence order,
+// every count < 2^16), built from ballots instead of 5 rounds of 12-word
+// shuffles + full_combine. Lane l's inclusive prefix over lanes [0, l]:
+//   s = last lane <= l whose fold holds a trace head (the segment start),
+//   j = last lane in [s, l] whose fold placed a layer;
+//   last_end1 = fold_j.last_end1, last_M1 = max(fold_j.last_M1, run over [s, j)),
+//   run_M1 = run over [s, l] (a segmented max-scan), counts = add-scans.
+// This is exactly the left fold of full_combine over the lanes.
+__device__ __forceinline__ Full warp_inclusive_fold(const Full& th, uint32_t lane) {
+  const uint32_t le = 0xffffffffu >> (31u - lane);
+  const uint32_t H = __ballot_sync(0xffffffffu, th.head != 0) & le;
+  const uint32_t L = __ballot_sync(0xffffffffu, th.last_end1 != 0) & le;
+  const int s = H ? 31 - __clz(H) : -1;
+  const int s0 = s < 0 ? 0 : s;
+  uint32_t p0 = th.c | (th.c_metric << 16), p1 = th.c_lay | (th.c_kl << 16), p2 = th.c_ex;
+  uint64_t R = th.run_M1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u0 = __shfl_up_sync(0xffffffffu, p0, o);
+    const uint32_t u1 = __shfl_up_sync(0xffffffffu, p1, o);
+    const uint32_t u2 = __shfl_up_sync(0xffffffffu, p2, o);
+    const uint64_t uR = __shfl_up_sync(0xffffffffu, R, o);
+    if (lane >= (uint32_t)o) {
+      p0 += u0;
+      p1 += u1;
+      p2 += u2;
+      if ((int)lane - o >= s0) R = max64(R, uR);
     }
-    bar_sync_compute();
-    if (threadIdx.x == 0) {
-      // publish the tile aggregate (tile 0: its inclusive prefix) for the successors
-      Full agg = s_wagg[0];
-      for (int w = 1; w < P1_CWARPS; ++w) agg = full_combine(agg, s_wagg[w]);
-      desc_store(a.tile_desc + 2 * tile + (tile == 0 ? 1 : 0), agg, tile == 0 ? DESC_INC : DESC_AGG);
-      s_agg = agg;
-      if (a.dbg) a.dbg[tile * 16 + 2] = gtimer();
+  }
+  const uint32_t Ls = s > 0 ? (L & ~((1u << s) - 1u)) : L;  // layer lanes in [s, l]
+  const int j = Ls ? 31 - __clz(Ls) : -1;
+  const uint64_t le_j = __shfl_sync(0xffffffffu, th.last_end1, j >= 0 ? j : 0);
+  const uint64_t lm_j = __shfl_sync(0xffffffffu, th.last_M1, j >= 0 ? j : 0);
+  const uint64_t r_j1 = __shfl_sync(0xffffffffu, R, j >= 1 ? j - 1 : 0);
+  Full r;
+  r.c = p0 & 0xFFFFu;
+  r.c_metric = p0 >> 16;
+  r.c_lay = p1 & 0xFFFFu;
+  r.c_kl = p1 >> 16;
+  r.c_ex = p2;
+  r.head = s >= 0;
+  r.run_M1 = R;
+  r.last_end1 = j >= 0 ? le_j : 0;
+  r.last_M1 = j >= 0 ? max64(lm_j, j - 1 >= s0 ? r_j1 : 0) : 0;
+  return r;
+}
+
+// Tile header shared by the reduce and emit kernels.
+struct TileHdr {
+  uint64_t tile_base;
+  uint32_t tile_n, tlo, thi;
+};
+__device__ __forceinline__ TileHdr tile_hdr(const P1Args& a, uint32_t tile) {
+  TileHdr h;
+  h.tile_base = (uint64_t)tile * P1_TILE;
+  h.tile_n = (uint32_t)min((uint64_t)P1_TILE, a.n - h.tile_base);
+  h.tlo = __ldg(a.tile_lo + tile);
+  h.thi = __ldg(a.tile_hi + tile) + 1;
+  return h;
+}
+
+__device__ __forceinline__ Full warp_reduce_ordered(Full v, uint32_t lane) {
+  // result in lane 0; lane order = sequence order
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Full u;
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
+    uint32_t* d = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int w = 0; w < 12; ++w) d[w] = __shfl_down_sync(0xffffffffu, s[w], o);
+    if ((lane & (2 * o - 1)) == 0) v = full_combine(v, u);
+  }
+  return v;
+}
+
+// L2 load of a Full written by another CTA of this grid (bypasses L1)
+__device__ __forceinline__ Full ld_full_cg(const Full* p) {
+  Full v;
+  const uint4* s = reinterpret_cast<const uint4*>(p);
+  uint32_t* d = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const uint4 w = __ldcg(s + q);
+    d[4 * q] = w.x; d[4 * q + 1] = w.y; d[4 * q + 2] = w.z; d[4 * q + 3] = w.w;
+  }
+  return v;
+}
+
+// ---- k_p1_reduce: tile aggregates (tile staged by TMA) ---------------
+// Reduce staging buffer: the three u64 columns the fold reads (TMA, 128-byte
+// swizzle as in TileSmem) and the flag bytes.
+struct RedSmem {
+  uint64_t begin[P1_TILE];
+  uint64_t end[P1_TILE];
+  uint64_t parent[P1_TILE];
+  uint8_t flags[P1_TILE];
+};
+constexpr size_t P1_RED_SMEM = sizeof(RedSmem) + 1024;
+
+__global__ void __launch_bounds__(P1_THREADS) k_p1_reduce(P1Args a, const __grid_constant__ P1Maps maps) {
+  extern __shared__ unsigned char red_dyn[];
+  RedSmem& sm = *reinterpret_cast<RedSmem*>(red_dyn + ((1024u - (smem_u32(red_dyn) & 1023u)) & 1023u));
+  __shared__ TraceCache tc;
+  __shared__ Full s_wagg[P1_WARPS];
+  __shared__ __align__(8) uint64_t s_bar;
+  const uint32_t tile = blockIdx.x, warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t j0 = threadIdx.x * P1_ITEMS;
+  const uint64_t tile_base = (uint64_t)tile * P1_TILE;
+  const uint32_t tile_n = (uint32_t)min((uint64_t)P1_TILE, a.n - tile_base);
+  const uint64_t i0 = tile_base + j0;
+  const bool bulk = a.bulk && tile_n == P1_TILE;
+  if (threadIdx.x == 0 && bulk) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&s_bar, P1_TILE * (3 * 8 + 1));
+    const int y = (int)(tile_base / 16);
+    tma_g2s_2d(sm.begin, &maps.begin, 0, y, &s_bar);
+    tma_g2s_2d(sm.end, &maps.end, 0, y, &s_bar);
+    tma_g2s_2d(sm.parent, &maps.parent, 0, y, &s_bar);
+    bulk_g2s(sm.flags, a.flags + tile_base, P1_TILE, &s_bar);
+  }
+  if (!bulk) {
+    for (uint32_t j = threadIdx.x; j < P1_TILE; j += P1_THREADS) {
+      const bool v = j < tile_n;
+      const uint64_t i = tile_base + j;
+      const uint32_t sw = sw128(j);
+      sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
+      sm.begin[sw] = v ? a.begin[i] : 0;
+      sm.end[sw] = v ? a.end[i] : 0;
+      sm.parent[sw] = v ? a.parent[i] : 0;
+    }
+  }
+  const uint32_t tlo = __ldg(a.tile_lo + tile), thi = __ldg(a.tile_hi + tile) + 1;
+  fill_trace_cache(a, tc, tlo, thi);
+  __syncthreads();
+  if (bulk) mbar_wait(&s_bar, 0);
+  const TileTraces tt{a, tc, tlo, thi - tlo <= (uint32_t)P1_TCACHE};
+  Full th = full_identity();
+  if (j0 < tile_n) {
+    const uint32_t r0 = tt.find(i0, thi);
+    const uint64_t fl8 = *reinterpret_cast<const uint64_t*>(sm.flags + j0);
+    th = fold_thread(tt, r0, i0, j0, tile_n, fl8,
+                     [&](int p, uint64_t (&bb)[2], uint64_t (&ee)[2], uint64_t (&pp)[2], uint8_t, uint8_t) {
+                       ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
+                       ld_pair(sm.end, j0 + 2 * p, ee[0], ee[1]);
+                       ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
+                     });
+  }
+  const Full inc = warp_inclusive_fold(th, lane);
+  if (lane == 31) s_wagg[warp] = inc;
+  __syncthreads();
+  if (warp != 0) return;
+  uint32_t last = 0;
+  if (lane == 0) {
+    Full agg = s_wagg[0];
+    for (int w = 1; w < P1_WARPS; ++w) agg = full_combine(agg, s_wagg[w]);
+    a.tile_agg[tile] = agg;
+    // the last tile of a 32-tile group to finish reduces the group
+    __threadfence();
+    const uint32_t g = tile >> 5, gsize = min(32u, a.ntiles - (g << 5));
+    last = atomicAdd(a.group_done + g, 1u) == gsize - 1;
+  }
+  if (__shfl_sync(0xffffffffu, last, 0)) {
+    __threadfence();
+    const uint32_t g = tile >> 5, k = (g << 5) + lane;
+    const Full v = warp_reduce_ordered(k < a.ntiles ? ld_full_cg(a.tile_agg + k) : full_identity(), lane);
+    if (lane == 0) a.group_sum[g] = v;
+  }
+}
+
+// ---- k_p1_scan: exclusive prefixes of the 32-tile group totals -------------
+// One CTA. The group totals come from k_p1_reduce (the last tile of each group
+// to finish reduces the group); a block scan gives gprefix[g] (exclusive) and
+// gprefix[ngroups] = the grand total. k_pass1 finishes a tile's prefix with one
+// warp reduction over the <= 31 preceding tiles of its group.
+__global__ void __launch_bounds__(P1_SCAN_THREADS) k_p1_scan(const Full* __restrict__ gsum, uint32_t ngroups,
+                                                             Full* __restrict__ gprefix) {
+  __shared__ Full s_w[P1_SCAN_THREADS / 32];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t per = (ngroups + P1_SCAN_THREADS - 1) / P1_SCAN_THREADS;
+  const uint32_t lo = min(ngroups, threadIdx.x * per), hi = min(ngroups, lo + per);
+  Full th = full_identity();
+  for (uint32_t k = lo; k < hi; ++k) th = full_combine(th, gsum[k]);
+  const Full inc = warp_inclusive(th, lane);
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) s_w[lane] = warp_inclusive(s_w[lane], lane);  // inclusive over warps
+  __syncthreads();
+  Full run = warp > 0 ? s_w[warp - 1] : full_identity();
+  {
+    Full ex;
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(&inc);
+    uint32_t* d = reinterpret_cast<uint32_t*>(&ex);
+#pragma unroll
+    for (int w = 0; w < 12; ++w) d[w] = __shfl_up_sync(0xffffffffu, s[w], 1);
+    if (lane > 0) run = full_combine(run, ex);
+  }
+  for (uint32_t k = lo; k < hi; ++k) {
+    gprefix[k] = run;
+    run = full_combine(run, gsum[k]);
+  }
+  if (threadIdx.x == P1_SCAN_THREADS - 1) gprefix[ngroups] = s_w[31];
+}
+
+// ---- k_p1_tile_prefix: exclusive prefix of every tile (one warp per tile) ---
+// group prefix + ordered reduction over the preceding tiles of the group.
+__global__ void k_p1_tile_prefix(const Full* __restrict__ agg, const Full* __restrict__ gprefix, uint32_t ntiles,
+                                 Full* __restrict__ excl) {
+  const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = lane_id();
+  if (tile >= ntiles) return;
+  const uint32_t gbase = tile & ~31u;
+  const Full v = warp_reduce_ordered(gbase + lane < tile ? agg[gbase + lane] : full_identity(), lane);
+  if (lane == 0) excl[tile] = full_combine(gprefix[tile >> 5], v);
+}
+
+// ---- k_pass1: per-span outputs ----------------------------------------------
+__global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const __grid_constant__ P1Maps maps) {
+  extern __shared__ unsigned char p1_dyn[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(p1_dyn + ((1024u - (smem_u32(p1_dyn) & 1023u)) & 1023u));
+  __shared__ Full s_wagg[P1_WARPS];
+  __shared__ Full s_prefix;
+  __shared__ TraceCache tc;
+  __shared__ __align__(8) uint64_t s_bar;
+
+  const uint32_t tile = blockIdx.x, warp = threadIdx.x >> 5, lane = lane_id();
+  const TileHdr hd = tile_hdr(a, tile);
+  const uint64_t tile_base = hd.tile_base;
+  const uint32_t tile_n = hd.tile_n, tlo = hd.tlo, thi = hd.thi;
+  const bool bulk = a.bulk && tile_n == P1_TILE;
+  if (threadIdx.x == 0 && bulk) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&s_bar, P1_TILE * (4 * 8 + 1));
+    const int y = (int)(tile_base / 16);
+    tma_g2s_2d(sm.begin, &maps.begin, 0, y, &s_bar);
+    tma_g2s_2d(sm.end, &maps.end, 0, y, &s_bar);
+    tma_g2s_2d(sm.cid, &maps.cid, 0, y, &s_bar);
+    tma_g2s_2d(sm.parent, &maps.parent, 0, y, &s_bar);
+    bulk_g2s(sm.flags, a.flags + tile_base, P1_TILE, &s_bar);
+  }
+  fill_trace_cache(a, tc, tlo, thi);
+  if (threadIdx.x == 0) s_prefix = a.tile_excl[tile];
+  if (!bulk) {
+    for (uint32_t j = threadIdx.x; j < P1_TILE; j += P1_THREADS) {
+      const bool v = j < tile_n;
+      const uint64_t i = tile_base + j;
+      const uint32_t s = sw128(j);
+      sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
+      sm.begin[s] = v ? a.begin[i] : 0;
+      sm.end[s] = v ? a.end[i] : 0;
+      sm.cid[s] = v ? a.cid[i] : 0;
+      sm.parent[s] = v ? a.parent[i] : 0;
     }
   }
   __syncthreads();
-  if (lbw) {
-    if (lane == 0 && tile > 0) desc_store(a.tile_desc + 2 * tile + 1, full_combine(s_prefix, s_agg), DESC_INC);
-    return;
-  }
-  if (a.dbg && threadIdx.x == 0) a.dbg[tile * 16 + 3] = gtimer();
+  if (bulk) mbar_wait(&s_bar, 0);
+  const TileTraces tt{a, tc, tlo, thi - tlo <= (uint32_t)P1_TCACHE};
+  const uint32_t j0 = threadIdx.x * P1_ITEMS;  // thread's first local index
+  const uint64_t i0 = tile_base + j0;
+  uint32_t r0 = 0;
+  if (j0 < tile_n) r0 = tt.find(i0, thi);
+  const uint64_t fl8 = *reinterpret_cast<const uint64_t*>(sm.flags + j0);
 
+  // ---- phase 1 (recomputed from shared memory): thread fold + warp scan
+  Full lane_ex;  // exclusive prefix of the thread within its warp
+  {
+    const Full th = j0 < tile_n ? fold_thread(tt, r0, i0, j0, tile_n, fl8,
+                                              [&](int p, uint64_t (&bb)[2], uint64_t (&ee)[2], uint64_t (&pp)[2],
+                                                  uint8_t, uint8_t) {
+                                                ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
+                                                ld_pair(sm.end, j0 + 2 * p, ee[0], ee[1]);
+                                                ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
+                                              })
+                                : full_identity();
+    const Full inc = warp_inclusive_fold(th, lane);
+    if (lane == 31) s_wagg[warp] = inc;
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(&inc);
+    uint32_t* d = reinterpret_cast<uint32_t*>(&lane_ex);
+#pragma unroll
+    for (int w = 0; w < 12; ++w) d[w] = __shfl_up_sync(0xffffffffu, s[w], 1);
+    if (lane == 0) lane_ex = full_identity();
+  }
+  __syncthreads();
   Full carry = s_prefix;
   for (uint32_t w = 0; w < warp; ++w) carry = full_combine(carry, s_wagg[w]);
   carry = full_combine(carry, lane_ex);
@@ -644,7 +818,7 @@ __global__ void __launch_bounds__(P1_THREADS, 3) k_pass1(P1Args a, const __grid_
   if (j0 >= tile_n) return;
   TraceAttrs ta;
   uint32_t r = r0;
-  load_attrs(r, ta);
+  tt.load(r, ta);
   uint32_t g = carry.c, c_metric = carry.c_metric, c_lay = carry.c_lay, c_kl = carry.c_kl, c_ex = carry.c_ex;
   uint64_t lastE = carry.last_end1, lastM = carry.last_M1, runM = carry.run_M1;
   // predecessor of the first span, for the timeline-order check
@@ -669,20 +843,20 @@ __global__ void __launch_bounds__(P1_THREADS, 3) k_pass1(P1Args a, const __grid_
       const uint8_t f = (uint8_t)(fl8 >> (8 * k));
       const uint64_t b = bb[h], e = ee[h];
       if (i >= ta.next) {
-        do { ++r; } while (t_off(r + 1) <= i);
-        load_attrs(r, ta);
+        do { ++r; } while (tt.off(r + 1) <= i);
+        tt.load(r, ta);
       }
       const uint32_t t = tlo + r;
       const bool head = ta.cur == i;
       if (head) {
         lastE = lastM = runM = 0;
-        int64_t tt = t;
+        int64_t tx = t;
         do {
-          a.t_layer_off[tt] = g;
-          a.t_kl_off[tt] = c_kl;
-          a.t_ex_off[tt] = c_ex;
-          --tt;
-        } while (tt >= 0 && __ldg(a.off + tt) == i);
+          a.t_layer_off[tx] = g;
+          a.t_kl_off[tx] = c_kl;
+          a.t_ex_off[tx] = c_ex;
+          --tx;
+        } while (tx >= 0 && __ldg(a.off + tx) == i);
       } else if (i > 0 && pb >= b) {
         // timeline order (begin_ns, rank, span_id) within the trace (span.hpp:161-163)
         bool bad = pb > b;
@@ -767,20 +941,14 @@ __global__ void __launch_bounds__(P1_THREADS, 3) k_pass1(P1Args a, const __grid_
       }
     }
   }
-  if (a.dbg && threadIdx.x == 0) a.dbg[tile * 16 + 4] = gtimer();
 }
 // Offsets of traces that start at or after the end of the span table (empty
 // trailing traces) and the [T] sentinel.
 __global__ void k_pass1_tail(const uint64_t* __restrict__ off, uint32_t T, uint64_t n,
-                             const TileDesc* __restrict__ tile_desc, uint32_t ntiles,
+                             const Full* __restrict__ tile_prefix, uint32_t ntiles,
                              uint32_t* t_layer_off, uint32_t* t_kl_off, uint32_t* t_ex_off,
                              uint32_t* totals) {
-  Full tot = full_identity();
-  if (ntiles) {
-    uint4 w[4];
-    for (int q = 0; q < 4; ++q) w[q] = tile_desc[2 * ntiles - 1].w[q];
-    desc_unpack(w, DESC_INC, tot);
-  }
+  const Full tot = ntiles ? tile_prefix[(ntiles + 31) / 32] : full_identity();
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= T; t += gridDim.x * blockDim.x) {
     if (off[t] >= n) {
       t_layer_off[t] = tot.c;
@@ -1454,16 +1622,15 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.mb = mb;
   a.me = me;
   a.msid = msid;
-  a.tile_ticket = ctx->d<uint32_t>("c.ticket", 1);
   a.tile_lo = tile_lo;
   a.tile_hi = tile_hi;
-  a.tile_desc = ctx->d<TileDesc>("c.tile_desc", 2ull * ntiles + 2);
-  a.dbg = nullptr;
-  const char* p1_trace = getenv("XSP_P1_TRACE");
-  if (p1_trace) {
-    a.dbg = ctx->d<unsigned long long>("c.p1dbg", 16ull * ntiles + 16);
-    XSP_CUDA(cudaMemsetAsync(a.dbg, 0, (16ull * ntiles + 16) * 8, st));
-  }
+  a.tile_agg = ctx->d<Full>("c.tile_agg", ntiles + 1);
+  a.tile_prefix = ctx->d<Full>("c.tile_prefix", ntiles / 32 + 2);
+  a.ntiles = ntiles;
+  a.tile_excl = ctx->d<Full>("c.tile_excl", ntiles + 1);
+  a.group_sum = ctx->d<Full>("c.tile_gsum", ntiles / 32 + 2);
+  a.group_done = ctx->d<uint32_t>("c.group_done", ntiles / 32 + 2);
+  XSP_CUDA(cudaMemsetAsync(a.group_done, 0, (ntiles / 32 + 2) * 4, st));
   a.unsorted = counters + 5;
   a.err_key = err_key;
   a.layer_row = ctx->d<uint32_t>("o.layer_row", n);
@@ -1489,11 +1656,10 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.amb_count = counters + 1;
   a.pend_kl = ctx->d<uint32_t>("c.pend_kl", n);
   a.pend_count = counters + 2;
-  XSP_CUDA(cudaMemsetAsync(a.tile_ticket, 0, 4, st));
-  XSP_CUDA(cudaMemsetAsync(a.tile_desc, 0, (2ull * ntiles + 2) * sizeof(TileDesc), st));
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   a.bulk = n >= (uint64_t)P1_TILE && al16(c->begin_ns) && al16(c->end_ns) && al16(c->cid) &&
            al16(c->parent_id) && al16(c->flags);
+  a.aligned = al16(c->begin_ns) && al16(c->end_ns) && (reinterpret_cast<uintptr_t>(c->flags) & 7u) == 0;
   P1Maps maps;
   memset(&maps, 0, sizeof(maps));
   if (a.bulk) {
@@ -1504,22 +1670,22 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   }
   if (ntiles) {
     XSP_CUDA(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM));
+    ctx->stage_begin("pass1_reduce", st);
+    XSP_CUDA(cudaFuncSetAttribute(k_p1_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_RED_SMEM));
+    k_p1_reduce<<<ntiles, P1_THREADS, P1_RED_SMEM, st>>>(a, maps);
+    ctx->stage_end("pass1_reduce", st);
+    ctx->stage_begin("pass1_scan", st);
+    k_p1_scan<<<1, P1_SCAN_THREADS, 0, st>>>(a.group_sum, (ntiles + 31) / 32, a.tile_prefix);
+    k_p1_tile_prefix<<<ceil_div((uint64_t)ntiles * 32, 256), 256, 0, st>>>(a.tile_agg, a.tile_prefix, ntiles,
+                                                                           a.tile_excl);
+    ctx->stage_end("pass1_scan", st);
     ctx->stage_begin("pass1", st);
     k_pass1<<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
     ctx->stage_end("pass1", st);
-    ++ctx->launches;
-    if (p1_trace) {
-      std::vector<unsigned long long> h(16ull * ntiles);
-      XSP_CUDA(cudaMemcpyAsync(h.data(), a.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st));
-      XSP_CUDA(cudaStreamSynchronize(st));
-      if (FILE* f = fopen(p1_trace, "wb")) {
-        fwrite(h.data(), 8, h.size(), f);
-        fclose(f);
-      }
-    }
+    ctx->launches += 4;
   }
   uint32_t* totals = ctx->d<uint32_t>("c.totals", 8);
-  k_pass1_tail<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(off, T, n, a.tile_desc, ntiles, a.t_layer_off,
+  k_pass1_tail<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(off, T, n, a.tile_prefix, ntiles, a.t_layer_off,
                                                                a.t_kl_off, a.t_ex_off, totals);
   ++ctx->launches;
   uint32_t* htot = ctx->h<uint32_t>("c.totals_h", 16);
