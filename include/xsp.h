@@ -14,7 +14,7 @@
  *   assign_parents + correlate_async (:154,161) (both inside xsp_correlate)
  *   a8..a15, model_roofline (analysis.hpp:256-366) xsp_analyze
  *   LeveledRunGroup + compute_overhead (leveled.hpp:60-109) xsp_leveled
- *   validate_bundle (span.hpp:187)              xsp_validate
+ *   validate_bundle (span.hpp:187)              xsp_validate / xsp_validate_host
  *   sort_timeline (span.hpp:190)                xsp_sort_timeline
  *
  * Ownership: the caller owns all inputs. Result columns live in ctx-owned device
@@ -278,6 +278,51 @@ typedef struct xsp_overhead_out {
   double* accurate;       /* [n_events] accurate_latency_ns, NaN if no set qualifies */
 } xsp_overhead_out;
 
+/* ---- bundle validation (stage a) ------------------------------------------- */
+
+/* validate_bundle (span.cpp:129-192) rules, in the reference's per-span report
+ * order, then the bundle-level rules. */
+enum {
+  XSP_V_NEG_DURATION = 0,  /* "negative duration"            */
+  XSP_V_CID_MISSING = 1,   /* "correlation_id missing"       */
+  XSP_V_CID_ON_SYNC = 2,   /* "correlation_id on sync span"  */
+  XSP_V_DUP_SPAN_ID = 3,   /* "duplicate span_id"            */
+  XSP_V_TRACE_ID = 4,      /* "trace_id mismatch"            */
+  XSP_V_OUT_OF_ORDER = 5,  /* "out of order"                 */
+  XSP_V_NEG_FLOPS = 6,     /* "negative metric" flop_count_sp    */
+  XSP_V_NEG_READ = 7,      /* "negative metric" dram_read_bytes  */
+  XSP_V_NEG_WRITE = 8,     /* "negative metric" dram_write_bytes */
+  XSP_V_OCC_RANGE = 9,     /* "occupancy out of range"       */
+  XSP_V_NO_MODEL = 10,     /* "model span missing"      (bundle level) */
+  XSP_V_MULTI_MODEL = 11,  /* "multiple model spans"    (bundle level) */
+  XSP_V_MODEL_LEVEL = 12   /* "model level disabled"    (bundle level) */
+};
+
+/* Raw-tag facts the decoded metric columns cannot carry (metrics_from_tags
+ * clamps negatives, span.cpp:88-101), recorded by the ingest side per span. */
+#define XSP_TAG_NEG_FLOPS 0x01u  /* flop_count_sp tag is an int64 < 0     */
+#define XSP_TAG_NEG_READ 0x02u   /* dram_read_bytes tag is an int64 < 0   */
+#define XSP_TAG_NEG_WRITE 0x04u  /* dram_write_bytes tag is an int64 < 0  */
+#define XSP_TAG_OCC_DOUBLE 0x08u /* achieved_occupancy tag holds a double */
+
+/* Optional validation inputs (any pointer may be NULL: the rule it feeds is
+ * then skipped). Same memory space as the columns. */
+typedef struct xsp_validate_in {
+  const uint64_t* trace_id;      /* [n_spans] Span::trace_id                      */
+  const uint64_t* meta_trace_id; /* [n_traces] RunMeta::trace_id (with trace_id)  */
+  const uint8_t* tag_bits;       /* [n_spans] XSP_TAG_* bits                       */
+} xsp_validate_in;
+
+/* ValidationReport of every trace: issues of trace t are
+ * [trace_issue_off[t], trace_issue_off[t+1]) in report order. issue_row is the
+ * global span row (UINT32_MAX for bundle-level issues, whose span_id is 0). */
+typedef struct xsp_validation_out {
+  uint64_t n_issues;
+  uint32_t* trace_issue_off; /* [n_traces + 1] */
+  uint32_t* issue_row;
+  uint8_t* issue_rule;       /* XSP_V_* */
+} xsp_validation_out;
+
 /* ---- API ------------------------------------------------------------------ */
 
 xsp_status xsp_ctx_create(int device, xsp_ctx** out);
@@ -343,6 +388,14 @@ xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* host_cols,
                         const xsp_traces* host_traces, const xsp_groups* groups,
                         const xsp_system_spec* spec, const xsp_analysis_opts* opts,
                         xsp_corr_out* corr_host, xsp_tables_out* tables_host, void* stream);
+
+/* validate_bundle (span.cpp:129-192) for every trace. Device pointers; the
+ * result columns are ctx-owned device memory. Synchronous (one count read-back). */
+xsp_status xsp_validate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
+                        const xsp_validate_in* in, xsp_validation_out* out, void* stream);
+/* Host-buffer form (results in ctx-owned pinned host memory). */
+xsp_status xsp_validate_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
+                             const xsp_validate_in* in, xsp_validation_out* out);
 
 /* Bytes moved host->device and device->host by the last xsp_run_host call. */
 void xsp_last_transfer_bytes(const xsp_ctx* ctx, uint64_t* h2d, uint64_t* d2h);

@@ -78,6 +78,8 @@ def lib() -> C.CDLL:
         L.xspref_analyze.argtypes = [C.POINTER(SoaIn), P, P, C.c_uint32, C.c_double, C.c_double]
         L.xspref_analyze.restype = P
         L.xspref_leveled.argtypes = [C.POINTER(SoaIn), C.c_double, C.c_double]
+        L.xspref_validate.argtypes = [C.POINTER(SoaIn), C.c_void_p, C.c_void_p]
+        L.xspref_validate.restype = P
         L.xspref_leveled.restype = P
         L.xspref_time_pipeline.argtypes = [C.POINTER(SoaIn), P, P, C.c_uint32, C.c_int, C.c_int]
         L.xspref_time_pipeline.restype = C.c_double
@@ -208,6 +210,19 @@ def analyze(b, first: Sequence[int], runs: Sequence[int], trim=0.2, noise=0.01):
     f = np.ascontiguousarray(first, dtype=np.uint32)
     r = np.ascontiguousarray(runs, dtype=np.uint32)
     return read_bag(lib().xspref_analyze(C.byref(s), f.ctypes.data, r.ctypes.data, f.size, trim, noise))
+
+
+def validate(b, span_trace_id=None, tag_bits=None):
+    """validate_bundle per trace: list (per trace) of (span_id, rule, detail)."""
+    s, keep = soa_in(b)
+    tid = None if span_trace_id is None else np.ascontiguousarray(span_trace_id, dtype=np.uint64)
+    tb = None if tag_bits is None else np.ascontiguousarray(tag_bits, dtype=np.uint8)
+    arrays, strings = read_bag(lib().xspref_validate(C.byref(s), None if tid is None else tid.ctypes.data,
+                                                     None if tb is None else tb.ctypes.data))
+    out = [[] for _ in range(b.n_traces)]
+    for t, sid, rule, det in zip(arrays["trace"], arrays["span_id"], strings["rule"], strings["detail"]):
+        out[int(t)].append((int(sid), rule.decode(), det.decode()))
+    return out
 
 
 def leveled(b, trim=0.2, noise=0.01):

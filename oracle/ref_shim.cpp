@@ -519,6 +519,46 @@ XSPREF_API void* xspref_correlate(const SoaIn* in) {
   return bag;
 }
 
+/// validate_bundle() (span.cpp:129-192) per trace. span_trace_id (optional)
+/// overrides Span::trace_id; tag_bits (optional, XSP_TAG_* of include/xsp.h)
+/// turns metric tags into raw forms the decoded columns cannot carry: bits 0-2
+/// store an int64 < 0 under flop_count_sp / dram_read_bytes / dram_write_bytes,
+/// and a metric span WITHOUT bit 3 stores achieved_occupancy as an int64 tag.
+XSPREF_API void* xspref_validate(const SoaIn* in, const std::uint64_t* span_trace_id,
+                                 const std::uint8_t* tag_bits) {
+  std::vector<TraceBundle> bundles = import_soa(*in);
+  std::uint64_t row = 0;
+  for (auto& b : bundles) {
+    for (auto& sp : b.spans) {
+      if (span_trace_id) sp.trace_id = span_trace_id[row];
+      if (tag_bits) {
+        const std::uint8_t tb = tag_bits[row];
+        const char* keys[3] = {kTagFlopCountSp, kTagDramReadBytes, kTagDramWriteBytes};
+        for (int k = 0; k < 3; ++k)
+          if (tb & (1u << k)) sp.tags[keys[k]] = static_cast<std::int64_t>(-1 - (std::int64_t)(row % 7));
+        auto it = sp.tags.find(kTagAchievedOccupancy);
+        if (it != sp.tags.end() && !(tb & 8u))
+          it->second = static_cast<std::int64_t>(std::get<double>(it->second));
+      }
+      ++row;
+    }
+  }
+  auto* bag = new Bag;
+  bag->ensure("trace", 'I');
+  bag->ensure("span_id", 'Q');
+  bag->str_init("rule");
+  bag->str_init("detail");
+  for (std::size_t t = 0; t < bundles.size(); ++t) {
+    for (const auto& issue : validate_bundle(bundles[t])) {
+      bag->u32("trace", static_cast<std::uint32_t>(t));
+      bag->u64("span_id", issue.span_id);
+      bag->str("rule", issue.rule);
+      bag->str("detail", issue.detail);
+    }
+  }
+  return bag;
+}
+
 /// Wall-clock timing of the reference hot path (correlate + a8..a15) over a
 /// set of groups, `threads` workers with one group per task. Returns seconds.
 /// groups: [first_trace, n_runs] pairs.

@@ -135,6 +135,33 @@ class OverheadOut(C.Structure):
                 ("overhead", f64p), ("step_flags", u8p), ("accurate", f64p)]
 
 
+class ValidateIn(C.Structure):
+    _fields_ = [("trace_id", u64p), ("meta_trace_id", u64p), ("tag_bits", u8p)]
+
+
+class ValidationOut(C.Structure):
+    _fields_ = [("n_issues", C.c_uint64), ("trace_issue_off", u32p), ("issue_row", u32p),
+                ("issue_rule", u8p)]
+
+
+# validate_bundle rules (xsp.h XSP_V_*) with the reference's (rule, detail) texts (span.cpp:129-192)
+VALIDATION_RULES = [
+    ("negative duration", "end_ns precedes begin_ns"),
+    ("correlation_id missing", "launch/exec spans require a correlation_id"),
+    ("correlation_id on sync span", "sync spans must not carry a correlation_id"),
+    ("duplicate span_id", ""),
+    ("trace_id mismatch", "span belongs to a different trace"),
+    ("out of order", "timeline must be sorted by (begin_ns, rank, span_id)"),
+    ("negative metric", "flop_count_sp"),
+    ("negative metric", "dram_read_bytes"),
+    ("negative metric", "dram_write_bytes"),
+    ("occupancy out of range", "achieved_occupancy must lie in [0,1]"),
+    ("model span missing", "a bundle requires exactly one model/sync span"),
+    ("multiple model spans", "a bundle requires exactly one model/sync span"),
+    ("model level disabled", "profiling_levels must always contain model"),
+]
+TAG_NEG_FLOPS, TAG_NEG_READ, TAG_NEG_WRITE, TAG_OCC_DOUBLE = 1, 2, 4, 8
+
 L_OK, L_TOO_FEW, L_NOT_CHAIN, L_AMBIGUOUS, L_TRACE_FAILED = range(5)
 EV_IN_NARROW, EV_IN_WIDE, EV_CLAMPED, EV_NEGATIVE = 1, 2, 4, 8
 
@@ -144,7 +171,7 @@ EXPORTS = [
     "xsp_analyze", "xsp_run_host", "xsp_last_transfer_bytes", "xsp_last_launch_count",
     "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host", "xsp_set_profiling", "xsp_stage_reset",
     "xsp_stage_times", "xsp_leveled", "xsp_sort_timeline_host", "xsp_correlate_host",
-    "xsp_analyze_host", "xsp_leveled_host",
+    "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host",
 ]
 
 _lib = None
@@ -203,5 +230,11 @@ def load() -> C.CDLL:
     lib.xsp_sort_timeline_host.restype = C.c_int32
     lib.xsp_correlate_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.c_int, C.POINTER(CorrOut)]
     lib.xsp_correlate_host.restype = C.c_int32
+    lib.xsp_validate.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(ValidateIn),
+                                 C.POINTER(ValidationOut), P]
+    lib.xsp_validate.restype = C.c_int32
+    lib.xsp_validate_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(ValidateIn),
+                                      C.POINTER(ValidationOut)]
+    lib.xsp_validate_host.restype = C.c_int32
     _lib = lib
     return lib

@@ -15,6 +15,8 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
                       xsp_tables_out* tab_host);
 void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const uint8_t* flags, const uint64_t* sid,
                        uint32_t T, const uint64_t* off, uint32_t* perm, uint32_t* was_sorted, cudaStream_t st);
+void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, const xsp_validate_in* vin,
+                  xsp_validation_out* out, cudaStream_t st);
 }
 
 namespace {
@@ -302,6 +304,43 @@ XSP_API xsp_status xsp_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xs
       throw std::invalid_argument("null level-set column");
     std::memset(out, 0, sizeof(*out));
     xsp::run_leveled(ctx, cols, corr, sets, opts, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_validate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
+                                const xsp_validate_in* in, xsp_validation_out* out, void* stream) {
+  return guard(ctx, "xsp_validate", [&] {
+    check_cols(cols, traces);
+    if (!traces || !out) throw std::invalid_argument("null argument");
+    std::memset(out, 0, sizeof(*out));
+    xsp::run_validate(ctx, cols, traces, in, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_validate_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht,
+                                     const xsp_validate_in* hin, xsp_validation_out* out) {
+  return guard(ctx, "xsp_validate_host", [&] {
+    check_cols(hc, ht);
+    if (!ht || !out) throw std::invalid_argument("null argument");
+    cudaStream_t st = nullptr;
+    ctx->h2d_bytes = ctx->d2h_bytes = 0;
+    xsp_span_cols dc = upload_cols(ctx, hc, st);
+    xsp_traces dt = upload_traces(ctx, ht, st);
+    xsp_validate_in din{nullptr, nullptr, nullptr};
+    if (hin) {
+      const uint64_t n = hc->n_spans;
+      if (hin->trace_id) din.trace_id = to_dev(ctx, "v.trace_id", hin->trace_id, n, st);
+      if (hin->meta_trace_id) din.meta_trace_id = to_dev(ctx, "v.meta_tid", hin->meta_trace_id, ht->n_traces, st);
+      if (hin->tag_bits) din.tag_bits = to_dev(ctx, "v.tag_bits", hin->tag_bits, n, st);
+    }
+    xsp_validation_out d;
+    std::memset(&d, 0, sizeof(d));
+    xsp::run_validate(ctx, &dc, &dt, &din, &d, st);
+    out->n_issues = d.n_issues;
+    out->trace_issue_off = to_host(ctx, "v.trace_off", d.trace_issue_off, (uint64_t)ht->n_traces + 1, st);
+    out->issue_row = to_host(ctx, "v.row", d.issue_row, d.n_issues, st);
+    out->issue_rule = to_host(ctx, "v.rule", d.issue_rule, d.n_issues, st);
+    XSP_CUDA(cudaStreamSynchronize(st));
   });
 }
 

@@ -239,6 +239,36 @@ class Engine:
         self.lib.xsp_stage_times(self.ctx, n, names, ms, cnt)
         return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(n)}
 
+    def validate(self, batch: SpanBatch, span_trace_id: Optional[np.ndarray] = None,
+                 tag_bits: Optional[np.ndarray] = None) -> List[List[Tuple[int, int]]]:
+        """validate_bundle (span.cpp:129-192) of every trace (xsp_validate_host).
+
+        span_trace_id: per-span Span::trace_id (checked against batch.trace_id);
+        tag_bits: per-span XSP_TAG_* raw-tag facts. Returns, per trace, the
+        (span row or -1, rule) issues in the reference's report order."""
+        cols, trs = batch.cols(), batch.traces()
+        vin = capi.ValidateIn()
+        keep = []
+        if span_trace_id is not None:
+            a = np.ascontiguousarray(span_trace_id, dtype=np.uint64)
+            m = np.ascontiguousarray(batch.trace_id, dtype=np.uint64)
+            keep += [a, m]
+            vin.trace_id, vin.meta_trace_id = a.ctypes.data_as(capi.u64p), m.ctypes.data_as(capi.u64p)
+        if tag_bits is not None:
+            tb = np.ascontiguousarray(tag_bits, dtype=np.uint8)
+            keep.append(tb)
+            vin.tag_bits = tb.ctypes.data_as(capi.u8p)
+        out = capi.ValidationOut()
+        self._check(self.lib.xsp_validate_host(self.ctx, C.byref(cols), C.byref(trs), C.byref(vin),
+                                               C.byref(out)))
+        n = int(out.n_issues)
+        off = _copy(out.trace_issue_off, capi.u32p, batch.n_traces + 1)
+        row = _copy(out.issue_row, capi.u32p, n).astype(np.int64)
+        rule = _copy(out.issue_rule, capi.u8p, n)
+        row[row == 0xFFFFFFFF] = -1
+        return [list(zip(row[off[t]:off[t + 1]].tolist(), rule[off[t]:off[t + 1]].tolist()))
+                for t in range(batch.n_traces)]
+
     def run_host(self, batch: SpanBatch, groups: Optional[Tuple[Sequence[int], Sequence[int], Sequence[int]]] = None,
                  trim=0.2, noise=0.01, top_k=3, peak_flops=None, mem_bw=None,
                  raw: bool = False) -> Tuple[CorrResult, Tables]:
