@@ -194,6 +194,58 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+class _ShuffledColumns:
+    """The sort_timeline input columns of a corpus with every trace's rows permuted
+    at random (on the device), in the DeviceBatch pointer interface."""
+
+    def __init__(self, dev, b, seed: int):
+        import torch
+        g = torch.Generator(device=dev.t["begin_ns"].device).manual_seed(seed)
+        n = b.n_spans
+        off = dev.t["trace_span_off"]
+        rows = torch.arange(n, device=off.device, dtype=torch.int64)
+        tr = torch.searchsorted(off, rows, right=True) - 1
+        key = tr * (1 << 31) + torch.randint(0, 1 << 31, (n,), device=off.device, generator=g)
+        perm = torch.argsort(key)
+        self.batch = b
+        self.t = {k: dev.t[k][perm].contiguous() for k in ("begin_ns", "flags", "span_id")}
+        self.t["trace_span_off"] = off
+
+    def ptr(self, k):
+        return self.t[k].data_ptr()
+
+
+def measure_sort(eng, dev, b, steps: int, local: int):
+    """sort_timeline on a per-trace shuffled copy of the corpus:
+    device-resident, CUDA events around `steps` calls."""
+    import torch
+    sh = _ShuffledColumns(dev, b, seed=11)
+    perm = torch.empty(b.n_spans, dtype=torch.int32, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        assert not eng.sort_timeline_device(sh, perm.data_ptr(), stream)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        eng.sort_timeline_device(sh, perm.data_ptr(), stream)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    # spot check against a stable lexsort on a sample of traces
+    off = b.trace_span_off
+    p = perm.cpu().numpy().view(np.uint32)
+    bg, fl, sid = (sh.t[k].cpu().numpy() for k in ("begin_ns", "flags", "span_id"))
+    for t in range(0, b.n_traces, max(1, b.n_traces // 16)):
+        lo, hi = int(off[t]), int(off[t + 1])
+        lv = fl[lo:hi].astype(np.int64) & 3
+        want = lo + np.lexsort((sid[lo:hi], np.where(lv >= 2, 3, lv + 1), bg[lo:hi]))
+        assert np.array_equal(p[lo:hi], want.astype(np.uint32)), f"sort mismatch in trace {t}"
+    return {"metric": "M spans/s sorted (sort_timeline, shuffled traces)", "value": b.n_spans / (ms / 1e3) / 1e6,
+            "unit": UNIT, "ms_per_step": ms, "gbs": 21.0 * b.n_spans / (ms / 1e3) / 1e9,
+            "input": "C3 corpus, rows of every trace permuted at random on the device"}
+
+
 def config(args):
     return {"workload": "C3: 65 synthetic models x 8 batch sizes (1..128) x R iterations, correlate + "
                         "a8..a15 + top-3, one group per (model,batch)",
@@ -212,6 +264,7 @@ def main():
     ap.add_argument("--models", type=int, default=65)
     ap.add_argument("--ref-sample-spans", type=int, default=3_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sort", action="store_true", help="skip the shuffled sort_timeline measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -285,6 +338,8 @@ def main():
     e2e = {"value": spans_total / (e_ms / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
 
+    sort_line = measure_sort(eng, dev, b, args.steps, local) if not args.no_sort else None
+
     if rank != 0:
         return
     peak, peak_kind = hbm_peak()
@@ -311,6 +366,12 @@ def main():
         "dominant_stage": dom,
         "clocks": clk.summary(),
     }
+    if sort_line:
+        sort_line["roofline"] = {"bound": "hbm", "bytes_per_span": 21.0, "achieved": sort_line.pop("gbs"),
+                                 "peak": peak, "unit": "GB/s",
+                                 "definition": "read begin_ns+flags+span_id (17 B), write perm (4 B) per span"}
+        sort_line["roofline"]["frac"] = sort_line["roofline"]["achieved"] / peak
+        line["sort_shuffled"] = sort_line
     if world == 1 and not args.no_cpu_baseline:
         from oracle import ref
         if ref.available():

@@ -15,7 +15,7 @@
  *   a8..a15, model_roofline (analysis.hpp:256-366) xsp_analyze
  *   LeveledRunGroup + compute_overhead (leveled.hpp:60-109) xsp_leveled
  *   validate_bundle (span.hpp:187)              xsp_validate / xsp_validate_host
- *   sort_timeline (span.hpp:190)                xsp_sort_timeline
+ *   sort_timeline (span.hpp:190)                xsp_sort_timeline / xsp_sort_timeline_host
  *
  * Ownership: the caller owns all inputs. Result columns live in ctx-owned device
  * memory and stay valid until the next call on the same ctx or xsp_ctx_destroy.
@@ -340,6 +340,13 @@ int xsp_abi_version(void);
 #define XSP_CORR_PARENTS_ONLY 2
 xsp_status xsp_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces, int mode,
                          xsp_corr_out* out, void* stream);
+
+/* sort_timeline (span.cpp:112-127) for every trace, DEVICE pointers (perm is a
+ * caller-owned device array of n_spans): as xsp_sort_timeline_host below.
+ * Synchronous (the presorted check and the fallback decision read back a flag). */
+xsp_status xsp_sort_timeline(xsp_ctx* ctx, uint64_t n_spans, const uint64_t* begin_ns, const uint8_t* flags,
+                             const uint64_t* span_id, uint32_t n_traces, const uint64_t* span_off,
+                             uint32_t* perm, int* was_sorted, void* stream);
 
 /* sort_timeline (span.cpp:112-127) for every trace: perm[j] = input row of the
  * span at position j once each trace [span_off[t], span_off[t+1]) is stably

@@ -171,7 +171,7 @@ EXPORTS = [
     "xsp_analyze", "xsp_run_host", "xsp_last_transfer_bytes", "xsp_last_launch_count",
     "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host", "xsp_set_profiling", "xsp_stage_reset",
     "xsp_stage_times", "xsp_leveled", "xsp_sort_timeline_host", "xsp_correlate_host",
-    "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host",
+    "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline",
 ]
 
 _lib = None
@@ -228,6 +228,8 @@ def load() -> C.CDLL:
     lib.xsp_sort_timeline_host.argtypes = [P, C.c_uint64, u64p, u8p, u64p, C.c_uint32, u64p, u32p,
                                            C.POINTER(C.c_int)]
     lib.xsp_sort_timeline_host.restype = C.c_int32
+    lib.xsp_sort_timeline.argtypes = [P, C.c_uint64, P, P, P, C.c_uint32, P, P, C.POINTER(C.c_int), P]
+    lib.xsp_sort_timeline.restype = C.c_int32
     lib.xsp_correlate_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.c_int, C.POINTER(CorrOut)]
     lib.xsp_correlate_host.restype = C.c_int32
     lib.xsp_validate.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(ValidateIn),

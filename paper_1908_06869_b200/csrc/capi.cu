@@ -344,6 +344,19 @@ XSP_API xsp_status xsp_validate_host(xsp_ctx* ctx, const xsp_span_cols* hc, cons
   });
 }
 
+XSP_API xsp_status xsp_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const uint8_t* flags,
+                                     const uint64_t* span_id, uint32_t n_traces, const uint64_t* span_off,
+                                     uint32_t* perm, int* was_sorted, void* stream) {
+  return guard(ctx, "xsp_sort_timeline", [&] {
+    if (!span_off || !perm || (n && (!begin || !flags || !span_id))) throw std::invalid_argument("null argument");
+    if (n >= 0xFFFFFFF0ull) throw std::invalid_argument("more than 2^32-16 spans in one call");
+    uint32_t sorted = 0;
+    xsp::run_sort_timeline(ctx, n, begin, flags, span_id, n_traces, span_off, perm, &sorted,
+                           static_cast<cudaStream_t>(stream));
+    if (was_sorted) *was_sorted = (int)sorted;
+  });
+}
+
 XSP_API xsp_status xsp_sort_timeline_host(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const uint8_t* flags,
                                           const uint64_t* span_id, uint32_t n_traces, const uint64_t* span_off,
                                           uint32_t* perm, int* was_sorted) {

@@ -1,9 +1,18 @@
 // Stage (b): sort_timeline (span.cpp:112-127) on the device — a stable sort of
-// every trace's spans by (begin_ns, rank(level), span_id), as one LSD radix
-// sort over the composite key (trace, begin_ns, rank, span_id): four stable
-// passes from the least significant field, each skipping the 8-bit digits that
-// are constant over the batch. Presorted input (the TraceBundle invariant) is
-// detected first and returns the identity without sorting.
+// every trace's spans by (begin_ns, rank(level), span_id).
+//
+// Presorted input (the TraceBundle invariant) is detected first and returns the
+// identity without sorting. Otherwise every trace of up to kSegCap spans is
+// sorted by ONE CTA in shared memory: the trace's begin / span_id ranges are
+// reduced, each span gets a packed 63-bit key
+//   (begin - min_begin) | rank | (span_id - min_span_id) | local index
+// (the index makes keys unique, so any sort is stable), a bitonic network
+// sorts the keys in place, and perm is written from the index bits. HBM
+// traffic is one read of begin/span_id/flags and one perm write (21 B/span).
+// Traces that are longer or whose packed key needs more than 63 bits fall back
+// to one global LSD radix sort over the composite key (trace, begin_ns, rank,
+// span_id): four stable passes from the least significant field, each skipping
+// the 8-bit digits that are constant over the batch.
 
 #include "ctx.h"
 #include "prims.cuh"
@@ -56,6 +65,102 @@ __global__ void k_sort_key(int field, const uint32_t* __restrict__ val, const ui
   key[j] = k;
 }
 
+constexpr uint32_t kSegCap = 16384;  // spans per CTA-sorted trace (128 KB of keys)
+constexpr int kSegThreads = 1024;
+
+__device__ __forceinline__ uint32_t bit_width64(uint64_t v) { return v ? 64 - __clzll(v) : 0; }
+
+// One CTA per trace; sets *fallback for traces it cannot take.
+__global__ void __launch_bounds__(kSegThreads) k_sort_seg(const uint64_t* __restrict__ begin,
+                                                          const uint8_t* __restrict__ flags,
+                                                          const uint64_t* __restrict__ sid,
+                                                          const uint64_t* __restrict__ off, uint32_t cap,
+                                                          uint32_t* __restrict__ perm, uint32_t* __restrict__ fallback) {
+  extern __shared__ unsigned long long keys[];
+  __shared__ unsigned long long red[4][kSegThreads / 32];
+  __shared__ uint32_t s_shift[3];
+  __shared__ int s_ok;
+  const uint32_t t = blockIdx.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint64_t lo = off[t], hi = off[t + 1];
+  const uint32_t len = (uint32_t)(hi - lo);
+  if (len <= 1) {
+    if (len == 1 && tid == 0) perm[lo] = (uint32_t)lo;
+    return;
+  }
+  if (len > cap) {
+    if (tid == 0) atomicOr(fallback, 1u);
+    return;
+  }
+  // ranges of begin and span_id
+  uint64_t bmin = ~0ull, bmax = 0, smin = ~0ull, smax = 0;
+  for (uint32_t j = tid; j < len; j += blockDim.x) {
+    const uint64_t b = begin[lo + j], s = sid[lo + j];
+    bmin = min(bmin, b); bmax = max(bmax, b);
+    smin = min(smin, s); smax = max(smax, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+    bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+    smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+  }
+  if (lane == 0) {
+    red[0][warp] = bmin; red[1][warp] = bmax; red[2][warp] = smin; red[3][warp] = smax;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (uint32_t w = 1; w < blockDim.x / 32; ++w) {
+      red[0][0] = min(red[0][0], red[0][w]); red[1][0] = max(red[1][0], red[1][w]);
+      red[2][0] = min(red[2][0], red[2][w]); red[3][0] = max(red[3][0], red[3][w]);
+    }
+    const uint32_t ib = bit_width64(len - 1), sb = bit_width64(red[3][0] - red[2][0]);
+    const uint32_t bb = bit_width64(red[1][0] - red[0][0]);
+    s_ok = ib + sb + 2 + bb <= 63;
+    s_shift[0] = ib;            // span_id field
+    s_shift[1] = ib + sb;       // rank field
+    s_shift[2] = ib + sb + 2;   // begin field
+    if (!s_ok) atomicOr(fallback, 1u);
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  bmin = red[0][0];
+  smin = red[2][0];
+  const uint32_t sh_s = s_shift[0], sh_r = s_shift[1], sh_b = s_shift[2];
+  uint32_t P = 2;
+  while (P < len) P <<= 1;
+  for (uint32_t j = tid; j < P; j += blockDim.x) {
+    unsigned long long k = ~0ull;  // padding sorts last (real keys use <= 63 bits)
+    if (j < len) {
+      const uint32_t l = f_level(flags[lo + j]);
+      const uint64_t r = l >= XSP_LEVEL_KERNEL ? 3 : l + 1;  // rank (span.hpp:51-59)
+      k = ((begin[lo + j] - bmin) << sh_b) | (r << sh_r) | ((sid[lo + j] - smin) << sh_s) | j;
+    }
+    keys[j] = k;
+  }
+  __syncthreads();
+  // bitonic network, ascending. Pair i of a stage with distance j <= 32 touches
+  // elements of the 64-element block 2*32*(i/32) only, and a warp owns whole
+  // blocks, so those stages synchronise the warp instead of the CTA.
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = tid; i < P / 2; i += blockDim.x) {
+        const uint32_t a = 2 * i - (i & (j - 1)), b = a + j;
+        const unsigned long long ka = keys[a], kb = keys[b];
+        const bool up = (a & k) == 0;
+        if ((ka > kb) == up) {
+          keys[a] = kb;
+          keys[b] = ka;
+        }
+      }
+      if (j > 32) __syncthreads(); else __syncwarp();
+    }
+    __syncthreads();
+  }
+  const unsigned long long imask = (1ull << sh_s) - 1;
+  for (uint32_t j = tid; j < len; j += blockDim.x) perm[lo + j] = (uint32_t)(lo + (keys[j] & imask));
+}
+
 }  // namespace
 
 void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const uint8_t* flags, const uint64_t* sid,
@@ -71,6 +176,18 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
   XSP_CUDA(cudaStreamSynchronize(st));
   *was_sorted = h[0] == 0;
   if (*was_sorted || n <= 1) return;
+  // per-trace CTA sort; the global radix sort only if some trace does not fit
+  XSP_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+  XSP_CUDA(cudaFuncSetAttribute(k_sort_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSegCap * 8)));
+  ctx->stage_begin("sort", st);
+  k_sort_seg<<<T, kSegThreads, kSegCap * 8, st>>>(begin, flags, sid, off, kSegCap, perm, flag);
+  ctx->stage_end("sort", st);
+  ++ctx->launches;
+  XSP_CUDA(cudaMemcpyAsync(h, flag, 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  if (!h[0] && !getenv("XSP_SORT_GLOBAL")) return;
+  k_iota_u32<<<blocks(n), 256, 0, st>>>(perm, n);
+  ++ctx->launches;
   uint64_t* key = ctx->d<uint64_t>("s.key", n);
   RadixScratch rs;
   rs.keys_alt = ctx->d<uint64_t>("rs.keys_alt", n);

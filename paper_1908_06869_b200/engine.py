@@ -128,6 +128,10 @@ class DeviceBatch:
             self.t[k] = torch.from_numpy(np.ascontiguousarray(a).view(view)).to(f"cuda:{device}")
         self.nbytes = sum(int(x.numel() * x.element_size()) for x in self.t.values())
 
+    def ptr(self, k) -> int:
+        x = self.t[k]
+        return x.data_ptr() if x.numel() else 0
+
     def _p(self, k, typ):
         x = self.t[k]
         return C.cast(C.c_void_p(x.data_ptr() if x.numel() else 0), typ)
@@ -238,6 +242,27 @@ class Engine:
         cnt = (C.c_uint64 * max(n, 1))()
         self.lib.xsp_stage_times(self.ctx, n, names, ms, cnt)
         return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(n)}
+
+    def sort_timeline(self, batch: SpanBatch) -> Tuple[np.ndarray, bool]:
+        """sort_timeline (span.cpp:112-127) of every trace: (perm, was_sorted), perm[j] =
+        input row of the span at position j (xsp_sort_timeline_host)."""
+        perm = np.zeros(max(batch.n_spans, 1), dtype=np.uint32)
+        ws = C.c_int()
+        self._check(self.lib.xsp_sort_timeline_host(
+            self.ctx, batch.n_spans, batch.begin_ns.ctypes.data_as(capi.u64p),
+            batch.flags.ctypes.data_as(capi.u8p), batch.span_id.ctypes.data_as(capi.u64p), batch.n_traces,
+            batch.trace_span_off.ctypes.data_as(capi.u64p), perm.ctypes.data_as(capi.u32p), C.byref(ws)))
+        return perm[:batch.n_spans], bool(ws.value)
+
+    def sort_timeline_device(self, dbatch: "DeviceBatch", perm_ptr: int, stream=None) -> bool:
+        """Device-resident sort_timeline into a caller-owned device u32 array."""
+        b = dbatch
+        ws = C.c_int()
+        self._check(self.lib.xsp_sort_timeline(
+            self.ctx, b.batch.n_spans, C.c_void_p(b.ptr("begin_ns")), C.c_void_p(b.ptr("flags")),
+            C.c_void_p(b.ptr("span_id")), b.batch.n_traces, C.c_void_p(b.ptr("trace_span_off")),
+            C.c_void_p(perm_ptr), C.byref(ws), C.c_void_p(stream)))
+        return bool(ws.value)
 
     def validate(self, batch: SpanBatch, span_trace_id: Optional[np.ndarray] = None,
                  tag_bits: Optional[np.ndarray] = None) -> List[List[Tuple[int, int]]]:
