@@ -246,6 +246,54 @@ def measure_sort(eng, dev, b, steps: int, local: int):
             "input": "C3 corpus, rows of every trace permuted at random on the device"}
 
 
+def measure_c4(eng, args, rank: int, world: int, local: int, dist):
+    """BASELINE config 4: one long trace (synth.c4), time-range sharded over the
+    ranks at quiescent cuts (timeshard.py); every rank correlates + analyses its
+    shard device-resident, timed with CUDA events, max over ranks. Total work is
+    fixed as ranks are added (strong scaling)."""
+    import torch
+    from paper_1908_06869_b200 import synth, timeshard
+    from paper_1908_06869_b200.engine import DeviceBatch
+    b = synth.c4(n_layers=args.c4_layers)
+    starts = timeshard.choose_cuts(timeshard.quiescent_cuts(b), b.n_spans, world)
+    bounds = starts + [b.n_spans]
+    if rank < len(starts):
+        rows = timeshard.shard_rows(b, bounds[rank], bounds[rank + 1])
+        sub = timeshard.sub_batch(b, rows)[0] if world > 1 else b
+    else:
+        sub = None
+    ms = 0.0
+    if sub is not None:
+        dev = DeviceBatch(sub, local)
+        groups = ([0], [1], [1])
+        stream = torch.cuda.current_stream().cuda_stream
+
+        def step():
+            co = eng.correlate_device(dev, stream=stream)
+            eng.analyze_device(dev, co, groups, stream=stream)
+
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(max(1, args.steps // 2)):
+            step()
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / max(1, args.steps // 2)
+        del dev
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"metric": "M spans/s correlated+analyzed, one long trace time-range sharded",
+            "value": b.n_spans / (ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": ms, "spans": b.n_spans,
+            "layers": args.c4_layers, "shards": len(starts), "scaling": "strong",
+            "workload": "C4: synth.c4, 1 model span, layers x ~3 kernels (1% long layers of 8..64), "
+                        "executions on 4 interleaved streams, a drain every 2000 layers"}
+
+
 def config(args):
     return {"workload": "C3: 65 synthetic models x 8 batch sizes (1..128) x R iterations, correlate + "
                         "a8..a15 + top-3, one group per (model,batch)",
@@ -265,6 +313,8 @@ def main():
     ap.add_argument("--ref-sample-spans", type=int, default=3_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sort", action="store_true", help="skip the shuffled sort_timeline measurement")
+    ap.add_argument("--c4-layers", type=int, default=28_600_000,
+                    help="layers of the C4 long trace (~7 spans per layer; 0 skips the C4 measurement)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -339,6 +389,8 @@ def main():
            "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
 
     sort_line = measure_sort(eng, dev, b, args.steps, local) if not args.no_sort else None
+    del dev
+    c4_line = measure_c4(eng, args, rank, world, local, dist) if args.c4_layers > 0 else None
 
     if rank != 0:
         return
@@ -372,6 +424,8 @@ def main():
                                  "definition": "read begin_ns+flags+span_id (17 B), write perm (4 B) per span"}
         sort_line["roofline"]["frac"] = sort_line["roofline"]["achieved"] / peak
         line["sort_shuffled"] = sort_line
+    if c4_line:
+        line["c4"] = c4_line
     if world == 1 and not args.no_cpu_baseline:
         from oracle import ref
         if ref.available():

@@ -11,6 +11,9 @@
 // are u64 sums (exact). Sequential fp64 chains (the Accumulator) are evaluated
 // by one thread per subject in tree order, as the reference does.
 
+#include <algorithm>
+#include <vector>
+
 #include "ctx.h"
 #include "prims.cuh"
 
@@ -418,6 +421,13 @@ struct ModelArgs {
   const uint64_t* k_read;
   const uint64_t* k_write;
   const double* l_kern_lat;
+  // long groups (> kBigGroup kernels or layers): chunk partials (k_big_chunks)
+  const uint32_t* gkc_off;  // [G + 1] kernel chunks of each group (empty range: not chunked)
+  const uint32_t* glc_off;  // [G + 1] layer chunks of each group
+  const double* pk_lat;     // per kernel chunk: sum of latencies
+  const double* pk_occw;    // per kernel chunk: sum of occ * lat
+  const uint64_t* pk_cnt;   // per kernel chunk: sums of flops, read, write
+  const double* pl_gpu;     // per layer chunk: sum of layer kernel latencies
   double trim, peak, bw;
   double* m_lat;
   double* m_kern_lat;
@@ -470,6 +480,24 @@ __global__ void k_models(ModelArgs a) {
   double lat = 0.0, occw = 0.0;
   uint64_t f = 0, rd = 0, wr = 0;
   const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
+  const bool big_k = a.gkc_off && a.gkc_off[g + 1] > a.gkc_off[g];
+  const bool big_l = a.glc_off && a.glc_off[g + 1] > a.glc_off[g];
+  if (big_k) {
+    // long group: the chunk partials in tree order (chunk sums of a one-run
+    // group's integer latencies are exact, so lat is the reference's double;
+    // sum(occ * lat) is re-associated at chunk boundaries)
+    if (lane == 0)
+      for (uint32_t c = a.gkc_off[g]; c < a.gkc_off[g + 1]; ++c) {
+        lat = __dadd_rn(lat, a.pk_lat[c]);
+        occw = __dadd_rn(occw, a.pk_occw[c]);
+      }
+    for (uint32_t c = a.gkc_off[g] + lane; c < a.gkc_off[g + 1]; c += 32) {
+      f += a.pk_cnt[3 * c];
+      rd += a.pk_cnt[3 * c + 1];
+      wr += a.pk_cnt[3 * c + 2];
+    }
+  }
+  if (!big_k) {
   // lanes load 32 consecutive rows (the next chunk while this one is consumed);
   // the fp64 chains then take them strictly left to right through register
   // broadcast, so the rounding sequence is exactly the reference's
@@ -511,12 +539,15 @@ __global__ void k_models(ModelArgs a) {
       }
     }
   }
+  }
   f = warp_sum_u64(f);
   rd = warp_sum_u64(rd);
   wr = warp_sum_u64(wr);
   const uint64_t n = k1 - k0;
   double gpu = 0.0;
-  const uint32_t l0 = a.gl_off[g], l1 = a.gl_off[g + 1];
+  const uint32_t l0 = a.gl_off[g], l1 = big_l ? a.gl_off[g] : a.gl_off[g + 1];
+  if (big_l && lane == 0)
+    for (uint32_t c = a.glc_off[g]; c < a.glc_off[g + 1]; ++c) gpu = __dadd_rn(gpu, a.pl_gpu[c]);
   double x_n = l0 + lane < l1 ? a.l_kern_lat[l0 + lane] : 0.0;
   for (uint32_t base = l0; base < l1; base += 32) {
     const double x = x_n;
@@ -554,6 +585,62 @@ __global__ void k_models(ModelArgs a) {
   a.m_in[g] = (ro.bound >= 0 && lat > 0.0) ? 1 : 0;
 }
 
+// ---- long groups (one long trace: BASELINE config 4) -------------------------
+// A group with more than kBigGroup kernels (or layers) would serialise one warp
+// on a chain of millions of fp64 additions. Its kernels / layers are cut into
+// chunks of kBigChunk; one warp per chunk folds the chunk in tree order, and the
+// model / name rows fold the chunk partials in order.
+constexpr uint32_t kBigGroup = 1u << 16;
+constexpr uint32_t kBigChunk = 8192;
+
+struct BigChunkArgs {
+  const uint32_t* desc;  // [n] (begin, end, kind): kind 0 kernel range, 1 layer range
+  uint32_t n;
+  const double* k_lat;
+  const double* k_occ;
+  const double* l_kern_lat;
+  const uint64_t* k_flops;
+  const uint64_t* k_read;
+  const uint64_t* k_write;
+  double* p_lat;   // kernel chunks: sum lat; layer chunks: sum kern_lat
+  double* p_occw;  // kernel chunks: sum occ * lat
+  uint64_t* p_cnt; // kernel chunks: [3 c + 0..2] sums of flops, read, write
+};
+
+__global__ void k_big_chunks(BigChunkArgs a) {
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+  if (c >= a.n) return;
+  const uint32_t b = a.desc[3 * c], e = a.desc[3 * c + 1], kind = a.desc[3 * c + 2];
+  const double* v = kind == 0 ? a.k_lat : a.l_kern_lat;
+  double s = 0.0, so = 0.0;
+  uint64_t f = 0, r = 0, w = 0;
+  for (uint32_t base = b; base < e; base += 32) {
+    const uint32_t x = base + lane;
+    const double l = x < e ? v[x] : 0.0;
+    if (kind == 0 && x < e) {
+      f += a.k_flops[x];
+      r += a.k_read[x];
+      w += a.k_write[x];
+    }
+    const double pr = (kind == 0 && x < e) ? __dmul_rn(a.k_occ[x], l) : 0.0;
+    const uint32_t cnt = min(32u, e - base);
+    for (uint32_t q = 0; q < cnt; ++q) {
+      s = __dadd_rn(s, __shfl_sync(0xffffffffu, l, q));
+      so = __dadd_rn(so, __shfl_sync(0xffffffffu, pr, q));
+    }
+  }
+  f = warp_sum_u64(f);
+  r = warp_sum_u64(r);
+  w = warp_sum_u64(w);
+  if (lane == 0) {
+    a.p_lat[c] = s;
+    a.p_occw[c] = so;
+    a.p_cnt[3 * c] = f;
+    a.p_cnt[3 * c + 1] = r;
+    a.p_cnt[3 * c + 2] = w;
+  }
+}
+
 // ---- a10 by name ------------------------------------------------------------
 //
 // Fast path: one warp per group with a shared-memory table keyed by name_id
@@ -579,6 +666,9 @@ struct NameTable {
 struct NameFastArgs {
   uint32_t G;
   const uint32_t* gk_off;
+  const uint32_t* gk_end;   // optional: group g = [gk_off[g], gk_end[g]) (chunk pseudo-groups)
+  const uint32_t* big;      // optional: gkc_off; groups with chunks are left to k_names_big
+  int raw;                  // chunk pseudo-groups: stage raw sums (s_lat, s_occ = sum occ*lat)
   const int32_t* gstatus;
   const uint32_t* k_name;
   const double* k_lat;
@@ -620,12 +710,13 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
   }
   if (lane == 0) T.nused = 0;
   __syncwarp();
-  if (a.gstatus[g] != XSP_G_OK) {
+  if (a.big && a.big[g + 1] > a.big[g]) return;  // long group: k_names_big
+  if (a.gstatus && a.gstatus[g] != XSP_G_OK) {
     if (lane == 0) a.g_count[g] = 0;
     return;
   }
   bool over = false;
-  const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
+  const uint32_t k0 = a.gk_off[g], k1 = a.gk_end ? a.gk_end[g] : a.gk_off[g + 1];
   const uint32_t lt = lanemask_lt();
   // pass A: slot per kernel and its stable rank within its name (the next
   // chunk's names are loaded while this chunk is hashed)
@@ -741,8 +832,138 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
     T.w[s] = wr;
   }
   __syncwarp();
+  if (a.raw) {
+    for (uint32_t u = lane; u < nu; u += 32) {
+      const uint32_t s = T.used[u];
+      const uint64_t o = (uint64_t)g * NCAP + u;
+      a.s_name[o] = T.key[s];
+      a.s_count[o] = T.cnt[s];
+      a.s_lat[o] = T.lat[s];
+      a.s_occ[o] = T.occw[s];
+      a.s_flops[o] = T.f[s];
+      a.s_read[o] = T.r[s];
+      a.s_write[o] = T.w[s];
+    }
+    if (lane == 0) a.g_count[g] = nu;
+    return;
+  }
   const double mlat = a.m_lat[g];
   // rank = position under (total latency desc, name asc) (analysis.cpp:424-430)
+  for (uint32_t u = lane; u < nu; u += 32) {
+    const uint32_t s = T.used[u];
+    const double l = T.lat[s];
+    const uint32_t nm = T.key[s];
+    uint32_t rank = 0;
+    for (uint32_t v2 = 0; v2 < nu; ++v2) {
+      const uint32_t s2 = T.used[v2];
+      const double l2 = T.lat[s2];
+      rank += (l2 > l) || (l2 == l && T.key[s2] < nm);
+    }
+    const uint64_t o = (uint64_t)g * NCAP + rank;
+    const Roof ro = roofline(T.f[s], T.r[s], T.w[s], l, a.peak, a.bw);
+    a.s_name[o] = nm;
+    a.s_count[o] = T.cnt[s];
+    a.s_lat[o] = l;
+    a.s_pct[o] = l / mlat * 100.0;
+    a.s_flops[o] = T.f[s];
+    a.s_read[o] = T.r[s];
+    a.s_write[o] = T.w[s];
+    a.s_occ[o] = l > 0.0 ? T.occw[s] / l : 0.0;
+    a.s_ai[o] = ro.ai;
+    a.s_tput[o] = ro.tput;
+    a.s_bound[o] = ro.bound;
+  }
+  if (lane == 0) a.g_count[g] = nu;
+}
+
+// a10 of a long group: the chunks' raw per-name sums (k_names_fast, raw mode)
+// folded chunk by chunk in tree order. Within a chunk every name appears once,
+// so lanes add distinct names concurrently; chunks are applied in order.
+struct NameBigArgs {
+  uint32_t G;
+  const uint32_t* gkc_off;
+  const int32_t* gstatus;
+  const uint32_t* c_count;  // names per chunk
+  const uint32_t* c_name;   // chunk rows [c * NCAP, + c_count[c])
+  const uint64_t* c_cnt;
+  const double* c_lat;
+  const double* c_occw;
+  const uint64_t* c_f;
+  const uint64_t* c_r;
+  const uint64_t* c_w;
+  const double* m_lat;
+  double peak, bw;
+  uint32_t* g_count;
+  uint32_t* overflow;
+  uint32_t* s_name;
+  uint64_t* s_count;
+  double* s_lat;
+  double* s_pct;
+  uint64_t* s_flops;
+  uint64_t* s_read;
+  uint64_t* s_write;
+  double* s_occ;
+  double* s_ai;
+  double* s_tput;
+  int8_t* s_bound;
+};
+
+__global__ void __launch_bounds__(32) k_names_big(NameBigArgs a) {
+  __shared__ NameTable T;
+  const uint32_t g = blockIdx.x, lane = threadIdx.x;
+  if (!(a.gkc_off[g + 1] > a.gkc_off[g])) return;
+  if (a.gstatus[g] != XSP_G_OK) {
+    if (lane == 0) a.g_count[g] = 0;
+    return;
+  }
+  for (uint32_t s = lane; s < NCAP; s += 32) {
+    T.key[s] = NEMPTY;
+    T.lat[s] = T.occw[s] = 0.0;
+    T.f[s] = T.r[s] = T.w[s] = T.cnt[s] = 0;
+  }
+  if (lane == 0) T.nused = 0;
+  __syncwarp();
+  bool over = false;
+  for (uint32_t c = a.gkc_off[g]; c < a.gkc_off[g + 1]; ++c) {
+    const uint32_t nc = a.c_count[c];
+    for (uint32_t e = lane; e < nc; e += 32) {
+      const uint64_t o = (uint64_t)c * NCAP + e;
+      const uint32_t nm = a.c_name[o];
+      uint32_t h = (nm * 2654435761u) & (NCAP - 1), probes = 0;
+      for (;;) {
+        const uint32_t old = atomicCAS(&T.key[h], NEMPTY, nm);
+        if (old == NEMPTY) {
+          T.used[atomicAdd(&T.nused, 1u)] = h;
+          break;
+        }
+        if (old == nm) break;
+        h = (h + 1) & (NCAP - 1);
+        if (++probes >= NCAP) {
+          over = true;
+          break;
+        }
+      }
+      if (over) break;
+      T.cnt[h] += a.c_cnt[o];
+      T.lat[h] = __dadd_rn(T.lat[h], a.c_lat[o]);
+      T.occw[h] = __dadd_rn(T.occw[h], a.c_occw[o]);
+      T.f[h] += a.c_f[o];
+      T.r[h] += a.c_r[o];
+      T.w[h] += a.c_w[o];
+    }
+    if (__any_sync(0xffffffffu, over)) break;
+    __syncwarp();
+  }
+  if (__any_sync(0xffffffffu, over)) {
+    if (lane == 0) {
+      a.g_count[g] = 0;
+      atomicOr(a.overflow, 1u);
+    }
+    return;
+  }
+  __syncwarp();
+  const uint32_t nu = T.nused;
+  const double mlat = a.m_lat[g];
   for (uint32_t u = lane; u < nu; u += 32) {
     const uint32_t s = T.used[u];
     const double l = T.lat[s];
@@ -959,8 +1180,52 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   uint32_t* htot = ctx->h<uint32_t>("a.tot_h", 4);
   xfer_small(htot, out->group_layer_off + G, 4, st);
   xfer_small(htot + 1, out->group_kernel_off + G, 4, st);
+  // group offsets on the host too (same sync) when some group may be long
+  uint32_t* hgl = ctx->h<uint32_t>("a.gl_h", G + 1);
+  uint32_t* hgk = ctx->h<uint32_t>("a.gk_h", G + 1);
+  xfer_small(hgl, out->group_layer_off, (G + 1) * 4ull, st);
+  xfer_small(hgk, out->group_kernel_off, (G + 1) * 4ull, st);
   XSP_CUDA(cudaStreamSynchronize(st));
   const uint32_t TL = htot[0], TK = htot[1];
+  // long groups (one long trace): chunk descriptors for k_big_chunks
+  std::vector<uint32_t> desc, gkc(G + 1, 0), glc(G + 1, 0);
+  uint32_t nkc = 0;
+  for (uint32_t g = 0; g < G; ++g) {
+    gkc[g] = nkc;
+    if (hgk[g + 1] - hgk[g] > kBigGroup || hgl[g + 1] - hgl[g] > kBigGroup)
+      for (uint32_t b = hgk[g]; b < hgk[g + 1]; b += kBigChunk, ++nkc)
+        desc.insert(desc.end(), {b, std::min(b + kBigChunk, hgk[g + 1]), 0u});
+  }
+  gkc[G] = nkc;
+  uint32_t nlc = 0;
+  for (uint32_t g = 0; g < G; ++g) {
+    glc[g] = nkc + nlc;
+    if (gkc[g + 1] > gkc[g])
+      for (uint32_t b = hgl[g]; b < hgl[g + 1]; b += kBigChunk, ++nlc)
+        desc.insert(desc.end(), {b, std::min(b + kBigChunk, hgl[g + 1]), 1u});
+  }
+  glc[G] = nkc + nlc;
+  const uint32_t n_chunks = nkc + nlc;
+  uint32_t *d_desc = nullptr, *d_gkc = nullptr, *d_glc = nullptr, *d_kcb = nullptr, *d_kce = nullptr;
+  if (n_chunks) {
+    uint32_t* hd = ctx->h<uint32_t>("a.big_h", desc.size() + 2ull * (G + 1) + 2ull * nkc);
+    std::memcpy(hd, desc.data(), desc.size() * 4);
+    std::memcpy(hd + desc.size(), gkc.data(), (G + 1) * 4ull);
+    std::memcpy(hd + desc.size() + G + 1, glc.data(), (G + 1) * 4ull);
+    uint32_t* kcb = hd + desc.size() + 2ull * (G + 1);
+    for (uint32_t c = 0; c < nkc; ++c) {
+      kcb[c] = desc[3 * c];
+      kcb[nkc + c] = desc[3 * c + 1];
+    }
+    const size_t words = desc.size() + 2ull * (G + 1) + 2ull * nkc;
+    uint32_t* dd = ctx->d<uint32_t>("a.big", words);
+    XSP_CUDA(cudaMemcpyAsync(dd, hd, words * 4, cudaMemcpyHostToDevice, st));
+    d_desc = dd;
+    d_gkc = dd + desc.size();
+    d_glc = d_gkc + G + 1;
+    d_kcb = d_glc + G + 1;
+    d_kce = d_kcb + nkc;
+  }
   launch(ctx, k_group_check_runs, total_runs, st, ga, total_runs, run_off);
   launch(ctx, k_group_check_layers, TL, st, ga, TL, out->group_layer_off);
   out->group_status = ctx->d<int32_t>("t.g_status", G);
@@ -1066,7 +1331,31 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->m_gpu_pct = ma.m_gpu_pct = ctx->d<double>("t.m_gpu_pct", G);
   out->m_throughput = ma.m_throughput = ctx->d<double>("t.m_tp", G);
   out->m_roofline_in = ma.m_in = ctx->d<uint8_t>("t.m_in", G);
+  ma.gkc_off = d_gkc;
+  ma.glc_off = d_glc;
+  ma.pk_lat = ma.pk_occw = ma.pl_gpu = nullptr;
+  ma.pk_cnt = nullptr;
+  double *p_lat = nullptr, *p_occw = nullptr;
   ctx->stage_begin("models", st);
+  if (n_chunks) {
+    BigChunkArgs bc;
+    bc.desc = d_desc;
+    bc.n = n_chunks;
+    bc.k_lat = la.k_lat;
+    bc.k_occ = la.k_occ;
+    bc.l_kern_lat = la.l_kern_lat;
+    bc.p_lat = p_lat = ctx->d<double>("a.p_lat", n_chunks);
+    bc.p_occw = p_occw = ctx->d<double>("a.p_occw", n_chunks);
+    bc.k_flops = la.k_flops;
+    bc.k_read = la.k_read;
+    bc.k_write = la.k_write;
+    bc.p_cnt = ctx->d<uint64_t>("a.p_cnt", 3ull * n_chunks);
+    ma.pk_cnt = bc.p_cnt;
+    launch(ctx, k_big_chunks, (uint64_t)n_chunks * 32, st, bc);
+    ma.pk_lat = p_lat;
+    ma.pk_occw = p_occw;
+    ma.pl_gpu = p_lat;
+  }
   launch(ctx, k_models, (uint64_t)G * 32, st, ma);
   ctx->stage_end("models", st);
 
@@ -1106,9 +1395,62 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     nf.s_ai = ctx->d<double>("a.s_ai", cap);
     nf.s_tput = ctx->d<double>("a.s_tput", cap);
     nf.s_bound = ctx->d<int8_t>("a.s_bound", cap);
+    nf.gk_end = nullptr;
+    nf.big = d_gkc;
+    nf.raw = 0;
     XSP_CUDA(cudaMemsetAsync(nf.overflow, 0, 4, st));
     k_names_fast<<<ceil_div(G, NAME_WARPS), NAME_WARPS * 32, 0, st>>>(nf);
     ++ctx->launches;
+    if (nkc) {
+      // long groups: raw per-name sums per kernel chunk, then folded in order
+      NameFastArgs nc = nf;
+      nc.G = nkc;
+      nc.gk_off = d_kcb;
+      nc.gk_end = d_kce;
+      nc.big = nullptr;
+      nc.gstatus = nullptr;
+      nc.raw = 1;
+      const uint64_t ccap = (uint64_t)nkc * NCAP;
+      nc.g_count = ctx->d<uint32_t>("a.c_count", nkc);
+      nc.s_name = ctx->d<uint32_t>("a.c_name", ccap);
+      nc.s_count = ctx->d<uint64_t>("a.c_cnt", ccap);
+      nc.s_lat = ctx->d<double>("a.c_lat", ccap);
+      nc.s_occ = ctx->d<double>("a.c_occw", ccap);
+      nc.s_flops = ctx->d<uint64_t>("a.c_f", ccap);
+      nc.s_read = ctx->d<uint64_t>("a.c_r", ccap);
+      nc.s_write = ctx->d<uint64_t>("a.c_w", ccap);
+      k_names_fast<<<ceil_div(nkc, NAME_WARPS), NAME_WARPS * 32, 0, st>>>(nc);
+      NameBigArgs nb;
+      nb.G = G;
+      nb.gkc_off = d_gkc;
+      nb.gstatus = out->group_status;
+      nb.c_count = nc.g_count;
+      nb.c_name = nc.s_name;
+      nb.c_cnt = nc.s_count;
+      nb.c_lat = nc.s_lat;
+      nb.c_occw = nc.s_occ;
+      nb.c_f = nc.s_flops;
+      nb.c_r = nc.s_read;
+      nb.c_w = nc.s_write;
+      nb.m_lat = ma.m_lat;
+      nb.peak = la.peak;
+      nb.bw = la.bw;
+      nb.g_count = nf.g_count;
+      nb.overflow = nf.overflow;
+      nb.s_name = nf.s_name;
+      nb.s_count = nf.s_count;
+      nb.s_lat = nf.s_lat;
+      nb.s_pct = nf.s_pct;
+      nb.s_flops = nf.s_flops;
+      nb.s_read = nf.s_read;
+      nb.s_write = nf.s_write;
+      nb.s_occ = nf.s_occ;
+      nb.s_ai = nf.s_ai;
+      nb.s_tput = nf.s_tput;
+      nb.s_bound = nf.s_bound;
+      k_names_big<<<G, 32, 0, st>>>(nb);
+      ctx->launches += 2;
+    }
     exclusive_scan<uint32_t, uint32_t>(nf.g_count, out->group_name_off, G, scan_tmp, out->group_name_off + G, st,
                                        &ctx->launches);
     xfer_small(htot + 2, out->group_name_off + G, 4, st);

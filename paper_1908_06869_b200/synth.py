@@ -219,3 +219,122 @@ def c3(runs: int = 20, n_models: int = 65, batches=(1, 2, 4, 8, 16, 32, 64, 128)
        **kw):
     """BASELINE config 3: 65-model x 8-batch sweep (~50M spans at runs=20)."""
     return corpus(make_models(n_models, seed=seed, **kw), batches, runs, seed=seed + 1000)
+
+
+def c4(n_layers: int = 1_000_000, seed: int = 4, streams: int = 4, block_layers: int = 2000,
+       long_frac: float = 0.01, long_max: int = 64, kernels: int = 3) -> SpanBatch:
+    """BASELINE config 4: ONE long-running trace (model span + n_layers layers).
+
+    * Layers run back to back; a layer has `kernels` launches, or U{8..long_max}
+      for a `long_frac` share of "long" layers (deep nesting within the 3-level
+      model), launches packed from the layer begin (simprof build_plan shape).
+    * Executions are spread over `streams` device streams (kernel k on stream
+      k % streams), each stream a cursor: exec begin = max(stream cursor, launch
+      end). Executions of different streams overlap each other and run past
+      the end of their layer into later layers ("interleaved streams").
+    * Every `block_layers` layers the host waits for all streams to drain (a
+      synchronisation point), so the trace has quiescent instants where no
+      layer interval and no launch->exec pair crosses: the time-range shards'
+      cut points (timeshard.py).
+    * Correlation ids increase in launch order; span ids follow record order.
+    At n_layers = 28.6M the trace has ~200M spans."""
+    rng = np.random.default_rng(seed)
+    names = sorted({f"c4/layer/{t}" for t in TYPES} | {"c4_model"} | set(KERNEL_VOCAB))
+    nid = {n: i for i, n in enumerate(names)}
+    layer_name = np.array([nid[f"c4/layer/{t}"] for t in TYPES], dtype=np.uint32)
+    vocab_ids = np.array([nid[n] for n in KERNEL_VOCAB], dtype=np.uint32)
+    parts = {k: [] for k in ("span_id", "parent_id", "begin_ns", "end_ns", "cid", "flags", "name_id",
+                             "flops", "dram_read", "dram_write", "occupancy", "alloc_bytes", "type_id")}
+    t_now = EPOCH_NS
+    next_sid = 2
+    next_cid = 1
+    KF = capi.LEVEL_KERNEL
+    for b0 in range(0, n_layers, block_layers):
+        L = min(block_layers, n_layers - b0)
+        kc = np.full(L, kernels, dtype=np.int64)
+        long = rng.random(L) < long_frac
+        kc[long] = rng.integers(8, long_max + 1, int(long.sum()))
+        K = int(kc.sum())
+        first_k = np.concatenate([[0], np.cumsum(kc)[:-1]])
+        lay_of_k = np.repeat(np.arange(L), kc)
+        k_in_layer = np.arange(K) - first_k[lay_of_k]
+        launch_ns = rng.integers(3_000, 6_001, K)
+        # launches packed from the layer begin; the layer body covers them
+        kl = np.cumsum(launch_ns) - launch_ns
+        kl = kl - kl[first_k][lay_of_k]
+        lsum = np.bincount(lay_of_k, weights=launch_ns, minlength=L).astype(np.int64)
+        body = np.maximum(rng.integers(20_000, 400_000, L), lsum + 1_000)
+        lbeg = t_now + np.concatenate([[0], np.cumsum(body)[:-1]])
+        lend = lbeg + body
+        a_beg = lbeg[lay_of_k] + kl
+        a_end = a_beg + launch_ns
+        d = rng.integers(5_000, 300_000, K)
+        e_beg = np.empty(K, dtype=np.int64)
+        for s in range(streams):
+            idx = np.arange(s, K, streams)
+            if idx.size == 0:
+                continue
+            ds = d[idx]
+            S = np.cumsum(ds)
+            Sprev = S - ds
+            e_end_s = S + np.maximum.accumulate(np.maximum(a_end[idx] - Sprev, t_now - Sprev))
+            e_beg[idx] = e_end_s - ds
+        e_end = e_beg + d
+        # span ids in record order: per layer [layer, (launch, exec) x K_l]
+        layer_sid = next_sid + np.arange(L) + 2 * first_k
+        launch_sid = layer_sid[lay_of_k] + 1 + 2 * k_in_layer
+        exec_sid = launch_sid + 1
+        next_sid = int(layer_sid[-1] + 1 + 2 * kc[-1])
+        cid = next_cid + np.arange(K)
+        next_cid += K
+        # timeline order (begin_ns, rank, span_id) of the block
+        n = L + 2 * K
+        beg = np.concatenate([lbeg, a_beg, e_beg])
+        end = np.concatenate([lend, a_end, e_end])
+        sid = np.concatenate([layer_sid, launch_sid, exec_sid])
+        rank = np.concatenate([np.full(L, 2), np.full(2 * K, 3)])
+        order = np.lexsort((sid, rank, beg))
+        role = np.concatenate([np.zeros(L, np.int8), np.ones(K, np.int8), np.full(K, 2, np.int8)])[order]
+        src = np.concatenate([np.arange(L), np.arange(K), np.arange(K)])[order]
+        flg = np.empty(n, dtype=np.uint8)
+        flg[role == 0] = capi.LEVEL_LAYER | capi.F_PARENT
+        flg[role == 1] = KF | (capi.KIND_LAUNCH << 2) | capi.F_CID
+        flg[role == 2] = KF | (capi.KIND_EXEC << 2) | capi.F_CID | capi.F_METRICS
+        kname = rng.integers(0, len(KERNEL_VOCAB), K)
+        ltype = (b0 + np.arange(L)) % 4
+        nm = np.where(role == 0, layer_name[ltype[np.minimum(src, L - 1)]], vocab_ids[kname[np.minimum(src, K - 1)]])
+        cc = np.where(role == 0, 0, cid[np.minimum(src, K - 1)]).astype(np.uint64)
+        par = np.where(role == 0, 1, 0).astype(np.uint64)
+        ex_src = src[role == 2]  # metric rows in span-row order
+        parts["span_id"].append(sid[order].astype(np.uint64))
+        parts["parent_id"].append(par)
+        parts["begin_ns"].append(beg[order].astype(np.uint64))
+        parts["end_ns"].append(end[order].astype(np.uint64))
+        parts["cid"].append(cc)
+        parts["flags"].append(flg)
+        parts["name_id"].append(nm.astype(np.uint32))
+        parts["flops"].append(rng.integers(10_000_000, 10_000_000_000, K)[ex_src])
+        parts["dram_read"].append(rng.integers(1_000_000, 100_000_000, K)[ex_src])
+        parts["dram_write"].append(rng.integers(1_000_000, 100_000_000, K)[ex_src])
+        parts["occupancy"].append((rng.integers(5, 96, K) / 100.0)[ex_src])
+        lay_src = src[role == 0]
+        parts["alloc_bytes"].append(rng.integers(100_000, 30_000_000, L)[lay_src])
+        parts["type_id"].append(ltype[lay_src].astype(np.uint32))
+        # synchronisation point: the next block starts once every stream drained
+        t_now = int(max(lend[-1], e_end.max())) + 1_000
+    mend = t_now
+    model = {"span_id": [1], "parent_id": [0], "begin_ns": [EPOCH_NS], "end_ns": [mend], "cid": [0],
+             "flags": [capi.LEVEL_MODEL], "name_id": [nid["c4_model"]]}
+    cols = {}
+    for k, v in parts.items():
+        if k in model:
+            cols[k] = np.concatenate([np.asarray(model[k], dtype=v[0].dtype)] + v)
+        else:
+            cols[k] = np.concatenate(v)
+    n = cols["span_id"].size
+    lv = (1 << capi.LEVEL_MODEL) | (1 << capi.LEVEL_LAYER) | (1 << capi.LEVEL_KERNEL)
+    return SpanBatch(**cols, trace_span_off=np.array([0, n], dtype=np.uint64), trace_id=np.array([1]),
+                     trace_levels=np.array([lv]), trace_batch=np.array([1]), trace_run=np.array([0]),
+                     trace_serialized=np.zeros(1), names=[x.encode() for x in names],
+                     types=[t.encode() for t in TYPES], system_name=b"tesla-v100-sxm2",
+                     peak_flops=15.7e12, mem_bw=900e9)
