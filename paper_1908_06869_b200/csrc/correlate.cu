@@ -211,6 +211,18 @@ __device__ __forceinline__ Full shfl_full(const Full& v, int src) {
 //                thread folds are recomputed, and every thread re-walks its
 //                spans from its exclusive prefix emitting outputs with plain
 //                counters.
+// Code size matters: the fully unrolled 8-span walks put k_pass1 at ~5.7 K SASS
+// instructions and ncu attributed 30% of its warp samples to stall_no_inst
+// (instruction fetch). The rarely taken general fold and the emit walk are
+// unrolled by pairs only.
+#ifndef XSP_P1_SLOW_UNROLL
+#define XSP_P1_SLOW_UNROLL 1
+#endif
+#ifndef XSP_P1_EMIT_UNROLL
+#define XSP_P1_EMIT_UNROLL 1
+#endif
+constexpr int kP1SlowUnroll = XSP_P1_SLOW_UNROLL;
+constexpr int kP1EmitUnroll = XSP_P1_EMIT_UNROLL;
 #ifndef XSP_P1_WARPS
 #define XSP_P1_WARPS 8
 #endif
@@ -477,7 +489,7 @@ __device__ __forceinline__ Full fold_thread(const TileTraces& tt, uint32_t r0, u
     }
     return th;
   }
-#pragma unroll
+#pragma unroll kP1SlowUnroll
   for (int p = 0; p < P1_ITEMS / 2; ++p) {
     uint64_t bb[2], ee[2], pp[2];
     ld(p, bb, ee, pp, (uint8_t)(fl8 >> (16 * p)), (uint8_t)(fl8 >> (16 * p + 8)));
@@ -828,7 +840,7 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
     pb = j0 > 0 ? sm.begin[sw128(j0 - 1)] : __ldg(a.begin + i0 - 1);
     pf = j0 > 0 ? sm.flags[j0 - 1] : __ldg(a.flags + i0 - 1);
   }
-#pragma unroll
+#pragma unroll kP1EmitUnroll
   for (int p = 0; p < P1_ITEMS / 2; ++p) {
     uint64_t bb[2], ee[2], pp[2], cc[2];
     ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
