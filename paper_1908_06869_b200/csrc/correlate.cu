@@ -263,6 +263,7 @@ struct P1Args {
   uint32_t* group_done;     // [ngroups] finished tiles per group (zeroed per call)
   Full* tile_prefix;        // [ngroups + 1] exclusive prefixes of 32-tile groups + total (k_p1_scan)
   Full* tile_excl;          // [ntiles] exclusive prefix of every tile (k_p1_tile_prefix)
+  Full* warp_excl;          // [ntiles * P1_WARPS] exclusive prefix of every warp within its tile
   uint32_t* unsorted;
   unsigned long long* err_key;
   uint32_t* layer_row;
@@ -692,6 +693,13 @@ __global__ void __launch_bounds__(P1_THREADS) k_p1_reduce(P1Args a, const __grid
   __syncthreads();
   if (warp != 0) return;
   uint32_t last = 0;
+  if (lane < P1_WARPS) {
+    // exclusive prefix of every warp within the tile: k_pass1's warps start
+    // from it without waiting for each other
+    Full ex = full_identity();
+    for (uint32_t w = 0; w < lane; ++w) ex = full_combine(ex, s_wagg[w]);
+    a.warp_excl[(uint64_t)tile * P1_WARPS + lane] = ex;
+  }
   if (lane == 0) {
     Full agg = s_wagg[0];
     for (int w = 1; w < P1_WARPS; ++w) agg = full_combine(agg, s_wagg[w]);
@@ -758,8 +766,6 @@ __global__ void k_p1_tile_prefix(const Full* __restrict__ agg, const Full* __res
 __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const __grid_constant__ P1Maps maps) {
   extern __shared__ unsigned char p1_dyn[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(p1_dyn + ((1024u - (smem_u32(p1_dyn) & 1023u)) & 1023u));
-  __shared__ Full s_wagg[P1_WARPS];
-  __shared__ Full s_prefix;
   __shared__ TraceCache tc;
   __shared__ __align__(8) uint64_t s_bar;
 
@@ -780,7 +786,8 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
     bulk_g2s(sm.flags, a.flags + tile_base, P1_TILE, &s_bar);
   }
   fill_trace_cache(a, tc, tlo, thi);
-  if (threadIdx.x == 0) s_prefix = a.tile_excl[tile];
+  const Full tile_pre = a.tile_excl[tile];
+  const Full warp_pre = a.warp_excl[(uint64_t)tile * P1_WARPS + warp];
   if (!bulk) {
     for (uint32_t j = threadIdx.x; j < P1_TILE; j += P1_THREADS) {
       const bool v = j < tile_n;
@@ -814,17 +821,14 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
                                               })
                                 : full_identity();
     const Full inc = warp_inclusive_fold(th, lane);
-    if (lane == 31) s_wagg[warp] = inc;
     const uint32_t* s = reinterpret_cast<const uint32_t*>(&inc);
     uint32_t* d = reinterpret_cast<uint32_t*>(&lane_ex);
 #pragma unroll
     for (int w = 0; w < 12; ++w) d[w] = __shfl_up_sync(0xffffffffu, s[w], 1);
     if (lane == 0) lane_ex = full_identity();
   }
-  __syncthreads();
-  Full carry = s_prefix;
-  for (uint32_t w = 0; w < warp; ++w) carry = full_combine(carry, s_wagg[w]);
-  carry = full_combine(carry, lane_ex);
+  // tile prefix + the warps before this one (k_p1_reduce): no CTA barrier
+  Full carry = full_combine(full_combine(tile_pre, warp_pre), lane_ex);
 
   // ---- phase 3: per-span outputs (serial over the thread's 8 spans) ----------
   if (j0 >= tile_n) return;
@@ -1640,6 +1644,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.tile_prefix = ctx->d<Full>("c.tile_prefix", ntiles / 32 + 2);
   a.ntiles = ntiles;
   a.tile_excl = ctx->d<Full>("c.tile_excl", ntiles + 1);
+  a.warp_excl = ctx->d<Full>("c.warp_excl", (uint64_t)ntiles * P1_WARPS + 1);
   a.group_sum = ctx->d<Full>("c.tile_gsum", ntiles / 32 + 2);
   a.group_done = ctx->d<uint32_t>("c.group_done", ntiles / 32 + 2);
   XSP_CUDA(cudaMemsetAsync(a.group_done, 0, (ntiles / 32 + 2) * 4, st));
