@@ -643,11 +643,11 @@ __global__ void k_big_chunks(BigChunkArgs a) {
 
 // ---- a10 by name ------------------------------------------------------------
 //
-// Fast path: one warp per group with a shared-memory table keyed by name_id
+// Fast path: one CTA per group with a shared-memory table keyed by name_id
 // (std::map<std::string, Accumulator> of analysis.cpp:402-407; ids are interned
 // in string order, so sorting by id is sorting by name). u64 counters use shared
-// atomics (order-free, exact); the two fp64 chains per name are applied by lane
-// 0 strictly in tree order. Groups with more than NCAP distinct names fall back
+// atomics (order-free, exact); the two fp64 chains per name are applied by one
+// thread per name strictly in tree order. Groups with more than NCAP distinct names fall back
 // to the sort-based path below.
 
 constexpr int NCAP = 128;
@@ -697,35 +697,45 @@ struct NameFastArgs {
   int8_t* s_bound;
 };
 
+// One CTA (NAME_WARPS warps) per group. Warp w hashes the w-th quarter of the
+// group's kernels; stable ranks within a name combine the warp's running count
+// with the counts of the earlier warps (tree order = warp order, then lane order).
 __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) {
-  __shared__ NameTable tab[NAME_WARPS];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  const uint32_t g = blockIdx.x * NAME_WARPS + warp;
+  __shared__ NameTable T;
+  __shared__ uint32_t wcnt[NAME_WARPS][NCAP];  // per-warp per-slot counts
+  __shared__ uint32_t s_over;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, tid = threadIdx.x;
+  const uint32_t g = blockIdx.x;
   if (g >= a.G) return;
-  NameTable& T = tab[warp];
-  for (uint32_t s = lane; s < NCAP; s += 32) {
+  if (a.big && a.big[g + 1] > a.big[g]) return;  // long group: k_names_big
+  if (a.gstatus && a.gstatus[g] != XSP_G_OK) {
+    if (tid == 0) a.g_count[g] = 0;
+    return;
+  }
+  for (uint32_t s = tid; s < NCAP; s += blockDim.x) {
     T.key[s] = NEMPTY;
     T.lat[s] = T.occw[s] = 0.0;
     T.f[s] = T.r[s] = T.w[s] = T.cnt[s] = 0;
+#pragma unroll
+    for (int w = 0; w < NAME_WARPS; ++w) wcnt[w][s] = 0;
   }
-  if (lane == 0) T.nused = 0;
-  __syncwarp();
-  if (a.big && a.big[g + 1] > a.big[g]) return;  // long group: k_names_big
-  if (a.gstatus && a.gstatus[g] != XSP_G_OK) {
-    if (lane == 0) a.g_count[g] = 0;
-    return;
+  if (tid == 0) {
+    T.nused = 0;
+    s_over = 0;
   }
-  bool over = false;
+  __syncthreads();
   const uint32_t k0 = a.gk_off[g], k1 = a.gk_end ? a.gk_end[g] : a.gk_off[g + 1];
+  const uint32_t q = (k1 - k0 + NAME_WARPS * 32 - 1) / (NAME_WARPS * 32) * 32;  // warp quarter, 32-aligned
+  const uint32_t w0 = min(k1, k0 + warp * q), w1 = min(k1, w0 + q);
   const uint32_t lt = lanemask_lt();
-  // pass A: slot per kernel and its stable rank within its name (the next
-  // chunk's names are loaded while this chunk is hashed)
-  uint32_t nm_next = k0 + lane < k1 ? a.k_name[k0 + lane] : 0;
-  for (uint32_t base = k0; base < k1; base += 32) {
+  bool over = false;
+  // pass A: slot per kernel and its rank within its name inside the warp's quarter
+  uint32_t nm_next = w0 + lane < w1 ? a.k_name[w0 + lane] : 0;
+  for (uint32_t base = w0; base < w1; base += 32) {
     const uint32_t x = base + lane;
-    const bool v = x < k1;
+    const bool v = x < w1;
     const uint32_t nm = nm_next;
-    if (base + 32 + lane < k1) nm_next = a.k_name[base + 32 + lane];
+    if (base + 32 + lane < w1) nm_next = a.k_name[base + 32 + lane];
     uint32_t slot = NCAP + lane;  // distinct dummy for idle lanes
     if (v) {
       uint32_t h = (nm * 2654435761u) & (NCAP - 1);
@@ -747,53 +757,69 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
     }
     if (__any_sync(0xffffffffu, over)) break;
     const uint32_t peers = __match_any_sync(0xffffffffu, slot);
-    unsigned long long rank = 0;
-    if (v) rank = T.cnt[slot];
+    uint32_t rank = 0;
+    if (v) rank = wcnt[warp][slot];
     __syncwarp();
-    if (v && (peers & lt) == 0) T.cnt[slot] = rank + __popc(peers);
+    if (v && (peers & lt) == 0) wcnt[warp][slot] = rank + __popc(peers);
     if (v) {
       a.ks_slot[x] = slot;
-      a.ks_rank[x] = (uint32_t)(rank + __popc(peers & lt));
+      a.ks_rank[x] = rank + __popc(peers & lt);
     }
     __syncwarp();
   }
-  if (__any_sync(0xffffffffu, over)) {
-    if (lane == 0) {
+  if (__any_sync(0xffffffffu, over) && lane == 0) s_over = 1;
+  __syncthreads();
+  if (s_over) {
+    if (tid == 0) {
       a.g_count[g] = 0;
       atomicOr(a.overflow, 1u);
     }
     return;
   }
-  __syncwarp();
   const uint32_t nu = T.nused;
-  // pass B: start of each name's run = exclusive prefix of counts over slots
-  {
-    unsigned long long c4[NCAP / 32], s = 0;
+  // pass B: per slot, counts of the earlier warps (wcnt becomes an exclusive
+  // prefix) and the total; then the start of each name's run
+  for (uint32_t s = tid; s < NCAP; s += blockDim.x) {
+    uint32_t run = 0;
 #pragma unroll
-    for (int q = 0; q < NCAP / 32; ++q) {
-      c4[q] = T.cnt[lane * (NCAP / 32) + q];
-      s += c4[q];
+    for (int w = 0; w < NAME_WARPS; ++w) {
+      const uint32_t c = wcnt[w][s];
+      wcnt[w][s] = run;
+      run += c;
     }
-    unsigned long long incl = s;
+    T.cnt[s] = run;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long c4[NCAP / 32], sum = 0;
+#pragma unroll
+    for (int k = 0; k < NCAP / 32; ++k) {
+      c4[k] = T.cnt[lane * (NCAP / 32) + k];
+      sum += c4[k];
+    }
+    unsigned long long incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
       if ((int)lane >= o) incl += y;
     }
-    unsigned long long run = incl - s;
+    unsigned long long run = incl - sum;
 #pragma unroll
-    for (int q = 0; q < NCAP / 32; ++q) {
-      T.start[lane * (NCAP / 32) + q] = (uint32_t)run;
-      run += c4[q];
+    for (int k = 0; k < NCAP / 32; ++k) {
+      T.start[lane * (NCAP / 32) + k] = (uint32_t)run;
+      run += c4[k];
     }
   }
-  __syncwarp();
+  __syncthreads();
   // pass C: stable scatter of kernel ordinals by name
-  for (uint32_t x = k0 + lane; x < k1; x += 32) a.perm[k0 + T.start[a.ks_slot[x]] + a.ks_rank[x]] = x;
-  __syncwarp();
-  // pass D: one lane per name walks that name's kernels in tree order
+  for (uint32_t x = w0 + lane; x < w1; x += 32) {
+    const uint32_t s = a.ks_slot[x];
+    a.perm[k0 + T.start[s] + wcnt[warp][s] + a.ks_rank[x]] = x;
+  }
+  __syncthreads();
+  // pass D: one thread per name walks that name's kernels in tree order
   // (Accumulator::add, analysis.cpp:181-188); the u64 counters ride along (exact)
-  for (uint32_t u = lane; u < nu; u += 32) {
+  for (uint32_t u = tid; u < nu; u += blockDim.x) {
     const uint32_t s = T.used[u];
     const uint32_t b = k0 + T.start[s], n = (uint32_t)T.cnt[s];
     double lat = 0.0, occw = 0.0;
@@ -831,9 +857,9 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
     T.r[s] = rd;
     T.w[s] = wr;
   }
-  __syncwarp();
+  __syncthreads();
   if (a.raw) {
-    for (uint32_t u = lane; u < nu; u += 32) {
+    for (uint32_t u = tid; u < nu; u += blockDim.x) {
       const uint32_t s = T.used[u];
       const uint64_t o = (uint64_t)g * NCAP + u;
       a.s_name[o] = T.key[s];
@@ -844,12 +870,12 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
       a.s_read[o] = T.r[s];
       a.s_write[o] = T.w[s];
     }
-    if (lane == 0) a.g_count[g] = nu;
+    if (tid == 0) a.g_count[g] = nu;
     return;
   }
   const double mlat = a.m_lat[g];
   // rank = position under (total latency desc, name asc) (analysis.cpp:424-430)
-  for (uint32_t u = lane; u < nu; u += 32) {
+  for (uint32_t u = tid; u < nu; u += blockDim.x) {
     const uint32_t s = T.used[u];
     const double l = T.lat[s];
     const uint32_t nm = T.key[s];
@@ -873,7 +899,7 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
     a.s_tput[o] = ro.tput;
     a.s_bound[o] = ro.bound;
   }
-  if (lane == 0) a.g_count[g] = nu;
+  if (tid == 0) a.g_count[g] = nu;
 }
 
 // a10 of a long group: the chunks' raw per-name sums (k_names_fast, raw mode)
@@ -1399,7 +1425,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     nf.big = d_gkc;
     nf.raw = 0;
     XSP_CUDA(cudaMemsetAsync(nf.overflow, 0, 4, st));
-    k_names_fast<<<ceil_div(G, NAME_WARPS), NAME_WARPS * 32, 0, st>>>(nf);
+    k_names_fast<<<G, NAME_WARPS * 32, 0, st>>>(nf);
     ++ctx->launches;
     if (nkc) {
       // long groups: raw per-name sums per kernel chunk, then folded in order
@@ -1419,7 +1445,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       nc.s_flops = ctx->d<uint64_t>("a.c_f", ccap);
       nc.s_read = ctx->d<uint64_t>("a.c_r", ccap);
       nc.s_write = ctx->d<uint64_t>("a.c_w", ccap);
-      k_names_fast<<<ceil_div(nkc, NAME_WARPS), NAME_WARPS * 32, 0, st>>>(nc);
+      k_names_fast<<<nkc, NAME_WARPS * 32, 0, st>>>(nc);
       NameBigArgs nb;
       nb.G = G;
       nb.gkc_off = d_gkc;
