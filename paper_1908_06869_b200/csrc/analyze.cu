@@ -452,122 +452,138 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
 }
 
 // model_aggregate_row (analysis.cpp:532-552), a13 totals (:495-499), a1 (:245-246).
-// One warp per group: lanes load 32 consecutive kernel rows (coalesced) and the
-// fp64 accumulators then consume them strictly left to right through register
-// broadcast, so the rounding sequence is exactly the reference's; u64 counters
-// are reduced in any order (exact).
-__global__ void k_models(ModelArgs a) {
-  const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31u;
+// One 2-warp CTA per group. Warp 0 runs the kernel chains (latency and
+// occupancy x latency) strictly left to right through register broadcast, with
+// loads issued kModelPrefetch chunks of 32 rows ahead so the chain does not wait
+// on memory; warp 1 sums the u64 counters (any order: exact), runs the layer
+// chain (a13 GPU latency) and the model latency.
+constexpr int kModelPrefetch = 4;
+
+// strictly ordered fp64 fold of `v` over rows [b, e) (and of occ*v when kOcc)
+template <bool kOcc>
+__device__ __forceinline__ void chain_fold(const double* __restrict__ v, const double* __restrict__ occ,
+                                           uint32_t b, uint32_t e, uint32_t lane, double& s, double& so) {
+  double x[kModelPrefetch], o[kModelPrefetch];
+#pragma unroll
+  for (int d = 0; d < kModelPrefetch; ++d) {
+    const uint32_t i = b + 32 * d + lane;
+    x[d] = i < e ? v[i] : 0.0;
+    o[d] = (kOcc && i < e) ? occ[i] : 0.0;
+  }
+  for (uint32_t base = b; base < e; base += 32 * kModelPrefetch) {
+#pragma unroll
+    for (int d = 0; d < kModelPrefetch; ++d) {
+      const uint32_t cb = base + 32 * d;
+      if (cb >= e) break;
+      const double xv = x[d], pr = __dmul_rn(o[d], x[d]);
+      const uint32_t i = cb + 32 * kModelPrefetch + lane;
+      x[d] = i < e ? v[i] : 0.0;
+      o[d] = (kOcc && i < e) ? occ[i] : 0.0;
+      const uint32_t cnt = min(32u, e - cb);
+      if (cnt == 32) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          s = __dadd_rn(s, __shfl_sync(0xffffffffu, xv, q));
+          if (kOcc) so = __dadd_rn(so, __shfl_sync(0xffffffffu, pr, q));
+        }
+      } else {
+        for (uint32_t q = 0; q < cnt; ++q) {
+          s = __dadd_rn(s, __shfl_sync(0xffffffffu, xv, q));
+          if (kOcc) so = __dadd_rn(so, __shfl_sync(0xffffffffu, pr, q));
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(64) k_models(ModelArgs a) {
+  __shared__ double s_gpu, s_mlat;
+  __shared__ unsigned long long s_cnt[3];
+  const uint32_t g = blockIdx.x;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   if (g >= a.G) return;
   if (a.gstatus[g] != XSP_G_OK) {
-    if (lane == 0) a.m_lat[g] = nan("");
+    if (threadIdx.x == 0) a.m_lat[g] = nan("");
     return;
   }
-  const uint32_t R = a.nr[g], t0 = a.ft[g];
-  // model latency: lane r loads run r's model span; every lane then runs the
-  // same trimmed mean over the shuffled values (warp-uniform, no idle lanes)
-  uint64_t mdur = 0;
-  if (lane < R) {
-    const uint32_t m = a.model_row[t0 + lane];
-    mdur = clamp_dur(a.begin[m], a.end[m]);
-  }
-  uint64_t mdur_hi = 0;  // runs 32..63 (kMaxRuns)
-  if (R > 32 && lane + 32 < R) {
-    const uint32_t m = a.model_row[t0 + 32 + lane];
-    mdur_hi = clamp_dur(a.begin[m], a.end[m]);
-  }
-  double lat = 0.0, occw = 0.0;
-  uint64_t f = 0, rd = 0, wr = 0;
   const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
   const bool big_k = a.gkc_off && a.gkc_off[g + 1] > a.gkc_off[g];
   const bool big_l = a.glc_off && a.glc_off[g + 1] > a.glc_off[g];
-  if (big_k) {
-    // long group: the chunk partials in tree order (chunk sums of a one-run
-    // group's integer latencies are exact, so lat is the reference's double;
-    // sum(occ * lat) is re-associated at chunk boundaries)
-    if (lane == 0)
-      for (uint32_t c = a.gkc_off[g]; c < a.gkc_off[g + 1]; ++c) {
-        lat = __dadd_rn(lat, a.pk_lat[c]);
-        occw = __dadd_rn(occw, a.pk_occw[c]);
-      }
-    for (uint32_t c = a.gkc_off[g] + lane; c < a.gkc_off[g + 1]; c += 32) {
-      f += a.pk_cnt[3 * c];
-      rd += a.pk_cnt[3 * c + 1];
-      wr += a.pk_cnt[3 * c + 2];
+  double lat = 0.0, occw = 0.0;
+  if (warp == 1) {
+    const uint32_t R = a.nr[g], t0 = a.ft[g];
+    // model latency: lane r loads run r's model span; every lane then runs the
+    // same trimmed mean over the shuffled values (warp-uniform, no idle lanes)
+    uint64_t mdur = 0;
+    if (lane < R) {
+      const uint32_t m = a.model_row[t0 + lane];
+      mdur = clamp_dur(a.begin[m], a.end[m]);
     }
-  }
-  if (!big_k) {
-  // lanes load 32 consecutive rows (the next chunk while this one is consumed);
-  // the fp64 chains then take them strictly left to right through register
-  // broadcast, so the rounding sequence is exactly the reference's
-  double kl_n = 0.0, oc_n = 0.0;
-  uint64_t f_n = 0, r_n = 0, w_n = 0;
-  if (k0 + lane < k1) {
-    kl_n = a.k_lat[k0 + lane];
-    oc_n = a.k_occ[k0 + lane];
-    f_n = a.k_flops[k0 + lane];
-    r_n = a.k_read[k0 + lane];
-    w_n = a.k_write[k0 + lane];
-  }
-  for (uint32_t base = k0; base < k1; base += 32) {
-    const double kl = kl_n, prod = __dmul_rn(oc_n, kl_n);
-    f += f_n;
-    rd += r_n;
-    wr += w_n;
-    const uint32_t jn = base + 32 + lane;
-    kl_n = oc_n = 0.0;
-    f_n = r_n = w_n = 0;
-    if (jn < k1) {
-      kl_n = a.k_lat[jn];
-      oc_n = a.k_occ[jn];
-      f_n = a.k_flops[jn];
-      r_n = a.k_read[jn];
-      w_n = a.k_write[jn];
+    uint64_t mdur_hi = 0;  // runs 32..63 (kMaxRuns)
+    if (R > 32 && lane + 32 < R) {
+      const uint32_t m = a.model_row[t0 + 32 + lane];
+      mdur_hi = clamp_dur(a.begin[m], a.end[m]);
     }
-    const uint32_t cnt = min(32u, k1 - base);
-    if (cnt == 32) {
-#pragma unroll
-      for (int s = 0; s < 32; ++s) {
-        lat = __dadd_rn(lat, __shfl_sync(0xffffffffu, kl, s));
-        occw = __dadd_rn(occw, __shfl_sync(0xffffffffu, prod, s));
+    // u64 counters: any order is exact
+    uint64_t f = 0, rd = 0, wr = 0;
+    if (big_k) {
+      for (uint32_t c = a.gkc_off[g] + lane; c < a.gkc_off[g + 1]; c += 32) {
+        f += a.pk_cnt[3 * c];
+        rd += a.pk_cnt[3 * c + 1];
+        wr += a.pk_cnt[3 * c + 2];
       }
     } else {
-      for (uint32_t s = 0; s < cnt; ++s) {
-        lat = __dadd_rn(lat, __shfl_sync(0xffffffffu, kl, s));
-        occw = __dadd_rn(occw, __shfl_sync(0xffffffffu, prod, s));
+#pragma unroll 8
+      for (uint32_t x = k0 + lane; x < k1; x += 32) {
+        f += a.k_flops[x];
+        rd += a.k_read[x];
+        wr += a.k_write[x];
       }
     }
+    f = warp_sum_u64(f);
+    rd = warp_sum_u64(rd);
+    wr = warp_sum_u64(wr);
+    // a13 model GPU latency: layer kernel latencies in layer order
+    double gpu = 0.0, unused = 0.0;
+    if (big_l) {
+      if (lane == 0)
+        for (uint32_t c = a.glc_off[g]; c < a.glc_off[g + 1]; ++c) gpu = __dadd_rn(gpu, a.pl_gpu[c]);
+    } else {
+      chain_fold<false>(a.l_kern_lat, nullptr, a.gl_off[g], a.gl_off[g + 1], lane, gpu, unused);
+    }
+    const double mlat = trimmed_mean_int(
+        [&](uint32_t r) {
+          const uint64_t lo = __shfl_sync(0xffffffffu, mdur, r & 31u);
+          const uint64_t hi = __shfl_sync(0xffffffffu, mdur_hi, r & 31u);
+          return r < 32 ? lo : hi;
+        },
+        R, a.trim);
+    if (lane == 0) {
+      s_gpu = gpu;
+      s_mlat = mlat;
+      s_cnt[0] = f;
+      s_cnt[1] = rd;
+      s_cnt[2] = wr;
+    }
+  } else {
+    if (big_k) {
+      // long group: the chunk partials in tree order (chunk sums of a one-run
+      // group's integer latencies are exact, so lat is the reference's double;
+      // sum(occ * lat) is re-associated at chunk boundaries)
+      if (lane == 0)
+        for (uint32_t c = a.gkc_off[g]; c < a.gkc_off[g + 1]; ++c) {
+          lat = __dadd_rn(lat, a.pk_lat[c]);
+          occw = __dadd_rn(occw, a.pk_occw[c]);
+        }
+    } else {
+      chain_fold<true>(a.k_lat, a.k_occ, k0, k1, lane, lat, occw);
+    }
   }
-  }
-  f = warp_sum_u64(f);
-  rd = warp_sum_u64(rd);
-  wr = warp_sum_u64(wr);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const uint64_t f = s_cnt[0], rd = s_cnt[1], wr = s_cnt[2];
+  const double gpu = s_gpu, mlat = s_mlat;
   const uint64_t n = k1 - k0;
-  double gpu = 0.0;
-  const uint32_t l0 = a.gl_off[g], l1 = big_l ? a.gl_off[g] : a.gl_off[g + 1];
-  if (big_l && lane == 0)
-    for (uint32_t c = a.glc_off[g]; c < a.glc_off[g + 1]; ++c) gpu = __dadd_rn(gpu, a.pl_gpu[c]);
-  double x_n = l0 + lane < l1 ? a.l_kern_lat[l0 + lane] : 0.0;
-  for (uint32_t base = l0; base < l1; base += 32) {
-    const double x = x_n;
-    x_n = base + 32 + lane < l1 ? a.l_kern_lat[base + 32 + lane] : 0.0;
-    const uint32_t cnt = min(32u, l1 - base);
-    if (cnt == 32) {
-#pragma unroll
-      for (int s = 0; s < 32; ++s) gpu = __dadd_rn(gpu, __shfl_sync(0xffffffffu, x, s));
-    } else {
-      for (uint32_t s = 0; s < cnt; ++s) gpu = __dadd_rn(gpu, __shfl_sync(0xffffffffu, x, s));
-    }
-  }
-  const double mlat = trimmed_mean_int(
-      [&](uint32_t r) {
-        const uint64_t lo = __shfl_sync(0xffffffffu, mdur, r & 31u);
-        const uint64_t hi = __shfl_sync(0xffffffffu, mdur_hi, r & 31u);
-        return r < 32 ? lo : hi;
-      },
-      R, a.trim);
-  if (lane != 0) return;
   Roof ro = roofline(f, rd, wr, lat, a.peak, a.bw);
   a.m_lat[g] = mlat;
   a.m_kern_lat[g] = lat;
@@ -1382,7 +1398,10 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     ma.pk_occw = p_occw;
     ma.pl_gpu = p_lat;
   }
-  launch(ctx, k_models, (uint64_t)G * 32, st, ma);
+  if (G) {
+    k_models<<<G, 64, 0, st>>>(ma);
+    ++ctx->launches;
+  }
   ctx->stage_end("models", st);
 
   // ---- a10
