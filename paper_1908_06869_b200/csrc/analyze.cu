@@ -1215,19 +1215,44 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->group_layer_off = ctx->d<uint32_t>("t.g_loff", G + 1);
   out->group_kernel_off = ctx->d<uint32_t>("t.g_koff", G + 1);
   uint32_t* scan_tmp = ctx->d<uint32_t>("a.scan", scan_scratch_elems(G + 16));
-  exclusive_scan<uint32_t, uint32_t>(ga.gl, out->group_layer_off, G, scan_tmp, out->group_layer_off + G, st,
-                                     &ctx->launches);
-  exclusive_scan<uint32_t, uint32_t>(ga.gk, out->group_kernel_off, G, scan_tmp, out->group_kernel_off + G, st,
-                                     &ctx->launches);
   uint32_t* htot = ctx->h<uint32_t>("a.tot_h", 4);
-  xfer_small(htot, out->group_layer_off + G, 4, st);
-  xfer_small(htot + 1, out->group_kernel_off + G, 4, st);
-  // group offsets on the host too (same sync) when some group may be long
   uint32_t* hgl = ctx->h<uint32_t>("a.gl_h", G + 1);
   uint32_t* hgk = ctx->h<uint32_t>("a.gk_h", G + 1);
-  xfer_small(hgl, out->group_layer_off, (G + 1) * 4ull, st);
-  xfer_small(hgk, out->group_kernel_off, (G + 1) * 4ull, st);
-  XSP_CUDA(cudaStreamSynchronize(st));
+  if (ctx->hc_layer_key == corr->trace_layer_off && ctx->hc_kernel_key == corr->trace_kernel_off &&
+      ctx->hc_T == corr->n_traces) {
+    // the correlation's offsets are already on the host: group tables of the
+    // canonical (first) runs without a device round trip
+    const uint32_t* tl = ctx->h<uint32_t>("c.hc_loff", corr->n_traces + 1);
+    const uint32_t* tk = ctx->h<uint32_t>("c.hc_koff", corr->n_traces + 1);
+    uint32_t* hoff = ctx->h<uint32_t>("a.goff_h", 2ull * (G + 1));
+    uint32_t sl = 0, sk = 0;
+    for (uint32_t g = 0; g < G; ++g) {
+      hgl[g] = hoff[g] = sl;
+      hgk[g] = hoff[G + 1 + g] = sk;
+      if (gr->n_runs[g]) {
+        const uint32_t t = gr->first_trace[g];
+        sl += tl[t + 1] - tl[t];
+        sk += tk[t + 1] - tk[t];
+      }
+    }
+    hgl[G] = hoff[G] = sl;
+    hgk[G] = hoff[2 * G + 1] = sk;
+    htot[0] = sl;
+    htot[1] = sk;
+    xfer_small(out->group_layer_off, hoff, (G + 1) * 4ull, st);
+    xfer_small(out->group_kernel_off, hoff + G + 1, (G + 1) * 4ull, st);
+  } else {
+    exclusive_scan<uint32_t, uint32_t>(ga.gl, out->group_layer_off, G, scan_tmp, out->group_layer_off + G, st,
+                                       &ctx->launches);
+    exclusive_scan<uint32_t, uint32_t>(ga.gk, out->group_kernel_off, G, scan_tmp, out->group_kernel_off + G, st,
+                                       &ctx->launches);
+    xfer_small(htot, out->group_layer_off + G, 4, st);
+    xfer_small(htot + 1, out->group_kernel_off + G, 4, st);
+    // group offsets on the host too (same sync) when some group may be long
+    xfer_small(hgl, out->group_layer_off, (G + 1) * 4ull, st);
+    xfer_small(hgk, out->group_kernel_off, (G + 1) * 4ull, st);
+    XSP_CUDA(cudaStreamSynchronize(st));
+  }
   const uint32_t TL = htot[0], TK = htot[1];
   // long groups (one long trace): chunk descriptors for k_big_chunks
   std::vector<uint32_t> desc, gkc(G + 1, 0), glc(G + 1, 0);

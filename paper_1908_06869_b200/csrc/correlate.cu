@@ -1582,6 +1582,19 @@ void col_tmap(CUtensorMap* m, const uint64_t* col, uint64_t n) {
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
+// Enqueue the host copies of the per-trace offsets (read with the final sync).
+void cache_offsets_begin(xsp_ctx* ctx, const uint32_t* t_loff, const uint32_t* t_koff, uint32_t T,
+                         cudaStream_t st) {
+  ctx->hc_layer_key = ctx->hc_kernel_key = nullptr;
+  xfer_small(ctx->h<uint32_t>("c.hc_loff", T + 1), t_loff, (T + 1) * 4ull, st);
+  xfer_small(ctx->h<uint32_t>("c.hc_koff", T + 1), t_koff, (T + 1) * 4ull, st);
+}
+void cache_offsets_end(xsp_ctx* ctx, const uint32_t* t_loff, const uint32_t* t_koff, uint32_t T) {
+  ctx->hc_layer_key = t_loff;
+  ctx->hc_kernel_key = t_koff;
+  ctx->hc_T = T;
+}
+
 uint32_t read_u32(xsp_ctx* ctx, const uint32_t* dptr, cudaStream_t st) {
   uint32_t* h = ctx->h<uint32_t>("readback.u32", 1);
   xfer_small(h, dptr, 4, st);
@@ -1806,9 +1819,11 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     launch(ctx, k_status, T, st, T, model_row, err_key, no_dup, no_dup, a.ex, a.kl, out->trace_status,
            out->trace_err_row, counters + 4);
     xfer_small(htot, counters + 4, 16, st);
+    cache_offsets_begin(ctx, a.t_layer_off, out->trace_kernel_off, T, st);
     XSP_CUDA(cudaStreamSynchronize(st));
     ctx->stage_end("gather", st);
     if (!htot[3]) {
+      cache_offsets_end(ctx, a.t_layer_off, out->trace_kernel_off, T);
       out->n_failed = htot[0];
       out->n_layers = nl;
       out->layer_row = a.layer_row;
@@ -1972,7 +1987,12 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   out->trace_model_row = model_row;
   launch(ctx, k_status, T, st, T, model_row, err_key, dup_ex, dup_kl, a.ex, a.kl, out->trace_status,
          out->trace_err_row, counters + 4);
-  out->n_failed = read_u32(ctx, counters + 4, st);
+  uint32_t* hf = ctx->h<uint32_t>("c.failed_h", 1);
+  xfer_small(hf, counters + 4, 4, st);
+  cache_offsets_begin(ctx, out->trace_layer_off, out->trace_kernel_off, T, st);
+  XSP_CUDA(cudaStreamSynchronize(st));
+  out->n_failed = *hf;
+  cache_offsets_end(ctx, out->trace_layer_off, out->trace_kernel_off, T);
 }
 
 }  // namespace xsp

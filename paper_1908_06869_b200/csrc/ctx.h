@@ -93,6 +93,13 @@ struct xsp_ctx {
     }
   }
 
+  // Host copies of the last correlation's per-trace layer / kernel offsets,
+  // fetched at its final read-back: xsp_analyze on that correlation sizes its
+  // group tables on the host instead of with another device round trip.
+  const void* hc_layer_key = nullptr;
+  const void* hc_kernel_key = nullptr;
+  uint32_t hc_T = 0;
+
   // Suffix appended to every device buffer name while set: the chunked host
   // pipeline runs consecutive chunks on two disjoint buffer sets, so one
   // chunk's results can stream out while the next chunk computes.

@@ -15,12 +15,16 @@ namespace xsp {
 // engine behind bulk copies that other streams have queued (csrc/pipeline.cu
 // streams the next chunk's columns while the current chunk computes).
 static __global__ void k_xfer_words(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n) {
-  for (uint32_t i = threadIdx.x; i < n; i += 32) dst[i] = src[i];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 // bytes: a multiple of 4, both pointers 4-byte aligned
 inline void xfer_small(void* dst, const void* src, size_t bytes, cudaStream_t st) {
-  k_xfer_words<<<1, 32, 0, st>>>(static_cast<uint32_t*>(dst), static_cast<const uint32_t*>(src),
-                                 static_cast<uint32_t>(bytes / 4));
+  const uint32_t n = static_cast<uint32_t>(bytes / 4);
+  const uint32_t threads = n <= 32 ? 32 : 256;
+  uint32_t blocks = (n + threads - 1) / threads;
+  if (blocks > 64) blocks = 64;
+  if (blocks == 0) blocks = 1;
+  k_xfer_words<<<blocks, threads, 0, st>>>(static_cast<uint32_t*>(dst), static_cast<const uint32_t*>(src), n);
 }
 
 // ---------------------------------------------------------------------------
