@@ -338,7 +338,9 @@ def main():
 
     def step():
         co = eng.correlate_device(dev, stream=stream)
+        n = eng.launches
         eng.analyze_device(dev, co, groups, stream=stream)
+        return n + eng.launches
 
     def barrier():
         if dist:
@@ -355,8 +357,7 @@ def main():
     with ClockSampler(local) as clk:
         t0.record()
         for _ in range(args.steps):
-            step()
-            launches += eng.launches
+            launches += step()
         t1.record()
         torch.cuda.synchronize()
     barrier()

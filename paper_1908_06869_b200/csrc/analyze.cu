@@ -1033,15 +1033,37 @@ __global__ void __launch_bounds__(32) k_names_big(NameBigArgs a) {
   if (lane == 0) a.g_count[g] = nu;
 }
 
-// staged rows [g * NCAP, + count) -> output [off[g], off[g+1])
-template <typename T>
-__global__ void k_names_place(uint32_t G, const uint32_t* __restrict__ off, const T* __restrict__ src,
-                              T* __restrict__ dst) {
+// every a10 column of the staged rows in one launch
+struct NamePlaceArgs {
+  uint32_t G;
+  const uint32_t* off;
+  const uint32_t* s_name; const uint64_t* s_count; const double* s_lat; const double* s_pct;
+  const uint64_t* s_flops; const uint64_t* s_read; const uint64_t* s_write; const double* s_occ;
+  const double* s_ai; const double* s_tput; const int8_t* s_bound;
+  uint32_t* n_name; uint64_t* n_count; double* n_lat; double* n_pct;
+  uint64_t* n_flops; uint64_t* n_read; uint64_t* n_write; double* n_occ;
+  double* n_ai; double* n_tput; int8_t* n_bound;
+};
+__global__ void k_names_place_all(NamePlaceArgs a) {
   const uint32_t g = blockIdx.x;
-  if (g >= G) return;
-  const uint32_t n = off[g + 1] - off[g];
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[off[g] + i] = src[(uint64_t)g * NCAP + i];
+  if (g >= a.G) return;
+  const uint32_t b = a.off[g], n = a.off[g + 1] - b;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t s = (uint64_t)g * NCAP + i;
+    a.n_name[b + i] = a.s_name[s];
+    a.n_count[b + i] = a.s_count[s];
+    a.n_lat[b + i] = a.s_lat[s];
+    a.n_pct[b + i] = a.s_pct[s];
+    a.n_flops[b + i] = a.s_flops[s];
+    a.n_read[b + i] = a.s_read[s];
+    a.n_write[b + i] = a.s_write[s];
+    a.n_occ[b + i] = a.s_occ[s];
+    a.n_ai[b + i] = a.s_ai[s];
+    a.n_tput[b + i] = a.s_tput[s];
+    a.n_bound[b + i] = a.s_bound[s];
+  }
 }
+
 
 // Sort-based fallback (any number of names per group).
 
@@ -1540,18 +1562,12 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       out->n_tput = ctx->d<double>("t.n_tput", NN);
       out->n_bound = ctx->d<int8_t>("t.n_bound", NN);
       const uint32_t* o = out->group_name_off;
-      k_names_place<uint32_t><<<G, 128, 0, st>>>(G, o, nf.s_name, out->n_name);
-      k_names_place<uint64_t><<<G, 128, 0, st>>>(G, o, nf.s_count, out->n_count);
-      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_lat, out->n_lat);
-      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_pct, out->n_pct);
-      k_names_place<uint64_t><<<G, 128, 0, st>>>(G, o, nf.s_flops, out->n_flops);
-      k_names_place<uint64_t><<<G, 128, 0, st>>>(G, o, nf.s_read, out->n_read);
-      k_names_place<uint64_t><<<G, 128, 0, st>>>(G, o, nf.s_write, out->n_write);
-      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_occ, out->n_occ);
-      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_ai, out->n_ai);
-      k_names_place<double><<<G, 128, 0, st>>>(G, o, nf.s_tput, out->n_tput);
-      k_names_place<int8_t><<<G, 128, 0, st>>>(G, o, nf.s_bound, out->n_bound);
-      ctx->launches += 11;
+      NamePlaceArgs pa{G, o, nf.s_name, nf.s_count, nf.s_lat, nf.s_pct, nf.s_flops, nf.s_read, nf.s_write,
+                       nf.s_occ, nf.s_ai, nf.s_tput, nf.s_bound, out->n_name, out->n_count, out->n_lat,
+                       out->n_pct, out->n_flops, out->n_read, out->n_write, out->n_occ, out->n_ai,
+                       out->n_tput, out->n_bound};
+      k_names_place_all<<<G, 128, 0, st>>>(pa);
+      ctx->launches += 1;
       names_done = true;
     }
     ctx->stage_end("names", st);
