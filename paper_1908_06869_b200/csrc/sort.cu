@@ -4,12 +4,12 @@
 // Presorted input (the TraceBundle invariant) is detected first and returns the
 // identity without sorting. Otherwise every trace of up to kSegCap spans is
 // sorted by ONE CTA in shared memory: the trace's begin / span_id ranges are
-// reduced, each span gets a packed 63-bit key
-//   (begin - min_begin) | rank | (span_id - min_span_id) | local index
-// (the index makes keys unique, so any sort is stable), a bitonic network
-// sorts the keys in place, and perm is written from the index bits. HBM
-// traffic is one read of begin/span_id/flags and one perm write (21 B/span).
-// Traces that are longer or whose packed key needs more than 63 bits fall back
+// reduced, each span gets a packed 64-bit key
+//   (begin - min_begin) | rank | (span_id - min_span_id)
+// and a stable LSD radix sort of the 16-bit index permutation (warp-level
+// histograms, a digit-major scan, __match_any_sync-ranked scatter) orders it.
+// HBM traffic is one read of begin/span_id/flags and one perm write (21 B/span).
+// Traces that are longer or whose packed key needs more than 64 bits fall back
 // to one global LSD radix sort over the composite key (trace, begin_ns, rank,
 // span_id): four stable passes from the least significant field, each skipping
 // the 8-bit digits that are constant over the batch.
@@ -65,21 +65,40 @@ __global__ void k_sort_key(int field, const uint32_t* __restrict__ val, const ui
   key[j] = k;
 }
 
-constexpr uint32_t kSegCap = 16384;  // spans per CTA-sorted trace (128 KB of keys)
+constexpr uint32_t kSegCap = 16384;  // spans per CTA-sorted trace
 constexpr int kSegThreads = 1024;
+constexpr int kSegWarps = kSegThreads / 32;
 
 __device__ __forceinline__ uint32_t bit_width64(uint64_t v) { return v ? 64 - __clzll(v) : 0; }
 
-// One CTA per trace; sets *fallback for traces it cannot take.
+// Shared memory of k_sort_seg: the packed keys stay in place; the LSD passes
+// permute 16-bit indices between two buffers (the trace's keys plus both index
+// buffers fit one SM: 128 + 64 KB).
+struct SegSmem {
+  unsigned long long key[kSegCap];
+  uint16_t idx[2][kSegCap];
+  uint16_t wcnt[kSegWarps][256];  // per-warp digit counts, then per-warp digit offsets
+};
+constexpr size_t kSegSmem = sizeof(SegSmem);
+
+// One CTA per trace: key = (begin - min) | rank | (span_id - min), packed into
+// 64 bits when the trace's ranges allow (else the trace falls back), then a
+// stable LSD radix sort (8-bit digits, constant digits skipped) of the index
+// permutation: per pass every warp histograms its contiguous segment of the
+// current order, a scan gives each (digit, warp) its output offset, and the
+// warp re-walks its segment placing indices with __match_any_sync ranks.
 __global__ void __launch_bounds__(kSegThreads) k_sort_seg(const uint64_t* __restrict__ begin,
                                                           const uint8_t* __restrict__ flags,
                                                           const uint64_t* __restrict__ sid,
                                                           const uint64_t* __restrict__ off, uint32_t cap,
                                                           uint32_t* __restrict__ perm, uint32_t* __restrict__ fallback) {
-  extern __shared__ unsigned long long keys[];
-  __shared__ unsigned long long red[4][kSegThreads / 32];
-  __shared__ uint32_t s_shift[3];
+  extern __shared__ __align__(16) unsigned char seg_dyn[];
+  SegSmem& sm = *reinterpret_cast<SegSmem*>(seg_dyn);
+  __shared__ unsigned long long red[4][kSegWarps];
+  __shared__ uint32_t s_shift[2];
   __shared__ int s_ok;
+  __shared__ unsigned long long s_and, s_or;
+  __shared__ uint32_t s_tot[256];
   const uint32_t t = blockIdx.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint64_t lo = off[t], hi = off[t + 1];
   const uint32_t len = (uint32_t)(hi - lo);
@@ -110,55 +129,117 @@ __global__ void __launch_bounds__(kSegThreads) k_sort_seg(const uint64_t* __rest
   }
   __syncthreads();
   if (tid == 0) {
-    for (uint32_t w = 1; w < blockDim.x / 32; ++w) {
+    for (uint32_t w = 1; w < kSegWarps; ++w) {
       red[0][0] = min(red[0][0], red[0][w]); red[1][0] = max(red[1][0], red[1][w]);
       red[2][0] = min(red[2][0], red[2][w]); red[3][0] = max(red[3][0], red[3][w]);
     }
-    const uint32_t ib = bit_width64(len - 1), sb = bit_width64(red[3][0] - red[2][0]);
+    const uint32_t sb = bit_width64(red[3][0] - red[2][0]);
     const uint32_t bb = bit_width64(red[1][0] - red[0][0]);
-    s_ok = ib + sb + 2 + bb <= 63;
-    s_shift[0] = ib;            // span_id field
-    s_shift[1] = ib + sb;       // rank field
-    s_shift[2] = ib + sb + 2;   // begin field
+    s_ok = sb + 2 + bb <= 64;
+    s_shift[0] = sb;      // rank field
+    s_shift[1] = sb + 2;  // begin field
+    s_and = ~0ull;
+    s_or = 0;
     if (!s_ok) atomicOr(fallback, 1u);
   }
   __syncthreads();
   if (!s_ok) return;
   bmin = red[0][0];
   smin = red[2][0];
-  const uint32_t sh_s = s_shift[0], sh_r = s_shift[1], sh_b = s_shift[2];
-  uint32_t P = 2;
-  while (P < len) P <<= 1;
-  for (uint32_t j = tid; j < P; j += blockDim.x) {
-    unsigned long long k = ~0ull;  // padding sorts last (real keys use <= 63 bits)
-    if (j < len) {
-      const uint32_t l = f_level(flags[lo + j]);
-      const uint64_t r = l >= XSP_LEVEL_KERNEL ? 3 : l + 1;  // rank (span.hpp:51-59)
-      k = ((begin[lo + j] - bmin) << sh_b) | (r << sh_r) | ((sid[lo + j] - smin) << sh_s) | j;
-    }
-    keys[j] = k;
+  const uint32_t sh_r = s_shift[0], sh_b = s_shift[1];
+  unsigned long long kand = ~0ull, kor = 0;
+  for (uint32_t j = tid; j < len; j += blockDim.x) {
+    const uint32_t l = f_level(flags[lo + j]);
+    const uint64_t r = l >= XSP_LEVEL_KERNEL ? 3 : l + 1;  // rank (span.hpp:51-59)
+    const unsigned long long k = ((begin[lo + j] - bmin) << sh_b) | (r << sh_r) | (sid[lo + j] - smin);
+    sm.key[j] = k;
+    sm.idx[0][j] = (uint16_t)j;
+    kand &= k;
+    kor |= k;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kand &= __shfl_xor_sync(0xffffffffu, kand, o);
+    kor |= __shfl_xor_sync(0xffffffffu, kor, o);
+  }
+  if (lane == 0) {
+    atomicAnd(&s_and, kand);
+    atomicOr(&s_or, kor);
   }
   __syncthreads();
-  // bitonic network, ascending. Pair i of a stage with distance j <= 32 touches
-  // elements of the 64-element block 2*32*(i/32) only, and a warp owns whole
-  // blocks, so those stages synchronise the warp instead of the CTA.
-  for (uint32_t k = 2; k <= P; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = tid; i < P / 2; i += blockDim.x) {
-        const uint32_t a = 2 * i - (i & (j - 1)), b = a + j;
-        const unsigned long long ka = keys[a], kb = keys[b];
-        const bool up = (a & k) == 0;
-        if ((ka > kb) == up) {
-          keys[a] = kb;
-          keys[b] = ka;
-        }
-      }
-      if (j > 32) __syncthreads(); else __syncwarp();
+  const unsigned long long varying = s_and ^ s_or;
+  // warp w owns positions [w * seg, (w + 1) * seg) of the current order
+  const uint32_t seg = ((len + kSegWarps - 1) / kSegWarps + 31) & ~31u;
+  const uint32_t p0 = min(len, warp * seg), p1 = min(len, p0 + seg);
+  int cur = 0;
+  for (int shift = 0; shift < 64; shift += 8) {
+    if (!((varying >> shift) & 0xFFull)) continue;
+    const uint16_t* src = sm.idx[cur];
+    uint16_t* dst = sm.idx[cur ^ 1];
+    for (uint32_t d = lane; d < 256; d += 32) sm.wcnt[warp][d] = 0;
+    __syncwarp();
+    // histogram of the warp's segment
+    for (uint32_t base = p0; base < p1; base += 32) {
+      const uint32_t i = base + lane;
+      const uint32_t d = i < p1 ? (uint32_t)(sm.key[src[i]] >> shift) & 0xFFu : 256u + lane;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      if (i < p1 && (peers & lanemask_lt()) == 0) sm.wcnt[warp][d] += (uint16_t)__popc(peers);
+      __syncwarp();
     }
     __syncthreads();
+    // per digit: totals and the exclusive offsets of the warps (digit-major)
+    if (tid < 256) {
+      uint32_t run = 0;
+#pragma unroll 8
+      for (int w = 0; w < kSegWarps; ++w) {
+        const uint32_t c = sm.wcnt[w][tid];
+        sm.wcnt[w][tid] = (uint16_t)run;
+        run += c;
+      }
+      s_tot[tid] = run;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 256 digit totals (8 per lane)
+      uint32_t v[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        v[q] = s_tot[lane * 8 + q];
+        sum += v[q];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      uint32_t run = incl - sum;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        s_tot[lane * 8 + q] = run;
+        run += v[q];
+      }
+    }
+    __syncthreads();
+    // stable scatter: digit start + earlier warps + running rank in this warp
+    for (uint32_t base = p0; base < p1; base += 32) {
+      const uint32_t i = base + lane;
+      const uint16_t x = i < p1 ? src[i] : 0;
+      const uint32_t d = i < p1 ? (uint32_t)(sm.key[x] >> shift) & 0xFFu : 256u + lane;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t below = __popc(peers & lanemask_lt());
+      uint32_t r0 = 0;
+      if (i < p1) r0 = sm.wcnt[warp][d];
+      __syncwarp();
+      if (i < p1) {
+        dst[s_tot[d] + r0 + below] = x;
+        if ((peers & lanemask_lt()) == 0) sm.wcnt[warp][d] = (uint16_t)(r0 + __popc(peers));
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    cur ^= 1;
   }
-  const unsigned long long imask = (1ull << sh_s) - 1;
-  for (uint32_t j = tid; j < len; j += blockDim.x) perm[lo + j] = (uint32_t)(lo + (keys[j] & imask));
+  for (uint32_t j = tid; j < len; j += blockDim.x) perm[lo + j] = (uint32_t)(lo + sm.idx[cur][j]);
 }
 
 }  // namespace
@@ -178,9 +259,9 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
   if (*was_sorted || n <= 1) return;
   // per-trace CTA sort; the global radix sort only if some trace does not fit
   XSP_CUDA(cudaMemsetAsync(flag, 0, 4, st));
-  XSP_CUDA(cudaFuncSetAttribute(k_sort_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSegCap * 8)));
+  XSP_CUDA(cudaFuncSetAttribute(k_sort_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSegSmem));
   ctx->stage_begin("sort", st);
-  k_sort_seg<<<T, kSegThreads, kSegCap * 8, st>>>(begin, flags, sid, off, kSegCap, perm, flag);
+  k_sort_seg<<<T, kSegThreads, kSegSmem, st>>>(begin, flags, sid, off, kSegCap, perm, flag);
   ctx->stage_end("sort", st);
   ++ctx->launches;
   XSP_CUDA(cudaMemcpyAsync(h, flag, 4, cudaMemcpyDeviceToHost, st));
