@@ -65,21 +65,20 @@ __global__ void k_sort_key(int field, const uint32_t* __restrict__ val, const ui
   key[j] = k;
 }
 
-constexpr uint32_t kSegCap = 16384;  // spans per CTA-sorted trace
-constexpr int kSegThreads = 1024;
-constexpr int kSegWarps = kSegThreads / 32;
+constexpr uint32_t kSegCap = 16384;  // spans per CTA-sorted trace (large class)
+constexpr uint32_t kSegCapSmall = 4096;  // small class: 4 CTAs per SM
 
 __device__ __forceinline__ uint32_t bit_width64(uint64_t v) { return v ? 64 - __clzll(v) : 0; }
 
 // Shared memory of k_sort_seg: the packed keys stay in place; the LSD passes
 // permute 16-bit indices between two buffers (the trace's keys plus both index
 // buffers fit one SM: 128 + 64 KB).
+template <uint32_t CAP, int WARPS>
 struct SegSmem {
-  unsigned long long key[kSegCap];
-  uint16_t idx[2][kSegCap];
-  uint16_t wcnt[kSegWarps][256];  // per-warp digit counts, then per-warp digit offsets
+  unsigned long long key[CAP];
+  uint16_t idx[2][CAP];
+  uint16_t wcnt[WARPS][256];  // per-warp digit counts, then per-warp digit offsets
 };
-constexpr size_t kSegSmem = sizeof(SegSmem);
 
 // One CTA per trace: key = (begin - min) | rank | (span_id - min), packed into
 // 64 bits when the trace's ranges allow (else the trace falls back), then a
@@ -87,13 +86,19 @@ constexpr size_t kSegSmem = sizeof(SegSmem);
 // permutation: per pass every warp histograms its contiguous segment of the
 // current order, a scan gives each (digit, warp) its output offset, and the
 // warp re-walks its segment placing indices with __match_any_sync ranks.
-__global__ void __launch_bounds__(kSegThreads) k_sort_seg(const uint64_t* __restrict__ begin,
-                                                          const uint8_t* __restrict__ flags,
-                                                          const uint64_t* __restrict__ sid,
-                                                          const uint64_t* __restrict__ off, uint32_t cap,
-                                                          uint32_t* __restrict__ perm, uint32_t* __restrict__ fallback) {
+// Size classes: traces of at most kSegCapSmall spans run as 256-thread CTAs with
+// 52 KB of shared memory (4 per SM); longer ones as 1024-thread CTAs with 210 KB.
+// Every launch covers all traces; a CTA leaves traces of the other class.
+template <uint32_t CAP, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_sort_seg(const uint64_t* __restrict__ begin,
+                                                      const uint8_t* __restrict__ flags,
+                                                      const uint64_t* __restrict__ sid,
+                                                      const uint64_t* __restrict__ off, uint32_t min_len,
+                                                      uint32_t* __restrict__ perm, uint32_t* __restrict__ fallback) {
+  constexpr int kSegWarps = THREADS / 32;
+  constexpr uint32_t cap = CAP;
   extern __shared__ __align__(16) unsigned char seg_dyn[];
-  SegSmem& sm = *reinterpret_cast<SegSmem*>(seg_dyn);
+  SegSmem<CAP, kSegWarps>& sm = *reinterpret_cast<SegSmem<CAP, kSegWarps>*>(seg_dyn);
   __shared__ unsigned long long red[4][kSegWarps];
   __shared__ uint32_t s_shift[2];
   __shared__ int s_ok;
@@ -102,11 +107,13 @@ __global__ void __launch_bounds__(kSegThreads) k_sort_seg(const uint64_t* __rest
   const uint32_t t = blockIdx.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint64_t lo = off[t], hi = off[t + 1];
   const uint32_t len = (uint32_t)(hi - lo);
+  if (len < min_len) return;  // the small class sorts it
   if (len <= 1) {
     if (len == 1 && tid == 0) perm[lo] = (uint32_t)lo;
     return;
   }
   if (len > cap) {
+    if (CAP < kSegCap) return;  // the large class sorts it
     if (tid == 0) atomicOr(fallback, 1u);
     return;
   }
@@ -188,15 +195,15 @@ __global__ void __launch_bounds__(kSegThreads) k_sort_seg(const uint64_t* __rest
     }
     __syncthreads();
     // per digit: totals and the exclusive offsets of the warps (digit-major)
-    if (tid < 256) {
+    for (uint32_t d = tid; d < 256; d += THREADS) {
       uint32_t run = 0;
 #pragma unroll 8
       for (int w = 0; w < kSegWarps; ++w) {
-        const uint32_t c = sm.wcnt[w][tid];
-        sm.wcnt[w][tid] = (uint16_t)run;
+        const uint32_t c = sm.wcnt[w][d];
+        sm.wcnt[w][d] = (uint16_t)run;
         run += c;
       }
-      s_tot[tid] = run;
+      s_tot[d] = run;
     }
     __syncthreads();
     if (warp == 0) {  // exclusive scan of the 256 digit totals (8 per lane)
@@ -259,11 +266,16 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
   if (*was_sorted || n <= 1) return;
   // per-trace CTA sort; the global radix sort only if some trace does not fit
   XSP_CUDA(cudaMemsetAsync(flag, 0, 4, st));
-  XSP_CUDA(cudaFuncSetAttribute(k_sort_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSegSmem));
+  auto* k_small = k_sort_seg<kSegCapSmall, 256>;
+  auto* k_large = k_sort_seg<kSegCap, 1024>;
+  constexpr size_t smem_small = sizeof(SegSmem<kSegCapSmall, 8>), smem_large = sizeof(SegSmem<kSegCap, 32>);
+  XSP_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small));
+  XSP_CUDA(cudaFuncSetAttribute(k_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_large));
   ctx->stage_begin("sort", st);
-  k_sort_seg<<<T, kSegThreads, kSegSmem, st>>>(begin, flags, sid, off, kSegCap, perm, flag);
+  k_small<<<T, 256, smem_small, st>>>(begin, flags, sid, off, 0, perm, flag);
+  k_large<<<T, 1024, smem_large, st>>>(begin, flags, sid, off, kSegCapSmall + 1, perm, flag);
   ctx->stage_end("sort", st);
-  ++ctx->launches;
+  ctx->launches += 2;
   XSP_CUDA(cudaMemcpyAsync(h, flag, 4, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
   if (!h[0] && !getenv("XSP_SORT_GLOBAL")) return;
