@@ -93,21 +93,20 @@ class ClockSampler:
 
 def pass1_bytes(b) -> int:
     """Algorithmic bytes of one k_pass1 launch: reads every span's
-    flags (1 B), begin and end (16 B), the parent_id of spans that carry one and
-    the cid of spans that carry one (8 B each); writes 16 B per placed layer
+    flags (1 B), begin and end (16 B), its placed-layer bit (k_p1_reduce, 1/8 B)
+    and the cid of spans that carry one (8 B); writes 16 B per placed layer
     (row, duration, attribute row), a 16 B entry per kernel launch / synchronous
     kernel (+4 B metric row for the latter), a 16 B entry per execution record
     with a cid, and 12 B of offsets per trace."""
     f = b.flags
     lvl, kind = f & 3, (f >> 2) & 3
     n = b.n_spans
-    has_p = int(((f & 0x10) != 0).sum())
     has_c = int(((f & 0x20) != 0).sum())
     layer = int(((lvl == 1) & (kind == 0)).sum())
     launch = int(((kind == 1) & (lvl >= 2)).sum())
     synck = int(((kind == 0) & (lvl == 2)).sum())
     exe = int(((kind == 2) & ((f & 0x20) != 0)).sum())
-    reads = n * 17 + has_p * 8 + has_c * 8
+    reads = n * 17 + n // 8 + has_c * 8
     writes = layer * 16 + (launch + synck) * 16 + synck * 4 + exe * 16 + b.n_traces * 12
     return reads + writes
 

@@ -264,6 +264,7 @@ struct P1Args {
   Full* tile_prefix;        // [ngroups + 1] exclusive prefixes of 32-tile groups + total (k_p1_scan)
   Full* tile_excl;          // [ntiles] exclusive prefix of every tile (k_p1_tile_prefix)
   Full* warp_excl;          // [ntiles * P1_WARPS] exclusive prefix of every warp within its tile
+  uint8_t* placed8;         // [n / 8] bit k of byte q: span 8q + k is a placed layer (k_p1_reduce)
   uint32_t* unsorted;
   unsigned long long* err_key;
   uint32_t* layer_row;
@@ -304,7 +305,6 @@ struct TileSmem {
   uint64_t begin[P1_TILE];
   uint64_t end[P1_TILE];
   uint64_t cid[P1_TILE];
-  uint64_t parent[P1_TILE];
   uint8_t flags[P1_TILE];
 };
 constexpr size_t P1_SMEM = sizeof(TileSmem) + 1024;  // + alignment slack
@@ -452,9 +452,12 @@ __device__ __forceinline__ RoleMasks role_masks(uint64_t fl8) {
   return m;
 }
 
-template <typename Load>
+// kHaveMask: the placement of the thread's layer spans is given by pmask (bit k
+// = span k is a placed layer, computed by k_p1_reduce), so parent_id is not
+// needed; otherwise placement is computed and recorded in pmask.
+template <bool kHaveMask, typename Load>
 __device__ __forceinline__ Full fold_thread(const TileTraces& tt, uint32_t r0, uint64_t i0, uint32_t j0,
-                                            uint32_t tile_n, uint64_t fl8, Load ld) {
+                                            uint32_t tile_n, uint64_t fl8, uint32_t& pmask, Load ld) {
   Full th = full_identity();
   TraceAttrs ta;
   uint32_t r = r0;
@@ -477,7 +480,14 @@ __device__ __forceinline__ Full fold_thread(const TileTraces& tt, uint32_t r0, u
         for (int h = 0; h < 2; ++h) {
           const int k = 2 * p + h;
           const uint8_t f = (uint8_t)(fl8 >> (8 * k));
-          if (((m.layer_sync >> k) & 1u) && placed_in(ta, f, bb[h], ee[h], pp[h])) {
+          bool placed;
+          if constexpr (kHaveMask) {
+            placed = (pmask >> k) & 1u;
+          } else {
+            placed = ((m.layer_sync >> k) & 1u) && placed_in(ta, f, bb[h], ee[h], pp[h]);
+            pmask |= (uint32_t)placed << k;
+          }
+          if (placed) {
             const uint64_t e = ee[h];
             const uint64_t w = e == ~0ull ? e : e + 1;
             th.last_M1 = th.run_M1;
@@ -510,7 +520,14 @@ __device__ __forceinline__ Full fold_thread(const TileTraces& tt, uint32_t r0, u
       }
       const bool is_layer = f_level(f) == XSP_LEVEL_LAYER;
       const uint64_t e = ee[h];
-      if (is_layer && f_kind(f) == XSP_KIND_SYNC && placed_in(ta, f, bb[h], e, pp[h])) {
+      bool placed;
+      if constexpr (kHaveMask) {
+        placed = (pmask >> k) & 1u;
+      } else {
+        placed = is_layer && f_kind(f) == XSP_KIND_SYNC && placed_in(ta, f, bb[h], e, pp[h]);
+        pmask |= (uint32_t)placed << k;
+      }
+      if (placed) {
         const uint64_t w = e == ~0ull ? e : e + 1;
         th.last_M1 = th.run_M1;
         th.last_end1 = w;
@@ -681,12 +698,14 @@ __global__ void __launch_bounds__(P1_THREADS) k_p1_reduce(P1Args a, const __grid
   if (j0 < tile_n) {
     const uint32_t r0 = tt.find(i0, thi);
     const uint64_t fl8 = *reinterpret_cast<const uint64_t*>(sm.flags + j0);
-    th = fold_thread(tt, r0, i0, j0, tile_n, fl8,
+    uint32_t pmask = 0;
+    th = fold_thread<false>(tt, r0, i0, j0, tile_n, fl8, pmask,
                      [&](int p, uint64_t (&bb)[2], uint64_t (&ee)[2], uint64_t (&pp)[2], uint8_t, uint8_t) {
                        ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
                        ld_pair(sm.end, j0 + 2 * p, ee[0], ee[1]);
                        ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
                      });
+    a.placed8[i0 >> 3] = (uint8_t)pmask;
   }
   const Full inc = warp_inclusive_fold(th, lane);
   if (lane == 31) s_wagg[warp] = inc;
@@ -777,12 +796,11 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
   if (threadIdx.x == 0 && bulk) {
     mbar_init(&s_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&s_bar, P1_TILE * (4 * 8 + 1));
+    mbar_expect_tx(&s_bar, P1_TILE * (3 * 8 + 1));
     const int y = (int)(tile_base / 16);
     tma_g2s_2d(sm.begin, &maps.begin, 0, y, &s_bar);
     tma_g2s_2d(sm.end, &maps.end, 0, y, &s_bar);
     tma_g2s_2d(sm.cid, &maps.cid, 0, y, &s_bar);
-    tma_g2s_2d(sm.parent, &maps.parent, 0, y, &s_bar);
     bulk_g2s(sm.flags, a.flags + tile_base, P1_TILE, &s_bar);
   }
   fill_trace_cache(a, tc, tlo, thi);
@@ -797,7 +815,6 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
       sm.begin[s] = v ? a.begin[i] : 0;
       sm.end[s] = v ? a.end[i] : 0;
       sm.cid[s] = v ? a.cid[i] : 0;
-      sm.parent[s] = v ? a.parent[i] : 0;
     }
   }
   __syncthreads();
@@ -808,17 +825,18 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
   uint32_t r0 = 0;
   if (j0 < tile_n) r0 = tt.find(i0, thi);
   const uint64_t fl8 = *reinterpret_cast<const uint64_t*>(sm.flags + j0);
+  uint32_t pmask = j0 < tile_n ? a.placed8[i0 >> 3] : 0u;
 
   // ---- phase 1 (recomputed from shared memory): thread fold + warp scan
   Full lane_ex;  // exclusive prefix of the thread within its warp
   {
-    const Full th = j0 < tile_n ? fold_thread(tt, r0, i0, j0, tile_n, fl8,
-                                              [&](int p, uint64_t (&bb)[2], uint64_t (&ee)[2], uint64_t (&pp)[2],
-                                                  uint8_t, uint8_t) {
-                                                ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
-                                                ld_pair(sm.end, j0 + 2 * p, ee[0], ee[1]);
-                                                ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
-                                              })
+    const Full th = j0 < tile_n ? fold_thread<true>(tt, r0, i0, j0, tile_n, fl8, pmask,
+                                                    [&](int p, uint64_t (&bb)[2], uint64_t (&ee)[2],
+                                                        uint64_t (&pp)[2], uint8_t, uint8_t) {
+                                                      ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
+                                                      ld_pair(sm.end, j0 + 2 * p, ee[0], ee[1]);
+                                                      pp[0] = pp[1] = 0;
+                                                    })
                                 : full_identity();
     const Full inc = warp_inclusive_fold(th, lane);
     const uint32_t* s = reinterpret_cast<const uint32_t*>(&inc);
@@ -846,10 +864,9 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
   }
 #pragma unroll kP1EmitUnroll
   for (int p = 0; p < P1_ITEMS / 2; ++p) {
-    uint64_t bb[2], ee[2], pp[2], cc[2];
+    uint64_t bb[2], ee[2], cc[2];
     ld_pair(sm.begin, j0 + 2 * p, bb[0], bb[1]);
     ld_pair(sm.end, j0 + 2 * p, ee[0], ee[1]);
-    ld_pair(sm.parent, j0 + 2 * p, pp[0], pp[1]);
     ld_pair(sm.cid, j0 + 2 * p, cc[0], cc[1]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -897,7 +914,7 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
       c_metric += met;
       if (f_level(f) == XSP_LEVEL_LAYER) {
         const bool layer_sync = f_kind(f) == XSP_KIND_SYNC;
-        if (layer_sync && placed_in(ta, f, b, e, pp[h])) {
+        if (layer_sync && ((pmask >> k) & 1u)) {
           a.layer_row[g] = (uint32_t)i;
           a.layer_dur[g] = clamp_dur(b, e);
           a.layer_attr_row[g] = c_lay;
@@ -1658,6 +1675,7 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.ntiles = ntiles;
   a.tile_excl = ctx->d<Full>("c.tile_excl", ntiles + 1);
   a.warp_excl = ctx->d<Full>("c.warp_excl", (uint64_t)ntiles * P1_WARPS + 1);
+  a.placed8 = ctx->d<uint8_t>("c.placed8", n / 8 + 16);
   a.group_sum = ctx->d<Full>("c.tile_gsum", ntiles / 32 + 2);
   a.group_done = ctx->d<uint32_t>("c.group_done", ntiles / 32 + 2);
   XSP_CUDA(cudaMemsetAsync(a.group_done, 0, (ntiles / 32 + 2) * 4, st));
