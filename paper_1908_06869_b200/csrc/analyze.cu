@@ -302,7 +302,10 @@ __device__ __forceinline__ uint32_t group_of(const uint32_t* __restrict__ off, u
 // Per (group, kernel ordinal): combine() over repetitions (analysis.cpp:146-167)
 // and the a8 / a9 row (:342-397). One thread per kernel keeps R independent
 // gathers in flight.
-__global__ void k_kernels(LayerArgs a, uint32_t total_kernels) {
+#ifndef XSP_KK_MINB
+#define XSP_KK_MINB 3  // 80 registers, no spills: 3 CTAs of 256 per SM
+#endif
+__global__ void __launch_bounds__(256, XSP_KK_MINB) k_kernels(LayerArgs a, uint32_t total_kernels) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= total_kernels) return;
   const uint32_t g = group_of(a.gk_off, a.G, q);
