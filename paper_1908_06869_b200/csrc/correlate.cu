@@ -1419,7 +1419,7 @@ __global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val, 
 // launches and execs, every entry a launch with a cid, equal cids at equal
 // rank, strictly increasing). The same pass verifies that; any failure sets
 // *fail and the caller reruns the general join.
-__global__ void k_gather_fast(uint32_t nk, uint32_t nex, const KlEnt* __restrict__ kl,
+__device__ __forceinline__ void gather_fast_one(uint32_t j, uint32_t first, uint32_t nl, uint32_t nk, uint32_t nex, const KlEnt* __restrict__ kl,
                               const ExEnt* __restrict__ ex, const uint8_t* __restrict__ flags,
                               const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
                               uint32_t T, const uint64_t* __restrict__ begin, const uint64_t* __restrict__ end,
@@ -1427,16 +1427,21 @@ __global__ void k_gather_fast(uint32_t nk, uint32_t nex, const KlEnt* __restrict
                               uint32_t* __restrict__ k_launch, uint32_t* __restrict__ k_exec,
                               uint32_t* __restrict__ k_mrow, uint64_t* __restrict__ k_dur,
                               uint32_t* __restrict__ k_name, double* __restrict__ k_occ,
-                              uint32_t* __restrict__ l_koff, uint32_t nl, uint32_t* __restrict__ fail) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t first = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+                              uint32_t* __restrict__ l_koff, uint32_t* __restrict__ fail) {
   if (first > nk) return;
   uint32_t t = 0;
   if (nk) t = warp_trace_of(t_kl_off, T, j < nk ? j : nk - 1, first < nk ? first : nk - 1);
   if (j > nk) return;
-  // layer CSR boundaries (keys = parents, non-decreasing)
-  const int64_t prev = j > 0 ? (int64_t)kl[j - 1].parent : -1;
-  const int64_t cur = j < nk ? (int64_t)kl[j].parent : (int64_t)nl;
+  // layer CSR boundaries (keys = parents, non-decreasing); a pending / orphan /
+  // ambiguous parent means the batch is not clean (the general path redoes it)
+  const uint32_t pp = j > 0 ? kl[j - 1].parent : 0u;
+  const uint32_t pc = j < nk ? kl[j].parent : nl;
+  if ((j > 0 && pp >= PAR_MAXROW) || pc >= PAR_MAXROW) {
+    *fail = 1;
+    return;
+  }
+  const int64_t prev = j > 0 ? (int64_t)pp : -1;
+  const int64_t cur = (int64_t)pc;
   for (int64_t g = prev + 1; g <= cur; ++g) l_koff[g] = j;
   if (j == nk) {
     if (nex != nk) *fail = 1;  // some trace has execs but no launches
@@ -1465,6 +1470,25 @@ __global__ void k_gather_fast(uint32_t nk, uint32_t nex, const KlEnt* __restrict
   k_dur[j] = clamp_dur(begin[e.row], end[e.row]);
   k_name[j] = name[e.row];
   k_occ[j] = e.mrow != kNone ? occ[e.mrow] : 0.0;
+}
+
+// Sizes come from pass 1's totals on the device and the grid strides over them,
+// so the clean path needs no host round trip before it runs.
+__global__ void __launch_bounds__(256) k_gather_fast(const uint32_t* __restrict__ totals,
+                              const KlEnt* __restrict__ kl,
+                              const ExEnt* __restrict__ ex, const uint8_t* __restrict__ flags,
+                              const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
+                              uint32_t T, const uint64_t* __restrict__ begin, const uint64_t* __restrict__ end,
+                              const uint32_t* __restrict__ name, const double* __restrict__ occ,
+                              uint32_t* __restrict__ k_launch, uint32_t* __restrict__ k_exec,
+                              uint32_t* __restrict__ k_mrow, uint64_t* __restrict__ k_dur,
+                              uint32_t* __restrict__ k_name, double* __restrict__ k_occ,
+                              uint32_t* __restrict__ l_koff, uint32_t* __restrict__ fail) {
+  const uint32_t nl = totals[0], nk = totals[1], nex = totals[2];
+  for (uint32_t base = blockIdx.x * blockDim.x; base <= nk; base += gridDim.x * blockDim.x)
+    gather_fast_one(base + threadIdx.x, base + (threadIdx.x & ~31u), nl, nk, nex, kl, ex, flags, t_kl_off,
+                    t_ex_off, T, begin, end, name, occ, k_launch, k_exec, k_mrow, k_dur, k_name, k_occ, l_koff,
+                    fail);
 }
 
 // layer_kernel_off[g] = first kernel j whose parent >= g (keys sorted): each
@@ -1737,8 +1761,41 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
                                                                a.t_kl_off, a.t_ex_off, totals);
   ++ctx->launches;
   uint32_t* htot = ctx->h<uint32_t>("c.totals_h", 16);
+  // ---- optimistic clean path, launched before any host round trip: a batch
+  // with no orphan, ambiguity or explicit-parent kernel whose traces are all
+  // merge-aligned fuses launch r with exec r (k_gather_fast verifies it). Buffers
+  // are sized by the span count; the device totals gate the kernels. ONE
+  // read-back then decides: done, unsorted, or the general path below.
+  const bool try_clean = !parents_only;
+  auto* no_dup = ctx->d<unsigned long long>("c.no_dup", T);
+  if (try_clean) {
+    out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", n);
+    out->kernel_exec_row = ctx->d<uint32_t>("o.k_exec", n);
+    out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", n);
+    out->kernel_dur = ctx->d<uint64_t>("o.k_dur", n);
+    out->kernel_name = ctx->d<uint32_t>("o.k_name", n);
+    out->kernel_occ = ctx->d<double>("o.k_occ", n);
+    out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", n + 1);
+    ctx->stage_begin("gather", st);
+    const unsigned gb = std::min<uint64_t>(ceil_div((uint64_t)n + 1, 256), 148u * 8u);
+    k_gather_fast<<<gb, 256, 0, st>>>(totals, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, c->begin_ns,
+                                      c->end_ns, c->name_id, c->occupancy, out->kernel_launch_row,
+                                      out->kernel_exec_row, out->kernel_metric_row, out->kernel_dur,
+                                      out->kernel_name, out->kernel_occ, out->layer_kernel_off, counters + 7);
+    ++ctx->launches;
+    out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
+    launch(ctx, k_trace_kernel_off, (uint64_t)T + 1, st, T, a.t_layer_off, out->layer_kernel_off,
+           out->trace_kernel_off);
+    XSP_CUDA(cudaMemsetAsync(no_dup, 0xFF, T * 8ull, st));
+    out->trace_status = ctx->d<int32_t>("o.t_status", T);
+    out->trace_err_row = ctx->d<uint32_t>("o.t_err_row", 2ull * T);
+    launch(ctx, k_status, T, st, T, model_row, err_key, no_dup, no_dup, a.ex, a.kl, out->trace_status,
+           out->trace_err_row, counters + 4);
+    cache_offsets_begin(ctx, a.t_layer_off, out->trace_kernel_off, T, st);
+    ctx->stage_end("gather", st);
+  }
   xfer_small(htot, totals, 5 * 4, st);
-  xfer_small(htot + 8, counters, 6 * 4, st);
+  xfer_small(htot + 8, counters, 8 * 4, st);
   XSP_CUDA(cudaStreamSynchronize(st));
   const uint32_t nl = htot[0], nkl = htot[1], nex = htot[2];
   const uint32_t n_amb_raw = htot[9], n_pend = htot[10];
@@ -1747,6 +1804,33 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     (void)sort_if_needed;
     throw std::runtime_error("UNSORTED");
   }
+  if (try_clean && htot[8] == 0 && n_pend == 0 && n_amb_raw == 0 && htot[15] == 0) {
+    cache_offsets_end(ctx, a.t_layer_off, out->trace_kernel_off, T);
+    out->n_traces = T;
+    out->n_failed = htot[12];
+    out->trace_model_row = model_row;
+    out->n_kernels = nkl;
+    out->n_layers = nl;
+    out->layer_row = a.layer_row;
+    out->layer_dur = a.layer_dur;
+    out->layer_attr_row = a.layer_attr_row;
+    out->trace_layer_off = a.t_layer_off;
+    out->n_orphans = 0;
+    out->orphan_row = ctx->d<uint32_t>("o.orphan_row", 1);
+    out->orphan_reason = ctx->d<uint8_t>("o.orphan_reason", 1);
+    out->trace_orphan_off = ctx->d<uint32_t>("o.t_orph_off", T + 1);
+    XSP_CUDA(cudaMemsetAsync(out->trace_orphan_off, 0, (T + 1) * 4ull, st));
+    out->n_ambiguities = 0;
+    out->n_candidates = 0;
+    out->trace_amb_off = ctx->d<uint32_t>("o.t_amb_off", T + 1);
+    out->amb_row = ctx->d<uint32_t>("o.amb_row", 1);
+    out->amb_cand_off = ctx->d<uint32_t>("o.amb_cand_off", 1);
+    out->amb_cand_row = ctx->d<uint32_t>("o.amb_cand_row", 1);
+    XSP_CUDA(cudaMemsetAsync(out->trace_amb_off, 0, (T + 1) * 4ull, st));
+    XSP_CUDA(cudaMemsetAsync(out->amb_cand_off, 0, 4, st));
+    return;
+  }
+  if (try_clean) XSP_CUDA(cudaMemsetAsync(counters + 4, 0, 4 * 4, st));  // general path: reset n_failed, flags
 
   // ---- explicit parents
   if (n_pend) {
@@ -1807,55 +1891,6 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
     out->amb_cand_row = ctx->d<uint32_t>("o.amb_cand_row", 1);
     XSP_CUDA(cudaMemsetAsync(out->trace_amb_off, 0, (T + 1) * 4ull, st));
     XSP_CUDA(cudaMemsetAsync(out->amb_cand_off, 0, 4, st));
-  }
-
-  // ---- clean batch: optimistic merge-aligned fusion (general path on failure)
-  if (htot[8] == 0 && n_pend == 0 && n_amb_raw == 0 && !parents_only) {
-    ctx->stage_begin("gather", st);
-    out->n_kernels = nkl;
-    out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", nkl);
-    out->kernel_exec_row = ctx->d<uint32_t>("o.k_exec", nkl);
-    out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", nkl);
-    out->kernel_dur = ctx->d<uint64_t>("o.k_dur", nkl);
-    out->kernel_name = ctx->d<uint32_t>("o.k_name", nkl);
-    out->kernel_occ = ctx->d<double>("o.k_occ", nkl);
-    out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", nl + 1);
-    uint32_t* fail = counters + 7;
-    launch(ctx, k_gather_fast, (uint64_t)nkl + 1, st, nkl, nex, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T,
-           c->begin_ns, c->end_ns, c->name_id, c->occupancy, out->kernel_launch_row, out->kernel_exec_row,
-           out->kernel_metric_row, out->kernel_dur, out->kernel_name, out->kernel_occ, out->layer_kernel_off, nl,
-           fail);
-    out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
-    launch(ctx, k_trace_kernel_off, (uint64_t)T + 1, st, T, a.t_layer_off, out->layer_kernel_off,
-           out->trace_kernel_off);
-    out->n_traces = T;
-    out->trace_status = ctx->d<int32_t>("o.t_status", T);
-    out->trace_err_row = ctx->d<uint32_t>("o.t_err_row", 2ull * T);
-    out->trace_model_row = model_row;
-    auto* no_dup = ctx->d<unsigned long long>("c.no_dup", T);
-    XSP_CUDA(cudaMemsetAsync(no_dup, 0xFF, T * 8ull, st));
-    launch(ctx, k_status, T, st, T, model_row, err_key, no_dup, no_dup, a.ex, a.kl, out->trace_status,
-           out->trace_err_row, counters + 4);
-    xfer_small(htot, counters + 4, 16, st);
-    cache_offsets_begin(ctx, a.t_layer_off, out->trace_kernel_off, T, st);
-    XSP_CUDA(cudaStreamSynchronize(st));
-    ctx->stage_end("gather", st);
-    if (!htot[3]) {
-      cache_offsets_end(ctx, a.t_layer_off, out->trace_kernel_off, T);
-      out->n_failed = htot[0];
-      out->n_layers = nl;
-      out->layer_row = a.layer_row;
-      out->layer_dur = a.layer_dur;
-      out->layer_attr_row = a.layer_attr_row;
-      out->trace_layer_off = a.t_layer_off;
-      out->n_orphans = 0;
-      out->orphan_row = ctx->d<uint32_t>("o.orphan_row", 1);
-      out->orphan_reason = ctx->d<uint8_t>("o.orphan_reason", 1);
-      out->trace_orphan_off = ctx->d<uint32_t>("o.t_orph_off", T + 1);
-      XSP_CUDA(cudaMemsetAsync(out->trace_orphan_off, 0, (T + 1) * 4ull, st));
-      return;
-    }
-    XSP_CUDA(cudaMemsetAsync(counters + 4, 0, 4 * 4, st));  // retry: reset n_failed, flags
   }
 
   // ---- cid join: merge-aligned check, hash table for the other traces
