@@ -699,7 +699,7 @@ struct NameFastArgs {
   double peak, bw;
   uint32_t* g_count;    // distinct names per group
   uint32_t* overflow;   // any group exceeded NCAP
-  uint32_t* ks_slot;    // [TK] scratch: name slot of each kernel
+  uint32_t* ks_slot;    // [TK] scratch: name slot of each kernel (groups above kNameSmemCap)
   uint32_t* ks_rank;    // [TK] scratch: rank of the kernel within its name
   uint32_t* perm;       // [TK] scratch: kernels grouped by name, tree order within
   // rows per group in final order, staged at [g * NCAP, g * NCAP + count)
@@ -719,7 +719,16 @@ struct NameFastArgs {
 // One CTA (NAME_WARPS warps) per group. Warp w hashes the w-th quarter of the
 // group's kernels; stable ranks within a name combine the warp's running count
 // with the counts of the earlier warps (tree order = warp order, then lane order).
+// Groups of at most kNameSmemCap kernels keep the per-kernel slot (u8), rank
+// and the by-name permutation (u16, group-local) in shared memory.
+constexpr uint32_t kNameSmemCap = 8192;
+constexpr size_t kNameSmem = kNameSmemCap * (1 + 2 + 2);
+
 __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) {
+  extern __shared__ __align__(16) unsigned char nm_dyn[];
+  uint8_t* s_slot = nm_dyn;
+  uint16_t* s_rank = reinterpret_cast<uint16_t*>(nm_dyn + kNameSmemCap);
+  uint16_t* s_perm = s_rank + kNameSmemCap;
   __shared__ NameTable T;
   __shared__ uint32_t wcnt[NAME_WARPS][NCAP];  // per-warp per-slot counts
   __shared__ uint32_t s_over;
@@ -744,6 +753,7 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
   }
   __syncthreads();
   const uint32_t k0 = a.gk_off[g], k1 = a.gk_end ? a.gk_end[g] : a.gk_off[g + 1];
+  const bool sm_ok = k1 - k0 <= kNameSmemCap;
   const uint32_t q = (k1 - k0 + NAME_WARPS * 32 - 1) / (NAME_WARPS * 32) * 32;  // warp quarter, 32-aligned
   const uint32_t w0 = min(k1, k0 + warp * q), w1 = min(k1, w0 + q);
   const uint32_t lt = lanemask_lt();
@@ -781,8 +791,13 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
     __syncwarp();
     if (v && (peers & lt) == 0) wcnt[warp][slot] = rank + __popc(peers);
     if (v) {
-      a.ks_slot[x] = slot;
-      a.ks_rank[x] = rank + __popc(peers & lt);
+      if (sm_ok) {
+        s_slot[x - k0] = (uint8_t)slot;
+        s_rank[x - k0] = (uint16_t)(rank + __popc(peers & lt));
+      } else {
+        a.ks_slot[x] = slot;
+        a.ks_rank[x] = rank + __popc(peers & lt);
+      }
     }
     __syncwarp();
   }
@@ -832,8 +847,13 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
   __syncthreads();
   // pass C: stable scatter of kernel ordinals by name
   for (uint32_t x = w0 + lane; x < w1; x += 32) {
-    const uint32_t s = a.ks_slot[x];
-    a.perm[k0 + T.start[s] + wcnt[warp][s] + a.ks_rank[x]] = x;
+    if (sm_ok) {
+      const uint32_t s = s_slot[x - k0];
+      s_perm[T.start[s] + wcnt[warp][s] + s_rank[x - k0]] = (uint16_t)(x - k0);
+    } else {
+      const uint32_t s = a.ks_slot[x];
+      a.perm[k0 + T.start[s] + wcnt[warp][s] + a.ks_rank[x]] = x;
+    }
   }
   __syncthreads();
   // pass D: one thread per name walks that name's kernels in tree order
@@ -848,7 +868,7 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
       double l8[8], o8[8];
 #pragma unroll
       for (int u2 = 0; u2 < 8; ++u2) {
-        const uint32_t x = a.perm[b + i + u2];
+        const uint32_t x = sm_ok ? k0 + s_perm[b - k0 + i + u2] : a.perm[b + i + u2];
         l8[u2] = a.k_lat[x];
         o8[u2] = a.k_occ[x];
         f += a.k_flops[x];
@@ -862,7 +882,7 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
       }
     }
     for (; i < n; ++i) {
-      const uint32_t x = a.perm[b + i];
+      const uint32_t x = sm_ok ? k0 + s_perm[b - k0 + i] : a.perm[b + i];
       const double l = a.k_lat[x];
       lat = __dadd_rn(lat, l);
       occw = __dadd_rn(occw, __dmul_rn(a.k_occ[x], l));
@@ -1494,7 +1514,8 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     nf.big = d_gkc;
     nf.raw = 0;
     XSP_CUDA(cudaMemsetAsync(nf.overflow, 0, 4, st));
-    k_names_fast<<<G, NAME_WARPS * 32, 0, st>>>(nf);
+    XSP_CUDA(cudaFuncSetAttribute(k_names_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNameSmem));
+    k_names_fast<<<G, NAME_WARPS * 32, kNameSmem, st>>>(nf);
     ++ctx->launches;
     if (nkc) {
       // long groups: raw per-name sums per kernel chunk, then folded in order
@@ -1514,7 +1535,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       nc.s_flops = ctx->d<uint64_t>("a.c_f", ccap);
       nc.s_read = ctx->d<uint64_t>("a.c_r", ccap);
       nc.s_write = ctx->d<uint64_t>("a.c_w", ccap);
-      k_names_fast<<<nkc, NAME_WARPS * 32, 0, st>>>(nc);
+      k_names_fast<<<nkc, NAME_WARPS * 32, kNameSmem, st>>>(nc);
       NameBigArgs nb;
       nb.G = G;
       nb.gkc_off = d_gkc;
