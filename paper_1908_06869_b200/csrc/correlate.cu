@@ -3,7 +3,7 @@
 //
 // Reference semantics: assign_parents (correlator.cpp:141-282) and
 // correlate_async (correlator.cpp:287-364). The reference walks an interval
-// tree per child span; here the whole batch is ONE decoupled-look-back scan
+// tree per child span; here the whole batch is ONE reduce-then-scan
 // over the timeline-ordered span columns (pass 1):
 //   * layers are placed by a per-span compare against their trace's model span
 //     and numbered by a global placed-layer count (layer_index = count - trace base);
@@ -145,7 +145,7 @@ __global__ void k_trace_prep(const uint8_t* __restrict__ flags, const uint64_t* 
 }
 
 // ---------------------------------------------------------------------------
-// Pass-1 scan state (the decoupled look-back payload). Ends are stored as
+// Pass-1 scan state (the scan payload of a tile / warp / thread). Ends are stored as
 // end+1 so that 0 means "no layer".
 struct Full {
   uint64_t last_end1;  // end+1 of the last placed layer of the current trace segment
@@ -239,7 +239,6 @@ constexpr int P1_SCAN_THREADS = 1024;
 
 struct P1Args {
   int bulk;     // full tiles staged by TMA tensor copies (columns 16-byte aligned)
-  int aligned;  // begin/end 16-byte and flags 8-byte aligned (vector loads in k_p1_reduce)
   int parents_only;
   const uint64_t* span_id;
   const uint8_t* flags;
@@ -1731,7 +1730,6 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   a.bulk = n >= (uint64_t)P1_TILE && al16(c->begin_ns) && al16(c->end_ns) && al16(c->cid) &&
            al16(c->parent_id) && al16(c->flags);
-  a.aligned = al16(c->begin_ns) && al16(c->end_ns) && (reinterpret_cast<uintptr_t>(c->flags) & 7u) == 0;
   P1Maps maps;
   memset(&maps, 0, sizeof(maps));
   if (a.bulk) {
