@@ -12,7 +12,7 @@
  *   TraceBundle / Span (span.hpp:81-171)        xsp_span_cols + trace offsets
  *   correlate()   (correlator.hpp:164)          xsp_correlate
  *   assign_parents + correlate_async (:154,161) (both inside xsp_correlate)
- *   a8..a15, model_roofline (analysis.hpp:256-366) xsp_analyze
+ *   a5..a15, model_roofline (analysis.hpp:128-366) xsp_analyze
  *   LeveledRunGroup + compute_overhead (leveled.hpp:60-109) xsp_leveled
  *   validate_bundle (span.hpp:187)              xsp_validate / xsp_validate_host
  *   sort_timeline (span.hpp:190)                xsp_sort_timeline / xsp_sort_timeline_host
@@ -231,6 +231,14 @@ typedef struct xsp_tables_out {
   double* m_occ; uint64_t* m_count; double* m_ai; double* m_tput; int8_t* m_bound;
   double* m_gpu; double* m_gpu_pct; double* m_throughput;
   uint8_t* m_roofline_in;
+  /* a5 / a6 / a7 (analysis.cpp:315-337): per (group, layer type) over the
+   * combined layers in execution order — layer count, total trimmed-mean
+   * latency (fp64, summed in layer order) and total alloc_bytes of the first
+   * run; rows sorted by total latency desc, type asc. type_id indexes the
+   * layer-type string table (byte-lexicographic, so id order = string order). */
+  uint64_t n_type_rows;
+  uint32_t* group_type_off; /* [n_groups + 1] */
+  uint32_t* y_type; uint64_t* y_count; double* y_lat; int64_t* y_alloc;
 } xsp_tables_out;
 
 /* ---- leveled measurement (stage f) ----------------------------------------- */
@@ -363,7 +371,8 @@ xsp_status xsp_sort_timeline_host(xsp_ctx* ctx, uint64_t n_spans, const uint64_t
  * existing entity trees); only the columns the analysis reads must be set:
  * trace_status, trace_model_row, trace_layer_off, trace_kernel_off,
  * trace_amb_off, layer_row, layer_kernel_off, layer_dur, kernel_metric_row,
- * kernel_dur, kernel_name, kernel_occ. */
+ * kernel_dur, kernel_name, kernel_occ; a5-a7 also read layer_attr_row and the
+ * layer table (type_id, alloc_bytes) when they are set. */
 xsp_status xsp_correlate_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces, int mode,
                               xsp_corr_out* out);
 xsp_status xsp_analyze_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,

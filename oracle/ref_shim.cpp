@@ -634,10 +634,16 @@ XSPREF_API void* xspref_analyze(const SoaIn* in, const std::uint32_t* group_firs
     bag->ensure(k, 'B');
   bag->ensure("g_status", 'i');
   bag->str_init("g_error");
-  std::uint64_t nk = 0, nl = 0, nn = 0;
+  bag->ensure("g_type_off", 'Q');
+  bag->ensure("y_count", 'Q');
+  bag->ensure("y_alloc", 'q');
+  bag->ensure("y_lat", 'd');
+  bag->str_init("y_type");
+  std::uint64_t nk = 0, nl = 0, nn = 0, ny = 0;
   bag->u64("g_kernel_off", 0);
   bag->u64("g_layer_off", 0);
   bag->u64("g_name_off", 0);
+  bag->u64("g_type_off", 0);
   for (std::uint32_t g = 0; g < n_groups; ++g) {
     try {
       AnalysisInput input;
@@ -653,6 +659,14 @@ XSPREF_API void* xspref_analyze(const SoaIn* in, const std::uint32_t* group_firs
       ModelAggregateTable a15 = a15_model_aggregate({input}, spec, opts);
       RooflineReport mr = model_roofline({input}, spec, opts);
       ModelInfoTable a1 = a1_model_info({input}, opts);
+      LayerTypeTable a5 = a5_a6_a7_by_type(input, opts);
+      for (const auto& row : a5.rows) {
+        bag->str("y_type", row.type);
+        bag->u64("y_count", row.count);
+        bag->f64("y_lat", row.total_latency_ns);
+        bag->i64("y_alloc", row.total_alloc_bytes);
+      }
+      ny += a5.rows.size();
       bag->i32("g_status", 0);
       bag->str("g_error", "");
       for (const auto& row : a8.rows) {
@@ -773,6 +787,7 @@ XSPREF_API void* xspref_analyze(const SoaIn* in, const std::uint32_t* group_firs
     bag->u64("g_kernel_off", nk);
     bag->u64("g_layer_off", nl);
     bag->u64("g_name_off", nn);
+    bag->u64("g_type_off", ny);
   }
   return bag;
 }

@@ -572,6 +572,9 @@ typedef struct {
   vu64 m_flops, m_read, m_write, m_count;
   vi8 m_bound;
   vu8 m_in;
+  vu32 goff_y, y_type;
+  vu64 y_count, y_alloc;
+  vf64 y_lat;
 } tab_acc;
 
 typedef struct {
@@ -600,6 +603,7 @@ int xspo_analyze(const xsp_span_cols* c, const xsp_corr_out* co, const xsp_group
   vu32_push(&A.goff_l, 0);
   vu32_push(&A.goff_k, 0);
   vu32_push(&A.goff_n, 0);
+  vu32_push(&A.goff_y, 0);
   for (uint32_t g = 0; g < gr->n_groups; ++g) {
     const uint32_t t0 = gr->first_trace[g], R = gr->n_runs[g];
     int32_t st = XSP_G_OK;
@@ -635,6 +639,7 @@ int xspo_analyze(const xsp_span_cols* c, const xsp_corr_out* co, const xsp_group
       vu32_push(&A.goff_l, (uint32_t)A.l_index.n);
       vu32_push(&A.goff_k, (uint32_t)A.k_lat.n);
       vu32_push(&A.goff_n, (uint32_t)A.n_name.n);
+      vu32_push(&A.goff_y, (uint32_t)A.y_type.n);
       vf64_push(&A.m_lat, NAN);
       vf64_push(&A.m_klat, 0);
       vu64_push(&A.m_flops, 0);
@@ -662,10 +667,27 @@ int xspo_analyze(const xsp_span_cols* c, const xsp_corr_out* co, const xsp_group
     const size_t kbase = A.k_lat.n;
     const uint32_t tk0 = co->trace_kernel_off[t0];
     double model_gpu = 0.0;
+    const size_t ybase = A.y_type.n;
     for (uint32_t li = 0; li < L0; ++li) {
       for (uint32_t r = 0; r < R; ++r) v[r] = (double)co->layer_dur[co->trace_layer_off[t0 + r] + li];
       const double llat = trimmed_mean(v, R, o->trim_fraction);
       const uint32_t gl0 = co->trace_layer_off[t0] + li;
+      {
+        /* a5-a7 by layer type (analysis.cpp:315-337): accumulate in execution order */
+        const uint32_t ar0 = co->layer_attr_row[gl0];
+        const uint32_t ty = c->type_id[ar0];
+        size_t y = ybase;
+        while (y < A.y_type.n && A.y_type.v[y] != ty) ++y;
+        if (y == A.y_type.n) {
+          vu32_push(&A.y_type, ty);
+          vu64_push(&A.y_count, 0);
+          vf64_push(&A.y_lat, 0.0);
+          vu64_push(&A.y_alloc, 0);
+        }
+        A.y_count.v[y] += 1;
+        A.y_lat.v[y] += llat;
+        A.y_alloc.v[y] += (uint64_t)c->alloc_bytes[ar0];
+      }
       double acc_lat = 0.0, acc_occw = 0.0;
       uint64_t af = 0, ar = 0, aw = 0, an = 0;
       krow* kr = (krow*)malloc((co->layer_kernel_off[gl0 + 1] - co->layer_kernel_off[gl0] + 1) * sizeof(krow));
@@ -829,8 +851,27 @@ int xspo_analyze(const xsp_span_cols* c, const xsp_corr_out* co, const xsp_group
       }
     }
     free(byname);
+    /* a5 rows: total latency desc, then type asc (std::map order + stable_sort) */
+    for (size_t i = ybase + 1; i < A.y_type.n; ++i) {
+      for (size_t j = i; j > ybase && (A.y_lat.v[j - 1] < A.y_lat.v[j] ||
+                                       (A.y_lat.v[j - 1] == A.y_lat.v[j] && A.y_type.v[j - 1] > A.y_type.v[j]));
+           --j) {
+#define SWAPY(vec, T)                \
+  do {                               \
+    T tmp_ = vec.v[j];               \
+    vec.v[j] = vec.v[j - 1];         \
+    vec.v[j - 1] = tmp_;             \
+  } while (0)
+        SWAPY(A.y_type, uint32_t);
+        SWAPY(A.y_count, uint64_t);
+        SWAPY(A.y_lat, double);
+        SWAPY(A.y_alloc, uint64_t);
+#undef SWAPY
+      }
+    }
     free(v);
     free(w);
+    vu32_push(&A.goff_y, (uint32_t)A.y_type.n);
     vu32_push(&A.goff_l, (uint32_t)A.l_index.n);
     vu32_push(&A.goff_k, (uint32_t)A.k_lat.n);
     vu32_push(&A.goff_n, (uint32_t)A.n_name.n);
@@ -899,6 +940,12 @@ int xspo_analyze(const xsp_span_cols* c, const xsp_corr_out* co, const xsp_group
   out->m_gpu_pct = A.m_gpct.v;
   out->m_throughput = A.m_tp.v;
   out->m_roofline_in = A.m_in.v;
+  out->n_type_rows = A.y_type.n;
+  out->group_type_off = A.goff_y.v;
+  out->y_type = A.y_type.v;
+  out->y_count = A.y_count.v;
+  out->y_lat = A.y_lat.v;
+  out->y_alloc = (int64_t*)A.y_alloc.v;
   return 0;
 }
 
@@ -912,7 +959,8 @@ void xspo_tables_free(xsp_tables_out* o) {
                 o->n_name, o->n_count, o->n_lat, o->n_pct, o->n_flops, o->n_read, o->n_write,
                 o->n_occ, o->n_ai, o->n_tput, o->n_bound, o->m_lat, o->m_kern_lat, o->m_flops,
                 o->m_read, o->m_write, o->m_occ, o->m_count, o->m_ai, o->m_tput, o->m_bound,
-                o->m_gpu, o->m_gpu_pct, o->m_throughput, o->m_roofline_in};
+                o->m_gpu, o->m_gpu_pct, o->m_throughput, o->m_roofline_in, o->group_type_off,
+                o->y_type, o->y_count, o->y_lat, o->y_alloc};
   for (size_t i = 0; i < sizeof(ps) / sizeof(ps[0]); ++i) free(ps[i]);
   memset(o, 0, sizeof(*o));
 }

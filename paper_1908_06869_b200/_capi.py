@@ -114,14 +114,21 @@ TABLE_FIELDS = [
     ("m_read", u64p, "G"), ("m_write", u64p, "G"), ("m_occ", f64p, "G"), ("m_count", u64p, "G"),
     ("m_ai", f64p, "G"), ("m_tput", f64p, "G"), ("m_bound", i8p, "G"), ("m_gpu", f64p, "G"),
     ("m_gpu_pct", f64p, "G"), ("m_throughput", f64p, "G"), ("m_roofline_in", u8p, "G"),
+    # a5 / a6 / a7 by layer type (after the n_type_rows count in the C struct)
+    ("group_type_off", u32p, "G1"), ("y_type", u32p, "Y"), ("y_count", u64p, "Y"), ("y_lat", f64p, "Y"),
+    ("y_alloc", i64p, "Y"),
 ]
+
+
+_TYPE_FIELDS = ("group_type_off", "y_type", "y_count", "y_lat", "y_alloc")
 
 
 class TablesOut(C.Structure):
     _fields_ = [
         ("n_groups", C.c_uint32),
         ("n_layers", C.c_uint64), ("n_kernels", C.c_uint64), ("n_names", C.c_uint64),
-    ] + [(n, t) for n, t, _ in TABLE_FIELDS]
+    ] + [(n, t) for n, t, _ in TABLE_FIELDS if n not in _TYPE_FIELDS] + [("n_type_rows", C.c_uint64)] + [
+        (n, t) for n, t, _ in TABLE_FIELDS if n in _TYPE_FIELDS]
 
 
 class LevelSets(C.Structure):

@@ -12,6 +12,7 @@
 // by one thread per subject in tree order, as the reference does.
 
 #include <algorithm>
+#include <functional>
 #include <vector>
 
 #include "ctx.h"
@@ -238,6 +239,11 @@ __global__ void k_group_status(uint32_t G, const uint32_t* __restrict__ nr,
 
 struct LayerArgs {
   uint32_t G, total_layers, top_k;
+  const uint32_t* layer_attr_row;  // layer-table row of each layer (type_id, alloc_bytes)
+  const uint32_t* type_id;
+  const int64_t* alloc_bytes;
+  uint32_t* l_type;    // canonical layer's type (a5 keys)
+  uint64_t* l_alloc;   // canonical layer's alloc_bytes (two's complement, a7 sums)
   const uint32_t* gl_off;
   const uint32_t* gk_off;
   const uint32_t* ft;
@@ -384,6 +390,14 @@ __global__ void k_layers(LayerArgs a) {
     }
   }
   const uint32_t lo_out = q;
+  if (a.layer_attr_row && a.type_id && a.alloc_bytes) {
+    const uint32_t ar = a.layer_attr_row[gl0];
+    a.l_type[lo_out] = a.type_id[ar];
+    a.l_alloc[lo_out] = (uint64_t)a.alloc_bytes[ar];
+  } else {  // no layer table: every layer of type 0, no allocations
+    a.l_type[lo_out] = 0;
+    a.l_alloc[lo_out] = 0;
+  }
   const Roof ro = roofline(acc_f, acc_r, acc_w, acc_lat, a.peak, a.bw);
   a.l_index[lo_out] = li;
   a.l_row[lo_out] = a.layer_row[gl0];
@@ -870,10 +884,10 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
       for (int u2 = 0; u2 < 8; ++u2) {
         const uint32_t x = sm_ok ? k0 + s_perm[b - k0 + i + u2] : a.perm[b + i + u2];
         l8[u2] = a.k_lat[x];
-        o8[u2] = a.k_occ[x];
+        o8[u2] = a.k_occ ? a.k_occ[x] : 0.0;
         f += a.k_flops[x];
-        rd += a.k_read[x];
-        wr += a.k_write[x];
+        if (a.k_read) rd += a.k_read[x];
+        if (a.k_write) wr += a.k_write[x];
       }
 #pragma unroll
       for (int u2 = 0; u2 < 8; ++u2) {
@@ -885,10 +899,10 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
       const uint32_t x = sm_ok ? k0 + s_perm[b - k0 + i] : a.perm[b + i];
       const double l = a.k_lat[x];
       lat = __dadd_rn(lat, l);
-      occw = __dadd_rn(occw, __dmul_rn(a.k_occ[x], l));
+      occw = __dadd_rn(occw, __dmul_rn(a.k_occ ? a.k_occ[x] : 0.0, l));
       f += a.k_flops[x];
-      rd += a.k_read[x];
-      wr += a.k_write[x];
+      if (a.k_read) rd += a.k_read[x];
+      if (a.k_write) wr += a.k_write[x];
     }
     T.lat[s] = lat;
     T.occw[s] = occw;
@@ -1054,6 +1068,107 @@ __global__ void __launch_bounds__(32) k_names_big(NameBigArgs a) {
     a.s_bound[o] = ro.bound;
   }
   if (lane == 0) a.g_count[g] = nu;
+}
+
+// a5 / a6 / a7: one CTA per group. The group's canonical layers (at most
+// kTypesCap) are staged in shared memory with their type slot (type_id mod 128;
+// two types on one slot set *over and the 128-wide a10 machinery redoes the
+// pass); then one thread per used slot walks the staged layers in order, so
+// every type's fp64 latency sum runs in layer order (analysis.cpp:315-337).
+// Long groups (layer chunks) are left to the chunked path.
+constexpr uint32_t kTypesCap = 2048;
+constexpr int kTypesThreads = 128;
+
+__global__ void __launch_bounds__(kTypesThreads) k_types(uint32_t G, const uint32_t* __restrict__ gl_off,
+                                                         const int32_t* __restrict__ gstatus,
+                                                         const uint32_t* __restrict__ big,
+                                                         const uint32_t* __restrict__ l_type,
+                                                         const double* __restrict__ l_lat,
+                                                         const uint64_t* __restrict__ l_alloc,
+                                                         uint32_t* __restrict__ g_count, uint32_t* __restrict__ over,
+                                                         uint32_t* __restrict__ s_key, uint64_t* __restrict__ s_count,
+                                                         double* __restrict__ s_lat, uint64_t* __restrict__ s_sum) {
+  __shared__ uint32_t key[NCAP];
+  __shared__ double y_lat[NCAP];
+  __shared__ uint8_t slot_of[kTypesCap];
+  __shared__ double lat[kTypesCap];
+  __shared__ uint64_t alloc[kTypesCap];
+  __shared__ int s_bad;
+  const uint32_t g = blockIdx.x, tid = threadIdx.x;
+  if (g >= G) return;
+  if (big && big[g + 1] > big[g]) return;  // long group: chunked path
+  if (gstatus[g] != XSP_G_OK) {
+    if (tid == 0) g_count[g] = 0;
+    return;
+  }
+  const uint32_t l0 = gl_off[g], n = gl_off[g + 1] - l0;
+  if (n > kTypesCap) {
+    if (tid == 0) atomicOr(over, 1u);
+    return;
+  }
+  for (uint32_t q = tid; q < NCAP; q += kTypesThreads) key[q] = NEMPTY;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (uint32_t i = tid; i < n; i += kTypesThreads) {
+    const uint32_t t = l_type[l0 + i];
+    const uint32_t sl = t & (NCAP - 1);
+    const uint32_t old = atomicCAS(&key[sl], NEMPTY, t);
+    if (old != NEMPTY && old != t) s_bad = 1;
+    slot_of[i] = (uint8_t)sl;
+    lat[i] = l_lat[l0 + i];
+    alloc[i] = l_alloc[l0 + i];
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) atomicOr(over, 1u);
+    return;
+  }
+  const uint32_t mykey = key[tid];
+  double acc = 0.0;
+  uint64_t cnt = 0, sum = 0;
+  if (mykey != NEMPTY) {
+    for (uint32_t i = 0; i < n; ++i)
+      if (slot_of[i] == tid) {
+        acc = __dadd_rn(acc, lat[i]);
+        ++cnt;
+        sum += alloc[i];
+      }
+  }
+  y_lat[tid] = acc;
+  const uint32_t nused = __syncthreads_count(mykey != NEMPTY);
+  if (mykey != NEMPTY) {
+    uint32_t rank = 0;
+    for (uint32_t q = 0; q < NCAP; ++q) {
+      const uint32_t kq = key[q];
+      if (kq == NEMPTY) continue;
+      const double lq = y_lat[q];
+      rank += (lq > acc) || (lq == acc && kq < mykey);
+    }
+    const uint64_t o = (uint64_t)g * NCAP + rank;
+    s_key[o] = mykey;
+    s_count[o] = cnt;
+    s_lat[o] = acc;
+    s_sum[o] = sum;
+  }
+  if (tid == 0) g_count[g] = nused;
+}
+
+// a5 rows: type, count, total latency, total alloc_bytes of the staged rows
+__global__ void k_types_place(uint32_t G, const uint32_t* __restrict__ off, const uint32_t* __restrict__ s_key,
+                              const uint64_t* __restrict__ s_count, const double* __restrict__ s_lat,
+                              const uint64_t* __restrict__ s_sum, uint32_t* __restrict__ y_type,
+                              uint64_t* __restrict__ y_count, double* __restrict__ y_lat,
+                              int64_t* __restrict__ y_alloc) {
+  const uint32_t g = blockIdx.x;
+  if (g >= G) return;
+  const uint32_t b = off[g], n = off[g + 1] - b;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t s = (uint64_t)g * NCAP + i;
+    y_type[b + i] = s_key[s];
+    y_count[b + i] = s_count[s];
+    y_lat[b + i] = s_lat[s];
+    y_alloc[b + i] = (int64_t)s_sum[s];
+  }
 }
 
 // every a10 column of the staged rows in one launch
@@ -1260,7 +1375,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->group_layer_off = ctx->d<uint32_t>("t.g_loff", G + 1);
   out->group_kernel_off = ctx->d<uint32_t>("t.g_koff", G + 1);
   uint32_t* scan_tmp = ctx->d<uint32_t>("a.scan", scan_scratch_elems(G + 16));
-  uint32_t* htot = ctx->h<uint32_t>("a.tot_h", 4);
+  uint32_t* htot = ctx->h<uint32_t>("a.tot_h", 8);
   uint32_t* hgl = ctx->h<uint32_t>("a.gl_h", G + 1);
   uint32_t* hgk = ctx->h<uint32_t>("a.gk_h", G + 1);
   if (ctx->hc_layer_key == corr->trace_layer_off && ctx->hc_kernel_key == corr->trace_kernel_off &&
@@ -1319,8 +1434,10 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   glc[G] = nkc + nlc;
   const uint32_t n_chunks = nkc + nlc;
   uint32_t *d_desc = nullptr, *d_gkc = nullptr, *d_glc = nullptr, *d_kcb = nullptr, *d_kce = nullptr;
+  uint32_t *d_lcb = nullptr, *d_lce = nullptr, *d_glc_rel = nullptr;
   if (n_chunks) {
-    uint32_t* hd = ctx->h<uint32_t>("a.big_h", desc.size() + 2ull * (G + 1) + 2ull * nkc);
+    const size_t words = desc.size() + 3ull * (G + 1) + 2ull * nkc + 2ull * nlc;
+    uint32_t* hd = ctx->h<uint32_t>("a.big_h", words);
     std::memcpy(hd, desc.data(), desc.size() * 4);
     std::memcpy(hd + desc.size(), gkc.data(), (G + 1) * 4ull);
     std::memcpy(hd + desc.size() + G + 1, glc.data(), (G + 1) * 4ull);
@@ -1329,7 +1446,13 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       kcb[c] = desc[3 * c];
       kcb[nkc + c] = desc[3 * c + 1];
     }
-    const size_t words = desc.size() + 2ull * (G + 1) + 2ull * nkc;
+    uint32_t* lcb = kcb + 2ull * nkc;  // layer chunks (a5 of long groups)
+    for (uint32_t c = 0; c < nlc; ++c) {
+      lcb[c] = desc[3 * (nkc + c)];
+      lcb[nlc + c] = desc[3 * (nkc + c) + 1];
+    }
+    uint32_t* grel = lcb + 2ull * nlc;
+    for (uint32_t g = 0; g <= G; ++g) grel[g] = glc[g] - nkc;
     uint32_t* dd = ctx->d<uint32_t>("a.big", words);
     XSP_CUDA(cudaMemcpyAsync(dd, hd, words * 4, cudaMemcpyHostToDevice, st));
     d_desc = dd;
@@ -1337,6 +1460,9 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     d_glc = d_gkc + G + 1;
     d_kcb = d_glc + G + 1;
     d_kce = d_kcb + nkc;
+    d_lcb = d_kce + nkc;
+    d_lce = d_lcb + nlc;
+    d_glc_rel = d_lce + nlc;
   }
   launch(ctx, k_group_check_runs, total_runs, st, ga, total_runs, run_off);
   launch(ctx, k_group_check_layers, TL, st, ga, TL, out->group_layer_off);
@@ -1359,6 +1485,11 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   la.t_kernel_off = corr->trace_kernel_off;
   la.l_koff = corr->layer_kernel_off;
   la.layer_dur = corr->layer_dur;
+  la.layer_attr_row = corr->layer_attr_row;
+  la.type_id = c->type_id;
+  la.alloc_bytes = c->alloc_bytes;
+  la.l_type = ctx->d<uint32_t>("a.l_type", TL);
+  la.l_alloc = ctx->d<uint64_t>("a.l_alloc", TL);
   la.layer_row = corr->layer_row;
   la.kernel_dur = corr->kernel_dur;
   la.kernel_mrow = corr->kernel_metric_row;
@@ -1474,6 +1605,141 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   }
   ctx->stage_end("models", st);
 
+  // ---- a5 / a6 / a7 by layer type: the a10 machinery keyed by the canonical
+  // layers' type ids (values: layer latency, alloc_bytes), launched before the
+  // a10 read-back so both totals come back with one sync
+  out->group_type_off = ctx->d<uint32_t>("t.g_yoff", G + 1);
+  bool types_wide = false;
+  std::function<void()> run_types;
+  run_types = [&]() {
+    if (!G) {
+      htot[4] = htot[5] = 0;
+      return;
+    }
+    NameFastArgs ty;
+    std::memset(&ty, 0, sizeof(ty));
+    ty.G = G;
+    ty.gk_off = out->group_layer_off;
+    ty.gk_end = nullptr;
+    ty.big = d_glc_rel;
+    ty.raw = 0;
+    ty.gstatus = out->group_status;
+    ty.k_name = la.l_type;
+    ty.k_lat = la.l_layer_lat;
+    ty.k_occ = nullptr;
+    ty.k_flops = la.l_alloc;
+    ty.k_read = ty.k_write = nullptr;
+    ty.m_lat = ma.m_lat;
+    ty.peak = la.peak;
+    ty.bw = la.bw;
+    ty.g_count = ctx->d<uint32_t>("a.y_gcount", G + 1);
+    ty.overflow = ctx->d<uint32_t>("a.y_over", 1);
+    ty.ks_slot = ctx->d<uint32_t>("a.y_ks_slot", TL + 1);
+    ty.ks_rank = ctx->d<uint32_t>("a.y_ks_rank", TL + 1);
+    ty.perm = ctx->d<uint32_t>("a.y_perm", TL + 1);
+    const uint64_t cap = (uint64_t)G * NCAP;
+    ty.s_name = ctx->d<uint32_t>("a.y_s_key", cap);
+    ty.s_count = ctx->d<uint64_t>("a.y_s_count", cap);
+    ty.s_lat = ctx->d<double>("a.y_s_lat", cap);
+    ty.s_pct = ctx->d<double>("a.y_s_pct", cap);
+    ty.s_flops = ctx->d<uint64_t>("a.y_s_sum", cap);
+    ty.s_read = ctx->d<uint64_t>("a.y_s_r", cap);
+    ty.s_write = ctx->d<uint64_t>("a.y_s_w", cap);
+    ty.s_occ = ctx->d<double>("a.y_s_occ", cap);
+    ty.s_ai = ctx->d<double>("a.y_s_ai", cap);
+    ty.s_tput = ctx->d<double>("a.y_s_tput", cap);
+    ty.s_bound = ctx->d<int8_t>("a.y_s_bound", cap);
+    XSP_CUDA(cudaMemsetAsync(ty.overflow, 0, 4, st));
+    if (!types_wide) {
+      k_types<<<G, kTypesThreads, 0, st>>>(G, out->group_layer_off, out->group_status, d_glc_rel,
+                                                            la.l_type, la.l_layer_lat, la.l_alloc, ty.g_count,
+                                                            ty.overflow, ty.s_name, ty.s_count, ty.s_lat,
+                                                            ty.s_flops);
+    } else {  // a type-slot collision or a group above kTypesCap: the a10 machinery
+      XSP_CUDA(cudaFuncSetAttribute(k_names_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNameSmem));
+      k_names_fast<<<G, NAME_WARPS * 32, kNameSmem, st>>>(ty);
+    }
+    ++ctx->launches;
+    if (nlc) {
+      NameFastArgs tc = ty;
+      tc.G = nlc;
+      tc.gk_off = d_lcb;
+      tc.gk_end = d_lce;
+      tc.big = nullptr;
+      tc.gstatus = nullptr;
+      tc.raw = 1;
+      const uint64_t ccap = (uint64_t)nlc * NCAP;
+      tc.g_count = ctx->d<uint32_t>("a.yc_count", nlc);
+      tc.s_name = ctx->d<uint32_t>("a.yc_key", ccap);
+      tc.s_count = ctx->d<uint64_t>("a.yc_cnt", ccap);
+      tc.s_lat = ctx->d<double>("a.yc_lat", ccap);
+      tc.s_occ = ctx->d<double>("a.yc_occw", ccap);
+      tc.s_flops = ctx->d<uint64_t>("a.yc_sum", ccap);
+      tc.s_read = ctx->d<uint64_t>("a.yc_r", ccap);
+      tc.s_write = ctx->d<uint64_t>("a.yc_w", ccap);
+      k_names_fast<<<nlc, NAME_WARPS * 32, kNameSmem, st>>>(tc);
+      NameBigArgs yb;
+      yb.G = G;
+      yb.gkc_off = d_glc_rel;
+      yb.gstatus = out->group_status;
+      yb.c_count = tc.g_count;
+      yb.c_name = tc.s_name;
+      yb.c_cnt = tc.s_count;
+      yb.c_lat = tc.s_lat;
+      yb.c_occw = tc.s_occ;
+      yb.c_f = tc.s_flops;
+      yb.c_r = tc.s_read;
+      yb.c_w = tc.s_write;
+      yb.m_lat = ma.m_lat;
+      yb.peak = la.peak;
+      yb.bw = la.bw;
+      yb.g_count = ty.g_count;
+      yb.overflow = ty.overflow;
+      yb.s_name = ty.s_name;
+      yb.s_count = ty.s_count;
+      yb.s_lat = ty.s_lat;
+      yb.s_pct = ty.s_pct;
+      yb.s_flops = ty.s_flops;
+      yb.s_read = ty.s_read;
+      yb.s_write = ty.s_write;
+      yb.s_occ = ty.s_occ;
+      yb.s_ai = ty.s_ai;
+      yb.s_tput = ty.s_tput;
+      yb.s_bound = ty.s_bound;
+      k_names_big<<<G, 32, 0, st>>>(yb);
+      ctx->launches += 2;
+    }
+    exclusive_scan<uint32_t, uint32_t>(ty.g_count, out->group_type_off, G, scan_tmp, out->group_type_off + G, st,
+                                       &ctx->launches);
+    xfer_small(htot + 4, out->group_type_off + G, 4, st);
+    xfer_small(htot + 5, ty.overflow, 4, st);
+    return;
+  };
+  auto place_types = [&]() {
+    if (htot[5] && !types_wide) {  // more than 32 types somewhere: redo with 128-wide tables
+      types_wide = true;
+      run_types();
+      XSP_CUDA(cudaStreamSynchronize(st));
+    }
+    if (htot[5]) throw std::invalid_argument("a5: more than 128 distinct layer types in one analysis group");
+    const uint32_t NY = G ? htot[4] : 0;
+    out->n_type_rows = NY;
+    out->y_type = ctx->d<uint32_t>("t.y_type", NY);
+    out->y_count = ctx->d<uint64_t>("t.y_count", NY);
+    out->y_lat = ctx->d<double>("t.y_lat", NY);
+    out->y_alloc = ctx->d<int64_t>("t.y_alloc", NY);
+    if (!G) {
+      XSP_CUDA(cudaMemsetAsync(out->group_type_off, 0, 4, st));
+      return;
+    }
+    k_types_place<<<G, 128, 0, st>>>(G, out->group_type_off, ctx->d<uint32_t>("a.y_s_key", 1),
+                                     ctx->d<uint64_t>("a.y_s_count", 1), ctx->d<double>("a.y_s_lat", 1),
+                                     ctx->d<uint64_t>("a.y_s_sum", 1), out->y_type, out->y_count, out->y_lat,
+                                     out->y_alloc);
+    ++ctx->launches;
+  };
+  bool types_done = false;
+
   // ---- a10
   out->group_name_off = ctx->d<uint32_t>("t.g_noff", G + 1);
   uint32_t NN = 0;
@@ -1571,7 +1837,10 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
                                        &ctx->launches);
     xfer_small(htot + 2, out->group_name_off + G, 4, st);
     xfer_small(htot + 3, nf.overflow, 4, st);
+    run_types();
+    types_done = true;
     XSP_CUDA(cudaStreamSynchronize(st));
+    place_types();
     if (!htot[3]) {
       NN = htot[2];
       out->n_name = ctx->d<uint32_t>("t.n_name", NN);
@@ -1686,6 +1955,11 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     out->n_bound = ctx->d<int8_t>("t.n_bound", 1);
   }
   out->n_names = NN;
+  if (!types_done) {
+    run_types();
+    XSP_CUDA(cudaStreamSynchronize(st));
+    place_types();
+  }
 }
 
 }  // namespace xsp

@@ -123,6 +123,7 @@ xsp_corr_out upload_corr(xsp_ctx* ctx, const xsp_corr_out* h, cudaStream_t st) {
   d.layer_row = to_dev(ctx, "c.l_row", h->layer_row, L, st);
   d.layer_kernel_off = to_dev(ctx, "c.l_koff", h->layer_kernel_off, L + 1, st);
   d.layer_dur = to_dev(ctx, "c.l_dur", h->layer_dur, L, st);
+  d.layer_attr_row = h->layer_attr_row ? to_dev(ctx, "c.l_attr", h->layer_attr_row, L, st) : nullptr;
   d.kernel_metric_row = to_dev(ctx, "c.k_mrow", h->kernel_metric_row, K, st);
   d.kernel_dur = to_dev(ctx, "c.k_dur", h->kernel_dur, K, st);
   d.kernel_name = to_dev(ctx, "c.k_name", h->kernel_name, K, st);
@@ -182,6 +183,9 @@ void download_tables(xsp_ctx* ctx, const xsp_tables_out& dtab, const xsp_analysi
   BACK(m_lat, G); BACK(m_kern_lat, G); BACK(m_flops, G); BACK(m_read, G); BACK(m_write, G);
   BACK(m_occ, G); BACK(m_count, G); BACK(m_ai, G); BACK(m_tput, G); BACK(m_bound, G);
   BACK(m_gpu, G); BACK(m_gpu_pct, G); BACK(m_throughput, G); BACK(m_roofline_in, G);
+  const uint64_t Y = dtab.n_type_rows;
+  BACK(group_type_off, G + 1ull);
+  BACK(y_type, Y); BACK(y_count, Y); BACK(y_lat, Y); BACK(y_alloc, Y);
 #undef BACK
 }
 

@@ -32,8 +32,8 @@ __global__ void k_rebase(uint32_t* __restrict__ p, uint64_t n, uint32_t base) {
 }
 
 // what a column counts / what its values index
-enum Count : uint8_t { N_T, N_2T, N_L, N_K, N_O, N_A, N_AC, N_G, N_TL, N_TK, N_TN, N_TLK };
-enum Base : uint8_t { B_NONE, B_SPAN, B_METRIC, B_LAYER, B_L, B_K, B_O, B_A, B_AC, B_TL, B_TK, B_TN };
+enum Count : uint8_t { N_T, N_2T, N_L, N_K, N_O, N_A, N_AC, N_G, N_TL, N_TK, N_TN, N_TLK, N_TY, N_COUNTS };
+enum Base : uint8_t { B_NONE, B_SPAN, B_METRIC, B_LAYER, B_L, B_K, B_O, B_A, B_AC, B_TL, B_TK, B_TN, B_TY, B_BASES };
 
 struct Field {
   size_t off;   // offsetof the pointer member
@@ -82,6 +82,8 @@ const Field kTableFields[] = {
     TF(m_write, uint64_t, N_G), TF(m_occ, double, N_G), TF(m_count, uint64_t, N_G), TF(m_ai, double, N_G),
     TF(m_tput, double, N_G), TF(m_bound, int8_t, N_G), TF(m_gpu, double, N_G), TF(m_gpu_pct, double, N_G),
     TF(m_throughput, double, N_G), TF(m_roofline_in, uint8_t, N_G),
+    TFB(group_type_off, uint32_t, N_G, true, B_TY),
+    TF(y_type, uint32_t, N_TY), TF(y_count, uint64_t, N_TY), TF(y_lat, double, N_TY), TF(y_alloc, int64_t, N_TY),
 };
 #undef TF
 #undef TFB
@@ -95,9 +97,9 @@ struct Chunk {
 
 // Per-chunk counts and global write positions, indexed by Count / Base.
 struct Pos {
-  uint64_t n[12] = {};    // element counts of this chunk
-  uint64_t at[12] = {};   // global element position of its first element
-  uint64_t base[12] = {}; // value to add (Base)
+  uint64_t n[N_COUNTS] = {};   // element counts of this chunk
+  uint64_t at[N_COUNTS] = {};  // global element position of its first element
+  uint64_t base[B_BASES] = {}; // value to add (Base)
 };
 
 __attribute__((target("popcnt"))) void count_rows(const uint8_t* f, uint64_t n, uint64_t& metric, uint64_t& layer) {
@@ -301,7 +303,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
   };
 
   // ---- outputs: totals so far, per Count kind
-  uint64_t tot[12] = {};
+  uint64_t tot[N_COUNTS] = {};
   std::memset(corr_host, 0, sizeof(*corr_host));
   std::memset(tab_host, 0, sizeof(*tab_host));
   const uint64_t tk = opts->top_k ? opts->top_k : 1;
@@ -384,7 +386,8 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     P.n[N_TK] = dtab.n_kernels;
     P.n[N_TN] = dtab.n_names;
     P.n[N_TLK] = dtab.n_layers * tk;
-    for (int k = 0; k < 12; ++k) P.at[k] = tot[k];
+    P.n[N_TY] = dtab.n_type_rows;
+    for (int k = 0; k < N_COUNTS; ++k) P.at[k] = tot[k];
     P.base[B_SPAN] = C.s0;
     P.base[B_METRIC] = C.m0;
     P.base[B_LAYER] = C.l0;
@@ -396,10 +399,11 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     P.base[B_TL] = tot[N_TL];
     P.base[B_TK] = tot[N_TK];
     P.base[B_TN] = tot[N_TN];
+    P.base[B_TY] = tot[N_TY];
     d2h_fields(kCorrFields, sizeof(kCorrFields) / sizeof(Field), &dcorr, corr_host, P, last);
     d2h_fields(kTableFields, sizeof(kTableFields) / sizeof(Field), &dtab, tab_host, P, last);
     XSP_CUDA(cudaEventRecord(S.out_done, os));
-    for (int k = 0; k < 12; ++k) tot[k] += P.n[k];
+    for (int k = 0; k < N_COUNTS; ++k) tot[k] += P.n[k];
     corr_host->n_failed += dcorr.n_failed;
     if (trace)
       std::fprintf(stderr, "chunk %zu spans %lu: stage %.2f  correlate-done %.2f  analyze-done %.2f  d2h-issued %.2f ms\n",
@@ -419,6 +423,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
   tab_host->n_layers = tot[N_TL];
   tab_host->n_kernels = tot[N_TK];
   tab_host->n_names = tot[N_TN];
+  tab_host->n_type_rows = tot[N_TY];
   return true;
 }
 

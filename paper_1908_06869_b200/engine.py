@@ -110,7 +110,7 @@ def _corr_counts(o: capi.CorrOut) -> Dict[str, int]:
 def _tab_counts(o: capi.TablesOut, top_k: int) -> Dict[str, int]:
     G = o.n_groups
     return {"G": G, "G1": G + 1, "K": o.n_kernels, "L": o.n_layers, "N": o.n_names,
-            "LK": o.n_layers * max(top_k, 1)}
+            "LK": o.n_layers * max(top_k, 1), "Y": o.n_type_rows}
 
 
 class DeviceBatch:

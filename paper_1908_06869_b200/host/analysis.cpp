@@ -79,6 +79,11 @@ struct Tables {
   std::vector<std::uint64_t> m_flops, m_read, m_write, m_count;
   std::vector<std::int8_t> m_bound;
   std::vector<std::uint8_t> m_in;
+  std::vector<std::string> types;
+  std::vector<std::uint32_t> yoff, y_type;
+  std::vector<std::uint64_t> y_count;
+  std::vector<double> y_lat;
+  std::vector<std::int64_t> y_alloc;
 
   // AnalysisError of group g, as combine() / trimmed_mean raise it
   void check(std::size_t g) const {
@@ -181,6 +186,13 @@ Tables run_tables(const std::vector<const AnalysisInput*>& groups, const SystemS
   r.m_count = take(t.m_count, G);
   r.m_bound = take(t.m_bound, G);
   r.m_in = take(t.m_roofline_in, G);
+  const std::size_t Y = t.n_type_rows;
+  r.types = p.types.sorted;
+  r.yoff = take(t.group_type_off, G + 1);
+  r.y_type = take(t.y_type, Y);
+  r.y_count = take(t.y_count, Y);
+  r.y_lat = take(t.y_lat, Y);
+  r.y_alloc = take(t.y_alloc, Y);
   return r;
 }
 
@@ -271,23 +283,19 @@ LayerSeries a3_a4_layer_series(const AnalysisInput& input, const AnalysisOptions
   return s;
 }
 
+// a5 / a6 / a7 rows come from the GPU (k_names_fast keyed by layer type, in
+// layer order; rows by total latency desc, type asc — analysis.cpp:315-337).
 LayerTypeTable a5_a6_a7_by_type(const AnalysisInput& input, const AnalysisOptions& options) {
   const Tables t = one(input, kNoSpec, options);
-  std::map<std::string, LayerTypeRow> by;
-  const auto& layers = input.runs.front().root.layers;
-  for (std::size_t i = 0; i < layers.size(); ++i) {
-    LayerTypeRow& r = by[layers[i].layer_type];
-    r.type = layers[i].layer_type;
-    r.count += 1;
-    r.total_latency_ns += t.l_layer_lat[i];
-    r.total_alloc_bytes += layers[i].alloc_bytes;
-  }
   LayerTypeTable table;
-  for (auto& kv : by) table.rows.push_back(std::move(kv.second));
-  std::stable_sort(table.rows.begin(), table.rows.end(), [](const LayerTypeRow& a, const LayerTypeRow& b) {
-    if (a.total_latency_ns != b.total_latency_ns) return a.total_latency_ns > b.total_latency_ns;
-    return a.type < b.type;
-  });
+  for (std::uint32_t j = t.yoff[0]; j < t.yoff[1]; ++j) {
+    LayerTypeRow r;
+    r.type = t.types[t.y_type[j]];
+    r.count = t.y_count[j];
+    r.total_latency_ns = t.y_lat[j];
+    r.total_alloc_bytes = t.y_alloc[j];
+    table.rows.push_back(std::move(r));
+  }
   return table;
 }
 

@@ -278,9 +278,9 @@ xsp_span_cols PackedTrees::cols() const {
   c.dram_read = ptr(dram_read);
   c.dram_write = ptr(dram_write);
   c.occupancy = ptr(occupancy);
-  c.n_layer_rows = 0;
-  c.alloc_bytes = nullptr;
-  c.type_id = nullptr;
+  c.n_layer_rows = alloc_bytes.size();
+  c.alloc_bytes = ptr(alloc_bytes);
+  c.type_id = ptr(type_id);
   return c;
 }
 
@@ -298,6 +298,7 @@ xsp_corr_out PackedTrees::corr() const {
   o.layer_row = ptr(layer_row);
   o.layer_kernel_off = ptr(layer_kernel_off);
   o.layer_dur = ptr(layer_dur);
+  o.layer_attr_row = ptr(layer_attr_row);
   o.kernel_metric_row = ptr(kernel_mrow);
   o.kernel_dur = ptr(kernel_dur);
   o.kernel_name = ptr(kernel_name);
@@ -311,10 +312,12 @@ PackedTrees pack_trees(const std::vector<const EntityTree*>& trees) {
     p.names.add(t->root.span.name);
     for (const LayerExec& L : t->root.layers) {
       p.names.add(L.span.name);
+      p.types.add(L.layer_type);
       for (const KernelExec& K : L.kernels) p.names.add(K.kernel_name());
     }
   }
   p.names.finish();
+  p.types.finish();
   p.t_layer_off.push_back(0);
   p.t_kernel_off.push_back(0);
   p.t_amb_off.push_back(0);
@@ -333,6 +336,9 @@ PackedTrees pack_trees(const std::vector<const EntityTree*>& trees) {
     for (const LayerExec& L : t->root.layers) {
       p.layer_row.push_back(add_span(L.span, Level::Layer));
       p.layer_dur.push_back(L.duration_ns());
+      p.layer_attr_row.push_back(static_cast<std::uint32_t>(p.alloc_bytes.size()));
+      p.alloc_bytes.push_back(L.alloc_bytes);
+      p.type_id.push_back(p.types.id.at(L.layer_type));
       for (const KernelExec& K : L.kernels) {
         p.kernel_dur.push_back(K.duration_ns());
         p.kernel_name.push_back(p.names.id.at(K.kernel_name()));

@@ -96,7 +96,10 @@ struct PackedTrees {
   std::vector<std::uint64_t> layer_dur, kernel_dur;
   std::vector<std::uint32_t> kernel_mrow, kernel_name;
   std::vector<double> kernel_occ;
-  Strings names;
+  // layer table (a5-a7): one row per layer, in layer order
+  std::vector<std::uint32_t> layer_attr_row, type_id;
+  std::vector<std::int64_t> alloc_bytes;
+  Strings names, types;
 
   xsp_span_cols cols() const;
   xsp_corr_out corr() const;

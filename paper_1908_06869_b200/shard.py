@@ -88,10 +88,12 @@ def combine(parts: List[Tuple[Tables, np.ndarray]], n_groups: int, top_k: int) -
     if (owner < 0).any():
         raise ValueError(f"combine: groups {np.nonzero(owner < 0)[0][:8].tolist()} missing")
     kinds = {n: k for n, _, k in capi.TABLE_FIELDS}
-    csr = {"K": "group_kernel_off", "L": "group_layer_off", "N": "group_name_off", "LK": "group_layer_off"}
+    csr = {"K": "group_kernel_off", "L": "group_layer_off", "N": "group_name_off", "LK": "group_layer_off",
+           "Y": "group_type_off"}
+    offsets = ("group_kernel_off", "group_layer_off", "group_name_off", "group_type_off")
     cols = {}
     for name, kind in kinds.items():
-        if name in ("group_kernel_off", "group_layer_off", "group_name_off"):
+        if name in offsets:
             continue
         if kind == "G":
             proto = parts[0][0].cols[name]
@@ -109,7 +111,7 @@ def combine(parts: List[Tuple[Tables, np.ndarray]], n_groups: int, top_k: int) -
             i = local[g]
             blocks.append(tabs.cols[name][int(o[i]) * mult:int(o[i + 1]) * mult])
         cols[name] = np.concatenate(blocks) if blocks else parts[0][0].cols[name][:0]
-    for offn in ("group_kernel_off", "group_layer_off", "group_name_off"):
+    for offn in offsets:
         sizes = np.zeros(n_groups, np.int64)
         for tabs, gids in parts:
             o = tabs.cols[offn].astype(np.int64)

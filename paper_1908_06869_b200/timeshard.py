@@ -300,6 +300,25 @@ def combine(b: SpanBatch, parts: Sequence[dict], top_k: int = 3) -> Tuple[CorrRe
                "n_flops": nf, "n_read": nr, "n_write": nw, "n_occ": nocc, "n_ai": ai, "n_tput": tput,
                "n_bound": bound})
     tc["group_name_off"] = u32([0, ids.size])
+    # a5 / a6 / a7: per-type sums across shards (integer latencies of one run:
+    # exact), then total latency desc, type asc
+    if "y_type" in t0.cols:
+        ytab: dict = {}
+        for t in tabs_parts:
+            for j in range(t.cols["y_type"].size):
+                e = ytab.setdefault(int(t.cols["y_type"][j]), [0, 0.0, 0])
+                e[0] += int(t.cols["y_count"][j])
+                e[1] += float(t.cols["y_lat"][j])
+                e[2] += int(t.cols["y_alloc"][j])
+        yid = np.array(sorted(ytab), np.uint32)
+        ylat = np.array([ytab[i][1] for i in yid.tolist()])
+        yo = np.lexsort((yid, -ylat))
+        yid, ylat = yid[yo], ylat[yo]
+        tc["y_type"] = yid
+        tc["y_count"] = np.array([ytab[i][0] for i in yid.tolist()], np.uint64)
+        tc["y_lat"] = ylat
+        tc["y_alloc"] = np.array([ytab[i][2] for i in yid.tolist()], np.int64)
+        tc["group_type_off"] = u32([0, yid.size])
     for name, _, _ in capi.TABLE_FIELDS:  # dtype parity with the engine's columns
         if name in tc and name in t0.cols:
             tc[name] = tc[name].astype(t0.cols[name].dtype)

@@ -144,6 +144,17 @@ def compare_tables(batch, tabs, ref_arrays, ref_strings, rtol=0.0):
             _eq(tabs.cols[gf][g:g + 1], ra[rf][g:g + 1], f"group {g} {rf}", rtol)
         _eq(_bound(tabs.m_bound[g:g + 1]), _bound(ra["m_bound"][g:g + 1]), f"group {g} m_bound")
         _eq(tabs.m_roofline_in[g:g + 1], ra["mr_in"][g:g + 1], f"group {g} model_roofline")
+        # a5 / a6 / a7 by layer type (analysis.cpp:315-337)
+        if "g_type_off" in ra and "group_type_off" in tabs.cols:
+            ry = ra["g_type_off"]
+            y0, y1 = int(tabs.group_type_off[g]), int(tabs.group_type_off[g + 1])
+            assert y1 - y0 == int(ry[g + 1] - ry[g]), f"group {g}: a5 rows"
+            types = [batch.types[int(t)].decode() for t in tabs.y_type[y0:y1]]
+            want = [x.decode() for x in ref_strings["y_type"][int(ry[g]):int(ry[g + 1])]]
+            assert types == want, f"group {g} a5 types {types[:4]} != {want[:4]}"
+            _eq(tabs.y_count[y0:y1], ra["y_count"][ry[g]:ry[g + 1]], f"group {g} a5 count")
+            _eq(tabs.y_lat[y0:y1], ra["y_lat"][ry[g]:ry[g + 1]], f"group {g} a5 latency", rtol)
+            _eq(tabs.y_alloc[y0:y1], ra["y_alloc"][ry[g]:ry[g + 1]], f"group {g} a7 alloc")
 
 
 def topk_oracle(k_lat: np.ndarray, k_layer: np.ndarray, k: int) -> np.ndarray:
