@@ -12,6 +12,7 @@
  *   TraceBundle / Span (span.hpp:81-171)        xsp_span_cols + trace offsets
  *   correlate()   (correlator.hpp:164)          xsp_correlate
  *   assign_parents + correlate_async (:154,161) (both inside xsp_correlate)
+ *   resolve_with_serialized (correlator.hpp:176) xsp_resolve_serialized
  *   a5..a15, model_roofline (analysis.hpp:128-366) xsp_analyze
  *   LeveledRunGroup + compute_overhead (leveled.hpp:60-109) xsp_leveled
  *   validate_bundle (span.hpp:187)              xsp_validate / xsp_validate_host
@@ -114,7 +115,11 @@ typedef enum xsp_trace_status {
   XSP_T_MULTI_MODEL = 2,     /* "bundle has more than one model span"                   (:147-150) */
   XSP_T_SKIP_LEVEL = 3,      /* "span <id> ('<name>') is kernel-level but ..."  row a   (:151-157) */
   XSP_T_DUP_EXEC_CID = 4,    /* "correlation id C is shared by execution spans A and B" (:296-302) */
-  XSP_T_DUP_LAUNCH_CID = 5   /* "... is shared by launch spans A and B"                 (:308-316) */
+  XSP_T_DUP_LAUNCH_CID = 5,  /* "... is shared by launch spans A and B"                 (:308-316) */
+  /* xsp_resolve_serialized only (correlator.cpp:381-386): */
+  XSP_T_SER_AMBIGUOUS = 6,   /* "serialized run is itself ambiguous (N span(s)); cannot resolve"; err_row[2t] = N */
+  XSP_T_SER_FAILED = 7       /* assign_parents(serialized) failed; err_row = the serialized trace's err rows
+                                (rows of the SERIALIZED batch) and that trace's status says which fault */
 } xsp_trace_status_code;
 
 /* Orphan reasons (OrphanSpan::reason text, correlator.cpp:168-363). */
@@ -348,6 +353,21 @@ int xsp_abi_version(void);
 #define XSP_CORR_PARENTS_ONLY 2
 xsp_status xsp_correlate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces, int mode,
                          xsp_corr_out* out, void* stream);
+
+/* resolve_with_serialized (correlator.cpp:379-456) for every trace pair: trace t
+ * of `original` (a concurrent run) is re-correlated with the parents its
+ * serialized twin (trace t of `serialized`) assigns to its ambiguous kernels,
+ * matched by (level, kind, name, occurrence in timeline order). Both batches
+ * must share one name table (equal name_id = equal name). The result is the
+ * correlate() of the patched original batch. DEVICE pointers; synchronous.
+ * A pair whose serialized trace is ambiguous or fails gets XSP_T_SER_*. */
+xsp_status xsp_resolve_serialized(xsp_ctx* ctx, const xsp_span_cols* original, const xsp_traces* original_traces,
+                                  const xsp_span_cols* serialized, const xsp_traces* serialized_traces,
+                                  xsp_corr_out* out, void* stream);
+/* Host-buffer form (results in ctx-owned pinned host memory, like xsp_correlate_host). */
+xsp_status xsp_resolve_serialized_host(xsp_ctx* ctx, const xsp_span_cols* original,
+                                       const xsp_traces* original_traces, const xsp_span_cols* serialized,
+                                       const xsp_traces* serialized_traces, xsp_corr_out* out);
 
 /* sort_timeline (span.cpp:112-127) for every trace, DEVICE pointers (perm is a
  * caller-owned device array of n_spans): as xsp_sort_timeline_host below.

@@ -79,6 +79,8 @@ def lib() -> C.CDLL:
         L.xspref_analyze.restype = P
         L.xspref_leveled.argtypes = [C.POINTER(SoaIn), C.c_double, C.c_double]
         L.xspref_validate.argtypes = [C.POINTER(SoaIn), C.c_void_p, C.c_void_p]
+        L.xspref_resolve.argtypes = [C.POINTER(SoaIn), C.POINTER(SoaIn)]
+        L.xspref_resolve.restype = P
         L.xspref_validate.restype = P
         L.xspref_leveled.restype = P
         L.xspref_time_pipeline.argtypes = [C.POINTER(SoaIn), P, P, C.c_uint32, C.c_int, C.c_int]
@@ -210,6 +212,13 @@ def analyze(b, first: Sequence[int], runs: Sequence[int], trim=0.2, noise=0.01):
     f = np.ascontiguousarray(first, dtype=np.uint32)
     r = np.ascontiguousarray(runs, dtype=np.uint32)
     return read_bag(lib().xspref_analyze(C.byref(s), f.ctypes.data, r.ctypes.data, f.size, trim, noise))
+
+
+def resolve(original, serialized):
+    """resolve_with_serialized per trace pair, as correlate() returns it."""
+    s1, k1 = soa_in(original)
+    s2, k2 = soa_in(serialized)
+    return read_bag(lib().xspref_resolve(C.byref(s1), C.byref(s2)))
 
 
 def validate(b, span_trace_id=None, tag_bits=None):

@@ -559,6 +559,27 @@ XSPREF_API void* xspref_validate(const SoaIn* in, const std::uint64_t* span_trac
   return bag;
 }
 
+/// resolve_with_serialized() (correlator.cpp:379-456) per trace pair: trace t of
+/// `in` against trace t of `ser`; TraceError -> status 1 + text.
+XSPREF_API void* xspref_resolve(const SoaIn* in, const SoaIn* ser) {
+  std::vector<TraceBundle> orig = import_soa(*in);
+  std::vector<TraceBundle> sers = import_soa(*ser);
+  std::vector<CorrelationResult> res(orig.size());
+  std::vector<CorrelationResult*> ptrs(orig.size(), nullptr);
+  std::vector<std::string> errs(orig.size());
+  for (std::size_t t = 0; t < orig.size(); ++t) {
+    try {
+      res[t] = resolve_with_serialized(orig[t], sers.at(t));
+      ptrs[t] = &res[t];
+    } catch (const TraceError& e) {
+      errs[t] = e.what();
+    }
+  }
+  auto* bag = new Bag;
+  export_correlation(orig, ptrs, errs, *bag);
+  return bag;
+}
+
 /// Wall-clock timing of the reference hot path (correlate + a8..a15) over a
 /// set of groups, `threads` workers with one group per task. Returns seconds.
 /// groups: [first_trace, n_runs] pairs.

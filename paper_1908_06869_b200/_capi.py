@@ -37,7 +37,7 @@ LEVEL_MODEL, LEVEL_LAYER, LEVEL_KERNEL, LEVEL_API = 0, 1, 2, 3
 KIND_SYNC, KIND_LAUNCH, KIND_EXEC = 0, 1, 2
 
 # per-trace status (xsp_trace_status)
-T_OK, T_NO_MODEL, T_MULTI_MODEL, T_SKIP_LEVEL, T_DUP_EXEC_CID, T_DUP_LAUNCH_CID = range(6)
+T_OK, T_NO_MODEL, T_MULTI_MODEL, T_SKIP_LEVEL, T_DUP_EXEC_CID, T_DUP_LAUNCH_CID, T_SER_AMBIGUOUS, T_SER_FAILED = range(8)
 # per-group status
 G_OK, G_NO_RUNS, G_LAYER_COUNT, G_KERNEL_COUNT, G_TRACE_FAILED, G_BAD_TRIM = range(6)
 
@@ -178,7 +178,8 @@ EXPORTS = [
     "xsp_analyze", "xsp_run_host", "xsp_last_transfer_bytes", "xsp_last_launch_count",
     "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host", "xsp_set_profiling", "xsp_stage_reset",
     "xsp_stage_times", "xsp_leveled", "xsp_sort_timeline_host", "xsp_correlate_host",
-    "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline",
+    "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline", "xsp_resolve_serialized",
+    "xsp_resolve_serialized_host",
 ]
 
 _lib = None
@@ -242,6 +243,9 @@ def load() -> C.CDLL:
     lib.xsp_validate.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(ValidateIn),
                                  C.POINTER(ValidationOut), P]
     lib.xsp_validate.restype = C.c_int32
+    lib.xsp_resolve_serialized_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(SpanCols),
+                                                C.POINTER(Traces), C.POINTER(CorrOut)]
+    lib.xsp_resolve_serialized_host.restype = C.c_int32
     lib.xsp_validate_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(ValidateIn),
                                       C.POINTER(ValidationOut)]
     lib.xsp_validate_host.restype = C.c_int32

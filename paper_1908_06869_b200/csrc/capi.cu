@@ -17,6 +17,8 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
                        uint32_t T, const uint64_t* off, uint32_t* perm, uint32_t* was_sorted, cudaStream_t st);
 void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, const xsp_validate_in* vin,
                   xsp_validation_out* out, cudaStream_t st);
+void run_resolve(xsp_ctx* ctx, const xsp_span_cols* oc, const xsp_traces* ot, const xsp_span_cols* sc,
+                 const xsp_traces* stt, xsp_corr_out* out, cudaStream_t st);
 }
 
 namespace {
@@ -308,6 +310,42 @@ XSP_API xsp_status xsp_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xs
       throw std::invalid_argument("null level-set column");
     std::memset(out, 0, sizeof(*out));
     xsp::run_leveled(ctx, cols, corr, sets, opts, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_resolve_serialized(xsp_ctx* ctx, const xsp_span_cols* oc, const xsp_traces* ot,
+                                          const xsp_span_cols* sc, const xsp_traces* stt, xsp_corr_out* out,
+                                          void* stream) {
+  return guard(ctx, "xsp_resolve_serialized", [&] {
+    check_cols(oc, ot);
+    check_cols(sc, stt);
+    if (!ot || !stt || !out) throw std::invalid_argument("null argument");
+    std::memset(out, 0, sizeof(*out));
+    xsp::run_resolve(ctx, oc, ot, sc, stt, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_resolve_serialized_host(xsp_ctx* ctx, const xsp_span_cols* hoc, const xsp_traces* hot,
+                                               const xsp_span_cols* hsc, const xsp_traces* hst,
+                                               xsp_corr_out* out) {
+  return guard(ctx, "xsp_resolve_serialized_host", [&] {
+    check_cols(hoc, hot);
+    check_cols(hsc, hst);
+    if (!hot || !hst || !out) throw std::invalid_argument("null argument");
+    cudaStream_t st = nullptr;
+    ctx->h2d_bytes = ctx->d2h_bytes = 0;
+    xsp_span_cols doc = upload_cols(ctx, hoc, st);
+    xsp_traces dot = upload_traces(ctx, hot, st);
+    // the serialized batch under its own buffer names
+    ctx->tag = ".ser";
+    xsp_span_cols dsc = upload_cols(ctx, hsc, st);
+    xsp_traces dst = upload_traces(ctx, hst, st);
+    ctx->tag.clear();
+    xsp_corr_out dcorr;
+    std::memset(&dcorr, 0, sizeof(dcorr));
+    xsp::run_resolve(ctx, &doc, &dot, &dsc, &dst, &dcorr, st);
+    download_corr(ctx, dcorr, out, st);
+    XSP_CUDA(cudaStreamSynchronize(st));
   });
 }
 

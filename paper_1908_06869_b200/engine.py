@@ -71,6 +71,10 @@ class CorrResult:
             return "bundle has no model span; nothing to correlate"
         if s == capi.T_MULTI_MODEL:
             return "bundle has more than one model span"
+        if s == capi.T_SER_AMBIGUOUS:
+            return f"serialized run is itself ambiguous ({a} span(s)); cannot resolve"
+        if s == capi.T_SER_FAILED:
+            return "serialized run failed to correlate (see the serialized batch)"
         if s == capi.T_SKIP_LEVEL:
             return (f"span {int(batch.span_id[a])} ('{batch.name(batch.name_id[a])}') is kernel-level "
                     "but the run did not profile the layer level; parents cannot skip a level")
@@ -263,6 +267,21 @@ class Engine:
             C.c_void_p(b.ptr("span_id")), b.batch.n_traces, C.c_void_p(b.ptr("trace_span_off")),
             C.c_void_p(perm_ptr), C.byref(ws), C.c_void_p(stream)))
         return bool(ws.value)
+
+    def resolve_serialized(self, original: SpanBatch, serialized: SpanBatch) -> CorrResult:
+        """resolve_with_serialized (correlator.cpp:379-456) for every trace pair
+        (xsp_resolve_serialized_host); both batches share one name table."""
+        if original.names != serialized.names:
+            raise ValueError("resolve_serialized: the batches must share one name table")
+        oc, ot = original.cols(), original.traces()
+        sc, stt = serialized.cols(), serialized.traces()
+        co = capi.CorrOut()
+        self._check(self.lib.xsp_resolve_serialized_host(self.ctx, C.byref(oc), C.byref(ot), C.byref(sc),
+                                                         C.byref(stt), C.byref(co)))
+        cc = _corr_counts(co)
+        return CorrResult(co.n_traces, co.n_failed,
+                          {n: _copy(getattr(co, n), t, cc[k]) for n, t, k in capi.CORR_FIELDS},
+                          co.n_layers, co.n_kernels, co.n_orphans, co.n_ambiguities, co.n_candidates)
 
     def validate(self, batch: SpanBatch, span_trace_id: Optional[np.ndarray] = None,
                  tag_bits: Optional[np.ndarray] = None) -> List[List[Tuple[int, int]]]:
