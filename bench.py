@@ -304,7 +304,7 @@ def config(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--runs", type=int, default=20, help="iterations per (model, batch) group")
@@ -348,8 +348,6 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    eng.set_profiling(True)
-    eng.stage_reset()
     barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
@@ -361,6 +359,15 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms = t0.elapsed_time(t1) / args.steps
+    # per-stage device times (and the roofline kernel's launch time): the same
+    # steps again with CUDA events around every stage on the launching stream
+    # (kept out of the timed loop above: the events and their host calls cost
+    # time of their own)
+    eng.set_profiling(True)
+    eng.stage_reset()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
     stages = eng.stage_times()
     eng.set_profiling(False)
     if dist:

@@ -6,6 +6,7 @@
 #include <stdexcept>
 
 #include "ctx.h"
+#include "prims.cuh"
 
 #define XSP_API extern "C" __attribute__((visibility("default")))
 
@@ -26,9 +27,11 @@ namespace {
 xsp_status guard(xsp_ctx* ctx, const char* what, auto&& body) {
   if (!ctx) return XSP_E_INVALID;
   ctx->launches = 0;
+  const uint64_t xfer0 = xsp::g_xfer_launches;
   try {
     XSP_CUDA(cudaSetDevice(ctx->device));
     body();
+    ctx->launches += xsp::g_xfer_launches - xfer0;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
     ctx->last_error.clear();

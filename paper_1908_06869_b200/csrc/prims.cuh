@@ -17,8 +17,11 @@ namespace xsp {
 static __global__ void k_xfer_words(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
+// launches of k_xfer_words by this host thread (added to the API call's count)
+inline thread_local uint64_t g_xfer_launches = 0;
 // bytes: a multiple of 4, both pointers 4-byte aligned
 inline void xfer_small(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  ++g_xfer_launches;
   const uint32_t n = static_cast<uint32_t>(bytes / 4);
   const uint32_t threads = n <= 32 ? 32 : 256;
   uint32_t blocks = (n + threads - 1) / threads;
