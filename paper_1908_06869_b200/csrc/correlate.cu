@@ -63,11 +63,13 @@ struct Orphans {
   uint32_t* row;
   uint8_t* reason;
   uint32_t* count;
+  uint32_t cap;   // entries beyond cap are counted, not written (the host retries larger)
 };
 
 __device__ __forceinline__ void emit_orphan(const Orphans& o, uint32_t t, uint32_t cat,
                                             uint64_t key, uint32_t row, uint8_t reason) {
   uint32_t s = atomicAdd(o.count, 1u);
+  if (s >= o.cap) return;
   o.tc[s] = ((uint64_t)t << 3) | cat;
   o.key[s] = key;
   o.row[s] = row;
@@ -281,6 +283,7 @@ struct P1Args {
   uint32_t* amb_count;
   uint32_t* pend_kl;
   uint32_t* pend_count;
+  uint32_t amb_cap, pend_cap;  // list capacities (counts beyond them trigger a retry)
 };
 
 // TMA descriptors of the four u64 columns, each viewed as a 2-D tensor of
@@ -936,7 +939,8 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
         uint32_t par;
         if (f & XSP_F_PARENT) {
           par = PAR_PENDING;
-          a.pend_kl[atomicAdd(a.pend_count, 1u)] = k_ex;
+          const uint32_t s = atomicAdd(a.pend_count, 1u);
+          if (s < a.pend_cap) a.pend_kl[s] = k_ex;
         } else {
           const bool in_j = lastE > e;  // end_j >= e (ends stored +1)
           const bool in_m = lastM > e;  // an earlier layer has end >= e
@@ -949,8 +953,10 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
             // >= 2 candidates, or an earlier layer outlives j: exact rare path
             par = PAR_AMBIG;
             const uint32_t s = atomicAdd(a.amb_count, 1u);
-            a.amb_kl[s] = k_ex;
-            a.amb_gx[s] = g;
+            if (s < a.amb_cap) {
+              a.amb_kl[s] = k_ex;
+              a.amb_gx[s] = g;
+            }
           }
         }
         KlEnt ent;
@@ -1644,8 +1650,25 @@ uint32_t read_u32(xsp_ctx* ctx, const uint32_t* dptr, cudaStream_t st) {
 
 }  // namespace
 
+struct ListOverflow {};
+
+void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, int mode,
+                        xsp_corr_out* out, cudaStream_t st);
+
 void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, int mode,
                    xsp_corr_out* out, cudaStream_t st) {
+  for (int attempt = 0;; ++attempt) {
+    try {
+      run_correlate_once(ctx, c, tr, mode, out, st);
+      return;
+    } catch (const ListOverflow&) {
+      if (attempt >= 2) throw std::runtime_error("correlate: exception lists kept overflowing");
+    }
+  }
+}
+
+void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, int mode,
+                        xsp_corr_out* out, cudaStream_t st) {
   const int sort_if_needed = mode & 1;
   const bool parents_only = (mode & XSP_CORR_PARENTS_ONLY) != 0;
   const uint64_t n = c->n_spans;
@@ -1714,18 +1737,28 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   a.t_kl_off = ctx->d<uint32_t>("c.t_kl_off", T + 1);
   a.t_ex_off = ctx->d<uint32_t>("c.t_ex_off", T + 1);
   Orphans orph;
-  const uint64_t orph_cap = n + 16;  // at most one per span (exec-level layers: two, but then no launch)
-  orph.tc = ctx->d<uint64_t>("c.o_tc", 2 * orph_cap);
-  orph.key = ctx->d<uint64_t>("c.o_key", 2 * orph_cap);
-  orph.row = ctx->d<uint32_t>("c.o_row", 2 * orph_cap);
-  orph.reason = ctx->d<uint8_t>("c.o_reason", 2 * orph_cap);
+  // Orphan / ambiguity / explicit-parent lists are rare: sized for a fraction
+  // of the spans (or the size a previous call needed); overflow is detected at
+  // the read-backs and the call is redone with room for every entry.
+  auto list_cap = [&](uint64_t hint) {
+    const uint64_t lo = std::min<uint64_t>(2 * n + 32, n / 16 + 4096);
+    return (uint32_t)std::min<uint64_t>(std::max<uint64_t>(hint, lo), 0xFFFFFFF0ull);
+  };
+  const uint32_t orph_cap = list_cap(ctx->cap_orph);
+  orph.tc = ctx->d<uint64_t>("c.o_tc", orph_cap);
+  orph.key = ctx->d<uint64_t>("c.o_key", orph_cap);
+  orph.row = ctx->d<uint32_t>("c.o_row", orph_cap);
+  orph.reason = ctx->d<uint8_t>("c.o_reason", orph_cap);
+  orph.cap = orph_cap;
   orph.count = counters + 0;
   a.orph = orph;
   a.parents_only = parents_only;
-  a.amb_kl = ctx->d<uint32_t>("c.amb_kl", n);
-  a.amb_gx = ctx->d<uint32_t>("c.amb_gx", n);
+  a.amb_cap = list_cap(ctx->cap_amb);
+  a.pend_cap = list_cap(ctx->cap_pend);
+  a.amb_kl = ctx->d<uint32_t>("c.amb_kl", a.amb_cap);
+  a.amb_gx = ctx->d<uint32_t>("c.amb_gx", a.amb_cap);
   a.amb_count = counters + 1;
-  a.pend_kl = ctx->d<uint32_t>("c.pend_kl", n);
+  a.pend_kl = ctx->d<uint32_t>("c.pend_kl", a.pend_cap);
   a.pend_count = counters + 2;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   a.bulk = n >= (uint64_t)P1_TILE && al16(c->begin_ns) && al16(c->end_ns) && al16(c->cid) &&
@@ -1797,6 +1830,12 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
   XSP_CUDA(cudaStreamSynchronize(st));
   const uint32_t nl = htot[0], nkl = htot[1], nex = htot[2];
   const uint32_t n_amb_raw = htot[9], n_pend = htot[10];
+  if (htot[8] > orph_cap || n_amb_raw > a.amb_cap || n_pend > a.pend_cap) {
+    ctx->cap_orph = std::max<uint64_t>(ctx->cap_orph, htot[8] + htot[8] / 4 + 1024);
+    ctx->cap_amb = std::max<uint64_t>(ctx->cap_amb, n_amb_raw + n_amb_raw / 4 + 1024);
+    ctx->cap_pend = std::max<uint64_t>(ctx->cap_pend, n_pend + n_pend / 4 + 1024);
+    throw ListOverflow{};
+  }
   if (htot[13]) {
     // not in timeline order (span.hpp:161-163)
     (void)sort_if_needed;
@@ -2011,6 +2050,10 @@ void run_correlate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, i
 
   // ---- orphans in reference order
   const uint32_t no = read_u32(ctx, orph.count, st);
+  if (no > orph_cap) {  // the fusion phases added more than the room left
+    ctx->cap_orph = std::max<uint64_t>(ctx->cap_orph, no + no / 4 + 1024);
+    throw ListOverflow{};
+  }
   out->n_orphans = no;
   out->orphan_row = ctx->d<uint32_t>("o.orphan_row", no);
   out->orphan_reason = ctx->d<uint8_t>("o.orphan_reason", no);

@@ -96,6 +96,9 @@ struct xsp_ctx {
   // Host copies of the last correlation's per-trace layer / kernel offsets,
   // fetched at its final read-back: xsp_analyze on that correlation sizes its
   // group tables on the host instead of with another device round trip.
+  // capacities the rare-entry lists of correlate needed (grow-only hints)
+  uint64_t cap_orph = 0, cap_amb = 0, cap_pend = 0;
+
   const void* hc_layer_key = nullptr;
   const void* hc_kernel_key = nullptr;
   uint32_t hc_T = 0;

@@ -198,3 +198,18 @@ def test_unsorted_input_is_rejected(engine):
     with pytest.raises(capi.XspError) as e:
         engine.run_host(b)
     assert e.value.status == capi.XSP_E_UNSORTED
+
+
+def test_orphan_heavy_batch_retries_with_larger_lists(engine, has_ref):
+    """Rare-entry lists start at n/16 + 4096 entries; a batch where most launches
+    and executions are orphans overflows them and is redone with room for all."""
+    from paper_1908_06869_b200 import synth
+    b, gf, gr, gb = synth.c3(runs=2, n_models=3, batches=(1, 4), seed=3)
+    kind = (b.flags >> 2) & 3
+    f = b.flags.copy()
+    f[kind == 1] &= ~np.uint8(0x20)  # every launch without a cid -> orphan (and its exec too)
+    b.flags = f
+    corr, tabs = engine.run_host(b)
+    assert corr.n_orphans > b.n_spans // 16 + 4096
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
