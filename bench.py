@@ -293,6 +293,84 @@ def measure_c4(eng, args, rank: int, world: int, local: int, dist):
                         "executions on 4 interleaved streams, a drain every 2000 layers"}
 
 
+class _Replica:
+    """DeviceBatch interface over slices of replicated device columns."""
+
+    def __init__(self, batch_ns, tensors):
+        from paper_1908_06869_b200.engine import DeviceBatch
+        self.batch, self.t = batch_ns, tensors
+        self._db = DeviceBatch
+
+    def _p(self, k, typ):
+        return self._db._p(self, k, typ)
+
+    def cols(self):
+        return self._db.cols(self)
+
+    def traces(self):
+        return self._db.traces(self)
+
+
+def measure_c5(eng, dev, b, groups, steps: int, copies: int = 21, per_call: int = 11):
+    """BASELINE config 5 on one GPU: a ~1 B-span multi-trace corpus (the C3 corpus
+    replicated `copies` times in HBM, independent traces) correlated + analysed
+    as device-resident calls of up to `per_call` copies (~0.5 B spans) each.
+    Every copy must come back with the C3 counts (no orphans, no failures)."""
+    import torch
+    from types import SimpleNamespace
+    n, T = b.n_spans, b.n_traces
+    M, Lr = b.flops.size, b.alloc_bytes.size
+    metric_cols = {"flops", "dram_read", "dram_write", "occupancy"}
+    layer_cols = {"alloc_bytes", "type_id"}
+    big = {k: t.repeat(copies) for k, t in dev.t.items() if k not in ("trace_span_off", "trace_levels")}
+    off = dev.t["trace_span_off"]
+    offs = torch.cat([off[:-1] + k * n for k in range(per_call)] + [off[-1:] + (per_call - 1) * n])
+    levels = dev.t["trace_levels"].repeat(per_call)
+    gf, gr, gb = (np.asarray(x) for x in groups)
+    ref_co = eng.correlate_device(dev)
+    want_l, want_k = int(ref_co.n_layers), int(ref_co.n_kernels)
+    calls = []
+    for k0 in range(0, copies, per_call):
+        kk = min(per_call, copies - k0)
+        t = {}
+        for key, tens in big.items():
+            per = M if key in metric_cols else (Lr if key in layer_cols else n)
+            t[key] = tens[k0 * per:(k0 + kk) * per]
+        t["trace_span_off"] = offs[:kk * T + 1]
+        t["trace_levels"] = levels[:kk * T]
+        ns = SimpleNamespace(n_spans=kk * n, n_traces=kk * T, flops=np.empty(kk * M, np.uint8),
+                             alloc_bytes=np.empty(kk * Lr, np.uint8), peak_flops=b.peak_flops, mem_bw=b.mem_bw)
+        g = (np.concatenate([gf + j * T for j in range(kk)]), np.tile(gr, kk), np.tile(gb, kk))
+        calls.append((_Replica(ns, t), g, kk))
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def step(check=False):
+        for view, g, kk in calls:
+            co = eng.correlate_device(view, stream=stream)
+            eng.analyze_device(view, co, g, stream=stream)
+            if check:
+                assert co.n_failed == 0 and co.n_orphans == 0, "C5: unexpected failures / orphans"
+                assert int(co.n_layers) == kk * want_l and int(co.n_kernels) == kk * want_k, "C5: counts"
+
+    step(check=True)
+    torch.cuda.synchronize()
+    reps = max(2, steps // 4)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(reps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / reps
+    total = n * copies
+    del big, calls
+    torch.cuda.empty_cache()
+    return {"metric": "M spans/s correlated+analyzed, ~1 B-span multi-trace corpus", "value": total / (ms / 1e3) / 1e6,
+            "unit": UNIT, "ms_per_step": ms, "spans": total, "calls_per_step": (copies + per_call - 1) // per_call,
+            "workload": f"C5: the C3 corpus replicated {copies}x in HBM ({copies * T} traces, {total} spans), "
+                        f"correlate + a5..a15 in device-resident calls of <= {per_call} copies"}
+
+
 def config(args):
     return {"workload": "C3: 65 synthetic models x 8 batch sizes (1..128) x R iterations, correlate + "
                         "a8..a15 + top-3, one group per (model,batch)",
@@ -312,6 +390,7 @@ def main():
     ap.add_argument("--ref-sample-spans", type=int, default=3_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sort", action="store_true", help="skip the shuffled sort_timeline measurement")
+    ap.add_argument("--c5", type=int, default=1, help="measure the ~1 B-span C5 corpus (0 skips)")
     ap.add_argument("--c4-layers", type=int, default=28_600_000,
                     help="layers of the C4 long trace (~7 spans per layer; 0 skips the C4 measurement)")
     args = ap.parse_args()
@@ -396,6 +475,7 @@ def main():
            "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
 
     sort_line = measure_sort(eng, dev, b, args.steps, local) if not args.no_sort else None
+    c5_line = measure_c5(eng, dev, b, groups, args.steps) if args.c5 else None
     del dev
     c4_line = measure_c4(eng, args, rank, world, local, dist) if args.c4_layers > 0 else None
 
@@ -433,6 +513,8 @@ def main():
         line["sort_shuffled"] = sort_line
     if c4_line:
         line["c4"] = c4_line
+    if c5_line:
+        line["c5"] = c5_line
     if world == 1 and not args.no_cpu_baseline:
         from oracle import ref
         if ref.available():
