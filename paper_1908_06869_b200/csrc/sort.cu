@@ -7,7 +7,7 @@
 // reduced, each span gets a packed 64-bit key
 //   (begin - min_begin) | rank | (span_id - min_span_id)
 // and a stable LSD radix sort of the 16-bit index permutation (warp-level
-// histograms, a digit-major scan, __match_any_sync-ranked scatter) orders it.
+// histograms, a digit-major scan, ballot-ranked scatter) orders it.
 // HBM traffic is one read of begin/span_id/flags and one perm write (21 B/span).
 // Traces that are longer or whose packed key needs more than 64 bits fall back
 // to one global LSD radix sort over the composite key (trace, begin_ns, rank,
@@ -21,15 +21,22 @@ namespace xsp {
 
 namespace {
 
+// Timeline-order check. A pair (i-1, i) needs the trace lookup only when
+// begin does not increase (a trace head or a tie); once some block has found
+// disorder the remaining blocks return at once.
 __global__ void k_sort_check(const uint64_t* __restrict__ begin, const uint8_t* __restrict__ flags,
                              const uint64_t* __restrict__ sid, const uint64_t* __restrict__ off, uint32_t T,
                              uint64_t n, uint32_t* __restrict__ unsorted) {
+  __shared__ uint32_t s_done;
+  if (threadIdx.x == 0) s_done = *reinterpret_cast<volatile uint32_t*>(unsorted);
+  __syncthreads();
+  if (s_done) return;
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0 || i >= n) return;
-  const uint32_t t = trace_of(off, 0, T, i);
-  if (off[t] == i) return;
   const uint64_t b0 = begin[i - 1], b1 = begin[i];
   if (b0 < b1) return;
+  const uint32_t t = trace_of(off, 0, T, i);
+  if (off[t] == i) return;
   if (b0 > b1) {
     *unsorted = 1;
     return;
@@ -67,8 +74,24 @@ __global__ void k_sort_key(int field, const uint32_t* __restrict__ val, const ui
 
 constexpr uint32_t kSegCap = 16384;  // spans per CTA-sorted trace (large class)
 constexpr uint32_t kSegCapSmall = 4096;  // small class: 4 CTAs per SM
+constexpr uint32_t kSegCapMid = 8192;    // middle class: 2 CTAs per SM
 
 __device__ __forceinline__ uint32_t bit_width64(uint64_t v) { return v ? 64 - __clzll(v) : 0; }
+
+// Lanes of `valid` holding the same 8-bit digit as this lane: one ballot per
+// digit bit (warp-level multisplit) instead of __match_any_sync; bits that are
+// constant over the trace (clear in `vary`) need no ballot.
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, uint32_t valid, uint32_t vary) {
+  uint32_t m = valid;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (!((vary >> b) & 1u)) continue;
+    const uint32_t bit = (d >> b) & 1u;
+    const uint32_t v = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? v : ~v;
+  }
+  return m;
+}
 
 // Shared memory of k_sort_seg: the packed keys stay in place; the LSD passes
 // permute 16-bit indices between two buffers (the trace's keys plus both index
@@ -77,7 +100,8 @@ template <uint32_t CAP, int WARPS>
 struct SegSmem {
   unsigned long long key[CAP];
   uint16_t idx[2][CAP];
-  uint16_t wcnt[WARPS][256];  // per-warp digit counts, then per-warp digit offsets
+  uint16_t wcnt[WARPS][258];  // per-warp digit counts, then per-warp digit offsets (rows padded
+                              // by one word: the digit scan reads them conflict-free)
 };
 
 // One CTA per trace: key = (begin - min) | rank | (span_id - min), packed into
@@ -85,9 +109,10 @@ struct SegSmem {
 // stable LSD radix sort (8-bit digits, constant digits skipped) of the index
 // permutation: per pass every warp histograms its contiguous segment of the
 // current order, a scan gives each (digit, warp) its output offset, and the
-// warp re-walks its segment placing indices with __match_any_sync ranks.
+// warp re-walks its segment placing indices with ballot (multisplit) ranks.
 // Size classes: traces of at most kSegCapSmall spans run as 256-thread CTAs with
-// 52 KB of shared memory (4 per SM); longer ones as 1024-thread CTAs with 210 KB.
+// 52 KB of shared memory (4 per SM), up to kSegCapMid as 512-thread CTAs with
+// 104 KB (2 per SM), longer ones as 1024-thread CTAs with 210 KB.
 // Every launch covers all traces; a CTA leaves traces of the other class.
 template <uint32_t CAP, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sort_seg(const uint64_t* __restrict__ begin,
@@ -97,6 +122,9 @@ __global__ void __launch_bounds__(THREADS) k_sort_seg(const uint64_t* __restrict
                                                       uint32_t* __restrict__ perm, uint32_t* __restrict__ fallback) {
   constexpr int kSegWarps = THREADS / 32;
   constexpr uint32_t cap = CAP;
+  // iterations of 32 spans per warp segment (a segment holds <= CAP / kSegWarps)
+  constexpr int kIters = (int)(CAP / (kSegWarps * 32));
+  static_assert(CAP <= 16384, "indices are packed in 14 bits");
   extern __shared__ __align__(16) unsigned char seg_dyn[];
   SegSmem<CAP, kSegWarps>& sm = *reinterpret_cast<SegSmem<CAP, kSegWarps>*>(seg_dyn);
   __shared__ unsigned long long red[4][kSegWarps];
@@ -185,25 +213,58 @@ __global__ void __launch_bounds__(THREADS) k_sort_seg(const uint64_t* __restrict
     uint16_t* dst = sm.idx[cur ^ 1];
     for (uint32_t d = lane; d < 256; d += 32) sm.wcnt[warp][d] = 0;
     __syncwarp();
-    // histogram of the warp's segment
-    for (uint32_t base = p0; base < p1; base += 32) {
+    // histogram of the warp's segment; every lane keeps, per iteration, its
+    // index, digit, rank among equal digits and whether it is the last of them
+    // (packed: x | d << 14 | below << 22 | last << 27 | valid << 28), so the
+    // scatter needs neither the keys nor the ballots again
+    const uint32_t vary = (uint32_t)(varying >> shift) & 0xFFu;
+    uint32_t pk[kIters];
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+      pk[it] = 0;
+      const uint32_t base = p0 + 32u * it;
+      if (base >= p1) continue;  // warp-uniform
       const uint32_t i = base + lane;
-      const uint32_t d = i < p1 ? (uint32_t)(sm.key[src[i]] >> shift) & 0xFFu : 256u + lane;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      if (i < p1 && (peers & lanemask_lt()) == 0) sm.wcnt[warp][d] += (uint16_t)__popc(peers);
+      const bool v = i < p1;
+      const uint32_t valid = __ballot_sync(0xffffffffu, v);
+      const uint32_t x = v ? src[i] : 0u;
+      const uint32_t d = v ? (uint32_t)(sm.key[x] >> shift) & 0xFFu : 0u;
+      const uint32_t peers = digit_peers(d, valid, vary);
+      const uint32_t below = __popc(peers & lanemask_lt());
+      const bool last = (peers >> lane) <= 1u;  // no equal digit in a higher lane
+      if (v && last) sm.wcnt[warp][d] += (uint16_t)(below + 1);
       __syncwarp();
+      if (v) pk[it] = x | d << 14 | below << 22 | (uint32_t)last << 27 | 1u << 28;
     }
     __syncthreads();
-    // per digit: totals and the exclusive offsets of the warps (digit-major)
-    for (uint32_t d = tid; d < 256; d += THREADS) {
-      uint32_t run = 0;
-#pragma unroll 8
-      for (int w = 0; w < kSegWarps; ++w) {
-        const uint32_t c = sm.wcnt[w][d];
-        sm.wcnt[w][d] = (uint16_t)run;
-        run += c;
+    // per digit: totals and the exclusive offsets of the warps (digit-major);
+    // kDP consecutive threads share a digit, each scanning kSegWarps / kDP warps
+    {
+      constexpr int kDP = THREADS >= 256 ? THREADS / 256 : 1;
+      constexpr int kWPT = kSegWarps / kDP;
+      static_assert(kSegWarps % kDP == 0, "warps per digit thread");
+      const uint32_t d = tid / kDP, q = tid % kDP;
+      if (d < 256) {
+        uint32_t c[kWPT], sum = 0;
+#pragma unroll
+        for (int w = 0; w < kWPT; ++w) {
+          c[w] = sm.wcnt[q * kWPT + w][d];
+          sum += c[w];
+        }
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < kDP; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o, kDP);
+          if (q >= (uint32_t)o) inc += y;
+        }
+        uint32_t run = inc - sum;
+#pragma unroll
+        for (int w = 0; w < kWPT; ++w) {
+          sm.wcnt[q * kWPT + w][d] = (uint16_t)run;
+          run += c[w];
+        }
+        if (q == kDP - 1) s_tot[d] = inc;
       }
-      s_tot[d] = run;
     }
     __syncthreads();
     if (warp == 0) {  // exclusive scan of the 256 digit totals (8 per lane)
@@ -228,18 +289,17 @@ __global__ void __launch_bounds__(THREADS) k_sort_seg(const uint64_t* __restrict
     }
     __syncthreads();
     // stable scatter: digit start + earlier warps + running rank in this warp
-    for (uint32_t base = p0; base < p1; base += 32) {
-      const uint32_t i = base + lane;
-      const uint16_t x = i < p1 ? src[i] : 0;
-      const uint32_t d = i < p1 ? (uint32_t)(sm.key[x] >> shift) & 0xFFu : 256u + lane;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      const uint32_t below = __popc(peers & lanemask_lt());
-      uint32_t r0 = 0;
-      if (i < p1) r0 = sm.wcnt[warp][d];
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+      if (p0 + 32u * it >= p1) continue;  // warp-uniform
+      const uint32_t u = pk[it];
+      const bool v = (u >> 28) & 1u;
+      const uint32_t x = u & 0x3FFFu, d = (u >> 14) & 0xFFu, below = (u >> 22) & 31u;
+      const uint32_t r0 = v ? sm.wcnt[warp][d] : 0u;
       __syncwarp();
-      if (i < p1) {
-        dst[s_tot[d] + r0 + below] = x;
-        if ((peers & lanemask_lt()) == 0) sm.wcnt[warp][d] = (uint16_t)(r0 + __popc(peers));
+      if (v) {
+        dst[s_tot[d] + r0 + below] = (uint16_t)x;
+        if ((u >> 27) & 1u) sm.wcnt[warp][d] = (uint16_t)(r0 + below + 1);
       }
       __syncwarp();
     }
@@ -267,15 +327,19 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
   // per-trace CTA sort; the global radix sort only if some trace does not fit
   XSP_CUDA(cudaMemsetAsync(flag, 0, 4, st));
   auto* k_small = k_sort_seg<kSegCapSmall, 256>;
+  auto* k_mid = k_sort_seg<kSegCapMid, 512>;
   auto* k_large = k_sort_seg<kSegCap, 1024>;
-  constexpr size_t smem_small = sizeof(SegSmem<kSegCapSmall, 8>), smem_large = sizeof(SegSmem<kSegCap, 32>);
+  constexpr size_t smem_small = sizeof(SegSmem<kSegCapSmall, 8>), smem_mid = sizeof(SegSmem<kSegCapMid, 16>),
+                   smem_large = sizeof(SegSmem<kSegCap, 32>);
   XSP_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small));
+  XSP_CUDA(cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mid));
   XSP_CUDA(cudaFuncSetAttribute(k_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_large));
   ctx->stage_begin("sort", st);
   k_small<<<T, 256, smem_small, st>>>(begin, flags, sid, off, 0, perm, flag);
-  k_large<<<T, 1024, smem_large, st>>>(begin, flags, sid, off, kSegCapSmall + 1, perm, flag);
+  k_mid<<<T, 512, smem_mid, st>>>(begin, flags, sid, off, kSegCapSmall + 1, perm, flag);
+  k_large<<<T, 1024, smem_large, st>>>(begin, flags, sid, off, kSegCapMid + 1, perm, flag);
   ctx->stage_end("sort", st);
-  ctx->launches += 2;
+  ctx->launches += 3;
   XSP_CUDA(cudaMemcpyAsync(h, flag, 4, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
   if (!h[0] && !getenv("XSP_SORT_GLOBAL")) return;

@@ -89,3 +89,24 @@ def test_fallback_wide_keys_and_long_trace(engine):
                   trace_run=np.zeros(len(lens)), trace_serialized=np.zeros(len(lens)), names=[b"x"], types=[])
     perm, was = engine.sort_timeline(b)
     assert np.array_equal(perm, expected_perm(b))
+
+
+def test_size_classes_boundaries(engine):
+    """Traces at the edges of every shared-memory size class (4096 / 8192 /
+    16384 spans per CTA), with begin ties broken by rank and span_id."""
+    rng = np.random.default_rng(7)
+    lens = [4096, 4097, 8192, 8193, 16384, 2, 31, 33, 5000]
+    n = sum(lens)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    beg = rng.integers(10 ** 9, 10 ** 9 + 20000, n).astype(np.uint64)
+    b = SpanBatch(span_id=rng.integers(0, 4000, n).astype(np.uint64), parent_id=np.zeros(n, np.uint64),
+                  begin_ns=beg, end_ns=beg + 5, cid=np.zeros(n, np.uint64),
+                  flags=rng.integers(0, 4, n).astype(np.uint8), name_id=np.zeros(n, np.uint32),
+                  flops=np.zeros(0, np.uint64), dram_read=np.zeros(0, np.uint64),
+                  dram_write=np.zeros(0, np.uint64), occupancy=np.zeros(0), alloc_bytes=np.zeros(0, np.int64),
+                  type_id=np.zeros(0, np.uint32), trace_span_off=off, trace_id=np.arange(len(lens)),
+                  trace_levels=np.full(len(lens), 7), trace_batch=np.ones(len(lens)),
+                  trace_run=np.zeros(len(lens)), trace_serialized=np.zeros(len(lens)), names=[b"x"], types=[])
+    perm, was = engine.sort_timeline(b)
+    assert not was
+    assert np.array_equal(perm, expected_perm(b))
