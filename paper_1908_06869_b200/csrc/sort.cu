@@ -21,29 +21,84 @@ namespace xsp {
 
 namespace {
 
-// Timeline-order check. A pair (i-1, i) needs the trace lookup only when
-// begin does not increase (a trace head or a tie); once some block has found
-// disorder the remaining blocks return at once.
-__global__ void k_sort_check(const uint64_t* __restrict__ begin, const uint8_t* __restrict__ flags,
-                             const uint64_t* __restrict__ sid, const uint64_t* __restrict__ off, uint32_t T,
-                             uint64_t n, uint32_t* __restrict__ unsorted) {
-  __shared__ uint32_t s_done;
-  if (threadIdx.x == 0) s_done = *reinterpret_cast<volatile uint32_t*>(unsorted);
+// Timeline-order check fused with the identity permutation. Every block owns a
+// contiguous run of 1024-span chunks; per chunk it marks the trace heads in a
+// shared bitmap (walking the trace offsets forward from the previous chunk, so
+// no per-span trace lookup), then checks every pair (i-1, i) that is not a
+// head: begin must not decrease, and equal begins are ordered by (rank,
+// span_id). One barrier per chunk: the begin / flags / offset loads and the
+// disorder flag are issued together, and the bitmaps and trace cursors are
+// triple-buffered (chunk q clears the buffers of chunk q + 2, which chunk q + 1's
+// barrier orders before their use). Once disorder has been found the remaining
+// chunks are skipped.
+constexpr int kCheckItems = 4;
+constexpr uint32_t kCheckChunk = 256 * kCheckItems;
+__global__ void __launch_bounds__(256) k_sort_check(const uint64_t* __restrict__ begin,
+                                                    const uint8_t* __restrict__ flags,
+                                                    const uint64_t* __restrict__ sid,
+                                                    const uint64_t* __restrict__ off, uint32_t T, uint64_t n,
+                                                    uint32_t* __restrict__ perm, uint32_t* __restrict__ unsorted) {
+  __shared__ uint32_t s_head[3][kCheckChunk / 32];
+  __shared__ uint32_t s_tn[3];  // last trace starting <= the chunk end
+  __shared__ uint32_t s_t0;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t nchunks = (n + kCheckChunk - 1) / kCheckChunk;
+  const uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const uint64_t q0 = (uint64_t)blockIdx.x * per, q1 = min(nchunks, q0 + per);
+  if (q0 >= q1) return;
+  if (tid < 3 * kCheckChunk / 32) (&s_head[0][0])[tid] = 0;
+  if (tid < 3) s_tn[tid] = 0;
+  if (tid == 0) s_t0 = trace_of(off, 0, T, q0 * kCheckChunk);  // last trace starting <= the run start
   __syncthreads();
-  if (s_done) return;
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0 || i >= n) return;
-  const uint64_t b0 = begin[i - 1], b1 = begin[i];
-  if (b0 < b1) return;
-  const uint32_t t = trace_of(off, 0, T, i);
-  if (off[t] == i) return;
-  if (b0 > b1) {
-    *unsorted = 1;
-    return;
+  uint32_t tcur = s_t0;
+  for (uint64_t q = q0; q < q1; ++q) {
+    const uint32_t buf = (uint32_t)(q % 3);
+    uint32_t* head = s_head[buf];
+    const uint64_t c0 = q * kCheckChunk, c1 = min(n, c0 + kCheckChunk);
+    uint64_t b0[kCheckItems], b1[kCheckItems];
+    uint32_t f01[kCheckItems];
+#pragma unroll
+    for (int k = 0; k < kCheckItems; ++k) {
+      const uint64_t i = c0 + k * 256 + tid;
+      const bool v = i > 0 && i < c1;
+      b0[k] = v ? begin[i - 1] : 0;
+      b1[k] = v ? begin[i] : 1;
+      f01[k] = v ? (uint32_t)flags[i - 1] << 8 | flags[i] : 0;
+      if (i < c1) perm[i] = (uint32_t)i;
+    }
+    const bool stop = tid == 0 && __ldcg(unsorted) != 0;
+    // heads: traces starting in [c0, c1)
+    uint64_t tb = tcur;
+    bool more;
+    for (;;) {
+      const uint64_t tt = tb + tid;
+      const uint64_t o = tt <= T ? off[tt] : ~0ull;
+      if (o >= c0 && o < c1) atomicOr(&head[(uint32_t)(o - c0) >> 5], 1u << ((uint32_t)(o - c0) & 31u));
+      if (o <= c1) atomicMax(&s_tn[buf], (uint32_t)tt);
+      more = tid == 255 && o <= c1;
+      if (__syncthreads_or(more || stop) == 0) break;
+      if (__syncthreads_or(stop)) return;
+      tb += 256;
+    }
+    tcur = max(tcur, s_tn[buf]);
+    if (tid < kCheckChunk / 32) s_head[(q + 2) % 3][tid] = 0;
+    if (tid == 0) s_tn[(q + 2) % 3] = 0;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < kCheckItems; ++k) {
+      const uint32_t j = k * 256 + tid;
+      const uint64_t i = c0 + j;
+      if (b0[k] < b1[k] || ((head[j >> 5] >> (j & 31u)) & 1u)) continue;
+      if (b0[k] > b1[k]) {
+        bad = true;
+        continue;
+      }
+      const uint32_t l0 = f_level((uint8_t)(f01[k] >> 8)), l1 = f_level((uint8_t)f01[k]);
+      const uint32_t r0 = l0 >= 2 ? 3 : l0 + 1, r1 = l1 >= 2 ? 3 : l1 + 1;
+      bad |= r0 > r1 || (r0 == r1 && sid[i - 1] > sid[i]);
+    }
+    if (bad) *unsorted = 1;
   }
-  const uint32_t l0 = f_level(flags[i - 1]), l1 = f_level(flags[i]);
-  const uint32_t r0 = l0 >= 2 ? 3 : l0 + 1, r1 = l1 >= 2 ? 3 : l1 + 1;
-  if (r0 > r1 || (r0 == r1 && sid[i - 1] > sid[i])) *unsorted = 1;
 }
 
 __global__ void k_iota_u32(uint32_t* v, uint64_t n) {
@@ -316,9 +371,9 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
   uint32_t* flag = ctx->d<uint32_t>("s.flag", 1);
   XSP_CUDA(cudaMemsetAsync(flag, 0, 4, st));
   auto blocks = [](uint64_t m) { return ceil_div(m ? m : 1, 256); };
-  k_sort_check<<<blocks(n), 256, 0, st>>>(begin, flags, sid, off, T, n, flag);
-  k_iota_u32<<<blocks(n), 256, 0, st>>>(perm, n);
-  ctx->launches += 2;
+  k_sort_check<<<(unsigned)std::min<uint64_t>(ceil_div(n ? n : 1, kCheckChunk), 148 * 8), 256, 0, st>>>(
+      begin, flags, sid, off, T, n, perm, flag);
+  ++ctx->launches;
   uint32_t* h = ctx->h<uint32_t>("s.flag_h", 1);
   XSP_CUDA(cudaMemcpyAsync(h, flag, 4, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));

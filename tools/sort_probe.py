@@ -23,3 +23,17 @@ eng = Engine(0)
 dev = DeviceBatch(b, 0)
 steps = int(os.environ.get("STEPS", "10"))
 print(bench.measure_sort(eng, dev, b, steps, 0))
+# presorted input (the TraceBundle invariant): the order check alone
+perm = torch.empty(b.n_spans, dtype=torch.int32, device="cuda:0")
+st = torch.cuda.current_stream().cuda_stream
+for _ in range(2):
+    assert eng.sort_timeline_device(dev, perm.data_ptr(), st)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(steps):
+    eng.sort_timeline_device(dev, perm.data_ptr(), st)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / steps
+print({"presorted_ms": ms, "M spans/s": b.n_spans / ms / 1e3})
