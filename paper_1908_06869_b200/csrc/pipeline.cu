@@ -102,24 +102,44 @@ struct Pos {
   uint64_t base[B_BASES] = {}; // value to add (Base)
 };
 
-__attribute__((target("popcnt"))) void count_rows(const uint8_t* f, uint64_t n, uint64_t& metric, uint64_t& layer) {
+__attribute__((target("popcnt"))) void count_rows(const uint8_t* f, uint64_t n, uint64_t& metric, uint64_t& layer,
+                                                  uint64_t& child_parent) {
   // eight flags per step: metric bit -> popcount; level == Layer -> bytes whose
-  // low two bits equal XSP_LEVEL_LAYER
+  // low two bits equal XSP_LEVEL_LAYER; child_parent = non-layer spans with an
+  // explicit parent_id (they take the explicit-parent path, which reads the
+  // span_id column densely)
   constexpr uint64_t kOnes = 0x0101010101010101ull;
-  uint64_t m = 0, l = 0, i = 0;
+  uint64_t m = 0, l = 0, cp = 0, i = 0;
   for (; i + 8 <= n; i += 8) {
     uint64_t w;
     std::memcpy(&w, f + i, 8);
     m += __builtin_popcountll(w & (kOnes * XSP_F_METRICS));
     const uint64_t x = (w ^ (kOnes * XSP_LEVEL_LAYER)) & (kOnes * 3u);
-    l += 8 - __builtin_popcountll((x | (x >> 1)) & kOnes);
+    const uint64_t not_layer = (x | (x >> 1)) & kOnes;
+    l += 8 - __builtin_popcountll(not_layer);
+    cp += __builtin_popcountll(not_layer & (w >> 4));  // XSP_F_PARENT = bit 4
   }
   for (; i < n; ++i) {
     m += (f[i] & XSP_F_METRICS) != 0;
     l += (f[i] & 3u) == XSP_LEVEL_LAYER;
+    cp += (f[i] & 3u) != XSP_LEVEL_LAYER && (f[i] & XSP_F_PARENT);
   }
   metric = m;
   layer = l;
+  child_parent = cp;
+}
+
+// Device alias of a page-locked host column (zero-copy reads over PCIe), or
+// nullptr when the memory is pageable or not mapped.
+const uint64_t* mapped_alias(const uint64_t* host) {
+  if (!host || std::getenv("XSP_NO_ZERO_COPY")) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+  return static_cast<const uint64_t*>(at.devicePointer);
 }
 
 // Large copies go out in pieces so that the small transfers of the compute
@@ -216,13 +236,15 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     xsp_span_cols cols;
     xsp_traces tr;
     uint64_t* h_off;  // pinned staging of the re-based trace offsets
+    uint64_t* sid_buf;  // device span_id column (unused while span_id is read zero-copy)
     cudaEvent_t in_ready, free;
     cudaEvent_t computed, out_done;  // this parity's ctx buffers: results ready / copied out
   } slot[2];
   for (int s = 0; s < 2; ++s) {
     const std::string p = "pl" + std::to_string(s) + ".";
     Slot& S = slot[s];
-    S.cols.span_id = ctx->d<uint64_t>(p + "sid", max_n);
+    S.sid_buf = ctx->d<uint64_t>(p + "sid", max_n);
+    S.cols.span_id = S.sid_buf;
     S.cols.parent_id = ctx->d<uint64_t>(p + "par", max_n);
     S.cols.begin_ns = ctx->d<uint64_t>(p + "beg", max_n);
     S.cols.end_ns = ctx->d<uint64_t>(p + "end", max_n);
@@ -256,6 +278,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     }
   } evback{ctx, slot};
 
+  const uint64_t* sid_alias = mapped_alias(hc->span_id);
   auto h2d = [&](void* dst, const void* src, uint64_t bytes) {
     if (!bytes) return;
     copy_pieces(dst, src, bytes, cudaMemcpyHostToDevice, cs);
@@ -273,10 +296,18 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     h2d(const_cast<uint64_t*>(S.cols.end_ns), hc->end_ns + s0, ns * 8);
     h2d(const_cast<uint64_t*>(S.cols.cid), hc->cid + s0, ns * 8);
     h2d(const_cast<uint64_t*>(S.cols.parent_id), hc->parent_id + s0, ns * 8);
-    h2d(const_cast<uint64_t*>(S.cols.span_id), hc->span_id + s0, ns * 8);
     h2d(const_cast<uint32_t*>(S.cols.name_id), hc->name_id + s0, ns * 4);
-    uint64_t mc, lc;
-    count_rows(hc->flags + s0, ns, mc, lc);
+    uint64_t mc, lc, cp;
+    count_rows(hc->flags + s0, ns, mc, lc, cp);
+    // span_id is read sparsely (model spans, timeline ties, orphans,
+    // ambiguities) unless kernels carry explicit parents: read it in place
+    // from page-locked host memory when possible instead of copying it
+    if (sid_alias && cp == 0) {
+      S.cols.span_id = sid_alias + s0;
+    } else {
+      S.cols.span_id = S.sid_buf;
+      h2d(S.sid_buf, hc->span_id + s0, ns * 8);
+    }
     C.m0 = m_run;
     C.m1 = m_run + mc;
     C.l0 = l_run;
