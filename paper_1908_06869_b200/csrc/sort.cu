@@ -1,18 +1,18 @@
 // Stage (b): sort_timeline (span.cpp:112-127) on the device — a stable sort of
 // every trace's spans by (begin_ns, rank(level), span_id).
 //
-// Presorted input (the TraceBundle invariant) is detected first and returns the
-// identity without sorting. Otherwise every trace of up to kSegCap spans is
-// sorted by ONE CTA in shared memory: the trace's begin / span_id ranges are
-// reduced, each span gets a packed 64-bit key
-//   (begin - min_begin) | rank | (span_id - min_span_id)
-// and a stable LSD radix sort of the 16-bit index permutation (warp-level
-// histograms, a digit-major scan, ballot-ranked scatter) orders it.
+// Presorted input (the TraceBundle invariant) is detected first (k_sort_check)
+// and returns the identity without sorting. Otherwise every trace of up to
+// kSegCap spans is sorted by ONE CTA in shared memory (k_sort_merge): the
+// trace's begin / span_id ranges are reduced, each span gets a unique packed
+// 64-bit key (begin - min, rank, span_id - min, local index), the thread-local
+// runs are sorted in registers and merged by merge path in shared memory.
+// Three size classes (4 K / 8 K / 16 K spans) keep 4 / 2 / 1 CTAs per SM.
 // HBM traffic is one read of begin/span_id/flags and one perm write (21 B/span).
-// Traces that are longer or whose packed key needs more than 64 bits fall back
-// to one global LSD radix sort over the composite key (trace, begin_ns, rank,
-// span_id): four stable passes from the least significant field, each skipping
-// the 8-bit digits that are constant over the batch.
+// Traces that are longer, or whose begin range alone needs more than 47 bits,
+// fall back to one global LSD radix sort over the composite key (trace,
+// begin_ns, rank, span_id): four stable passes from the least significant
+// field, each skipping the 8-bit digits that are constant over the batch.
 
 #include "ctx.h"
 #include "prims.cuh"
@@ -133,79 +133,78 @@ constexpr uint32_t kSegCapMid = 8192;    // middle class: 2 CTAs per SM
 
 __device__ __forceinline__ uint32_t bit_width64(uint64_t v) { return v ? 64 - __clzll(v) : 0; }
 
-// Lanes of `valid` holding the same 8-bit digit as this lane: one ballot per
-// digit bit (warp-level multisplit) instead of __match_any_sync; bits that are
-// constant over the trace (clear in `vary`) need no ballot.
-__device__ __forceinline__ uint32_t digit_peers(uint32_t d, uint32_t valid, uint32_t vary) {
-  uint32_t m = valid;
+// ---- per-trace merge sort ----------------------------------------------------
+// Keys are unique u64s: (begin - min) | rank | (span_id - min) | local index j
+// (14 bits) when that fits 63 bits ("full" keys), else (begin - min) | rank | j
+// and runs of equal (begin, rank) are ordered by span_id afterwards (stable:
+// j ascends inside a run). Every thread sorts ITEMS keys in registers (Batcher's
+// odd-even merge network), then log2(THREADS) merge-path rounds double the
+// sorted runs in shared memory: a thread binary-searches where its ITEMS
+// outputs start on the two runs' cross diagonal and merges them serially into
+// registers. Only the keys of the trace (rounded up to ITEMS) take part, so
+// the work follows the trace length, not the class capacity. The shared-memory
+// layout pads one word per 16 so that a thread's ITEMS consecutive keys are
+// stored and loaded without bank conflicts.
+__device__ __forceinline__ uint32_t mpad(uint32_t p) { return p + (p >> 4); }
+
+// Bitonic sorting network over a thread's registers (N a power of two; fixed
+// loop bounds so that it unrolls completely and the array stays in registers).
+template <int N>
+__device__ __forceinline__ void sort_network(uint64_t (&a)[N]) {
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    if (!((vary >> b) & 1u)) continue;
-    const uint32_t bit = (d >> b) & 1u;
-    const uint32_t v = __ballot_sync(0xffffffffu, bit);
-    m &= bit ? v : ~v;
-  }
-  return m;
+  for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int l = i ^ j;
+        if (l <= i) continue;
+        const bool up = (i & k) == 0;
+        const uint64_t x = a[i], y = a[l];
+        const bool sw = up ? x > y : x < y;
+        a[i] = sw ? y : x;
+        a[l] = sw ? x : y;
+      }
 }
 
-// Shared memory of k_sort_seg: the packed keys stay in place; the LSD passes
-// permute 16-bit indices between two buffers (the trace's keys plus both index
-// buffers fit one SM: 128 + 64 KB).
-template <uint32_t CAP, int WARPS>
-struct SegSmem {
-  unsigned long long key[CAP];
-  uint16_t idx[2][CAP];
-  uint16_t wcnt[WARPS][258];  // per-warp digit counts, then per-warp digit offsets (rows padded
-                              // by one word: the digit scan reads them conflict-free)
-};
-
-// One CTA per trace: key = (begin - min) | rank | (span_id - min), packed into
-// 64 bits when the trace's ranges allow (else the trace falls back), then a
-// stable LSD radix sort (8-bit digits, constant digits skipped) of the index
-// permutation: per pass every warp histograms its contiguous segment of the
-// current order, a scan gives each (digit, warp) its output offset, and the
-// warp re-walks its segment placing indices with ballot (multisplit) ranks.
-// Size classes: traces of at most kSegCapSmall spans run as 256-thread CTAs with
-// 52 KB of shared memory (4 per SM), up to kSegCapMid as 512-thread CTAs with
-// 104 KB (2 per SM), longer ones as 1024-thread CTAs with 210 KB.
-// Every launch covers all traces; a CTA leaves traces of the other class.
-template <uint32_t CAP, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_sort_seg(const uint64_t* __restrict__ begin,
-                                                      const uint8_t* __restrict__ flags,
-                                                      const uint64_t* __restrict__ sid,
-                                                      const uint64_t* __restrict__ off, uint32_t min_len,
-                                                      uint32_t* __restrict__ perm, uint32_t* __restrict__ fallback) {
-  constexpr int kSegWarps = THREADS / 32;
-  constexpr uint32_t cap = CAP;
-  // iterations of 32 spans per warp segment (a segment holds <= CAP / kSegWarps)
-  constexpr int kIters = (int)(CAP / (kSegWarps * 32));
-  static_assert(CAP <= 16384, "indices are packed in 14 bits");
-  extern __shared__ __align__(16) unsigned char seg_dyn[];
-  SegSmem<CAP, kSegWarps>& sm = *reinterpret_cast<SegSmem<CAP, kSegWarps>*>(seg_dyn);
-  __shared__ unsigned long long red[4][kSegWarps];
-  __shared__ uint32_t s_shift[2];
-  __shared__ int s_ok;
-  __shared__ unsigned long long s_and, s_or;
-  __shared__ uint32_t s_tot[256];
+template <int THREADS, int ITEMS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_sort_merge(const uint64_t* __restrict__ begin,
+                                                        const uint8_t* __restrict__ flags,
+                                                        const uint64_t* __restrict__ sid,
+                                                        const uint64_t* __restrict__ off, uint32_t min_len,
+                                                        uint32_t* __restrict__ perm,
+                                                        uint32_t* __restrict__ fallback) {
+  constexpr uint32_t CAP = (uint32_t)THREADS * ITEMS;
+  constexpr int kWarps = THREADS / 32;
+  static_assert(CAP <= 16384, "local indices are packed in 14 bits");
+  extern __shared__ __align__(16) unsigned long long mkeys[];  // [mpad(CAP)]
+  __shared__ unsigned long long red[4][kWarps];
+  __shared__ uint32_t s_mode, s_sh_r, s_sh_b;
   const uint32_t t = blockIdx.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint64_t lo = off[t], hi = off[t + 1];
   const uint32_t len = (uint32_t)(hi - lo);
-  if (len < min_len) return;  // the small class sorts it
+  if (len < min_len) return;  // a smaller class sorts it
   if (len <= 1) {
     if (len == 1 && tid == 0) perm[lo] = (uint32_t)lo;
     return;
   }
-  if (len > cap) {
-    if (CAP < kSegCap) return;  // the large class sorts it
+  if (len > CAP) {
+    if (CAP < kSegCap) return;  // a larger class sorts it
     if (tid == 0) atomicOr(fallback, 1u);
     return;
   }
-  // ranges of begin and span_id
+  // ranges of begin and span_id; begin is staged in the key buffer (the loads
+  // of a thread's ITEMS spans are independent and issued together)
   uint64_t bmin = ~0ull, bmax = 0, smin = ~0ull, smax = 0;
-  for (uint32_t j = tid; j < len; j += blockDim.x) {
-    const uint64_t b = begin[lo + j], s = sid[lo + j];
-    bmin = min(bmin, b); bmax = max(bmax, b);
-    smin = min(smin, s); smax = max(smax, s);
+#pragma unroll 8
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t j = tid + k * THREADS;
+    if (j < len) {
+      const uint64_t b = begin[lo + j], s = sid[lo + j];
+      mkeys[mpad(j)] = b;
+      bmin = min(bmin, b); bmax = max(bmax, b);
+      smin = min(smin, s); smax = max(smax, s);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -219,149 +218,113 @@ __global__ void __launch_bounds__(THREADS) k_sort_seg(const uint64_t* __restrict
   }
   __syncthreads();
   if (tid == 0) {
-    for (uint32_t w = 1; w < kSegWarps; ++w) {
+    for (int w = 1; w < kWarps; ++w) {
       red[0][0] = min(red[0][0], red[0][w]); red[1][0] = max(red[1][0], red[1][w]);
       red[2][0] = min(red[2][0], red[2][w]); red[3][0] = max(red[3][0], red[3][w]);
     }
     const uint32_t sb = bit_width64(red[3][0] - red[2][0]);
     const uint32_t bb = bit_width64(red[1][0] - red[0][0]);
-    s_ok = sb + 2 + bb <= 64;
-    s_shift[0] = sb;      // rank field
-    s_shift[1] = sb + 2;  // begin field
-    s_and = ~0ull;
-    s_or = 0;
-    if (!s_ok) atomicOr(fallback, 1u);
+    // mode 0: full keys; 1: (begin, rank, j) + span_id fix-up of equal runs; 2: too wide
+    s_mode = bb + 2 + sb + 14 <= 63 ? 0u : (bb + 2 + 14 <= 63 ? 1u : 2u);
+    s_sh_r = (s_mode == 0 ? sb : 0) + 14;
+    s_sh_b = s_sh_r + 2;
+    if (s_mode == 2) atomicOr(fallback, 1u);
   }
   __syncthreads();
-  if (!s_ok) return;
+  const uint32_t mode = s_mode;
+  if (mode == 2) return;
   bmin = red[0][0];
   smin = red[2][0];
-  const uint32_t sh_r = s_shift[0], sh_b = s_shift[1];
-  unsigned long long kand = ~0ull, kor = 0;
-  for (uint32_t j = tid; j < len; j += blockDim.x) {
-    const uint32_t l = f_level(flags[lo + j]);
-    const uint64_t r = l >= XSP_LEVEL_KERNEL ? 3 : l + 1;  // rank (span.hpp:51-59)
-    const unsigned long long k = ((begin[lo + j] - bmin) << sh_b) | (r << sh_r) | (sid[lo + j] - smin);
-    sm.key[j] = k;
-    sm.idx[0][j] = (uint16_t)j;
-    kand &= k;
-    kor |= k;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    kand &= __shfl_xor_sync(0xffffffffu, kand, o);
-    kor |= __shfl_xor_sync(0xffffffffu, kor, o);
-  }
-  if (lane == 0) {
-    atomicAnd(&s_and, kand);
-    atomicOr(&s_or, kor);
+  const uint32_t sh_r = s_sh_r, sh_b = s_sh_b;
+  const uint32_t n_act = (len + ITEMS - 1) / ITEMS * ITEMS;  // keys taking part (sentinel-padded)
+#pragma unroll 8
+  for (int q = 0; q < ITEMS; ++q) {
+    const uint32_t j = tid + q * THREADS;
+    if (j >= n_act) continue;
+    uint64_t k = ~0ull;
+    if (j < len) {
+      const uint32_t l = f_level(flags[lo + j]);
+      const uint64_t r = l >= XSP_LEVEL_KERNEL ? 3 : l + 1;  // rank (span.hpp:51-59)
+      k = ((mkeys[mpad(j)] - bmin) << sh_b) | (r << sh_r) | j;
+      if (mode == 0) k |= (sid[lo + j] - smin) << 14;
+    }
+    mkeys[mpad(j)] = k;
   }
   __syncthreads();
-  const unsigned long long varying = s_and ^ s_or;
-  // warp w owns positions [w * seg, (w + 1) * seg) of the current order
-  const uint32_t seg = ((len + kSegWarps - 1) / kSegWarps + 31) & ~31u;
-  const uint32_t p0 = min(len, warp * seg), p1 = min(len, p0 + seg);
-  int cur = 0;
-  for (int shift = 0; shift < 64; shift += 8) {
-    if (!((varying >> shift) & 0xFFull)) continue;
-    const uint16_t* src = sm.idx[cur];
-    uint16_t* dst = sm.idx[cur ^ 1];
-    for (uint32_t d = lane; d < 256; d += 32) sm.wcnt[warp][d] = 0;
-    __syncwarp();
-    // histogram of the warp's segment; every lane keeps, per iteration, its
-    // index, digit, rank among equal digits and whether it is the last of them
-    // (packed: x | d << 14 | below << 22 | last << 27 | valid << 28), so the
-    // scatter needs neither the keys nor the ballots again
-    const uint32_t vary = (uint32_t)(varying >> shift) & 0xFFu;
-    uint32_t pk[kIters];
+  const uint32_t my0 = tid * ITEMS;
+  const bool active = my0 < n_act;
+  uint64_t v[ITEMS];
+  if (active) {
 #pragma unroll
-    for (int it = 0; it < kIters; ++it) {
-      pk[it] = 0;
-      const uint32_t base = p0 + 32u * it;
-      if (base >= p1) continue;  // warp-uniform
-      const uint32_t i = base + lane;
-      const bool v = i < p1;
-      const uint32_t valid = __ballot_sync(0xffffffffu, v);
-      const uint32_t x = v ? src[i] : 0u;
-      const uint32_t d = v ? (uint32_t)(sm.key[x] >> shift) & 0xFFu : 0u;
-      const uint32_t peers = digit_peers(d, valid, vary);
-      const uint32_t below = __popc(peers & lanemask_lt());
-      const bool last = (peers >> lane) <= 1u;  // no equal digit in a higher lane
-      if (v && last) sm.wcnt[warp][d] += (uint16_t)(below + 1);
-      __syncwarp();
-      if (v) pk[it] = x | d << 14 | below << 22 | (uint32_t)last << 27 | 1u << 28;
-    }
-    __syncthreads();
-    // per digit: totals and the exclusive offsets of the warps (digit-major);
-    // kDP consecutive threads share a digit, each scanning kSegWarps / kDP warps
-    {
-      constexpr int kDP = THREADS >= 256 ? THREADS / 256 : 1;
-      constexpr int kWPT = kSegWarps / kDP;
-      static_assert(kSegWarps % kDP == 0, "warps per digit thread");
-      const uint32_t d = tid / kDP, q = tid % kDP;
-      if (d < 256) {
-        uint32_t c[kWPT], sum = 0;
-#pragma unroll
-        for (int w = 0; w < kWPT; ++w) {
-          c[w] = sm.wcnt[q * kWPT + w][d];
-          sum += c[w];
-        }
-        uint32_t inc = sum;
-#pragma unroll
-        for (int o = 1; o < kDP; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o, kDP);
-          if (q >= (uint32_t)o) inc += y;
-        }
-        uint32_t run = inc - sum;
-#pragma unroll
-        for (int w = 0; w < kWPT; ++w) {
-          sm.wcnt[q * kWPT + w][d] = (uint16_t)run;
-          run += c[w];
-        }
-        if (q == kDP - 1) s_tot[d] = inc;
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan of the 256 digit totals (8 per lane)
-      uint32_t v[8], sum = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        v[q] = s_tot[lane * 8 + q];
-        sum += v[q];
-      }
-      uint32_t incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-      }
-      uint32_t run = incl - sum;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        s_tot[lane * 8 + q] = run;
-        run += v[q];
-      }
-    }
-    __syncthreads();
-    // stable scatter: digit start + earlier warps + running rank in this warp
-#pragma unroll
-    for (int it = 0; it < kIters; ++it) {
-      if (p0 + 32u * it >= p1) continue;  // warp-uniform
-      const uint32_t u = pk[it];
-      const bool v = (u >> 28) & 1u;
-      const uint32_t x = u & 0x3FFFu, d = (u >> 14) & 0xFFu, below = (u >> 22) & 31u;
-      const uint32_t r0 = v ? sm.wcnt[warp][d] : 0u;
-      __syncwarp();
-      if (v) {
-        dst[s_tot[d] + r0 + below] = (uint16_t)x;
-        if ((u >> 27) & 1u) sm.wcnt[warp][d] = (uint16_t)(r0 + below + 1);
-      }
-      __syncwarp();
-    }
-    __syncthreads();
-    cur ^= 1;
+    for (int k = 0; k < ITEMS; ++k) v[k] = mkeys[mpad(my0 + k)];
+    sort_network(v);
   }
-  for (uint32_t j = tid; j < len; j += blockDim.x) perm[lo + j] = (uint32_t)(lo + sm.idx[cur][j]);
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) mkeys[mpad(my0 + k)] = v[k];
+  }
+  for (uint32_t w = ITEMS; w < n_act; w <<= 1) {
+    __syncthreads();
+    if (active) {
+      const uint32_t g0 = my0 / (2 * w) * (2 * w);
+      const uint32_t a0 = g0, a1 = min(g0 + w, n_act), b1 = min(g0 + 2 * w, n_act);
+      const uint32_t na = a1 - a0, nb = b1 - a1, d = my0 - g0;
+      // merge path: i keys of A and d - i of B precede this thread's outputs
+      uint32_t l = d > nb ? d - nb : 0, h = min(d, na);
+      while (l < h) {
+        const uint32_t m = (l + h) >> 1;
+        if (mkeys[mpad(a0 + m)] < mkeys[mpad(a1 + d - 1 - m)]) l = m + 1; else h = m;
+      }
+      uint32_t ia = a0 + l, ib = a1 + (d - l);
+      uint64_t xa = ia < a1 ? mkeys[mpad(ia)] : ~0ull, xb = ib < b1 ? mkeys[mpad(ib)] : ~0ull;
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        // branch-free step: one load from the side that advanced
+        const bool ta = xa < xb;
+        v[k] = ta ? xa : xb;
+        ia += ta;
+        ib += !ta;
+        const uint32_t nx = ta ? ia : ib;
+        const bool in = ta ? ia < a1 : ib < b1;
+        const uint64_t y = in ? mkeys[mpad(nx)] : ~0ull;
+        xa = ta ? y : xa;
+        xb = ta ? xb : y;
+      }
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) mkeys[mpad(my0 + k)] = v[k];
+    }
+  }
+  __syncthreads();
+  if (mode == 1) {
+    // runs of equal (begin, rank): order by span_id, stably (j ascends in a run)
+    for (uint32_t p = tid; p < len; p += THREADS) {
+      const uint64_t kp = mkeys[mpad(p)] >> 14;
+      if (p > 0 && (mkeys[mpad(p - 1)] >> 14) == kp) continue;  // not a run start
+      uint32_t e = p + 1;
+      while (e < len && (mkeys[mpad(e)] >> 14) == kp) ++e;
+      if (e - p < 2) continue;
+      if (e - p > 1024) {  // pathological tie run: the global sort handles the batch
+        atomicOr(fallback, 1u);
+        continue;
+      }
+      for (uint32_t q = p + 1; q < e; ++q) {  // insertion by span_id
+        const uint64_t kq = mkeys[mpad(q)];
+        const uint64_t sq = sid[lo + (kq & 0x3FFFu)];
+        uint32_t r = q;
+        while (r > p && sid[lo + (mkeys[mpad(r - 1)] & 0x3FFFu)] > sq) {
+          mkeys[mpad(r)] = mkeys[mpad(r - 1)];
+          --r;
+        }
+        mkeys[mpad(r)] = kq;
+      }
+    }
+    __syncthreads();
+  }
+  for (uint32_t j = tid; j < len; j += THREADS) perm[lo + j] = (uint32_t)(lo + (mkeys[mpad(j)] & 0x3FFFu));
 }
 
 }  // namespace
@@ -381,18 +344,20 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
   if (*was_sorted || n <= 1) return;
   // per-trace CTA sort; the global radix sort only if some trace does not fit
   XSP_CUDA(cudaMemsetAsync(flag, 0, 4, st));
-  auto* k_small = k_sort_seg<kSegCapSmall, 256>;
-  auto* k_mid = k_sort_seg<kSegCapMid, 512>;
-  auto* k_large = k_sort_seg<kSegCap, 1024>;
-  constexpr size_t smem_small = sizeof(SegSmem<kSegCapSmall, 8>), smem_mid = sizeof(SegSmem<kSegCapMid, 16>),
-                   smem_large = sizeof(SegSmem<kSegCap, 32>);
-  XSP_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small));
-  XSP_CUDA(cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mid));
-  XSP_CUDA(cudaFuncSetAttribute(k_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_large));
   ctx->stage_begin("sort", st);
-  k_small<<<T, 256, smem_small, st>>>(begin, flags, sid, off, 0, perm, flag);
-  k_mid<<<T, 512, smem_mid, st>>>(begin, flags, sid, off, kSegCapSmall + 1, perm, flag);
-  k_large<<<T, 1024, smem_large, st>>>(begin, flags, sid, off, kSegCapMid + 1, perm, flag);
+  // register budgets sized for 4 / 2 / 1 resident CTAs per SM
+  auto* k_small = k_sort_merge<256, 16, 4>;
+  auto* k_mid = k_sort_merge<512, 16, 2>;
+  auto* k_large = k_sort_merge<512, 32, 1>;
+  auto smem = [](uint32_t cap) { return (size_t)(cap + cap / 16) * 8; };
+  XSP_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(kSegCapSmall)));
+  XSP_CUDA(cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(kSegCapMid)));
+  XSP_CUDA(cudaFuncSetAttribute(k_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(kSegCap)));
+  for (const void* f : {(const void*)k_small, (const void*)k_mid, (const void*)k_large})
+    XSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  k_small<<<T, 256, smem(kSegCapSmall), st>>>(begin, flags, sid, off, 0, perm, flag);
+  k_mid<<<T, 512, smem(kSegCapMid), st>>>(begin, flags, sid, off, kSegCapSmall + 1, perm, flag);
+  k_large<<<T, 512, smem(kSegCap), st>>>(begin, flags, sid, off, kSegCapMid + 1, perm, flag);
   ctx->stage_end("sort", st);
   ctx->launches += 3;
   XSP_CUDA(cudaMemcpyAsync(h, flag, 4, cudaMemcpyDeviceToHost, st));

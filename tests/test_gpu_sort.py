@@ -110,3 +110,46 @@ def test_size_classes_boundaries(engine):
     perm, was = engine.sort_timeline(b)
     assert not was
     assert np.array_equal(perm, expected_perm(b))
+
+
+def _batch(lens, beg, sid, flags):
+    n = sum(lens)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    return SpanBatch(span_id=sid, parent_id=np.zeros(n, np.uint64), begin_ns=beg, end_ns=beg + 5,
+                     cid=np.zeros(n, np.uint64), flags=flags, name_id=np.zeros(n, np.uint32),
+                     flops=np.zeros(0, np.uint64), dram_read=np.zeros(0, np.uint64),
+                     dram_write=np.zeros(0, np.uint64), occupancy=np.zeros(0), alloc_bytes=np.zeros(0, np.int64),
+                     type_id=np.zeros(0, np.uint32), trace_span_off=off, trace_id=np.arange(len(lens)),
+                     trace_levels=np.full(len(lens), 7), trace_batch=np.ones(len(lens)),
+                     trace_run=np.zeros(len(lens)), trace_serialized=np.zeros(len(lens)), names=[b"x"], types=[])
+
+
+def test_wide_span_ids_tie_runs(engine):
+    """span_id ranges too wide to pack beside begin (random 64-bit ids): keys
+    carry (begin, rank, index) and runs of equal (begin, rank) are ordered by
+    span_id afterwards; duplicate span_ids stay in input order."""
+    rng = np.random.default_rng(8)
+    lens = [300, 5000, 9000, 40, 1]
+    n = sum(lens)
+    beg = rng.integers(10 ** 12, 10 ** 12 + 400, n).astype(np.uint64)
+    sid = rng.integers(0, 2 ** 63, n).astype(np.uint64)
+    sid[::7] = sid[1::7][: len(sid[::7])]  # duplicates
+    b = _batch(lens, beg, sid, rng.integers(0, 4, n).astype(np.uint8))
+    perm, was = engine.sort_timeline(b)
+    assert not was
+    assert np.array_equal(perm, expected_perm(b))
+
+
+def test_long_tie_run_falls_back(engine):
+    """A run of > 1024 spans with equal (begin, rank) and wide span_ids takes the
+    global radix sort."""
+    rng = np.random.default_rng(9)
+    lens = [3000, 200]
+    n = sum(lens)
+    beg = np.full(n, 7, np.uint64)
+    beg[3000:] = rng.integers(0, 50, 200).astype(np.uint64)
+    sid = rng.integers(0, 2 ** 63, n).astype(np.uint64)
+    b = _batch(lens, beg, sid, np.full(n, 2, np.uint8))
+    perm, was = engine.sort_timeline(b)
+    assert not was
+    assert np.array_equal(perm, expected_perm(b))
