@@ -1171,10 +1171,12 @@ __global__ void k_join_counts(const uint32_t* __restrict__ t_kl_off, const uint3
   if (mismatch) *any_slow = 1;
 }
 
+// t_nomono[t] = 1 when some kernel-list entry of t is not a cid launch or its cid
+// does not exceed the previous entry's (the direct-address join needs both).
 __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const ExEnt* __restrict__ ex,
                              const uint8_t* __restrict__ flags, const uint32_t* __restrict__ t_kl_off,
                              const uint32_t* __restrict__ t_ex_off, uint32_t T, uint32_t* __restrict__ t_slow,
-                             uint32_t* __restrict__ any_slow) {
+                             uint32_t* __restrict__ any_slow, uint32_t* __restrict__ t_nomono) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t first = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
   if (first >= nkl) return;
@@ -1183,13 +1185,51 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
   const uint32_t r = k - t_kl_off[t];
   const KlEnt ent = kl[k];
   const uint8_t f = flags[ent.row];
-  bool ok = !t_slow[t] && f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID);
+  const bool mono = f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID) && (r == 0 || kl[k - 1].cid < ent.cid);
+  if (!mono) t_nomono[t] = 1;
+  bool ok = mono && !t_slow[t];
   if (ok) ok = ex[t_ex_off[t] + r].cid == ent.cid;
-  if (ok && r > 0) ok = kl[k - 1].cid < ent.cid;
   if (!ok) {
     t_slow[t] = 1;
     *any_slow = 1;
   }
+}
+
+// Direct-address join for slow traces whose launches carry strictly increasing
+// cids over a dense range (e.g. executions reordered across streams): the slot
+// of a cid is cid - lmin, with no hashing or probing. t_lmin[t] = the first
+// launch cid, or ~0 when t uses the hash table.
+__global__ void k_join_direct(const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_slow,
+                              const uint32_t* __restrict__ t_nomono, const KlEnt* __restrict__ kl, uint32_t T,
+                              uint64_t* __restrict__ t_lmin, uint64_t* __restrict__ t_lmax) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const uint32_t k0 = t_kl_off[t], k1 = t_kl_off[t + 1];
+  uint64_t lmin = ~0ull, lmax = 0;
+  if (t_slow[t] && !t_nomono[t] && k1 > k0) {
+    const uint64_t a = kl[k0].cid, b = kl[k1 - 1].cid;
+    if (b - a < 4ull * (k1 - k0) + 64) {
+      lmin = a;
+      lmax = b;
+    }
+  }
+  t_lmin[t] = lmin;
+  t_lmax[t] = lmax;
+}
+
+// An exec whose cid lies outside its direct trace's launch range matches no
+// launch but may still duplicate another exec: that trace uses the hash table.
+__global__ void k_join_far(uint32_t nex, const ExEnt* __restrict__ ex, const uint32_t* __restrict__ t_ex_off,
+                           uint32_t T, uint64_t* __restrict__ t_lmin, const uint64_t* __restrict__ t_lmax) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t first = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  if (first >= nex) return;
+  const uint32_t t = warp_trace_of(t_ex_off, T, x < nex ? x : nex - 1, first);
+  if (x >= nex) return;
+  const uint64_t lmin = t_lmin[t];
+  if (lmin == ~0ull) return;
+  const uint64_t c = ex[x].cid;
+  if (c < lmin || c > t_lmax[t]) t_lmin[t] = ~0ull;
 }
 
 __device__ __forceinline__ uint32_t mix32(uint64_t x) {
@@ -1202,9 +1242,14 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
 }
 
 __global__ void k_region_size(const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
-                              const uint32_t* __restrict__ t_slow, uint32_t T, uint64_t* __restrict__ rsize) {
+                              const uint32_t* __restrict__ t_slow, const uint64_t* __restrict__ t_lmin,
+                              const uint64_t* __restrict__ t_lmax, uint32_t T, uint64_t* __restrict__ rsize) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
+  if (t_lmin[t] != ~0ull) {  // direct-address region: one slot per cid of the launch range
+    rsize[t] = t_lmax[t] - t_lmin[t] + 1;
+    return;
+  }
   uint64_t items = (uint64_t)(t_kl_off[t + 1] - t_kl_off[t]) + (t_ex_off[t + 1] - t_ex_off[t]);
   uint64_t s = 16;
   while (s < items * 2) s <<= 1;
@@ -1218,6 +1263,7 @@ struct JoinArgs {
   const uint32_t* t_ex_off;
   const uint32_t* t_kl_off;
   const uint32_t* t_slow;
+  const uint64_t* t_lmin;  // direct-address traces: first launch cid, else ~0
   uint32_t T;
   uint32_t n_ex, n_kl;
   const uint64_t* roff;  // region offsets [T+1]
@@ -1250,9 +1296,10 @@ __global__ void k_join_insert(JoinArgs a) {
     cid = a.kl[k].cid;
   }
   const uint64_t base = a.roff[t];
+  const uint64_t lmin = a.t_lmin[t];
   const uint32_t mask = (uint32_t)(a.roff[t + 1] - base - 1);
-  uint32_t h = mix32(cid) & mask;
-  for (;;) {
+  uint32_t h = lmin != ~0ull ? (uint32_t)(cid - lmin) : mix32(cid) & mask;
+  for (; lmin == ~0ull;) {
     uint32_t* slot = a.owner + base + h;
     uint32_t o = *((volatile uint32_t*)slot);
     if (o == 0) {
@@ -1939,15 +1986,17 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   j.t_ex_off = a.t_ex_off;
   j.t_kl_off = a.t_kl_off;
   uint32_t* t_slow = ctx->d<uint32_t>("c.t_slow", T + 1);
+  uint32_t* t_nomono = ctx->d<uint32_t>("c.t_nomono", T + 1);
   j.t_slow = t_slow;
   j.T = T;
   j.n_ex = nex;
   j.n_kl = nkl;
   uint32_t any_slow = 0;
   if (!parents_only) {
+    XSP_CUDA(cudaMemsetAsync(t_nomono, 0, (T + 1) * 4ull, st));
     launch(ctx, k_join_counts, T, st, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
     launch(ctx, k_join_check, nkl, st, nkl, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, t_slow,
-           counters + 7);
+           counters + 7, t_nomono);
     any_slow = read_u32(ctx, counters + 7, st);
   }
   auto* dup_ex = ctx->d<unsigned long long>("c.dup_ex", T);
@@ -1959,7 +2008,16 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   if (any_slow) {
     uint64_t* rsize = ctx->d<uint64_t>("c.rsize", T + 1);
     uint64_t* roff = ctx->d<uint64_t>("c.roff", T + 1);
-    launch(ctx, k_region_size, T, st, a.t_kl_off, a.t_ex_off, t_slow, T, rsize);
+    uint64_t* t_lmin = ctx->d<uint64_t>("c.t_lmin", T + 1);
+    uint64_t* t_lmax = ctx->d<uint64_t>("c.t_lmax", T + 1);
+    if (getenv("XSP_JOIN_HASH")) {
+      XSP_CUDA(cudaMemsetAsync(t_lmin, 0xFF, (T + 1) * 8ull, st));
+    } else {
+      launch(ctx, k_join_direct, T, st, a.t_kl_off, t_slow, t_nomono, a.kl, T, t_lmin, t_lmax);
+      launch(ctx, k_join_far, nex, st, nex, a.ex, a.t_ex_off, T, t_lmin, t_lmax);
+    }
+    j.t_lmin = t_lmin;
+    launch(ctx, k_region_size, T, st, a.t_kl_off, a.t_ex_off, t_slow, t_lmin, t_lmax, T, rsize);
     uint64_t* scan64 = ctx->d<uint64_t>("c.scan64", scan_scratch_elems(T + 1));
     exclusive_scan<uint64_t, uint64_t>(rsize, roff, T, scan64, roff + T, st, &ctx->launches);
     uint64_t* hroff = ctx->h<uint64_t>("c.roff_h", 1);

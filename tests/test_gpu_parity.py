@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import cases
-from builders import API, KERNEL, LAYER, MLG, MODEL, batch_of
+from builders import API, EXEC, KERNEL, LAUNCH, LAYER, MLG, MODEL, batch_of, span
 from oracle import ref
 from parity import compare_correlation, compare_tables, topk_oracle
 
@@ -213,3 +213,47 @@ def test_orphan_heavy_batch_retries_with_larger_lists(engine, has_ref):
     assert corr.n_orphans > b.n_spans // 16 + 4096
     ra, rs = ref.correlate(b)
     compare_correlation(b, corr, ra, rs)
+
+
+def _async_trace(n, cids, exec_order, extra=()):
+    """Model + one layer + n launches carrying `cids`; their executions in
+    `exec_order` (a permutation: executions on interleaved streams), plus extra
+    exec spans (cid, ...)."""
+    sp = [span(1, MODEL, 0, 10 ** 7), span(2, LAYER, 10, 10 ** 6)]
+    for i in range(n):
+        sp.append(span(10 + i, KERNEL, 100 + 10 * i, 101 + 10 * i, kind=LAUNCH, cid=int(cids[i])))
+    for j, i in enumerate(exec_order):
+        sp.append(span(10 ** 5 + i, KERNEL, 2 * 10 ** 6 + 7 * j, 2 * 10 ** 6 + 7 * j + 3, kind=EXEC,
+                       cid=int(cids[i])))
+    for q, c in enumerate(extra):
+        sp.append(span(10 ** 6 + q, KERNEL, 3 * 10 ** 6 + 5 * q, 3 * 10 ** 6 + 5 * q + 2, kind=EXEC, cid=int(c)))
+    return sp
+
+
+def test_cid_join_direct_and_hash_regions(engine, has_ref, monkeypatch):
+    """Slow (not merge-aligned) traces: dense increasing launch cids take the
+    direct-address join, the rest the hash table; results equal the reference
+    and the all-hash run, including duplicate-exec errors and far leftovers."""
+    rng = np.random.default_rng(3)
+    n = 300
+    dense = np.arange(1000, 1000 + n)
+    sparse = np.sort(rng.choice(10 ** 9, n, replace=False))
+    shuffled = rng.permutation(n)
+    traces = [
+        _async_trace(n, dense, shuffled),                            # direct
+        _async_trace(n, dense, shuffled, extra=[1100]),              # direct, duplicate exec cid -> error
+        _async_trace(n, dense, shuffled, extra=[5, 10 ** 8]),        # far execs -> hash, leftovers
+        _async_trace(n, dense, shuffled, extra=[7, 7]),              # far duplicate -> hash, error
+        _async_trace(n, sparse, shuffled),                           # range too wide -> hash
+        _async_trace(n, dense[::-1].copy(), shuffled),               # decreasing launch cids -> hash
+        _async_trace(n, dense, np.arange(n)),                        # merge-aligned fast path
+    ]
+    b = batch_of(traces)
+    corr, _ = engine.run_host(b)
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+    assert list(corr.trace_status)[:4] == [0, 4, 0, 4]
+    monkeypatch.setenv("XSP_JOIN_HASH", "1")
+    c2, _ = engine.run_host(b)
+    for k in corr.cols:
+        assert np.array_equal(np.asarray(corr.cols[k]), np.asarray(c2.cols[k])), k
