@@ -987,14 +987,10 @@ struct NameBigArgs {
   int8_t* s_bound;
 };
 
-__global__ void __launch_bounds__(32) k_names_big(NameBigArgs a) {
-  __shared__ NameTable T;
-  const uint32_t g = blockIdx.x, lane = threadIdx.x;
-  if (!(a.gkc_off[g + 1] > a.gkc_off[g])) return;
-  if (a.gstatus[g] != XSP_G_OK) {
-    if (lane == 0) a.g_count[g] = 0;
-    return;
-  }
+// Folds chunk tables [c0, c1) in order into T (one warp). Returns true when
+// more than NCAP distinct names appear.
+__device__ __forceinline__ bool fold_name_chunks(NameTable& T, const NameBigArgs& a, uint32_t c0, uint32_t c1,
+                                                 uint32_t lane) {
   for (uint32_t s = lane; s < NCAP; s += 32) {
     T.key[s] = NEMPTY;
     T.lat[s] = T.occw[s] = 0.0;
@@ -1003,7 +999,7 @@ __global__ void __launch_bounds__(32) k_names_big(NameBigArgs a) {
   if (lane == 0) T.nused = 0;
   __syncwarp();
   bool over = false;
-  for (uint32_t c = a.gkc_off[g]; c < a.gkc_off[g + 1]; ++c) {
+  for (uint32_t c = c0; c < c1; ++c) {
     const uint32_t nc = a.c_count[c];
     for (uint32_t e = lane; e < nc; e += 32) {
       const uint64_t o = (uint64_t)c * NCAP + e;
@@ -1030,17 +1026,70 @@ __global__ void __launch_bounds__(32) k_names_big(NameBigArgs a) {
       T.r[h] += a.c_r[o];
       T.w[h] += a.c_w[o];
     }
-    if (__any_sync(0xffffffffu, over)) break;
+    if (__any_sync(0xffffffffu, over)) return true;
     __syncwarp();
   }
-  if (__any_sync(0xffffffffu, over)) {
+  __syncwarp();
+  return false;
+}
+
+// First level of a long group's fold: partial p folds the chunk tables
+// [pc0[p], pc1[p]) (consecutive chunks of one group) into one table of the
+// chunk layout, so that k_names_big folds ~1/kNamePart as many tables
+// serially. Integer latencies stay exact; the occupancy-weighted sums are
+// re-associated (within 1e-12, as for the chunks themselves).
+constexpr uint32_t kNamePart = 32;
+struct NamePartOut {
+  uint32_t* count;
+  uint32_t* name;
+  uint64_t* cnt;
+  double* lat;
+  double* occw;
+  uint64_t* f;
+  uint64_t* r;
+  uint64_t* w;
+};
+__global__ void __launch_bounds__(32) k_names_partial(NameBigArgs a, const uint32_t* __restrict__ pc0,
+                                                      const uint32_t* __restrict__ pc1, NamePartOut o) {
+  __shared__ NameTable T;
+  const uint32_t p = blockIdx.x, lane = threadIdx.x;
+  if (fold_name_chunks(T, a, pc0[p], pc1[p], lane)) {
+    if (lane == 0) {
+      o.count[p] = 0;
+      atomicOr(a.overflow, 1u);
+    }
+    return;
+  }
+  const uint32_t nu = T.nused;
+  for (uint32_t u = lane; u < nu; u += 32) {
+    const uint32_t sl = T.used[u];
+    const uint64_t q = (uint64_t)p * NCAP + u;
+    o.name[q] = T.key[sl];
+    o.cnt[q] = T.cnt[sl];
+    o.lat[q] = T.lat[sl];
+    o.occw[q] = T.occw[sl];
+    o.f[q] = T.f[sl];
+    o.r[q] = T.r[sl];
+    o.w[q] = T.w[sl];
+  }
+  if (lane == 0) o.count[p] = nu;
+}
+
+__global__ void __launch_bounds__(32) k_names_big(NameBigArgs a) {
+  __shared__ NameTable T;
+  const uint32_t g = blockIdx.x, lane = threadIdx.x;
+  if (!(a.gkc_off[g + 1] > a.gkc_off[g])) return;
+  if (a.gstatus[g] != XSP_G_OK) {
+    if (lane == 0) a.g_count[g] = 0;
+    return;
+  }
+  if (fold_name_chunks(T, a, a.gkc_off[g], a.gkc_off[g + 1], lane)) {
     if (lane == 0) {
       a.g_count[g] = 0;
       atomicOr(a.overflow, 1u);
     }
     return;
   }
-  __syncwarp();
   const uint32_t nu = T.nused;
   const double mlat = a.m_lat[g];
   for (uint32_t u = lane; u < nu; u += 32) {
@@ -1433,10 +1482,25 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   }
   glc[G] = nkc + nlc;
   const uint32_t n_chunks = nkc + nlc;
+  // partial folds of the chunk tables (k_names_partial): kNamePart consecutive
+  // chunks of one group each; [pc0 | pc1] ranges and per-group partial offsets
+  std::vector<uint32_t> pk_rng, pl_rng, pk_off(G + 1, 0), pl_off(G + 1, 0);
+  for (uint32_t g = 0; g < G; ++g) {
+    pk_off[g] = (uint32_t)(pk_rng.size() / 2);
+    for (uint32_t c = gkc[g]; c < gkc[g + 1]; c += kNamePart)
+      pk_rng.insert(pk_rng.end(), {c, std::min(c + kNamePart, gkc[g + 1])});
+    pl_off[g] = (uint32_t)(pl_rng.size() / 2);
+    for (uint32_t c = glc[g] - nkc; c < glc[g + 1] - nkc; c += kNamePart)
+      pl_rng.insert(pl_rng.end(), {c, std::min(c + kNamePart, glc[g + 1] - nkc)});
+  }
+  const uint32_t npk = (uint32_t)(pk_rng.size() / 2), npl = (uint32_t)(pl_rng.size() / 2);
+  pk_off[G] = npk;
+  pl_off[G] = npl;
   uint32_t *d_desc = nullptr, *d_gkc = nullptr, *d_glc = nullptr, *d_kcb = nullptr, *d_kce = nullptr;
   uint32_t *d_lcb = nullptr, *d_lce = nullptr, *d_glc_rel = nullptr;
+  uint32_t *d_pk = nullptr, *d_pk_off = nullptr, *d_pl = nullptr, *d_pl_off = nullptr;
   if (n_chunks) {
-    const size_t words = desc.size() + 3ull * (G + 1) + 2ull * nkc + 2ull * nlc;
+    const size_t words = desc.size() + 3ull * (G + 1) + 2ull * nkc + 2ull * nlc + 2ull * (npk + npl) + 2ull * (G + 1);
     uint32_t* hd = ctx->h<uint32_t>("a.big_h", words);
     std::memcpy(hd, desc.data(), desc.size() * 4);
     std::memcpy(hd + desc.size(), gkc.data(), (G + 1) * 4ull);
@@ -1453,6 +1517,18 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     }
     uint32_t* grel = lcb + 2ull * nlc;
     for (uint32_t g = 0; g <= G; ++g) grel[g] = glc[g] - nkc;
+    uint32_t* hp = grel + G + 1;  // [pk0 | pk1 | pk_off | pl0 | pl1 | pl_off]
+    for (uint32_t q = 0; q < npk; ++q) {
+      hp[q] = pk_rng[2 * q];
+      hp[npk + q] = pk_rng[2 * q + 1];
+    }
+    std::memcpy(hp + 2ull * npk, pk_off.data(), (G + 1) * 4ull);
+    uint32_t* hq = hp + 2ull * npk + G + 1;
+    for (uint32_t q = 0; q < npl; ++q) {
+      hq[q] = pl_rng[2 * q];
+      hq[npl + q] = pl_rng[2 * q + 1];
+    }
+    std::memcpy(hq + 2ull * npl, pl_off.data(), (G + 1) * 4ull);
     uint32_t* dd = ctx->d<uint32_t>("a.big", words);
     XSP_CUDA(cudaMemcpyAsync(dd, hd, words * 4, cudaMemcpyHostToDevice, st));
     d_desc = dd;
@@ -1463,7 +1539,40 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     d_lcb = d_kce + nkc;
     d_lce = d_lcb + nlc;
     d_glc_rel = d_lce + nlc;
+    d_pk = d_glc_rel + G + 1;
+    d_pk_off = d_pk + 2ull * npk;
+    d_pl = d_pk_off + G + 1;
+    d_pl_off = d_pl + 2ull * npl;
   }
+  // a long group's chunk tables: partial folds, then the ordered fold + ranking
+  auto fold_big = [&](NameBigArgs nb, const uint32_t* d_rng, const uint32_t* d_poff, uint32_t np,
+                      const std::string& tag) {
+    if (np) {
+      const uint64_t cap = (uint64_t)np * NCAP;
+      NamePartOut po;
+      po.count = ctx->d<uint32_t>(tag + ".count", np);
+      po.name = ctx->d<uint32_t>(tag + ".name", cap);
+      po.cnt = ctx->d<uint64_t>(tag + ".cnt", cap);
+      po.lat = ctx->d<double>(tag + ".lat", cap);
+      po.occw = ctx->d<double>(tag + ".occw", cap);
+      po.f = ctx->d<uint64_t>(tag + ".f", cap);
+      po.r = ctx->d<uint64_t>(tag + ".r", cap);
+      po.w = ctx->d<uint64_t>(tag + ".w", cap);
+      k_names_partial<<<np, 32, 0, st>>>(nb, d_rng, d_rng + np, po);
+      ++ctx->launches;
+      nb.gkc_off = d_poff;
+      nb.c_count = po.count;
+      nb.c_name = po.name;
+      nb.c_cnt = po.cnt;
+      nb.c_lat = po.lat;
+      nb.c_occw = po.occw;
+      nb.c_f = po.f;
+      nb.c_r = po.r;
+      nb.c_w = po.w;
+    }
+    k_names_big<<<G, 32, 0, st>>>(nb);
+    ++ctx->launches;
+  };
   launch(ctx, k_group_check_runs, total_runs, st, ga, total_runs, run_off);
   launch(ctx, k_group_check_layers, TL, st, ga, TL, out->group_layer_off);
   out->group_status = ctx->d<int32_t>("t.g_status", G);
@@ -1706,8 +1815,8 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       yb.s_ai = ty.s_ai;
       yb.s_tput = ty.s_tput;
       yb.s_bound = ty.s_bound;
-      k_names_big<<<G, 32, 0, st>>>(yb);
-      ctx->launches += 2;
+      fold_big(yb, d_pl, d_pl_off, npl, "a.yp");
+      ++ctx->launches;
     }
     exclusive_scan<uint32_t, uint32_t>(ty.g_count, out->group_type_off, G, scan_tmp, out->group_type_off + G, st,
                                        &ctx->launches);
@@ -1830,8 +1939,8 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       nb.s_ai = nf.s_ai;
       nb.s_tput = nf.s_tput;
       nb.s_bound = nf.s_bound;
-      k_names_big<<<G, 32, 0, st>>>(nb);
-      ctx->launches += 2;
+      fold_big(nb, d_pk, d_pk_off, npk, "a.np");
+      ++ctx->launches;
     }
     exclusive_scan<uint32_t, uint32_t>(nf.g_count, out->group_name_off, G, scan_tmp, out->group_name_off + G, st,
                                        &ctx->launches);
