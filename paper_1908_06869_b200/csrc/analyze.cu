@@ -871,8 +871,44 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
   }
   __syncthreads();
   // pass D: one thread per name walks that name's kernels in tree order
-  // (Accumulator::add, analysis.cpp:181-188); the u64 counters ride along (exact)
-  for (uint32_t u = tid; u < nu; u += blockDim.x) {
+  // (Accumulator::add, analysis.cpp:181-188); the u64 counters ride along (exact).
+  // Raw mode (a chunk of a long group, whose sums are re-associated at chunk
+  // boundaries anyway): one warp per name, lane-strided partial sums and a
+  // fixed xor-butterfly, so a frequent name no longer serialises the chunk.
+  if (a.raw) {
+    for (uint32_t u = warp; u < nu; u += NAME_WARPS) {
+      const uint32_t s = T.used[u];
+      const uint32_t b = k0 + T.start[s], n = (uint32_t)T.cnt[s];
+      double lat = 0.0, occw = 0.0;
+      unsigned long long f = 0, rd = 0, wr = 0;
+#pragma unroll 4
+      for (uint32_t i = lane; i < n; i += 32) {
+        const uint32_t x = sm_ok ? k0 + s_perm[b - k0 + i] : a.perm[b + i];
+        const double l = a.k_lat[x];
+        lat = __dadd_rn(lat, l);
+        occw = __dadd_rn(occw, __dmul_rn(a.k_occ ? a.k_occ[x] : 0.0, l));
+        f += a.k_flops[x];
+        if (a.k_read) rd += a.k_read[x];
+        if (a.k_write) wr += a.k_write[x];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lat = __dadd_rn(lat, __shfl_xor_sync(0xffffffffu, lat, o));
+        occw = __dadd_rn(occw, __shfl_xor_sync(0xffffffffu, occw, o));
+        f += __shfl_xor_sync(0xffffffffu, f, o);
+        rd += __shfl_xor_sync(0xffffffffu, rd, o);
+        wr += __shfl_xor_sync(0xffffffffu, wr, o);
+      }
+      if (lane == 0) {
+        T.lat[s] = lat;
+        T.occw[s] = occw;
+        T.f[s] = f;
+        T.r[s] = rd;
+        T.w[s] = wr;
+      }
+    }
+  }
+  for (uint32_t u = tid; u < (a.raw ? 0u : nu); u += blockDim.x) {
     const uint32_t s = T.used[u];
     const uint32_t b = k0 + T.start[s], n = (uint32_t)T.cnt[s];
     double lat = 0.0, occw = 0.0;
