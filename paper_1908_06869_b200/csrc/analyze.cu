@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256, XSP_KK_MINB) k_kernels(LayerArgs a, uint3
 
 // Per (group, layer): combine() layer latency (:135-144), the Accumulator over
 // the layer's kernels in tree order (:173-211), a11-a14 rows and top-k.
-__global__ void k_layers(LayerArgs a) {
+__global__ void __launch_bounds__(256, 3) k_layers(LayerArgs a) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= a.total_layers) return;
   const uint32_t g = group_of(a.gl_off, a.G, q);
