@@ -1187,9 +1187,10 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
   const uint8_t f = flags[ent.row];
   const bool mono = f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID) && (r == 0 || kl[k - 1].cid < ent.cid);
   if (!mono) t_nomono[t] = 1;
-  bool ok = mono && !t_slow[t];
-  if (ok) ok = ex[t_ex_off[t] + r].cid == ent.cid;
-  if (!ok) {
+  const bool was_slow = t_slow[t] != 0;
+  // only the first mismatch of a trace stores (a reordered long trace would
+  // otherwise have every launch store to the same two words)
+  if (!was_slow && !(mono && ex[t_ex_off[t] + r].cid == ent.cid)) {
     t_slow[t] = 1;
     *any_slow = 1;
   }
