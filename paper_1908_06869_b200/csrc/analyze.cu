@@ -647,20 +647,23 @@ __global__ void k_big_chunks(BigChunkArgs a) {
   const double* v = kind == 0 ? a.k_lat : a.l_kern_lat;
   double s = 0.0, so = 0.0;
   uint64_t f = 0, r = 0, w = 0;
-  for (uint32_t base = b; base < e; base += 32) {
-    const uint32_t x = base + lane;
-    const double l = x < e ? v[x] : 0.0;
-    if (kind == 0 && x < e) {
+  // lane-strided partial sums and a fixed xor-butterfly: the chunk sums are
+  // re-associated at chunk boundaries anyway (integer latencies stay exact)
+#pragma unroll 4
+  for (uint32_t x = b + lane; x < e; x += 32) {
+    const double l = v[x];
+    s = __dadd_rn(s, l);
+    if (kind == 0) {
       f += a.k_flops[x];
       r += a.k_read[x];
       w += a.k_write[x];
+      so = __dadd_rn(so, __dmul_rn(a.k_occ[x], l));
     }
-    const double pr = (kind == 0 && x < e) ? __dmul_rn(a.k_occ[x], l) : 0.0;
-    const uint32_t cnt = min(32u, e - base);
-    for (uint32_t q = 0; q < cnt; ++q) {
-      s = __dadd_rn(s, __shfl_sync(0xffffffffu, l, q));
-      so = __dadd_rn(so, __shfl_sync(0xffffffffu, pr, q));
-    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+    so = __dadd_rn(so, __shfl_xor_sync(0xffffffffu, so, o));
   }
   f = warp_sum_u64(f);
   r = warp_sum_u64(r);
