@@ -84,6 +84,7 @@ __device__ __forceinline__ double trimmed_mean_net(Load load, uint32_t n, double
 
 template <typename Load>
 __device__ __forceinline__ double trimmed_mean_any(Load load, uint32_t n, double f) {
+  if (n == 1) return load(0);  // one run: nothing is trimmed, the mean is the sample
   if (n <= 8) return trimmed_mean_net<8>(load, n, f);
   if (n <= 16) return trimmed_mean_net<16>(load, n, f);
   if (n <= 32) return trimmed_mean_net<32>(load, n, f);
@@ -120,6 +121,7 @@ __device__ __forceinline__ bool trimmed_mean_u32(Load load, uint32_t n, double f
 template <typename Load>  // load(r) -> uint64_t
 __device__ __forceinline__ double trimmed_mean_int(Load load, uint32_t n, double f) {
   double out;
+  if (n == 1) return (double)load(0);  // one run (long traces): the sample itself
   if (n <= 8 && trimmed_mean_u32<8>(load, n, f, out)) return out;
   if (n > 8 && n <= 16 && trimmed_mean_u32<16>(load, n, f, out)) return out;
   if (n > 16 && n <= 32 && trimmed_mean_u32<32>(load, n, f, out)) return out;
