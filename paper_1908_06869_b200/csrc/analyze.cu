@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
       if (!over) slot = h;
     }
     if (__any_sync(0xffffffffu, over)) break;
-    const uint32_t peers = __match_any_sync(0xffffffffu, slot);
+    const uint32_t peers = match8(slot, 0xffffffffu);  // idle lanes hold distinct dummies >= NCAP
     uint32_t rank = 0;
     if (v) rank = wcnt[warp][slot];
     __syncwarp();

@@ -191,8 +191,8 @@ static __global__ void k_rs_scatter(const uint64_t* __restrict__ kin, const uint
     bool valid = i < n;
     uint64_t key = valid ? kin[i] : 0;
     uint32_t val = valid ? vin[i] : 0;
-    uint32_t d = valid ? (uint32_t)((key >> shift) & 255u) : 256u;
-    uint32_t mask = __match_any_sync(0xffffffffu, d);
+    uint32_t d = valid ? (uint32_t)((key >> shift) & 255u) : 0u;
+    uint32_t mask = match8(d, __ballot_sync(0xffffffffu, valid));
     uint32_t rank = __popc(mask & lanemask_lt());
     uint32_t leader = __ffs(mask) - 1;
     if (valid && lane == leader) wcnt[warp][d] = __popc(mask);

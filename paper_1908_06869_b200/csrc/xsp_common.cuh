@@ -45,6 +45,19 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // Last trace t with off[t] <= i, searching t in [lo, hi) (off has n_traces+1
 // entries; empty traces are skipped because off[t] == off[t+1]).
+// Lanes of `valid` holding the same 8-bit value as this lane: one ballot per
+// bit (warp multisplit). Several times cheaper than __match_any_sync here.
+__device__ __forceinline__ uint32_t match8(uint32_t d, uint32_t valid) {
+  uint32_t m = valid;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t bit = (d >> b) & 1u;
+    const uint32_t v = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? v : ~v;
+  }
+  return m;
+}
+
 __device__ __forceinline__ uint32_t trace_of(const uint64_t* __restrict__ off, uint32_t lo,
                                              uint32_t hi, uint64_t i) {
   // invariant: off[lo] <= i < off[hi]
