@@ -789,7 +789,10 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
       uint32_t h = (nm * 2654435761u) & (NCAP - 1);
       uint32_t probes = 0;
       for (;;) {
-        const uint32_t old = atomicCAS(&T.key[h], NEMPTY, nm);
+        // plain read first: most kernels find their name already present, and
+        // lanes of one name would otherwise serialise on the same CAS
+        uint32_t old = *reinterpret_cast<volatile uint32_t*>(&T.key[h]);
+        if (old == NEMPTY) old = atomicCAS(&T.key[h], NEMPTY, nm);
         if (old == NEMPTY) {
           T.used[atomicAdd(&T.nused, 1u)] = h;
           break;
