@@ -864,6 +864,108 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
     pb = j0 > 0 ? sm.begin[sw128(j0 - 1)] : __ldg(a.begin + i0 - 1);
     pf = j0 > 0 ? sm.flags[j0 - 1] : __ldg(a.flags + i0 - 1);
   }
+  // Fast emit: the 8 spans lie inside one trace with no trace head, no model
+  // span, and the trace profiles the layer level. The roles come from the flag
+  // bytes as bit masks and each output list is filled by walking its mask in
+  // span order (the same entries, positions and counters as the general walk).
+  if (j0 + P1_ITEMS <= tile_n && ta.cur < i0 && ta.next >= i0 + P1_ITEMS &&
+      (ta.levels & (1u << XSP_LEVEL_LAYER)) && !byte_mask_eq(fl8, 0x0F0F0F0Fu, 0u)) {
+    const uint32_t t = tlo + r;
+    // timeline order (begin_ns, rank, span_id) within the trace (span.hpp:161-163)
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < P1_ITEMS; ++k) {
+      const uint64_t b = sm.begin[sw128(j0 + k)];
+      const uint8_t f = (uint8_t)(fl8 >> (8 * k));
+      if (pb >= b) {
+        bool bk = pb > b;
+        if (!bk) {
+          const uint32_t l0 = f_level(pf), l1 = f_level(f);
+          const uint32_t r0_ = l0 >= 2 ? 3 : l0 + 1, r1_ = l1 >= 2 ? 3 : l1 + 1;
+          bk = r0_ > r1_ || (r0_ == r1_ && __ldg(a.span_id + i0 + k - 1) > __ldg(a.span_id + i0 + k));
+        }
+        bad |= bk;
+      }
+      pb = b;
+      pf = f;
+    }
+    if (bad) atomicOr(a.unsorted, 1u);
+    const RoleMasks m = role_masks(fl8);
+    const uint32_t exec_m = byte_mask_eq(fl8, 0x0C0C0C0Cu, 0x08080808u);
+    const uint32_t sync_k = byte_mask_eq(fl8, 0x0F0F0F0Fu, 0x02020202u);
+    const uint32_t placed = pmask & m.layer_sync;
+    // placed layers (in order, with the containment state) and kernel-list entries
+    for (uint32_t ev = placed | m.kl; ev; ev &= ev - 1) {
+      const int k = __ffs(ev) - 1;
+      const uint32_t below = (1u << k) - 1u;
+      const uint64_t i = i0 + k;
+      const uint64_t e = sm.end[sw128(j0 + k)];
+      if ((placed >> k) & 1u) {
+        a.layer_row[g] = (uint32_t)i;
+        a.layer_dur[g] = clamp_dur(sm.begin[sw128(j0 + k)], e);
+        a.layer_attr_row[g] = c_lay + __popc(m.layer & below);
+        ++g;
+        const uint64_t w = e == ~0ull ? e : e + 1;
+        lastM = runM;
+        lastE = w;
+        runM = max64(runM, w);
+        continue;
+      }
+      const uint8_t f = (uint8_t)(fl8 >> (8 * k));
+      const uint32_t k_ex = c_kl++;
+      uint32_t par;
+      if (f & XSP_F_PARENT) {
+        par = PAR_PENDING;
+        const uint32_t s = atomicAdd(a.pend_count, 1u);
+        if (s < a.pend_cap) a.pend_kl[s] = k_ex;
+      } else {
+        const bool in_j = lastE > e;  // end_j >= e (ends stored +1)
+        const bool in_m = lastM > e;  // an earlier layer has end >= e
+        if (in_j && !in_m) {
+          par = g - 1;
+        } else if (!in_j && !in_m) {
+          par = PAR_ORPHAN;
+          emit_orphan(a.orph, t, CAT_KERNEL, i, (uint32_t)i, XSP_O_KERNEL_NO_LAYER);
+        } else {
+          par = PAR_AMBIG;
+          const uint32_t s = atomicAdd(a.amb_count, 1u);
+          if (s < a.amb_cap) {
+            a.amb_kl[s] = k_ex;
+            a.amb_gx[s] = g;
+          }
+        }
+      }
+      KlEnt ent;
+      ent.row = (uint32_t)i;
+      ent.parent = par;
+      ent.cid = (f & XSP_F_CID) ? sm.cid[sw128(j0 + k)] : 0;
+      a.kl[k_ex] = ent;
+      if ((sync_k >> k) & 1u) a.kl_mrow[k_ex] = ((m.metric >> k) & 1u) ? c_metric + __popc(m.metric & below) : kNone;
+    }
+    // layers that are not placed (correlator.cpp:169-194)
+    for (uint32_t lo = m.layer & ~placed; lo; lo &= lo - 1) {
+      const int k = __ffs(lo) - 1;
+      const uint8_t f = (uint8_t)(fl8 >> (8 * k));
+      emit_orphan(a.orph, t, CAT_LAYER, i0 + k, (uint32_t)(i0 + k),
+                  !((m.layer_sync >> k) & 1u)
+                      ? XSP_O_LAYER_NON_SYNC
+                      : ((f & XSP_F_PARENT) ? XSP_O_LAYER_BAD_PARENT : XSP_O_LAYER_OUTSIDE_MODEL));
+    }
+    // executions: with a cid into the exec list, without one an orphan
+    for (uint32_t ex = exec_m; ex; ex &= ex - 1) {
+      const int k = __ffs(ex) - 1;
+      if ((m.ex_cid >> k) & 1u) {
+        ExEnt ent;
+        ent.row = (uint32_t)(i0 + k);
+        ent.mrow = ((m.metric >> k) & 1u) ? c_metric + __popc(m.metric & ((1u << k) - 1u)) : kNone;
+        ent.cid = sm.cid[sw128(j0 + k)];
+        a.ex[c_ex++] = ent;
+      } else if (!a.parents_only) {
+        emit_orphan(a.orph, t, CAT_EXEC_NOCID, i0 + k, (uint32_t)(i0 + k), XSP_O_EXEC_NO_CID);
+      }
+    }
+    return;
+  }
 #pragma unroll kP1EmitUnroll
   for (int p = 0; p < P1_ITEMS / 2; ++p) {
     uint64_t bb[2], ee[2], cc[2];
