@@ -311,13 +311,18 @@ class _Replica:
         return self._db.traces(self)
 
 
-def measure_c5(eng, dev, b, groups, steps: int, copies: int = 21, per_call: int = 11):
-    """BASELINE config 5 on one GPU: a ~1 B-span multi-trace corpus (the C3 corpus
+def measure_c5(eng, dev, b, groups, steps: int, copies: int = 21, per_call: int = 11,
+               rank: int = 0, world: int = 1, dist=None):
+    """BASELINE config 5: a ~1 B-span multi-trace corpus (the C3 corpus
     replicated `copies` times in HBM, independent traces) correlated + analysed
     as device-resident calls of up to `per_call` copies (~0.5 B spans) each.
-    Every copy must come back with the C3 counts (no orphans, no failures)."""
+    Under N ranks the copies are trace-sharded over the ranks (rank r holds
+    copies r, r+N, ...; strong scaling, max over ranks). Every copy must come
+    back with the C3 counts (no orphans, no failures)."""
     import torch
     from types import SimpleNamespace
+    copies_all = copies
+    copies = len(range(rank, copies_all, world))
     n, T = b.n_spans, b.n_traces
     M, Lr = b.flops.size, b.alloc_bytes.size
     metric_cols = {"flops", "dram_read", "dram_write", "occupancy"}
@@ -362,13 +367,19 @@ def measure_c5(eng, dev, b, groups, steps: int, copies: int = 21, per_call: int 
     t1.record()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / reps
-    total = n * copies
+    if dist:
+        tm = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ms = float(tm.item())
+    total = n * copies_all
     del big, calls
     torch.cuda.empty_cache()
     return {"metric": "M spans/s correlated+analyzed, ~1 B-span multi-trace corpus", "value": total / (ms / 1e3) / 1e6,
             "unit": UNIT, "ms_per_step": ms, "spans": total, "calls_per_step": (copies + per_call - 1) // per_call,
-            "workload": f"C5: the C3 corpus replicated {copies}x in HBM ({copies * T} traces, {total} spans), "
-                        f"correlate + a5..a15 in device-resident calls of <= {per_call} copies"}
+            "scaling": "strong", "copies_per_rank": copies,
+            "workload": f"C5: the C3 corpus replicated {copies_all}x in HBM ({copies_all * T} traces, {total} spans), "
+                        f"trace-sharded over {world} rank(s), correlate + a5..a15 in device-resident calls of "
+                        f"<= {per_call} copies"}
 
 
 def config(args):
@@ -475,7 +486,7 @@ def main():
            "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
 
     sort_line = measure_sort(eng, dev, b, args.steps, local) if not args.no_sort else None
-    c5_line = measure_c5(eng, dev, b, groups, args.steps) if args.c5 else None
+    c5_line = measure_c5(eng, dev, b, groups, args.steps, rank=rank, world=world, dist=dist) if args.c5 else None
     del dev
     c4_line = measure_c4(eng, args, rank, world, local, dist) if args.c4_layers > 0 else None
 
