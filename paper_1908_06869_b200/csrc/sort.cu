@@ -7,7 +7,7 @@
 // trace's begin / span_id ranges are reduced, each span gets a unique packed
 // 64-bit key (begin - min, rank, span_id - min, local index), the thread-local
 // runs are sorted in registers and merged by merge path in shared memory.
-// Three size classes (4 K / 8 K / 16 K spans) keep 4 / 2 / 1 CTAs per SM.
+// Three size classes (4 K / 8 K / 16 K spans) keep 6 / 3 / 1 CTAs per SM.
 // HBM traffic is one read of begin/span_id/flags and one perm write (21 B/span).
 // Traces that are longer, or whose begin range alone needs more than 47 bits,
 // fall back to one global LSD radix sort over the composite key (trace,
@@ -345,9 +345,10 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
   // per-trace CTA sort; the global radix sort only if some trace does not fit
   XSP_CUDA(cudaMemsetAsync(flag, 0, 4, st));
   ctx->stage_begin("sort", st);
-  // register budgets sized for 4 / 2 / 1 resident CTAs per SM
-  auto* k_small = k_sort_merge<256, 16, 4>;
-  auto* k_mid = k_sort_merge<512, 16, 2>;
+  // register budgets sized for 6 / 3 / 1 resident CTAs per SM (a few spilled
+  // registers cost less than the lost occupancy)
+  auto* k_small = k_sort_merge<256, 16, 6>;
+  auto* k_mid = k_sort_merge<512, 16, 3>;
   auto* k_large = k_sort_merge<512, 32, 1>;
   auto smem = [](uint32_t cap) { return (size_t)(cap + cap / 16) * 8; };
   XSP_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(kSegCapSmall)));
