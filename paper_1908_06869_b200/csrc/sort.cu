@@ -7,7 +7,8 @@
 // trace's begin / span_id ranges are reduced, each span gets a unique packed
 // 64-bit key (begin - min, rank, span_id - min, local index), the thread-local
 // runs are sorted in registers and merged by merge path in shared memory.
-// Three size classes (4 K / 8 K / 16 K spans) keep 6 / 3 / 1 CTAs per SM.
+// Three size classes (4 K / 8 K / 16 K spans) keep 6 / 3 / 1 CTAs per SM
+// (256 / 512 / 1024 threads, 16 keys per thread).
 // HBM traffic is one read of begin/span_id/flags and one perm write (21 B/span).
 // Traces that are longer, or whose begin range alone needs more than 47 bits,
 // fall back to one global LSD radix sort over the composite key (trace,
@@ -349,7 +350,7 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
   // registers cost less than the lost occupancy)
   auto* k_small = k_sort_merge<256, 16, 6>;
   auto* k_mid = k_sort_merge<512, 16, 3>;
-  auto* k_large = k_sort_merge<512, 32, 1>;
+  auto* k_large = k_sort_merge<1024, 16, 1>;
   auto smem = [](uint32_t cap) { return (size_t)(cap + cap / 16) * 8; };
   XSP_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(kSegCapSmall)));
   XSP_CUDA(cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(kSegCapMid)));
@@ -358,7 +359,7 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
     XSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   k_small<<<T, 256, smem(kSegCapSmall), st>>>(begin, flags, sid, off, 0, perm, flag);
   k_mid<<<T, 512, smem(kSegCapMid), st>>>(begin, flags, sid, off, kSegCapSmall + 1, perm, flag);
-  k_large<<<T, 512, smem(kSegCap), st>>>(begin, flags, sid, off, kSegCapMid + 1, perm, flag);
+  k_large<<<T, 1024, smem(kSegCap), st>>>(begin, flags, sid, off, kSegCapMid + 1, perm, flag);
   ctx->stage_end("sort", st);
   ctx->launches += 3;
   XSP_CUDA(cudaMemcpyAsync(h, flag, 4, cudaMemcpyDeviceToHost, st));
