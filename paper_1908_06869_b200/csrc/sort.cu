@@ -301,17 +301,29 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sort_merge(const uint64_t* __
   }
   __syncthreads();
   if (mode == 1) {
-    // runs of equal (begin, rank): order by span_id, stably (j ascends in a run)
+    // runs of equal (begin, rank): order by span_id, stably (j ascends in a run).
+    // Phase 1 (read-only) records each run's length at its start in the perm
+    // slots of the trace (scratch until the final write); phase 2 sorts every
+    // run by its own thread, touching only that run's keys.
     for (uint32_t p = tid; p < len; p += THREADS) {
       const uint64_t kp = mkeys[mpad(p)] >> 14;
-      if (p > 0 && (mkeys[mpad(p - 1)] >> 14) == kp) continue;  // not a run start
-      uint32_t e = p + 1;
-      while (e < len && (mkeys[mpad(e)] >> 14) == kp) ++e;
-      if (e - p < 2) continue;
-      if (e - p > 1024) {  // pathological tie run: the global sort handles the batch
+      uint32_t run = 0;
+      if (p == 0 || (mkeys[mpad(p - 1)] >> 14) != kp) {
+        uint32_t e = p + 1;
+        while (e < len && (mkeys[mpad(e)] >> 14) == kp) ++e;
+        run = e - p;
+      }
+      perm[lo + p] = run;
+    }
+    __syncthreads();
+    for (uint32_t p = tid; p < len; p += THREADS) {
+      const uint32_t run = perm[lo + p];
+      if (run < 2) continue;
+      if (run > 1024) {  // pathological tie run: the global sort handles the batch
         atomicOr(fallback, 1u);
         continue;
       }
+      const uint32_t e = p + run;
       for (uint32_t q = p + 1; q < e; ++q) {  // insertion by span_id
         const uint64_t kq = mkeys[mpad(q)];
         const uint64_t sq = sid[lo + (kq & 0x3FFFu)];
