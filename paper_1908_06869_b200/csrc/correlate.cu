@@ -51,10 +51,13 @@ struct __align__(16) KlEnt {
   uint64_t cid;     // correlation id (0 if absent)
 };
 // Execution-list entry: an exec span carrying a correlation id.
+// Its correlation id is read back from the cid column by row when needed; the
+// duration is computed by pass 1 from the staged tile, so the gather does not
+// re-read begin_ns / end_ns at the (strided) exec rows.
 struct __align__(16) ExEnt {
   uint32_t row;   // span row
   uint32_t mrow;  // metric-table row, kNone if none
-  uint64_t cid;
+  uint64_t dur;   // clamped end - begin of the exec span
 };
 
 struct Orphans {
@@ -958,7 +961,7 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
         ExEnt ent;
         ent.row = (uint32_t)(i0 + k);
         ent.mrow = ((m.metric >> k) & 1u) ? c_metric + __popc(m.metric & ((1u << k) - 1u)) : kNone;
-        ent.cid = sm.cid[sw128(j0 + k)];
+        ent.dur = clamp_dur(sm.begin[sw128(j0 + k)], sm.end[sw128(j0 + k)]);
         a.ex[c_ex++] = ent;
       } else if (!a.parents_only) {
         emit_orphan(a.orph, t, CAT_EXEC_NOCID, i0 + k, (uint32_t)(i0 + k), XSP_O_EXEC_NO_CID);
@@ -1073,7 +1076,7 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
           ExEnt ent;
           ent.row = (uint32_t)i;
           ent.mrow = mrow;
-          ent.cid = cc[h];
+          ent.dur = clamp_dur(b, e);
           a.ex[c_ex++] = ent;
         } else if (!a.parents_only) {
           emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
@@ -1276,6 +1279,7 @@ __global__ void k_join_counts(const uint32_t* __restrict__ t_kl_off, const uint3
 // t_nomono[t] = 1 when some kernel-list entry of t is not a cid launch or its cid
 // does not exceed the previous entry's (the direct-address join needs both).
 __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const ExEnt* __restrict__ ex,
+                             const uint64_t* __restrict__ cid,
                              const uint8_t* __restrict__ flags, const uint32_t* __restrict__ t_kl_off,
                              const uint32_t* __restrict__ t_ex_off, uint32_t T, uint32_t* __restrict__ t_slow,
                              uint32_t* __restrict__ any_slow, uint32_t* __restrict__ t_nomono) {
@@ -1292,7 +1296,7 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
   const bool was_slow = t_slow[t] != 0;
   // only the first mismatch of a trace stores (a reordered long trace would
   // otherwise have every launch store to the same two words)
-  if (!was_slow && !(mono && ex[t_ex_off[t] + r].cid == ent.cid)) {
+  if (!was_slow && !(mono && cid[ex[t_ex_off[t] + r].row] == ent.cid)) {
     t_slow[t] = 1;
     *any_slow = 1;
   }
@@ -1322,7 +1326,8 @@ __global__ void k_join_direct(const uint32_t* __restrict__ t_kl_off, const uint3
 
 // An exec whose cid lies outside its direct trace's launch range matches no
 // launch but may still duplicate another exec: that trace uses the hash table.
-__global__ void k_join_far(uint32_t nex, const ExEnt* __restrict__ ex, const uint32_t* __restrict__ t_ex_off,
+__global__ void k_join_far(uint32_t nex, const ExEnt* __restrict__ ex, const uint64_t* __restrict__ cid,
+                           const uint32_t* __restrict__ t_ex_off,
                            uint32_t T, uint64_t* __restrict__ t_lmin, const uint64_t* __restrict__ t_lmax) {
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t first = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
@@ -1331,7 +1336,7 @@ __global__ void k_join_far(uint32_t nex, const ExEnt* __restrict__ ex, const uin
   if (x >= nex) return;
   const uint64_t lmin = t_lmin[t];
   if (lmin == ~0ull) return;
-  const uint64_t c = ex[x].cid;
+  const uint64_t c = cid[ex[x].row];
   if (c < lmin || c > t_lmax[t]) t_lmin[t] = ~0ull;
 }
 
@@ -1361,6 +1366,7 @@ __global__ void k_region_size(const uint32_t* __restrict__ t_kl_off, const uint3
 
 struct JoinArgs {
   const ExEnt* ex;
+  const uint64_t* cid;  // span cid column (exec cids by row)
   const KlEnt* kl;
   const uint8_t* flags;
   const uint32_t* t_ex_off;
@@ -1389,7 +1395,7 @@ __global__ void k_join_insert(JoinArgs a) {
   if (is_ex) {
     t = trace_of32(a.t_ex_off, a.T, it);
     if (!a.t_slow[t]) return;
-    cid = a.ex[it].cid;
+    cid = a.cid[a.ex[it].row];
   } else {
     uint32_t k = it - a.n_ex;
     t = trace_of32(a.t_kl_off, a.T, k);
@@ -1410,7 +1416,7 @@ __global__ void k_join_insert(JoinArgs a) {
       if (o == 0) break;
     }
     uint32_t oi = o - 1;
-    uint64_t ocid = oi < a.n_ex ? a.ex[oi].cid : a.kl[oi - a.n_ex].cid;
+    uint64_t ocid = oi < a.n_ex ? a.cid[a.ex[oi].row] : a.kl[oi - a.n_ex].cid;
     if (ocid == cid) break;
     h = (h + 1) & mask;
   }
@@ -1557,8 +1563,13 @@ __global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val, 
     return;
   } else {
     const ExEnt e = ex[x];
-    er = e.row;
-    mr = e.mrow;
+    k_launch[j] = r;
+    k_exec[j] = e.row;
+    k_mrow[j] = e.mrow;
+    k_dur[j] = e.dur;
+    k_name[j] = name[e.row];
+    k_occ[j] = e.mrow != kNone ? occ[e.mrow] : 0.0;
+    return;
   }
   k_launch[j] = r;
   k_exec[j] = er;
@@ -1577,7 +1588,7 @@ __global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val, 
 __device__ __forceinline__ void gather_fast_one(uint32_t j, uint32_t first, uint32_t nl, uint32_t nk, uint32_t nex, const KlEnt* __restrict__ kl,
                               const ExEnt* __restrict__ ex, const uint8_t* __restrict__ flags,
                               const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
-                              uint32_t T, const uint64_t* __restrict__ begin, const uint64_t* __restrict__ end,
+                              uint32_t T, const uint64_t* __restrict__ cid,
                               const uint32_t* __restrict__ name, const double* __restrict__ occ,
                               uint32_t* __restrict__ k_launch, uint32_t* __restrict__ k_exec,
                               uint32_t* __restrict__ k_mrow, uint64_t* __restrict__ k_dur,
@@ -1610,10 +1621,10 @@ __device__ __forceinline__ void gather_fast_one(uint32_t j, uint32_t first, uint
   ExEnt e;
   e.row = ent.row;
   e.mrow = kNone;
-  e.cid = 0;
+  e.dur = 0;
   if (ok) {
     e = ex[xb + r];
-    ok = e.cid == ent.cid && (r == 0 || kl[j - 1].cid < ent.cid);
+    ok = cid[e.row] == ent.cid && (r == 0 || kl[j - 1].cid < ent.cid);
   }
   if (!ok) {
     *fail = 1;
@@ -1622,7 +1633,7 @@ __device__ __forceinline__ void gather_fast_one(uint32_t j, uint32_t first, uint
   k_launch[j] = ent.row;
   k_exec[j] = e.row;
   k_mrow[j] = e.mrow;
-  k_dur[j] = clamp_dur(begin[e.row], end[e.row]);
+  k_dur[j] = e.dur;
   k_name[j] = name[e.row];
   k_occ[j] = e.mrow != kNone ? occ[e.mrow] : 0.0;
 }
@@ -1633,7 +1644,7 @@ __global__ void __launch_bounds__(256) k_gather_fast(const uint32_t* __restrict_
                               const KlEnt* __restrict__ kl,
                               const ExEnt* __restrict__ ex, const uint8_t* __restrict__ flags,
                               const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
-                              uint32_t T, const uint64_t* __restrict__ begin, const uint64_t* __restrict__ end,
+                              uint32_t T, const uint64_t* __restrict__ cid,
                               const uint32_t* __restrict__ name, const double* __restrict__ occ,
                               uint32_t* __restrict__ k_launch, uint32_t* __restrict__ k_exec,
                               uint32_t* __restrict__ k_mrow, uint64_t* __restrict__ k_dur,
@@ -1642,7 +1653,7 @@ __global__ void __launch_bounds__(256) k_gather_fast(const uint32_t* __restrict_
   const uint32_t nl = totals[0], nk = totals[1], nex = totals[2];
   for (uint32_t base = blockIdx.x * blockDim.x; base <= nk; base += gridDim.x * blockDim.x)
     gather_fast_one(base + threadIdx.x, base + (threadIdx.x & ~31u), nl, nk, nex, kl, ex, flags, t_kl_off,
-                    t_ex_off, T, begin, end, name, occ, k_launch, k_exec, k_mrow, k_dur, k_name, k_occ, l_koff,
+                    t_ex_off, T, cid, name, occ, k_launch, k_exec, k_mrow, k_dur, k_name, k_occ, l_koff,
                     fail);
 }
 
@@ -1959,8 +1970,8 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", n + 1);
     ctx->stage_begin("gather", st);
     const unsigned gb = std::min<uint64_t>(ceil_div((uint64_t)n + 1, 256), 148u * 8u);
-    k_gather_fast<<<gb, 256, 0, st>>>(totals, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, c->begin_ns,
-                                      c->end_ns, c->name_id, c->occupancy, out->kernel_launch_row,
+    k_gather_fast<<<gb, 256, 0, st>>>(totals, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, c->cid,
+                                      c->name_id, c->occupancy, out->kernel_launch_row,
                                       out->kernel_exec_row, out->kernel_metric_row, out->kernel_dur,
                                       out->kernel_name, out->kernel_occ, out->layer_kernel_off, counters + 7);
     ++ctx->launches;
@@ -2084,6 +2095,7 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   ctx->stage_begin("join", st);
   JoinArgs j;
   j.ex = a.ex;
+  j.cid = c->cid;
   j.kl = a.kl;
   j.flags = c->flags;
   j.t_ex_off = a.t_ex_off;
@@ -2098,7 +2110,7 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   if (!parents_only) {
     XSP_CUDA(cudaMemsetAsync(t_nomono, 0, (T + 1) * 4ull, st));
     launch(ctx, k_join_counts, T, st, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
-    launch(ctx, k_join_check, nkl, st, nkl, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, t_slow,
+    launch(ctx, k_join_check, nkl, st, nkl, a.kl, a.ex, c->cid, c->flags, a.t_kl_off, a.t_ex_off, T, t_slow,
            counters + 7, t_nomono);
     any_slow = read_u32(ctx, counters + 7, st);
   }
@@ -2117,7 +2129,7 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
       XSP_CUDA(cudaMemsetAsync(t_lmin, 0xFF, (T + 1) * 8ull, st));
     } else {
       launch(ctx, k_join_direct, T, st, a.t_kl_off, t_slow, t_nomono, a.kl, T, t_lmin, t_lmax);
-      launch(ctx, k_join_far, nex, st, nex, a.ex, a.t_ex_off, T, t_lmin, t_lmax);
+      launch(ctx, k_join_far, nex, st, nex, a.ex, c->cid, a.t_ex_off, T, t_lmin, t_lmax);
     }
     j.t_lmin = t_lmin;
     launch(ctx, k_region_size, T, st, a.t_kl_off, a.t_ex_off, t_slow, t_lmin, t_lmax, T, rsize);
