@@ -257,3 +257,27 @@ def test_cid_join_direct_and_hash_regions(engine, has_ref, monkeypatch):
     c2, _ = engine.run_host(b)
     for k in corr.cols:
         assert np.array_equal(np.asarray(corr.cols[k]), np.asarray(c2.cols[k])), k
+
+
+@pytest.mark.parametrize("seed", [101, 202, 303])
+def test_mixed_batch_stress(engine, has_ref, seed):
+    """Many traces of every generator in one batch (nested with explicit-parent
+    fractions, shuffled async pairs, simprof models with jitter, overlap
+    ambiguities): every correlation output and analysis table equals the
+    reference, across the pass-1 fast/general emit, merge-aligned / direct /
+    hash joins and the a10 fast path."""
+    rng = np.random.default_rng(seed)
+    g = ref.Generator()
+    for k in range(12):
+        g.random_nested(seed * 100 + k, int(rng.integers(50, 3000)), float(rng.choice([0.0, 0.2, 0.7])))
+    for k in range(6):
+        g.random_async(seed * 10 + k, int(rng.integers(10, 4000)))
+    for r in range(4):
+        g.emit("resnet-like", batch=1 + r, run_index=0, jitter_max=500, jitter_seed=seed + r)
+    g.emit("overlap")
+    b = g.batch()
+    corr, tabs = engine.run_host(b)
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+    aa, ast = ref.analyze(b, np.arange(b.n_traces), np.ones(b.n_traces))
+    compare_tables(b, tabs, aa, ast)
