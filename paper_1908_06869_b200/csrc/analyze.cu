@@ -777,6 +777,120 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
   const uint32_t w0 = min(k1, k0 + warp * q), w1 = min(k1, w0 + q);
   const uint32_t lt = lanemask_lt();
   bool over = false;
+  if (a.raw) {
+    // Raw mode (a chunk of a long group; its sums are re-associated at chunk
+    // boundaries anyway): stream the warp's quarter in order with coalesced
+    // loads. Per 32 kernels, each name's leader lane adds its peers' values in
+    // lane order into the warp's table; the four warp tables are then added in
+    // warp order. Deterministic, and no gathers through a name permutation.
+    struct RawAcc {
+      double lat[NAME_WARPS][NCAP], occw[NAME_WARPS][NCAP];
+      unsigned long long f[NAME_WARPS][NCAP], r[NAME_WARPS][NCAP], w[NAME_WARPS][NCAP];
+      uint32_t cnt[NAME_WARPS][NCAP];
+      double st_l[NAME_WARPS][32], st_o[NAME_WARPS][32];
+      unsigned long long st_f[NAME_WARPS][32], st_r[NAME_WARPS][32], st_w[NAME_WARPS][32];
+    };
+    static_assert(sizeof(RawAcc) <= kNameSmem, "raw accumulators fit the scratch");
+    RawAcc& R = *reinterpret_cast<RawAcc*>(nm_dyn);
+    for (uint32_t s = lane; s < NCAP; s += 32) {
+      R.lat[warp][s] = R.occw[warp][s] = 0.0;
+      R.f[warp][s] = R.r[warp][s] = R.w[warp][s] = 0;
+      R.cnt[warp][s] = 0;
+    }
+    __syncwarp();
+    for (uint32_t base = w0; base < w1; base += 32) {
+      const uint32_t x = base + lane;
+      const bool v = x < w1;
+      uint32_t slot = NCAP + lane;  // distinct dummy for idle lanes
+      double l = 0.0, ow = 0.0;
+      unsigned long long f = 0, rd = 0, wr = 0;
+      if (v) {
+        const uint32_t nm = a.k_name[x];
+        l = a.k_lat[x];
+        ow = __dmul_rn(a.k_occ ? a.k_occ[x] : 0.0, l);
+        f = a.k_flops[x];
+        if (a.k_read) rd = a.k_read[x];
+        if (a.k_write) wr = a.k_write[x];
+        uint32_t h = (nm * 2654435761u) & (NCAP - 1), probes = 0;
+        for (;;) {
+          uint32_t old = *reinterpret_cast<volatile uint32_t*>(&T.key[h]);
+          if (old == NEMPTY) old = atomicCAS(&T.key[h], NEMPTY, nm);
+          if (old == NEMPTY) {
+            T.used[atomicAdd(&T.nused, 1u)] = h;
+            break;
+          }
+          if (old == nm) break;
+          h = (h + 1) & (NCAP - 1);
+          if (++probes >= NCAP) {
+            over = true;
+            break;
+          }
+        }
+        if (!over) slot = h;
+      }
+      if (__any_sync(0xffffffffu, over)) break;
+      R.st_l[warp][lane] = l;
+      R.st_o[warp][lane] = ow;
+      R.st_f[warp][lane] = f;
+      R.st_r[warp][lane] = rd;
+      R.st_w[warp][lane] = wr;
+      const uint32_t peers = match8(slot, 0xffffffffu);
+      __syncwarp();
+      if (v && (peers & lt) == 0) {  // leader: the name's kernels of this step, in lane order
+        double sl = R.lat[warp][slot], so = R.occw[warp][slot];
+        unsigned long long sf = R.f[warp][slot], sr = R.r[warp][slot], sw = R.w[warp][slot];
+        for (uint32_t m = peers; m; m &= m - 1) {
+          const uint32_t qq = __ffs(m) - 1;
+          sl = __dadd_rn(sl, R.st_l[warp][qq]);
+          so = __dadd_rn(so, R.st_o[warp][qq]);
+          sf += R.st_f[warp][qq];
+          sr += R.st_r[warp][qq];
+          sw += R.st_w[warp][qq];
+        }
+        R.lat[warp][slot] = sl;
+        R.occw[warp][slot] = so;
+        R.f[warp][slot] = sf;
+        R.r[warp][slot] = sr;
+        R.w[warp][slot] = sw;
+        R.cnt[warp][slot] += __popc(peers);
+      }
+      __syncwarp();
+    }
+    if (__any_sync(0xffffffffu, over) && lane == 0) s_over = 1;
+    __syncthreads();
+    if (s_over) {
+      if (tid == 0) {
+        a.g_count[g] = 0;
+        atomicOr(a.overflow, 1u);
+      }
+      return;
+    }
+    const uint32_t nu = T.nused;
+    for (uint32_t u = tid; u < nu; u += blockDim.x) {
+      const uint32_t sl = T.used[u];
+      double lat = 0.0, occw = 0.0;
+      unsigned long long f = 0, rd = 0, wr = 0, cnt = 0;
+#pragma unroll
+      for (int w = 0; w < NAME_WARPS; ++w) {
+        lat = __dadd_rn(lat, R.lat[w][sl]);
+        occw = __dadd_rn(occw, R.occw[w][sl]);
+        f += R.f[w][sl];
+        rd += R.r[w][sl];
+        wr += R.w[w][sl];
+        cnt += R.cnt[w][sl];
+      }
+      const uint64_t o = (uint64_t)g * NCAP + u;
+      a.s_name[o] = T.key[sl];
+      a.s_count[o] = cnt;
+      a.s_lat[o] = lat;
+      a.s_occ[o] = occw;
+      a.s_flops[o] = f;
+      a.s_read[o] = rd;
+      a.s_write[o] = wr;
+    }
+    if (tid == 0) a.g_count[g] = nu;
+    return;
+  }
   // pass A: slot per kernel and its rank within its name inside the warp's quarter
   uint32_t nm_next = w0 + lane < w1 ? a.k_name[w0 + lane] : 0;
   for (uint32_t base = w0; base < w1; base += 32) {
