@@ -345,6 +345,38 @@ __global__ void __launch_bounds__(256, XSP_KK_MINB) k_kernels(LayerArgs a, uint3
   a.k_in[q] = (ro.bound >= 0 && klat > 0.0) ? 1 : 0;  // classify (analysis.cpp:59-71)
 }
 
+// Groups of one run each (a long single trace): kernel q's only sample is row
+// j = t_kernel_off[ft[g]] + ord and its "trimmed mean" is that sample, so this
+// variant carries none of the sorting-network code and its register budget
+// (and resident warps) follows the loads alone.
+__global__ void __launch_bounds__(256) k_kernels_r1(LayerArgs a, uint32_t total_kernels) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= total_kernels) return;
+  const uint32_t g = group_of(a.gk_off, a.G, q);
+  if (a.gstatus[g] != XSP_G_OK) return;
+  const uint32_t j = a.t_kernel_off[a.ft[g]] + (q - a.gk_off[g]);
+  const double klat = (double)a.kernel_dur[j];
+  const double kocc = a.kernel_occ[j];
+  const uint32_t mr0 = a.kernel_mrow[j];
+  uint64_t f = 0, rd = 0, wr = 0;
+  if (mr0 != kNone) {  // counters of the (only) repetition (:162-166)
+    f = a.m_flops[mr0];
+    rd = a.m_read[mr0];
+    wr = a.m_write[mr0];
+  }
+  const Roof ro = roofline(f, rd, wr, klat, a.peak, a.bw);
+  a.k_name[q] = a.kernel_name[j];
+  a.k_lat[q] = klat;
+  a.k_flops[q] = f;
+  a.k_read[q] = rd;
+  a.k_write[q] = wr;
+  a.k_occ[q] = kocc;
+  a.k_ai[q] = ro.ai;
+  a.k_tput[q] = ro.tput;
+  a.k_bound[q] = ro.bound;
+  a.k_in[q] = (ro.bound >= 0 && klat > 0.0) ? 1 : 0;  // classify (analysis.cpp:59-71)
+}
+
 // Per (group, layer): combine() layer latency (:135-144), the Accumulator over
 // the layer's kernels in tree order (:173-211), a11-a14 rows and top-k.
 __global__ void __launch_bounds__(256, 3) k_layers(LayerArgs a) {
@@ -1548,7 +1580,9 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   // group descriptors are host arrays
   uint32_t* hg = ctx->h<uint32_t>("a.groups_h", 4ull * G + 4);
   uint32_t total_runs = 0;
+  bool all_one_run = G > 0;
   for (uint32_t g = 0; g < G; ++g) {
+    all_one_run &= gr->n_runs[g] == 1;
     hg[g] = gr->first_trace[g];
     hg[G + g] = gr->n_runs[g];
     hg[2 * G + g] = gr->batch_size[g];
@@ -1802,7 +1836,10 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->l_roofline_in = la.l_in = ctx->d<uint8_t>("t.l_in", TL);
   out->l_topk = la.l_topk = ctx->d<uint32_t>("t.l_topk", (uint64_t)TL * (opts->top_k ? opts->top_k : 1));
   ctx->stage_begin("layers", st);
-  launch(ctx, k_kernels, TK, st, la, TK);
+  if (all_one_run)
+    launch(ctx, k_kernels_r1, TK, st, la, TK);
+  else
+    launch(ctx, k_kernels, TK, st, la, TK);
   launch(ctx, k_layers, TL, st, la);
   ctx->stage_end("layers", st);
 
