@@ -379,15 +379,21 @@ __global__ void __launch_bounds__(256) k_kernels_r1(LayerArgs a, uint32_t total_
 
 // Per (group, layer): combine() layer latency (:135-144), the Accumulator over
 // the layer's kernels in tree order (:173-211), a11-a14 rows and top-k.
-__global__ void __launch_bounds__(256, 3) k_layers(LayerArgs a) {
+// kOneRun: every group has one run (a long single trace), so the layer latency
+// is its only sample and the trimmed-mean code is not instantiated.
+template <bool kOneRun>
+__global__ void __launch_bounds__(256, kOneRun ? 4 : 3) k_layers(LayerArgs a) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= a.total_layers) return;
   const uint32_t g = group_of(a.gl_off, a.G, q);
   const uint32_t li = q - a.gl_off[g];
   if (a.gstatus[g] != XSP_G_OK) return;
   const uint32_t R = a.nr[g], t0 = a.ft[g];
-  const double layer_lat =
-      trimmed_mean_int([&](uint32_t r) { return a.layer_dur[a.t_layer_off[t0 + r] + li]; }, R, a.trim);
+  double layer_lat;
+  if constexpr (kOneRun)
+    layer_lat = (double)a.layer_dur[a.t_layer_off[t0] + li];
+  else
+    layer_lat = trimmed_mean_int([&](uint32_t r) { return a.layer_dur[a.t_layer_off[t0 + r] + li]; }, R, a.trim);
 
   const uint32_t gl0 = a.t_layer_off[t0] + li;
   const uint32_t trace_kbase = a.t_kernel_off[t0];
@@ -1836,11 +1842,13 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->l_roofline_in = la.l_in = ctx->d<uint8_t>("t.l_in", TL);
   out->l_topk = la.l_topk = ctx->d<uint32_t>("t.l_topk", (uint64_t)TL * (opts->top_k ? opts->top_k : 1));
   ctx->stage_begin("layers", st);
-  if (all_one_run)
+  if (all_one_run) {
     launch(ctx, k_kernels_r1, TK, st, la, TK);
-  else
+    launch(ctx, k_layers<true>, TL, st, la);
+  } else {
     launch(ctx, k_kernels, TK, st, la, TK);
-  launch(ctx, k_layers, TL, st, la);
+    launch(ctx, k_layers<false>, TL, st, la);
+  }
   ctx->stage_end("layers", st);
 
   // ---- per model
