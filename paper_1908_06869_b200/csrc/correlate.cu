@@ -1474,6 +1474,7 @@ struct FuseArgs {
   Orphans orph;
   bool any_slow;
   bool parents_only;  // assign_parents without correlate_async
+  uint32_t* drop;     // [0] entries not kept, [1] kept parents not in timeline order
 };
 
 __global__ void k_fuse(FuseArgs a) {
@@ -1502,6 +1503,8 @@ __global__ void k_fuse(FuseArgs a) {
   }
   a.kept[k] = keep;
   a.kl_exec[k] = x;
+  if (!keep) atomicAdd(a.drop, 1u);
+  else if (k > 0 && a.kl[k - 1].parent > ent.parent) atomicOr(a.drop + 1, 1u);
 }
 
 __global__ void k_leftover(FuseArgs a) {
@@ -1546,7 +1549,7 @@ __global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val, 
                                  uint32_t* __restrict__ k_name, double* __restrict__ k_occ) {
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nk) return;
-  const uint32_t k = val[j];
+  const uint32_t k = val ? val[j] : j;  // no val: every entry kept, in order
   const uint32_t r = kl[k].row;
   const uint32_t x = kl_exec[k];
   uint32_t er, mr;
@@ -1665,6 +1668,15 @@ __global__ void k_layer_kernel_off(uint32_t nl, uint32_t nk, const uint64_t* __r
   if (j > nk) return;
   const int64_t prev = j > 0 ? (int64_t)key[j - 1] : -1;
   const int64_t cur = j < nk ? (int64_t)key[j] : (int64_t)nl;
+  for (int64_t g = prev + 1; g <= cur; ++g) off[g] = j;
+}
+// the same with every kernel-list entry kept, in order: keys are the parents
+__global__ void k_layer_kernel_off_kl(uint32_t nl, uint32_t nk, const KlEnt* __restrict__ kl,
+                                      uint32_t* __restrict__ off) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > nk) return;
+  const int64_t prev = j > 0 ? (int64_t)kl[j - 1].parent : -1;
+  const int64_t cur = j < nk ? (int64_t)kl[j].parent : (int64_t)nl;
   for (int64_t g = prev + 1; g <= cur; ++g) off[g] = j;
 }
 
@@ -2177,21 +2189,33 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   fa.orph = orph;
   fa.any_slow = any_slow != 0;
   fa.parents_only = parents_only;
+  fa.drop = ctx->d<uint32_t>("c.fuse_drop", 2);
+  XSP_CUDA(cudaMemsetAsync(fa.drop, 0, 8, st));
   launch(ctx, k_fuse, nkl, st, fa);
   if (any_slow) launch(ctx, k_leftover, nex, st, fa);
-
-  uint32_t* kpos = ctx->d<uint32_t>("c.kpos", nkl + 1);
-  uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
-  uint32_t* nk_d = ctx->d<uint32_t>("c.nk", 1);
-  exclusive_scan<uint32_t, uint32_t>(fa.kept, kpos, nkl, scan_tmp, nk_d, st, &ctx->launches);
-  uint64_t* kkey = ctx->d<uint64_t>("c.kkey", nkl + 1);
-  uint32_t* kval = ctx->d<uint32_t>("c.kval", nkl + 1);
-  launch(ctx, k_compact_kernels, nkl, st, nkl, fa.kept, kpos, a.kl, kkey, kval, counters + 3);
-  launch(ctx, k_check_mono, nkl, st, nk_d, kkey, counters + 3);
-  xfer_small(htot, nk_d, 4, st);
-  xfer_small(htot + 1, counters + 3, 4, st);
+  // every entry kept and in timeline order (the common case, e.g. executions
+  // reordered across streams): no compaction, the kernel list is the order
+  xfer_small(htot, fa.drop, 8, st);
   XSP_CUDA(cudaStreamSynchronize(st));
-  const uint32_t nk = htot[0];
+  const bool all_kept = htot[0] == 0 && htot[1] == 0;
+  uint64_t* kkey = nullptr;
+  uint32_t* kval = nullptr;
+  uint32_t nk = nkl;
+  htot[1] = 0;
+  if (!all_kept) {
+    uint32_t* kpos = ctx->d<uint32_t>("c.kpos", nkl + 1);
+    uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
+    uint32_t* nk_d = ctx->d<uint32_t>("c.nk", 1);
+    exclusive_scan<uint32_t, uint32_t>(fa.kept, kpos, nkl, scan_tmp, nk_d, st, &ctx->launches);
+    kkey = ctx->d<uint64_t>("c.kkey", nkl + 1);
+    kval = ctx->d<uint32_t>("c.kval", nkl + 1);
+    launch(ctx, k_compact_kernels, nkl, st, nkl, fa.kept, kpos, a.kl, kkey, kval, counters + 3);
+    launch(ctx, k_check_mono, nkl, st, nk_d, kkey, counters + 3);
+    xfer_small(htot, nk_d, 4, st);
+    xfer_small(htot + 1, counters + 3, 4, st);
+    XSP_CUDA(cudaStreamSynchronize(st));
+    nk = htot[0];
+  }
   ctx->stage_end("fuse", st);
   if (htot[1]) {
     // explicit parents broke the timeline order of layers: stable sort by layer
@@ -2214,7 +2238,10 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   out->layer_dur = a.layer_dur;
   out->layer_attr_row = a.layer_attr_row;
   out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", nl + 1);
-  launch(ctx, k_layer_kernel_off, (uint64_t)nk + 1, st, nl, nk, kkey, out->layer_kernel_off);
+  if (all_kept)
+    launch(ctx, k_layer_kernel_off_kl, (uint64_t)nk + 1, st, nl, nk, a.kl, out->layer_kernel_off);
+  else
+    launch(ctx, k_layer_kernel_off, (uint64_t)nk + 1, st, nl, nk, kkey, out->layer_kernel_off);
   out->trace_layer_off = a.t_layer_off;
   out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
   launch(ctx, k_trace_kernel_off, (uint64_t)T + 1, st, T, a.t_layer_off, out->layer_kernel_off,
