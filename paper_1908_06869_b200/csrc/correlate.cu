@@ -1654,10 +1654,15 @@ __global__ void __launch_bounds__(256) k_gather_fast(const uint32_t* __restrict_
                               uint32_t* __restrict__ k_name, double* __restrict__ k_occ,
                               uint32_t* __restrict__ l_koff, uint32_t* __restrict__ fail) {
   const uint32_t nl = totals[0], nk = totals[1], nex = totals[2];
-  for (uint32_t base = blockIdx.x * blockDim.x; base <= nk; base += gridDim.x * blockDim.x)
+  // a batch found not clean is redone by the general path: stop early (the
+  // flag is polled every 16 strides so the clean case pays almost nothing)
+  uint32_t it = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base <= nk; base += gridDim.x * blockDim.x, ++it) {
+    if ((it & 15u) == 15u && __ldcg(fail)) return;
     gather_fast_one(base + threadIdx.x, base + (threadIdx.x & ~31u), nl, nk, nex, kl, ex, flags, t_kl_off,
                     t_ex_off, T, cid, name, occ, k_launch, k_exec, k_mrow, k_dur, k_name, k_occ, l_koff,
                     fail);
+  }
 }
 
 // layer_kernel_off[g] = first kernel j whose parent >= g (keys sorted): each
