@@ -505,7 +505,8 @@ def main():
     achieved = p1_bytes / (p1_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": "k_pass1 (parent join + list compaction, 1 launch/step)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_kind": peak_kind, "traffic": measured_traffic("k_pass1"), "bytes_per_launch": p1_bytes,
+                "peak_kind": peak_kind, "traffic": (measured_traffic("k_pass1") or {}).get("bytes"),
+                "traffic_source": measured_traffic("k_pass1"), "bytes_per_launch": p1_bytes,
                 "ms_per_launch": p1_ms}
     sv = survey_bytes(b)
     pipe_gbs = sv * world / (ms / 1e3) / 1e9
