@@ -1,3 +1,5 @@
+"""PCIe floor for bench.py e2e: 2.5 GB pinned H2D alone, then concurrently with a
+0.83 GB D2H (the per-step transfer volumes of a C3 xsp_run_host call)."""
 import torch, time
 n = 2_500_000_000
 h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
