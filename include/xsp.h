@@ -419,7 +419,10 @@ xsp_status xsp_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_o
 /* End-to-end convenience for host-resident inputs: copies the HOST columns to the
  * device, runs xsp_correlate + xsp_analyze, and copies every result column back
  * into ctx-owned pinned host memory (pointers in *corr_host / *tables_host are
- * HOST pointers valid until the next call). Synchronous. */
+ * HOST pointers valid until the next call). Synchronous. Large batches are cut
+ * at group boundaries into chunks whose copies and kernels overlap; with
+ * page-locked inputs the span_id column is read in place (zero-copy) by chunks
+ * without explicit-parent kernels (XSP_NO_ZERO_COPY=1 disables that). */
 xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* host_cols,
                         const xsp_traces* host_traces, const xsp_groups* groups,
                         const xsp_system_spec* spec, const xsp_analysis_opts* opts,
