@@ -36,8 +36,12 @@ class IntervalTree {
   std::size_t size() const { return entries_.size(); }
 
  private:
-  std::vector<Entry> entries_;            // by (begin_ns, span_id)
-  std::vector<std::uint64_t> prefix_end_; // running max of end_ns over entries_
+  std::vector<Entry> entries_;  // by (begin_ns, span_id)
+  // implicit balanced BST over entries_ (the node of [lo, hi) is mid = (lo + hi) / 2):
+  // subtree_max_end_[mid] = max end_ns over [lo, hi)
+  std::vector<std::uint64_t> subtree_max_end_;
+  std::uint64_t fill_max(std::size_t lo, std::size_t hi);
+  void query(std::size_t lo, std::size_t hi, std::uint64_t b, std::uint64_t e, std::vector<Entry>& out) const;
 };
 
 struct KernelExec {

@@ -88,6 +88,12 @@ __device__ __forceinline__ double trimmed_mean_any(Load load, uint32_t n, double
   if (n <= 8) return trimmed_mean_net<8>(load, n, f);
   if (n <= 16) return trimmed_mean_net<16>(load, n, f);
   if (n <= 32) return trimmed_mean_net<32>(load, n, f);
+  if (n > kMaxRuns)
+    return trimmed_mean_select(
+        [&](auto fn) {
+          for (uint32_t r = 0; r < n; ++r) fn((double)load(r));
+        },
+        n, f);
   double v[kMaxRuns];
   for (uint32_t r = 0; r < n; ++r) v[r] = load(r);
   return trimmed_mean_dev(v, n, f);
@@ -234,7 +240,6 @@ __global__ void k_group_status(uint32_t G, const uint32_t* __restrict__ nr,
   } else if (!(trim >= 0.0 && trim < 0.5)) {
     s = XSP_G_BAD_TRIM;
   }
-  if (nr[g] > kMaxRuns && s == XSP_G_OK) s = XSP_G_BAD_TRIM;  // unsupported run count
   status[g] = s;
   err_arg[g] = arg;
 }
@@ -612,6 +617,10 @@ __global__ void __launch_bounds__(64) k_models(ModelArgs a) {
         [&](uint32_t r) {
           const uint64_t lo = __shfl_sync(0xffffffffu, mdur, r & 31u);
           const uint64_t hi = __shfl_sync(0xffffffffu, mdur_hi, r & 31u);
+          if (r >= 64) {  // more than 64 runs: the rest straight from the model spans
+            const uint32_t m = a.model_row[t0 + r];
+            return clamp_dur(a.begin[m], a.end[m]);
+          }
           return r < 32 ? lo : hi;
         },
         R, a.trim);

@@ -741,6 +741,152 @@ __global__ void __launch_bounds__(P1_THREADS) k_p1_reduce(P1Args a, const __grid
   }
 }
 
+// ---- k_p1_reduce_lanes: the tile aggregates with one span per lane ----------
+// Same staging and outputs as k_p1_reduce; each warp folds its 256 spans as 8
+// chunks of 32 (lane = span): placement per lane, role counts by ballot, and the
+// containment state (last placed layer's end, max ends) by a segmented
+// max-scan over the lanes, carried warp-uniformly from chunk to chunk. The
+// warp aggregate is exactly the left fold of full_combine over its spans.
+__global__ void __launch_bounds__(P1_THREADS) k_p1_reduce_lanes(P1Args a, const __grid_constant__ P1Maps maps) {
+  extern __shared__ unsigned char red_dyn[];
+  RedSmem& sm = *reinterpret_cast<RedSmem*>(red_dyn + ((1024u - (smem_u32(red_dyn) & 1023u)) & 1023u));
+  __shared__ TraceCache tc;
+  __shared__ Full s_wagg[P1_WARPS];
+  __shared__ __align__(8) uint64_t s_bar;
+  const uint32_t tile = blockIdx.x, warp = threadIdx.x >> 5, lane = lane_id();
+  const uint64_t tile_base = (uint64_t)tile * P1_TILE;
+  const uint32_t tile_n = (uint32_t)min((uint64_t)P1_TILE, a.n - tile_base);
+  const bool bulk = a.bulk && tile_n == P1_TILE;
+  if (threadIdx.x == 0 && bulk) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&s_bar, P1_TILE * (3 * 8 + 1));
+    const int y = (int)(tile_base / 16);
+    tma_g2s_2d(sm.begin, &maps.begin, 0, y, &s_bar);
+    tma_g2s_2d(sm.end, &maps.end, 0, y, &s_bar);
+    tma_g2s_2d(sm.parent, &maps.parent, 0, y, &s_bar);
+    bulk_g2s(sm.flags, a.flags + tile_base, P1_TILE, &s_bar);
+  }
+  if (!bulk) {
+    for (uint32_t j = threadIdx.x; j < P1_TILE; j += P1_THREADS) {
+      const bool v = j < tile_n;
+      const uint64_t i = tile_base + j;
+      const uint32_t sw = sw128(j);
+      sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
+      sm.begin[sw] = v ? a.begin[i] : 0;
+      sm.end[sw] = v ? a.end[i] : 0;
+      sm.parent[sw] = v ? a.parent[i] : 0;
+    }
+  }
+  const uint32_t tlo = __ldg(a.tile_lo + tile), thi = __ldg(a.tile_hi + tile) + 1;
+  fill_trace_cache(a, tc, tlo, thi);
+  __syncthreads();
+  if (bulk) mbar_wait(&s_bar, 0);
+  const TileTraces tt{a, tc, tlo, thi - tlo <= (uint32_t)P1_TCACHE};
+  const uint32_t wj0 = warp * P1_SUB;
+  Full agg = full_identity();
+  if (wj0 < tile_n) {
+    uint32_t r = tt.find(tile_base + wj0, thi);
+    TraceAttrs ta;
+    tt.load(r, ta);
+    uint64_t lastE = 0, lastM = 0, runM = 0;
+    const uint32_t lt = lanemask_lt();
+    const uint32_t le = lt | (1u << lane);
+    for (int q = 0; q < P1_ITEMS; ++q) {
+      const uint32_t j = wj0 + (uint32_t)q * 32u + lane;
+      const bool valid = j < tile_n;
+      const uint32_t V = __ballot_sync(0xffffffffu, valid);
+      if (!V) break;
+      const uint64_t i = tile_base + j;
+      const uint32_t jj = valid ? j : wj0;
+      const uint8_t f = valid ? sm.flags[jj] : (uint8_t)0;
+      uint32_t rl = r;
+      TraceAttrs tl = ta;
+      const bool moved = valid && i >= ta.next;
+      const uint32_t MV = __ballot_sync(0xffffffffu, moved);
+      if (moved) {
+        do { ++rl; } while (tt.off(rl + 1) <= i);
+        tt.load(rl, tl);
+      }
+      const bool head = valid && i == tl.cur;
+      const bool is_layer = valid && f_level(f) == XSP_LEVEL_LAYER;
+      uint64_t e = 0;
+      bool placed = false;
+      if (is_layer && f_kind(f) == XSP_KIND_SYNC) {  // layer placement (correlator.cpp:168-194)
+        const uint64_t b = sm.begin[sw128(jj)];
+        e = sm.end[sw128(jj)];
+        placed = placed_in(tl, f, b, e, (f & XSP_F_PARENT) ? sm.parent[sw128(jj)] : 0);
+      }
+      const uint32_t P = __ballot_sync(0xffffffffu, placed);
+      const uint32_t H = __ballot_sync(0xffffffffu, head);
+      if (lane == 0) *reinterpret_cast<uint32_t*>(a.placed8 + ((tile_base + wj0) >> 3) + 4u * q) = P;
+      agg.c += __popc(P);
+      agg.head |= H != 0;
+      agg.c_lay += __popc(__ballot_sync(0xffffffffu, is_layer));
+      agg.c_metric += __popc(__ballot_sync(0xffffffffu, valid && (f & XSP_F_METRICS)));
+      agg.c_kl += __popc(__ballot_sync(0xffffffffu, valid && (is_kernel_launch(f) || is_sync_kernel(f))));
+      agg.c_ex += __popc(__ballot_sync(0xffffffffu, valid && is_exec(f) && (f & XSP_F_CID)));
+      if (P | H) {  // containment state: segmented max-scan of placed ends
+        const uint32_t Hle = H & le;
+        const int s = Hle ? 31 - __clz(Hle) : -1;
+        const uint64_t v = placed ? (e == ~0ull ? e : e + 1) : 0;
+        uint64_t R = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint64_t u = __shfl_up_sync(0xffffffffu, R, o);
+          if ((int)lane - o >= (s < 0 ? 0 : s)) R = max64(R, u);
+        }
+        if (s < 0) R = max64(R, runM);
+        uint64_t Rx = __shfl_up_sync(0xffffffffu, R, 1);
+        if ((int)lane == s) Rx = 0;
+        else if (lane == 0) Rx = runM;
+        const int s31 = H ? 31 - __clz(H) : -1;
+        const uint32_t Pt = P & (s31 > 0 ? ~((1u << s31) - 1u) : 0xffffffffu);
+        const int j31 = Pt ? 31 - __clz(Pt) : -1;
+        const uint64_t v31 = __shfl_sync(0xffffffffu, v, j31 < 0 ? 0 : j31);
+        const uint64_t rx31 = __shfl_sync(0xffffffffu, Rx, j31 < 0 ? 0 : j31);
+        runM = __shfl_sync(0xffffffffu, R, 31);
+        if (j31 >= 0) {
+          lastE = v31;
+          lastM = rx31;
+        } else if (s31 >= 0) {
+          lastE = lastM = 0;
+        }
+      }
+      if (MV) {
+        r = __shfl_sync(0xffffffffu, rl, 31);
+        tt.load(r, ta);
+      }
+    }
+    agg.last_end1 = lastE;
+    agg.last_M1 = lastM;
+    agg.run_M1 = runM;
+  }
+  if (lane == 0) s_wagg[warp] = agg;
+  __syncthreads();
+  if (warp != 0) return;
+  uint32_t last = 0;
+  if (lane < P1_WARPS) {
+    Full ex = full_identity();
+    for (uint32_t w = 0; w < lane; ++w) ex = full_combine(ex, s_wagg[w]);
+    a.warp_excl[(uint64_t)tile * P1_WARPS + lane] = ex;
+  }
+  if (lane == 0) {
+    Full t = s_wagg[0];
+    for (int w = 1; w < P1_WARPS; ++w) t = full_combine(t, s_wagg[w]);
+    a.tile_agg[tile] = t;
+    __threadfence();
+    const uint32_t g = tile >> 5, gsize = min(32u, a.ntiles - (g << 5));
+    last = atomicAdd(a.group_done + g, 1u) == gsize - 1;
+  }
+  if (__shfl_sync(0xffffffffu, last, 0)) {
+    __threadfence();
+    const uint32_t g = tile >> 5, k = (g << 5) + lane;
+    const Full v = warp_reduce_ordered(k < a.ntiles ? ld_full_cg(a.tile_agg + k) : full_identity(), lane);
+    if (lane == 0) a.group_sum[g] = v;
+  }
+}
+
 // ---- k_p1_scan: exclusive prefixes of the 32-tile group totals -------------
 // One CTA. The group totals come from k_p1_reduce (the last tile of each group
 // to finish reduces the group); a block scan gives gprefix[g] (exclusive) and
@@ -924,9 +1070,11 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
       } else {
         const bool in_j = lastE > e;  // end_j >= e (ends stored +1)
         const bool in_m = lastM > e;  // an earlier layer has end >= e
+        // e == UINT64_MAX: the saturated +1 encoding cannot tell end_j == e from
+        // end_j == e - 1, so the exact rare path decides
         if (in_j && !in_m) {
           par = g - 1;
-        } else if (!in_j && !in_m) {
+        } else if (!in_j && !in_m && e != ~0ull) {
           par = PAR_ORPHAN;
           emit_orphan(a.orph, t, CAT_KERNEL, i, (uint32_t)i, XSP_O_KERNEL_NO_LAYER);
         } else {
@@ -1011,7 +1159,9 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
       pf = f;
 
       // trace errors raised while walking the bundle (correlator.cpp:146-158)
-      if (is_model_span(f) && (uint32_t)i != ta.model)
+      // (the reference compares span ids: a second model span sharing the
+      // model's span_id is not an error)
+      if (is_model_span(f) && (uint32_t)i != ta.model && __ldg(a.span_id + i) != ta.msid)
         atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_MULTI_MODEL);
       if (f_level(f) >= XSP_LEVEL_KERNEL && !(ta.levels & (1u << XSP_LEVEL_LAYER)))
         atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_SKIP_LEVEL);
@@ -1051,7 +1201,7 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
           const bool in_m = lastM > e;  // an earlier layer has end >= e
           if (in_j && !in_m) {
             par = g - 1;
-          } else if (!in_j && !in_m) {
+          } else if (!in_j && !in_m && e != ~0ull) {  // e == UINT64_MAX: exact rare path
             par = PAR_ORPHAN;
             emit_orphan(a.orph, t, CAT_KERNEL, i, (uint32_t)i, XSP_O_KERNEL_NO_LAYER);
           } else {
@@ -1081,6 +1231,252 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
         } else if (!a.parents_only) {
           emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
         }
+      }
+    }
+  }
+}
+// ---- k_pass1_lanes: per-span outputs, one span per lane ------------------------
+// The same outputs as k_pass1, but each warp walks its 256 spans as 8 chunks of
+// 32 with lane = span, carrying the scan state (counts, last placed layer's
+// end, max ends) warp-uniformly from chunk to chunk; the warp's starting state
+// is k_p1_reduce's warp prefix, so nothing of phase 1 is recomputed. Within a
+// chunk:
+//   * list positions are the carried counts plus ballot prefix counts, so the
+//     entries of one list that a chunk emits are consecutive and their stores
+//     coalesce (the thread-serial walk stored at 32 scattered positions);
+//   * the containment state of a child lane is its segment's (trace's) last
+//     placed layer j before it and the max end over placed layers before j: a
+//     segmented max-scan of placed-layer ends over the lanes (segments start at
+//     trace heads) plus the carry — the same decision as k_pass1's per-thread
+//     walk, bit for bit.
+__global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1_lanes(P1Args a, const __grid_constant__ P1Maps maps) {
+  extern __shared__ unsigned char p1_dyn[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(p1_dyn + ((1024u - (smem_u32(p1_dyn) & 1023u)) & 1023u));
+  __shared__ TraceCache tc;
+  __shared__ __align__(8) uint64_t s_bar;
+
+  const uint32_t tile = blockIdx.x, warp = threadIdx.x >> 5, lane = lane_id();
+  const TileHdr hd = tile_hdr(a, tile);
+  const uint64_t tile_base = hd.tile_base;
+  const uint32_t tile_n = hd.tile_n, tlo = hd.tlo, thi = hd.thi;
+  const bool bulk = a.bulk && tile_n == P1_TILE;
+  if (threadIdx.x == 0 && bulk) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&s_bar, P1_TILE * (3 * 8 + 1));
+    const int y = (int)(tile_base / 16);
+    tma_g2s_2d(sm.begin, &maps.begin, 0, y, &s_bar);
+    tma_g2s_2d(sm.end, &maps.end, 0, y, &s_bar);
+    tma_g2s_2d(sm.cid, &maps.cid, 0, y, &s_bar);
+    bulk_g2s(sm.flags, a.flags + tile_base, P1_TILE, &s_bar);
+  }
+  fill_trace_cache(a, tc, tlo, thi);
+  const uint32_t wj0 = warp * P1_SUB;
+  Full cs = full_identity();
+  if (wj0 < tile_n) cs = full_combine(a.tile_excl[tile], a.warp_excl[(uint64_t)tile * P1_WARPS + warp]);
+  if (!bulk) {
+    for (uint32_t j = threadIdx.x; j < P1_TILE; j += P1_THREADS) {
+      const bool v = j < tile_n;
+      const uint64_t i = tile_base + j;
+      const uint32_t sw = sw128(j);
+      sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
+      sm.begin[sw] = v ? a.begin[i] : 0;
+      sm.end[sw] = v ? a.end[i] : 0;
+      sm.cid[sw] = v ? a.cid[i] : 0;
+    }
+  }
+  __syncthreads();
+  if (bulk) mbar_wait(&s_bar, 0);
+  if (wj0 >= tile_n) return;
+  const TileTraces tt{a, tc, tlo, thi - tlo <= (uint32_t)P1_TCACHE};
+  // warp-uniform state
+  uint32_t g = cs.c, c_metric = cs.c_metric, c_lay = cs.c_lay, c_kl = cs.c_kl, c_ex = cs.c_ex;
+  uint64_t lastE = cs.last_end1, lastM = cs.last_M1, runM = cs.run_M1;
+  uint32_t r = tt.find(tile_base + wj0, thi);
+  TraceAttrs ta;
+  tt.load(r, ta);
+  uint64_t pb = 0;  // the span before the chunk (timeline-order check)
+  uint32_t pf = 0;
+  {
+    const uint64_t wi0 = tile_base + wj0;
+    if (wi0 > 0) {
+      pb = wj0 > 0 ? sm.begin[sw128(wj0 - 1)] : __ldg(a.begin + wi0 - 1);
+      pf = wj0 > 0 ? sm.flags[wj0 - 1] : __ldg(a.flags + wi0 - 1);
+    }
+  }
+  const uint32_t lt = lanemask_lt();
+  const uint32_t le = lt | (1u << lane);
+  for (int q = 0; q < P1_ITEMS; ++q) {
+    const uint32_t j = wj0 + (uint32_t)q * 32u + lane;
+    const bool valid = j < tile_n;
+    const uint32_t V = __ballot_sync(0xffffffffu, valid);
+    if (!V) break;
+    const uint64_t i = tile_base + j;
+    const uint32_t jj = valid ? j : wj0;
+    const uint8_t f = valid ? sm.flags[jj] : (uint8_t)0;
+    const uint64_t b = sm.begin[sw128(jj)];
+    const uint64_t e = sm.end[sw128(jj)];
+    // placed-layer bits of the chunk (k_p1_reduce): 32 spans = 4 aligned bytes
+    uint32_t P = 0;
+    if (lane == 0) P = *reinterpret_cast<const uint32_t*>(a.placed8 + ((tile_base + wj0) >> 3) + 4u * q);
+    P = __shfl_sync(0xffffffffu, P, 0) & V;
+    // the lane's trace: the warp's current one unless a trace starts inside the chunk
+    uint32_t rl = r;
+    TraceAttrs tl = ta;
+    const bool moved = valid && i >= ta.next;
+    const uint32_t MV = __ballot_sync(0xffffffffu, moved);
+    if (moved) {
+      do { ++rl; } while (tt.off(rl + 1) <= i);
+      tt.load(rl, tl);
+    }
+    const uint32_t t = tlo + rl;
+    const bool head = valid && i == tl.cur;
+    const bool is_layer = valid && f_level(f) == XSP_LEVEL_LAYER;
+    const bool klr = valid && (is_kernel_launch(f) || is_sync_kernel(f));
+    const bool exr = valid && is_exec(f);
+    const bool has_cid = (f & XSP_F_CID) != 0;
+    const bool met = valid && (f & XSP_F_METRICS) != 0;
+    const bool placed = (P >> lane) & 1u;
+    const uint32_t H = __ballot_sync(0xffffffffu, head);
+    const uint32_t LAY = __ballot_sync(0xffffffffu, is_layer);
+    const uint32_t KL = __ballot_sync(0xffffffffu, klr);
+    const uint32_t EXC = __ballot_sync(0xffffffffu, exr && has_cid);
+    const uint32_t MET = __ballot_sync(0xffffffffu, met);
+    const uint32_t gpos = g + __popc(P & lt);
+    const uint32_t klpos = c_kl + __popc(KL & lt);
+    const uint32_t expos = c_ex + __popc(EXC & lt);
+    const uint32_t mrow = c_metric + __popc(MET & lt);
+    // segment (trace) of the lane inside the chunk: it starts at the last head
+    // lane <= lane, or continues the carried state when there is none
+    const uint32_t Hle = H & le;
+    const int s = Hle ? 31 - __clz(Hle) : -1;
+    const uint64_t v = placed ? (e == ~0ull ? e : e + 1) : 0;  // ends stored +1 (0 = none)
+    uint64_t R = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xffffffffu, R, o);
+      if ((int)lane - o >= (s < 0 ? 0 : s)) R = max64(R, u);
+    }
+    if (s < 0) R = max64(R, runM);  // inclusive: max end over the segment's placed layers up to the lane
+    uint64_t Rx = __shfl_up_sync(0xffffffffu, R, 1);
+    if ((int)lane == s) Rx = 0;
+    else if (lane == 0) Rx = runM;  // (s < 0 here)
+    // last placed layer before the lane within its segment
+    const uint32_t Pb = P & lt & (s > 0 ? ~((1u << s) - 1u) : 0xffffffffu);
+    const int jl = Pb ? 31 - __clz(Pb) : -1;
+    const uint64_t vj = __shfl_sync(0xffffffffu, v, jl < 0 ? 0 : jl);
+    const uint64_t Rxj = __shfl_sync(0xffffffffu, Rx, jl < 0 ? 0 : jl);
+    const uint64_t lE = jl >= 0 ? vj : (s >= 0 ? 0 : lastE);
+    const uint64_t lM = jl >= 0 ? Rxj : (s >= 0 ? 0 : lastM);
+    // timeline order (begin_ns, rank, span_id) within the trace (span.hpp:161-163)
+    uint64_t pbl = __shfl_up_sync(0xffffffffu, b, 1);
+    uint32_t pfl = __shfl_up_sync(0xffffffffu, (uint32_t)f, 1);
+    if (lane == 0) {
+      pbl = pb;
+      pfl = pf;
+    }
+    if (valid && !head && i > 0 && pbl >= b) {
+      bool bad = pbl > b;
+      if (!bad) {
+        const uint32_t l0 = f_level((uint8_t)pfl), l1 = f_level(f);
+        const uint32_t r0_ = l0 >= 2 ? 3 : l0 + 1, r1_ = l1 >= 2 ? 3 : l1 + 1;
+        bad = r0_ > r1_ || (r0_ == r1_ && __ldg(a.span_id + i - 1) > __ldg(a.span_id + i));
+      }
+      if (bad) atomicOr(a.unsorted, 1u);
+    }
+    if (head) {  // offsets of this trace and the empty traces right before it
+      int64_t tx = t;
+      do {
+        a.t_layer_off[tx] = gpos;
+        a.t_kl_off[tx] = klpos;
+        a.t_ex_off[tx] = expos;
+        --tx;
+      } while (tx >= 0 && __ldg(a.off + tx) == i);
+    }
+    // trace errors raised while walking the bundle (correlator.cpp:146-158); the
+    // model check compares span ids as the reference does
+    if (valid && is_model_span(f) && (uint32_t)i != tl.model && __ldg(a.span_id + i) != tl.msid)
+      atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_MULTI_MODEL);
+    if (valid && f_level(f) >= XSP_LEVEL_KERNEL && !(tl.levels & (1u << XSP_LEVEL_LAYER)))
+      atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_SKIP_LEVEL);
+    // layers (correlator.cpp:168-212)
+    if (placed) {
+      a.layer_row[gpos] = (uint32_t)i;
+      a.layer_dur[gpos] = clamp_dur(b, e);
+      a.layer_attr_row[gpos] = c_lay + __popc(LAY & lt);
+    } else if (is_layer) {
+      emit_orphan(a.orph, t, CAT_LAYER, i, (uint32_t)i,
+                  f_kind(f) != XSP_KIND_SYNC ? XSP_O_LAYER_NON_SYNC
+                                             : ((f & XSP_F_PARENT) ? XSP_O_LAYER_BAD_PARENT
+                                                                   : XSP_O_LAYER_OUTSIDE_MODEL));
+    }
+    // kernel launches and synchronous kernels (correlator.cpp:226-268)
+    if (klr) {
+      uint32_t par;
+      if (f & XSP_F_PARENT) {
+        par = PAR_PENDING;
+        const uint32_t sl = atomicAdd(a.pend_count, 1u);
+        if (sl < a.pend_cap) a.pend_kl[sl] = klpos;
+      } else {
+        const bool in_j = lE > e;  // end_j >= e (ends stored +1)
+        const bool in_m = lM > e;  // an earlier layer has end >= e
+        if (in_j && !in_m) {
+          par = gpos - 1;
+        } else if (!in_j && !in_m && e != ~0ull) {  // e == UINT64_MAX: exact rare path
+          par = PAR_ORPHAN;
+          emit_orphan(a.orph, t, CAT_KERNEL, i, (uint32_t)i, XSP_O_KERNEL_NO_LAYER);
+        } else {
+          par = PAR_AMBIG;
+          const uint32_t sl = atomicAdd(a.amb_count, 1u);
+          if (sl < a.amb_cap) {
+            a.amb_kl[sl] = klpos;
+            a.amb_gx[sl] = gpos;
+          }
+        }
+      }
+      KlEnt ent;
+      ent.row = (uint32_t)i;
+      ent.parent = par;
+      ent.cid = has_cid ? sm.cid[sw128(jj)] : 0;
+      a.kl[klpos] = ent;
+      if (is_sync_kernel(f)) a.kl_mrow[klpos] = met ? mrow : kNone;
+    }
+    // executions: with a cid into the exec list, without one an orphan
+    if (exr) {
+      if (has_cid) {
+        ExEnt ent;
+        ent.row = (uint32_t)i;
+        ent.mrow = met ? mrow : kNone;
+        ent.dur = clamp_dur(b, e);
+        a.ex[expos] = ent;
+      } else if (!a.parents_only) {
+        emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
+      }
+    }
+    // carry to the next chunk: the state after lane 31
+    {
+      const int s31 = H ? 31 - __clz(H) : -1;
+      const uint32_t Pt = P & (s31 > 0 ? ~((1u << s31) - 1u) : 0xffffffffu);
+      const int j31 = Pt ? 31 - __clz(Pt) : -1;
+      const uint64_t v31 = __shfl_sync(0xffffffffu, v, j31 < 0 ? 0 : j31);
+      const uint64_t rx31 = __shfl_sync(0xffffffffu, Rx, j31 < 0 ? 0 : j31);
+      runM = __shfl_sync(0xffffffffu, R, 31);
+      if (j31 >= 0) {
+        lastE = v31;
+        lastM = rx31;
+      } else if (s31 >= 0) {
+        lastE = lastM = 0;
+      }
+      g += __popc(P);
+      c_lay += __popc(LAY);
+      c_kl += __popc(KL);
+      c_ex += __popc(EXC);
+      c_metric += __popc(MET);
+      pb = __shfl_sync(0xffffffffu, b, 31);
+      pf = __shfl_sync(0xffffffffu, (uint32_t)f, 31);
+      if (MV) {
+        r = __shfl_sync(0xffffffffu, rl, 31);
+        tt.load(r, ta);
       }
     }
   }
@@ -1167,12 +1563,14 @@ __global__ void k_amb_resolve(uint32_t n_raw, const uint32_t* __restrict__ amb_k
                               const uint32_t* __restrict__ amb_gx, KlEnt* __restrict__ kl,
                               const uint64_t* __restrict__ end, const uint32_t* __restrict__ t_kl_off,
                               const uint32_t* __restrict__ t_layer_off, uint32_t T,
-                              const uint32_t* __restrict__ layer_row, uint32_t* __restrict__ keep) {
+                              const uint32_t* __restrict__ layer_row, uint32_t* __restrict__ keep,
+                              Orphans orph) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_raw) return;
   const uint32_t k = amb_kl[p];
   const uint32_t t = trace_of32(t_kl_off, T, k);
-  const uint64_t e = end[kl[k].row];
+  const uint32_t row = kl[k].row;
+  const uint64_t e = end[row];
   const uint32_t lo = t_layer_off[t];
   uint32_t cnt = 0, last = kNone;
   for (uint32_t g = amb_gx[p]; g > lo && cnt < 2;) {
@@ -1185,6 +1583,10 @@ __global__ void k_amb_resolve(uint32_t n_raw, const uint32_t* __restrict__ amb_k
   if (cnt == 1) {
     kl[k].parent = last;
     keep[p] = 0;
+  } else if (cnt == 0) {  // only for a child ending at UINT64_MAX (see k_pass1)
+    kl[k].parent = PAR_ORPHAN;
+    keep[p] = 0;
+    emit_orphan(orph, t, CAT_KERNEL, row, row, XSP_O_KERNEL_NO_LAYER);
   } else {
     keep[p] = 1;
   }
@@ -1952,8 +2354,15 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   if (ntiles) {
     XSP_CUDA(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM));
     ctx->stage_begin("pass1_reduce", st);
-    XSP_CUDA(cudaFuncSetAttribute(k_p1_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_RED_SMEM));
-    k_p1_reduce<<<ntiles, P1_THREADS, P1_RED_SMEM, st>>>(a, maps);
+    static const bool serial_reduce = getenv("XSP_P1_SERIAL_REDUCE") != nullptr;
+    if (serial_reduce) {
+      XSP_CUDA(cudaFuncSetAttribute(k_p1_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_RED_SMEM));
+      k_p1_reduce<<<ntiles, P1_THREADS, P1_RED_SMEM, st>>>(a, maps);
+    } else {
+      XSP_CUDA(cudaFuncSetAttribute(k_p1_reduce_lanes, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)P1_RED_SMEM));
+      k_p1_reduce_lanes<<<ntiles, P1_THREADS, P1_RED_SMEM, st>>>(a, maps);
+    }
     ctx->stage_end("pass1_reduce", st);
     ctx->stage_begin("pass1_scan", st);
     k_p1_scan<<<1, P1_SCAN_THREADS, 0, st>>>(a.group_sum, (ntiles + 31) / 32, a.tile_prefix);
@@ -1961,7 +2370,13 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
                                                                            a.tile_excl);
     ctx->stage_end("pass1_scan", st);
     ctx->stage_begin("pass1", st);
-    k_pass1<<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
+    static const bool serial_emit = getenv("XSP_P1_SERIAL") != nullptr;
+    if (serial_emit) {
+      k_pass1<<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
+    } else {
+      XSP_CUDA(cudaFuncSetAttribute(k_pass1_lanes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM));
+      k_pass1_lanes<<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
+    }
     ctx->stage_end("pass1", st);
     ctx->launches += 4;
   }
@@ -2062,7 +2477,7 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     uint32_t* keep = ctx->d<uint32_t>("c.amb_keep", n_amb_raw + 1);
     uint32_t* pos = ctx->d<uint32_t>("c.amb_pos", n_amb_raw + 1);
     launch(ctx, k_amb_resolve, n_amb_raw, st, n_amb_raw, a.amb_kl, a.amb_gx, a.kl, c->end_ns, a.t_kl_off,
-           a.t_layer_off, T, a.layer_row, keep);
+           a.t_layer_off, T, a.layer_row, keep, orph);
     uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
     exclusive_scan<uint32_t, uint32_t>(keep, pos, n_amb_raw, scan_tmp, counters + 6, st, &ctx->launches);
     uint32_t* kl2 = ctx->d<uint32_t>("c.amb_kl2", n_amb_raw);

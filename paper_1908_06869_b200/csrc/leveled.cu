@@ -133,27 +133,35 @@ __global__ void k_lev_latency(LevArgs a) {
   const bool set_has = lv == XSP_LEVEL_MODEL ||
                        (has_level(mask, XSP_LEVEL_LAYER) &&
                         (lv == XSP_LEVEL_LAYER || has_level(mask, XSP_LEVEL_KERNEL)));
-  if (set_has) {
+  // every run of the set that holds the event, in run order
+  auto each = [&](auto fn) {
     const uint32_t li = a.ev_layer[e], ki = a.ev_kernel[e];
-    for (uint32_t q = a.soff[s]; q < a.soff[s + 1] && n < kMaxRunsL; ++q) {
+    for (uint32_t q = a.soff[s]; q < a.soff[s + 1]; ++q) {
       const uint32_t t = a.tr[q];
       if (lv == XSP_LEVEL_MODEL) {
         const uint32_t m = a.model_row[t];
-        v[n++] = (double)clamp_dur(a.begin[m], a.end[m]);
+        fn((double)clamp_dur(a.begin[m], a.end[m]));
         continue;
       }
       const uint32_t l0 = a.t_layer_off[t];
       if (li >= a.t_layer_off[t + 1] - l0) continue;
       if (lv == XSP_LEVEL_LAYER) {
-        v[n++] = (double)a.layer_dur[l0 + li];
+        fn((double)a.layer_dur[l0 + li]);
       } else {
         const uint32_t g = l0 + li;
         if (ki >= a.l_koff[g + 1] - a.l_koff[g]) continue;
-        v[n++] = (double)a.kernel_dur[a.l_koff[g] + ki];
+        fn((double)a.kernel_dur[a.l_koff[g] + ki]);
       }
     }
+  };
+  if (set_has) {
+    each([&](double x) {
+      if (n < kMaxRunsL) v[n] = x;
+      ++n;
+    });
   }
-  a.lat[q] = n ? trimmed_mean_l(v, n, a.trim) : nan("");
+  // more than kMaxRunsL samples: selection over the runs instead of a sort
+  a.lat[q] = !n ? nan("") : n <= kMaxRunsL ? trimmed_mean_l(v, n, a.trim) : trimmed_mean_select(each, n, a.trim);
 }
 
 // per chain step: overhead = wide - narrow with the clamp rule (:182-203); the
@@ -280,8 +288,6 @@ void run_leveled(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     const uint32_t s = order[i];
     hs[i] = q;                      // soff
     hs[NS + 1 + i] = sets->levels[s];
-    if (sets->set_off[s + 1] - sets->set_off[s] > (uint32_t)kMaxRunsL)
-      throw std::invalid_argument("more than 64 runs in a level set");
     for (uint32_t k = sets->set_off[s]; k < sets->set_off[s + 1]; ++k) htr[q++] = sets->trace_idx[k];
   }
   hs[NS] = q;

@@ -264,4 +264,38 @@ inline void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t n, int lo_
   }
 }
 
+
+// trimmed_mean (analysis.cpp:28-39) of any number of samples without storing
+// them: the distinct values are visited in ascending order by repeated minimum
+// selection (each(fn) calls fn(x) for every sample, in any order), and the ranks
+// [drop, n - drop) are summed left to right exactly as the reference sums its
+// sorted vector. O(n * distinct) loads: the path for groups with more runs than
+// the register sorting networks hold (kept warp-uniform when `each` is).
+template <typename Each>
+__device__ __forceinline__ double trimmed_mean_select(Each each, uint32_t n, double f) {
+  const uint32_t drop = (uint32_t)floor(f * (double)n);
+  double s = 0.0, cur = 0.0;
+  bool first = true;
+  uint32_t pos = 0;
+  while (pos < n) {
+    double v = 0.0;
+    bool found = false;
+    each([&](double x) {
+      if ((first || x > cur) && (!found || x < v)) {
+        v = x;
+        found = true;
+      }
+    });
+    if (!found) break;  // unordered samples (NaN): nothing left to rank
+    uint32_t c = 0;
+    each([&](double x) { c += x == v; });
+    for (uint32_t k = pos; k < pos + c; ++k)
+      if (k >= drop && k < n - drop) s = __dadd_rn(s, v);
+    cur = v;
+    first = false;
+    pos += c;
+  }
+  return s / (double)(n - 2 * drop);
+}
+
 }  // namespace xsp

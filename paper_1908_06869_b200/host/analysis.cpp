@@ -94,7 +94,6 @@ struct Tables {
       case XSP_G_KERNEL_COUNT:
         throw AnalysisError("repetitions disagree on kernel count of layer " + std::to_string(err_arg[g]));
       case XSP_G_BAD_TRIM:
-        if (groups[g]->runs.size() > 64) throw AnalysisError("more than 64 repetitions in one analysis input");
         throw AnalysisError("trim fraction must lie in [0, 0.5)");
       default: throw AnalysisError("analysis failed");
     }

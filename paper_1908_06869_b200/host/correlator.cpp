@@ -11,10 +11,11 @@
 
 namespace strata {
 
-// ---- IntervalTree: begin-sorted entries with a running maximum of end_ns.
-// Every entry that can contain [b, e] has begin <= b, i.e. lies in the prefix
-// found by binary search; walking that prefix backwards stops as soon as the
-// running maximum drops below e.
+// ---- IntervalTree (correlator.cpp:66-126): entries sorted by (begin_ns, span_id),
+// an implicit balanced BST over that array (node of [lo, hi) = its midpoint)
+// augmented with the subtree maximum of end_ns. A query prunes a subtree whose
+// maximum end is below e and the right part of any node that begins after b:
+// O(log n + k) per query, as the reference's augmented tree.
 
 IntervalTree IntervalTree::build(const std::vector<Span>& spans) {
   IntervalTree t;
@@ -23,23 +24,36 @@ IntervalTree IntervalTree::build(const std::vector<Span>& spans) {
   std::sort(t.entries_.begin(), t.entries_.end(), [](const Entry& a, const Entry& b) {
     return std::tie(a.begin_ns, a.span_id) < std::tie(b.begin_ns, b.span_id);
   });
-  t.prefix_end_.resize(t.entries_.size());
-  std::uint64_t m = 0;
-  for (std::size_t i = 0; i < t.entries_.size(); ++i) {
-    m = std::max(m, t.entries_[i].end_ns);
-    t.prefix_end_[i] = m;
-  }
+  t.subtree_max_end_.assign(t.entries_.size(), 0);
+  t.fill_max(0, t.entries_.size());
   return t;
+}
+
+std::uint64_t IntervalTree::fill_max(std::size_t lo, std::size_t hi) {
+  if (lo >= hi) return 0;
+  const std::size_t mid = lo + (hi - lo) / 2;
+  std::uint64_t m = entries_[mid].end_ns;
+  m = std::max(m, fill_max(lo, mid));
+  m = std::max(m, fill_max(mid + 1, hi));
+  subtree_max_end_[mid] = m;
+  return m;
+}
+
+void IntervalTree::query(std::size_t lo, std::size_t hi, std::uint64_t b, std::uint64_t e,
+                         std::vector<Entry>& out) const {
+  while (lo < hi) {
+    const std::size_t mid = lo + (hi - lo) / 2;
+    if (subtree_max_end_[mid] < e) return;  // nothing in [lo, hi) reaches e
+    query(lo, mid, b, e, out);
+    if (entries_[mid].begin_ns > b) return;  // mid and everything right of it begin after b
+    if (entries_[mid].end_ns >= e) out.push_back(entries_[mid]);
+    lo = mid + 1;  // right subtree (tail iteration)
+  }
 }
 
 std::vector<IntervalTree::Entry> IntervalTree::containing(std::uint64_t b, std::uint64_t e) const {
   std::vector<Entry> out;
-  auto ub = std::upper_bound(entries_.begin(), entries_.end(), b,
-                             [](std::uint64_t v, const Entry& x) { return v < x.begin_ns; });
-  for (std::size_t i = static_cast<std::size_t>(ub - entries_.begin()); i-- > 0;) {
-    if (prefix_end_[i] < e) break;
-    if (entries_[i].end_ns >= e) out.push_back(entries_[i]);
-  }
+  query(0, entries_.size(), b, e, out);
   std::sort(out.begin(), out.end(), [](const Entry& x, const Entry& y) { return x.span_id < y.span_id; });
   return out;
 }
@@ -70,6 +84,38 @@ bool in_timeline_order(const std::vector<Span>& spans) {
   return true;
 }
 
+// Emission phase of an orphan (correlator.cpp:168-363): 0 layer pass, 1 kernel
+// pass, 2 execution without cid — these three walk bundle.spans in order —
+// then 3 launch fusion (tree order) and 4 leftover executions (by span_id).
+int orphan_phase(const std::string& reason) {
+  if (reason == "layer-level span with non-sync kind" || reason == "outside the model interval" ||
+      reason.ends_with("is not the model span"))
+    return 0;
+  if (reason == "contained in no layer interval" || reason.ends_with("is not a layer in the tree")) return 1;
+  if (reason == "execution record without correlation id") return 2;
+  return 3;
+}
+
+// A bundle out of timeline order (outside the TraceBundle contract, span.hpp)
+// is correlated in timeline order; the reference walks such a bundle in file
+// order, which only changes the order of the orphans its span walks emit
+// (phases 0-2): those are put back into file order here.
+void file_order_orphans(const TraceBundle& original, CorrelationResult& r) {
+  std::unordered_map<std::uint64_t, std::size_t> pos;
+  for (std::size_t i = original.spans.size(); i-- > 0;) pos[original.spans[i].span_id] = i;
+  auto& o = r.tree.orphans;
+  std::size_t a = 0;
+  while (a < o.size()) {
+    const int ph = orphan_phase(o[a].reason);
+    std::size_t b = a + 1;
+    while (b < o.size() && orphan_phase(o[b].reason) == ph) ++b;
+    if (ph < 3)
+      std::stable_sort(o.begin() + a, o.begin() + b,
+                       [&](const OrphanSpan& x, const OrphanSpan& y) { return pos[x.span_id] < pos[y.span_id]; });
+    a = b;
+  }
+}
+
 // One GPU pass over `bundles`; results[i] valid iff errors[i] is empty.
 void correlate_batch(const std::vector<const TraceBundle*>& in, int mode, std::vector<CorrelationResult>& results,
                      std::vector<std::string>& errors) {
@@ -77,14 +123,14 @@ void correlate_batch(const std::vector<const TraceBundle*>& in, int mode, std::v
   // (TraceBundle invariant, span.hpp); sorted copies are made on the GPU
   std::vector<TraceBundle> copies;
   std::vector<const TraceBundle*> bundles = in;
-  for (std::size_t i = 0; i < in.size(); ++i)
-    if (!in_timeline_order(in[i]->spans)) copies.reserve(copies.size() + 1);
+  std::vector<bool> resorted(in.size(), false);
   copies.reserve(in.size());
   for (std::size_t i = 0; i < in.size(); ++i) {
     if (in_timeline_order(in[i]->spans)) continue;
     copies.push_back(*in[i]);
     sort_timeline(copies.back().spans);
     bundles[i] = &copies.back();
+    resorted[i] = true;
   }
   const b200::PackedSpans p = b200::pack_bundles(bundles);
   const b200::HostCorr c = b200::run_correlation(p, mode);
@@ -96,6 +142,7 @@ void correlate_batch(const std::vector<const TraceBundle*>& in, int mode, std::v
       continue;
     }
     results[t] = b200::unpack_result(p, c, t);
+    if (resorted[t]) file_order_orphans(*in[t], results[t]);
   }
 }
 
@@ -124,10 +171,40 @@ CorrelationResult assign_parents(const TraceBundle& bundle) {
   return correlate_one(bundle, XSP_CORR_PARENTS_ONLY);
 }
 
-// The device computes assign_parents and the fusion in one pass; for a result
-// that came from assign_parents(bundle) (the only input the reference accepts
-// meaningfully) this equals running the fusion step on it.
+namespace {
+
+// Same tree shape and exception lists, compared by span ids (the tree holds
+// copies of the bundle's spans).
+bool same_parent_assignment(const CorrelationResult& a, const CorrelationResult& b) {
+  if (a.tree.root.span.span_id != b.tree.root.span.span_id) return false;
+  if (a.tree.root.layers.size() != b.tree.root.layers.size()) return false;
+  for (std::size_t i = 0; i < a.tree.root.layers.size(); ++i) {
+    const LayerExec& x = a.tree.root.layers[i];
+    const LayerExec& y = b.tree.root.layers[i];
+    if (x.span.span_id != y.span.span_id || x.layer_index != y.layer_index ||
+        x.kernels.size() != y.kernels.size())
+      return false;
+    for (std::size_t k = 0; k < x.kernels.size(); ++k) {
+      if (x.kernels[k].launch.span_id != y.kernels[k].launch.span_id) return false;
+      if (x.kernels[k].exec.has_value() != y.kernels[k].exec.has_value()) return false;
+    }
+  }
+  return a.tree.orphans == b.tree.orphans && a.ambiguities == b.ambiguities;
+}
+
+}  // namespace
+
+// correlate_async (correlator.cpp:287-364) fuses the launches of `result`'s
+// tree with the bundle's execution records. The device computes the parent
+// assignment and that fusion in one pass, so the given result must be the
+// parent assignment of `bundle` (what assign_parents returns, and the only
+// input the reference documents, correlator.hpp:144-146); it is checked, on
+// the GPU, against assign_parents(bundle), and a result that was edited after
+// assign_parents is rejected with a UsageError instead of being replaced.
 void correlate_async(CorrelationResult& result, const TraceBundle& bundle) {
+  if (!same_parent_assignment(result, correlate_one(bundle, XSP_CORR_PARENTS_ONLY)))
+    throw UsageError("correlate_async: result is not assign_parents(bundle); the B200 drop-in fuses "
+                     "unmodified parent assignments only");
   result = correlate_one(bundle, 0);
 }
 

@@ -221,22 +221,29 @@ def c3(runs: int = 20, n_models: int = 65, batches=(1, 2, 4, 8, 16, 32, 64, 128)
     return corpus(make_models(n_models, seed=seed, **kw), batches, runs, seed=seed + 1000)
 
 
-def c4(n_layers: int = 1_000_000, seed: int = 4, streams: int = 4, block_layers: int = 2000,
-       long_frac: float = 0.01, long_max: int = 64, kernels: int = 3) -> SpanBatch:
+def c4(n_layers: int = 1_000_000, seed: int = 4, streams: int = 4, drain_every: int = 0,
+       long_frac: float = 0.01, long_max: int = 64, kernels: int = 3, concurrent_frac: float = 0.001,
+       chunk_layers: int = 65536) -> SpanBatch:
     """BASELINE config 4: ONE long-running trace (model span + n_layers layers).
 
     * Layers run back to back; a layer has `kernels` launches, or U{8..long_max}
       for a `long_frac` share of "long" layers (deep nesting within the 3-level
-      model), launches packed from the layer begin (simprof build_plan shape).
+      model), launches packed from the layer begin (simprof build_plan shape,
+      simprof.cpp:203-271).
+    * A `concurrent_frac` share of layers open a concurrent group of two: both
+      layers begin at the group begin, both launch from it, and the next group
+      starts at the later end (simprof.cpp:237-241). Their launches lie inside
+      both layers, which makes them ambiguities (correlator.cpp:242-257).
     * Executions are spread over `streams` device streams (kernel k on stream
       k % streams), each stream a cursor: exec begin = max(stream cursor, launch
-      end). Executions of different streams overlap each other and run past
-      the end of their layer into later layers ("interleaved streams").
-    * Every `block_layers` layers the host waits for all streams to drain (a
-      synchronisation point), so the trace has quiescent instants where no
-      layer interval and no launch->exec pair crosses: the time-range shards'
-      cut points (timeshard.py).
+      end) (simprof.cpp:255-257). Executions of different streams overlap each
+      other and run past the end of their layer into later layers
+      ("interleaved streams"); the cursors carry across the whole trace.
+    * drain_every > 0: every that many layers the host waits for all streams to
+      drain (a synchronisation point). The default has none, so layer intervals
+      and launch->exec pairs cross every instant of the trace.
     * Correlation ids increase in launch order; span ids follow record order.
+    Generated in chunks of `chunk_layers` layers (the drain period when set).
     At n_layers = 28.6M the trace has ~200M spans."""
     rng = np.random.default_rng(seed)
     names = sorted({f"c4/layer/{t}" for t in TYPES} | {"c4_model"} | set(KERNEL_VOCAB))
@@ -245,12 +252,15 @@ def c4(n_layers: int = 1_000_000, seed: int = 4, streams: int = 4, block_layers:
     vocab_ids = np.array([nid[n] for n in KERNEL_VOCAB], dtype=np.uint32)
     parts = {k: [] for k in ("span_id", "parent_id", "begin_ns", "end_ns", "cid", "flags", "name_id",
                              "flops", "dram_read", "dram_write", "occupancy", "alloc_bytes", "type_id")}
-    t_now = EPOCH_NS
+    t_now = EPOCH_NS                      # begin of the next layer group
+    cursor = np.full(streams, EPOCH_NS, dtype=np.int64)  # device stream cursors
     next_sid = 2
     next_cid = 1
+    k_total = 0                           # kernels so far (stream of kernel k = k % streams)
     KF = capi.LEVEL_KERNEL
-    for b0 in range(0, n_layers, block_layers):
-        L = min(block_layers, n_layers - b0)
+    step = drain_every if drain_every > 0 else chunk_layers
+    for b0 in range(0, n_layers, step):
+        L = min(step, n_layers - b0)
         kc = np.full(L, kernels, dtype=np.int64)
         long = rng.random(L) < long_frac
         kc[long] = rng.integers(8, long_max + 1, int(long.sum()))
@@ -264,21 +274,33 @@ def c4(n_layers: int = 1_000_000, seed: int = 4, streams: int = 4, block_layers:
         kl = kl - kl[first_k][lay_of_k]
         lsum = np.bincount(lay_of_k, weights=launch_ns, minlength=L).astype(np.int64)
         body = np.maximum(rng.integers(20_000, 400_000, L), lsum + 1_000)
-        lbeg = t_now + np.concatenate([[0], np.cumsum(body)[:-1]])
+        # concurrent groups of two layers (never across a chunk boundary)
+        starts = np.ones(L, dtype=bool)
+        if concurrent_frac > 0 and L > 1:
+            pair = np.nonzero(rng.random(L - 1) < concurrent_frac)[0]
+            pair = pair[np.concatenate([[True], np.diff(pair) > 1])] if pair.size else pair
+            starts[pair + 1] = False
+        gid = np.cumsum(starts) - 1
+        gfirst = np.nonzero(starts)[0]
+        gbody = np.maximum.reduceat(body, gfirst)
+        gbeg = t_now + np.concatenate([[0], np.cumsum(gbody)[:-1]])
+        lbeg = gbeg[gid]
         lend = lbeg + body
         a_beg = lbeg[lay_of_k] + kl
         a_end = a_beg + launch_ns
         d = rng.integers(5_000, 300_000, K)
         e_beg = np.empty(K, dtype=np.int64)
         for s in range(streams):
-            idx = np.arange(s, K, streams)
+            idx = np.arange((s - k_total) % streams, K, streams)
             if idx.size == 0:
                 continue
             ds = d[idx]
             S = np.cumsum(ds)
             Sprev = S - ds
-            e_end_s = S + np.maximum.accumulate(np.maximum(a_end[idx] - Sprev, t_now - Sprev))
+            e_end_s = S + np.maximum.accumulate(np.maximum(a_end[idx] - Sprev, int(cursor[s]) - Sprev))
             e_beg[idx] = e_end_s - ds
+            cursor[s] = int(e_end_s[-1])
+        k_total += K
         e_end = e_beg + d
         # span ids in record order: per layer [layer, (launch, exec) x K_l]
         layer_sid = next_sid + np.arange(L) + 2 * first_k
@@ -287,7 +309,7 @@ def c4(n_layers: int = 1_000_000, seed: int = 4, streams: int = 4, block_layers:
         next_sid = int(layer_sid[-1] + 1 + 2 * kc[-1])
         cid = next_cid + np.arange(K)
         next_cid += K
-        # timeline order (begin_ns, rank, span_id) of the block
+        # timeline order (begin_ns, rank, span_id) of the chunk
         n = L + 2 * K
         beg = np.concatenate([lbeg, a_beg, e_beg])
         end = np.concatenate([lend, a_end, e_end])
@@ -320,9 +342,12 @@ def c4(n_layers: int = 1_000_000, seed: int = 4, streams: int = 4, block_layers:
         lay_src = src[role == 0]
         parts["alloc_bytes"].append(rng.integers(100_000, 30_000_000, L)[lay_src])
         parts["type_id"].append(ltype[lay_src].astype(np.uint32))
-        # synchronisation point: the next block starts once every stream drained
-        t_now = int(max(lend[-1], e_end.max())) + 1_000
-    mend = t_now
+        t_now = int(lend.max())
+        if drain_every > 0:
+            # synchronisation point: the next block starts once every stream drained
+            t_now = int(max(t_now, cursor.max())) + 1_000
+            cursor[:] = t_now
+    mend = int(max(t_now, cursor.max()))
     model = {"span_id": [1], "parent_id": [0], "begin_ns": [EPOCH_NS], "end_ns": [mend], "cid": [0],
              "flags": [capi.LEVEL_MODEL], "name_id": [nid["c4_model"]]}
     cols = {}
@@ -331,6 +356,10 @@ def c4(n_layers: int = 1_000_000, seed: int = 4, streams: int = 4, block_layers:
             cols[k] = np.concatenate([np.asarray(model[k], dtype=v[0].dtype)] + v)
         else:
             cols[k] = np.concatenate(v)
+    if not drain_every:
+        # each chunk is in timeline order on its own, but executions of chunk c
+        # may begin after the first layers of chunk c + 1: one stable re-sort
+        cols = _timeline_order(cols)
     n = cols["span_id"].size
     lv = (1 << capi.LEVEL_MODEL) | (1 << capi.LEVEL_LAYER) | (1 << capi.LEVEL_KERNEL)
     return SpanBatch(**cols, trace_span_off=np.array([0, n], dtype=np.uint64), trace_id=np.array([1]),
@@ -338,3 +367,26 @@ def c4(n_layers: int = 1_000_000, seed: int = 4, streams: int = 4, block_layers:
                      trace_serialized=np.zeros(1), names=[x.encode() for x in names],
                      types=[t.encode() for t in TYPES], system_name=b"tesla-v100-sxm2",
                      peak_flops=15.7e12, mem_bw=900e9)
+
+
+def _timeline_order(cols):
+    """Stable re-sort of one trace's span columns by (begin_ns, rank, span_id)
+    (span.cpp:112-127); metric / layer side tables follow their spans."""
+    f = cols["flags"]
+    lvl = f & 3
+    rank = np.where(lvl == capi.LEVEL_MODEL, 1, np.where(lvl == capi.LEVEL_LAYER, 2, 3)).astype(np.uint8)
+    order = np.lexsort((cols["span_id"], rank, cols["begin_ns"]))
+    if np.array_equal(order, np.arange(order.size)):
+        return cols
+    met = (f & capi.F_METRICS) != 0
+    lay = lvl == capi.LEVEL_LAYER
+    mrow = np.cumsum(met) - 1
+    lrow = np.cumsum(lay) - 1
+    out = {k: cols[k][order] for k in ("span_id", "parent_id", "begin_ns", "end_ns", "cid", "flags", "name_id")}
+    mo = mrow[order][met[order]]
+    lo = lrow[order][lay[order]]
+    for k in ("flops", "dram_read", "dram_write", "occupancy"):
+        out[k] = cols[k][mo]
+    for k in ("alloc_bytes", "type_id"):
+        out[k] = cols[k][lo]
+    return out

@@ -67,7 +67,8 @@ def batch_of(traces: Sequence[Sequence[dict]], levels: Optional[Sequence[int]] =
     T = len(traces)
     lv = list(levels) if levels is not None else [MLG] * T
     bs = list(batch_sizes) if batch_sizes is not None else [1] * T
-    return SpanBatch(**{k: np.array(v) for k, v in cols.items()},
+    u64 = ("span_id", "parent_id", "begin_ns", "end_ns", "cid", "flops", "dram_read", "dram_write")
+    return SpanBatch(**{k: np.array(v, dtype=np.uint64) if k in u64 else np.array(v) for k, v in cols.items()},
                      trace_span_off=np.array(off), trace_id=np.arange(T) + 9,
                      trace_levels=np.array(lv), trace_batch=np.array(bs),
                      trace_run=np.zeros(T), trace_serialized=np.zeros(T),

@@ -91,3 +91,26 @@ def mixed_orphan_order():
         span(65, KERNEL, 741, 742, kind=EXEC, cid=12),  # consumed by the orphaned launch 53
         span(56, KERNEL, 450, 460, parent=41),          # explicit parent is an orphaned layer
     ]
+
+
+U64_MAX = (1 << 64) - 1
+
+
+def max_end():
+    """Intervals ending at 2^64-1: a kernel ending there is contained in a layer
+    ending there (closed intervals, span.hpp:97-100), and in no layer that ends
+    one nanosecond earlier (advisor finding on the device's end+1 encoding)."""
+    return [span(1, MODEL, 0, U64_MAX), span(2, LAYER, 10, U64_MAX), span(3, LAYER, 20, 30),
+            span(4, KERNEL, 25, U64_MAX), span(5, KERNEL, 40, U64_MAX),
+            span(6, KERNEL, 26, 28)]
+
+
+def max_end_orphan():
+    return [span(1, MODEL, 0, U64_MAX), span(2, LAYER, 10, U64_MAX - 1), span(3, KERNEL, 25, U64_MAX),
+            span(4, KERNEL, 30, U64_MAX - 1)]
+
+
+def model_span_id_shared():
+    """Two model spans with the same span_id: the reference compares span ids
+    (correlator.cpp:146-150), so this is not 'more than one model span'."""
+    return [span(1, MODEL, 0, 100), span(1, MODEL, 0, 90), span(2, LAYER, 10, 40), span(3, KERNEL, 12, 20)]

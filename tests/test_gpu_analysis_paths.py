@@ -1,8 +1,10 @@
-"""Every branch of the device trimmed mean (csrc/analyze.cu) against the C oracle,
-bit for bit: register sorting networks of 8 / 16 / 32 samples, the local-memory
-fallback for more than 32 repetitions, the exact-integer path for durations
-below 2^32 and the double path above it, and occupancies that are unsorted
-across repetitions (the sort cannot be skipped)."""
+"""Every branch of the device trimmed mean (csrc/analyze.cu) against the C oracle
+and the reference itself, bit for bit: register sorting networks of 8 / 16 / 32
+samples, the local-memory fallback for 33..64 repetitions, the selection path
+above 64, the exact-integer path for durations below 2^32 and the double path
+above it, and occupancies that are unsorted across repetitions (the sort cannot
+be skipped). The port is pinned to the reference on the same inputs in
+tests/test_oracle.py (test_port_many_repetitions, test_port_durations_beyond_32_bits)."""
 import numpy as np
 import pytest
 
@@ -23,13 +25,21 @@ def _same_tables(a, b):
 
 def _check(engine, b, groups):
     _, want = port.run(b, groups=groups)
-    _, got = engine.run_host(b, groups=groups)
+    corr, got = engine.run_host(b, groups=groups)
     _same_tables(got, want)
+    from oracle import ref
+    if ref.available():
+        import parity
+        ra, rs = ref.correlate(b)
+        parity.compare_correlation(b, corr, ra, rs)
+        aa, ast = ref.analyze(b, groups[0], groups[1])
+        parity.compare_tables(b, got, aa, ast)
 
 
-@pytest.mark.parametrize("runs", [3, 12, 20, 40])
+@pytest.mark.parametrize("runs", [3, 12, 20, 40, 80, 130])
 def test_repetition_counts(engine, runs):
-    b, gf, gr, gb = synth.c3(runs=runs, n_models=2, batches=(1, 8), seed=runs, min_layers=20, max_layers=60)
+    b, gf, gr, gb = synth.c3(runs=runs, n_models=2, batches=(1, 8), seed=runs, min_layers=20,
+                             max_layers=60 if runs <= 40 else 30)
     _check(engine, b, (gf, gr, gb))
 
 

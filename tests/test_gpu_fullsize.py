@@ -1,17 +1,29 @@
-"""Full-size GPU checks (BASELINE configs 3 and 4) through size-independent
-properties — the reference cannot hold these corpora in RAM at once — plus
-exact parity against the reference on a random sample of C3's groups.
+"""Full-size GPU parity (BASELINE configs 3 and 4).
 
-C3: 65 models x 8 batches x 20 iterations = 47.75 M spans (the bench workload).
-C4: one long trace (synth.c4), 5 M layers = 38 M spans (the bench runs 28.6 M
-layers; the properties do not depend on the size).
+C3 (65 models x 8 batches x 20 iterations = 47.75 M spans, the bench corpus):
+EVERY one of the 520 (model, batch) groups is diffed against the reference
+(oracle/_ref), every correlation and table column, rtol = 0. The reference
+cannot hold the corpus at once (~1 KB/span), so it runs group by group on a
+thread pool over slices of the corpus, against the product's ONE full-batch
+call.
+
+C4 (one long trace, synth.c4 with no drains, 0.1 % concurrent layer groups):
+the plain-C port (oracle/xsp_oracle.c) is first pinned to the reference on a
+5.4 M-span trace of the same generator, then diffed against the product at the
+bench size (28.6 M layers, ~219 M spans). The C4 diff takes minutes and ~80 GB
+of host memory, so it runs when XSP_FULLSCALE=1 (its log is committed under
+profiles/); a 5 M-layer property check always runs.
 """
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import pytest
 
 from paper_1908_06869_b200 import synth
 
 pytestmark = pytest.mark.gpu
+FULLSCALE = os.environ.get("XSP_FULLSCALE") == "1"
 
 
 def _roles(b):
@@ -23,13 +35,15 @@ def _check_correlation_properties(b, corr):
     lvl, kind = _roles(b)
     layers = np.nonzero((lvl == 1) & (kind == 0))[0]
     launches = np.nonzero((lvl >= 2) & (kind == 1))[0]
-    assert corr.n_failed == 0 and corr.n_orphans == 0 and corr.n_ambiguities == 0
-    assert corr.n_layers == layers.size and corr.n_kernels == launches.size
+    assert corr.n_failed == 0 and corr.n_orphans == 0
+    assert corr.n_layers == layers.size and corr.n_kernels + corr.n_ambiguities == launches.size
     # every placed layer once, in timeline (= layer_index) order per trace
     assert np.array_equal(np.sort(corr.layer_row.astype(np.int64)), layers)
     # kernels: every launch once; its exec carries the same cid; the exec is an exec span
     kl = corr.kernel_launch_row.astype(np.int64)
     ke = corr.kernel_exec_row.astype(np.int64)
+    if corr.n_ambiguities:  # ambiguous launches stay out of the tree
+        launches = np.setdiff1d(launches, corr.amb_row.astype(np.int64))
     assert np.array_equal(np.sort(kl), launches)
     assert np.array_equal(b.cid[kl], b.cid[ke])
     assert np.all(kind[ke] == 2)
@@ -45,60 +59,104 @@ def _check_correlation_properties(b, corr):
     return kl, ke
 
 
-def test_c3_full_properties_and_sampled_parity(engine, has_ref):
+def test_c3_every_group_equals_reference(engine, has_ref):
     from oracle import ref
-    import os
     import sys
     sys.path.insert(0, os.path.dirname(__file__))
-    from parity import compare_tables
+    from parity import compare_correlation, compare_tables, topk_oracle
     b, gf, gr, gb = synth.c3()
     assert b.n_spans > 47_000_000
     corr, tabs = engine.run_host(b, groups=(gf, gr, gb))
+    assert corr.n_ambiguities == 0
     _check_correlation_properties(b, corr)
-    # analysis totals: u64 counters are exact sums of the first run's kernels
     G = len(gf)
-    assert np.all(tabs.group_status == 0)
-    goff = tabs.group_kernel_off.astype(np.int64)
-    assert np.array_equal(tabs.m_count, np.diff(goff).astype(np.uint64))
-    fl = tabs.k_flops.astype(np.uint64)
-    sums = np.add.reduceat(fl, goff[:-1]) if tabs.n_kernels else np.zeros(G, np.uint64)
-    assert np.array_equal(tabs.m_flops, sums)
-    noff = tabs.group_name_off.astype(np.int64)
-    ncount = np.add.reduceat(tabs.n_count.astype(np.uint64), noff[:-1])
-    assert np.array_equal(ncount, np.diff(goff).astype(np.uint64))
-    # a10 order: total latency descending within every group
-    for g in range(0, G, 37):
-        lat = tabs.n_lat[noff[g]:noff[g + 1]]
-        assert np.all(np.diff(lat) <= 0)
-    # exact parity with the reference on a random sample of groups
-    rng = np.random.default_rng(12)
-    for g in rng.choice(G, size=3, replace=False):
+    off = b.trace_span_off.astype(np.int64)
+
+    def reference(g):
         t0, t1 = int(gf[g]), int(gf[g] + gr[g])
         sub = b.trace_slice(t0, t1)
-        c2, t2 = engine.run_host(sub, groups=([0], [t1 - t0], [int(gb[g])]))
-        aa, ast = ref.analyze(sub, [0], [t1 - t0])
-        compare_tables(sub, t2, aa, ast)
-        # and the full-batch tables of that group equal the per-group run bit for bit
-        k0, k1 = int(goff[g]), int(goff[g + 1])
-        assert np.array_equal(tabs.k_lat[k0:k1].view(np.uint64), t2.k_lat.view(np.uint64))
-        assert tabs.m_lat[g] == t2.m_lat[0] and tabs.m_occ[g] == t2.m_occ[0]
+        return g, ref.correlate(sub), ref.analyze(sub, [0], [t1 - t0])
+
+    checked = 0
+    with ThreadPoolExecutor(max(1, (os.cpu_count() or 2) - 1)) as ex:
+        for lo in range(0, G, 32):  # bounded: at most 32 groups' reference results in memory
+            for g, (ca, cs), (aa, ast) in ex.map(reference, range(lo, min(G, lo + 32))):
+                t0 = int(gf[g])
+                compare_correlation(b, corr, ca, cs, t_base=t0, row_base=int(off[t0]), whole=False)
+                compare_tables(b, tabs, aa, ast, g_base=g, whole=False)
+                # top-3 per layer ranks the reference's own a8 rows
+                l0, l1 = int(tabs.group_layer_off[g]), int(tabs.group_layer_off[g + 1])
+                want = topk_oracle(aa["k_lat"], aa["k_layer"], 3)
+                np.testing.assert_array_equal(tabs.l_topk[3 * l0:3 * l1].reshape(-1, 3), want)
+                checked += 1
+    assert checked == G == 520
 
 
 def test_c4_long_trace_properties(engine):
     b = synth.c4(n_layers=5_000_000)
     assert b.n_spans > 35_000_000
     corr, tabs = engine.run_host(b)
+    assert corr.n_ambiguities > 0  # the concurrent layer groups
     kl, ke = _check_correlation_properties(b, corr)
     # one run: integer latencies, so the model's kernel latency is the exact sum
     dur = (b.end_ns[ke] - b.begin_ns[ke]).astype(np.uint64)
     assert tabs.m_kern_lat[0] == float(int(dur.sum()))
     assert tabs.m_count[0] == corr.n_kernels
-    lvl, kind = _roles(b)
     metric_rows = np.cumsum((b.flags & 0x40) != 0) - 1
     assert tabs.m_flops[0] == np.uint64(int(b.flops[metric_rows[ke]].astype(np.uint64).sum()))
     # a10 rows: every kernel counted once
     assert int(tabs.n_count.sum()) == corr.n_kernels
-    # time-range shards agree with the single-GPU run
-    from paper_1908_06869_b200 import timeshard
-    starts = timeshard.choose_cuts(timeshard.quiescent_cuts(b), b.n_spans, 3)
-    assert len(starts) == 3
+
+
+C4_PIN_LAYERS = 700_000          # ~5.4 M spans: the reference needs ~14 GB for it
+C4_BENCH_LAYERS = 28_600_000     # bench.py's C4 (~219 M spans)
+
+
+@pytest.mark.skipif(not FULLSCALE, reason="XSP_FULLSCALE=1 runs the minutes-long C4 diffs")
+def test_c4_port_pinned_to_reference(has_ref):
+    """The C port equals the reference on a ~5.4 M-span trace of the C4 generator
+    (concurrent groups, interleaved streams, no drains) before it judges the
+    bench-size trace."""
+    from oracle import port, ref
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from parity import compare_correlation, compare_tables
+    b = synth.c4(n_layers=C4_PIN_LAYERS)
+    assert b.n_spans > 5_000_000
+    corr, tabs = port.run(b)
+    assert corr.n_ambiguities > 0
+    ra, rs = ref.correlate(b)
+    compare_correlation(b, corr, ra, rs)
+    del ra, rs
+    aa, ast = ref.analyze(b, [0], [1])
+    compare_tables(b, tabs, aa, ast)
+
+
+# Occupancy-weighted sums of ONE long group (a single trace above 65,536
+# kernels) are added in 8,192-kernel chunks and then across chunks (DESIGN.md
+# §4 "Long groups"): re-associated, so equal to 1e-12 relative, not bitwise.
+# Every other column, including every latency sum (integers below 2^53), is
+# compared bit for bit.
+LONG_GROUP_REASSOCIATED = {"m_occ", "n_occ"}
+
+
+@pytest.mark.skipif(not FULLSCALE, reason="XSP_FULLSCALE=1 runs the minutes-long C4 diffs")
+def test_c4_bench_size_equals_port(engine):
+    from oracle import port
+    b = synth.c4(n_layers=C4_BENCH_LAYERS)
+    assert b.n_spans > 200_000_000
+    corr, tabs = engine.run_host(b)
+    want_c, want_t = port.run(b)
+    assert (corr.n_layers, corr.n_kernels, corr.n_orphans, corr.n_ambiguities, corr.n_candidates) == \
+        (want_c.n_layers, want_c.n_kernels, want_c.n_orphans, want_c.n_ambiguities, want_c.n_candidates)
+    for k in want_c.cols:
+        assert np.array_equal(np.asarray(corr.cols[k]), np.asarray(want_c.cols[k])), k
+    del want_c
+    assert (tabs.n_layers, tabs.n_kernels, tabs.n_names) == (want_t.n_layers, want_t.n_kernels, want_t.n_names)
+    for k in want_t.cols:
+        x, y = np.asarray(tabs.cols[k]), np.asarray(want_t.cols[k])
+        assert x.shape == y.shape, k
+        if k in LONG_GROUP_REASSOCIATED:
+            np.testing.assert_allclose(x, y, rtol=1e-12, atol=0, err_msg=k)
+        else:
+            assert np.array_equal(x.view(np.uint8), y.view(np.uint8)), k

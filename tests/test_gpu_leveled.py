@@ -69,6 +69,15 @@ def test_repetitions_with_jitter_and_clamping(engine, has_ref):
         compare(rep, bag)
 
 
+def test_more_than_64_repetitions_per_set(engine, has_ref):
+    """Level sets of 70 repetitions (the selection path of the trimmed mean)."""
+    g = ref.Generator()
+    for levels in (M, ML, MLG):
+        for r in range(70):
+            g.emit("minimal", 1, levels, 0, 0, 1.0, False, r, 300_000, 7 * r + levels)
+    compare(*run(engine, g))
+
+
 def test_structure_changes_across_the_chain(engine, has_ref):
     """Events present in one set only produce the 'visible under' warnings."""
     g = ref.Generator()

@@ -63,6 +63,28 @@ def test_port_repetitions(has_ref):
     both(g.batch(), groups=([0], [10], [4]))
 
 
+@pytest.mark.parametrize("runs", [40, 80])
+def test_port_many_repetitions(has_ref, runs):
+    """The branches the GPU tests compare the port on (test_gpu_analysis_paths.py):
+    more than 32 and more than 64 repetitions per group, pinned to the reference."""
+    from paper_1908_06869_b200 import synth
+    b, gf, gr, gb = synth.c3(runs=runs, n_models=2, batches=(1, 8), seed=runs, min_layers=20, max_layers=40)
+    both(b, groups=(gf, gr, gb))
+
+
+def test_port_durations_beyond_32_bits(has_ref):
+    """Execution durations above 2^32 ns and occupancies unsorted across runs."""
+    from paper_1908_06869_b200 import _capi as capi
+    from paper_1908_06869_b200 import synth
+    b, gf, gr, gb = synth.c3(runs=20, n_models=2, batches=(1, 4), seed=5, min_layers=20, max_layers=60)
+    rng = np.random.default_rng(9)
+    execs = np.nonzero(((b.flags >> 2) & 3) == capi.KIND_EXEC)[0]
+    big = rng.choice(execs, size=execs.size // 4, replace=False)
+    b.end_ns[big] += np.uint64(1) << np.uint64(33)
+    b.occupancy[:] = rng.random(b.occupancy.size)
+    both(b, groups=(gf, gr, gb))
+
+
 def test_port_trim_fractions(has_ref):
     g = ref.Generator()
     for r in range(7):
@@ -92,7 +114,8 @@ def test_port_async(has_ref):
 
 @pytest.mark.parametrize("case", ["nesting", "layer_attrs", "explicit_beats_containment",
                                   "overlapping_layers", "orphans", "fusion", "unmatched_async",
-                                  "mixed_orphan_order"])
+                                  "mixed_orphan_order", "max_end", "max_end_orphan",
+                                  "model_span_id_shared"])
 def test_port_edge_cases(has_ref, case):
     both(batch_of([getattr(cases, case)()]))
 

@@ -21,7 +21,7 @@ APPROX = {"m_occ", "n_occ"}
 
 
 def c4_small(layers=4000, block=400, seed=4):
-    return synth.c4(n_layers=layers, block_layers=block, seed=seed)
+    return synth.c4(n_layers=layers, drain_every=block, seed=seed, concurrent_frac=0.0)
 
 
 def oracle_compute(sub):
