@@ -287,6 +287,18 @@ struct P1Args {
   uint32_t* pend_kl;
   uint32_t* pend_count;
   uint32_t amb_cap, pend_cap;  // list capacities (counts beyond them trigger a retry)
+  // direct mode (k_pass1<true>, a clean-batch guess): pass 1 writes the kernel
+  // table itself — launch r of a trace at its kernel-list position, exec r at its
+  // exec-list position, which coincide when every trace is merge-aligned — and
+  // records per trace the min / max of (cid - list position) over its launches
+  // and execs (equal <=> the cids are one dense run shared by both lists)
+  uint32_t *k_launch, *k_exec, *k_mrow, *k_name, *l_koff;
+  uint64_t* k_dur;
+  double* k_occ;
+  const uint32_t* name;
+  const double* occ;
+  unsigned long long *t_dmin, *t_dmax;
+  uint32_t* direct_fail;  // a kernel-list entry that is not a launch with a cid
 };
 
 // TMA descriptors of the four u64 columns, each viewed as a 2-D tensor of
@@ -741,152 +753,6 @@ __global__ void __launch_bounds__(P1_THREADS) k_p1_reduce(P1Args a, const __grid
   }
 }
 
-// ---- k_p1_reduce_lanes: the tile aggregates with one span per lane ----------
-// Same staging and outputs as k_p1_reduce; each warp folds its 256 spans as 8
-// chunks of 32 (lane = span): placement per lane, role counts by ballot, and the
-// containment state (last placed layer's end, max ends) by a segmented
-// max-scan over the lanes, carried warp-uniformly from chunk to chunk. The
-// warp aggregate is exactly the left fold of full_combine over its spans.
-__global__ void __launch_bounds__(P1_THREADS) k_p1_reduce_lanes(P1Args a, const __grid_constant__ P1Maps maps) {
-  extern __shared__ unsigned char red_dyn[];
-  RedSmem& sm = *reinterpret_cast<RedSmem*>(red_dyn + ((1024u - (smem_u32(red_dyn) & 1023u)) & 1023u));
-  __shared__ TraceCache tc;
-  __shared__ Full s_wagg[P1_WARPS];
-  __shared__ __align__(8) uint64_t s_bar;
-  const uint32_t tile = blockIdx.x, warp = threadIdx.x >> 5, lane = lane_id();
-  const uint64_t tile_base = (uint64_t)tile * P1_TILE;
-  const uint32_t tile_n = (uint32_t)min((uint64_t)P1_TILE, a.n - tile_base);
-  const bool bulk = a.bulk && tile_n == P1_TILE;
-  if (threadIdx.x == 0 && bulk) {
-    mbar_init(&s_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&s_bar, P1_TILE * (3 * 8 + 1));
-    const int y = (int)(tile_base / 16);
-    tma_g2s_2d(sm.begin, &maps.begin, 0, y, &s_bar);
-    tma_g2s_2d(sm.end, &maps.end, 0, y, &s_bar);
-    tma_g2s_2d(sm.parent, &maps.parent, 0, y, &s_bar);
-    bulk_g2s(sm.flags, a.flags + tile_base, P1_TILE, &s_bar);
-  }
-  if (!bulk) {
-    for (uint32_t j = threadIdx.x; j < P1_TILE; j += P1_THREADS) {
-      const bool v = j < tile_n;
-      const uint64_t i = tile_base + j;
-      const uint32_t sw = sw128(j);
-      sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
-      sm.begin[sw] = v ? a.begin[i] : 0;
-      sm.end[sw] = v ? a.end[i] : 0;
-      sm.parent[sw] = v ? a.parent[i] : 0;
-    }
-  }
-  const uint32_t tlo = __ldg(a.tile_lo + tile), thi = __ldg(a.tile_hi + tile) + 1;
-  fill_trace_cache(a, tc, tlo, thi);
-  __syncthreads();
-  if (bulk) mbar_wait(&s_bar, 0);
-  const TileTraces tt{a, tc, tlo, thi - tlo <= (uint32_t)P1_TCACHE};
-  const uint32_t wj0 = warp * P1_SUB;
-  Full agg = full_identity();
-  if (wj0 < tile_n) {
-    uint32_t r = tt.find(tile_base + wj0, thi);
-    TraceAttrs ta;
-    tt.load(r, ta);
-    uint64_t lastE = 0, lastM = 0, runM = 0;
-    const uint32_t lt = lanemask_lt();
-    const uint32_t le = lt | (1u << lane);
-    for (int q = 0; q < P1_ITEMS; ++q) {
-      const uint32_t j = wj0 + (uint32_t)q * 32u + lane;
-      const bool valid = j < tile_n;
-      const uint32_t V = __ballot_sync(0xffffffffu, valid);
-      if (!V) break;
-      const uint64_t i = tile_base + j;
-      const uint32_t jj = valid ? j : wj0;
-      const uint8_t f = valid ? sm.flags[jj] : (uint8_t)0;
-      uint32_t rl = r;
-      TraceAttrs tl = ta;
-      const bool moved = valid && i >= ta.next;
-      const uint32_t MV = __ballot_sync(0xffffffffu, moved);
-      if (moved) {
-        do { ++rl; } while (tt.off(rl + 1) <= i);
-        tt.load(rl, tl);
-      }
-      const bool head = valid && i == tl.cur;
-      const bool is_layer = valid && f_level(f) == XSP_LEVEL_LAYER;
-      uint64_t e = 0;
-      bool placed = false;
-      if (is_layer && f_kind(f) == XSP_KIND_SYNC) {  // layer placement (correlator.cpp:168-194)
-        const uint64_t b = sm.begin[sw128(jj)];
-        e = sm.end[sw128(jj)];
-        placed = placed_in(tl, f, b, e, (f & XSP_F_PARENT) ? sm.parent[sw128(jj)] : 0);
-      }
-      const uint32_t P = __ballot_sync(0xffffffffu, placed);
-      const uint32_t H = __ballot_sync(0xffffffffu, head);
-      if (lane == 0) *reinterpret_cast<uint32_t*>(a.placed8 + ((tile_base + wj0) >> 3) + 4u * q) = P;
-      agg.c += __popc(P);
-      agg.head |= H != 0;
-      agg.c_lay += __popc(__ballot_sync(0xffffffffu, is_layer));
-      agg.c_metric += __popc(__ballot_sync(0xffffffffu, valid && (f & XSP_F_METRICS)));
-      agg.c_kl += __popc(__ballot_sync(0xffffffffu, valid && (is_kernel_launch(f) || is_sync_kernel(f))));
-      agg.c_ex += __popc(__ballot_sync(0xffffffffu, valid && is_exec(f) && (f & XSP_F_CID)));
-      if (P | H) {  // containment state: segmented max-scan of placed ends
-        const uint32_t Hle = H & le;
-        const int s = Hle ? 31 - __clz(Hle) : -1;
-        const uint64_t v = placed ? (e == ~0ull ? e : e + 1) : 0;
-        uint64_t R = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint64_t u = __shfl_up_sync(0xffffffffu, R, o);
-          if ((int)lane - o >= (s < 0 ? 0 : s)) R = max64(R, u);
-        }
-        if (s < 0) R = max64(R, runM);
-        uint64_t Rx = __shfl_up_sync(0xffffffffu, R, 1);
-        if ((int)lane == s) Rx = 0;
-        else if (lane == 0) Rx = runM;
-        const int s31 = H ? 31 - __clz(H) : -1;
-        const uint32_t Pt = P & (s31 > 0 ? ~((1u << s31) - 1u) : 0xffffffffu);
-        const int j31 = Pt ? 31 - __clz(Pt) : -1;
-        const uint64_t v31 = __shfl_sync(0xffffffffu, v, j31 < 0 ? 0 : j31);
-        const uint64_t rx31 = __shfl_sync(0xffffffffu, Rx, j31 < 0 ? 0 : j31);
-        runM = __shfl_sync(0xffffffffu, R, 31);
-        if (j31 >= 0) {
-          lastE = v31;
-          lastM = rx31;
-        } else if (s31 >= 0) {
-          lastE = lastM = 0;
-        }
-      }
-      if (MV) {
-        r = __shfl_sync(0xffffffffu, rl, 31);
-        tt.load(r, ta);
-      }
-    }
-    agg.last_end1 = lastE;
-    agg.last_M1 = lastM;
-    agg.run_M1 = runM;
-  }
-  if (lane == 0) s_wagg[warp] = agg;
-  __syncthreads();
-  if (warp != 0) return;
-  uint32_t last = 0;
-  if (lane < P1_WARPS) {
-    Full ex = full_identity();
-    for (uint32_t w = 0; w < lane; ++w) ex = full_combine(ex, s_wagg[w]);
-    a.warp_excl[(uint64_t)tile * P1_WARPS + lane] = ex;
-  }
-  if (lane == 0) {
-    Full t = s_wagg[0];
-    for (int w = 1; w < P1_WARPS; ++w) t = full_combine(t, s_wagg[w]);
-    a.tile_agg[tile] = t;
-    __threadfence();
-    const uint32_t g = tile >> 5, gsize = min(32u, a.ntiles - (g << 5));
-    last = atomicAdd(a.group_done + g, 1u) == gsize - 1;
-  }
-  if (__shfl_sync(0xffffffffu, last, 0)) {
-    __threadfence();
-    const uint32_t g = tile >> 5, k = (g << 5) + lane;
-    const Full v = warp_reduce_ordered(k < a.ntiles ? ld_full_cg(a.tile_agg + k) : full_identity(), lane);
-    if (lane == 0) a.group_sum[g] = v;
-  }
-}
-
 // ---- k_p1_scan: exclusive prefixes of the 32-tile group totals -------------
 // One CTA. The group totals come from k_p1_reduce (the last tile of each group
 // to finish reduces the group); a block scan gives gprefix[g] (exclusive) and
@@ -933,6 +799,63 @@ __global__ void k_p1_tile_prefix(const Full* __restrict__ agg, const Full* __res
 }
 
 // ---- k_pass1: per-span outputs ----------------------------------------------
+// Per-trace min / max with atomics, warp-aggregated when every lane holding a
+// value (t != kNone) has the same trace (one atomic pair per warp), else per lane.
+__device__ __forceinline__ void minmax_atomic_warp(uint32_t t, uint64_t mn, uint64_t mx,
+                                                   unsigned long long* __restrict__ dmin,
+                                                   unsigned long long* __restrict__ dmax) {
+  const uint32_t act = __activemask();
+  if (act == 0xffffffffu) {
+    const uint32_t has = __ballot_sync(act, t != kNone);
+    if (!has) return;
+    const uint32_t t0 = __shfl_sync(act, t, __ffs(has) - 1);
+    if (__ballot_sync(act, t == t0 || t == kNone) == act) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t b0 = __shfl_xor_sync(act, mn, o), b1 = __shfl_xor_sync(act, mx, o);
+        mn = b0 < mn ? b0 : mn;
+        mx = b1 > mx ? b1 : mx;
+      }
+      if (lane_id() == 0) {
+        atomicMin(dmin + t0, (unsigned long long)mn);
+        atomicMax(dmax + t0, (unsigned long long)mx);
+      }
+      return;
+    }
+  }
+  if (t != kNone) {
+    atomicMin(dmin + t, (unsigned long long)mn);
+    atomicMax(dmax + t, (unsigned long long)mx);
+  }
+}
+
+// Per-trace min / max of (cid - list position) in direct mode: a thread keeps
+// the run of its current trace and flushes it with atomics; the final runs of a
+// warp whose lanes share one trace are reduced first (one atomic pair per warp).
+struct DirectAcc {
+  uint64_t mn = ~0ull, mx = 0;
+  uint32_t t = kNone;
+  __device__ __forceinline__ void flush(const P1Args& a) {
+    if (t != kNone) {
+      atomicMin(a.t_dmin + t, (unsigned long long)mn);
+      atomicMax(a.t_dmax + t, (unsigned long long)mx);
+    }
+    mn = ~0ull;
+    mx = 0;
+    t = kNone;
+  }
+  __device__ __forceinline__ void add(const P1Args& a, uint32_t tr, uint64_t d) {
+    if (tr != t) {
+      flush(a);
+      t = tr;
+    }
+    mn = d < mn ? d : mn;
+    mx = d > mx ? d : mx;
+  }
+  __device__ __forceinline__ void finish(const P1Args& a) { minmax_atomic_warp(t, mn, mx, a.t_dmin, a.t_dmax); }
+};
+
+template <bool kDirect>
 __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const __grid_constant__ P1Maps maps) {
   extern __shared__ unsigned char p1_dyn[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(p1_dyn + ((1024u - (smem_u32(p1_dyn) & 1023u)) & 1023u));
@@ -1013,6 +936,7 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
     pb = j0 > 0 ? sm.begin[sw128(j0 - 1)] : __ldg(a.begin + i0 - 1);
     pf = j0 > 0 ? sm.flags[j0 - 1] : __ldg(a.flags + i0 - 1);
   }
+  DirectAcc dacc;
   // Fast emit: the 8 spans lie inside one trace with no trace head, no model
   // span, and the trace profiles the layer level. The roles come from the flag
   // bytes as bit masks and each output list is filled by walking its mask in
@@ -1053,6 +977,7 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
         a.layer_row[g] = (uint32_t)i;
         a.layer_dur[g] = clamp_dur(sm.begin[sw128(j0 + k)], e);
         a.layer_attr_row[g] = c_lay + __popc(m.layer & below);
+        if constexpr (kDirect) a.l_koff[g] = c_kl;  // kernels before it = the layer's first kernel
         ++g;
         const uint64_t w = e == ~0ull ? e : e + 1;
         lastM = runM;
@@ -1086,12 +1011,21 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
           }
         }
       }
-      KlEnt ent;
-      ent.row = (uint32_t)i;
-      ent.parent = par;
-      ent.cid = (f & XSP_F_CID) ? sm.cid[sw128(j0 + k)] : 0;
-      a.kl[k_ex] = ent;
-      if ((sync_k >> k) & 1u) a.kl_mrow[k_ex] = ((m.metric >> k) & 1u) ? c_metric + __popc(m.metric & below) : kNone;
+      if constexpr (kDirect) {
+        a.k_launch[k_ex] = (uint32_t)i;
+        if (f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID))
+          dacc.add(a, t, sm.cid[sw128(j0 + k)] - k_ex);
+        else
+          *a.direct_fail = 1;
+        (void)par;
+      } else {
+        KlEnt ent;
+        ent.row = (uint32_t)i;
+        ent.parent = par;
+        ent.cid = (f & XSP_F_CID) ? sm.cid[sw128(j0 + k)] : 0;
+        a.kl[k_ex] = ent;
+        if ((sync_k >> k) & 1u) a.kl_mrow[k_ex] = ((m.metric >> k) & 1u) ? c_metric + __popc(m.metric & below) : kNone;
+      }
     }
     // layers that are not placed (correlator.cpp:169-194)
     for (uint32_t lo = m.layer & ~placed; lo; lo &= lo - 1) {
@@ -1106,15 +1040,28 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
     for (uint32_t ex = exec_m; ex; ex &= ex - 1) {
       const int k = __ffs(ex) - 1;
       if ((m.ex_cid >> k) & 1u) {
-        ExEnt ent;
-        ent.row = (uint32_t)(i0 + k);
-        ent.mrow = ((m.metric >> k) & 1u) ? c_metric + __popc(m.metric & ((1u << k) - 1u)) : kNone;
-        ent.dur = clamp_dur(sm.begin[sw128(j0 + k)], sm.end[sw128(j0 + k)]);
-        a.ex[c_ex++] = ent;
+        const uint32_t mr = ((m.metric >> k) & 1u) ? c_metric + __popc(m.metric & ((1u << k) - 1u)) : kNone;
+        const uint64_t dur = clamp_dur(sm.begin[sw128(j0 + k)], sm.end[sw128(j0 + k)]);
+        if constexpr (kDirect) {
+          const uint32_t x = c_ex++;
+          a.k_exec[x] = (uint32_t)(i0 + k);
+          a.k_mrow[x] = mr;
+          a.k_dur[x] = dur;
+          a.k_name[x] = __ldg(a.name + i0 + k);
+          a.k_occ[x] = mr != kNone ? __ldg(a.occ + mr) : 0.0;
+          dacc.add(a, t, sm.cid[sw128(j0 + k)] - x);
+        } else {
+          ExEnt ent;
+          ent.row = (uint32_t)(i0 + k);
+          ent.mrow = mr;
+          ent.dur = dur;
+          a.ex[c_ex++] = ent;
+        }
       } else if (!a.parents_only) {
         emit_orphan(a.orph, t, CAT_EXEC_NOCID, i0 + k, (uint32_t)(i0 + k), XSP_O_EXEC_NO_CID);
       }
     }
+    if constexpr (kDirect) dacc.finish(a);
     return;
   }
 #pragma unroll kP1EmitUnroll
@@ -1175,6 +1122,7 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
           a.layer_row[g] = (uint32_t)i;
           a.layer_dur[g] = clamp_dur(b, e);
           a.layer_attr_row[g] = c_lay;
+          if constexpr (kDirect) a.l_koff[g] = c_kl;
           ++g;
           const uint64_t w = e == ~0ull ? e : e + 1;
           lastM = runM;
@@ -1214,272 +1162,63 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
             }
           }
         }
-        KlEnt ent;
-        ent.row = (uint32_t)i;
-        ent.parent = par;
-        ent.cid = has_cid ? cc[h] : 0;
-        a.kl[k_ex] = ent;
-        if (sync) a.kl_mrow[k_ex] = mrow;
+        if constexpr (kDirect) {
+          a.k_launch[k_ex] = (uint32_t)i;
+          if (f_kind(f) == XSP_KIND_LAUNCH && has_cid)
+            dacc.add(a, t, cc[h] - k_ex);
+          else
+            *a.direct_fail = 1;
+          (void)par;
+        } else {
+          KlEnt ent;
+          ent.row = (uint32_t)i;
+          ent.parent = par;
+          ent.cid = has_cid ? cc[h] : 0;
+          a.kl[k_ex] = ent;
+          if (sync) a.kl_mrow[k_ex] = mrow;
+        }
       }
       if (is_exec(f)) {
         if (has_cid) {
-          ExEnt ent;
-          ent.row = (uint32_t)i;
-          ent.mrow = mrow;
-          ent.dur = clamp_dur(b, e);
-          a.ex[c_ex++] = ent;
+          if constexpr (kDirect) {
+            const uint32_t x = c_ex++;
+            a.k_exec[x] = (uint32_t)i;
+            a.k_mrow[x] = mrow;
+            a.k_dur[x] = clamp_dur(b, e);
+            a.k_name[x] = __ldg(a.name + i);
+            a.k_occ[x] = mrow != kNone ? __ldg(a.occ + mrow) : 0.0;
+            dacc.add(a, t, cc[h] - x);
+          } else {
+            ExEnt ent;
+            ent.row = (uint32_t)i;
+            ent.mrow = mrow;
+            ent.dur = clamp_dur(b, e);
+            a.ex[c_ex++] = ent;
+          }
         } else if (!a.parents_only) {
           emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
         }
       }
     }
   }
+  if constexpr (kDirect) dacc.finish(a);
 }
-// ---- k_pass1_lanes: per-span outputs, one span per lane ------------------------
-// The same outputs as k_pass1, but each warp walks its 256 spans as 8 chunks of
-// 32 with lane = span, carrying the scan state (counts, last placed layer's
-// end, max ends) warp-uniformly from chunk to chunk; the warp's starting state
-// is k_p1_reduce's warp prefix, so nothing of phase 1 is recomputed. Within a
-// chunk:
-//   * list positions are the carried counts plus ballot prefix counts, so the
-//     entries of one list that a chunk emits are consecutive and their stores
-//     coalesce (the thread-serial walk stored at 32 scattered positions);
-//   * the containment state of a child lane is its segment's (trace's) last
-//     placed layer j before it and the max end over placed layers before j: a
-//     segmented max-scan of placed-layer ends over the lanes (segments start at
-//     trace heads) plus the carry — the same decision as k_pass1's per-thread
-//     walk, bit for bit.
-__global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1_lanes(P1Args a, const __grid_constant__ P1Maps maps) {
-  extern __shared__ unsigned char p1_dyn[];
-  TileSmem& sm = *reinterpret_cast<TileSmem*>(p1_dyn + ((1024u - (smem_u32(p1_dyn) & 1023u)) & 1023u));
-  __shared__ TraceCache tc;
-  __shared__ __align__(8) uint64_t s_bar;
 
-  const uint32_t tile = blockIdx.x, warp = threadIdx.x >> 5, lane = lane_id();
-  const TileHdr hd = tile_hdr(a, tile);
-  const uint64_t tile_base = hd.tile_base;
-  const uint32_t tile_n = hd.tile_n, tlo = hd.tlo, thi = hd.thi;
-  const bool bulk = a.bulk && tile_n == P1_TILE;
-  if (threadIdx.x == 0 && bulk) {
-    mbar_init(&s_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&s_bar, P1_TILE * (3 * 8 + 1));
-    const int y = (int)(tile_base / 16);
-    tma_g2s_2d(sm.begin, &maps.begin, 0, y, &s_bar);
-    tma_g2s_2d(sm.end, &maps.end, 0, y, &s_bar);
-    tma_g2s_2d(sm.cid, &maps.cid, 0, y, &s_bar);
-    bulk_g2s(sm.flags, a.flags + tile_base, P1_TILE, &s_bar);
-  }
-  fill_trace_cache(a, tc, tlo, thi);
-  const uint32_t wj0 = warp * P1_SUB;
-  Full cs = full_identity();
-  if (wj0 < tile_n) cs = full_combine(a.tile_excl[tile], a.warp_excl[(uint64_t)tile * P1_WARPS + warp]);
-  if (!bulk) {
-    for (uint32_t j = threadIdx.x; j < P1_TILE; j += P1_THREADS) {
-      const bool v = j < tile_n;
-      const uint64_t i = tile_base + j;
-      const uint32_t sw = sw128(j);
-      sm.flags[j] = v ? a.flags[i] : (uint8_t)0xFF;
-      sm.begin[sw] = v ? a.begin[i] : 0;
-      sm.end[sw] = v ? a.end[i] : 0;
-      sm.cid[sw] = v ? a.cid[i] : 0;
-    }
-  }
-  __syncthreads();
-  if (bulk) mbar_wait(&s_bar, 0);
-  if (wj0 >= tile_n) return;
-  const TileTraces tt{a, tc, tlo, thi - tlo <= (uint32_t)P1_TCACHE};
-  // warp-uniform state
-  uint32_t g = cs.c, c_metric = cs.c_metric, c_lay = cs.c_lay, c_kl = cs.c_kl, c_ex = cs.c_ex;
-  uint64_t lastE = cs.last_end1, lastM = cs.last_M1, runM = cs.run_M1;
-  uint32_t r = tt.find(tile_base + wj0, thi);
-  TraceAttrs ta;
-  tt.load(r, ta);
-  uint64_t pb = 0;  // the span before the chunk (timeline-order check)
-  uint32_t pf = 0;
-  {
-    const uint64_t wi0 = tile_base + wj0;
-    if (wi0 > 0) {
-      pb = wj0 > 0 ? sm.begin[sw128(wj0 - 1)] : __ldg(a.begin + wi0 - 1);
-      pf = wj0 > 0 ? sm.flags[wj0 - 1] : __ldg(a.flags + wi0 - 1);
-    }
-  }
-  const uint32_t lt = lanemask_lt();
-  const uint32_t le = lt | (1u << lane);
-  for (int q = 0; q < P1_ITEMS; ++q) {
-    const uint32_t j = wj0 + (uint32_t)q * 32u + lane;
-    const bool valid = j < tile_n;
-    const uint32_t V = __ballot_sync(0xffffffffu, valid);
-    if (!V) break;
-    const uint64_t i = tile_base + j;
-    const uint32_t jj = valid ? j : wj0;
-    const uint8_t f = valid ? sm.flags[jj] : (uint8_t)0;
-    const uint64_t b = sm.begin[sw128(jj)];
-    const uint64_t e = sm.end[sw128(jj)];
-    // placed-layer bits of the chunk (k_p1_reduce): 32 spans = 4 aligned bytes
-    uint32_t P = 0;
-    if (lane == 0) P = *reinterpret_cast<const uint32_t*>(a.placed8 + ((tile_base + wj0) >> 3) + 4u * q);
-    P = __shfl_sync(0xffffffffu, P, 0) & V;
-    // the lane's trace: the warp's current one unless a trace starts inside the chunk
-    uint32_t rl = r;
-    TraceAttrs tl = ta;
-    const bool moved = valid && i >= ta.next;
-    const uint32_t MV = __ballot_sync(0xffffffffu, moved);
-    if (moved) {
-      do { ++rl; } while (tt.off(rl + 1) <= i);
-      tt.load(rl, tl);
-    }
-    const uint32_t t = tlo + rl;
-    const bool head = valid && i == tl.cur;
-    const bool is_layer = valid && f_level(f) == XSP_LEVEL_LAYER;
-    const bool klr = valid && (is_kernel_launch(f) || is_sync_kernel(f));
-    const bool exr = valid && is_exec(f);
-    const bool has_cid = (f & XSP_F_CID) != 0;
-    const bool met = valid && (f & XSP_F_METRICS) != 0;
-    const bool placed = (P >> lane) & 1u;
-    const uint32_t H = __ballot_sync(0xffffffffu, head);
-    const uint32_t LAY = __ballot_sync(0xffffffffu, is_layer);
-    const uint32_t KL = __ballot_sync(0xffffffffu, klr);
-    const uint32_t EXC = __ballot_sync(0xffffffffu, exr && has_cid);
-    const uint32_t MET = __ballot_sync(0xffffffffu, met);
-    const uint32_t gpos = g + __popc(P & lt);
-    const uint32_t klpos = c_kl + __popc(KL & lt);
-    const uint32_t expos = c_ex + __popc(EXC & lt);
-    const uint32_t mrow = c_metric + __popc(MET & lt);
-    // segment (trace) of the lane inside the chunk: it starts at the last head
-    // lane <= lane, or continues the carried state when there is none
-    const uint32_t Hle = H & le;
-    const int s = Hle ? 31 - __clz(Hle) : -1;
-    const uint64_t v = placed ? (e == ~0ull ? e : e + 1) : 0;  // ends stored +1 (0 = none)
-    uint64_t R = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t u = __shfl_up_sync(0xffffffffu, R, o);
-      if ((int)lane - o >= (s < 0 ? 0 : s)) R = max64(R, u);
-    }
-    if (s < 0) R = max64(R, runM);  // inclusive: max end over the segment's placed layers up to the lane
-    uint64_t Rx = __shfl_up_sync(0xffffffffu, R, 1);
-    if ((int)lane == s) Rx = 0;
-    else if (lane == 0) Rx = runM;  // (s < 0 here)
-    // last placed layer before the lane within its segment
-    const uint32_t Pb = P & lt & (s > 0 ? ~((1u << s) - 1u) : 0xffffffffu);
-    const int jl = Pb ? 31 - __clz(Pb) : -1;
-    const uint64_t vj = __shfl_sync(0xffffffffu, v, jl < 0 ? 0 : jl);
-    const uint64_t Rxj = __shfl_sync(0xffffffffu, Rx, jl < 0 ? 0 : jl);
-    const uint64_t lE = jl >= 0 ? vj : (s >= 0 ? 0 : lastE);
-    const uint64_t lM = jl >= 0 ? Rxj : (s >= 0 ? 0 : lastM);
-    // timeline order (begin_ns, rank, span_id) within the trace (span.hpp:161-163)
-    uint64_t pbl = __shfl_up_sync(0xffffffffu, b, 1);
-    uint32_t pfl = __shfl_up_sync(0xffffffffu, (uint32_t)f, 1);
-    if (lane == 0) {
-      pbl = pb;
-      pfl = pf;
-    }
-    if (valid && !head && i > 0 && pbl >= b) {
-      bool bad = pbl > b;
-      if (!bad) {
-        const uint32_t l0 = f_level((uint8_t)pfl), l1 = f_level(f);
-        const uint32_t r0_ = l0 >= 2 ? 3 : l0 + 1, r1_ = l1 >= 2 ? 3 : l1 + 1;
-        bad = r0_ > r1_ || (r0_ == r1_ && __ldg(a.span_id + i - 1) > __ldg(a.span_id + i));
-      }
-      if (bad) atomicOr(a.unsorted, 1u);
-    }
-    if (head) {  // offsets of this trace and the empty traces right before it
-      int64_t tx = t;
-      do {
-        a.t_layer_off[tx] = gpos;
-        a.t_kl_off[tx] = klpos;
-        a.t_ex_off[tx] = expos;
-        --tx;
-      } while (tx >= 0 && __ldg(a.off + tx) == i);
-    }
-    // trace errors raised while walking the bundle (correlator.cpp:146-158); the
-    // model check compares span ids as the reference does
-    if (valid && is_model_span(f) && (uint32_t)i != tl.model && __ldg(a.span_id + i) != tl.msid)
-      atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_MULTI_MODEL);
-    if (valid && f_level(f) >= XSP_LEVEL_KERNEL && !(tl.levels & (1u << XSP_LEVEL_LAYER)))
-      atomicMin(a.err_key + t, ((unsigned long long)i << 8) | XSP_T_SKIP_LEVEL);
-    // layers (correlator.cpp:168-212)
-    if (placed) {
-      a.layer_row[gpos] = (uint32_t)i;
-      a.layer_dur[gpos] = clamp_dur(b, e);
-      a.layer_attr_row[gpos] = c_lay + __popc(LAY & lt);
-    } else if (is_layer) {
-      emit_orphan(a.orph, t, CAT_LAYER, i, (uint32_t)i,
-                  f_kind(f) != XSP_KIND_SYNC ? XSP_O_LAYER_NON_SYNC
-                                             : ((f & XSP_F_PARENT) ? XSP_O_LAYER_BAD_PARENT
-                                                                   : XSP_O_LAYER_OUTSIDE_MODEL));
-    }
-    // kernel launches and synchronous kernels (correlator.cpp:226-268)
-    if (klr) {
-      uint32_t par;
-      if (f & XSP_F_PARENT) {
-        par = PAR_PENDING;
-        const uint32_t sl = atomicAdd(a.pend_count, 1u);
-        if (sl < a.pend_cap) a.pend_kl[sl] = klpos;
-      } else {
-        const bool in_j = lE > e;  // end_j >= e (ends stored +1)
-        const bool in_m = lM > e;  // an earlier layer has end >= e
-        if (in_j && !in_m) {
-          par = gpos - 1;
-        } else if (!in_j && !in_m && e != ~0ull) {  // e == UINT64_MAX: exact rare path
-          par = PAR_ORPHAN;
-          emit_orphan(a.orph, t, CAT_KERNEL, i, (uint32_t)i, XSP_O_KERNEL_NO_LAYER);
-        } else {
-          par = PAR_AMBIG;
-          const uint32_t sl = atomicAdd(a.amb_count, 1u);
-          if (sl < a.amb_cap) {
-            a.amb_kl[sl] = klpos;
-            a.amb_gx[sl] = gpos;
-          }
-        }
-      }
-      KlEnt ent;
-      ent.row = (uint32_t)i;
-      ent.parent = par;
-      ent.cid = has_cid ? sm.cid[sw128(jj)] : 0;
-      a.kl[klpos] = ent;
-      if (is_sync_kernel(f)) a.kl_mrow[klpos] = met ? mrow : kNone;
-    }
-    // executions: with a cid into the exec list, without one an orphan
-    if (exr) {
-      if (has_cid) {
-        ExEnt ent;
-        ent.row = (uint32_t)i;
-        ent.mrow = met ? mrow : kNone;
-        ent.dur = clamp_dur(b, e);
-        a.ex[expos] = ent;
-      } else if (!a.parents_only) {
-        emit_orphan(a.orph, t, CAT_EXEC_NOCID, i, (uint32_t)i, XSP_O_EXEC_NO_CID);
-      }
-    }
-    // carry to the next chunk: the state after lane 31
-    {
-      const int s31 = H ? 31 - __clz(H) : -1;
-      const uint32_t Pt = P & (s31 > 0 ? ~((1u << s31) - 1u) : 0xffffffffu);
-      const int j31 = Pt ? 31 - __clz(Pt) : -1;
-      const uint64_t v31 = __shfl_sync(0xffffffffu, v, j31 < 0 ? 0 : j31);
-      const uint64_t rx31 = __shfl_sync(0xffffffffu, Rx, j31 < 0 ? 0 : j31);
-      runM = __shfl_sync(0xffffffffu, R, 31);
-      if (j31 >= 0) {
-        lastE = v31;
-        lastM = rx31;
-      } else if (s31 >= 0) {
-        lastE = lastM = 0;
-      }
-      g += __popc(P);
-      c_lay += __popc(LAY);
-      c_kl += __popc(KL);
-      c_ex += __popc(EXC);
-      c_metric += __popc(MET);
-      pb = __shfl_sync(0xffffffffu, b, 31);
-      pf = __shfl_sync(0xffffffffu, (uint32_t)f, 31);
-      if (MV) {
-        r = __shfl_sync(0xffffffffu, rl, 31);
-        tt.load(r, ta);
-      }
-    }
-  }
+// Direct mode: a trace is merge-aligned iff it has as many execs (with a cid)
+// as kernel-list entries and all of them share one (cid - position) value;
+// then launch r and exec r carry the same cid, the cids increase strictly and
+// none repeats — what the reference's hash join produces (correlator.cpp:287-364).
+// Since the positions are global, equal per-trace counts make launch r and
+// exec r of every trace share one position.
+__global__ void k_direct_check(uint32_t T, const uint32_t* __restrict__ t_kl_off,
+                               const uint32_t* __restrict__ t_ex_off, const unsigned long long* __restrict__ dmin,
+                               const unsigned long long* __restrict__ dmax, const uint32_t* __restrict__ totals,
+                               uint32_t* __restrict__ l_koff, uint32_t* __restrict__ fail) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t == 0) l_koff[totals[0]] = totals[1];
+  if (t >= T) return;
+  const uint32_t nk = t_kl_off[t + 1] - t_kl_off[t], nx = t_ex_off[t + 1] - t_ex_off[t];
+  if (nk != nx || (nk && dmin[t] != dmax[t])) *fail = 1;
 }
 // Offsets of traces that start at or after the end of the span table (empty
 // trailing traces) and the [T] sentinel.
@@ -1557,14 +1296,86 @@ __global__ void k_resolve_explicit(const uint32_t* __restrict__ pend_kl, const u
 // Ambiguities (correlator.cpp:242-257): all placed layers of the trace that
 // precede the child in timeline order (g < gx) with end >= child end.
 
+// The candidates are found through a 32-ary max tree over the placed layers'
+// ends (level 0 = end[layer_row[g]], level L+1 = max of 32 level-L nodes):
+// walking back from the child, a node whose max end is below the child's end is
+// skipped whole, so each candidate costs O(32 * levels) loads however far back
+// it lies (the reference's IntervalTree prunes on subtree max end the same way,
+// correlator.cpp:79-109). Scanning layer by layer was O(layers of the trace) per
+// child: quadratic on one long trace with concurrent layer groups (C4).
+constexpr int kMtLevels = 7;  // 32^6 > 2^30 leaves under the top level
+struct MaxTree {
+  const uint64_t* lv[kMtLevels];  // lv[0] unused (leaves are read through layer_row)
+  uint32_t n[kMtLevels];
+  int levels;  // number of levels in use (>= 1); the top one has <= 32 nodes
+  const uint32_t* layer_row;
+  const uint64_t* end;
+};
+
+__device__ __forceinline__ uint64_t mt_val(const MaxTree& m, int L, uint32_t i) {
+  return L == 0 ? __ldg(m.end + __ldg(m.layer_row + i)) : __ldg(m.lv[L] + i);
+}
+
+// Largest layer index g' in [lo, g) with end >= e, or kNone.
+__device__ uint32_t mt_prev(const MaxTree& m, uint32_t g, uint32_t lo, uint64_t e) {
+  if (g <= lo) return kNone;
+  int L = 0;
+  uint32_t i = g;  // exclusive bound at level L
+  uint32_t j = kNone;
+  for (;;) {  // ascend until a node of the bound's 32-group (and >= lo) holds an end >= e
+    const uint32_t lo_l = lo >> (5 * L);
+    const uint32_t grp = (i - 1) & ~31u;
+    const uint32_t stop = grp > lo_l ? grp : lo_l;
+    for (uint32_t x = i; x > stop;) {
+      --x;
+      if (mt_val(m, L, x) >= e) {
+        j = x;
+        break;
+      }
+    }
+    if (j != kNone) break;
+    if (grp <= lo_l || L + 1 >= m.levels) return kNone;
+    i = grp >> 5;
+    ++L;
+  }
+  while (L > 0) {  // descend into the rightmost child holding an end >= e
+    --L;
+    const uint32_t lo_l = lo >> (5 * L);
+    const uint32_t c0 = j << 5, c1 = min(c0 + 32u, m.n[L]);
+    const uint32_t stop = c0 > lo_l ? c0 : lo_l;
+    uint32_t k = kNone;
+    for (uint32_t x = c1; x > stop;) {
+      --x;
+      if (mt_val(m, L, x) >= e) {
+        k = x;
+        break;
+      }
+    }
+    if (k == kNone) return kNone;  // only the node straddling lo: its max came from below lo
+    j = k;
+  }
+  return j;
+}
+
+__global__ void k_mt_level(const uint64_t* __restrict__ in, const uint32_t* __restrict__ layer_row,
+                           const uint64_t* __restrict__ end, uint32_t n_in, uint64_t* __restrict__ out) {
+  const uint32_t o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = lane_id();
+  const uint32_t x = o * 32u + lane;
+  if (o * 32u >= n_in) return;
+  uint64_t v = 0;
+  if (x < n_in) v = in ? in[x] : end[layer_row[x]];
+#pragma unroll
+  for (int s = 16; s; s >>= 1) v = max64(v, __shfl_xor_sync(0xffffffffu, v, s));
+  if (lane == 0) out[o] = v;
+}
+
 // Children flagged in pass 1 with >= 2 candidates, or whose last preceding
 // layer does not contain them while an earlier one might: count exactly.
 __global__ void k_amb_resolve(uint32_t n_raw, const uint32_t* __restrict__ amb_kl,
                               const uint32_t* __restrict__ amb_gx, KlEnt* __restrict__ kl,
                               const uint64_t* __restrict__ end, const uint32_t* __restrict__ t_kl_off,
                               const uint32_t* __restrict__ t_layer_off, uint32_t T,
-                              const uint32_t* __restrict__ layer_row, uint32_t* __restrict__ keep,
-                              Orphans orph) {
+                              const __grid_constant__ MaxTree mt, uint32_t* __restrict__ keep, Orphans orph) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_raw) return;
   const uint32_t k = amb_kl[p];
@@ -1572,18 +1383,12 @@ __global__ void k_amb_resolve(uint32_t n_raw, const uint32_t* __restrict__ amb_k
   const uint32_t row = kl[k].row;
   const uint64_t e = end[row];
   const uint32_t lo = t_layer_off[t];
-  uint32_t cnt = 0, last = kNone;
-  for (uint32_t g = amb_gx[p]; g > lo && cnt < 2;) {
-    --g;
-    if (end[layer_row[g]] >= e) {
-      ++cnt;
-      last = g;
-    }
-  }
-  if (cnt == 1) {
-    kl[k].parent = last;
+  const uint32_t g1 = mt_prev(mt, amb_gx[p], lo, e);
+  const uint32_t g2 = g1 == kNone ? kNone : mt_prev(mt, g1, lo, e);
+  if (g1 != kNone && g2 == kNone) {
+    kl[k].parent = g1;
     keep[p] = 0;
-  } else if (cnt == 0) {  // only for a child ending at UINT64_MAX (see k_pass1)
+  } else if (g1 == kNone) {  // only for a child ending at UINT64_MAX (see k_pass1)
     kl[k].parent = PAR_ORPHAN;
     keep[p] = 0;
     emit_orphan(orph, t, CAT_KERNEL, row, row, XSP_O_KERNEL_NO_LAYER);
@@ -1617,15 +1422,16 @@ __global__ void k_amb_count(const uint32_t* __restrict__ order, uint32_t n_amb,
                             const uint32_t* __restrict__ amb_kl, const uint32_t* __restrict__ amb_gx,
                             const KlEnt* __restrict__ kl, const uint64_t* __restrict__ end,
                             const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_layer_off,
-                            uint32_t T, const uint32_t* __restrict__ layer_row, uint32_t* __restrict__ cnt) {
+                            uint32_t T, const __grid_constant__ MaxTree mt, uint32_t* __restrict__ cnt) {
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n_amb) return;
   uint32_t p = order[q];
   uint32_t k = amb_kl[p];
   uint32_t t = trace_of32(t_kl_off, T, k);
   uint64_t e = end[kl[k].row];
+  const uint32_t lo = t_layer_off[t];
   uint32_t c = 0;
-  for (uint32_t g = t_layer_off[t]; g < amb_gx[p]; ++g) c += end[layer_row[g]] >= e;
+  for (uint32_t g = mt_prev(mt, amb_gx[p], lo, e); g != kNone; g = mt_prev(mt, g, lo, e)) ++c;
   cnt[q] = c;
 }
 
@@ -1633,9 +1439,9 @@ __global__ void k_amb_fill(const uint32_t* __restrict__ order, uint32_t n_amb,
                            const uint32_t* __restrict__ amb_kl, const uint32_t* __restrict__ amb_gx,
                            const KlEnt* __restrict__ kl, const uint64_t* __restrict__ end,
                            const uint64_t* __restrict__ sid, const uint32_t* __restrict__ t_kl_off,
-                           const uint32_t* __restrict__ t_layer_off, uint32_t T,
-                           const uint32_t* __restrict__ layer_row, const uint32_t* __restrict__ cand_off,
-                           uint32_t* __restrict__ amb_row, uint32_t* __restrict__ cand_row) {
+                           const uint32_t* __restrict__ t_layer_off, uint32_t T, const __grid_constant__ MaxTree mt,
+                           const uint32_t* __restrict__ cand_off, uint32_t* __restrict__ amb_row,
+                           uint32_t* __restrict__ cand_row) {
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n_amb) return;
   uint32_t p = order[q];
@@ -1643,10 +1449,10 @@ __global__ void k_amb_fill(const uint32_t* __restrict__ order, uint32_t n_amb,
   uint32_t t = trace_of32(t_kl_off, T, k);
   uint64_t e = end[kl[k].row];
   amb_row[q] = kl[k].row;
+  const uint32_t lo = t_layer_off[t];
   uint32_t o = cand_off[q], n = 0;
-  for (uint32_t g = t_layer_off[t]; g < amb_gx[p]; ++g) {
-    uint32_t r = layer_row[g];
-    if (end[r] < e) continue;
+  for (uint32_t g = mt_prev(mt, amb_gx[p], lo, e); g != kNone; g = mt_prev(mt, g, lo, e)) {
+    uint32_t r = mt.layer_row[g];
     // insertion by span_id (IntervalTree::containing sorts by span_id, :115-117)
     uint64_t s = sid[r];
     uint32_t j = n;
@@ -1684,46 +1490,50 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
                              const uint64_t* __restrict__ cid,
                              const uint8_t* __restrict__ flags, const uint32_t* __restrict__ t_kl_off,
                              const uint32_t* __restrict__ t_ex_off, uint32_t T, uint32_t* __restrict__ t_slow,
-                             uint32_t* __restrict__ any_slow, uint32_t* __restrict__ t_nomono) {
+                             uint32_t* __restrict__ any_slow, unsigned long long* __restrict__ t_lmin,
+                             unsigned long long* __restrict__ t_lmax) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t first = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
   if (first >= nkl) return;
   const uint32_t t = warp_trace_of(t_kl_off, T, k < nkl ? k : nkl - 1, first);
-  if (k >= nkl) return;
-  const uint32_t r = k - t_kl_off[t];
-  const KlEnt ent = kl[k];
-  const uint8_t f = flags[ent.row];
-  const bool mono = f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID) && (r == 0 || kl[k - 1].cid < ent.cid);
-  if (!mono) t_nomono[t] = 1;
-  const bool was_slow = t_slow[t] != 0;
-  // only the first mismatch of a trace stores (a reordered long trace would
-  // otherwise have every launch store to the same two words)
-  if (!was_slow && !(mono && cid[ex[t_ex_off[t] + r].row] == ent.cid)) {
-    t_slow[t] = 1;
-    *any_slow = 1;
+  uint32_t tl = kNone;
+  uint64_t c = 0;
+  if (k < nkl) {
+    const uint32_t r = k - t_kl_off[t];
+    const KlEnt ent = kl[k];
+    const uint8_t f = flags[ent.row];
+    const bool launch = f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID);
+    const bool mono = launch && (r == 0 || kl[k - 1].cid < ent.cid);
+    if (launch) {
+      tl = t;
+      c = ent.cid;
+    }
+    const bool was_slow = t_slow[t] != 0;
+    // only the first mismatch of a trace stores (a reordered long trace would
+    // otherwise have every launch store to the same two words)
+    if (!was_slow && !(mono && cid[ex[t_ex_off[t] + r].row] == ent.cid)) {
+      t_slow[t] = 1;
+      *any_slow = 1;
+    }
   }
+  minmax_atomic_warp(tl, c, c, t_lmin, t_lmax);  // the launch cid range of every trace
 }
 
-// Direct-address join for slow traces whose launches carry strictly increasing
-// cids over a dense range (e.g. executions reordered across streams): the slot
-// of a cid is cid - lmin, with no hashing or probing. t_lmin[t] = the first
-// launch cid, or ~0 when t uses the hash table.
+// Direct-address join for slow traces whose launch cids span a dense range
+// (in any order: executions reordered across streams, concurrent layers'
+// interleaved launches): the slot of a cid is cid - lmin, with no hashing or
+// probing. t_lmin[t] = the least launch cid (k_join_check), or ~0 when t uses
+// the hash table.
 __global__ void k_join_direct(const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_slow,
-                              const uint32_t* __restrict__ t_nomono, const KlEnt* __restrict__ kl, uint32_t T,
-                              uint64_t* __restrict__ t_lmin, uint64_t* __restrict__ t_lmax) {
+                              uint32_t T, uint64_t* __restrict__ t_lmin, uint64_t* __restrict__ t_lmax) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   const uint32_t k0 = t_kl_off[t], k1 = t_kl_off[t + 1];
-  uint64_t lmin = ~0ull, lmax = 0;
-  if (t_slow[t] && !t_nomono[t] && k1 > k0) {
-    const uint64_t a = kl[k0].cid, b = kl[k1 - 1].cid;
-    if (b - a < 4ull * (k1 - k0) + 64) {
-      lmin = a;
-      lmax = b;
-    }
+  const uint64_t a = t_lmin[t], b = t_lmax[t];
+  if (!(t_slow[t] && a != ~0ull && b - a < 4ull * (k1 - k0) + 64)) {
+    t_lmin[t] = ~0ull;
+    t_lmax[t] = 0;
   }
-  t_lmin[t] = lmin;
-  t_lmax[t] = lmax;
 }
 
 // An exec whose cid lies outside its direct trace's launch range matches no
@@ -2351,18 +2161,39 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     col_tmap(&maps.cid, c->cid, n);
     col_tmap(&maps.parent, c->parent_id, n);
   }
+  const bool try_clean = !parents_only;
+  const bool direct = try_clean && ctx->direct_hint;
+  if (try_clean) {
+    out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", n);
+    out->kernel_exec_row = ctx->d<uint32_t>("o.k_exec", n);
+    out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", n);
+    out->kernel_dur = ctx->d<uint64_t>("o.k_dur", n);
+    out->kernel_name = ctx->d<uint32_t>("o.k_name", n);
+    out->kernel_occ = ctx->d<double>("o.k_occ", n);
+    out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", n + 1);
+  }
+  if (direct) {
+    a.k_launch = out->kernel_launch_row;
+    a.k_exec = out->kernel_exec_row;
+    a.k_mrow = out->kernel_metric_row;
+    a.k_dur = out->kernel_dur;
+    a.k_name = out->kernel_name;
+    a.k_occ = out->kernel_occ;
+    a.l_koff = out->layer_kernel_off;
+    a.name = c->name_id;
+    a.occ = c->occupancy;
+    a.t_dmin = ctx->d<unsigned long long>("c.t_dmin", T + 1);
+    a.t_dmax = ctx->d<unsigned long long>("c.t_dmax", T + 1);
+    a.direct_fail = counters + 7;
+    XSP_CUDA(cudaMemsetAsync(a.t_dmin, 0xFF, (T + 1) * 8ull, st));
+    XSP_CUDA(cudaMemsetAsync(a.t_dmax, 0, (T + 1) * 8ull, st));
+  }
   if (ntiles) {
-    XSP_CUDA(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM));
+    XSP_CUDA(cudaFuncSetAttribute(k_pass1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM));
+    XSP_CUDA(cudaFuncSetAttribute(k_pass1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM));
     ctx->stage_begin("pass1_reduce", st);
-    static const bool serial_reduce = getenv("XSP_P1_SERIAL_REDUCE") != nullptr;
-    if (serial_reduce) {
-      XSP_CUDA(cudaFuncSetAttribute(k_p1_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_RED_SMEM));
-      k_p1_reduce<<<ntiles, P1_THREADS, P1_RED_SMEM, st>>>(a, maps);
-    } else {
-      XSP_CUDA(cudaFuncSetAttribute(k_p1_reduce_lanes, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)P1_RED_SMEM));
-      k_p1_reduce_lanes<<<ntiles, P1_THREADS, P1_RED_SMEM, st>>>(a, maps);
-    }
+    XSP_CUDA(cudaFuncSetAttribute(k_p1_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_RED_SMEM));
+    k_p1_reduce<<<ntiles, P1_THREADS, P1_RED_SMEM, st>>>(a, maps);
     ctx->stage_end("pass1_reduce", st);
     ctx->stage_begin("pass1_scan", st);
     k_p1_scan<<<1, P1_SCAN_THREADS, 0, st>>>(a.group_sum, (ntiles + 31) / 32, a.tile_prefix);
@@ -2370,13 +2201,10 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
                                                                            a.tile_excl);
     ctx->stage_end("pass1_scan", st);
     ctx->stage_begin("pass1", st);
-    static const bool serial_emit = getenv("XSP_P1_SERIAL") != nullptr;
-    if (serial_emit) {
-      k_pass1<<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
-    } else {
-      XSP_CUDA(cudaFuncSetAttribute(k_pass1_lanes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM));
-      k_pass1_lanes<<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
-    }
+    if (direct)
+      k_pass1<true><<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
+    else
+      k_pass1<false><<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
     ctx->stage_end("pass1", st);
     ctx->launches += 4;
   }
@@ -2390,22 +2218,19 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   // merge-aligned fuses launch r with exec r (k_gather_fast verifies it). Buffers
   // are sized by the span count; the device totals gate the kernels. ONE
   // read-back then decides: done, unsorted, or the general path below.
-  const bool try_clean = !parents_only;
   auto* no_dup = ctx->d<unsigned long long>("c.no_dup", T);
   if (try_clean) {
-    out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", n);
-    out->kernel_exec_row = ctx->d<uint32_t>("o.k_exec", n);
-    out->kernel_metric_row = ctx->d<uint32_t>("o.k_mrow", n);
-    out->kernel_dur = ctx->d<uint64_t>("o.k_dur", n);
-    out->kernel_name = ctx->d<uint32_t>("o.k_name", n);
-    out->kernel_occ = ctx->d<double>("o.k_occ", n);
-    out->layer_kernel_off = ctx->d<uint32_t>("o.l_koff", n + 1);
     ctx->stage_begin("gather", st);
-    const unsigned gb = std::min<uint64_t>(ceil_div((uint64_t)n + 1, 256), 148u * 8u);
-    k_gather_fast<<<gb, 256, 0, st>>>(totals, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, c->cid,
-                                      c->name_id, c->occupancy, out->kernel_launch_row,
-                                      out->kernel_exec_row, out->kernel_metric_row, out->kernel_dur,
-                                      out->kernel_name, out->kernel_occ, out->layer_kernel_off, counters + 7);
+    if (direct) {
+      k_direct_check<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(T, a.t_kl_off, a.t_ex_off, a.t_dmin, a.t_dmax,
+                                                                      totals, out->layer_kernel_off, counters + 7);
+    } else {
+      const unsigned gb = std::min<uint64_t>(ceil_div((uint64_t)n + 1, 256), 148u * 8u);
+      k_gather_fast<<<gb, 256, 0, st>>>(totals, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, c->cid,
+                                        c->name_id, c->occupancy, out->kernel_launch_row,
+                                        out->kernel_exec_row, out->kernel_metric_row, out->kernel_dur,
+                                        out->kernel_name, out->kernel_occ, out->layer_kernel_off, counters + 7);
+    }
     ++ctx->launches;
     out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
     launch(ctx, k_trace_kernel_off, (uint64_t)T + 1, st, T, a.t_layer_off, out->layer_kernel_off,
@@ -2434,7 +2259,9 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     (void)sort_if_needed;
     throw std::runtime_error("UNSORTED");
   }
-  if (try_clean && htot[8] == 0 && n_pend == 0 && n_amb_raw == 0 && htot[15] == 0) {
+  const bool clean = try_clean && htot[8] == 0 && n_pend == 0 && n_amb_raw == 0 && htot[15] == 0;
+  if (try_clean) ctx->direct_hint = clean;
+  if (clean) {
     cache_offsets_end(ctx, a.t_layer_off, out->trace_kernel_off, T);
     out->n_traces = T;
     out->n_failed = htot[12];
@@ -2461,6 +2288,18 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     return;
   }
   if (try_clean) XSP_CUDA(cudaMemsetAsync(counters + 4, 0, 4 * 4, st));  // general path: reset n_failed, flags
+  if (direct) {
+    // the guess was wrong: pass 1 again, writing the kernel-list / exec entries
+    // the general join needs (same outputs otherwise; the rare-entry lists are
+    // refilled, so their counters restart)
+    XSP_CUDA(cudaMemsetAsync(counters, 0, 3 * 4, st));
+    if (ntiles) {
+      ctx->stage_begin("pass1", st);
+      k_pass1<false><<<ntiles, P1_THREADS, P1_SMEM, st>>>(a, maps);
+      ctx->stage_end("pass1", st);
+      ++ctx->launches;
+    }
+  }
 
   // ---- explicit parents
   if (n_pend) {
@@ -2473,11 +2312,30 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
 
   // ---- rare containment cases: exact candidate count by scanning back
   uint32_t n_amb = 0;
-  if (n_amb_raw) {
+  MaxTree mt;
+  memset(&mt, 0, sizeof(mt));
+  if (n_amb_raw) {  // the layers' max tree for the exact candidate walks
+    mt.layer_row = a.layer_row;
+    mt.end = c->end_ns;
+    mt.n[0] = nl;
+    mt.levels = 1;
+    const uint64_t* prev = nullptr;
+    while (mt.n[mt.levels - 1] > 32 && mt.levels < kMtLevels) {
+      const int L = mt.levels;
+      const uint32_t nin = mt.n[L - 1];
+      mt.n[L] = (nin + 31) / 32;
+      uint64_t* lv = ctx->d<uint64_t>(L == 1 ? "c.mt1" : L == 2 ? "c.mt2" : L == 3 ? "c.mt3" : L == 4 ? "c.mt4"
+                                                                    : L == 5 ? "c.mt5" : "c.mt6", mt.n[L]);
+      k_mt_level<<<ceil_div((uint64_t)mt.n[L], 8), 256, 0, st>>>(prev, a.layer_row, c->end_ns, nin, lv);
+      ++ctx->launches;
+      mt.lv[L] = lv;
+      prev = lv;
+      ++mt.levels;
+    }
     uint32_t* keep = ctx->d<uint32_t>("c.amb_keep", n_amb_raw + 1);
     uint32_t* pos = ctx->d<uint32_t>("c.amb_pos", n_amb_raw + 1);
     launch(ctx, k_amb_resolve, n_amb_raw, st, n_amb_raw, a.amb_kl, a.amb_gx, a.kl, c->end_ns, a.t_kl_off,
-           a.t_layer_off, T, a.layer_row, keep, orph);
+           a.t_layer_off, T, mt, keep, orph);
     uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
     exclusive_scan<uint32_t, uint32_t>(keep, pos, n_amb_raw, scan_tmp, counters + 6, st, &ctx->launches);
     uint32_t* kl2 = ctx->d<uint32_t>("c.amb_kl2", n_amb_raw);
@@ -2506,7 +2364,7 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     radix_sort_pairs(ktr2, idx, n_amb, 0, 32, rs, st, &ctx->launches);
     uint32_t* cnt = ctx->d<uint32_t>("c.amb_cnt", n_amb + 1);
     launch(ctx, k_amb_count, n_amb, st, idx, n_amb, a.amb_kl, a.amb_gx, a.kl, c->end_ns, a.t_kl_off,
-           a.t_layer_off, T, a.layer_row, cnt);
+           a.t_layer_off, T, mt, cnt);
     uint32_t* scan_tmp = ctx->d<uint32_t>("c.scan_tmp", scan_scratch_elems(n + 16));
     uint32_t* tot = ctx->d<uint32_t>("c.amb_tot", 1);
     exclusive_scan<uint32_t, uint32_t>(cnt, out->amb_cand_off, n_amb, scan_tmp, tot, st, &ctx->launches);
@@ -2515,7 +2373,7 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     out->n_candidates = ncand;
     out->amb_cand_row = ctx->d<uint32_t>("o.amb_cand_row", ncand);
     launch(ctx, k_amb_fill, n_amb, st, idx, n_amb, a.amb_kl, a.amb_gx, a.kl, c->end_ns, c->span_id, a.t_kl_off,
-           a.t_layer_off, T, a.layer_row, out->amb_cand_off, out->amb_row, out->amb_cand_row);
+           a.t_layer_off, T, mt, out->amb_cand_off, out->amb_row, out->amb_cand_row);
     launch(ctx, k_csr_by_trace, (uint64_t)T + 1, st, T, n_amb, ktr2, 0, out->trace_amb_off);
   } else {
     out->amb_cand_row = ctx->d<uint32_t>("o.amb_cand_row", 1);
@@ -2533,17 +2391,20 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   j.t_ex_off = a.t_ex_off;
   j.t_kl_off = a.t_kl_off;
   uint32_t* t_slow = ctx->d<uint32_t>("c.t_slow", T + 1);
-  uint32_t* t_nomono = ctx->d<uint32_t>("c.t_nomono", T + 1);
+  uint64_t* t_lmin = ctx->d<uint64_t>("c.t_lmin", T + 1);
+  uint64_t* t_lmax = ctx->d<uint64_t>("c.t_lmax", T + 1);
   j.t_slow = t_slow;
   j.T = T;
   j.n_ex = nex;
   j.n_kl = nkl;
   uint32_t any_slow = 0;
   if (!parents_only) {
-    XSP_CUDA(cudaMemsetAsync(t_nomono, 0, (T + 1) * 4ull, st));
+    XSP_CUDA(cudaMemsetAsync(t_lmin, 0xFF, (T + 1) * 8ull, st));
+    XSP_CUDA(cudaMemsetAsync(t_lmax, 0, (T + 1) * 8ull, st));
     launch(ctx, k_join_counts, T, st, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
     launch(ctx, k_join_check, nkl, st, nkl, a.kl, a.ex, c->cid, c->flags, a.t_kl_off, a.t_ex_off, T, t_slow,
-           counters + 7, t_nomono);
+           counters + 7, reinterpret_cast<unsigned long long*>(t_lmin),
+           reinterpret_cast<unsigned long long*>(t_lmax));
     any_slow = read_u32(ctx, counters + 7, st);
   }
   auto* dup_ex = ctx->d<unsigned long long>("c.dup_ex", T);
@@ -2555,12 +2416,10 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   if (any_slow) {
     uint64_t* rsize = ctx->d<uint64_t>("c.rsize", T + 1);
     uint64_t* roff = ctx->d<uint64_t>("c.roff", T + 1);
-    uint64_t* t_lmin = ctx->d<uint64_t>("c.t_lmin", T + 1);
-    uint64_t* t_lmax = ctx->d<uint64_t>("c.t_lmax", T + 1);
     if (getenv("XSP_JOIN_HASH")) {
       XSP_CUDA(cudaMemsetAsync(t_lmin, 0xFF, (T + 1) * 8ull, st));
     } else {
-      launch(ctx, k_join_direct, T, st, a.t_kl_off, t_slow, t_nomono, a.kl, T, t_lmin, t_lmax);
+      launch(ctx, k_join_direct, T, st, a.t_kl_off, t_slow, T, t_lmin, t_lmax);
       launch(ctx, k_join_far, nex, st, nex, a.ex, c->cid, a.t_ex_off, T, t_lmin, t_lmax);
     }
     j.t_lmin = t_lmin;

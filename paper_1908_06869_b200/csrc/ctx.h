@@ -98,6 +98,10 @@ struct xsp_ctx {
   // group tables on the host instead of with another device round trip.
   // capacities the rare-entry lists of correlate needed (grow-only hints)
   uint64_t cap_orph = 0, cap_amb = 0, cap_pend = 0;
+  // correlate tries pass 1 in direct mode (kernel table written by pass 1) while
+  // the previous call on this context was a clean batch (a guess: a wrong one
+  // costs a second pass 1, never a different result)
+  bool direct_hint = true;
 
   const void* hc_layer_key = nullptr;
   const void* hc_kernel_key = nullptr;
