@@ -558,34 +558,55 @@ __device__ __forceinline__ void chain_fold(const double* __restrict__ v, const d
   }
 }
 
+// a15 model latency (trimmed mean over the runs' model spans, analysis.cpp:
+// 154-157): one warp per group, launched before the per-kernel pass so the a10
+// and a15 passes that divide by it can run concurrently. Lane r loads run r's
+// model span; every lane then runs the same trimmed mean over the shuffled
+// values (warp-uniform, no idle lanes).
+__global__ void k_model_lat(ModelArgs a) {
+  const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+  if (g >= a.G) return;
+  if (a.gstatus[g] != XSP_G_OK) {
+    if (lane == 0) a.m_lat[g] = nan("");
+    return;
+  }
+  const uint32_t R = a.nr[g], t0 = a.ft[g];
+  uint64_t mdur = 0;
+  if (lane < R) {
+    const uint32_t m = a.model_row[t0 + lane];
+    mdur = clamp_dur(a.begin[m], a.end[m]);
+  }
+  uint64_t mdur_hi = 0;  // runs 32..63
+  if (R > 32 && lane + 32 < R) {
+    const uint32_t m = a.model_row[t0 + 32 + lane];
+    mdur_hi = clamp_dur(a.begin[m], a.end[m]);
+  }
+  const double mlat = trimmed_mean_int(
+      [&](uint32_t r) {
+        const uint64_t lo = __shfl_sync(0xffffffffu, mdur, r & 31u);
+        const uint64_t hi = __shfl_sync(0xffffffffu, mdur_hi, r & 31u);
+        if (r >= 64) {  // more than 64 runs: the rest straight from the model spans
+          const uint32_t m = a.model_row[t0 + r];
+          return clamp_dur(a.begin[m], a.end[m]);
+        }
+        return r < 32 ? lo : hi;
+      },
+      R, a.trim);
+  if (lane == 0) a.m_lat[g] = mlat;
+}
+
 __global__ void __launch_bounds__(64) k_models(ModelArgs a) {
-  __shared__ double s_gpu, s_mlat;
+  __shared__ double s_gpu;
   __shared__ unsigned long long s_cnt[3];
   const uint32_t g = blockIdx.x;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   if (g >= a.G) return;
-  if (a.gstatus[g] != XSP_G_OK) {
-    if (threadIdx.x == 0) a.m_lat[g] = nan("");
-    return;
-  }
+  if (a.gstatus[g] != XSP_G_OK) return;  // m_lat = NaN (k_model_lat)
   const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
   const bool big_k = a.gkc_off && a.gkc_off[g + 1] > a.gkc_off[g];
   const bool big_l = a.glc_off && a.glc_off[g + 1] > a.glc_off[g];
   double lat = 0.0, occw = 0.0;
   if (warp == 1) {
-    const uint32_t R = a.nr[g], t0 = a.ft[g];
-    // model latency: lane r loads run r's model span; every lane then runs the
-    // same trimmed mean over the shuffled values (warp-uniform, no idle lanes)
-    uint64_t mdur = 0;
-    if (lane < R) {
-      const uint32_t m = a.model_row[t0 + lane];
-      mdur = clamp_dur(a.begin[m], a.end[m]);
-    }
-    uint64_t mdur_hi = 0;  // runs 32..63 (kMaxRuns)
-    if (R > 32 && lane + 32 < R) {
-      const uint32_t m = a.model_row[t0 + 32 + lane];
-      mdur_hi = clamp_dur(a.begin[m], a.end[m]);
-    }
     // u64 counters: any order is exact
     uint64_t f = 0, rd = 0, wr = 0;
     if (big_k) {
@@ -613,20 +634,8 @@ __global__ void __launch_bounds__(64) k_models(ModelArgs a) {
     } else {
       chain_fold<false>(a.l_kern_lat, nullptr, a.gl_off[g], a.gl_off[g + 1], lane, gpu, unused);
     }
-    const double mlat = trimmed_mean_int(
-        [&](uint32_t r) {
-          const uint64_t lo = __shfl_sync(0xffffffffu, mdur, r & 31u);
-          const uint64_t hi = __shfl_sync(0xffffffffu, mdur_hi, r & 31u);
-          if (r >= 64) {  // more than 64 runs: the rest straight from the model spans
-            const uint32_t m = a.model_row[t0 + r];
-            return clamp_dur(a.begin[m], a.end[m]);
-          }
-          return r < 32 ? lo : hi;
-        },
-        R, a.trim);
     if (lane == 0) {
       s_gpu = gpu;
-      s_mlat = mlat;
       s_cnt[0] = f;
       s_cnt[1] = rd;
       s_cnt[2] = wr;
@@ -648,10 +657,9 @@ __global__ void __launch_bounds__(64) k_models(ModelArgs a) {
   __syncthreads();
   if (threadIdx.x != 0) return;
   const uint64_t f = s_cnt[0], rd = s_cnt[1], wr = s_cnt[2];
-  const double gpu = s_gpu, mlat = s_mlat;
+  const double gpu = s_gpu, mlat = a.m_lat[g];
   const uint64_t n = k1 - k0;
   Roof ro = roofline(f, rd, wr, lat, a.peak, a.bw);
-  a.m_lat[g] = mlat;
   a.m_kern_lat[g] = lat;
   a.m_flops[g] = f;
   a.m_read[g] = rd;
@@ -1753,7 +1761,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   }
   // a long group's chunk tables: partial folds, then the ordered fold + ranking
   auto fold_big = [&](NameBigArgs nb, const uint32_t* d_rng, const uint32_t* d_poff, uint32_t np,
-                      const std::string& tag) {
+                      const std::string& tag, cudaStream_t st) {
     if (np) {
       const uint64_t cap = (uint64_t)np * NCAP;
       NamePartOut po;
@@ -1921,6 +1929,22 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     ma.pl_gpu = p_lat;
   }
   if (G) {
+    k_model_lat<<<ceil_div((uint64_t)G * 32, 256), 256, 0, st>>>(ma);
+    ++ctx->launches;
+  }
+  // a15, a10 and a5 are independent once the kernel / layer rows and the model
+  // latencies exist, and each is bound by its longest group's ordered fp64
+  // chain, not by memory: they run concurrently on three streams
+  const bool fork = G > 0 && TK > 0;
+  cudaStream_t sn = st, sy = st;
+  if (fork) {
+    sn = ctx->side_stream(0);
+    sy = ctx->side_stream(1);
+    XSP_CUDA(cudaEventRecord(ctx->fork_event(), st));
+    XSP_CUDA(cudaStreamWaitEvent(sn, ctx->fork_event(), 0));
+    XSP_CUDA(cudaStreamWaitEvent(sy, ctx->fork_event(), 0));
+  }
+  if (G) {
     k_models<<<G, 64, 0, st>>>(ma);
     ++ctx->launches;
   }
@@ -1931,8 +1955,8 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   // a10 read-back so both totals come back with one sync
   out->group_type_off = ctx->d<uint32_t>("t.g_yoff", G + 1);
   bool types_wide = false;
-  std::function<void()> run_types;
-  run_types = [&]() {
+  std::function<void(cudaStream_t)> run_types;
+  run_types = [&](cudaStream_t st) {
     if (!G) {
       htot[4] = htot[5] = 0;
       return;
@@ -2027,10 +2051,10 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       yb.s_ai = ty.s_ai;
       yb.s_tput = ty.s_tput;
       yb.s_bound = ty.s_bound;
-      fold_big(yb, d_pl, d_pl_off, npl, "a.yp");
+      fold_big(yb, d_pl, d_pl_off, npl, "a.yp", st);
       ++ctx->launches;
     }
-    exclusive_scan<uint32_t, uint32_t>(ty.g_count, out->group_type_off, G, scan_tmp, out->group_type_off + G, st,
+    exclusive_scan<uint32_t, uint32_t>(ty.g_count, out->group_type_off, G, ctx->d<uint32_t>("a.scan_y", scan_scratch_elems(G + 16)), out->group_type_off + G, st,
                                        &ctx->launches);
     xfer_small(htot + 4, out->group_type_off + G, 4, st);
     xfer_small(htot + 5, ty.overflow, 4, st);
@@ -2039,7 +2063,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   auto place_types = [&]() {
     if (htot[5] && !types_wide) {  // more than 32 types somewhere: redo with 128-wide tables
       types_wide = true;
-      run_types();
+      run_types(st);
       XSP_CUDA(cudaStreamSynchronize(st));
     }
     if (htot[5]) throw std::invalid_argument("a5: more than 128 distinct layer types in one analysis group");
@@ -2066,7 +2090,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   uint32_t NN = 0;
   bool names_done = false;
   if (TK && G) {
-    ctx->stage_begin("names", st);
+    ctx->stage_begin("names", sn);
     NameFastArgs nf;
     nf.G = G;
     nf.gk_off = out->group_kernel_off;
@@ -2100,9 +2124,9 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     nf.gk_end = nullptr;
     nf.big = d_gkc;
     nf.raw = 0;
-    XSP_CUDA(cudaMemsetAsync(nf.overflow, 0, 4, st));
+    XSP_CUDA(cudaMemsetAsync(nf.overflow, 0, 4, sn));
     XSP_CUDA(cudaFuncSetAttribute(k_names_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNameSmem));
-    k_names_fast<<<G, NAME_WARPS * 32, kNameSmem, st>>>(nf);
+    k_names_fast<<<G, NAME_WARPS * 32, kNameSmem, sn>>>(nf);
     ++ctx->launches;
     if (nkc) {
       // long groups: raw per-name sums per kernel chunk, then folded in order
@@ -2122,7 +2146,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       nc.s_flops = ctx->d<uint64_t>("a.c_f", ccap);
       nc.s_read = ctx->d<uint64_t>("a.c_r", ccap);
       nc.s_write = ctx->d<uint64_t>("a.c_w", ccap);
-      k_names_fast<<<nkc, NAME_WARPS * 32, kNameSmem, st>>>(nc);
+      k_names_fast<<<nkc, NAME_WARPS * 32, kNameSmem, sn>>>(nc);
       NameBigArgs nb;
       nb.G = G;
       nb.gkc_off = d_gkc;
@@ -2151,15 +2175,21 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       nb.s_ai = nf.s_ai;
       nb.s_tput = nf.s_tput;
       nb.s_bound = nf.s_bound;
-      fold_big(nb, d_pk, d_pk_off, npk, "a.np");
+      fold_big(nb, d_pk, d_pk_off, npk, "a.np", sn);
       ++ctx->launches;
     }
-    exclusive_scan<uint32_t, uint32_t>(nf.g_count, out->group_name_off, G, scan_tmp, out->group_name_off + G, st,
+    exclusive_scan<uint32_t, uint32_t>(nf.g_count, out->group_name_off, G, scan_tmp, out->group_name_off + G, sn,
                                        &ctx->launches);
-    xfer_small(htot + 2, out->group_name_off + G, 4, st);
-    xfer_small(htot + 3, nf.overflow, 4, st);
-    run_types();
+    xfer_small(htot + 2, out->group_name_off + G, 4, sn);
+    xfer_small(htot + 3, nf.overflow, 4, sn);
+    run_types(sy);
     types_done = true;
+    if (fork) {  // join the side streams
+      XSP_CUDA(cudaEventRecord(ctx->join_event(0), sn));
+      XSP_CUDA(cudaEventRecord(ctx->join_event(1), sy));
+      XSP_CUDA(cudaStreamWaitEvent(st, ctx->join_event(0), 0));
+      XSP_CUDA(cudaStreamWaitEvent(st, ctx->join_event(1), 0));
+    }
     XSP_CUDA(cudaStreamSynchronize(st));
     place_types();
     if (!htot[3]) {
@@ -2277,7 +2307,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   }
   out->n_names = NN;
   if (!types_done) {
-    run_types();
+    run_types(st);
     XSP_CUDA(cudaStreamSynchronize(st));
     place_types();
   }

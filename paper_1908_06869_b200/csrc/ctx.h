@@ -189,8 +189,29 @@ struct xsp_ctx {
       throw CudaError("cudaStreamCreate failed");
     return work_stream;
   }
+  // side streams + events for fork/join inside one API call (xsp_analyze runs
+  // its a15 / a10 / a5 passes concurrently); ordered with the caller's stream
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  cudaStream_t side_stream(int i) {
+    if (!side[i] && cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking) != cudaSuccess)
+      throw CudaError("cudaStreamCreate failed");
+    return side[i];
+  }
+  static cudaEvent_t lazy_event(cudaEvent_t& e) {
+    if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      throw CudaError("cudaEventCreate failed");
+    return e;
+  }
+  cudaEvent_t fork_event() { return lazy_event(ev_fork); }
+  cudaEvent_t join_event(int i) { return lazy_event(ev_join[i]); }
   ~xsp_ctx() {
     stage_collect();
+    for (cudaStream_t& s : side)
+      if (s) cudaStreamDestroy(s);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    for (cudaEvent_t& e : ev_join)
+      if (e) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (work_stream) cudaStreamDestroy(work_stream);
     if (out_stream) cudaStreamDestroy(out_stream);

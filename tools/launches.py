@@ -22,7 +22,7 @@ def main(path, skip_ids=0):
         a = agg.setdefault(k, [0, 0.0, 0.0])
         a[0] += 1
         t = d.get("gpu__time_duration.sum", 0.0)
-        a[1] += t / 1e3 if t > 1e4 else t  # ns -> us heuristically
+        a[1] += t / 1e3  # ns -> us
         a[2] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
     tot = sum(a[1] for a in agg.values())
     print(f"{'kernel':40s} {'n':>4s} {'us':>10s} {'share':>6s} {'MB':>9s} {'GB/s':>7s}")
