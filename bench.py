@@ -432,10 +432,8 @@ def main():
     stream = torch.cuda.current_stream().cuda_stream
 
     def step():
-        co = eng.correlate_device(dev, stream=stream)
-        n = eng.launches
-        eng.analyze_device(dev, co, groups, stream=stream)
-        return n + eng.launches
+        eng.run_device(dev, groups, stream=stream)
+        return eng.launches
 
     def barrier():
         if dist:

@@ -428,6 +428,15 @@ xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* host_cols,
                         const xsp_system_spec* spec, const xsp_analysis_opts* opts,
                         xsp_corr_out* corr_host, xsp_tables_out* tables_host, void* stream);
 
+/* correlate + analyze in one call on device-resident columns: xsp_correlate
+ * (mode 1) then xsp_analyze over its result, the reference's pipeline of
+ * correlate (correlator.cpp:366-370) followed by a8..a15 per analysis group
+ * (analysis.cpp:342-586). Outputs as for the two calls; one host round trip
+ * fewer between them. */
+xsp_status xsp_run(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
+                   const xsp_groups* groups, const xsp_system_spec* spec, const xsp_analysis_opts* opts,
+                   xsp_corr_out* corr, xsp_tables_out* tables, void* stream);
+
 /* validate_bundle (span.cpp:129-192) for every trace. Device pointers; the
  * result columns are ctx-owned device memory. Synchronous (one count read-back). */
 xsp_status xsp_validate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,

@@ -175,7 +175,7 @@ EV_IN_NARROW, EV_IN_WIDE, EV_CLAMPED, EV_NEGATIVE = 1, 2, 4, 8
 # exported symbols of libxsp.so, i.e. the functions include/xsp.h declares
 EXPORTS = [
     "xsp_abi_version", "xsp_ctx_create", "xsp_ctx_destroy", "xsp_last_error", "xsp_correlate",
-    "xsp_analyze", "xsp_run_host", "xsp_last_transfer_bytes", "xsp_last_launch_count",
+    "xsp_analyze", "xsp_run", "xsp_run_host", "xsp_last_transfer_bytes", "xsp_last_launch_count",
     "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host", "xsp_set_profiling", "xsp_stage_reset",
     "xsp_stage_times", "xsp_leveled", "xsp_sort_timeline_host", "xsp_correlate_host",
     "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline", "xsp_resolve_serialized",
@@ -214,6 +214,10 @@ def load() -> C.CDLL:
                                 C.POINTER(SystemSpec), C.POINTER(AnalysisOpts),
                                 C.POINTER(TablesOut), P]
     lib.xsp_analyze.restype = C.c_int32
+    lib.xsp_run.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(Groups),
+                            C.POINTER(SystemSpec), C.POINTER(AnalysisOpts),
+                            C.POINTER(CorrOut), C.POINTER(TablesOut), P]
+    lib.xsp_run.restype = C.c_int32
     lib.xsp_run_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(Groups),
                                  C.POINTER(SystemSpec), C.POINTER(AnalysisOpts),
                                  C.POINTER(CorrOut), C.POINTER(TablesOut), P]

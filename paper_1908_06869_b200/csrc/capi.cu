@@ -304,6 +304,22 @@ XSP_API xsp_status xsp_analyze(xsp_ctx* ctx, const xsp_span_cols* cols, const xs
   });
 }
 
+XSP_API xsp_status xsp_run(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
+                           const xsp_groups* groups, const xsp_system_spec* spec, const xsp_analysis_opts* opts,
+                           xsp_corr_out* corr, xsp_tables_out* tables, void* stream) {
+  return guard(ctx, "xsp_run", [&] {
+    check_cols(cols, traces);
+    if (!traces || !corr || !groups || !spec || !opts || !tables) throw std::invalid_argument("null argument");
+    if (groups->n_groups && (!groups->first_trace || !groups->n_runs || !groups->batch_size))
+      throw std::invalid_argument("null group column");
+    std::memset(corr, 0, sizeof(*corr));
+    std::memset(tables, 0, sizeof(*tables));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    xsp::run_correlate(ctx, cols, traces, 1, corr, st);
+    xsp::run_analyze(ctx, cols, corr, groups, spec, opts, tables, st);
+  });
+}
+
 XSP_API xsp_status xsp_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
                                const xsp_level_sets* sets, const xsp_analysis_opts* opts,
                                xsp_overhead_out* out, void* stream) {

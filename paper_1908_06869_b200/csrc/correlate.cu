@@ -1204,22 +1204,6 @@ __global__ void __launch_bounds__(P1_THREADS, P1_MINB) k_pass1(P1Args a, const _
   if constexpr (kDirect) dacc.finish(a);
 }
 
-// Direct mode: a trace is merge-aligned iff it has as many execs (with a cid)
-// as kernel-list entries and all of them share one (cid - position) value;
-// then launch r and exec r carry the same cid, the cids increase strictly and
-// none repeats — what the reference's hash join produces (correlator.cpp:287-364).
-// Since the positions are global, equal per-trace counts make launch r and
-// exec r of every trace share one position.
-__global__ void k_direct_check(uint32_t T, const uint32_t* __restrict__ t_kl_off,
-                               const uint32_t* __restrict__ t_ex_off, const unsigned long long* __restrict__ dmin,
-                               const unsigned long long* __restrict__ dmax, const uint32_t* __restrict__ totals,
-                               uint32_t* __restrict__ l_koff, uint32_t* __restrict__ fail) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t == 0) l_koff[totals[0]] = totals[1];
-  if (t >= T) return;
-  const uint32_t nk = t_kl_off[t + 1] - t_kl_off[t], nx = t_ex_off[t + 1] - t_ex_off[t];
-  if (nk != nx || (nk && dmin[t] != dmax[t])) *fail = 1;
-}
 // Offsets of traces that start at or after the end of the span table (empty
 // trailing traces) and the [T] sentinel.
 __global__ void k_pass1_tail(const uint64_t* __restrict__ off, uint32_t T, uint64_t n,
@@ -1240,6 +1224,92 @@ __global__ void k_pass1_tail(const uint64_t* __restrict__ off, uint32_t T, uint6
     totals[2] = tot.c_ex;
     totals[3] = tot.c_metric;
     totals[4] = tot.c_lay;
+  }
+}
+
+// Direct mode, everything after pass 1 in one launch: the trailing empty
+// traces' offsets and the totals (k_pass1_tail), the merge-alignment check
+// (a trace is merge-aligned iff it has as many
+// execs with a cid as kernel-list entries and all of them share one (cid -
+// position) value: then launch r and exec r carry the same cid, the cids
+// increase strictly and none repeats — what the reference's hash join
+// produces, correlator.cpp:287-364), the layer CSR sentinel, per-trace kernel offsets
+// (k_trace_kernel_off) and trace status (k_status without duplicate cids: a
+// merge-aligned batch has none). The values the host decides on — totals,
+// counters, per-trace layer / kernel offsets — are stored straight into pinned
+// host memory (device-addressable under UVA); the last block to finish copies
+// the counters once every block's flags are in.
+struct FinishArgs {
+  const uint64_t* off;
+  uint32_t T;
+  uint64_t n;
+  const Full* tile_prefix;
+  uint32_t ntiles;
+  uint32_t *t_layer_off, *t_kl_off, *t_ex_off;
+  uint32_t* totals;
+  const unsigned long long *dmin, *dmax;
+  uint32_t* l_koff;
+  uint32_t* t_koff;
+  const uint32_t* model_row;
+  const unsigned long long* err_key;
+  int32_t* status;
+  uint32_t* err_row;
+  uint32_t* counters;  // [0..7] as in run_correlate_once, [8] finished blocks
+  uint32_t* h_totals;  // pinned: [0..4] totals, [8..15] counters
+  uint32_t *h_loff, *h_koff;  // pinned: [T + 1] each
+};
+__global__ void k_direct_finish(FinishArgs a) {
+  const Full tot = a.ntiles ? a.tile_prefix[(a.ntiles + 31) / 32] : full_identity();
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t <= a.T) {
+    const bool tail = a.off[t] >= a.n;
+    const uint32_t lc = tail ? tot.c : a.t_layer_off[t];
+    const uint32_t kc = tail ? tot.c_kl : a.t_kl_off[t];
+    if (tail) {
+      a.t_layer_off[t] = tot.c;
+      a.t_kl_off[t] = tot.c_kl;
+      a.t_ex_off[t] = tot.c_ex;
+    }
+    const uint32_t koff = lc == tot.c ? tot.c_kl : a.l_koff[lc];
+    a.t_koff[t] = koff;
+    a.h_loff[t] = lc;
+    a.h_koff[t] = koff;
+    if (t < a.T) {
+      const bool ntail = a.off[t + 1] >= a.n;
+      const uint32_t kn = ntail ? tot.c_kl : a.t_kl_off[t + 1];
+      const uint32_t xc = tail ? tot.c_ex : a.t_ex_off[t];
+      const uint32_t xn = ntail ? tot.c_ex : a.t_ex_off[t + 1];
+      if (kn - kc != xn - xc || (kn != kc && a.dmin[t] != a.dmax[t])) atomicOr(a.counters + 7, 1u);
+      int32_t st = XSP_T_OK;
+      uint32_t ra = kNone;
+      if (a.model_row[t] == kNone) {
+        st = XSP_T_NO_MODEL;
+      } else if (a.err_key[t] != ~0ull) {
+        st = (int32_t)(a.err_key[t] & 0xFF);
+        ra = (uint32_t)(a.err_key[t] >> 8);
+      }
+      a.status[t] = st;
+      a.err_row[2 * t] = ra;
+      a.err_row[2 * t + 1] = kNone;
+      if (st != XSP_T_OK) atomicAdd(a.counters + 4, 1u);
+    }
+  }
+  if (t == 0) {
+    a.l_koff[tot.c] = tot.c_kl;
+    a.totals[0] = a.h_totals[0] = tot.c;
+    a.totals[1] = a.h_totals[1] = tot.c_kl;
+    a.totals[2] = a.h_totals[2] = tot.c_ex;
+    a.totals[3] = a.h_totals[3] = tot.c_metric;
+    a.totals[4] = a.h_totals[4] = tot.c_lay;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.counters + 8, 1u) == gridDim.x - 1) {
+      __threadfence();
+      for (int q = 0; q < 8; ++q) a.h_totals[8 + q] = __ldcg(a.counters + q);
+      __threadfence_system();
+    }
   }
 }
 
@@ -2087,8 +2157,8 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   // ---- pass 1
   // counters: [0] orphans [1] ambiguities [2] pending [3] nonmono [4] n_failed
   //           [5] unsorted [6] ambiguities after resolution [7] any slow trace
-  uint32_t* counters = ctx->d<uint32_t>("c.counters", 8);
-  XSP_CUDA(cudaMemsetAsync(counters, 0, 8 * 4, st));
+  uint32_t* counters = ctx->d<uint32_t>("c.counters", 16);
+  XSP_CUDA(cudaMemsetAsync(counters, 0, 16 * 4, st));
   P1Args a;
   a.span_id = c->span_id;
   a.flags = c->flags;
@@ -2209,22 +2279,52 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     ctx->launches += 4;
   }
   uint32_t* totals = ctx->d<uint32_t>("c.totals", 8);
-  k_pass1_tail<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(off, T, n, a.tile_prefix, ntiles, a.t_layer_off,
-                                                               a.t_kl_off, a.t_ex_off, totals);
-  ++ctx->launches;
   uint32_t* htot = ctx->h<uint32_t>("c.totals_h", 16);
+  if (direct) {
+    out->trace_kernel_off = ctx->d<uint32_t>("o.t_koff", T + 1);
+    out->trace_status = ctx->d<int32_t>("o.t_status", T);
+    out->trace_err_row = ctx->d<uint32_t>("o.t_err_row", 2ull * T);
+    FinishArgs fa;
+    fa.off = off;
+    fa.T = T;
+    fa.n = n;
+    fa.tile_prefix = a.tile_prefix;
+    fa.ntiles = ntiles;
+    fa.t_layer_off = a.t_layer_off;
+    fa.t_kl_off = a.t_kl_off;
+    fa.t_ex_off = a.t_ex_off;
+    fa.totals = totals;
+    fa.dmin = a.t_dmin;
+    fa.dmax = a.t_dmax;
+    fa.l_koff = out->layer_kernel_off;
+    fa.t_koff = out->trace_kernel_off;
+    fa.model_row = model_row;
+    fa.err_key = err_key;
+    fa.status = out->trace_status;
+    fa.err_row = out->trace_err_row;
+    fa.counters = counters;
+    fa.h_totals = htot;
+    ctx->hc_layer_key = ctx->hc_kernel_key = nullptr;
+    fa.h_loff = ctx->h<uint32_t>("c.hc_loff", T + 1);
+    fa.h_koff = ctx->h<uint32_t>("c.hc_koff", T + 1);
+    ctx->stage_begin("gather", st);
+    k_direct_finish<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(fa);
+    ctx->stage_end("gather", st);
+    ++ctx->launches;
+  } else {
+    k_pass1_tail<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(off, T, n, a.tile_prefix, ntiles, a.t_layer_off,
+                                                                 a.t_kl_off, a.t_ex_off, totals);
+    ++ctx->launches;
+  }
   // ---- optimistic clean path, launched before any host round trip: a batch
   // with no orphan, ambiguity or explicit-parent kernel whose traces are all
   // merge-aligned fuses launch r with exec r (k_gather_fast verifies it). Buffers
   // are sized by the span count; the device totals gate the kernels. ONE
   // read-back then decides: done, unsorted, or the general path below.
   auto* no_dup = ctx->d<unsigned long long>("c.no_dup", T);
-  if (try_clean) {
+  if (try_clean && !direct) {
     ctx->stage_begin("gather", st);
-    if (direct) {
-      k_direct_check<<<ceil_div((uint64_t)T + 1, 256), 256, 0, st>>>(T, a.t_kl_off, a.t_ex_off, a.t_dmin, a.t_dmax,
-                                                                      totals, out->layer_kernel_off, counters + 7);
-    } else {
+    {
       const unsigned gb = std::min<uint64_t>(ceil_div((uint64_t)n + 1, 256), 148u * 8u);
       k_gather_fast<<<gb, 256, 0, st>>>(totals, a.kl, a.ex, c->flags, a.t_kl_off, a.t_ex_off, T, c->cid,
                                         c->name_id, c->occupancy, out->kernel_launch_row,
@@ -2243,8 +2343,10 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     cache_offsets_begin(ctx, a.t_layer_off, out->trace_kernel_off, T, st);
     ctx->stage_end("gather", st);
   }
-  xfer_small(htot, totals, 5 * 4, st);
-  xfer_small(htot + 8, counters, 8 * 4, st);
+  if (!direct) {
+    xfer_small(htot, totals, 5 * 4, st);
+    xfer_small(htot + 8, counters, 8 * 4, st);
+  }
   XSP_CUDA(cudaStreamSynchronize(st));
   const uint32_t nl = htot[0], nkl = htot[1], nex = htot[2];
   const uint32_t n_amb_raw = htot[9], n_pend = htot[10];

@@ -233,6 +233,22 @@ class Engine:
                                          C.byref(spec), C.byref(opts), C.byref(to), C.c_void_p(stream)))
         return to
 
+    def run_device(self, dbatch: DeviceBatch, groups, trim=0.2, noise=0.01, top_k=3, stream=None):
+        """correlate + analyze of device-resident columns in one C-ABI call (xsp_run);
+        the argument structs are built once per (batch, groups) and reused."""
+        key = (id(dbatch), id(groups), trim, noise, top_k)
+        if getattr(self, "_run_key", None) != key:
+            g, keep = self.make_groups(*groups)
+            spec = capi.SystemSpec(dbatch.batch.peak_flops, dbatch.batch.mem_bw)
+            self._run_args = (dbatch.cols(), dbatch.traces(), g, spec, self.make_opts(trim=trim, noise=noise,
+                                                                                      top_k=top_k), keep, dbatch)
+            self._run_key = key
+        cols, trs, g, spec, opts, _, _ = self._run_args
+        co, to = capi.CorrOut(), capi.TablesOut()
+        self._check(self.lib.xsp_run(self.ctx, C.byref(cols), C.byref(trs), C.byref(g), C.byref(spec),
+                                     C.byref(opts), C.byref(co), C.byref(to), C.c_void_p(stream)))
+        return co, to
+
     def set_profiling(self, on: bool):
         self.lib.xsp_set_profiling(self.ctx, int(on))
 
