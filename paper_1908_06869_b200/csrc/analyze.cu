@@ -197,27 +197,30 @@ __global__ void k_group_check_runs(GroupArgs a, uint32_t total_runs, const uint3
   if (L != a.gl[g]) atomicMin(a.gerr + g, ((unsigned long long)(r + 1) << 32) | 0ull);
 }
 
+// One thread per (canonical layer, repetition r >= 1): grid.y = r - 1, so the
+// repetitions of a layer are checked in parallel instead of one dependent
+// load chain per layer. The least (run, layer) mismatch wins (atomicMin), as
+// the reference's loop order reports it (analysis.cpp:107-118).
 __global__ void k_group_check_layers(GroupArgs a, uint32_t total_layers, const uint32_t* __restrict__ gl_off) {
-  uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= total_layers) return;
   uint32_t lo = 0, hi = a.G;
   while (hi - lo > 1) {
     uint32_t mid = (lo + hi) >> 1;
     if (gl_off[mid] <= q) lo = mid; else hi = mid;
   }
-  uint32_t g = lo, li = q - gl_off[g];
-  uint32_t t0 = a.ft[g];
-  uint32_t gl0 = a.t_layer_off[t0] + li;
-  uint32_t k0 = a.l_koff[gl0 + 1] - a.l_koff[gl0];
-  for (uint32_t r = 1; r < a.nr[g]; ++r) {
-    uint32_t t = t0 + r;
-    if (a.t_status[t] != XSP_T_OK) continue;
-    uint32_t L = a.t_layer_off[t + 1] - a.t_layer_off[t];
-    if (L != a.gl[g]) continue;
-    uint32_t glr = a.t_layer_off[t] + li;
-    uint32_t kr = a.l_koff[glr + 1] - a.l_koff[glr];
-    if (kr != k0) atomicMin(a.gerr + g, ((unsigned long long)(r + 1) << 32) | (li + 1));
-  }
+  const uint32_t g = lo, li = q - gl_off[g];
+  const uint32_t r = blockIdx.y + 1;
+  if (r >= a.nr[g]) return;
+  const uint32_t t0 = a.ft[g], t = t0 + r;
+  if (a.t_status[t] != XSP_T_OK) return;
+  const uint32_t L = a.t_layer_off[t + 1] - a.t_layer_off[t];
+  if (L != a.gl[g]) return;
+  const uint32_t gl0 = a.t_layer_off[t0] + li;
+  const uint32_t k0 = a.l_koff[gl0 + 1] - a.l_koff[gl0];
+  const uint32_t glr = a.t_layer_off[t] + li;
+  const uint32_t kr = a.l_koff[glr + 1] - a.l_koff[glr];
+  if (kr != k0) atomicMin(a.gerr + g, ((unsigned long long)(r + 1) << 32) | (li + 1));
 }
 
 __global__ void k_group_status(uint32_t G, const uint32_t* __restrict__ nr,
@@ -1602,10 +1605,11 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   if (opts->top_k > 8) throw std::invalid_argument("top_k must be <= 8");
   // group descriptors are host arrays
   uint32_t* hg = ctx->h<uint32_t>("a.groups_h", 4ull * G + 4);
-  uint32_t total_runs = 0;
+  uint32_t total_runs = 0, max_runs = 0;
   bool all_one_run = G > 0;
   for (uint32_t g = 0; g < G; ++g) {
     all_one_run &= gr->n_runs[g] == 1;
+    max_runs = std::max(max_runs, gr->n_runs[g]);
     hg[g] = gr->first_trace[g];
     hg[G + g] = gr->n_runs[g];
     hg[2 * G + g] = gr->batch_size[g];
@@ -1789,7 +1793,11 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     ++ctx->launches;
   };
   launch(ctx, k_group_check_runs, total_runs, st, ga, total_runs, run_off);
-  launch(ctx, k_group_check_layers, TL, st, ga, TL, out->group_layer_off);
+  if (TL && max_runs > 1) {
+    k_group_check_layers<<<dim3(ceil_div((uint64_t)TL, 256), max_runs - 1), 256, 0, st>>>(ga, TL,
+                                                                                         out->group_layer_off);
+    ++ctx->launches;
+  }
   out->group_status = ctx->d<int32_t>("t.g_status", G);
   out->group_err_arg = ctx->d<uint32_t>("t.g_arg", G);
   launch(ctx, k_group_status, G, st, G, nr, ga.gerr, opts->trim_fraction, out->group_status,
