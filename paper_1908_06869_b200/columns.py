@@ -185,3 +185,26 @@ class SpanBatch:
             kw[k] = getattr(self, k)[t0:t1]
         return SpanBatch(**kw, names=self.names, types=self.types, system_name=self.system_name,
                          peak_flops=self.peak_flops, mem_bw=self.mem_bw)
+
+    def select_traces(self, idx: Sequence[int]) -> "SpanBatch":
+        """Traces idx (any order, repeats allowed) as a new batch (same string tables)."""
+        idx = np.asarray(idx, dtype=np.int64)
+        off = self.trace_span_off.astype(np.int64)
+        lay = (self.level() == capi.LEVEL_LAYER).astype(np.int64)
+        met = ((self.flags & capi.F_METRICS) != 0).astype(np.int64)
+        moff = np.concatenate([[0], np.cumsum(met)])[off]
+        loff = np.concatenate([[0], np.cumsum(lay)])[off]
+
+        def rows(o):
+            return np.concatenate([np.arange(o[t], o[t + 1]) for t in idx.tolist()]) if idx.size else \
+                np.zeros(0, np.int64)
+
+        sr, mr, lr = rows(off), rows(moff), rows(loff)
+        kw = {k: getattr(self, k)[sr] for k in SPAN_COLS}
+        kw.update({k: getattr(self, k)[mr] for k in METRIC_COLS})
+        kw.update({k: getattr(self, k)[lr] for k in LAYER_COLS})
+        kw["trace_span_off"] = np.concatenate([[0], np.cumsum(off[idx + 1] - off[idx])]).astype(np.uint64)
+        for k in ("trace_id", "trace_levels", "trace_batch", "trace_run", "trace_serialized"):
+            kw[k] = getattr(self, k)[idx]
+        return SpanBatch(**kw, names=self.names, types=self.types, system_name=self.system_name,
+                         peak_flops=self.peak_flops, mem_bw=self.mem_bw)
