@@ -95,33 +95,40 @@ class ClockSampler:
 
 
 def pass1_bytes(b) -> int:
-    """Algorithmic bytes of one k_pass1 launch: reads every span's
-    flags (1 B), begin and end (16 B), its placed-layer bit (k_p1_reduce, 1/8 B)
-    and the cid of spans that carry one (8 B); writes 16 B per placed layer
-    (row, duration, attribute row), a 16 B entry per kernel launch / synchronous
-    kernel (+4 B metric row for the latter), a 16 B entry per execution record
-    with a cid, and 12 B of offsets per trace."""
+    """Algorithmic bytes of one k_pass1 launch in direct mode (k_pass1<true>, the
+    clean-batch path the bench runs): reads every span's flags
+    (1 B), begin and end (16 B), its placed-layer bit (1/8 B, from k_p1_reduce)
+    and the cid of spans that carry one (8 B), plus the name_id (4 B) and the
+    occupancy (8 B, by metric row) of every execution record with a cid; writes
+    the kernel table row of every kernel (launch row, exec row, metric row,
+    name: 4 B each; duration, occupancy: 8 B each = 32 B), 20 B per placed layer
+    (row, duration, layer-table row, first-kernel offset) and 12 B of offsets
+    per trace."""
     f = b.flags
     lvl, kind = f & 3, (f >> 2) & 3
     n = b.n_spans
     has_c = int(((f & 0x20) != 0).sum())
     layer = int(((lvl == 1) & (kind == 0)).sum())
-    launch = int(((kind == 1) & (lvl >= 2)).sum())
-    synck = int(((kind == 0) & (lvl == 2)).sum())
     exe = int(((kind == 2) & ((f & 0x20) != 0)).sum())
-    reads = n * 17 + n // 8 + has_c * 8
-    writes = layer * 16 + (launch + synck) * 16 + synck * 4 + exe * 16 + b.n_traces * 12
+    reads = n * 17 + n // 8 + has_c * 8 + exe * (4 + 8)
+    writes = layer * 20 + exe * 32 + b.n_traces * 12
     return reads + writes
 
 
-def measured_traffic(kernel: str):
+def measured_traffic(kernel: str, spans: int = 0):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed
-    ncu --set full capture summary (profiles/traffic.json), per launch, or None."""
+    ncu --set full capture summary (profiles/traffic.json, tools/traffic_from_ncu.py),
+    scaled per span to a launch over `spans` spans (the captured launch's own
+    count if 0), or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)[kernel]
-        return {"bytes": d["dram_bytes"], "capture": d["capture"], "workload": d["workload"]}
+        n = spans or d["spans"]
+        return {"bytes": int(round(d["bytes_per_span"] * n)), "bytes_per_span": d["bytes_per_span"],
+                "captured_launch": {"spans": d["spans"], "dram_bytes": d["dram_bytes"],
+                                    "duration_us": d["duration_us"]},
+                "capture": d["capture"], "workload": d["workload"]}
     except Exception:
         return None
 
@@ -315,6 +322,60 @@ def measure_c4(eng, args, rank: int, world: int, local: int, dist):
     return out
 
 
+def measure_leveled(eng, args, local: int):
+    """BASELINE config 2 at scale (stage (f), leveled.cpp:145-231): 65 synthetic
+    models, each profiled at {M}, {M,L}, {M,L,G} x 10 repetitions (synth.
+    leveled_corpus, simprof's leveled-chain shape with per-level profiling
+    overhead); one step = correlate every run (one call) + compute_overhead of
+    each model's LeveledRunGroup (65 xsp_leveled calls, synchronous: the chain
+    order is decided on the host). Device-resident, CUDA events."""
+    import torch
+    from paper_1908_06869_b200 import synth
+    from paper_1908_06869_b200.engine import DeviceBatch
+    models = synth.make_models(args.leveled_models, seed=3)
+    b, sets = synth.leveled_corpus(models, runs=args.leveled_runs)
+    dev = DeviceBatch(b, local)
+    ls = [eng.make_level_sets(s) for s in sets]
+    stream = torch.cuda.current_stream().cuda_stream
+    n_events = sum(1 + m.layer_ns.size + m.exec_ns.size for m in models)
+    runs_per_model = 3 * args.leveled_runs
+
+    def step():
+        co = eng.correlate_device(dev, stream=stream)
+        for s, _ in ls:
+            out = eng.leveled_device(dev, co, s, stream=stream)
+            assert out.status == 0 and out.n_sets == 3
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    steps = max(2, args.steps // 4)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    eng.set_profiling(True)
+    eng.stage_reset()
+    step()
+    torch.cuda.synchronize()
+    st = eng.stage_times()
+    eng.set_profiling(False)
+    lev_ms = sum(v[0] for k, v in st.items() if k.startswith("lev"))
+    byts = n_events * runs_per_model * 8 + n_events * 24
+    return {"metric": "M spans/s correlated + leveled (compute_overhead), device-resident",
+            "value": b.n_spans / (ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": ms, "spans": b.n_spans,
+            "models": len(models), "runs_per_level_set": args.leveled_runs, "events": n_events,
+            "workload": "C2 at scale: 65 synthetic models x level sets {M},{M,L},{M,L,G} x 10 runs, batch 1",
+            "stages_ms": {k: v[0] for k, v in st.items()},
+            "roofline": {"bound": "hbm", "kernels": "k_lev_*", "bytes": byts,
+                         "definition": "SURVEY 8(d): 8 B per (event, run) + 24 B per event",
+                         "achieved": byts / (lev_ms / 1e3) / 1e9 if lev_ms else None, "unit": "GB/s",
+                         "note": "65 tiny synchronous calls per step: launch/sync bound, not HBM bound"}}
+
+
 class _Replica:
     """DeviceBatch interface over slices of replicated device columns."""
 
@@ -445,6 +506,8 @@ def main():
     ap.add_argument("--no-sort", action="store_true", help="skip the shuffled sort_timeline measurement")
     ap.add_argument("--c5-copies", type=int, default=21, help="C3 copies of the C5 corpus (headline)")
     ap.add_argument("--e2e-steps", type=int, default=2, help="steps of the end-to-end (host buffer) C5 timing")
+    ap.add_argument("--leveled-models", type=int, default=65, help="0 skips the leveled (C2 at scale) line")
+    ap.add_argument("--leveled-runs", type=int, default=10)
     ap.add_argument("--c4-layers", type=int, default=28_600_000,
                     help="layers of the C4 long trace (~7 spans per layer; 0 skips the C4 measurement)")
     args = ap.parse_args()
@@ -565,6 +628,7 @@ def main():
     del dev
     torch.cuda.empty_cache()
     c4_line = measure_c4(eng, args, rank, world, local, dist) if args.c4_layers > 0 else None
+    lev_line = measure_leveled(eng, args, local) if args.leveled_models > 0 and rank == 0 else None
 
     if rank != 0:
         if dist:
@@ -574,8 +638,10 @@ def main():
     achieved = p1_bytes / (p1_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": "k_pass1 (parent join + direct kernel-table emit, 1 launch per call)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_kind": peak_kind, "traffic": (measured_traffic("k_pass1") or {}).get("bytes"),
-                "traffic_source": measured_traffic("k_pass1"), "bytes_per_launch": p1_bytes,
+                "peak_kind": peak_kind,
+                "traffic": (measured_traffic("k_pass1", c5.spans_mine // max(calls, 1)) or {}).get("bytes"),
+                "traffic_source": measured_traffic("k_pass1", c5.spans_mine // max(calls, 1)),
+                "bytes_per_launch": p1_bytes,
                 "ms_per_launch": p1_ms, "launches_per_step": calls}
     sv = survey_bytes(b) * args.c5_copies
     pipe_gbs = sv / (ms / 1e3) / 1e9
@@ -601,6 +667,8 @@ def main():
         line["sort_shuffled"] = sort_line
     if c4_line:
         line["c4"] = c4_line
+    if lev_line:
+        line["leveled"] = lev_line
     if world == 1 and not args.no_cpu_baseline:
         from oracle import ref
         if ref.available():

@@ -304,6 +304,7 @@ struct LayerArgs {
   uint8_t* l_flagged;
   uint8_t* l_in;
   uint32_t* l_topk;
+  double* l_occw;  // optional (one-run long groups): the layer's raw sum(occ * lat) for the model fold
 };
 
 __device__ __forceinline__ uint32_t group_of(const uint32_t* __restrict__ off, uint32_t G, uint32_t q) {
@@ -414,13 +415,21 @@ __global__ void __launch_bounds__(256, kOneRun ? 4 : 3) k_layers(LayerArgs a) {
   double top_lat[8];
   uint32_t ntop = 0;
   for (uint32_t x = kb; x < ke; ++x) {
-    const double klat = a.k_lat[x];
+    double klat, kocc;
+    uint64_t f, rd, wr;
+    {
+      klat = a.k_lat[x];
+      kocc = a.k_occ[x];
+      f = a.k_flops[x];
+      rd = a.k_read[x];
+      wr = a.k_write[x];
+    }
     a.k_layer[x] = li;
     acc_lat = __dadd_rn(acc_lat, klat);
-    acc_f += a.k_flops[x];
-    acc_r += a.k_read[x];
-    acc_w += a.k_write[x];
-    acc_occw = __dadd_rn(acc_occw, __dmul_rn(a.k_occ[x], klat));
+    acc_f += f;
+    acc_r += rd;
+    acc_w += wr;
+    acc_occw = __dadd_rn(acc_occw, __dmul_rn(kocc, klat));
     // top-k by latency desc, ordinal asc
     if (K) {
       uint32_t pos = ntop;
@@ -437,6 +446,7 @@ __global__ void __launch_bounds__(256, kOneRun ? 4 : 3) k_layers(LayerArgs a) {
       }
     }
   }
+  if (a.l_occw) a.l_occw[q] = acc_occw;
   const uint32_t lo_out = q;
   if (a.layer_attr_row && a.type_id && a.alloc_bytes) {
     const uint32_t ar = a.layer_attr_row[gl0];
@@ -489,6 +499,7 @@ struct ModelArgs {
   // long groups (> kBigGroup kernels or layers): chunk partials (k_big_chunks)
   const uint32_t* gkc_off;  // [G + 1] kernel chunks of each group (empty range: not chunked)
   const uint32_t* glc_off;  // [G + 1] layer chunks of each group
+  bool layer_sums;          // one-run groups: the layer chunks carry the kernel sums
   const double* pk_lat;     // per kernel chunk: sum of latencies
   const double* pk_occw;    // per kernel chunk: sum of occ * lat
   const uint64_t* pk_cnt;   // per kernel chunk: sums of flops, read, write
@@ -608,12 +619,15 @@ __global__ void __launch_bounds__(64) k_models(ModelArgs a) {
   const uint32_t k0 = a.gk_off[g], k1 = a.gk_off[g + 1];
   const bool big_k = a.gkc_off && a.gkc_off[g + 1] > a.gkc_off[g];
   const bool big_l = a.glc_off && a.glc_off[g + 1] > a.glc_off[g];
+  // kernel sums of a one-run long group come from its layer chunks (layer_sums)
+  const uint32_t kc0 = a.layer_sums ? a.glc_off[g] : (big_k ? a.gkc_off[g] : 0);
+  const uint32_t kc1 = a.layer_sums ? a.glc_off[g + 1] : (big_k ? a.gkc_off[g + 1] : 0);
   double lat = 0.0, occw = 0.0;
   if (warp == 1) {
     // u64 counters: any order is exact
     uint64_t f = 0, rd = 0, wr = 0;
     if (big_k) {
-      for (uint32_t c = a.gkc_off[g] + lane; c < a.gkc_off[g + 1]; c += 32) {
+      for (uint32_t c = kc0 + lane; c < kc1; c += 32) {
         f += a.pk_cnt[3 * c];
         rd += a.pk_cnt[3 * c + 1];
         wr += a.pk_cnt[3 * c + 2];
@@ -649,7 +663,7 @@ __global__ void __launch_bounds__(64) k_models(ModelArgs a) {
       // group's integer latencies are exact, so lat is the reference's double;
       // sum(occ * lat) is re-associated at chunk boundaries)
       if (lane == 0)
-        for (uint32_t c = a.gkc_off[g]; c < a.gkc_off[g + 1]; ++c) {
+        for (uint32_t c = kc0; c < kc1; ++c) {
           lat = __dadd_rn(lat, a.pk_lat[c]);
           occw = __dadd_rn(occw, a.pk_occw[c]);
         }
@@ -698,10 +712,17 @@ struct BigChunkArgs {
   double* p_lat;   // kernel chunks: sum lat; layer chunks: sum kern_lat
   double* p_occw;  // kernel chunks: sum occ * lat
   uint64_t* p_cnt; // kernel chunks: [3 c + 0..2] sums of flops, read, write
+  // one-run groups: layer chunks also fold the layers' kernel sums (occ * lat,
+  // flops, read, write) so the kernel chunks need not be read at all
+  const double* l_occw;
+  const uint64_t* l_flops;
+  const uint64_t* l_read;
+  const uint64_t* l_write;
+  uint32_t c0;     // first chunk of this launch
 };
 
 __global__ void k_big_chunks(BigChunkArgs a) {
-  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+  const uint32_t c = a.c0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31u;
   if (c >= a.n) return;
   const uint32_t b = a.desc[3 * c], e = a.desc[3 * c + 1], kind = a.desc[3 * c + 2];
   const double* v = kind == 0 ? a.k_lat : a.l_kern_lat;
@@ -709,16 +730,28 @@ __global__ void k_big_chunks(BigChunkArgs a) {
   uint64_t f = 0, r = 0, w = 0;
   // lane-strided partial sums and a fixed xor-butterfly: the chunk sums are
   // re-associated at chunk boundaries anyway (integer latencies stay exact)
+  if (kind == 0) {
 #pragma unroll 4
-  for (uint32_t x = b + lane; x < e; x += 32) {
-    const double l = v[x];
-    s = __dadd_rn(s, l);
-    if (kind == 0) {
+    for (uint32_t x = b + lane; x < e; x += 32) {
+      const double l = v[x];
+      s = __dadd_rn(s, l);
       f += a.k_flops[x];
       r += a.k_read[x];
       w += a.k_write[x];
       so = __dadd_rn(so, __dmul_rn(a.k_occ[x], l));
     }
+  } else if (a.l_occw) {
+#pragma unroll 4
+    for (uint32_t x = b + lane; x < e; x += 32) {
+      s = __dadd_rn(s, v[x]);
+      so = __dadd_rn(so, a.l_occw[x]);
+      f += a.l_flops[x];
+      r += a.l_read[x];
+      w += a.l_write[x];
+    }
+  } else {
+#pragma unroll 4
+    for (uint32_t x = b + lane; x < e; x += 32) s = __dadd_rn(s, v[x]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1867,7 +1900,9 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->l_roofline_in = la.l_in = ctx->d<uint8_t>("t.l_in", TL);
   out->l_topk = la.l_topk = ctx->d<uint32_t>("t.l_topk", (uint64_t)TL * (opts->top_k ? opts->top_k : 1));
   ctx->stage_begin("layers", st);
+  la.l_occw = nullptr;
   if (all_one_run) {
+    if (n_chunks) la.l_occw = ctx->d<double>("t.l_occw", TL);
     launch(ctx, k_kernels_r1, TK, st, la, TK);
     launch(ctx, k_layers<true>, TL, st, la);
   } else {
@@ -1913,6 +1948,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
   out->m_roofline_in = ma.m_in = ctx->d<uint8_t>("t.m_in", G);
   ma.gkc_off = d_gkc;
   ma.glc_off = d_glc;
+  ma.layer_sums = all_one_run && n_chunks;
   ma.pk_lat = ma.pk_occw = ma.pl_gpu = nullptr;
   ma.pk_cnt = nullptr;
   double *p_lat = nullptr, *p_occw = nullptr;
@@ -1931,7 +1967,13 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     bc.k_write = la.k_write;
     bc.p_cnt = ctx->d<uint64_t>("a.p_cnt", 3ull * n_chunks);
     ma.pk_cnt = bc.p_cnt;
-    launch(ctx, k_big_chunks, (uint64_t)n_chunks * 32, st, bc);
+    bc.l_occw = la.l_occw;
+    bc.l_flops = la.l_flops;
+    bc.l_read = la.l_read;
+    bc.l_write = la.l_write;
+    // one-run: only the layer chunks are folded (they carry the kernel sums)
+    bc.c0 = all_one_run ? nkc : 0;
+    launch(ctx, k_big_chunks, (uint64_t)(n_chunks - bc.c0) * 32, st, bc);
     ma.pk_lat = p_lat;
     ma.pk_occw = p_occw;
     ma.pl_gpu = p_lat;

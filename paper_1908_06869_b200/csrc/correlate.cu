@@ -816,16 +816,16 @@ __device__ __forceinline__ void minmax_atomic_warp(uint32_t t, uint64_t mn, uint
         mn = b0 < mn ? b0 : mn;
         mx = b1 > mx ? b1 : mx;
       }
-      if (lane_id() == 0) {
-        atomicMin(dmin + t0, (unsigned long long)mn);
-        atomicMax(dmax + t0, (unsigned long long)mx);
+      if (lane_id() == 0) {  // skip atomics that cannot change the value (one hot word per long trace)
+        if (mn < *((volatile unsigned long long*)(dmin + t0))) atomicMin(dmin + t0, (unsigned long long)mn);
+        if (mx > *((volatile unsigned long long*)(dmax + t0))) atomicMax(dmax + t0, (unsigned long long)mx);
       }
       return;
     }
   }
   if (t != kNone) {
-    atomicMin(dmin + t, (unsigned long long)mn);
-    atomicMax(dmax + t, (unsigned long long)mx);
+    if (mn < *((volatile unsigned long long*)(dmin + t))) atomicMin(dmin + t, (unsigned long long)mn);
+    if (mx > *((volatile unsigned long long*)(dmax + t))) atomicMax(dmax + t, (unsigned long long)mx);
   }
 }
 
@@ -1554,39 +1554,60 @@ __global__ void k_join_counts(const uint32_t* __restrict__ t_kl_off, const uint3
   if (mismatch) *any_slow = 1;
 }
 
-// t_nomono[t] = 1 when some kernel-list entry of t is not a cid launch or its cid
-// does not exceed the previous entry's (the direct-address join needs both).
+// t_slow[t] = 1 when some kernel-list entry of t is not a cid launch, its cid
+// does not exceed the previous entry's, or launch r and exec r disagree on the
+// cid (not merge-aligned); t_lmin / t_lmax = the launch cid range of every
+// trace (the direct-address join needs it). A warp covers 32 x JC_ITEMS
+// consecutive entries (lane-strided, coalesced) and keeps running min / max per
+// lane, so a long trace issues one atomic pair per warp, not per 32 entries.
+constexpr uint32_t JC_ITEMS = 8;
 __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const ExEnt* __restrict__ ex,
                              const uint64_t* __restrict__ cid,
                              const uint8_t* __restrict__ flags, const uint32_t* __restrict__ t_kl_off,
                              const uint32_t* __restrict__ t_ex_off, uint32_t T, uint32_t* __restrict__ t_slow,
                              uint32_t* __restrict__ any_slow, unsigned long long* __restrict__ t_lmin,
                              unsigned long long* __restrict__ t_lmax) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t first = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
-  if (first >= nkl) return;
-  const uint32_t t = warp_trace_of(t_kl_off, T, k < nkl ? k : nkl - 1, first);
+  const uint32_t lane = lane_id();
+  const uint64_t wbase64 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32ull * JC_ITEMS;
+  if (wbase64 >= nkl) return;
+  const uint32_t wbase = (uint32_t)wbase64;
+  uint32_t t0 = 0;
+  if (lane == 0) t0 = trace_of32(t_kl_off, T, wbase);
+  uint32_t t = __shfl_sync(0xffffffffu, t0, 0);
   uint32_t tl = kNone;
-  uint64_t c = 0;
-  if (k < nkl) {
+  uint64_t mn = ~0ull, mx = 0;
+#pragma unroll 1
+  for (uint32_t i = 0; i < JC_ITEMS; ++i) {
+    const uint32_t k = wbase + i * 32 + lane;
+    if (k >= nkl) break;
+    while (t + 1 < T && __ldg(t_kl_off + t + 1) <= k) ++t;
     const uint32_t r = k - t_kl_off[t];
     const KlEnt ent = kl[k];
     const uint8_t f = flags[ent.row];
     const bool launch = f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID);
     const bool mono = launch && (r == 0 || kl[k - 1].cid < ent.cid);
     if (launch) {
-      tl = t;
-      c = ent.cid;
+      if (tl != t) {
+        if (tl != kNone) {
+          atomicMin(t_lmin + tl, (unsigned long long)mn);
+          atomicMax(t_lmax + tl, (unsigned long long)mx);
+        }
+        tl = t;
+        mn = ~0ull;
+        mx = 0;
+      }
+      mn = ent.cid < mn ? ent.cid : mn;
+      mx = ent.cid > mx ? ent.cid : mx;
     }
-    const bool was_slow = t_slow[t] != 0;
     // only the first mismatch of a trace stores (a reordered long trace would
     // otherwise have every launch store to the same two words)
-    if (!was_slow && !(mono && cid[ex[t_ex_off[t] + r].row] == ent.cid)) {
+    if (!*((volatile uint32_t*)(t_slow + t)) && !(mono && cid[ex[t_ex_off[t] + r].row] == ent.cid)) {
       t_slow[t] = 1;
       *any_slow = 1;
     }
   }
-  minmax_atomic_warp(tl, c, c, t_lmin, t_lmax);  // the launch cid range of every trace
+  __syncwarp();
+  minmax_atomic_warp(tl, mn, mx, t_lmin, t_lmax);
 }
 
 // Direct-address join for slow traces whose launch cids span a dense range
@@ -2231,7 +2252,11 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     col_tmap(&maps.cid, c->cid, n);
     col_tmap(&maps.parent, c->parent_id, n);
   }
-  const bool try_clean = !parents_only;
+  // hints from the previous call on this ctx: a clean batch goes straight to the
+  // direct kernel-table emit; after a batch with exceptions or reordered
+  // executions the optimistic clean gather is skipped (a wrong hint costs time,
+  // never correctness: both paths verify)
+  const bool try_clean = !parents_only && !ctx->unclean_hint;
   const bool direct = try_clean && ctx->direct_hint;
   if (try_clean) {
     out->kernel_launch_row = ctx->d<uint32_t>("o.k_launch", n);
@@ -2362,7 +2387,10 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     throw std::runtime_error("UNSORTED");
   }
   const bool clean = try_clean && htot[8] == 0 && n_pend == 0 && n_amb_raw == 0 && htot[15] == 0;
-  if (try_clean) ctx->direct_hint = clean;
+  if (try_clean) {
+    ctx->direct_hint = clean;
+    ctx->unclean_hint = !clean && (htot[8] || n_pend || n_amb_raw || htot[15]);
+  }
   if (clean) {
     cache_offsets_end(ctx, a.t_layer_off, out->trace_kernel_off, T);
     out->n_traces = T;
@@ -2504,8 +2532,8 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     XSP_CUDA(cudaMemsetAsync(t_lmin, 0xFF, (T + 1) * 8ull, st));
     XSP_CUDA(cudaMemsetAsync(t_lmax, 0, (T + 1) * 8ull, st));
     launch(ctx, k_join_counts, T, st, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
-    launch(ctx, k_join_check, nkl, st, nkl, a.kl, a.ex, c->cid, c->flags, a.t_kl_off, a.t_ex_off, T, t_slow,
-           counters + 7, reinterpret_cast<unsigned long long*>(t_lmin),
+    launch(ctx, k_join_check, ceil_div((uint64_t)nkl, JC_ITEMS), st, nkl, a.kl, a.ex, c->cid, c->flags,
+           a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7, reinterpret_cast<unsigned long long*>(t_lmin),
            reinterpret_cast<unsigned long long*>(t_lmax));
     any_slow = read_u32(ctx, counters + 7, st);
   }
@@ -2668,6 +2696,11 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   XSP_CUDA(cudaStreamSynchronize(st));
   out->n_failed = *hf;
   cache_offsets_end(ctx, out->trace_layer_off, out->trace_kernel_off, T);
+  if (!parents_only) {
+    const bool was_clean = no == 0 && n_pend == 0 && n_amb_raw == 0 && any_slow == 0;
+    ctx->unclean_hint = !was_clean;
+    ctx->direct_hint = was_clean;
+  }
 }
 
 }  // namespace xsp

@@ -102,6 +102,7 @@ struct xsp_ctx {
   // the previous call on this context was a clean batch (a guess: a wrong one
   // costs a second pass 1, never a different result)
   bool direct_hint = true;
+  bool unclean_hint = false;
 
   const void* hc_layer_key = nullptr;
   const void* hc_kernel_key = nullptr;

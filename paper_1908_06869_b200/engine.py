@@ -249,6 +249,32 @@ class Engine:
                                      C.byref(opts), C.byref(co), C.byref(to), C.c_void_p(stream)))
         return co, to
 
+    @staticmethod
+    def make_level_sets(sets):
+        """xsp_level_sets of [(level mask, trace indices)] (one LeveledRunGroup);
+        returns (struct, arrays to keep alive)."""
+        off = np.zeros(len(sets) + 1, dtype=np.uint32)
+        tr = []
+        for i, (_, idx) in enumerate(sets):
+            tr.extend(idx)
+            off[i + 1] = len(tr)
+        tr = np.array(tr, dtype=np.uint32)
+        lv = np.array([m for m, _ in sets], dtype=np.uint32)
+        ls = capi.LevelSets(len(sets), off.ctypes.data_as(capi.u32p), tr.ctypes.data_as(capi.u32p),
+                            lv.ctypes.data_as(capi.u32p))
+        return ls, (off, tr, lv)
+
+    def leveled_device(self, dbatch: DeviceBatch, corr: capi.CorrOut, level_sets, trim=0.2, noise=0.01,
+                       stream=None) -> capi.OverheadOut:
+        """compute_overhead (leveled.cpp:145-231) of one LeveledRunGroup over a
+        device correlation (xsp_leveled); level_sets from make_level_sets."""
+        cols = dbatch.cols()
+        out = capi.OverheadOut()
+        opts = self.make_opts(trim=trim, noise=noise)
+        self._check(self.lib.xsp_leveled(self.ctx, C.byref(cols), C.byref(corr), C.byref(level_sets),
+                                         C.byref(opts), C.byref(out), C.c_void_p(stream)))
+        return out
+
     def set_profiling(self, on: bool):
         self.lib.xsp_set_profiling(self.ctx, int(on))
 

@@ -390,3 +390,53 @@ def _timeline_order(cols):
     for k in ("alloc_bytes", "type_id"):
         out[k] = cols[k][lo]
     return out
+
+
+def _keep_levels(b: SpanBatch, mask: int) -> SpanBatch:
+    """The spans of b whose level is in `mask` (timeline order kept), with their
+    metric / layer-table rows; every trace's level set becomes `mask`."""
+    lvl = b.flags & 3
+    keep = ((1 << lvl.astype(np.int64)) & mask) != 0
+    met = (b.flags & capi.F_METRICS) != 0
+    lay = lvl == capi.LEVEL_LAYER
+    off = b.trace_span_off.astype(np.int64)
+    cnt = np.add.reduceat(keep.astype(np.int64), off[:-1]) if b.n_traces else np.zeros(0, np.int64)
+    cnt[np.diff(off) == 0] = 0
+    kw = {k: getattr(b, k)[keep] for k in ("span_id", "parent_id", "begin_ns", "end_ns", "cid", "flags",
+                                            "name_id")}
+    mk = keep[met]
+    lk = keep[lay]
+    kw.update({k: getattr(b, k)[mk] for k in ("flops", "dram_read", "dram_write", "occupancy")})
+    kw.update({k: getattr(b, k)[lk] for k in ("alloc_bytes", "type_id")})
+    return SpanBatch(**kw, trace_span_off=np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint64),
+                     trace_id=b.trace_id, trace_levels=np.full(b.n_traces, mask), trace_batch=b.trace_batch,
+                     trace_run=b.trace_run, trace_serialized=b.trace_serialized, names=b.names, types=b.types,
+                     system_name=b.system_name, peak_flops=b.peak_flops, mem_bw=b.mem_bw)
+
+
+def leveled_corpus(models: Sequence[Model], runs: int = 10, layer_oh_ns: int = 20_000,
+                   kernel_oh_ns: int = 8_000, seed: int = 11):
+    """BASELINE config 2 at scale: every model profiled at the level sets {M},
+    {M,L}, {M,L,G} (simprof emit_leveled_chain shape, simprof.cpp:300-340),
+    `runs` repetitions each, batch 1. Profiling a level adds overhead to the
+    host time of the levels above it: +layer_oh per layer under {M,L}, and
+    +kernel_oh per kernel on top under {M,L,G}; a shallower run records only
+    its levels. Returns (batch, level_sets) with level_sets[m] = [(mask, trace
+    indices)] for model m (one LeveledRunGroup per model, leveled.cpp:56-84)."""
+    parts, sets = [], []
+    t0 = 0
+    full = (1 << capi.LEVEL_MODEL) | (1 << capi.LEVEL_LAYER) | (1 << capi.LEVEL_KERNEL)
+    for mi, m in enumerate(models):
+        msets = []
+        for mask, loh, koh in ((1 << capi.LEVEL_MODEL, 0, 0),
+                               ((1 << capi.LEVEL_MODEL) | (1 << capi.LEVEL_LAYER), layer_oh_ns, 0),
+                               (full, layer_oh_ns, kernel_oh_ns)):
+            mm = Model(**{**m.__dict__, "layer_ns": m.layer_ns + loh + koh * m.kcount})
+            b, _, _, _ = corpus([mm], [1], runs, seed=seed + 97 * mi + mask)
+            b = _keep_levels(b, mask) if mask != full else b
+            b.trace_id = np.full(b.n_traces, 1_000 + mi, np.uint64)  # one workload per model
+            parts.append(b)
+            msets.append((mask, list(range(t0, t0 + b.n_traces))))
+            t0 += b.n_traces
+        sets.append(msets)
+    return SpanBatch.concat(parts), sets

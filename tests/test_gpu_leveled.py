@@ -112,3 +112,25 @@ def test_faults(engine, has_ref):
     b = ref.Generator().emit("minimal", 1, M).emit("minimal", 2, ML).batch()
     with pytest.raises(LeveledError, match="runs mix batch sizes 1 and 2"):
         compute_overhead(engine, b)
+
+
+def test_synthetic_leveled_corpus_per_model(engine, has_ref):
+    """The bench's leveled workload (synth.leveled_corpus: C2 at scale): each
+    model's {M}, {M,L}, {M,L,G} x R runs, one LeveledRunGroup per model, against
+    the reference; and the device path the bench times (one correlation of the
+    whole corpus, one xsp_leveled per model) agrees with the per-model report."""
+    from paper_1908_06869_b200 import synth
+    from paper_1908_06869_b200.engine import DeviceBatch
+    models = synth.make_models(4, seed=3, max_layers=400)
+    b, sets = synth.leveled_corpus(models, runs=5)
+    dev = DeviceBatch(b)
+    co = engine.correlate_device(dev)
+    for s in sets:
+        idx = [t for _, tr in s for t in tr]
+        sub = b.select_traces(idx)
+        rep = compute_overhead(engine, sub)
+        compare(rep, ref.leveled(sub))
+        assert rep.model_overhead_by_added_levels  # the injected per-level overhead is visible
+        ls, keep = engine.make_level_sets(s)
+        out = engine.leveled_device(dev, co, ls)
+        assert out.status == 0 and out.n_sets == 3 and out.n_events == len(rep.rows)

@@ -84,3 +84,19 @@ def test_grouped_batch_on_gpu(engine, has_ref):
     groups.check_unambiguous(corr, sel)
     aa, ast = ref.analyze(sel, g[0], g[1])
     compare_tables(sel, tabs, aa, ast)
+
+
+def test_leveled_corpus_is_a_valid_chain():
+    """synth.leveled_corpus: per model three level sets whose runs the reference
+    accepts as one LeveledRunGroup, with the injected overhead recovered."""
+    from oracle import ref
+    from paper_1908_06869_b200 import synth
+    models = synth.make_models(2, seed=3, max_layers=200)
+    b, sets = synth.leveled_corpus(models, runs=3)
+    for s in sets:
+        assert [m for m, _ in s] == [0b001, 0b011, 0b111]
+        sub = b.select_traces([t for _, tr in s for t in tr])
+        arrays, strings = ref.leveled(sub)
+        assert int(arrays["status"][0]) == 0, strings["error"]
+        ov = dict(zip(arrays["model_ov_mask"].tolist(), arrays["model_ov_val"].tolist()))
+        assert ov[0b010] > 0 and ov[0b100] > 0
