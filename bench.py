@@ -605,6 +605,13 @@ def main():
     c3_line["roofline"]["frac"] = c3_line["roofline"]["achieved"] / peak
     sort_line = measure_sort(eng, dev, b, args.steps, local) if not args.no_sort else None
 
+    if args.c5_copies <= 0:  # quick iteration: the C3 line alone
+        if rank == 0:
+            print(json.dumps({"c3": c3_line, "sort_shuffled": sort_line}))
+        if dist:
+            dist.destroy_process_group()
+        return
+
     # ---------------- C5 headline: ~1 B spans, device-resident
     c5 = C5(eng, dev, b, groups, copies=args.c5_copies, rank=rank, world=world)
     c5.step(stream, check=True)
