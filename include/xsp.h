@@ -445,6 +445,36 @@ xsp_status xsp_validate(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_trace
 xsp_status xsp_validate_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_traces* traces,
                              const xsp_validate_in* in, xsp_validation_out* out);
 
+/* ---- report emission --------------------------------------
+ * A string table: n strings, string i = bytes[off[i], off[i+1]) (HOST arrays,
+ * off has n + 1 entries). names = the batch's name table (name_id order),
+ * types = its layer-type table (type_id order). */
+typedef struct xsp_string_table {
+  uint32_t n;
+  const char* bytes;
+  const uint64_t* off;
+} xsp_string_table;
+
+/* The reference report's CSV file of one analysis table of one group
+ * (report.cpp:42-147 to_csv over the :166-330 to_table converters), written on
+ * the GPU from the device tables of the preceding xsp_analyze / xsp_run on this
+ * ctx (which stay valid): table = 8 (a8 kernel info), 9 (a9 kernel roofline),
+ * 10 (a10 by name), 11 (a11 by layer), 12 (a12 metrics per layer), 13 (a13 GPU
+ * vs non-GPU), 14 (a14 layer roofline). cols / corr / groups are the arguments
+ * of that analysis (device columns; corr is read for a11's layer types).
+ * *text is ctx-owned device memory (xsp_report_csv) or ctx-owned pinned host
+ * memory, NUL-terminated (xsp_report_csv_host), valid until the next report
+ * call; *len excludes the NUL. Doubles are printed like std::to_chars (shortest
+ * round trip), integers like std::to_string, cells CSV-quoted as csv_quote. */
+xsp_status xsp_report_csv(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                          const xsp_groups* groups, const xsp_tables_out* tables,
+                          const xsp_string_table* names, const xsp_string_table* types, uint32_t group,
+                          int table, char** text, uint64_t* len, void* stream);
+xsp_status xsp_report_csv_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                               const xsp_groups* groups, const xsp_tables_out* tables,
+                               const xsp_string_table* names, const xsp_string_table* types, uint32_t group,
+                               int table, char** text, uint64_t* len, void* stream);
+
 /* Bytes moved host->device and device->host by the last xsp_run_host call. */
 void xsp_last_transfer_bytes(const xsp_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 

@@ -214,6 +214,23 @@ def analyze(b, first: Sequence[int], runs: Sequence[int], trim=0.2, noise=0.01):
     return read_bag(lib().xspref_analyze(C.byref(s), f.ctypes.data, r.ctypes.data, f.size, trim, noise))
 
 
+def report_csv(b, first: int, runs: int, table: int, trim=0.2, noise=0.01) -> bytes:
+    """The reference report's CSV (to_csv(to_table(aN(...)))) of analysis table N of
+    the group of traces [first, first + runs)."""
+    L = lib()
+    L.xspref_report_csv.restype = C.c_void_p
+    L.xspref_report_csv.argtypes = [C.POINTER(SoaIn), C.c_uint32, C.c_uint32, C.c_int, C.c_double, C.c_double]
+    L.xspref_free_text.argtypes = [C.c_void_p]
+    s, keep = soa_in(b)
+    p = L.xspref_report_csv(C.byref(s), first, runs, table, trim, noise)
+    if not p:
+        raise RuntimeError(L.xspref_last_error().decode())
+    try:
+        return C.string_at(p)
+    finally:
+        L.xspref_free_text(p)
+
+
 def resolve(original, serialized):
     """resolve_with_serialized per trace pair, as correlate() returns it."""
     s1, k1 = soa_in(original)

@@ -32,6 +32,7 @@
 #include "strata/collector.hpp"
 #include "strata/correlator.hpp"
 #include "strata/leveled.hpp"
+#include "strata/report.hpp"
 #include "strata/simprof.hpp"
 #include "strata/span.hpp"
 #include "test_support.hpp"  // reference tests/test_support.hpp (generators)
@@ -869,3 +870,40 @@ XSPREF_API void* xspref_leveled(const SoaIn* in, double trim, double noise) {
 XSPREF_API double xspref_trimmed_mean(const double* v, std::uint64_t n, double f) {
   return trimmed_mean(std::vector<double>(v, v + n), f);
 }
+
+// The reference report's CSV of one analysis table (a8..a14) of analysis group g
+// (report.cpp to_csv(to_table(...))). Returns malloc'd NUL-terminated text (free
+// with xspref_free_text), or nullptr with xspref_last_error set.
+XSPREF_API char* xspref_report_csv(const SoaIn* in, std::uint32_t first, std::uint32_t runs, int table,
+                                   double trim, double noise) {
+  try {
+    std::vector<TraceBundle> bundles = import_soa(*in);
+    SystemSpec spec{in->system_name, in->peak_flops, in->mem_bw};
+    AnalysisOptions opts;
+    opts.trim_fraction = trim;
+    opts.noise_tolerance = noise;
+    AnalysisInput input;
+    input.batch_size = bundles[first].meta.batch_size;
+    for (std::uint32_t r = 0; r < runs; ++r) input.runs.push_back(correlate(bundles[first + r]).tree);
+    Table t;
+    switch (table) {
+      case 8: t = to_table(a8_kernel_table(input, spec, opts)); break;
+      case 9: t = to_table(a9_kernel_roofline(input, spec, opts), "a9"); break;
+      case 10: t = to_table(a10_by_name(input, spec, opts)); break;
+      case 11: t = to_table(a11_by_layer(input, spec, opts)); break;
+      case 12: t = to_table(a12_metrics_per_layer(input, opts)); break;
+      case 13: t = to_table(a13_gpu_vs_nongpu(input, opts)); break;
+      case 14: t = to_table(a14_layer_roofline(input, spec, opts), "a14"); break;
+      default: throw std::invalid_argument("table");
+    }
+    const std::string csv = to_csv(t);
+    char* out = static_cast<char*>(std::malloc(csv.size() + 1));
+    std::memcpy(out, csv.data(), csv.size() + 1);
+    return out;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+XSPREF_API void xspref_free_text(char* p) { std::free(p); }

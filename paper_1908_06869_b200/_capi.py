@@ -169,6 +169,14 @@ VALIDATION_RULES = [
 ]
 TAG_NEG_FLOPS, TAG_NEG_READ, TAG_NEG_WRITE, TAG_OCC_DOUBLE = 1, 2, 4, 8
 
+
+class StringTable(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("bytes", C.c_char_p), ("off", u64p)]
+
+
+# report tables (xsp_report_csv): a8..a14
+REPORT_TABLES = {"a8": 8, "a9": 9, "a10": 10, "a11": 11, "a12": 12, "a13": 13, "a14": 14}
+
 L_OK, L_TOO_FEW, L_NOT_CHAIN, L_AMBIGUOUS, L_TRACE_FAILED = range(5)
 EV_IN_NARROW, EV_IN_WIDE, EV_CLAMPED, EV_NEGATIVE = 1, 2, 4, 8
 
@@ -179,7 +187,7 @@ EXPORTS = [
     "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host", "xsp_set_profiling", "xsp_stage_reset",
     "xsp_stage_times", "xsp_leveled", "xsp_sort_timeline_host", "xsp_correlate_host",
     "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline", "xsp_resolve_serialized",
-    "xsp_resolve_serialized_host",
+    "xsp_resolve_serialized_host", "xsp_report_csv", "xsp_report_csv_host",
 ]
 
 _lib = None
@@ -253,5 +261,10 @@ def load() -> C.CDLL:
     lib.xsp_validate_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(ValidateIn),
                                       C.POINTER(ValidationOut)]
     lib.xsp_validate_host.restype = C.c_int32
+    for fn in (lib.xsp_report_csv, lib.xsp_report_csv_host):
+        fn.argtypes = [P, C.POINTER(SpanCols), C.POINTER(CorrOut), C.POINTER(Groups), C.POINTER(TablesOut),
+                       C.POINTER(StringTable), C.POINTER(StringTable), C.c_uint32, C.c_int,
+                       C.POINTER(C.c_char_p), u64p, P]
+        fn.restype = C.c_int32
     _lib = lib
     return lib

@@ -18,6 +18,9 @@ void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const ui
                        uint32_t T, const uint64_t* off, uint32_t* perm, uint32_t* was_sorted, cudaStream_t st);
 void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, const xsp_validate_in* vin,
                   xsp_validation_out* out, cudaStream_t st);
+void run_report_csv(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr, const xsp_groups* groups,
+                    const xsp_tables_out* t, const xsp_string_table* names, const xsp_string_table* types,
+                    uint32_t group, int table, char** text, uint64_t* len, int to_host, cudaStream_t st);
 void run_resolve(xsp_ctx* ctx, const xsp_span_cols* oc, const xsp_traces* ot, const xsp_span_cols* sc,
                  const xsp_traces* stt, xsp_corr_out* out, cudaStream_t st);
 }
@@ -469,6 +472,28 @@ XSP_API xsp_status xsp_analyze_host(xsp_ctx* ctx, const xsp_span_cols* hc, const
     xsp::run_analyze(ctx, &dc, &dcorr, groups, spec, opts, &dtab, st);
     download_tables(ctx, dtab, opts, out, st);
     XSP_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+XSP_API xsp_status xsp_report_csv(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                                  const xsp_groups* groups, const xsp_tables_out* tables,
+                                  const xsp_string_table* names, const xsp_string_table* types, uint32_t group,
+                                  int table, char** text, uint64_t* len, void* stream) {
+  return guard(ctx, "xsp_report_csv", [&] {
+    if (!cols || !corr || !groups || !tables || !names || !text || !len) throw std::invalid_argument("null argument");
+    xsp::run_report_csv(ctx, cols, corr, groups, tables, names, types, group, table, text, len, 0,
+                        static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_report_csv_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                                       const xsp_groups* groups, const xsp_tables_out* tables,
+                                       const xsp_string_table* names, const xsp_string_table* types,
+                                       uint32_t group, int table, char** text, uint64_t* len, void* stream) {
+  return guard(ctx, "xsp_report_csv_host", [&] {
+    if (!cols || !corr || !groups || !tables || !names || !text || !len) throw std::invalid_argument("null argument");
+    xsp::run_report_csv(ctx, cols, corr, groups, tables, names, types, group, table, text, len, 1,
+                        static_cast<cudaStream_t>(stream));
   });
 }
 

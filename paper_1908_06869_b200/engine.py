@@ -250,6 +250,33 @@ class Engine:
         return co, to
 
     @staticmethod
+    def string_table(strings):
+        """xsp_string_table of a list of byte strings; returns (struct, arrays to keep alive)."""
+        blob = b"".join(strings)
+        off = np.zeros(len(strings) + 1, dtype=np.uint64)
+        if strings:
+            off[1:] = np.cumsum([len(x) for x in strings])
+        st = capi.StringTable(len(strings), blob, off.ctypes.data_as(capi.u64p))
+        return st, (blob, off)
+
+    def report_csv(self, dbatch: DeviceBatch, corr: capi.CorrOut, groups, tables: capi.TablesOut, group: int,
+                   table: str, stream=None) -> bytes:
+        """The reference report's CSV file (report.cpp to_csv(to_table(...))) of one
+        analysis table of one group, formatted on the GPU (xsp_report_csv_host) from
+        the tables of the preceding analyze_device / run_device on this engine."""
+        g, keep = self.make_groups(*groups)
+        names, k1 = self.string_table(dbatch.batch.names)
+        types, k2 = self.string_table(dbatch.batch.types)
+        cols = dbatch.cols()
+        text = C.c_char_p()
+        n = C.c_uint64()
+        self._check(self.lib.xsp_report_csv_host(self.ctx, C.byref(cols), C.byref(corr), C.byref(g),
+                                                 C.byref(tables), C.byref(names), C.byref(types), group,
+                                                 capi.REPORT_TABLES[table], C.byref(text), C.byref(n),
+                                                 C.c_void_p(stream)))
+        return C.string_at(C.cast(text, C.c_void_p).value, n.value)
+
+    @staticmethod
     def make_level_sets(sets):
         """xsp_level_sets of [(level mask, trace indices)] (one LeveledRunGroup);
         returns (struct, arrays to keep alive)."""
