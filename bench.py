@@ -279,9 +279,11 @@ def measure_c4(eng, args, rank: int, world: int, local: int, dist):
     groups = ([0], [1], [1])
     stream = torch.cuda.current_stream().cuda_stream
 
+    last = {}
+
     def step():
         co = eng.correlate_device(dev, stream=stream)
-        eng.analyze_device(dev, co, groups, stream=stream)
+        last["co"], last["to"] = co, eng.analyze_device(dev, co, groups, stream=stream)
 
     for _ in range(2):
         step()
@@ -295,6 +297,30 @@ def measure_c4(eng, args, rank: int, world: int, local: int, dist):
     t1.record()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / max(1, args.steps // 2)
+    # report emission: the a8 CSV (one row per kernel) of the
+    # trace, formatted on the GPU from the device tables (text left in HBM)
+    report = None
+    if rank == 0:
+        names, k1 = eng.string_table(sub.names)
+        types, k2 = eng.string_table(sub.types)
+        g, k3 = eng.make_groups(*groups)
+        cols = dev.cols()
+        import ctypes as C
+        text, n = C.c_char_p(), C.c_uint64()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for rep in range(2):
+            r0.record()
+            eng._check(eng.lib.xsp_report_csv(eng.ctx, C.byref(cols), C.byref(last["co"]), C.byref(g),
+                                              C.byref(last["to"]), C.byref(names), C.byref(types), 0, 8,
+                                              C.byref(text), C.byref(n), C.c_void_p(stream)))
+            r1.record()
+            torch.cuda.synchronize()
+        rms = r0.elapsed_time(r1)
+        report = {"table": "a8 (one CSV row per kernel)", "rows": int(last["to"].n_kernels), "bytes": n.value,
+                  "ms": rms, "GB_per_s": n.value / (rms / 1e3) / 1e9,
+                  "M_rows_per_s": last["to"].n_kernels / (rms / 1e3) / 1e6,
+                  "how": "xsp_report_csv into HBM (size pass, scan, write pass; includes two small count "
+                         "read-backs), CUDA events"}
     del dev
     combine_ms = None
     if dist:
@@ -315,6 +341,8 @@ def measure_c4(eng, args, rank: int, world: int, local: int, dist):
            "layers": args.c4_layers, "shards": world, "scaling": "strong",
            "workload": "C4: synth.c4, 1 model span, layers x ~3 kernels (1% long layers of 8..64, 0.1% "
                        "concurrent pairs), executions on 4 interleaved streams, no drains (no quiescent instant)"}
+    if report:
+        out["report_a8_csv"] = report
     if combine_ms is not None:
         out["combine_ms"] = combine_ms
         out["value_incl_combine"] = b.n_spans / ((ms + combine_ms) / 1e3) / 1e6

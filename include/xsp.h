@@ -475,6 +475,28 @@ xsp_status xsp_report_csv_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xs
                                const xsp_string_table* names, const xsp_string_table* types, uint32_t group,
                                int table, char** text, uint64_t* len, void* stream);
 
+/* ---- multi-GPU table combine over NCCL -----------------
+ * xsp_comm_unique_id: rank 0 creates the 128-byte NCCL unique id, which the
+ * caller shares with the other ranks out of band (e.g. a torch.distributed
+ * broadcast). xsp_comm_init: every rank joins the communicator (world ranks,
+ * one ctx / GPU per rank). NCCL is loaded at run time (libnccl.so.2). */
+xsp_status xsp_comm_unique_id(void* id128);
+xsp_status xsp_comm_init(xsp_ctx* ctx, int world, int rank, const void* id128);
+
+/* Trace-sharded analysis: rank r analysed the groups group_ids[0..n_local)
+ * (HOST array of global group indices, in its local group order) with
+ * xsp_analyze on this ctx (`local` = those device tables). Every rank calls;
+ * the tables travel to rank 0 with NCCL send/recv (one contiguous block per
+ * column and rank) and rank 0 lays them out in global group order (0 ..
+ * n_groups_total - 1) — the tables of an unsharded run — in ctx-owned device
+ * memory (*out; zeroed on other ranks). l_row_map (device, optional): global
+ * span row of every local span row; the sender rewrites its l_row with it.
+ * top_k as given to xsp_analyze. *bytes_sent (optional): table bytes this rank
+ * sent. Synchronous. */
+xsp_status xsp_combine_tables(xsp_ctx* ctx, xsp_tables_out* local, const uint32_t* group_ids, uint32_t n_local,
+                              uint32_t n_groups_total, const uint32_t* l_row_map, uint32_t top_k,
+                              xsp_tables_out* out, uint64_t* bytes_sent, void* stream);
+
 /* Bytes moved host->device and device->host by the last xsp_run_host call. */
 void xsp_last_transfer_bytes(const xsp_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 

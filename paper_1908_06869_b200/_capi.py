@@ -187,7 +187,8 @@ EXPORTS = [
     "xsp_host_alloc", "xsp_host_free", "xsp_copy_to_host", "xsp_set_profiling", "xsp_stage_reset",
     "xsp_stage_times", "xsp_leveled", "xsp_sort_timeline_host", "xsp_correlate_host",
     "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline", "xsp_resolve_serialized",
-    "xsp_resolve_serialized_host", "xsp_report_csv", "xsp_report_csv_host",
+    "xsp_resolve_serialized_host", "xsp_report_csv", "xsp_report_csv_host", "xsp_comm_unique_id",
+    "xsp_comm_init", "xsp_combine_tables",
 ]
 
 _lib = None
@@ -266,5 +267,12 @@ def load() -> C.CDLL:
                        C.POINTER(StringTable), C.POINTER(StringTable), C.c_uint32, C.c_int,
                        C.POINTER(C.c_char_p), u64p, P]
         fn.restype = C.c_int32
+    lib.xsp_comm_unique_id.argtypes = [P]
+    lib.xsp_comm_unique_id.restype = C.c_int32
+    lib.xsp_comm_init.argtypes = [P, C.c_int, C.c_int, P]
+    lib.xsp_comm_init.restype = C.c_int32
+    lib.xsp_combine_tables.argtypes = [P, C.POINTER(TablesOut), u32p, C.c_uint32, C.c_uint32, P, C.c_uint32,
+                                       C.POINTER(TablesOut), u64p, P]
+    lib.xsp_combine_tables.restype = C.c_int32
     _lib = lib
     return lib

@@ -21,6 +21,11 @@ void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, co
 void run_report_csv(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr, const xsp_groups* groups,
                     const xsp_tables_out* t, const xsp_string_table* names, const xsp_string_table* types,
                     uint32_t group, int table, char** text, uint64_t* len, int to_host, cudaStream_t st);
+void comm_unique_id(void* id);
+void comm_init(xsp_ctx* ctx, int world, int rank, const void* id);
+void run_combine_tables(xsp_ctx* ctx, xsp_tables_out* local, const uint32_t* group_ids, uint32_t G_local,
+                        uint32_t G_total, const uint32_t* l_row_map, int top_k, xsp_tables_out* out,
+                        uint64_t* bytes_sent, cudaStream_t st);
 void run_resolve(xsp_ctx* ctx, const xsp_span_cols* oc, const xsp_traces* ot, const xsp_span_cols* sc,
                  const xsp_traces* stt, xsp_corr_out* out, cudaStream_t st);
 }
@@ -494,6 +499,34 @@ XSP_API xsp_status xsp_report_csv_host(xsp_ctx* ctx, const xsp_span_cols* cols, 
     if (!cols || !corr || !groups || !tables || !names || !text || !len) throw std::invalid_argument("null argument");
     xsp::run_report_csv(ctx, cols, corr, groups, tables, names, types, group, table, text, len, 1,
                         static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_comm_unique_id(void* id128) {
+  if (!id128) return XSP_E_INVALID;
+  try {
+    xsp::comm_unique_id(id128);
+    return XSP_OK;
+  } catch (...) {
+    return XSP_E_CUDA;
+  }
+}
+
+XSP_API xsp_status xsp_comm_init(xsp_ctx* ctx, int world, int rank, const void* id128) {
+  return guard(ctx, "xsp_comm_init", [&] {
+    if (!id128) throw std::invalid_argument("null argument");
+    xsp::comm_init(ctx, world, rank, id128);
+  });
+}
+
+XSP_API xsp_status xsp_combine_tables(xsp_ctx* ctx, xsp_tables_out* local, const uint32_t* group_ids,
+                                      uint32_t n_local, uint32_t n_groups_total, const uint32_t* l_row_map,
+                                      uint32_t top_k, xsp_tables_out* out, uint64_t* bytes_sent, void* stream) {
+  return guard(ctx, "xsp_combine_tables", [&] {
+    if (!local || !out || (n_local && !group_ids)) throw std::invalid_argument("null argument");
+    if (top_k > 8) throw std::invalid_argument("top_k must be <= 8");
+    xsp::run_combine_tables(ctx, local, group_ids, n_local, n_groups_total, l_row_map, (int)top_k, out,
+                            bytes_sent, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -25,6 +25,10 @@ struct CudaError : std::runtime_error {
 
 struct xsp_ctx {
   int device = 0;
+  // NCCL communicator of the multi-GPU table combine (xsp_comm_init)
+  void* nccl_comm = nullptr;
+  int comm_world = 0, comm_rank = 0;
+  void (*comm_destroy)(void*) = nullptr;
   std::string last_error;
   uint64_t launches = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
@@ -208,6 +212,7 @@ struct xsp_ctx {
   cudaEvent_t join_event(int i) { return lazy_event(ev_join[i]); }
   ~xsp_ctx() {
     stage_collect();
+    if (nccl_comm && comm_destroy) comm_destroy(nccl_comm);
     for (cudaStream_t& s : side)
       if (s) cudaStreamDestroy(s);
     if (ev_fork) cudaEventDestroy(ev_fork);

@@ -249,6 +249,42 @@ class Engine:
                                      C.byref(opts), C.byref(co), C.byref(to), C.c_void_p(stream)))
         return co, to
 
+    # ---- multi-GPU table combine (xsp_comm_init / xsp_combine_tables)
+    def comm_init(self, world: int, rank: int, dist=None):
+        """Join an NCCL communicator of `world` ranks; rank 0's unique id travels
+        over torch.distributed (`dist`, any backend) when world > 1."""
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            st = self.lib.xsp_comm_unique_id(uid)
+            if st != capi.XSP_OK:
+                raise capi.XspError(st, "ncclGetUniqueId failed")
+        if world > 1:
+            obj = [bytes(uid) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            C.memmove(uid, obj[0], 128)
+        self._check(self.lib.xsp_comm_init(self.ctx, world, rank, uid))
+
+    def combine_tables(self, local: capi.TablesOut, group_ids, n_groups_total: int, l_row_map_ptr: int = 0,
+                       top_k: int = 3, stream=None) -> Tuple[capi.TablesOut, int]:
+        """xsp_combine_tables: every rank's device tables to rank 0 in global group
+        order over NCCL; returns (rank 0's device tables, bytes this rank sent)."""
+        gid = np.ascontiguousarray(group_ids, dtype=np.uint32)
+        out = capi.TablesOut()
+        sent = C.c_uint64(0)
+        self._check(self.lib.xsp_combine_tables(self.ctx, C.byref(local), gid.ctypes.data_as(capi.u32p), gid.size,
+                                                n_groups_total, C.c_void_p(l_row_map_ptr or None), top_k,
+                                                C.byref(out), C.byref(sent), C.c_void_p(stream)))
+        return out, sent.value
+
+    def tables_to_host(self, to: capi.TablesOut, top_k: int = 3) -> "Tables":
+        """Host copy of device tables (xsp_copy_to_host per column)."""
+        from .leveled import _d2h
+        tc = _tab_counts(to, top_k)
+        cols = {}
+        for name, typ, kind in capi.TABLE_FIELDS:
+            cols[name] = _d2h(self.lib, self.ctx, getattr(to, name), _NP[typ], tc[kind])
+        return Tables(to.n_groups, cols, to.n_layers, to.n_kernels, to.n_names)
+
     @staticmethod
     def string_table(strings):
         """xsp_string_table of a list of byte strings; returns (struct, arrays to keep alive)."""

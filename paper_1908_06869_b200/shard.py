@@ -121,25 +121,90 @@ def combine(parts: List[Tuple[Tables, np.ndarray]], n_groups: int, top_k: int) -
                   int(cols["group_name_off"][-1]))
 
 
+_NPT = {capi.u8p: np.uint8, capi.i8p: np.int8, capi.u32p: np.uint32, capi.i32p: np.int32,
+        capi.u64p: np.uint64, capi.i64p: np.int64, capi.f64p: np.float64}
+
+
+def pack_tables(tabs: Optional[Tables], gids: np.ndarray) -> np.ndarray:
+    """One rank's tables + global group ids as a flat byte array (column sizes
+    first, then the columns in include/xsp.h order; no pickling)."""
+    cols = [np.asarray(gids, np.int64)]
+    if tabs is not None:
+        cols += [np.asarray(tabs.cols[name]) for name, _, _ in capi.TABLE_FIELDS]
+    sizes = np.array([c.nbytes for c in cols], np.int64)
+    head = np.concatenate([[sizes.size], sizes]).astype(np.int64)
+    return np.concatenate([head.view(np.uint8)] + [np.ascontiguousarray(c).view(np.uint8).reshape(-1) for c in cols])
+
+
+def unpack_tables(buf: np.ndarray) -> Optional[Tuple[Tables, np.ndarray]]:
+    n = int(buf[:8].view(np.int64)[0])
+    sizes = buf[8:8 + 8 * n].view(np.int64)
+    off = 8 + 8 * n
+    chunks = []
+    for sz in sizes.tolist():
+        chunks.append(buf[off:off + sz])
+        off += sz
+    gids = chunks[0].view(np.int64)
+    if n == 1:
+        return None
+    cols = {name: chunks[1 + i].view(_NPT[t]) for i, (name, t, _) in enumerate(capi.TABLE_FIELDS)}
+    G = int(cols["group_status"].size)
+    return Tables(G, cols), gids
+
+
 def run_sharded(batch: SpanBatch, groups: Groups, compute: Callable[[SpanBatch, Groups], Tables],
-                rank: int, world: int, top_k: int = 3, dist=None) -> Optional[Tables]:
+                rank: int, world: int, top_k: int = 3, dist=None, comm=None) -> Optional[Tables]:
     """Correlate + analyse this rank's share and gather the tables on rank 0
-    (returns them there, None elsewhere). `dist` is torch.distributed (already
-    initialised; gloo or nccl) or None for world == 1."""
+    (returns them there, None elsewhere). The tables travel as one byte tensor
+    per rank over `comm` (timeshard.TorchComm over torch.distributed — gloo in
+    the CPU tests; run_sharded_device uses the NCCL C-ABI combine on GPUs) or,
+    given only `dist`, a TorchComm on CPU tensors. world == 1 needs neither."""
     n_groups = len(groups[0])
     ranks = assign_groups(group_spans(batch, groups), world)
     sub, lgroups, gids, span_base = shard(batch, groups, ranks, rank)
-    part = None
+    tabs = None
     if sub is not None:
         tabs = compute(sub, lgroups)
         tabs.cols["l_row"] = _local_to_global_rows(tabs.cols["l_row"], sub, span_base)
-        part = (tabs.n_groups, tabs.cols, gids)
     if world == 1:
-        gathered = [part]
+        gathered = [pack_tables(tabs, gids)]
     else:
-        gathered = [None] * world if rank == 0 else None
-        dist.gather_object(part, gathered, dst=0)
+        if comm is None:
+            from .timeshard import TorchComm
+            comm = TorchComm(dist, "cpu")
+        gathered = comm.gather_bytes(pack_tables(tabs, gids))
     if rank != 0:
         return None
-    parts = [(Tables(p[0], p[1]), p[2]) for p in gathered if p is not None]
+    parts = [p for p in (unpack_tables(b) for b in gathered) if p is not None]
     return combine(parts, n_groups, top_k)
+
+
+def l_row_map(sub: SpanBatch, span_base: np.ndarray) -> np.ndarray:
+    """Global span row of every span row of a rank's sub-batch."""
+    off = sub.trace_span_off.astype(np.int64)
+    out = np.empty(sub.n_spans, np.uint32)
+    for t in range(sub.n_traces):
+        out[off[t]:off[t + 1]] = span_base[t] + np.arange(off[t + 1] - off[t])
+    return out
+
+
+def run_sharded_device(engine, batch: SpanBatch, groups: Groups, rank: int, world: int, dist=None,
+                       top_k: int = 3, stream=None):
+    """The GPU form: rank r correlates + analyses its groups device-resident
+    (xsp_run) and the device tables are combined on rank 0 with NCCL
+    (xsp_combine_tables; the engine must have joined the communicator with
+    Engine.comm_init). Returns (rank 0's host Tables or None, bytes sent)."""
+    import torch
+    from .engine import DeviceBatch
+    n_groups = len(groups[0])
+    ranks = assign_groups(group_spans(batch, groups), world)
+    sub, lgroups, gids, span_base = shard(batch, groups, ranks, rank)
+    if sub is None:  # no groups on this rank: an empty batch still takes part in the combine
+        raise ValueError("run_sharded_device: every rank needs at least one group")
+    dev = DeviceBatch(sub, torch.cuda.current_device())
+    _, to = engine.run_device(dev, lgroups, top_k=top_k, stream=stream)
+    rmap = torch.from_numpy(l_row_map(sub, span_base).view(np.int32)).to(f"cuda:{torch.cuda.current_device()}")
+    out, sent = engine.combine_tables(to, gids, n_groups, rmap.data_ptr(), top_k=top_k, stream=stream)
+    if rank != 0:
+        return None, sent
+    return engine.tables_to_host(out, top_k), sent

@@ -111,3 +111,41 @@ def test_gpu_sharded_compute_matches_oracle(engine):
         t.cols["l_row"] = shard._local_to_global_rows(t.cols["l_row"], sub, base)
         parts.append((t, gids))
     _tables_equal(shard.combine(parts, len(gf), 3), whole)
+
+
+@pytest.mark.gpu
+def test_gpu_nccl_combine_reorders_groups(engine):
+    """xsp_combine_tables over a world-1 NCCL communicator: the rank holds the
+    groups in a permuted order (its sub-batch lists their traces in that order);
+    the combine lays them out in global group order with l_row rebased to the
+    original batch — the unsharded device tables bit for bit."""
+    import torch
+    from paper_1908_06869_b200.engine import DeviceBatch
+    b, gf, gr, gb = synth.c3(runs=3, n_models=5, max_layers=120)
+    groups = (gf, gr, gb)
+    whole_c, whole_t = engine.run_host(b, groups=groups)
+    G = len(gf)
+    perm = np.random.default_rng(1).permutation(G)
+    ranks = np.zeros(G, np.int64)
+    parts, lfirst, bases, t = [], [], [], 0
+    for g in perm:
+        t0, t1 = int(gf[g]), int(gf[g] + gr[g])
+        parts.append(b.trace_slice(t0, t1))
+        bases.append(b.trace_span_off[t0:t1].astype(np.int64))
+        lfirst.append(t)
+        t += t1 - t0
+    from paper_1908_06869_b200.columns import SpanBatch
+    sub = SpanBatch.concat(parts)
+    lgroups = (np.array(lfirst), np.asarray(gr)[perm], np.asarray(gb)[perm])
+    engine.comm_init(1, 0)
+    dev = DeviceBatch(sub)
+    _, to = engine.run_device(dev, lgroups)
+    rmap = torch.from_numpy(shard.l_row_map(sub, np.concatenate(bases)).view(np.int32)).cuda()
+    out, sent = engine.combine_tables(to, perm, G, rmap.data_ptr())
+    torch.cuda.synchronize()
+    got = engine.tables_to_host(out)
+    assert sent == 0  # rank 0 keeps its own tables
+    for k in whole_t.cols:
+        x, y = np.asarray(got.cols[k]), np.asarray(whole_t.cols[k])
+        assert x.shape == y.shape and np.array_equal(x.view(np.uint8), y.view(np.uint8)), k
+    del ranks
