@@ -475,6 +475,40 @@ xsp_status xsp_report_csv_host(xsp_ctx* ctx, const xsp_span_cols* cols, const xs
                                const xsp_string_table* names, const xsp_string_table* types, uint32_t group,
                                int table, char** text, uint64_t* len, void* stream);
 
+/* ---- JSONL ingest -------------------------------------------
+ * ingest() (collector.cpp:219-266) of n_streams JSONL streams on the GPU: stream
+ * i = text[stream_off[i], stream_off[i+1]) (HOST text) is one TraceBundle,
+ * trace i of the result. Span columns (device, ctx-owned, each trace in
+ * timeline order: sort_timeline applied) carry the same values the C++
+ * drop-in's packing of the ingested bundles gives, names / layer types interned
+ * in lexicographic order over all streams. XSP_INGEST_HOST: stream bad_stream
+ * holds something the device path does not cover exactly (string escapes or
+ * non-ASCII bytes, a non-canonical record layout, a number outside the exact
+ * cases, a missing / repeated meta record, a trace_id mismatch or a validation
+ * issue): the caller parses with the host ingest, which returns the result or
+ * the reference's IngestError text. Host pointers in *out stay valid until the
+ * next xsp_ingest_jsonl call on the same thread. */
+#define XSP_INGEST_OK 0
+#define XSP_INGEST_HOST 1
+typedef struct xsp_ingest_out {
+  int32_t status;
+  uint32_t bad_stream;
+  xsp_span_cols cols;        /* device */
+  xsp_traces traces;         /* device span_off / levels */
+  const uint64_t* span_off_host;
+  const uint32_t* levels_host;
+  const uint64_t* trace_id;  /* host, per stream (RunMeta) */
+  const uint32_t* trace_batch;
+  const uint32_t* trace_run;
+  const uint8_t* trace_serialized;
+  xsp_string_table names;    /* host */
+  xsp_string_table types;    /* host */
+  const char* system_name;   /* stream 0's system spec */
+  double peak_flops, mem_bw;
+} xsp_ingest_out;
+xsp_status xsp_ingest_jsonl(xsp_ctx* ctx, const char* text, const uint64_t* stream_off, uint32_t n_streams,
+                            xsp_ingest_out* out, void* stream);
+
 /* ---- multi-GPU table combine over NCCL -----------------
  * xsp_comm_unique_id: rank 0 creates the 128-byte NCCL unique id, which the
  * caller shares with the other ranks out of band (e.g. a torch.distributed

@@ -214,6 +214,35 @@ def analyze(b, first: Sequence[int], runs: Sequence[int], trim=0.2, noise=0.01):
     return read_bag(lib().xspref_analyze(C.byref(s), f.ctypes.data, r.ctypes.data, f.size, trim, noise))
 
 
+def list_jsonl(gen: "Generator", i: int) -> bytes:
+    """to_jsonl of bundle i of a generator's list (the reference's wire form)."""
+    L = lib()
+    L.xspref_list_jsonl.restype = C.c_void_p
+    L.xspref_list_jsonl.argtypes = [C.c_void_p, C.c_uint64]
+    L.xspref_free_text.argtypes = [C.c_void_p]
+    p = L.xspref_list_jsonl(gen.h, i)
+    try:
+        return C.string_at(p)
+    finally:
+        L.xspref_free_text(p)
+
+
+def ingest(streams):
+    """The reference's ingest() of each JSONL stream -> SpanBatch (one trace per
+    stream); raises RuntimeError(IngestError text) on failure."""
+    from paper_1908_06869_b200.columns import SpanBatch
+    L = lib()
+    L.xspref_ingest.restype = C.c_void_p
+    L.xspref_ingest.argtypes = [C.c_char_p, C.c_void_p, C.c_uint32]
+    blob = b"".join(streams)
+    off = np.concatenate([[0], np.cumsum([len(x) for x in streams])]).astype(np.uint64)
+    h = L.xspref_ingest(blob, off.ctypes.data, len(streams))
+    if not h:
+        raise RuntimeError(L.xspref_last_error().decode())
+    arrays, strings = read_bag(h)
+    return SpanBatch.from_bag(arrays, strings)
+
+
 def report_csv(b, first: int, runs: int, table: int, trim=0.2, noise=0.01) -> bytes:
     """The reference report's CSV (to_csv(to_table(aN(...)))) of analysis table N of
     the group of traces [first, first + runs)."""

@@ -907,3 +907,28 @@ XSPREF_API char* xspref_report_csv(const SoaIn* in, std::uint32_t first, std::ui
 }
 
 XSPREF_API void xspref_free_text(char* p) { std::free(p); }
+
+// The reference's JSONL wire form (collector.cpp to_jsonl) of bundle i of a list.
+XSPREF_API char* xspref_list_jsonl(void* list, std::uint64_t i) {
+  const auto& b = static_cast<BundleList*>(list)->bundles;
+  const std::string t = to_jsonl(b.at(i));
+  char* out = static_cast<char*>(std::malloc(t.size() + 1));
+  std::memcpy(out, t.data(), t.size() + 1);
+  return out;
+}
+
+// The reference's ingest() (collector.cpp:219-266) of each NUL-separated JSONL
+// stream, exported as SoA columns like xspref_list_export; nullptr with
+// xspref_last_error = the IngestError text on failure.
+XSPREF_API void* xspref_ingest(const char* text, const std::uint64_t* off, std::uint32_t n) {
+  try {
+    std::vector<TraceBundle> bundles;
+    for (std::uint32_t i = 0; i < n; ++i) bundles.push_back(ingest_string(std::string(text + off[i], text + off[i + 1])));
+    auto* bag = new Bag;
+    export_soa(bundles, *bag);
+    return bag;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}

@@ -174,6 +174,20 @@ class StringTable(C.Structure):
     _fields_ = [("n", C.c_uint32), ("bytes", C.c_char_p), ("off", u64p)]
 
 
+class StringTableOut(C.Structure):  # xsp_string_table as returned by the library
+    _fields_ = [("n", C.c_uint32), ("bytes", C.c_void_p), ("off", u64p)]
+
+
+class IngestOut(C.Structure):
+    _fields_ = [("status", C.c_int32), ("bad_stream", C.c_uint32), ("cols", SpanCols), ("traces", Traces),
+                ("span_off_host", u64p), ("levels_host", u32p), ("trace_id", u64p), ("trace_batch", u32p),
+                ("trace_run", u32p), ("trace_serialized", u8p), ("names", StringTableOut),
+                ("types", StringTableOut), ("system_name", C.c_char_p), ("peak_flops", C.c_double),
+                ("mem_bw", C.c_double)]
+
+
+INGEST_OK, INGEST_HOST = 0, 1
+
 # report tables (xsp_report_csv): a8..a14
 REPORT_TABLES = {"a8": 8, "a9": 9, "a10": 10, "a11": 11, "a12": 12, "a13": 13, "a14": 14}
 
@@ -188,7 +202,7 @@ EXPORTS = [
     "xsp_stage_times", "xsp_leveled", "xsp_sort_timeline_host", "xsp_correlate_host",
     "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline", "xsp_resolve_serialized",
     "xsp_resolve_serialized_host", "xsp_report_csv", "xsp_report_csv_host", "xsp_comm_unique_id",
-    "xsp_comm_init", "xsp_combine_tables",
+    "xsp_comm_init", "xsp_combine_tables", "xsp_ingest_jsonl",
 ]
 
 _lib = None
@@ -267,6 +281,8 @@ def load() -> C.CDLL:
                        C.POINTER(StringTable), C.POINTER(StringTable), C.c_uint32, C.c_int,
                        C.POINTER(C.c_char_p), u64p, P]
         fn.restype = C.c_int32
+    lib.xsp_ingest_jsonl.argtypes = [P, C.c_char_p, u64p, C.c_uint32, C.POINTER(IngestOut), P]
+    lib.xsp_ingest_jsonl.restype = C.c_int32
     lib.xsp_comm_unique_id.argtypes = [P]
     lib.xsp_comm_unique_id.restype = C.c_int32
     lib.xsp_comm_init.argtypes = [P, C.c_int, C.c_int, P]

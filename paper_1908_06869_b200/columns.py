@@ -208,3 +208,52 @@ class SpanBatch:
             kw[k] = getattr(self, k)[idx]
         return SpanBatch(**kw, names=self.names, types=self.types, system_name=self.system_name,
                          peak_flops=self.peak_flops, mem_bw=self.mem_bw)
+
+
+_LEVEL_NAMES = ["model", "layer", "kernel", "api"]
+_KIND_NAMES = ["sync", "launch", "exec"]
+
+
+def to_jsonl(b: SpanBatch, t: int) -> bytes:
+    """Trace t of b in the reference's JSONL wire form (encode_meta_record /
+    encode_span_record: keys in order, no whitespace; collector.cpp:188-194):
+    the metric table row of a span becomes its four metric tags, the layer table
+    row its alloc_bytes / layer_type tags. Doubles are written as Python's
+    shortest round-trip repr (the reference's writer may pick other digits of
+    the same double). Used to build ingest workloads and tests."""
+    import json
+    lv = int(b.trace_levels[t])
+    s0, s1 = int(b.trace_span_off[t]), int(b.trace_span_off[t + 1])
+    met = (b.flags & capi.F_METRICS) != 0
+    lay = (b.flags & 3) == capi.LEVEL_LAYER
+    mrow = np.cumsum(met) - met
+    arow = np.cumsum(lay) - lay
+    dq = lambda x: json.dumps(x)
+    num = lambda x: repr(float(x)) if float(x) != int(float(x)) or abs(float(x)) >= 1e16 else repr(float(x))
+    sysname = b.system_name.decode() if isinstance(b.system_name, bytes) else b.system_name
+    out = [("{\"batch_size\":%d,\"levels\":[%s],\"rec\":\"meta\",\"run_index\":%d,\"serialized\":%s,"
+            "\"system\":{\"mem_bw\":%s,\"name\":%s,\"peak_flops\":%s},\"trace_id\":%d}")
+           % (int(b.trace_batch[t]), ",".join(dq(_LEVEL_NAMES[i]) for i in range(4) if lv >> i & 1),
+              int(b.trace_run[t]), "true" if int(b.trace_serialized[t]) else "false", num(b.mem_bw), dq(sysname),
+              num(b.peak_flops), int(b.trace_id[t]))]
+    tid = int(b.trace_id[t])
+    names = [n.decode() for n in b.names]
+    types = [n.decode() for n in b.types]
+    for i in range(s0, s1):
+        f = int(b.flags[i])
+        tags = []
+        if f & capi.F_METRICS:
+            m = int(mrow[i])
+            tags = ["\"achieved_occupancy\":" + repr(float(b.occupancy[m])),
+                    "\"dram_read_bytes\":%d" % int(b.dram_read[m]), "\"dram_write_bytes\":%d" % int(b.dram_write[m]),
+                    "\"flop_count_sp\":%d" % int(b.flops[m])]
+        if (f & 3) == capi.LEVEL_LAYER:
+            a = int(arow[i])
+            tags = ["\"alloc_bytes\":%d" % int(b.alloc_bytes[a]), "\"layer_type\":" + dq(types[int(b.type_id[a])])]
+        out.append("{\"begin_ns\":%d,\"correlation_id\":%s,\"end_ns\":%d,\"kind\":\"%s\",\"level\":\"%s\","
+                   "\"name\":%s,\"parent_id\":%s,\"rec\":\"span\",\"span_id\":%d,\"tags\":{%s},\"trace_id\":%d}"
+                   % (int(b.begin_ns[i]), str(int(b.cid[i])) if f & capi.F_CID else "null", int(b.end_ns[i]),
+                      _KIND_NAMES[(f >> 2) & 3], _LEVEL_NAMES[f & 3], dq(names[int(b.name_id[i])]),
+                      str(int(b.parent_id[i])) if f & capi.F_PARENT else "null", int(b.span_id[i]),
+                      ",".join(tags), tid))
+    return ("\n".join(out) + "\n").encode()

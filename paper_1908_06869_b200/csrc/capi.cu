@@ -21,6 +21,8 @@ void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, co
 void run_report_csv(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr, const xsp_groups* groups,
                     const xsp_tables_out* t, const xsp_string_table* names, const xsp_string_table* types,
                     uint32_t group, int table, char** text, uint64_t* len, int to_host, cudaStream_t st);
+void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uint32_t S, xsp_ingest_out* out,
+                      cudaStream_t st);
 void comm_unique_id(void* id);
 void comm_init(xsp_ctx* ctx, int world, int rank, const void* id);
 void run_combine_tables(xsp_ctx* ctx, xsp_tables_out* local, const uint32_t* group_ids, uint32_t G_local,
@@ -499,6 +501,14 @@ XSP_API xsp_status xsp_report_csv_host(xsp_ctx* ctx, const xsp_span_cols* cols, 
     if (!cols || !corr || !groups || !tables || !names || !text || !len) throw std::invalid_argument("null argument");
     xsp::run_report_csv(ctx, cols, corr, groups, tables, names, types, group, table, text, len, 1,
                         static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_ingest_jsonl(xsp_ctx* ctx, const char* text, const uint64_t* stream_off,
+                                    uint32_t n_streams, xsp_ingest_out* out, void* stream) {
+  return guard(ctx, "xsp_ingest_jsonl", [&] {
+    if (!out || !stream_off || (n_streams && !text)) throw std::invalid_argument("null argument");
+    xsp::run_ingest_jsonl(ctx, text, stream_off, n_streams, out, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -1,0 +1,1091 @@
+// JSONL wire-format ingest on the GPU: the reference's
+// ingest() (collector.cpp:219-266) of many JSONL streams — one TraceBundle each
+// — straight into the SoA span columns the correlate/analyze path reads.
+//
+//   1. H2D of the text; newline positions (a per-chunk count, a scan, a write);
+//   2. one thread per line parses a span record in the reference writer's
+//      canonical layout (encode_span_record: keys in order, no whitespace):
+//      exact u64 fields, kind / level names, the name and layer_type strings as
+//      byte ranges, the metric tags (integers exact; decimal doubles by the
+//      exact Clinger fast path: <= 2^53 significand, |exp10| <= 22, one
+//      correctly rounded multiply / divide), and the raw-tag facts validation
+//      needs; it also hashes the name (FNV-1a 64);
+//   3. names and layer types are interned in lexicographic order: the hashes
+//      are radix-sorted, every span is checked byte for byte against its run's
+//      representative (a hash collision sends the batch to the host), the few
+//      distinct strings are ordered on the host and their ranks scattered back;
+//   4. sort_timeline (stage (b)) and validate_bundle (stage (a)) on the device.
+//
+// Meta records are parsed on the host (one short line per stream, canonical
+// layout). Anything the fast path does not cover exactly — escapes or non-ASCII
+// bytes in strings, other layouts or whitespace, numbers outside the exact
+// cases, unknown record kinds, a missing or repeated meta record, a trace_id
+// mismatch, validation issues — is reported as XSP_INGEST_HOST with the first
+// such stream: the caller runs the reference-exact host parser (the C++
+// drop-in's strata::ingest) for the error text or the result.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "ctx.h"
+#include "prims.cuh"
+#include "xsp_common.cuh"
+
+namespace xsp {
+
+void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const uint8_t* flags, const uint64_t* sid,
+                       uint32_t T, const uint64_t* off, uint32_t* perm, uint32_t* was_sorted, cudaStream_t st);
+void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, const xsp_validate_in* vin,
+                  xsp_validation_out* out, cudaStream_t st);
+
+namespace {
+
+constexpr uint32_t LK_BLANK = 0, LK_SPAN = 1, LK_META = 2, LK_HOST = 3;
+
+struct LineOut {
+  uint8_t* kind;       // LK_*
+  uint64_t* span_id;
+  uint64_t* parent;
+  uint64_t* begin;
+  uint64_t* end;
+  uint64_t* cid;
+  uint64_t* trace_id;
+  uint8_t* flags;
+  uint64_t* name_hash;
+  uint64_t* name_off;  // byte range of the name in the text
+  uint32_t* name_len;
+  uint64_t* type_hash;
+  uint64_t* type_off;
+  uint32_t* type_len;  // layer_type string (layers; "" when absent)
+  uint64_t* flops;
+  uint64_t* dread;
+  uint64_t* dwrite;
+  double* occ;
+  int64_t* alloc;
+  uint8_t* tag_bits;
+};
+
+__device__ __forceinline__ uint64_t fnv_step(uint64_t h, uint8_t c) { return (h ^ c) * 0x100000001b3ull; }
+constexpr uint64_t kFnv0 = 0xcbf29ce484222325ull;
+
+struct Cur {
+  const char* p;
+  const char* e;
+  __device__ bool lit(const char* s) {
+    const char* q = p;
+    for (; *s; ++s, ++q)
+      if (q >= e || *q != *s) return false;
+    p = q;
+    return true;
+  }
+  __device__ bool u64(uint64_t& v) {
+    if (p >= e || *p < '0' || *p > '9') return false;
+    if (*p == '0') {
+      ++p;
+      v = 0;
+      return p >= e || *p < '0' || *p > '9';
+    }
+    uint64_t x = 0;
+    while (p < e && *p >= '0' && *p <= '9') {
+      const uint64_t d = (uint64_t)(*p - '0');
+      if (x > (~0ull - d) / 10) return false;  // beyond u64: a double in JSON terms
+      x = x * 10 + d;
+      ++p;
+    }
+    v = x;
+    return true;
+  }
+  __device__ bool u64_or_null(uint64_t& v, bool& has) {
+    if (lit("null")) {
+      has = false;
+      v = 0;
+      return true;
+    }
+    has = true;
+    return u64(v);
+  }
+  // a plain string (no escapes, printable ASCII): its byte range and FNV-1a hash
+  __device__ bool str(const char* base, uint64_t& off, uint32_t& len, uint64_t& h) {
+    if (p >= e || *p != '"') return false;
+    ++p;
+    const char* s = p;
+    uint64_t x = kFnv0;
+    while (p < e && *p != '"') {
+      const unsigned char c = (unsigned char)*p;
+      if (c < 0x20 || c >= 0x80 || c == '\\') return false;
+      x = fnv_step(x, c);
+      ++p;
+    }
+    if (p >= e) return false;
+    off = (uint64_t)(s - base);
+    len = (uint32_t)(p - s);
+    h = x;
+    ++p;
+    return true;
+  }
+  __device__ bool key(const char*& ks, int& kn) {
+    if (p >= e || *p != '"') return false;
+    ++p;
+    ks = p;
+    while (p < e && *p != '"') {
+      const unsigned char c = (unsigned char)*p;
+      if (c < 0x20 || c >= 0x80 || c == '\\') return false;
+      ++p;
+    }
+    if (p >= e) return false;
+    kn = (int)(p - ks);
+    ++p;
+    return p < e && *p++ == ':';
+  }
+};
+
+__device__ __forceinline__ bool key_is(const char* ks, int kn, const char* s) {
+  int i = 0;
+  for (; s[i]; ++i)
+    if (i >= kn || ks[i] != s[i]) return false;
+  return i == kn;
+}
+
+// a JSON tag value: t = 1 integer (i), 2 double (d), 3 string, 4 bool (i = 0/1);
+// false when outside the exactly handled cases (the host decides)
+__device__ bool tag_value(Cur& c, int& t, int64_t& i, double& d, const char* base, uint64_t& soff, uint32_t& slen,
+                          uint64_t& sh) {
+  if (c.p >= c.e) return false;
+  const char ch = *c.p;
+  if (ch == '"') {
+    t = 3;
+    return c.str(base, soff, slen, sh);
+  }
+  if (c.lit("true")) {
+    t = 4;
+    i = 1;
+    return true;
+  }
+  if (c.lit("false")) {
+    t = 4;
+    i = 0;
+    return true;
+  }
+  // number: -?(0|[1-9][0-9]*)(.[0-9]+)?([eE][+-]?[0-9]+)?
+  bool neg = false;
+  if (*c.p == '-') {
+    neg = true;
+    ++c.p;
+  }
+  if (c.p >= c.e || *c.p < '0' || *c.p > '9') return false;
+  uint64_t m = 0;
+  int nd = 0, e10 = 0;
+  bool big = false;
+  if (*c.p == '0') {
+    ++c.p;
+    if (c.p < c.e && *c.p >= '0' && *c.p <= '9') return false;
+  } else {
+    while (c.p < c.e && *c.p >= '0' && *c.p <= '9') {
+      if (nd < 19) {
+        m = m * 10 + (uint64_t)(*c.p - '0');
+        if (m) ++nd;
+      } else {
+        big = true;
+      }
+      ++c.p;
+    }
+  }
+  bool frac = false;
+  if (c.p < c.e && *c.p == '.') {
+    frac = true;
+    ++c.p;
+    if (c.p >= c.e || *c.p < '0' || *c.p > '9') return false;
+    while (c.p < c.e && *c.p >= '0' && *c.p <= '9') {
+      if (nd < 19) {
+        m = m * 10 + (uint64_t)(*c.p - '0');
+        if (m) ++nd;
+        --e10;
+      } else {
+        big = true;
+      }
+      ++c.p;
+    }
+  }
+  if (c.p < c.e && (*c.p == 'e' || *c.p == 'E')) {
+    frac = true;
+    ++c.p;
+    bool eneg = false;
+    if (c.p < c.e && (*c.p == '+' || *c.p == '-')) eneg = *c.p++ == '-';
+    if (c.p >= c.e || *c.p < '0' || *c.p > '9') return false;
+    int x = 0;
+    while (c.p < c.e && *c.p >= '0' && *c.p <= '9') {
+      if (x < 100000) x = x * 10 + (*c.p - '0');
+      ++c.p;
+    }
+    e10 += eneg ? -x : x;
+  }
+  if (big) return false;
+  if (!frac) {  // JSON integer: u64 when non-negative, i64 when negative (a tag keeps it as i64)
+    if (neg) {
+      if (m > (1ull << 63)) return false;
+      t = 1;
+      i = (int64_t)(0 - m);
+      return true;
+    }
+    t = 1;
+    i = (int64_t)m;  // u64 beyond i64 wraps, as get<int64_t>() of an unsigned does
+    return true;
+  }
+  // Clinger's exact case: m and 10^|e10| are exact doubles, one rounding
+  if (m > (1ull << 53) || e10 < -22 || e10 > 22) return false;
+  constexpr double p10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
+                              1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+  double v = (double)m;
+  v = e10 >= 0 ? __dmul_rn(v, p10[e10]) : __ddiv_rn(v, p10[-e10]);
+  t = 2;
+  d = neg ? -v : v;
+  return true;
+}
+
+
+__device__ uint32_t parse_span(const char* base, const char* s, const char* e, uint64_t li, const LineOut& o) {
+  Cur c{s, e};
+  uint64_t begin, end, cid, parent, sid, tid;
+  bool has_cid, has_par;
+  uint64_t noff, th = 0, toff = 0, nh;
+  uint32_t nlen, tlen = 0;
+  if (!c.lit("{\"begin_ns\":") || !c.u64(begin)) return LK_HOST;
+  if (!c.lit(",\"correlation_id\":") || !c.u64_or_null(cid, has_cid)) return LK_HOST;
+  if (!c.lit(",\"end_ns\":") || !c.u64(end)) return LK_HOST;
+  uint32_t kind, level;
+  if (!c.lit(",\"kind\":\"")) return LK_HOST;
+  if (c.lit("sync\"")) kind = XSP_KIND_SYNC;
+  else if (c.lit("launch\"")) kind = XSP_KIND_LAUNCH;
+  else if (c.lit("exec\"")) kind = XSP_KIND_EXEC;
+  else return LK_HOST;
+  if (!c.lit(",\"level\":\"")) return LK_HOST;
+  if (c.lit("model\"")) level = XSP_LEVEL_MODEL;
+  else if (c.lit("layer\"")) level = XSP_LEVEL_LAYER;
+  else if (c.lit("kernel\"")) level = XSP_LEVEL_KERNEL;
+  else if (c.lit("api\"")) level = XSP_LEVEL_API;
+  else return LK_HOST;
+  if (!c.lit(",\"name\":") || !c.str(base, noff, nlen, nh)) return LK_HOST;
+  if (!c.lit(",\"parent_id\":") || !c.u64_or_null(parent, has_par)) return LK_HOST;
+  if (!c.lit(",\"rec\":\"span\",\"span_id\":") || !c.u64(sid)) return LK_HOST;
+  if (!c.lit(",\"tags\":{")) return LK_HOST;
+  // tags (metrics_from_tags / tag_int / tag_string semantics, span.cpp / correlator.cpp)
+  bool hf = false, hr = false, hw = false, ho = false, ht = false, ha = false;
+  int64_t vf = 0, vr = 0, vw = 0, va = 0;
+  double vo = 0.0;
+  uint8_t tb = 0;
+  if (!c.lit("}")) {
+    for (;;) {
+      const char* ks;
+      int kn;
+      if (!c.key(ks, kn)) return LK_HOST;
+      int t;
+      int64_t iv = 0;
+      double dv = 0.0;
+      uint64_t so = 0, sh = 0;
+      uint32_t sl = 0;
+      if (!tag_value(c, t, iv, dv, base, so, sl, sh)) return LK_HOST;
+      const bool num = t == 1 || t == 2 || t == 4;
+      // integer value of a number tag: an int, or a double truncated toward zero
+      auto as_int = [&](int64_t& out) -> bool {
+        if (t == 2) {
+          if (!(dv > -9.2233720368547758e18 && dv < 9.2233720368547758e18)) return false;
+          out = (int64_t)dv;
+        } else {
+          out = iv;
+        }
+        return true;
+      };
+      if (key_is(ks, kn, "flop_count_sp")) {
+        if (hf) return LK_HOST;
+        if (num) {
+          if (!as_int(vf)) return LK_HOST;
+          hf = true;
+          if (t == 1 && iv < 0) tb |= XSP_TAG_NEG_FLOPS;
+        }
+      } else if (key_is(ks, kn, "dram_read_bytes")) {
+        if (hr) return LK_HOST;
+        if (num) {
+          if (!as_int(vr)) return LK_HOST;
+          hr = true;
+          if (t == 1 && iv < 0) tb |= XSP_TAG_NEG_READ;
+        }
+      } else if (key_is(ks, kn, "dram_write_bytes")) {
+        if (hw) return LK_HOST;
+        if (num) {
+          if (!as_int(vw)) return LK_HOST;
+          hw = true;
+          if (t == 1 && iv < 0) tb |= XSP_TAG_NEG_WRITE;
+        }
+      } else if (key_is(ks, kn, "achieved_occupancy")) {
+        if (ho) return LK_HOST;
+        if (num) {
+          ho = true;
+          vo = t == 2 ? dv : (double)iv;
+          if (t == 2) tb |= XSP_TAG_OCC_DOUBLE;
+        }
+      } else if (key_is(ks, kn, "alloc_bytes")) {
+        if (ha) return LK_HOST;
+        if (num) {
+          if (!as_int(va)) return LK_HOST;
+          ha = true;
+        }
+      } else if (key_is(ks, kn, "layer_type")) {
+        if (ht) return LK_HOST;
+        if (t == 3) {
+          ht = true;
+          toff = so;
+          tlen = sl;
+          th = sh;
+        }
+      }
+      if (c.lit(",")) continue;
+      if (c.lit("}")) break;
+      return LK_HOST;
+    }
+  }
+  if (!c.lit(",\"trace_id\":") || !c.u64(tid) || !c.lit("}") || c.p != e) return LK_HOST;
+  const bool met = hf || hr || hw || ho;
+  uint8_t f = (uint8_t)(level | (kind << 2));
+  if (has_par) f |= XSP_F_PARENT;
+  if (has_cid) f |= XSP_F_CID;
+  if (met) f |= XSP_F_METRICS;
+  o.span_id[li] = sid;
+  o.parent[li] = has_par ? parent : 0;
+  o.begin[li] = begin;
+  o.end[li] = end;
+  o.cid[li] = has_cid ? cid : 0;
+  o.trace_id[li] = tid;
+  o.flags[li] = f;
+  o.name_hash[li] = nh;
+  o.name_off[li] = noff;
+  o.name_len[li] = nlen;
+  if (!ht) {
+    toff = 0;
+    tlen = 0;
+    th = kFnv0;
+  }
+  o.type_hash[li] = th;
+  o.type_off[li] = toff;
+  o.type_len[li] = tlen;
+  o.flops[li] = hf && vf > 0 ? (uint64_t)vf : 0;
+  o.dread[li] = hr && vr > 0 ? (uint64_t)vr : 0;
+  o.dwrite[li] = hw && vw > 0 ? (uint64_t)vw : 0;
+  o.occ[li] = ho ? vo : 0.0;
+  o.alloc[li] = ha ? va : 0;
+  o.tag_bits[li] = tb;
+  return LK_SPAN;
+}
+
+// ---- line index
+constexpr uint32_t kNlChunk = 64;
+
+__global__ void k_nl_count(const char* __restrict__ t, uint64_t n, uint32_t* __restrict__ cnt) {
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t b = c * kNlChunk;
+  if (b >= n) return;
+  const uint64_t e = b + kNlChunk < n ? b + kNlChunk : n;
+  uint32_t k = 0;
+  for (uint64_t i = b; i < e; ++i) k += t[i] == '\n';
+  cnt[c] = k;
+}
+
+__global__ void k_nl_write(const char* __restrict__ t, uint64_t n, const uint32_t* __restrict__ pos,
+                           uint64_t* __restrict__ nl) {
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t b = c * kNlChunk;
+  if (b >= n) return;
+  const uint64_t e = b + kNlChunk < n ? b + kNlChunk : n;
+  uint32_t k = pos[c];
+  for (uint64_t i = b; i < e; ++i)
+    if (t[i] == '\n') nl[k++] = i;
+}
+
+// line l = [start[l], end[l]) (end: its newline, or its stream's end)
+__global__ void k_parse_lines(const char* __restrict__ t, uint64_t n, const uint64_t* __restrict__ start,
+                              const uint64_t* __restrict__ nl, uint64_t nlines, LineOut o) {
+  const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nlines) return;
+  const uint64_t s = start[l];
+  const uint64_t e = nl[l];
+  // blank line: only ' ', '\t', '\r'
+  bool blank = true;
+  for (uint64_t i = s; i < e && blank; ++i) blank = t[i] == ' ' || t[i] == '\t' || t[i] == '\r';
+  if (blank) {
+    o.kind[l] = LK_BLANK;
+    return;
+  }
+  const char* p = t + s;
+  if (e - s >= 14 && p[0] == '{' && p[1] == '"' && p[2] == 'b' && p[3] == 'a') {  // {"batch_size": meta
+    o.kind[l] = LK_META;
+    return;
+  }
+  o.kind[l] = (uint8_t)parse_span(t, p, t + e, l, o);
+}
+
+// span index of every span line; the stream of every line
+__global__ void k_span_flags(const uint8_t* __restrict__ kind, uint64_t nlines, uint32_t* __restrict__ isspan) {
+  const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < nlines) isspan[l] = kind[l] == LK_SPAN;
+}
+
+struct Gather {
+  const uint32_t* isspan;
+  const uint32_t* spos;
+  const uint64_t* nl;
+  uint64_t nlines;
+  LineOut lo;
+  // outputs in file order (span index)
+  uint64_t *span_id, *parent, *begin, *end, *cid, *trace_id, *name_hash, *type_hash, *name_off, *type_off;
+  uint32_t *name_len, *type_len, *line_of;
+  uint8_t *flags, *tag_bits;
+  uint64_t *flops, *dread, *dwrite;
+  double* occ;
+  int64_t* alloc;
+};
+
+__global__ void k_gather_spans(Gather g) {
+  const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= g.nlines || !g.isspan[l]) return;
+  const uint32_t j = g.spos[l];
+  g.span_id[j] = g.lo.span_id[l];
+  g.parent[j] = g.lo.parent[l];
+  g.begin[j] = g.lo.begin[l];
+  g.end[j] = g.lo.end[l];
+  g.cid[j] = g.lo.cid[l];
+  g.trace_id[j] = g.lo.trace_id[l];
+  g.flags[j] = g.lo.flags[l];
+  g.name_hash[j] = g.lo.name_hash[l];
+  g.name_off[j] = g.lo.name_off[l];
+  g.name_len[j] = g.lo.name_len[l];
+  g.type_hash[j] = g.lo.type_hash[l];
+  g.type_off[j] = g.lo.type_off[l];
+  g.type_len[j] = g.lo.type_len[l];
+  g.flops[j] = g.lo.flops[l];
+  g.dread[j] = g.lo.dread[l];
+  g.dwrite[j] = g.lo.dwrite[l];
+  g.occ[j] = g.lo.occ[l];
+  g.alloc[j] = g.lo.alloc[l];
+  g.tag_bits[j] = g.lo.tag_bits[l];
+  g.line_of[j] = (uint32_t)l;
+}
+
+// ---- interning: runs of equal hashes in sorted order
+__global__ void k_iota32(uint32_t* v, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (uint32_t)i;
+}
+
+__global__ void k_run_heads(const uint64_t* __restrict__ h, uint64_t n, uint32_t* __restrict__ head) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) head[i] = (i == 0 || h[i] != h[i - 1]) ? 1u : 0u;
+}
+
+// uid[idx[i]] = run number; rep[run] = first member; byte-compare each member with the representative
+__global__ void k_run_assign(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ head,
+                             const uint32_t* __restrict__ runpos, uint64_t n, uint32_t* __restrict__ uid,
+                             uint32_t* __restrict__ rep) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t r = runpos[i] + head[i] - 1;
+  uid[idx[i]] = r;
+  if (head[i]) rep[r] = idx[i];
+}
+
+__global__ void k_run_verify(const char* __restrict__ t, const uint64_t* __restrict__ off,
+                             const uint32_t* __restrict__ len, const uint32_t* __restrict__ uid,
+                             const uint32_t* __restrict__ rep, const uint8_t* __restrict__ use, uint64_t n,
+                             uint32_t* __restrict__ collision) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n || (use && !use[j])) return;
+  const uint32_t r = rep[uid[j]];
+  if (r == j) return;
+  if (len[r] != len[j]) {
+    *collision = 1;
+    return;
+  }
+  const char* a = t + off[j];
+  const char* b = t + off[r];
+  for (uint32_t k = 0; k < len[j]; ++k)
+    if (a[k] != b[k]) {
+      *collision = 1;
+      return;
+    }
+}
+
+__global__ void k_rep_ranges(const uint32_t* __restrict__ rep, const uint64_t* __restrict__ off,
+                             const uint32_t* __restrict__ len, uint32_t U, uint64_t* __restrict__ ro,
+                             uint32_t* __restrict__ rl) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < U) {
+    ro[r] = off[rep[r]];
+    rl[r] = len[rep[r]];
+  }
+}
+
+__global__ void k_mark_used(const uint32_t* __restrict__ uid, const uint8_t* __restrict__ use, uint64_t n,
+                            uint8_t* __restrict__ used) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n && use[j]) used[uid[j]] = 1;
+}
+
+__global__ void k_is_layer(const uint8_t* __restrict__ flags, uint64_t n, uint8_t* __restrict__ out) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) out[j] = (flags[j] & 3u) == XSP_LEVEL_LAYER ? 1 : 0;
+}
+
+// ingest's trace_id check (collector.cpp:248-255): the first stream holding a
+// span whose trace_id differs from its meta record's
+__global__ void k_tid_check(const uint64_t* __restrict__ tid, const uint64_t* __restrict__ soff, uint32_t S,
+                            const uint64_t* __restrict__ mtid, uint64_t n, uint32_t* __restrict__ bad) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  uint32_t lo = 0, hi = S;  // soff[lo] <= j < soff[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (soff[mid] <= j) lo = mid; else hi = mid;
+  }
+  if (tid[j] != mtid[lo]) atomicMin(bad, lo);
+}
+
+__global__ void k_map_ids(const uint32_t* __restrict__ uid, const uint32_t* __restrict__ rank, uint64_t n,
+                          uint32_t* __restrict__ out) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) out[j] = rank[uid[j]];
+}
+
+// ---- final columns in timeline order (perm = file index of timeline position)
+struct Final {
+  const uint32_t* perm;
+  uint64_t n;
+  const uint64_t *span_id, *parent, *begin, *end, *cid, *trace_id;
+  const uint8_t *flags, *tag_bits;
+  const uint32_t *name_id, *type_id;
+  const uint64_t *flops, *dread, *dwrite;
+  const double* occ;
+  const int64_t* alloc;
+  uint64_t *o_span_id, *o_parent, *o_begin, *o_end, *o_cid, *o_trace_id;
+  uint8_t *o_flags, *o_tag_bits;
+  uint32_t* o_name_id;
+  uint32_t* met;  // metric / layer flags for the scans
+  uint32_t* lay;
+};
+
+__global__ void k_final_spans(Final f) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  const uint32_t j = f.perm ? f.perm[i] : (uint32_t)i;
+  f.o_span_id[i] = f.span_id[j];
+  f.o_parent[i] = f.parent[j];
+  f.o_begin[i] = f.begin[j];
+  f.o_end[i] = f.end[j];
+  f.o_cid[i] = f.cid[j];
+  f.o_trace_id[i] = f.trace_id[j];
+  const uint8_t fl = f.flags[j];
+  f.o_flags[i] = fl;
+  f.o_tag_bits[i] = f.tag_bits[j];
+  f.o_name_id[i] = f.name_id[j];
+  f.met[i] = (fl & XSP_F_METRICS) ? 1u : 0u;
+  f.lay[i] = (fl & 3u) == XSP_LEVEL_LAYER ? 1u : 0u;
+}
+
+__global__ void k_final_tables(Final f, const uint32_t* __restrict__ mpos, const uint32_t* __restrict__ lpos,
+                               uint64_t* __restrict__ flops, uint64_t* __restrict__ dread,
+                               uint64_t* __restrict__ dwrite, double* __restrict__ occ,
+                               int64_t* __restrict__ alloc, uint32_t* __restrict__ type_id) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  const uint32_t j = f.perm ? f.perm[i] : (uint32_t)i;
+  if (f.met[i]) {
+    const uint32_t m = mpos[i];
+    flops[m] = f.flops[j];
+    dread[m] = f.dread[j];
+    dwrite[m] = f.dwrite[j];
+    occ[m] = f.occ[j];
+  }
+  if (f.lay[i]) {
+    const uint32_t q = lpos[i];
+    alloc[q] = f.alloc[j];
+    type_id[q] = f.type_id[j];
+  }
+}
+
+RadixScratch radix_scratch_ing(xsp_ctx* ctx, uint64_t n) {
+  RadixScratch s;
+  s.keys_alt = ctx->d<uint64_t>("ig.rs.keys_alt", n);
+  s.vals_alt = ctx->d<uint32_t>("ig.rs.vals_alt", n);
+  const uint64_t ce = radix_counts_elems(n);
+  s.counts = ctx->d<uint32_t>("ig.rs.counts", ce);
+  s.scan_tmp = ctx->d<uint32_t>("ig.rs.scan", scan_scratch_elems(ce));
+  s.and_or = ctx->d<unsigned long long>("ig.rs.andor", 2);
+  s.and_or_host = ctx->h<unsigned long long>("ig.rs.andor_h", 2);
+  return s;
+}
+
+unsigned blocks(uint64_t n) { return ceil_div(n ? n : 1, 256); }
+
+// ---- canonical meta record on the host (encode_meta_record layout)
+struct HostCur {
+  const char* p;
+  const char* e;
+  bool lit(const char* s) {
+    const size_t k = std::strlen(s);
+    if ((size_t)(e - p) < k || std::memcmp(p, s, k) != 0) return false;
+    p += k;
+    return true;
+  }
+  bool u64(uint64_t& v) {
+    if (p >= e || *p < '0' || *p > '9') return false;
+    if (*p == '0') {
+      ++p;
+      v = 0;
+      return p >= e || *p < '0' || *p > '9';
+    }
+    uint64_t x = 0;
+    while (p < e && *p >= '0' && *p <= '9') {
+      const uint64_t d = (uint64_t)(*p - '0');
+      if (x > (~0ull - d) / 10) return false;
+      x = x * 10 + d;
+      ++p;
+    }
+    v = x;
+    return true;
+  }
+  bool str(std::string& out) {
+    if (p >= e || *p != '"') return false;
+    const char* s = ++p;
+    while (p < e && *p != '"') {
+      const unsigned char c = (unsigned char)*p;
+      if (c < 0x20 || c >= 0x80 || c == '\\') return false;
+      ++p;
+    }
+    if (p >= e) return false;
+    out.assign(s, p);
+    ++p;
+    return true;
+  }
+  bool number(double& d) {  // JSON number -> double (strtod: correctly rounded)
+    const char* s = p;
+    if (p < e && *p == '-') ++p;
+    if (p >= e || *p < '0' || *p > '9') return false;
+    if (*p == '0') {
+      ++p;
+      if (p < e && *p >= '0' && *p <= '9') return false;
+    }
+    while (p < e && *p >= '0' && *p <= '9') ++p;
+    if (p < e && *p == '.') {
+      ++p;
+      if (p >= e || *p < '0' || *p > '9') return false;
+      while (p < e && *p >= '0' && *p <= '9') ++p;
+    }
+    if (p < e && (*p == 'e' || *p == 'E')) {
+      ++p;
+      if (p < e && (*p == '+' || *p == '-')) ++p;
+      if (p >= e || *p < '0' || *p > '9') return false;
+      while (p < e && *p >= '0' && *p <= '9') ++p;
+    }
+    const std::string t(s, p);
+    d = std::strtod(t.c_str(), nullptr);
+    return std::isfinite(d);
+  }
+};
+
+struct Meta {
+  uint64_t trace_id = 0, batch = 0, run = 0;
+  uint32_t levels = 0;
+  bool serialized = false;
+  std::string sys_name;
+  double peak = 0.0, bw = 0.0;
+};
+
+bool parse_meta(const char* s, const char* e, Meta& m) {
+  HostCur c{s, e};
+  if (!c.lit("{\"batch_size\":") || !c.u64(m.batch) || !c.lit(",\"levels\":[")) return false;
+  if (!c.lit("]")) {
+    for (;;) {
+      std::string l;
+      if (!c.str(l)) return false;
+      int bit = l == "model" ? 0 : l == "layer" ? 1 : l == "kernel" ? 2 : l == "api" ? 3 : -1;
+      if (bit < 0) return false;
+      m.levels |= 1u << bit;
+      if (c.lit(",")) continue;
+      if (c.lit("]")) break;
+      return false;
+    }
+  }
+  if (!c.lit(",\"rec\":\"meta\",\"run_index\":") || !c.u64(m.run)) return false;
+  if (!c.lit(",\"serialized\":")) return false;
+  if (c.lit("true")) m.serialized = true;
+  else if (!c.lit("false")) return false;
+  if (!c.lit(",\"system\":{\"mem_bw\":") || !c.number(m.bw)) return false;
+  if (!c.lit(",\"name\":") || !c.str(m.sys_name)) return false;
+  if (!c.lit(",\"peak_flops\":") || !c.number(m.peak)) return false;
+  if (!c.lit("},\"trace_id\":") || !c.u64(m.trace_id) || !c.lit("}")) return false;
+  while (c.p < c.e && (*c.p == '\r' || *c.p == ' ' || *c.p == '\t')) ++c.p;
+  return c.p == c.e && m.batch <= 0xFFFFFFFFull && m.run <= 0xFFFFFFFFull;
+}
+
+// interning: returns false on a hash collision; fills the string table (sorted)
+// and ids[j] for the used entries
+bool intern(xsp_ctx* ctx, const std::string& tag, const char* dtext, const char* htext, uint64_t n,
+            const uint64_t* hash, const uint64_t* off, const uint32_t* len, const uint8_t* use, uint32_t* ids,
+            std::vector<std::string>& table, cudaStream_t st) {
+  table.clear();
+  if (n == 0) return true;
+  uint64_t* keys = ctx->d<uint64_t>(tag + ".k", n);
+  uint32_t* idx = ctx->d<uint32_t>(tag + ".i", n);
+  XSP_CUDA(cudaMemcpyAsync(keys, hash, n * 8, cudaMemcpyDeviceToDevice, st));
+  k_iota32<<<blocks(n), 256, 0, st>>>(idx, n);
+  RadixScratch rs = radix_scratch_ing(ctx, n);
+  radix_sort_pairs(keys, idx, n, 0, 64, rs, st, &ctx->launches);
+  uint32_t* head = ctx->d<uint32_t>(tag + ".h", n + 1);
+  uint32_t* runpos = ctx->d<uint32_t>(tag + ".rp", n + 1);
+  uint32_t* nrun = ctx->d<uint32_t>(tag + ".nr", 1);
+  k_run_heads<<<blocks(n), 256, 0, st>>>(keys, n, head);
+  uint32_t* scr = ctx->d<uint32_t>(tag + ".sc", scan_scratch_elems(n + 1));
+  exclusive_scan<uint32_t, uint32_t>(head, runpos, n, scr, nrun, st, &ctx->launches);
+  uint32_t* uid = ctx->d<uint32_t>(tag + ".u", n);
+  uint32_t* rep = ctx->d<uint32_t>(tag + ".r", n);
+  k_run_assign<<<blocks(n), 256, 0, st>>>(idx, head, runpos, n, uid, rep);
+  uint32_t* col = ctx->d<uint32_t>(tag + ".c", 1);
+  XSP_CUDA(cudaMemsetAsync(col, 0, 4, st));
+  k_run_verify<<<blocks(n), 256, 0, st>>>(dtext, off, len, uid, rep, use, n, col);
+  uint32_t h2[2];
+  XSP_CUDA(cudaMemcpyAsync(h2, nrun, 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(h2 + 1, col, 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  if (h2[1]) return false;
+  const uint32_t U = h2[0];
+  // the representatives' byte ranges and which runs hold a used entry
+  uint64_t* d_ro = ctx->d<uint64_t>(tag + ".ro", U + 1ull);
+  uint32_t* d_rl = ctx->d<uint32_t>(tag + ".rl", U + 1ull);
+  uint8_t* d_used = ctx->d<uint8_t>(tag + ".used", U + 1ull);
+  XSP_CUDA(cudaMemsetAsync(d_used, use ? 0 : 1, U, st));
+  k_rep_ranges<<<blocks(U), 256, 0, st>>>(rep, off, len, U, d_ro, d_rl);
+  if (use) k_mark_used<<<blocks(n), 256, 0, st>>>(uid, use, n, d_used);
+  std::vector<uint64_t> roff(U);
+  std::vector<uint32_t> rlen(U);
+  std::vector<uint8_t> used_run(U);
+  XSP_CUDA(cudaMemcpyAsync(roff.data(), d_ro, U * 8ull, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(rlen.data(), d_rl, U * 4ull, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(used_run.data(), d_used, U, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  std::vector<uint32_t> order;
+  order.reserve(U);
+  for (uint32_t r = 0; r < U; ++r)
+    if (used_run[r]) order.push_back(r);
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    return std::string_view(htext + roff[a], rlen[a]) < std::string_view(htext + roff[b], rlen[b]);
+  });
+  std::vector<uint32_t> rank(U, 0);
+  table.reserve(order.size());
+  for (uint32_t k = 0; k < order.size(); ++k) {
+    rank[order[k]] = k;
+    table.emplace_back(htext + roff[order[k]], rlen[order[k]]);
+  }
+  uint32_t* d_rank = ctx->d<uint32_t>(tag + ".rank", U + 1);
+  XSP_CUDA(cudaMemcpyAsync(d_rank, rank.data(), U * 4ull, cudaMemcpyHostToDevice, st));
+  k_map_ids<<<blocks(n), 256, 0, st>>>(uid, d_rank, n, ids);
+  XSP_CUDA(cudaStreamSynchronize(st));
+  ctx->launches += 7;
+  return true;
+}
+
+}  // namespace
+
+// ctx-owned host storage of one ingest result
+struct IngestHost {
+  std::vector<std::string> names, types;
+  std::string blob_names, blob_types;
+  std::vector<uint64_t> off_names, off_types;
+  std::vector<uint64_t> span_off, trace_id;
+  std::vector<uint32_t> levels, batch, run;
+  std::vector<uint8_t> serialized;
+  std::string sys_name;
+};
+
+void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uint32_t S, xsp_ingest_out* out,
+                      cudaStream_t st) {
+  static thread_local IngestHost H;  // one result per thread (pointers valid until the next call)
+  std::memset(out, 0, sizeof(*out));
+  out->status = XSP_INGEST_HOST;
+  out->bad_stream = 0;
+  const uint64_t n_text = soff[S];
+  // ---- text to the device; one line boundary per stream end so lines never straddle streams
+  char* dtext = ctx->d<char>("ig.text", n_text + 1);
+  XSP_CUDA(cudaMemcpyAsync(dtext, htext, n_text, cudaMemcpyHostToDevice, st));
+  ctx->h2d_bytes = n_text;
+  const uint64_t nch = ceil_div(n_text ? n_text : 1, kNlChunk);
+  uint32_t* cnt = ctx->d<uint32_t>("ig.nlc", nch + 1);
+  uint32_t* pos = ctx->d<uint32_t>("ig.nlp", nch + 1);
+  uint32_t* tot = ctx->d<uint32_t>("ig.nlt", 1);
+  k_nl_count<<<blocks(nch), 256, 0, st>>>(dtext, n_text, cnt);
+  uint32_t* scr = ctx->d<uint32_t>("ig.scan", scan_scratch_elems(nch + 1));
+  exclusive_scan<uint32_t, uint32_t>(cnt, pos, nch, scr, tot, st, &ctx->launches);
+  uint32_t hnl = 0;
+  XSP_CUDA(cudaMemcpyAsync(&hnl, tot, 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  // newline positions + the stream ends (a stream's last line may lack '\n')
+  uint64_t* nl = ctx->d<uint64_t>("ig.nl", hnl + S + 1);
+  k_nl_write<<<blocks(nch), 256, 0, st>>>(dtext, n_text, pos, nl);
+  std::vector<uint64_t> hnlpos(hnl);
+  XSP_CUDA(cudaMemcpyAsync(hnlpos.data(), nl, hnl * 8ull, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  // merge stream ends that are not already line ends; the line -> stream map
+  std::vector<uint64_t> ends, starts;
+  ends.reserve(hnl + S);
+  starts.reserve(hnl + S);
+  std::vector<uint32_t> line_stream;
+  line_stream.reserve(hnl + S);
+  {
+    uint64_t k = 0;
+    for (uint32_t s = 0; s < S; ++s) {
+      uint64_t at = soff[s];
+      while (k < hnl && hnlpos[k] < soff[s + 1]) {
+        starts.push_back(at);
+        ends.push_back(hnlpos[k]);
+        at = hnlpos[k++] + 1;
+        line_stream.push_back(s);
+      }
+      if (at < soff[s + 1]) {  // unterminated last line of stream s
+        starts.push_back(at);
+        ends.push_back(soff[s + 1]);
+        line_stream.push_back(s);
+      }
+    }
+  }
+  const uint64_t L = ends.size();
+  XSP_CUDA(cudaMemcpyAsync(nl, ends.data(), L * 8, cudaMemcpyHostToDevice, st));
+  uint64_t* lstart = ctx->d<uint64_t>("ig.ls", L + 1);
+  XSP_CUDA(cudaMemcpyAsync(lstart, starts.data(), L * 8, cudaMemcpyHostToDevice, st));
+  // ---- parse every line
+  LineOut lo;
+  lo.kind = ctx->d<uint8_t>("ig.kind", L + 1);
+  lo.span_id = ctx->d<uint64_t>("ig.l.sid", L);
+  lo.parent = ctx->d<uint64_t>("ig.l.par", L);
+  lo.begin = ctx->d<uint64_t>("ig.l.b", L);
+  lo.end = ctx->d<uint64_t>("ig.l.e", L);
+  lo.cid = ctx->d<uint64_t>("ig.l.cid", L);
+  lo.trace_id = ctx->d<uint64_t>("ig.l.tid", L);
+  lo.flags = ctx->d<uint8_t>("ig.l.f", L);
+  lo.name_hash = ctx->d<uint64_t>("ig.l.nh", L);
+  lo.name_off = ctx->d<uint64_t>("ig.l.no", L);
+  lo.name_len = ctx->d<uint32_t>("ig.l.nl", L);
+  lo.type_hash = ctx->d<uint64_t>("ig.l.th", L);
+  lo.type_off = ctx->d<uint64_t>("ig.l.to", L);
+  lo.type_len = ctx->d<uint32_t>("ig.l.tl", L);
+  lo.flops = ctx->d<uint64_t>("ig.l.fl", L);
+  lo.dread = ctx->d<uint64_t>("ig.l.dr", L);
+  lo.dwrite = ctx->d<uint64_t>("ig.l.dw", L);
+  lo.occ = ctx->d<double>("ig.l.oc", L);
+  lo.alloc = ctx->d<int64_t>("ig.l.al", L);
+  lo.tag_bits = ctx->d<uint8_t>("ig.l.tb", L);
+  if (L) k_parse_lines<<<blocks(L), 256, 0, st>>>(dtext, n_text, lstart, nl, L, lo);
+  std::vector<uint8_t> hkind(L);
+  XSP_CUDA(cudaMemcpyAsync(hkind.data(), lo.kind, L, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  ctx->launches += 4;
+  // ---- per stream: exactly one meta record (host), no line the fast path left to the host
+  std::vector<Meta> meta(S);
+  std::vector<int> nmeta(S, 0);
+  std::vector<uint64_t> nspan(S, 0);
+  for (uint64_t l = 0; l < L; ++l) {
+    const uint32_t s = line_stream[l];
+    if (hkind[l] == LK_HOST) {
+      out->bad_stream = s;
+      return;
+    }
+    if (hkind[l] == LK_META) {
+      if (++nmeta[s] > 1 || !parse_meta(htext + starts[l], htext + ends[l], meta[s])) {
+        out->bad_stream = s;
+        return;
+      }
+    }
+    if (hkind[l] == LK_SPAN) ++nspan[s];
+  }
+  for (uint32_t s = 0; s < S; ++s)
+    if (nmeta[s] != 1) {
+      out->bad_stream = s;
+      return;
+    }
+  uint64_t n = 0;
+  H.span_off.assign(S + 1, 0);
+  for (uint32_t s = 0; s < S; ++s) H.span_off[s + 1] = H.span_off[s] + nspan[s];
+  n = H.span_off[S];
+  if (n >= 0xFFFFFFF0ull) throw std::invalid_argument("more than 2^32-16 spans in one call");
+  // ---- span lines -> spans (file order)
+  uint32_t* isspan = ctx->d<uint32_t>("ig.iss", L + 1);
+  uint32_t* spos = ctx->d<uint32_t>("ig.spos", L + 1);
+  uint32_t* stot = ctx->d<uint32_t>("ig.stot", 1);
+  k_span_flags<<<blocks(L), 256, 0, st>>>(lo.kind, L, isspan);
+  uint32_t* scr2 = ctx->d<uint32_t>("ig.scan2", scan_scratch_elems(L + 1));
+  exclusive_scan<uint32_t, uint32_t>(isspan, spos, L, scr2, stot, st, &ctx->launches);
+  Gather g;
+  g.isspan = isspan;
+  g.spos = spos;
+  g.nl = nl;
+  g.nlines = L;
+  g.lo = lo;
+  g.span_id = ctx->d<uint64_t>("ig.s.sid", n + 1);
+  g.parent = ctx->d<uint64_t>("ig.s.par", n + 1);
+  g.begin = ctx->d<uint64_t>("ig.s.b", n + 1);
+  g.end = ctx->d<uint64_t>("ig.s.e", n + 1);
+  g.cid = ctx->d<uint64_t>("ig.s.cid", n + 1);
+  g.trace_id = ctx->d<uint64_t>("ig.s.tid", n + 1);
+  g.name_hash = ctx->d<uint64_t>("ig.s.nh", n + 1);
+  g.type_hash = ctx->d<uint64_t>("ig.s.th", n + 1);
+  g.name_off = ctx->d<uint64_t>("ig.s.no", n + 1);
+  g.type_off = ctx->d<uint64_t>("ig.s.to", n + 1);
+  g.name_len = ctx->d<uint32_t>("ig.s.nl", n + 1);
+  g.type_len = ctx->d<uint32_t>("ig.s.tl", n + 1);
+  g.line_of = ctx->d<uint32_t>("ig.s.line", n + 1);
+  g.flags = ctx->d<uint8_t>("ig.s.f", n + 1);
+  g.tag_bits = ctx->d<uint8_t>("ig.s.tb", n + 1);
+  g.flops = ctx->d<uint64_t>("ig.s.fl", n + 1);
+  g.dread = ctx->d<uint64_t>("ig.s.dr", n + 1);
+  g.dwrite = ctx->d<uint64_t>("ig.s.dw", n + 1);
+  g.occ = ctx->d<double>("ig.s.oc", n + 1);
+  g.alloc = ctx->d<int64_t>("ig.s.al", n + 1);
+  k_gather_spans<<<blocks(L), 256, 0, st>>>(g);
+  ctx->launches += 2;
+  // ---- intern names (every span) and layer types (layer spans only)
+  uint32_t* name_fid = ctx->d<uint32_t>("ig.s.nid", n + 1);
+  uint32_t* type_fid = ctx->d<uint32_t>("ig.s.tyid", n + 1);
+  uint8_t* is_layer = ctx->d<uint8_t>("ig.s.isl", n + 1);
+  if (n) k_is_layer<<<blocks(n), 256, 0, st>>>(g.flags, n, is_layer);
+  if (!intern(ctx, "ig.in", dtext, htext, n, g.name_hash, g.name_off, g.name_len, nullptr, name_fid, H.names, st) ||
+      !intern(ctx, "ig.it", dtext, htext, n, g.type_hash, g.type_off, g.type_len, is_layer, type_fid, H.types, st)) {
+    out->bad_stream = 0;  // a hash collision: the host interns
+    return;
+  }
+  // ---- trace arrays (host) and the trace_id check (ingest's own fault, collector.cpp:248-255)
+  H.trace_id.resize(S);
+  H.levels.resize(S);
+  H.batch.resize(S);
+  H.run.resize(S);
+  H.serialized.resize(S);
+  for (uint32_t s = 0; s < S; ++s) {
+    H.trace_id[s] = meta[s].trace_id;
+    H.levels[s] = meta[s].levels;
+    H.batch[s] = (uint32_t)meta[s].batch;
+    H.run[s] = (uint32_t)meta[s].run;
+    H.serialized[s] = meta[s].serialized;
+  }
+  H.sys_name = S ? meta[0].sys_name : std::string();
+  uint64_t* d_soff = ctx->d<uint64_t>("ig.soff", S + 1ull);
+  XSP_CUDA(cudaMemcpyAsync(d_soff, H.span_off.data(), (S + 1ull) * 8, cudaMemcpyHostToDevice, st));
+  uint64_t* d_mtid = ctx->d<uint64_t>("ig.mtid", S + 1ull);
+  XSP_CUDA(cudaMemcpyAsync(d_mtid, H.trace_id.data(), S * 8ull, cudaMemcpyHostToDevice, st));
+  uint32_t* d_lv = ctx->d<uint32_t>("ig.lv", S + 1ull);
+  XSP_CUDA(cudaMemcpyAsync(d_lv, H.levels.data(), S * 4ull, cudaMemcpyHostToDevice, st));
+  {
+    uint32_t* bad = ctx->d<uint32_t>("ig.badtid", 1);
+    XSP_CUDA(cudaMemsetAsync(bad, 0xFF, 4, st));
+    if (n) k_tid_check<<<blocks(n), 256, 0, st>>>(g.trace_id, d_soff, S, d_mtid, n, bad);
+    uint32_t hb = 0;
+    XSP_CUDA(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaStreamSynchronize(st));
+    if (hb != 0xFFFFFFFFu) {
+      out->bad_stream = hb;
+      return;
+    }
+  }
+  // ---- sort_timeline per trace (stage (b)), then the final columns
+  uint32_t* perm = ctx->d<uint32_t>("ig.perm", n + 1);
+  uint32_t sorted = 1;
+  if (n) run_sort_timeline(ctx, n, g.begin, g.flags, g.span_id, S, d_soff, perm, &sorted, st);
+  Final f;
+  f.perm = sorted ? nullptr : perm;
+  f.n = n;
+  f.span_id = g.span_id; f.parent = g.parent; f.begin = g.begin; f.end = g.end; f.cid = g.cid;
+  f.trace_id = g.trace_id; f.flags = g.flags; f.tag_bits = g.tag_bits; f.name_id = name_fid;
+  f.type_id = type_fid; f.flops = g.flops; f.dread = g.dread; f.dwrite = g.dwrite; f.occ = g.occ;
+  f.alloc = g.alloc;
+  xsp_span_cols& c = out->cols;
+  c.n_spans = n;
+  c.span_id = f.o_span_id = ctx->d<uint64_t>("ig.o.sid", n + 1);
+  c.parent_id = f.o_parent = ctx->d<uint64_t>("ig.o.par", n + 1);
+  c.begin_ns = f.o_begin = ctx->d<uint64_t>("ig.o.b", n + 1);
+  c.end_ns = f.o_end = ctx->d<uint64_t>("ig.o.e", n + 1);
+  c.cid = f.o_cid = ctx->d<uint64_t>("ig.o.cid", n + 1);
+  f.o_trace_id = ctx->d<uint64_t>("ig.o.tid", n + 1);
+  c.flags = f.o_flags = ctx->d<uint8_t>("ig.o.f", n + 1);
+  f.o_tag_bits = ctx->d<uint8_t>("ig.o.tb", n + 1);
+  c.name_id = f.o_name_id = ctx->d<uint32_t>("ig.o.nid", n + 1);
+  f.met = ctx->d<uint32_t>("ig.o.met", n + 1);
+  f.lay = ctx->d<uint32_t>("ig.o.lay", n + 1);
+  if (n) k_final_spans<<<blocks(n), 256, 0, st>>>(f);
+  uint32_t* mpos = ctx->d<uint32_t>("ig.mpos", n + 1);
+  uint32_t* lpos = ctx->d<uint32_t>("ig.lpos", n + 1);
+  uint32_t* mtot = ctx->d<uint32_t>("ig.mtot", 2);
+  uint32_t* scr3 = ctx->d<uint32_t>("ig.scan3", scan_scratch_elems(n + 1));
+  exclusive_scan<uint32_t, uint32_t>(f.met, mpos, n, scr3, mtot, st, &ctx->launches);
+  exclusive_scan<uint32_t, uint32_t>(f.lay, lpos, n, scr3, mtot + 1, st, &ctx->launches);
+  uint32_t ht[2] = {0, 0};
+  XSP_CUDA(cudaMemcpyAsync(ht, mtot, 8, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaStreamSynchronize(st));
+  c.n_metric_rows = ht[0];
+  c.n_layer_rows = ht[1];
+  uint64_t* o_fl = ctx->d<uint64_t>("ig.o.fl", ht[0] + 1ull);
+  uint64_t* o_dr = ctx->d<uint64_t>("ig.o.dr", ht[0] + 1ull);
+  uint64_t* o_dw = ctx->d<uint64_t>("ig.o.dw", ht[0] + 1ull);
+  double* o_oc = ctx->d<double>("ig.o.oc", ht[0] + 1ull);
+  int64_t* o_al = ctx->d<int64_t>("ig.o.al", ht[1] + 1ull);
+  uint32_t* o_ty = ctx->d<uint32_t>("ig.o.ty", ht[1] + 1ull);
+  c.flops = o_fl;
+  c.dram_read = o_dr;
+  c.dram_write = o_dw;
+  c.occupancy = o_oc;
+  c.alloc_bytes = o_al;
+  c.type_id = o_ty;
+  if (n) k_final_tables<<<blocks(n), 256, 0, st>>>(f, mpos, lpos, o_fl, o_dr, o_dw, o_oc, o_al, o_ty);
+  ctx->launches += 2;
+  out->traces.n_traces = S;
+  out->traces.span_off = d_soff;
+  out->traces.levels = d_lv;
+  // ---- validate_bundle (stage (a)); any issue: the host reproduces ingest's exact fault
+  xsp_validate_in vin{f.o_trace_id, d_mtid, f.o_tag_bits};
+  xsp_validation_out vout;
+  std::memset(&vout, 0, sizeof(vout));
+  run_validate(ctx, &c, &out->traces, &vin, &vout, st);
+  if (vout.n_issues) {
+    std::vector<uint32_t> toff(S + 1);
+    XSP_CUDA(cudaMemcpyAsync(toff.data(), vout.trace_issue_off, (S + 1ull) * 4, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t s = 0; s < S; ++s)
+      if (toff[s + 1] > toff[s]) {
+        out->bad_stream = s;
+        break;
+      }
+    return;
+  }
+  // ---- host side of the result
+  auto blob = [](const std::vector<std::string>& v, std::string& b, std::vector<uint64_t>& off) {
+    b.clear();
+    off.assign(v.size() + 1, 0);
+    for (size_t i = 0; i < v.size(); ++i) {
+      b += v[i];
+      off[i + 1] = b.size();
+    }
+  };
+  blob(H.names, H.blob_names, H.off_names);
+  blob(H.types, H.blob_types, H.off_types);
+  out->names = {(uint32_t)H.names.size(), H.blob_names.data(), H.off_names.data()};
+  out->types = {(uint32_t)H.types.size(), H.blob_types.data(), H.off_types.data()};
+  out->trace_id = H.trace_id.data();
+  out->trace_batch = H.batch.data();
+  out->trace_run = H.run.data();
+  out->trace_serialized = H.serialized.data();
+  out->span_off_host = H.span_off.data();
+  out->levels_host = H.levels.data();
+  out->system_name = H.sys_name.c_str();
+  out->peak_flops = S ? meta[0].peak : 0.0;
+  out->mem_bw = S ? meta[0].bw : 0.0;
+  out->status = XSP_INGEST_OK;
+  XSP_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace xsp

@@ -249,6 +249,44 @@ class Engine:
                                      C.byref(opts), C.byref(co), C.byref(to), C.c_void_p(stream)))
         return co, to
 
+    # ---- JSONL ingest (xsp_ingest_jsonl)
+    def ingest_jsonl(self, streams, stream=None) -> Tuple[Optional[SpanBatch], int]:
+        """ingest() of each JSONL stream (bytes) on the GPU -> (SpanBatch with one
+        trace per stream, -1), or (None, stream) when that stream needs the
+        reference-exact host parser (xsp.h XSP_INGEST_HOST)."""
+        from .leveled import _d2h
+        blob = b"".join(streams)
+        off = np.zeros(len(streams) + 1, dtype=np.uint64)
+        if streams:
+            off[1:] = np.cumsum([len(x) for x in streams])
+        out = capi.IngestOut()
+        self._check(self.lib.xsp_ingest_jsonl(self.ctx, blob, off.ctypes.data_as(capi.u64p), len(streams),
+                                              C.byref(out), C.c_void_p(stream)))
+        if out.status != capi.INGEST_OK:
+            return None, int(out.bad_stream)
+        c = out.cols
+        n, M, Lr, T = int(c.n_spans), int(c.n_metric_rows), int(c.n_layer_rows), len(streams)
+        d = lambda ptr, dt, k: _d2h(self.lib, self.ctx, ptr, dt, k)
+        h = lambda ptr, dt, k: _copy(ptr, {np.uint64: capi.u64p, np.uint32: capi.u32p, np.uint8: capi.u8p}[dt], k)
+
+        def strings(t):
+            o = _copy(t.off, capi.u64p, t.n + 1)
+            raw = C.string_at(t.bytes, int(o[-1])) if t.n and o[-1] else b""
+            return [raw[int(o[i]):int(o[i + 1])] for i in range(t.n)]
+
+        b = SpanBatch(span_id=d(c.span_id, np.uint64, n), parent_id=d(c.parent_id, np.uint64, n),
+                      begin_ns=d(c.begin_ns, np.uint64, n), end_ns=d(c.end_ns, np.uint64, n),
+                      cid=d(c.cid, np.uint64, n), flags=d(c.flags, np.uint8, n), name_id=d(c.name_id, np.uint32, n),
+                      flops=d(c.flops, np.uint64, M), dram_read=d(c.dram_read, np.uint64, M),
+                      dram_write=d(c.dram_write, np.uint64, M), occupancy=d(c.occupancy, np.float64, M),
+                      alloc_bytes=d(c.alloc_bytes, np.int64, Lr), type_id=d(c.type_id, np.uint32, Lr),
+                      trace_span_off=h(out.span_off_host, np.uint64, T + 1), trace_id=h(out.trace_id, np.uint64, T),
+                      trace_levels=h(out.levels_host, np.uint32, T), trace_batch=h(out.trace_batch, np.uint32, T),
+                      trace_run=h(out.trace_run, np.uint32, T), trace_serialized=h(out.trace_serialized, np.uint8, T),
+                      names=strings(out.names), types=strings(out.types),
+                      system_name=out.system_name or b"", peak_flops=out.peak_flops, mem_bw=out.mem_bw)
+        return b, -1
+
     # ---- multi-GPU table combine (xsp_comm_init / xsp_combine_tables)
     def comm_init(self, world: int, rank: int, dist=None):
         """Join an NCCL communicator of `world` ranks; rank 0's unique id travels
