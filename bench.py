@@ -404,6 +404,55 @@ def measure_leveled(eng, args, local: int):
                          "note": "65 tiny synchronous calls per step: launch/sync bound, not HBM bound"}}
 
 
+def measure_ingest(eng, args, local: int, with_cpu: bool):
+    """JSONL wire-format ingest on the GPU (xsp_ingest_jsonl):
+    H2D of the text, line parse, name / type interning, sort_timeline and
+    validate_bundle, columns left in HBM. Workload: one run of every (model,
+    batch) group of the C3 family as JSONL streams (one TraceBundle each; the
+    reference writer's record layout). cpu_baseline: the reference's own
+    ingest() (oracle/_ref, one thread) on a bounded sample of the same streams."""
+    import ctypes as C
+    import torch
+    from paper_1908_06869_b200 import _capi as capi
+    from paper_1908_06869_b200 import columns, synth
+    b, *_ = synth.c3(runs=1, n_models=args.ingest_models)
+    streams = [columns.to_jsonl(b, t) for t in range(b.n_traces)]
+    blob = b"".join(streams)
+    off = np.zeros(len(streams) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(x) for x in streams])
+    out = capi.IngestOut()
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def call():
+        eng._check(eng.lib.xsp_ingest_jsonl(eng.ctx, blob, off.ctypes.data_as(capi.u64p), len(streams),
+                                            C.byref(out), C.c_void_p(stream)))
+        assert out.status == capi.INGEST_OK and out.cols.n_spans == b.n_spans
+
+    call()
+    torch.cuda.synchronize()
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        call()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) / reps * 1e3
+    line = {"metric": "M spans/s ingested from JSONL (GPU, host text to device columns)",
+            "value": b.n_spans / (ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": ms, "spans": b.n_spans,
+            "streams": len(streams), "text_bytes": len(blob), "text_GB_per_s": len(blob) / (ms / 1e3) / 1e9,
+            "how": "xsp_ingest_jsonl wall time (synchronous call: H2D of the text + parse + intern + sort + validate)",
+            "workload": f"C3 family, {args.ingest_models} models x 8 batch sizes x 1 run as JSONL streams"}
+    if with_cpu:
+        from oracle import ref
+        if ref.available():
+            k = max(1, min(len(streams), 24))
+            t0 = time.perf_counter()
+            rb = ref.ingest(streams[:k])
+            sec = time.perf_counter() - t0
+            line["cpu_baseline"] = {"value": rb.n_spans / sec / 1e6, "unit": UNIT, "cores": 1, "kind": "reference",
+                                    "sample": f"first {k} streams = {rb.n_spans} spans through the reference's ingest()"}
+    return line
+
+
 class _Replica:
     """DeviceBatch interface over slices of replicated device columns."""
 
@@ -536,6 +585,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2, help="steps of the end-to-end (host buffer) C5 timing")
     ap.add_argument("--leveled-models", type=int, default=65, help="0 skips the leveled (C2 at scale) line")
     ap.add_argument("--leveled-runs", type=int, default=10)
+    ap.add_argument("--ingest-models", type=int, default=24, help="0 skips the JSONL ingest line")
     ap.add_argument("--c4-layers", type=int, default=28_600_000,
                     help="layers of the C4 long trace (~7 spans per layer; 0 skips the C4 measurement)")
     args = ap.parse_args()
@@ -664,6 +714,8 @@ def main():
     torch.cuda.empty_cache()
     c4_line = measure_c4(eng, args, rank, world, local, dist) if args.c4_layers > 0 else None
     lev_line = measure_leveled(eng, args, local) if args.leveled_models > 0 and rank == 0 else None
+    ing_line = measure_ingest(eng, args, local, world == 1 and not args.no_cpu_baseline) \
+        if args.ingest_models > 0 and rank == 0 else None
 
     if rank != 0:
         if dist:
@@ -704,6 +756,8 @@ def main():
         line["c4"] = c4_line
     if lev_line:
         line["leveled"] = lev_line
+    if ing_line:
+        line["ingest_jsonl"] = ing_line
     if world == 1 and not args.no_cpu_baseline:
         from oracle import ref
         if ref.available():

@@ -224,36 +224,45 @@ def to_jsonl(b: SpanBatch, t: int) -> bytes:
     import json
     lv = int(b.trace_levels[t])
     s0, s1 = int(b.trace_span_off[t]), int(b.trace_span_off[t + 1])
-    met = (b.flags & capi.F_METRICS) != 0
-    lay = (b.flags & 3) == capi.LEVEL_LAYER
-    mrow = np.cumsum(met) - met
-    arow = np.cumsum(lay) - lay
-    dq = lambda x: json.dumps(x)
-    num = lambda x: repr(float(x)) if float(x) != int(float(x)) or abs(float(x)) >= 1e16 else repr(float(x))
+    f_all = b.flags
+    met = (f_all & capi.F_METRICS) != 0
+    lay = (f_all & 3) == capi.LEVEL_LAYER
+    m0, a0 = int(met[:s0].sum()), int(lay[:s0].sum())
     sysname = b.system_name.decode() if isinstance(b.system_name, bytes) else b.system_name
     out = [("{\"batch_size\":%d,\"levels\":[%s],\"rec\":\"meta\",\"run_index\":%d,\"serialized\":%s,"
-            "\"system\":{\"mem_bw\":%s,\"name\":%s,\"peak_flops\":%s},\"trace_id\":%d}")
-           % (int(b.trace_batch[t]), ",".join(dq(_LEVEL_NAMES[i]) for i in range(4) if lv >> i & 1),
-              int(b.trace_run[t]), "true" if int(b.trace_serialized[t]) else "false", num(b.mem_bw), dq(sysname),
-              num(b.peak_flops), int(b.trace_id[t]))]
+            "\"system\":{\"mem_bw\":%r,\"name\":%s,\"peak_flops\":%r},\"trace_id\":%d}")
+           % (int(b.trace_batch[t]), ",".join(json.dumps(_LEVEL_NAMES[i]) for i in range(4) if lv >> i & 1),
+              int(b.trace_run[t]), "true" if int(b.trace_serialized[t]) else "false", float(b.mem_bw),
+              json.dumps(sysname), float(b.peak_flops), int(b.trace_id[t]))]
     tid = int(b.trace_id[t])
-    names = [n.decode() for n in b.names]
-    types = [n.decode() for n in b.types]
-    for i in range(s0, s1):
-        f = int(b.flags[i])
-        tags = []
-        if f & capi.F_METRICS:
-            m = int(mrow[i])
-            tags = ["\"achieved_occupancy\":" + repr(float(b.occupancy[m])),
-                    "\"dram_read_bytes\":%d" % int(b.dram_read[m]), "\"dram_write_bytes\":%d" % int(b.dram_write[m]),
-                    "\"flop_count_sp\":%d" % int(b.flops[m])]
-        if (f & 3) == capi.LEVEL_LAYER:
-            a = int(arow[i])
-            tags = ["\"alloc_bytes\":%d" % int(b.alloc_bytes[a]), "\"layer_type\":" + dq(types[int(b.type_id[a])])]
-        out.append("{\"begin_ns\":%d,\"correlation_id\":%s,\"end_ns\":%d,\"kind\":\"%s\",\"level\":\"%s\","
-                   "\"name\":%s,\"parent_id\":%s,\"rec\":\"span\",\"span_id\":%d,\"tags\":{%s},\"trace_id\":%d}"
-                   % (int(b.begin_ns[i]), str(int(b.cid[i])) if f & capi.F_CID else "null", int(b.end_ns[i]),
-                      _KIND_NAMES[(f >> 2) & 3], _LEVEL_NAMES[f & 3], dq(names[int(b.name_id[i])]),
-                      str(int(b.parent_id[i])) if f & capi.F_PARENT else "null", int(b.span_id[i]),
-                      ",".join(tags), tid))
+    qn = [json.dumps(n.decode()) for n in b.names]
+    qt = [json.dumps(n.decode()) for n in b.types]
+    fl = f_all[s0:s1].tolist()
+    beg, end = b.begin_ns[s0:s1].tolist(), b.end_ns[s0:s1].tolist()
+    cid, par, sid = b.cid[s0:s1].tolist(), b.parent_id[s0:s1].tolist(), b.span_id[s0:s1].tolist()
+    nid = b.name_id[s0:s1].tolist()
+    nm = int(met[s0:s1].sum())
+    na = int(lay[s0:s1].sum())
+    occ = b.occupancy[m0:m0 + nm].tolist()
+    rd, wr, fo = b.dram_read[m0:m0 + nm].tolist(), b.dram_write[m0:m0 + nm].tolist(), b.flops[m0:m0 + nm].tolist()
+    al, ty = b.alloc_bytes[a0:a0 + na].tolist(), b.type_id[a0:a0 + na].tolist()
+    kinds = ["sync", "launch", "exec", "?"]
+    levels = _LEVEL_NAMES
+    mi = ai = 0
+    tail = ',"trace_id":%d}' % tid
+    for k in range(s1 - s0):
+        f = fl[k]
+        if f & 0x40:
+            tags = '"achieved_occupancy":%r,"dram_read_bytes":%d,"dram_write_bytes":%d,"flop_count_sp":%d' % (
+                occ[mi], rd[mi], wr[mi], fo[mi])
+            mi += 1
+        else:
+            tags = ""
+        if (f & 3) == 1:
+            tags = '"alloc_bytes":%d,"layer_type":%s' % (al[ai], qt[ty[ai]])
+            ai += 1
+        out.append('{"begin_ns":%d,"correlation_id":%s,"end_ns":%d,"kind":"%s","level":"%s","name":%s,'
+                   '"parent_id":%s,"rec":"span","span_id":%d,"tags":{%s}' % (
+                       beg[k], cid[k] if f & 0x20 else "null", end[k], kinds[(f >> 2) & 3], levels[f & 3],
+                       qn[nid[k]], par[k] if f & 0x10 else "null", sid[k], tags) + tail)
     return ("\n".join(out) + "\n").encode()
