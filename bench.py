@@ -533,18 +533,26 @@ class C5:
         torch.cuda.empty_cache()
 
 
-def e2e_host(eng, hb, groups, copies: int, steps: int, barrier, dist):
-    """End to end through the host-buffer C ABI (xsp_run_host): every step runs
-    `copies` calls on pinned host columns, each with H2D of its inputs and D2H of
-    every result column inside the timed region (wall clock around the calls,
-    device synchronised on both sides; max over ranks)."""
+def e2e_host(eng, hb, groups, copies: int, steps: int, barrier, dist, packed=None):
+    """End to end through the host-buffer C ABI (xsp_run_host, or
+    xsp_run_host_packed when `packed` is given): every step runs `copies` calls
+    on pinned host columns, each with H2D of its inputs and D2H of every result
+    column inside the timed region (wall clock around the calls, device
+    synchronised on both sides; max over ranks)."""
     import torch
-    eng.run_host(hb, groups=groups, raw=True)
+
+    def call():
+        if packed is not None:
+            eng.run_host_packed(packed, hb, groups=groups, raw=True)
+        else:
+            eng.run_host(hb, groups=groups, raw=True)
+
+    call()
     barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         for _ in range(copies):
-            eng.run_host(hb, groups=groups, raw=True)
+            call()
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / steps
     h2d, d2h = eng.transfer_bytes()
@@ -668,11 +676,18 @@ def main():
     sv3 = survey_bytes(b)
     p1_ms3 = c3_stages["pass1"][0] / max(c3_stages["pass1"][1], 1)
     hb = b.pinned()
-    e3_ms, h2d3, d2h3 = e2e_host(eng, hb, groups, 1, max(2, args.steps // 4), barrier, dist)
+    # the packed wire form (xsp_pack_host: u32 begin deltas / durations / cid
+    # offsets, sparse parent / cid lists), built once like the columns themselves
+    pk = eng.pack_host(hb)
+    e3_ms, h2d3, d2h3 = e2e_host(eng, hb, groups, 1, max(2, args.steps // 4), barrier, dist, packed=pk)
+    e3d_ms, h2d3d, d2h3d = e2e_host(eng, hb, groups, 1, max(2, args.steps // 4), barrier, dist)
     c3_line = {"metric": METRIC, "value": b.n_spans * world / (c3_ms / 1e3) / 1e6, "unit": UNIT,
                "ms_per_step": c3_ms, "spans_per_gpu": b.n_spans, "scaling": "weak", "config": c3_config(args),
                "e2e": {"value": b.n_spans * world / (e3_ms / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d3,
-                       "d2h_bytes_per_step": d2h3, "ms_per_step": e3_ms},
+                       "d2h_bytes_per_step": d2h3, "ms_per_step": e3_ms, "input": "packed (xsp_run_host_packed)"},
+               "e2e_dense": {"value": b.n_spans * world / (e3d_ms / 1e3) / 1e6, "unit": UNIT,
+                             "h2d_bytes_per_step": h2d3d, "d2h_bytes_per_step": d2h3d, "ms_per_step": e3d_ms,
+                             "input": "dense span columns (xsp_run_host)"},
                "roofline": {"bound": "hbm", "kernel": "k_pass1", "achieved": pass1_bytes(b) / (p1_ms3 / 1e3) / 1e9,
                             "peak": peak, "unit": "GB/s", "bytes_per_launch": pass1_bytes(b),
                             "ms_per_launch": p1_ms3},
@@ -701,11 +716,15 @@ def main():
     value = c5.spans_all / (ms / 1e3) / 1e6
     # end to end: the same corpus from pinned host buffers through xsp_run_host
     # (one call per copy: H2D of its columns, D2H of every result column)
-    e_ms, h2d, d2h = e2e_host(eng, hb, groups, len(c5.mine), args.e2e_steps, barrier, dist)
+    e_ms, h2d, d2h = e2e_host(eng, hb, groups, len(c5.mine), args.e2e_steps, barrier, dist, packed=pk)
     e2e = {"value": c5.spans_all / (e_ms / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "steps": args.e2e_steps,
            "calls_per_step": len(c5.mine),
-           "how": "xsp_run_host per C3 copy on the same pinned host columns (every copy's H2D and D2H happen)"}
+           "how": "xsp_run_host_packed per C3 copy on the same pinned host buffers (every copy's H2D and D2H "
+                  "happen); the span columns in the packed wire form (xsp_pack_host, built once outside the "
+                  "timed region like the columns themselves: u32 begin deltas / durations / cid offsets, "
+                  "parent_id and cid only where flagged), unpacked on the device",
+           "dense_c3_e2e_value": c3_line["e2e_dense"]["value"]}
     calls = len(c5.calls)
     p1_ms = stages["pass1"][0] / max(stages["pass1"][1], 1)  # per launch
     p1_bytes = pass1_bytes(b) * len(c5.mine) // max(calls, 1)

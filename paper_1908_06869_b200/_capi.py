@@ -174,6 +174,13 @@ class StringTable(C.Structure):
     _fields_ = [("n", C.c_uint32), ("bytes", C.c_char_p), ("off", u64p)]
 
 
+class PackedCols(C.Structure):
+    _fields_ = [("n_spans", C.c_uint64), ("flags", u8p), ("name_id", u32p), ("dbegin", u32p), ("dur", u32p),
+                ("n_cid", C.c_uint64), ("dcid", u32p), ("n_parent", C.c_uint64), ("parent", u64p),
+                ("n_blocks", C.c_uint64), ("blk_cid_base", u64p), ("blk_cid0", u32p), ("blk_par0", u32p),
+                ("n_esc", C.c_uint64), ("esc_key", u64p), ("esc_val", u64p)]
+
+
 class StringTableOut(C.Structure):  # xsp_string_table as returned by the library
     _fields_ = [("n", C.c_uint32), ("bytes", C.c_void_p), ("off", u64p)]
 
@@ -202,7 +209,7 @@ EXPORTS = [
     "xsp_stage_times", "xsp_leveled", "xsp_sort_timeline_host", "xsp_correlate_host",
     "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline", "xsp_resolve_serialized",
     "xsp_resolve_serialized_host", "xsp_report_csv", "xsp_report_csv_host", "xsp_comm_unique_id",
-    "xsp_comm_init", "xsp_combine_tables", "xsp_ingest_jsonl",
+    "xsp_comm_init", "xsp_combine_tables", "xsp_ingest_jsonl", "xsp_pack_host", "xsp_run_host_packed",
 ]
 
 _lib = None
@@ -281,6 +288,12 @@ def load() -> C.CDLL:
                        C.POINTER(StringTable), C.POINTER(StringTable), C.c_uint32, C.c_int,
                        C.POINTER(C.c_char_p), u64p, P]
         fn.restype = C.c_int32
+    lib.xsp_pack_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(PackedCols)]
+    lib.xsp_pack_host.restype = C.c_int32
+    lib.xsp_run_host_packed.argtypes = [P, C.POINTER(PackedCols), C.POINTER(SpanCols), C.POINTER(Traces),
+                                        C.POINTER(Groups), C.POINTER(SystemSpec), C.POINTER(AnalysisOpts),
+                                        C.POINTER(CorrOut), C.POINTER(TablesOut), P]
+    lib.xsp_run_host_packed.restype = C.c_int32
     lib.xsp_ingest_jsonl.argtypes = [P, C.c_char_p, u64p, C.c_uint32, C.POINTER(IngestOut), P]
     lib.xsp_ingest_jsonl.restype = C.c_int32
     lib.xsp_comm_unique_id.argtypes = [P]

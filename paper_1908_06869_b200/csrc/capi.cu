@@ -11,9 +11,14 @@
 #define XSP_API extern "C" __attribute__((visibility("default")))
 
 namespace xsp {
+void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_packed_cols* out);
+uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint64_t s1, uint8_t* flags,
+                      uint32_t* name_id, uint64_t* begin, uint64_t* end, uint64_t* cid, uint64_t* parent,
+                      const std::string& tag, cudaStream_t st);
 bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht, const xsp_groups* groups,
                       const xsp_system_spec* spec, const xsp_analysis_opts* opts, xsp_corr_out* corr_host,
-                      xsp_tables_out* tab_host);
+                      xsp_tables_out* tab_host,
+                      const xsp_packed_cols* pk = nullptr);
 void run_sort_timeline(xsp_ctx* ctx, uint64_t n, const uint64_t* begin, const uint8_t* flags, const uint64_t* sid,
                        uint32_t T, const uint64_t* off, uint32_t* perm, uint32_t* was_sorted, cudaStream_t st);
 void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, const xsp_validate_in* vin,
@@ -509,6 +514,68 @@ XSP_API xsp_status xsp_ingest_jsonl(xsp_ctx* ctx, const char* text, const uint64
   return guard(ctx, "xsp_ingest_jsonl", [&] {
     if (!out || !stream_off || (n_streams && !text)) throw std::invalid_argument("null argument");
     xsp::run_ingest_jsonl(ctx, text, stream_off, n_streams, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_pack_host(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht,
+                                 xsp_packed_cols* out) {
+  return guard(ctx, "xsp_pack_host", [&] {
+    check_cols(hc, ht);
+    if (!ht || !out) throw std::invalid_argument("null argument");
+    xsp::pack_host(ctx, hc, ht, out);
+  });
+}
+
+XSP_API xsp_status xsp_run_host_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, const xsp_span_cols* hc,
+                                       const xsp_traces* ht, const xsp_groups* groups, const xsp_system_spec* spec,
+                                       const xsp_analysis_opts* opts, xsp_corr_out* corr_host,
+                                       xsp_tables_out* tab_host, void* stream) {
+  return guard(ctx, "xsp_run_host_packed", [&] {
+    if (!pk || !hc || !ht || !groups || !spec || !opts || !corr_host || !tab_host)
+      throw std::invalid_argument("null argument");
+    if (pk->n_spans != hc->n_spans) throw std::invalid_argument("packed and host columns disagree on n_spans");
+    if (groups->n_groups && (!groups->first_trace || !groups->n_runs || !groups->batch_size))
+      throw std::invalid_argument("null group column");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ctx->h2d_bytes = ctx->d2h_bytes = 0;
+    if (xsp::run_host_chunked(ctx, hc, ht, groups, spec, opts, corr_host, tab_host, pk)) return;
+    // single shot: span_id and the tables as xsp_run_host uploads them, the
+    // span columns unpacked on the device
+    const uint64_t n = pk->n_spans;
+    xsp_span_cols dc;
+    dc.n_spans = n;
+    dc.span_id = to_dev(ctx, "span_id", hc->span_id, n, st);
+    dc.n_metric_rows = hc->n_metric_rows;
+    dc.flops = to_dev(ctx, "flops", hc->flops, hc->n_metric_rows, st);
+    dc.dram_read = to_dev(ctx, "read", hc->dram_read, hc->n_metric_rows, st);
+    dc.dram_write = to_dev(ctx, "write", hc->dram_write, hc->n_metric_rows, st);
+    dc.occupancy = to_dev(ctx, "occ", hc->occupancy, hc->n_metric_rows, st);
+    dc.n_layer_rows = hc->n_layer_rows;
+    dc.alloc_bytes = to_dev(ctx, "alloc", hc->alloc_bytes, hc->n_layer_rows, st);
+    dc.type_id = to_dev(ctx, "type", hc->type_id, hc->n_layer_rows, st);
+    uint8_t* f = ctx->d<uint8_t>("pk1.f", n + 1);
+    uint32_t* nm = ctx->d<uint32_t>("pk1.n", n + 1);
+    uint64_t* b = ctx->d<uint64_t>("pk1.b", n + 1);
+    uint64_t* e = ctx->d<uint64_t>("pk1.e", n + 1);
+    uint64_t* c = ctx->d<uint64_t>("pk1.c", n + 1);
+    uint64_t* p = ctx->d<uint64_t>("pk1.p", n + 1);
+    ctx->h2d_bytes += xsp::stage_packed(ctx, pk, 0, n, f, nm, b, e, c, p, "pk1.", st);
+    dc.flags = f;
+    dc.name_id = nm;
+    dc.begin_ns = b;
+    dc.end_ns = e;
+    dc.cid = c;
+    dc.parent_id = p;
+    xsp_traces dt = upload_traces(ctx, ht, st);
+    xsp_corr_out dcorr;
+    std::memset(&dcorr, 0, sizeof(dcorr));
+    xsp::run_correlate(ctx, &dc, &dt, 0, &dcorr, st);
+    xsp_tables_out dtab;
+    std::memset(&dtab, 0, sizeof(dtab));
+    xsp::run_analyze(ctx, &dc, &dcorr, groups, spec, opts, &dtab, st);
+    download_corr(ctx, dcorr, corr_host, st);
+    download_tables(ctx, dtab, opts, tab_host, st);
+    XSP_CUDA(cudaStreamSynchronize(st));
   });
 }
 

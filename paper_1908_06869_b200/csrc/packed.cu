@@ -1,0 +1,288 @@
+// Packed host input for xsp_run_host_packed (include/xsp.h xsp_packed_cols).
+//
+// The end-to-end path is PCIe-bound: xsp_run_host moves ~52 B per span to the
+// device, 37 of them in the five 8-byte span columns. Packed, the wire carries
+// begin as a u32 delta, end as a u32 duration, cid as a u32 offset from its
+// block base (cid spans only) and parent_id for explicit-parent spans only —
+// ~34 B per span for C3 — and one CTA per 256-span block rebuilds the full
+// columns in HBM (segmented scan of the begin deltas, in-block ranks of the
+// sparse entries). Values that do not fit (trace and block starts, negative
+// or >= 2^32 deltas, durations, cid offsets) travel raw in a sorted escape
+// list.
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "ctx.h"
+#include "xsp_common.cuh"
+
+namespace xsp {
+
+constexpr uint32_t kPB = XSP_PACK_BLOCK;
+
+// ---- host packer -----------------------------------------------------------
+void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_packed_cols* out) {
+  const uint64_t n = c->n_spans;
+  const uint64_t nb = (n + kPB - 1) / kPB;
+  uint64_t ncid = 0, npar = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    ncid += (c->flags[i] & XSP_F_CID) != 0;
+    npar += (c->flags[i] & XSP_F_PARENT) != 0;
+  }
+  uint32_t* dbeg = ctx->h<uint32_t>("pk.dbeg", n + 1);
+  uint32_t* dur = ctx->h<uint32_t>("pk.dur", n + 1);
+  uint32_t* dcid = ctx->h<uint32_t>("pk.dcid", ncid + 1);
+  uint64_t* par = ctx->h<uint64_t>("pk.par", npar + 1);
+  uint64_t* cbase = ctx->h<uint64_t>("pk.cbase", nb + 1);
+  uint32_t* cid0 = ctx->h<uint32_t>("pk.cid0", nb + 1);
+  uint32_t* par0 = ctx->h<uint32_t>("pk.par0", nb + 1);
+  std::vector<uint64_t> ekey, eval;
+  ekey.reserve(nb + tr->n_traces + 1024);
+  eval.reserve(nb + tr->n_traces + 1024);
+  std::vector<uint8_t> head(n ? n : 1, 0);
+  for (uint32_t t = 0; t < tr->n_traces; ++t)
+    if (tr->span_off[t] < n) head[tr->span_off[t]] = 1;
+  uint64_t ci = 0, pi = 0;
+  for (uint64_t b = 0; b < nb; ++b) {
+    const uint64_t r0 = b * kPB, r1 = std::min(n, r0 + kPB);
+    uint64_t base = ~0ull;
+    for (uint64_t i = r0; i < r1; ++i)
+      if (c->flags[i] & XSP_F_CID) base = std::min(base, c->cid[i]);
+    cbase[b] = base == ~0ull ? 0 : base;
+    cid0[b] = (uint32_t)ci;
+    par0[b] = (uint32_t)pi;
+    for (uint64_t i = r0; i < r1; ++i) {
+      const uint64_t bg = c->begin_ns[i], en = c->end_ns[i];
+      // begin: delta from the previous span (a reset at trace / block starts)
+      const bool reset = i == r0 || head[i] || bg < c->begin_ns[i - 1] || bg - c->begin_ns[i - 1] >= XSP_PACK_ESC;
+      if (reset) {
+        dbeg[i] = XSP_PACK_ESC;
+        ekey.push_back(i << 2 | 0);
+        eval.push_back(bg);
+      } else {
+        dbeg[i] = (uint32_t)(bg - c->begin_ns[i - 1]);
+      }
+      if (en < bg || en - bg >= XSP_PACK_ESC) {
+        dur[i] = XSP_PACK_ESC;
+        ekey.push_back(i << 2 | 1);
+        eval.push_back(en);
+      } else {
+        dur[i] = (uint32_t)(en - bg);
+      }
+      if (c->flags[i] & XSP_F_CID) {
+        const uint64_t d = c->cid[i] - cbase[b];
+        if (d >= XSP_PACK_ESC) {
+          dcid[ci] = XSP_PACK_ESC;
+          ekey.push_back(i << 2 | 2);
+          eval.push_back(c->cid[i]);
+        } else {
+          dcid[ci] = (uint32_t)d;
+        }
+        ++ci;
+      }
+      if (c->flags[i] & XSP_F_PARENT) par[pi++] = c->parent_id[i];
+    }
+  }
+  uint64_t* ek = ctx->h<uint64_t>("pk.ekey", ekey.size() + 1);
+  uint64_t* ev = ctx->h<uint64_t>("pk.eval", eval.size() + 1);
+  std::memcpy(ek, ekey.data(), ekey.size() * 8);
+  std::memcpy(ev, eval.data(), eval.size() * 8);
+  out->n_spans = n;
+  out->flags = c->flags;
+  out->name_id = c->name_id;
+  out->dbegin = dbeg;
+  out->dur = dur;
+  out->n_cid = ncid;
+  out->dcid = dcid;
+  out->n_parent = npar;
+  out->parent = par;
+  out->n_blocks = nb;
+  out->blk_cid_base = cbase;
+  out->blk_cid0 = cid0;
+  out->blk_par0 = par0;
+  out->n_esc = ekey.size();
+  out->esc_key = ek;
+  out->esc_val = ev;
+}
+
+// ---- device unpack -----------------------------------------------------------
+__device__ uint64_t esc_lookup(const uint64_t* __restrict__ key, const uint64_t* __restrict__ val, uint32_t n,
+                               uint64_t k) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (key[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return val[lo < n ? lo : n - 1];
+}
+
+struct UnpackArgs {
+  uint64_t s0, s1;             // the chunk's global rows
+  uint64_t b0;                 // its first global block
+  const uint8_t* flags;        // chunk-local (already on the device)
+  const uint32_t* dbegin;      // chunk-local
+  const uint32_t* dur;         // chunk-local
+  const uint32_t* dcid;        // chunk-local list (entries from the chunk's first cid span)
+  const uint64_t* parent;      // chunk-local list
+  const uint64_t* cbase;       // blocks b0 ..
+  const uint32_t* cid0;        // blocks b0 .. (global counts)
+  const uint32_t* par0;
+  uint64_t cid_first, par_first;  // global list index of the chunk's first entries
+  const uint64_t* esc_key;     // the chunk's escapes
+  const uint64_t* esc_val;
+  uint32_t n_esc;
+  uint64_t* begin;             // outputs, chunk-local rows
+  uint64_t* end;
+  uint64_t* cid;
+  uint64_t* parent_out;
+};
+
+// one CTA (kPB threads) per global block overlapping the chunk
+__global__ void __launch_bounds__(kPB) k_unpack(UnpackArgs a) {
+  __shared__ uint64_t s_val[kPB / 32];
+  __shared__ uint32_t s_rst[kPB / 32];
+  __shared__ uint32_t s_cnt[2][kPB / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint64_t b = a.b0 + blockIdx.x;
+  const uint64_t row = b * kPB + tid;
+  const bool in = row >= a.s0 && row < a.s1;
+  const uint64_t r = row - a.s0;
+  const uint8_t f = in ? a.flags[r] : 0;
+  // begin: segmented inclusive scan of (reset, value) within the block
+  uint64_t v = 0;
+  bool rst = true;
+  if (in) {
+    const uint32_t d = a.dbegin[r];
+    rst = d == XSP_PACK_ESC;
+    v = rst ? esc_lookup(a.esc_key, a.esc_val, a.n_esc, row << 2 | 0) : d;
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t pv = __shfl_up_sync(0xffffffffu, v, o);
+    const uint32_t pr = __shfl_up_sync(0xffffffffu, (uint32_t)rst, o);
+    if (lane >= (uint32_t)o && !rst) {
+      v += pv;
+      rst = pr;
+    }
+  }
+  if (lane == 31) {
+    s_val[warp] = v;
+    s_rst[warp] = rst;
+  }
+  // sparse-entry ranks within the block
+  const uint32_t hc = __ballot_sync(0xffffffffu, (f & XSP_F_CID) != 0);
+  const uint32_t hp = __ballot_sync(0xffffffffu, (f & XSP_F_PARENT) != 0);
+  if (lane == 0) {
+    s_cnt[0][warp] = __popc(hc);
+    s_cnt[1][warp] = __popc(hp);
+  }
+  __syncthreads();
+  if (!in) return;
+  // carry from the earlier warps of the block, up to the last reset
+  if (!rst) {
+    for (int w = (int)warp - 1; w >= 0; --w) {
+      v += s_val[w];
+      if (s_rst[w]) break;
+    }
+  }
+  const uint64_t begin = v;
+  a.begin[r] = begin;
+  const uint32_t du = a.dur[r];
+  a.end[r] = du == XSP_PACK_ESC ? esc_lookup(a.esc_key, a.esc_val, a.n_esc, row << 2 | 1) : begin + du;
+  const uint32_t below = (1u << lane) - 1u;
+  uint32_t pc = __popc(hc & below), pp = __popc(hp & below);
+  for (uint32_t w = 0; w < warp; ++w) {
+    pc += s_cnt[0][w];
+    pp += s_cnt[1][w];
+  }
+  const uint64_t bi = b - a.b0;
+  // list positions: entries of this chunk before the block (the chunk's first
+  // block starts at s0, whose earlier rows are not part of the chunk)
+  const uint64_t cbefore = bi == 0 ? 0 : a.cid0[bi] - a.cid_first;
+  const uint64_t pbefore = bi == 0 ? 0 : a.par0[bi] - a.par_first;
+  if (f & XSP_F_CID) {
+    const uint64_t j = cbefore + pc;
+    const uint32_t dc = a.dcid[j];
+    a.cid[r] = dc == XSP_PACK_ESC ? esc_lookup(a.esc_key, a.esc_val, a.n_esc, row << 2 | 2) : a.cbase[bi] + dc;
+  } else {
+    a.cid[r] = 0;
+  }
+  a.parent_out[r] = (f & XSP_F_PARENT) ? a.parent[pbefore + pp] : 0;
+}
+
+// Stages rows [s0, s1) of a packed batch on stream st into the device columns
+// of `dst` (begin / end / cid / parent_id rebuilt; flags and name_id copied),
+// using `tag`-named staging buffers. Returns the H2D bytes issued.
+uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint64_t s1, uint8_t* flags,
+                      uint32_t* name_id, uint64_t* begin, uint64_t* end, uint64_t* cid, uint64_t* parent,
+                      const std::string& tag, cudaStream_t st) {
+  const uint64_t ns = s1 - s0;
+  if (!ns) return 0;
+  uint64_t bytes = 0;
+  auto h2d = [&](void* d, const void* h, uint64_t nbytes) {
+    if (!nbytes) return;
+    XSP_CUDA(cudaMemcpyAsync(d, h, nbytes, cudaMemcpyHostToDevice, st));
+    bytes += nbytes;
+  };
+  const uint64_t b0 = s0 / kPB, b1 = (s1 + kPB - 1) / kPB, nbk = b1 - b0;
+  // global list positions of the chunk's first / past-the-end sparse entries
+  auto rank = [&](const uint32_t* blk0, uint8_t bit, uint64_t s) -> uint64_t {
+    if (s >= pk->n_spans) return bit == XSP_F_CID ? pk->n_cid : pk->n_parent;
+    const uint64_t b = s / kPB;
+    uint64_t k = blk0[b];
+    for (uint64_t i = b * kPB; i < s; ++i) k += (pk->flags[i] & bit) != 0;
+    return k;
+  };
+  const uint64_t c0 = rank(pk->blk_cid0, XSP_F_CID, s0), c1 = rank(pk->blk_cid0, XSP_F_CID, s1);
+  const uint64_t p0 = rank(pk->blk_par0, XSP_F_PARENT, s0), p1 = rank(pk->blk_par0, XSP_F_PARENT, s1);
+  const uint64_t* e0 = std::lower_bound(pk->esc_key, pk->esc_key + pk->n_esc, s0 << 2);
+  const uint64_t* e1 = std::lower_bound(pk->esc_key, pk->esc_key + pk->n_esc, s1 << 2);
+  const uint64_t ne = e1 - e0;
+  uint32_t* d_dbeg = ctx->d<uint32_t>(tag + "pk.dbeg", ns);
+  uint32_t* d_dur = ctx->d<uint32_t>(tag + "pk.dur", ns);
+  uint32_t* d_dcid = ctx->d<uint32_t>(tag + "pk.dcid", c1 - c0 + 1);
+  uint64_t* d_par = ctx->d<uint64_t>(tag + "pk.par", p1 - p0 + 1);
+  uint64_t* d_cb = ctx->d<uint64_t>(tag + "pk.cb", nbk + 1);
+  uint32_t* d_c0 = ctx->d<uint32_t>(tag + "pk.c0", nbk + 1);
+  uint32_t* d_p0 = ctx->d<uint32_t>(tag + "pk.p0", nbk + 1);
+  uint64_t* d_ek = ctx->d<uint64_t>(tag + "pk.ek", ne + 1);
+  uint64_t* d_ev = ctx->d<uint64_t>(tag + "pk.ev", ne + 1);
+  h2d(flags, pk->flags + s0, ns);
+  h2d(name_id, pk->name_id + s0, ns * 4);
+  h2d(d_dbeg, pk->dbegin + s0, ns * 4);
+  h2d(d_dur, pk->dur + s0, ns * 4);
+  h2d(d_dcid, pk->dcid + c0, (c1 - c0) * 4);
+  h2d(d_par, pk->parent + p0, (p1 - p0) * 8);
+  h2d(d_cb, pk->blk_cid_base + b0, nbk * 8);
+  h2d(d_c0, pk->blk_cid0 + b0, nbk * 4);
+  h2d(d_p0, pk->blk_par0 + b0, nbk * 4);
+  h2d(d_ek, e0, ne * 8);
+  h2d(d_ev, pk->esc_val + (e0 - pk->esc_key), ne * 8);
+  UnpackArgs a;
+  a.s0 = s0;
+  a.s1 = s1;
+  a.b0 = b0;
+  a.flags = flags;
+  a.dbegin = d_dbeg;
+  a.dur = d_dur;
+  a.dcid = d_dcid;
+  a.parent = d_par;
+  a.cbase = d_cb;
+  a.cid0 = d_c0;
+  a.par0 = d_p0;
+  a.cid_first = c0;
+  a.par_first = p0;
+  a.esc_key = d_ek;
+  a.esc_val = d_ev;
+  a.n_esc = (uint32_t)ne;
+  a.begin = begin;
+  a.end = end;
+  a.cid = cid;
+  a.parent_out = parent;
+  k_unpack<<<(unsigned)nbk, kPB, 0, st>>>(a);
+  ++ctx->launches;
+  return bytes;
+}
+
+}  // namespace xsp

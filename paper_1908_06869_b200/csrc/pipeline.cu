@@ -156,9 +156,13 @@ void copy_pieces(void* dst, const void* src, uint64_t bytes, cudaMemcpyKind kind
 
 // Returns false (nothing done) when the batch is too small or the groups are
 // not an ordered partition of trace ranges; the caller then runs single-shot.
+uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint64_t s1, uint8_t* flags,
+                      uint32_t* name_id, uint64_t* begin, uint64_t* end, uint64_t* cid, uint64_t* parent,
+                      const std::string& tag, cudaStream_t st);
+
 bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht, const xsp_groups* groups,
                       const xsp_system_spec* spec, const xsp_analysis_opts* opts, xsp_corr_out* corr_host,
-                      xsp_tables_out* tab_host) {
+                      xsp_tables_out* tab_host, const xsp_packed_cols* pk) {
   uint64_t target = 6000000;
   if (const char* e = std::getenv("XSP_CHUNK_SPANS")) target = std::strtoull(e, nullptr, 10);
   const uint64_t n = hc->n_spans;
@@ -291,14 +295,22 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     if (c >= 2) XSP_CUDA(cudaStreamWaitEvent(cs, S.free, 0));
     const uint64_t s0 = C.s0, ns = C.s1 - C.s0;
     // span columns first: they do not depend on the table-row counts below
-    h2d(const_cast<uint8_t*>(S.cols.flags), hc->flags + s0, ns);
-    h2d(const_cast<uint64_t*>(S.cols.begin_ns), hc->begin_ns + s0, ns * 8);
-    h2d(const_cast<uint64_t*>(S.cols.end_ns), hc->end_ns + s0, ns * 8);
-    h2d(const_cast<uint64_t*>(S.cols.cid), hc->cid + s0, ns * 8);
-    h2d(const_cast<uint64_t*>(S.cols.parent_id), hc->parent_id + s0, ns * 8);
-    h2d(const_cast<uint32_t*>(S.cols.name_id), hc->name_id + s0, ns * 4);
+    if (pk) {  // packed wire form: unpacked on the copy stream into the slot's columns
+      ctx->h2d_bytes += stage_packed(ctx, pk, s0, C.s1, const_cast<uint8_t*>(S.cols.flags),
+                                     const_cast<uint32_t*>(S.cols.name_id), const_cast<uint64_t*>(S.cols.begin_ns),
+                                     const_cast<uint64_t*>(S.cols.end_ns), const_cast<uint64_t*>(S.cols.cid),
+                                     const_cast<uint64_t*>(S.cols.parent_id), "plk" + std::to_string(c & 1) + ".",
+                                     cs);
+    } else {
+      h2d(const_cast<uint8_t*>(S.cols.flags), hc->flags + s0, ns);
+      h2d(const_cast<uint64_t*>(S.cols.begin_ns), hc->begin_ns + s0, ns * 8);
+      h2d(const_cast<uint64_t*>(S.cols.end_ns), hc->end_ns + s0, ns * 8);
+      h2d(const_cast<uint64_t*>(S.cols.cid), hc->cid + s0, ns * 8);
+      h2d(const_cast<uint64_t*>(S.cols.parent_id), hc->parent_id + s0, ns * 8);
+      h2d(const_cast<uint32_t*>(S.cols.name_id), hc->name_id + s0, ns * 4);
+    }
     uint64_t mc, lc, cp;
-    count_rows(hc->flags + s0, ns, mc, lc, cp);
+    count_rows((pk ? pk->flags : hc->flags) + s0, ns, mc, lc, cp);
     // span_id is read sparsely (model spans, timeline ties, orphans,
     // ambiguities) unless kernels carry explicit parents: read it in place
     // from page-locked host memory when possible instead of copying it

@@ -376,6 +376,40 @@ class Engine:
                                          C.byref(opts), C.byref(out), C.c_void_p(stream)))
         return out
 
+    def pack_host(self, batch: SpanBatch) -> capi.PackedCols:
+        """xsp_pack_host: the batch's span columns in the packed wire form (ctx-owned
+        pinned arrays, valid until the next pack_host on this engine)."""
+        self._pack_src = batch  # flags / name_id are referenced, not copied
+        cols, trs = batch.cols(), batch.traces()
+        pk = capi.PackedCols()
+        self._check(self.lib.xsp_pack_host(self.ctx, C.byref(cols), C.byref(trs), C.byref(pk)))
+        return pk
+
+    def run_host_packed(self, packed: capi.PackedCols, batch: SpanBatch, groups=None, trim=0.2, noise=0.01,
+                        top_k=3, raw: bool = False):
+        """xsp_run_host_packed: run_host with the span columns taken from `packed`
+        (batch supplies span_id and the metric / layer tables)."""
+        if groups is None:
+            T = batch.n_traces
+            groups = (np.arange(T), np.ones(T), batch.trace_batch)
+        g, keep = self.make_groups(*groups)
+        spec = capi.SystemSpec(batch.peak_flops, batch.mem_bw)
+        opts = self.make_opts(trim=trim, noise=noise, top_k=top_k)
+        cols, trs = batch.cols(), batch.traces()
+        co, to = capi.CorrOut(), capi.TablesOut()
+        self._check(self.lib.xsp_run_host_packed(self.ctx, C.byref(packed), C.byref(cols), C.byref(trs), C.byref(g),
+                                                 C.byref(spec), C.byref(opts), C.byref(co), C.byref(to), None))
+        if raw:
+            return co, to
+        cc = _corr_counts(co)
+        corr = CorrResult(co.n_traces, co.n_failed,
+                          {n: _copy(getattr(co, n), t, cc[k]) for n, t, k in capi.CORR_FIELDS},
+                          co.n_layers, co.n_kernels, co.n_orphans, co.n_ambiguities, co.n_candidates)
+        tc = _tab_counts(to, top_k)
+        tabs = Tables(to.n_groups, {n: _copy(getattr(to, n), t, tc[k]) for n, t, k in capi.TABLE_FIELDS},
+                      to.n_layers, to.n_kernels, to.n_names)
+        return corr, tabs
+
     def set_profiling(self, on: bool):
         self.lib.xsp_set_profiling(self.ctx, int(on))
 

@@ -1,0 +1,58 @@
+"""Packed host input (csrc/packed.cu, xsp_pack_host + xsp_run_host_packed): the
+span columns cross PCIe as u32 deltas / durations / cid offsets with sparse
+parent and cid lists and an escape list, and are rebuilt on the device. The
+results must equal xsp_run_host's bit for bit — single-shot and chunked
+pipeline, with escapes of every kind (trace / block starts, long durations,
+wide cid ranges, backward begins) — and the wire bytes must shrink."""
+import numpy as np
+import pytest
+
+from paper_1908_06869_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def same(a, b):
+    for k in b.cols:
+        x, y = np.asarray(a.cols[k]), np.asarray(b.cols[k])
+        assert x.shape == y.shape and np.array_equal(x.view(np.uint8), y.view(np.uint8)), k
+
+
+def run_both(engine, b, groups, chunk=None, monkeypatch=None):
+    if chunk is not None:
+        monkeypatch.setenv("XSP_CHUNK_SPANS", str(chunk))
+    c0, t0 = engine.run_host(b, groups=groups)
+    h0, _ = engine.transfer_bytes()
+    pk = engine.pack_host(b)
+    c1, t1 = engine.run_host_packed(pk, b, groups=groups)
+    h1, _ = engine.transfer_bytes()
+    same(c1, c0)
+    same(t1, t0)
+    return h0, h1
+
+
+@pytest.mark.parametrize("chunk", [None, 50_000])
+def test_packed_equals_dense_c3(engine, monkeypatch, chunk):
+    b, gf, gr, gb = synth.c3(runs=3, n_models=6, max_layers=400)
+    h0, h1 = run_both(engine, b, (gf, gr, gb), chunk if chunk else 0, monkeypatch)
+    assert h1 < 0.8 * h0, (h0, h1)
+
+
+def test_packed_escapes(engine, monkeypatch):
+    """Long durations, cids far apart, backward begins inside a trace (an
+    out-of-order bundle is rejected the same way by both paths)."""
+    from oracle import ref
+    g = ref.Generator()
+    for r in range(4):
+        g.emit("resnet-like", batch=2, run_index=r, jitter_max=2000, jitter_seed=r + 3)
+    g.random_nested(5, 2500).random_async(6, 300)
+    b = g.batch()
+    # cids spread over 2^40 within blocks; a few layers last > 2^32 ns
+    has = (b.flags & 0x20) != 0
+    b.cid = np.where(has, b.cid * np.uint64(1 << 20) + np.uint64(7), b.cid).astype(np.uint64)
+    lay = np.nonzero((b.flags & 3) == 1)[0][::17]
+    b.end_ns = b.end_ns.copy()
+    b.end_ns[lay] += np.uint64(5 << 32)
+    T = b.n_traces
+    run_both(engine, b, (np.arange(T), np.ones(T), b.trace_batch), 0, monkeypatch)
+    run_both(engine, b, (np.arange(T), np.ones(T), b.trace_batch), 3000, monkeypatch)
