@@ -255,6 +255,42 @@ def measure_sort(eng, dev, b, steps: int, local: int):
             "input": "C3 corpus, rows of every trace permuted at random on the device"}
 
 
+def measure_validate(eng, dev, b, steps: int):
+    """validate_bundle (stage (a), span.cpp:129-192) of every C3 trace on the
+    device (xsp_validate: per-span rules, timeline order, duplicate span ids by
+    a device hash table, bundle-level rules): CUDA events around `steps` calls.
+    Algorithmic bytes: span_id, begin, end, cid (32 B) + flags (1 B) per span
+    + the metric table (32 B per metric row)."""
+    import ctypes as C
+    import torch
+    from paper_1908_06869_b200 import _capi as capi
+    cols, trs = dev.cols(), dev.traces()
+    vin = capi.ValidateIn()
+    out = capi.ValidationOut()
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def call():
+        eng._check(eng.lib.xsp_validate(eng.ctx, C.byref(cols), C.byref(trs), C.byref(vin), C.byref(out),
+                                        C.c_void_p(stream)))
+
+    call()
+    assert out.n_issues == 0
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        call()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    met = int(((b.flags & 0x40) != 0).sum())
+    byts = 33 * b.n_spans + 32 * met
+    return {"metric": "M spans/s validated (validate_bundle, device-resident)", "value": b.n_spans / (ms / 1e3) / 1e6,
+            "unit": UNIT, "ms_per_step": ms, "issues": int(out.n_issues),
+            "roofline": {"bound": "hbm", "bytes": byts, "achieved": byts / (ms / 1e3) / 1e9, "unit": "GB/s"},
+            "input": "C3 corpus (every trace valid)"}
+
+
 def measure_c4(eng, args, rank: int, world: int, local: int, dist):
     """BASELINE config 4: one long trace (synth.c4, no quiescent instants),
     time-range sharded over the ranks with a carried open-parent boundary
@@ -697,6 +733,7 @@ def main():
                "stages_ms": {k: v[0] / max(v[1], 1) for k, v in c3_stages.items()}}
     c3_line["roofline"]["frac"] = c3_line["roofline"]["achieved"] / peak
     sort_line = measure_sort(eng, dev, b, args.steps, local) if not args.no_sort else None
+    val_line = measure_validate(eng, dev, b, max(2, args.steps // 4)) if not args.no_sort else None
 
     if args.c5_copies <= 0:  # quick iteration: the C3 line alone
         if rank == 0:
@@ -771,6 +808,10 @@ def main():
                                  "definition": "read begin_ns+flags+span_id (17 B), write perm (4 B) per span"}
         sort_line["roofline"]["frac"] = sort_line["roofline"]["achieved"] / peak
         line["sort_shuffled"] = sort_line
+    if val_line:
+        val_line["roofline"]["peak"] = peak
+        val_line["roofline"]["frac"] = val_line["roofline"]["achieved"] / peak
+        line["validate"] = val_line
     if c4_line:
         line["c4"] = c4_line
     if lev_line:

@@ -386,6 +386,64 @@ __global__ void __launch_bounds__(256) k_kernels_r1(LayerArgs a, uint32_t total_
   a.k_in[q] = (ro.bound >= 0 && klat > 0.0) ? 1 : 0;  // classify (analysis.cpp:59-71)
 }
 
+// a11-a14 row of layer q (group-local index li, correlation layer gl0) from its
+// Accumulator (analysis.cpp:173-211, 458-494) and top-k
+__device__ __forceinline__ void layer_row_out(const LayerArgs& a, uint32_t q, uint32_t li, uint32_t gl0,
+                                              double layer_lat, uint32_t nk, double acc_lat, double acc_occw,
+                                              uint64_t acc_f, uint64_t acc_r, uint64_t acc_w,
+                                              const uint32_t* top_idx, uint32_t ntop) {
+  const uint32_t K = a.top_k;
+  if (a.l_occw) a.l_occw[q] = acc_occw;
+  const uint32_t lo_out = q;
+  if (a.layer_attr_row && a.type_id && a.alloc_bytes) {
+    const uint32_t ar = a.layer_attr_row[gl0];
+    a.l_type[lo_out] = a.type_id[ar];
+    a.l_alloc[lo_out] = (uint64_t)a.alloc_bytes[ar];
+  } else {  // no layer table: every layer of type 0, no allocations
+    a.l_type[lo_out] = 0;
+    a.l_alloc[lo_out] = 0;
+  }
+  const Roof ro = roofline(acc_f, acc_r, acc_w, acc_lat, a.peak, a.bw);
+  a.l_index[lo_out] = li;
+  a.l_row[lo_out] = a.layer_row[gl0];
+  a.l_layer_lat[lo_out] = layer_lat;
+  a.l_kern_lat[lo_out] = acc_lat;
+  a.l_flops[lo_out] = acc_f;
+  a.l_read[lo_out] = acc_r;
+  a.l_write[lo_out] = acc_w;
+  a.l_occ[lo_out] = acc_lat > 0.0 ? acc_occw / acc_lat : 0.0;
+  a.l_count[lo_out] = nk;
+  a.l_ai[lo_out] = ro.ai;
+  a.l_tput[lo_out] = ro.tput;
+  a.l_bound[lo_out] = ro.bound;
+  a.l_in[lo_out] = (ro.bound >= 0 && acc_lat > 0.0) ? 1 : 0;
+  // a13 (analysis.cpp:484-494)
+  const double nongpu = __dsub_rn(layer_lat, acc_lat);
+  a.l_nongpu[lo_out] = nongpu;
+  a.l_gpu_share[lo_out] = layer_lat > 0.0 ? acc_lat / layer_lat : 0.0;
+  a.l_nongpu_share[lo_out] = layer_lat > 0.0 ? nongpu / layer_lat : 0.0;
+  a.l_flagged[lo_out] = nongpu < -(__dmul_rn(a.noise, layer_lat)) ? 1 : 0;
+  for (uint32_t s = 0; s < K; ++s) a.l_topk[(uint64_t)lo_out * K + s] = s < ntop ? top_idx[s] : kNone;
+}
+
+// top-k insertion: latency desc, ordinal asc
+__device__ __forceinline__ void topk_push(uint32_t K, double klat, uint32_t ord, uint32_t* top_idx, double* top_lat,
+                                          uint32_t& ntop) {
+  if (!K) return;
+  uint32_t pos = ntop;
+  while (pos > 0 && top_lat[pos - 1] < klat) --pos;
+  if (pos < K) {
+    const uint32_t last = ntop < K ? ntop : K - 1;
+    for (uint32_t s = last; s > pos; --s) {
+      top_lat[s] = top_lat[s - 1];
+      top_idx[s] = top_idx[s - 1];
+    }
+    top_lat[pos] = klat;
+    top_idx[pos] = ord;
+    if (ntop < K) ++ntop;
+  }
+}
+
 // Per (group, layer): combine() layer latency (:135-144), the Accumulator over
 // the layer's kernels in tree order (:173-211), a11-a14 rows and top-k.
 // kOneRun: every group has one run (a long single trace), so the layer latency
@@ -430,53 +488,9 @@ __global__ void __launch_bounds__(256, kOneRun ? 4 : 3) k_layers(LayerArgs a) {
     acc_r += rd;
     acc_w += wr;
     acc_occw = __dadd_rn(acc_occw, __dmul_rn(kocc, klat));
-    // top-k by latency desc, ordinal asc
-    if (K) {
-      uint32_t pos = ntop;
-      while (pos > 0 && top_lat[pos - 1] < klat) --pos;
-      if (pos < K) {
-        const uint32_t last = ntop < K ? ntop : K - 1;
-        for (uint32_t s = last; s > pos; --s) {
-          top_lat[s] = top_lat[s - 1];
-          top_idx[s] = top_idx[s - 1];
-        }
-        top_lat[pos] = klat;
-        top_idx[pos] = x - a.gk_off[g];
-        if (ntop < K) ++ntop;
-      }
-    }
+    topk_push(K, klat, x - a.gk_off[g], top_idx, top_lat, ntop);
   }
-  if (a.l_occw) a.l_occw[q] = acc_occw;
-  const uint32_t lo_out = q;
-  if (a.layer_attr_row && a.type_id && a.alloc_bytes) {
-    const uint32_t ar = a.layer_attr_row[gl0];
-    a.l_type[lo_out] = a.type_id[ar];
-    a.l_alloc[lo_out] = (uint64_t)a.alloc_bytes[ar];
-  } else {  // no layer table: every layer of type 0, no allocations
-    a.l_type[lo_out] = 0;
-    a.l_alloc[lo_out] = 0;
-  }
-  const Roof ro = roofline(acc_f, acc_r, acc_w, acc_lat, a.peak, a.bw);
-  a.l_index[lo_out] = li;
-  a.l_row[lo_out] = a.layer_row[gl0];
-  a.l_layer_lat[lo_out] = layer_lat;
-  a.l_kern_lat[lo_out] = acc_lat;
-  a.l_flops[lo_out] = acc_f;
-  a.l_read[lo_out] = acc_r;
-  a.l_write[lo_out] = acc_w;
-  a.l_occ[lo_out] = acc_lat > 0.0 ? acc_occw / acc_lat : 0.0;
-  a.l_count[lo_out] = ke - kb;
-  a.l_ai[lo_out] = ro.ai;
-  a.l_tput[lo_out] = ro.tput;
-  a.l_bound[lo_out] = ro.bound;
-  a.l_in[lo_out] = (ro.bound >= 0 && acc_lat > 0.0) ? 1 : 0;
-  // a13 (analysis.cpp:484-494)
-  const double nongpu = __dsub_rn(layer_lat, acc_lat);
-  a.l_nongpu[lo_out] = nongpu;
-  a.l_gpu_share[lo_out] = layer_lat > 0.0 ? acc_lat / layer_lat : 0.0;
-  a.l_nongpu_share[lo_out] = layer_lat > 0.0 ? nongpu / layer_lat : 0.0;
-  a.l_flagged[lo_out] = nongpu < -(__dmul_rn(a.noise, layer_lat)) ? 1 : 0;
-  for (uint32_t s = 0; s < K; ++s) a.l_topk[(uint64_t)lo_out * K + s] = s < ntop ? top_idx[s] : kNone;
+  layer_row_out(a, q, li, gl0, layer_lat, ke - kb, acc_lat, acc_occw, acc_f, acc_r, acc_w, top_idx, ntop);
 }
 
 struct ModelArgs {
@@ -721,18 +735,22 @@ struct BigChunkArgs {
   uint32_t c0;     // first chunk of this launch
 };
 
-__global__ void k_big_chunks(BigChunkArgs a) {
-  const uint32_t c = a.c0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31u;
+// One CTA (kBigThreads) per chunk: thread-strided partial sums, then a fixed
+// reduction order (xor-butterfly in each warp, warps in order) — the chunk sums
+// are re-associated at chunk boundaries anyway (integer latencies stay exact).
+constexpr int kBigThreads = 256;
+__global__ void __launch_bounds__(kBigThreads) k_big_chunks(BigChunkArgs a) {
+  __shared__ double s_s[kBigThreads / 32], s_so[kBigThreads / 32];
+  __shared__ unsigned long long s_c[3][kBigThreads / 32];
+  const uint32_t c = a.c0 + blockIdx.x, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   if (c >= a.n) return;
   const uint32_t b = a.desc[3 * c], e = a.desc[3 * c + 1], kind = a.desc[3 * c + 2];
   const double* v = kind == 0 ? a.k_lat : a.l_kern_lat;
   double s = 0.0, so = 0.0;
   uint64_t f = 0, r = 0, w = 0;
-  // lane-strided partial sums and a fixed xor-butterfly: the chunk sums are
-  // re-associated at chunk boundaries anyway (integer latencies stay exact)
   if (kind == 0) {
 #pragma unroll 4
-    for (uint32_t x = b + lane; x < e; x += 32) {
+    for (uint32_t x = b + threadIdx.x; x < e; x += kBigThreads) {
       const double l = v[x];
       s = __dadd_rn(s, l);
       f += a.k_flops[x];
@@ -742,7 +760,7 @@ __global__ void k_big_chunks(BigChunkArgs a) {
     }
   } else if (a.l_occw) {
 #pragma unroll 4
-    for (uint32_t x = b + lane; x < e; x += 32) {
+    for (uint32_t x = b + threadIdx.x; x < e; x += kBigThreads) {
       s = __dadd_rn(s, v[x]);
       so = __dadd_rn(so, a.l_occw[x]);
       f += a.l_flops[x];
@@ -751,7 +769,7 @@ __global__ void k_big_chunks(BigChunkArgs a) {
     }
   } else {
 #pragma unroll 4
-    for (uint32_t x = b + lane; x < e; x += 32) s = __dadd_rn(s, v[x]);
+    for (uint32_t x = b + threadIdx.x; x < e; x += kBigThreads) s = __dadd_rn(s, v[x]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -762,11 +780,28 @@ __global__ void k_big_chunks(BigChunkArgs a) {
   r = warp_sum_u64(r);
   w = warp_sum_u64(w);
   if (lane == 0) {
-    a.p_lat[c] = s;
-    a.p_occw[c] = so;
-    a.p_cnt[3 * c] = f;
-    a.p_cnt[3 * c + 1] = r;
-    a.p_cnt[3 * c + 2] = w;
+    s_s[warp] = s;
+    s_so[warp] = so;
+    s_c[0][warp] = f;
+    s_c[1][warp] = r;
+    s_c[2][warp] = w;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ts = 0.0, tso = 0.0;
+    uint64_t tf = 0, tr = 0, tw = 0;
+    for (int q = 0; q < kBigThreads / 32; ++q) {
+      ts = __dadd_rn(ts, s_s[q]);
+      tso = __dadd_rn(tso, s_so[q]);
+      tf += s_c[0][q];
+      tr += s_c[1][q];
+      tw += s_c[2][q];
+    }
+    a.p_lat[c] = ts;
+    a.p_occw[c] = tso;
+    a.p_cnt[3 * c] = tf;
+    a.p_cnt[3 * c + 1] = tr;
+    a.p_cnt[3 * c + 2] = tw;
   }
 }
 
@@ -1973,7 +2008,8 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     bc.l_write = la.l_write;
     // one-run: only the layer chunks are folded (they carry the kernel sums)
     bc.c0 = all_one_run ? nkc : 0;
-    launch(ctx, k_big_chunks, (uint64_t)(n_chunks - bc.c0) * 32, st, bc);
+    k_big_chunks<<<n_chunks - bc.c0, kBigThreads, 0, st>>>(bc);
+    ++ctx->launches;
     ma.pk_lat = p_lat;
     ma.pk_occw = p_occw;
     ma.pl_gpu = p_lat;

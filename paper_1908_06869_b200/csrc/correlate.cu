@@ -1576,11 +1576,19 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
   uint32_t t = __shfl_sync(0xffffffffu, t0, 0);
   uint32_t tl = kNone;
   uint64_t mn = ~0ull, mx = 0;
+  // a trace already known to be slow needs no alignment check (one L2 read per
+  // trace change, not per entry)
+  uint32_t tslow = kNone;
+  bool slow = false;
 #pragma unroll 1
   for (uint32_t i = 0; i < JC_ITEMS; ++i) {
     const uint32_t k = wbase + i * 32 + lane;
     if (k >= nkl) break;
     while (t + 1 < T && __ldg(t_kl_off + t + 1) <= k) ++t;
+    if (t != tslow) {
+      tslow = t;
+      slow = *((volatile uint32_t*)(t_slow + t)) != 0;
+    }
     const uint32_t r = k - t_kl_off[t];
     const KlEnt ent = kl[k];
     const uint8_t f = flags[ent.row];
@@ -1601,9 +1609,10 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
     }
     // only the first mismatch of a trace stores (a reordered long trace would
     // otherwise have every launch store to the same two words)
-    if (!*((volatile uint32_t*)(t_slow + t)) && !(mono && cid[ex[t_ex_off[t] + r].row] == ent.cid)) {
+    if (!slow && !(mono && cid[ex[t_ex_off[t] + r].row] == ent.cid)) {
       t_slow[t] = 1;
       *any_slow = 1;
+      slow = true;
     }
   }
   __syncwarp();
