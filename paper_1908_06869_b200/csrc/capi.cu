@@ -14,7 +14,7 @@ namespace xsp {
 void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_packed_cols* out);
 uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint64_t s1, uint8_t* flags,
                       uint32_t* name_id, uint64_t* begin, uint64_t* end, uint64_t* cid, uint64_t* parent,
-                      const std::string& tag, cudaStream_t st);
+                      const std::string& tag, cudaStream_t st, void* deferred = nullptr);
 bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht, const xsp_groups* groups,
                       const xsp_system_spec* spec, const xsp_analysis_opts* opts, xsp_corr_out* corr_host,
                       xsp_tables_out* tab_host,

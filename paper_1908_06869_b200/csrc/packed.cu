@@ -211,12 +211,26 @@ __global__ void __launch_bounds__(kPB) k_unpack(UnpackArgs a) {
   a.parent_out[r] = (f & XSP_F_PARENT) ? a.parent[pbefore + pp] : 0;
 }
 
+void launch_unpack(xsp_ctx* ctx, const void* args, cudaStream_t st) {
+  const UnpackArgs& a = *static_cast<const UnpackArgs*>(args);
+  const uint64_t nbk = (a.s1 + kPB - 1) / kPB - a.b0;
+  if (a.s1 > a.s0) {
+    k_unpack<<<(unsigned)nbk, kPB, 0, st>>>(a);
+    ++ctx->launches;
+  }
+}
+
+size_t unpack_args_bytes() { return sizeof(UnpackArgs); }
+
 // Stages rows [s0, s1) of a packed batch on stream st into the device columns
 // of `dst` (begin / end / cid / parent_id rebuilt; flags and name_id copied),
-// using `tag`-named staging buffers. Returns the H2D bytes issued.
+// using `tag`-named staging buffers. Returns the H2D bytes issued. With
+// `deferred` the unpack kernel is not launched: its arguments are stored there
+// for launch_unpack on the stream that consumes the columns (so the copy
+// stream carries copies only and never waits for SMs).
 uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint64_t s1, uint8_t* flags,
                       uint32_t* name_id, uint64_t* begin, uint64_t* end, uint64_t* cid, uint64_t* parent,
-                      const std::string& tag, cudaStream_t st) {
+                      const std::string& tag, cudaStream_t st, void* deferred) {
   const uint64_t ns = s1 - s0;
   if (!ns) return 0;
   uint64_t bytes = 0;
@@ -280,8 +294,12 @@ uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint
   a.end = end;
   a.cid = cid;
   a.parent_out = parent;
-  k_unpack<<<(unsigned)nbk, kPB, 0, st>>>(a);
-  ++ctx->launches;
+  if (deferred) {
+    std::memcpy(deferred, &a, sizeof(a));
+  } else {
+    k_unpack<<<(unsigned)nbk, kPB, 0, st>>>(a);
+    ++ctx->launches;
+  }
   return bytes;
 }
 

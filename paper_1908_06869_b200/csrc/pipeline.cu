@@ -158,7 +158,9 @@ void copy_pieces(void* dst, const void* src, uint64_t bytes, cudaMemcpyKind kind
 // not an ordered partition of trace ranges; the caller then runs single-shot.
 uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint64_t s1, uint8_t* flags,
                       uint32_t* name_id, uint64_t* begin, uint64_t* end, uint64_t* cid, uint64_t* parent,
-                      const std::string& tag, cudaStream_t st);
+                      const std::string& tag, cudaStream_t st, void* deferred);
+void launch_unpack(xsp_ctx* ctx, const void* args, cudaStream_t st);
+size_t unpack_args_bytes();
 
 bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht, const xsp_groups* groups,
                       const xsp_system_spec* spec, const xsp_analysis_opts* opts, xsp_corr_out* corr_host,
@@ -210,6 +212,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     ch.push_back(c);
   }
   if (ch.size() < 2) return false;
+  if (unpack_args_bytes() > 256) throw std::logic_error("UnpackArgs outgrew its slot");
   uint64_t max_n = 0;
   uint32_t max_t = 0;
   for (auto& c : ch) {
@@ -241,6 +244,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     xsp_traces tr;
     uint64_t* h_off;  // pinned staging of the re-based trace offsets
     uint64_t* sid_buf;  // device span_id column (unused while span_id is read zero-copy)
+    alignas(16) unsigned char unpack[256];  // deferred k_unpack arguments (packed input)
     cudaEvent_t in_ready, free;
     cudaEvent_t computed, out_done;  // this parity's ctx buffers: results ready / copied out
   } slot[2];
@@ -300,7 +304,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
                                      const_cast<uint32_t*>(S.cols.name_id), const_cast<uint64_t*>(S.cols.begin_ns),
                                      const_cast<uint64_t*>(S.cols.end_ns), const_cast<uint64_t*>(S.cols.cid),
                                      const_cast<uint64_t*>(S.cols.parent_id), "plk" + std::to_string(c & 1) + ".",
-                                     cs);
+                                     cs, S.unpack);
     } else {
       h2d(const_cast<uint8_t*>(S.cols.flags), hc->flags + s0, ns);
       h2d(const_cast<uint64_t*>(S.cols.begin_ns), hc->begin_ns + s0, ns * 8);
@@ -395,6 +399,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     XSP_CUDA(cudaStreamWaitEvent(ws, S.in_ready, 0));
     // this parity's ctx buffers are free once chunk c-2's results are copied out
     if (c >= 2) XSP_CUDA(cudaStreamWaitEvent(ws, S.out_done, 0));
+    if (pk) launch_unpack(ctx, S.unpack, ws);  // packed input: rebuild the span columns first
     ctx->tag = (c & 1) ? "#p1" : "#p0";
     xsp_corr_out dcorr;
     std::memset(&dcorr, 0, sizeof(dcorr));
