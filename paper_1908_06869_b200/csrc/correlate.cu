@@ -1566,7 +1566,7 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
                              const uint8_t* __restrict__ flags, const uint32_t* __restrict__ t_kl_off,
                              const uint32_t* __restrict__ t_ex_off, uint32_t T, uint32_t* __restrict__ t_slow,
                              uint32_t* __restrict__ any_slow, unsigned long long* __restrict__ t_lmin,
-                             unsigned long long* __restrict__ t_lmax) {
+                             unsigned long long* __restrict__ t_lmax, uint32_t* __restrict__ t_nonmono) {
   const uint32_t lane = lane_id();
   const uint64_t wbase64 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32ull * JC_ITEMS;
   if (wbase64 >= nkl) return;
@@ -1578,22 +1578,42 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
   uint64_t mn = ~0ull, mx = 0;
   // a trace already known to be slow needs no alignment check (one L2 read per
   // trace change, not per entry)
-  uint32_t tslow = kNone;
+  uint32_t tslow = kNone, tnm = kNone;
   bool slow = false;
-#pragma unroll 1
+  // all of the lane's entries and their flag bytes are loaded up front (the
+  // loads of an entry no longer wait for the previous entry's checks)
+  KlEnt e[JC_ITEMS];
+  uint8_t fb[JC_ITEMS];
+#pragma unroll
   for (uint32_t i = 0; i < JC_ITEMS; ++i) {
     const uint32_t k = wbase + i * 32 + lane;
-    if (k >= nkl) break;
+    if (k < nkl) e[i] = kl[k];
+    else e[i] = KlEnt{0, 0, 0};
+  }
+#pragma unroll
+  for (uint32_t i = 0; i < JC_ITEMS; ++i) {
+    const uint32_t k = wbase + i * 32 + lane;
+    fb[i] = k < nkl ? flags[e[i].row] : (uint8_t)0;
+  }
+  uint64_t prev_last = (wbase > 0 && lane == 0) ? kl[wbase - 1].cid : 0;  // entry before the warp's first
+#pragma unroll
+  for (uint32_t i = 0; i < JC_ITEMS; ++i) {
+    const uint32_t k = wbase + i * 32 + lane;
+    // the previous entry's cid: the lane below, or lane 31 of the previous item
+    uint64_t pc = __shfl_up_sync(0xffffffffu, e[i].cid, 1);
+    const uint64_t last = __shfl_sync(0xffffffffu, i == 0 ? prev_last : e[i - (i > 0)].cid, i == 0 ? 0 : 31);
+    if (lane == 0) pc = last;
+    if (k >= nkl) continue;
     while (t + 1 < T && __ldg(t_kl_off + t + 1) <= k) ++t;
     if (t != tslow) {
       tslow = t;
       slow = *((volatile uint32_t*)(t_slow + t)) != 0;
     }
     const uint32_t r = k - t_kl_off[t];
-    const KlEnt ent = kl[k];
-    const uint8_t f = flags[ent.row];
+    const KlEnt ent = e[i];
+    const uint8_t f = fb[i];
     const bool launch = f_kind(f) == XSP_KIND_LAUNCH && (f & XSP_F_CID);
-    const bool mono = launch && (r == 0 || kl[k - 1].cid < ent.cid);
+    const bool mono = launch && (r == 0 || pc < ent.cid);
     if (launch) {
       if (tl != t) {
         if (tl != kNone) {
@@ -1609,6 +1629,10 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
     }
     // only the first mismatch of a trace stores (a reordered long trace would
     // otherwise have every launch store to the same two words)
+    if (!mono && t != tnm) {  // once per trace per thread
+      t_nonmono[t] = 1;
+      tnm = t;
+    }
     if (!slow && !(mono && cid[ex[t_ex_off[t] + r].row] == ent.cid)) {
       t_slow[t] = 1;
       *any_slow = 1;
@@ -1661,13 +1685,20 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
   return (uint32_t)x;
 }
 
+// A direct-address trace is "dense" when its kernel-list entries are all cid
+// launches with strictly increasing cids covering the range without gaps: the
+// r-th launch owns slot r, so launches need no insert, no duplicate check and
+// no leftover pass (every in-range execution has its launch).
 __global__ void k_region_size(const uint32_t* __restrict__ t_kl_off, const uint32_t* __restrict__ t_ex_off,
                               const uint32_t* __restrict__ t_slow, const uint64_t* __restrict__ t_lmin,
-                              const uint64_t* __restrict__ t_lmax, uint32_t T, uint64_t* __restrict__ rsize) {
+                              const uint64_t* __restrict__ t_lmax, uint32_t T, uint64_t* __restrict__ rsize,
+                              const uint32_t* __restrict__ t_nonmono, uint32_t* __restrict__ t_dense) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
+  t_dense[t] = 0;
   if (t_lmin[t] != ~0ull) {  // direct-address region: one slot per cid of the launch range
     rsize[t] = t_lmax[t] - t_lmin[t] + 1;
+    t_dense[t] = !t_nonmono[t] && rsize[t] == (uint64_t)(t_kl_off[t + 1] - t_kl_off[t]);
     return;
   }
   uint64_t items = (uint64_t)(t_kl_off[t + 1] - t_kl_off[t]) + (t_ex_off[t + 1] - t_ex_off[t]);
@@ -1694,6 +1725,7 @@ struct JoinArgs {
   uint32_t* ex_slot;
   uint32_t* kl_slot;
   uint32_t* t_dup;       // bit0 exec dup, bit1 launch dup
+  const uint32_t* t_dense;  // dense direct-address traces (k_region_size)
 };
 
 // Items 0..n_ex-1 are execs, n_ex..n_ex+n_kl-1 kernel-list entries (launches
@@ -1711,7 +1743,7 @@ __global__ void k_join_insert(JoinArgs a) {
   } else {
     uint32_t k = it - a.n_ex;
     t = trace_of32(a.t_kl_off, a.T, k);
-    if (!a.t_slow[t]) return;
+    if (!a.t_slow[t] || a.t_dense[t]) return;  // dense: launch r owns slot r (no insert)
     const uint8_t f = a.flags[a.kl[k].row];
     if (!is_kernel_launch(f) || !(f & XSP_F_CID)) return;
     cid = a.kl[k].cid;
@@ -1786,6 +1818,8 @@ struct FuseArgs {
   Orphans orph;
   bool any_slow;
   bool parents_only;  // assign_parents without correlate_async
+  const uint32_t* t_dense;  // dense direct-address traces: slot of launch k = roff[t] + (k - t_kl_off[t])
+  const uint64_t* roff;
   uint32_t* drop;     // [0] entries not kept, [1] kept parents not in timeline order
 };
 
@@ -1805,7 +1839,10 @@ __global__ void k_fuse(FuseArgs a) {
     } else if (!(f & XSP_F_CID)) {
       emit_orphan(a.orph, t, CAT_LAUNCH, ((uint64_t)ent.parent << 32) | k, ent.row, XSP_O_LAUNCH_NO_CID);
     } else {
-      x = (a.any_slow && a.t_slow[t]) ? a.sl_exec[a.kl_slot[k]] : a.t_ex_off[t] + (k - a.t_kl_off[t]);
+      if (a.any_slow && a.t_slow[t])
+        x = a.sl_exec[a.t_dense[t] ? (uint32_t)(a.roff[t] + (k - a.t_kl_off[t])) : a.kl_slot[k]];
+      else
+        x = a.t_ex_off[t] + (k - a.t_kl_off[t]);
       if (x != kNone) {
         keep = 1;
       } else {
@@ -1823,7 +1860,7 @@ __global__ void k_leftover(FuseArgs a) {
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= a.n_ex) return;
   const uint32_t t = trace_of32(a.t_ex_off, a.T, x);
-  if (!a.t_slow[t]) return;  // merge-aligned traces consume every exec
+  if (!a.t_slow[t] || a.t_dense[t]) return;  // merge-aligned / dense traces consume every exec
   if (a.sl_launch[a.ex_slot[x]] == kNone) {
     const uint32_t r = a.ex[x].row;
     emit_orphan(a.orph, t, CAT_LEFTOVER, a.sid[r], r, XSP_O_EXEC_NO_LAUNCH);
@@ -2530,6 +2567,8 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   j.t_ex_off = a.t_ex_off;
   j.t_kl_off = a.t_kl_off;
   uint32_t* t_slow = ctx->d<uint32_t>("c.t_slow", T + 1);
+  uint32_t* t_nonmono = ctx->d<uint32_t>("c.t_nonmono", T + 1);
+  uint32_t* t_dense = ctx->d<uint32_t>("c.t_dense", T + 1);
   uint64_t* t_lmin = ctx->d<uint64_t>("c.t_lmin", T + 1);
   uint64_t* t_lmax = ctx->d<uint64_t>("c.t_lmax", T + 1);
   j.t_slow = t_slow;
@@ -2540,10 +2579,11 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   if (!parents_only) {
     XSP_CUDA(cudaMemsetAsync(t_lmin, 0xFF, (T + 1) * 8ull, st));
     XSP_CUDA(cudaMemsetAsync(t_lmax, 0, (T + 1) * 8ull, st));
+    XSP_CUDA(cudaMemsetAsync(t_nonmono, 0, (T + 1) * 4ull, st));
     launch(ctx, k_join_counts, T, st, a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7);
     launch(ctx, k_join_check, ceil_div((uint64_t)nkl, JC_ITEMS), st, nkl, a.kl, a.ex, c->cid, c->flags,
            a.t_kl_off, a.t_ex_off, T, t_slow, counters + 7, reinterpret_cast<unsigned long long*>(t_lmin),
-           reinterpret_cast<unsigned long long*>(t_lmax));
+           reinterpret_cast<unsigned long long*>(t_lmax), t_nonmono);
     any_slow = read_u32(ctx, counters + 7, st);
   }
   auto* dup_ex = ctx->d<unsigned long long>("c.dup_ex", T);
@@ -2552,9 +2592,10 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   XSP_CUDA(cudaMemsetAsync(dup_kl, 0xFF, T * 8ull, st));
   j.ex_slot = ctx->d<uint32_t>("c.ex_slot", nex + 1);
   j.kl_slot = ctx->d<uint32_t>("c.kl_slot", nkl + 1);
+  uint64_t* roff = nullptr;
   if (any_slow) {
     uint64_t* rsize = ctx->d<uint64_t>("c.rsize", T + 1);
-    uint64_t* roff = ctx->d<uint64_t>("c.roff", T + 1);
+    roff = ctx->d<uint64_t>("c.roff", T + 1);
     if (getenv("XSP_JOIN_HASH")) {
       XSP_CUDA(cudaMemsetAsync(t_lmin, 0xFF, (T + 1) * 8ull, st));
     } else {
@@ -2562,7 +2603,8 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
       launch(ctx, k_join_far, nex, st, nex, a.ex, c->cid, a.t_ex_off, T, t_lmin, t_lmax);
     }
     j.t_lmin = t_lmin;
-    launch(ctx, k_region_size, T, st, a.t_kl_off, a.t_ex_off, t_slow, t_lmin, t_lmax, T, rsize);
+    launch(ctx, k_region_size, T, st, a.t_kl_off, a.t_ex_off, t_slow, t_lmin, t_lmax, T, rsize, t_nonmono,
+           t_dense);
     uint64_t* scan64 = ctx->d<uint64_t>("c.scan64", scan_scratch_elems(T + 1));
     exclusive_scan<uint64_t, uint64_t>(rsize, roff, T, scan64, roff + T, st, &ctx->launches);
     uint64_t* hroff = ctx->h<uint64_t>("c.roff_h", 1);
@@ -2574,6 +2616,7 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     j.sl_exec = ctx->d<uint32_t>("c.sl_exec", nslots);
     j.sl_launch = ctx->d<uint32_t>("c.sl_launch", nslots);
     j.t_dup = ctx->d<uint32_t>("c.t_dup", T);
+    j.t_dense = t_dense;
     XSP_CUDA(cudaMemsetAsync(j.owner, 0, nslots * 4, st));
     XSP_CUDA(cudaMemsetAsync(j.sl_exec, 0xFF, nslots * 4, st));
     XSP_CUDA(cudaMemsetAsync(j.sl_launch, 0xFF, nslots * 4, st));
@@ -2595,6 +2638,8 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   fa.ex = a.ex;
   fa.flags = c->flags;
   fa.t_slow = t_slow;
+  fa.t_dense = t_dense;
+  fa.roff = roff;
   fa.kl_slot = j.kl_slot;
   fa.sl_exec = j.sl_exec;
   fa.sl_launch = j.sl_launch;

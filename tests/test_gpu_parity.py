@@ -250,12 +250,16 @@ def test_cid_join_direct_and_hash_regions(engine, has_ref, monkeypatch):
         _async_trace(n, sparse, shuffled),                           # range too wide -> hash
         _async_trace(n, dense[::-1].copy(), shuffled),               # decreasing launch cids -> hash
         _async_trace(n, dense, np.arange(n)),                        # merge-aligned fast path
+        _async_trace(n, dense, shuffled[:-3]),                       # dense, launches without execs
+        _async_trace(n, np.arange(1000, 1000 + 2 * n, 2), shuffled),  # direct with gaps (not dense)
+        _async_trace(n, dense, shuffled, extra=[1000 + n - 1]),      # dense, duplicate of the last cid
     ]
     b = batch_of(traces)
     corr, _ = engine.run_host(b)
     ra, rs = ref.correlate(b)
     compare_correlation(b, corr, ra, rs)
     assert list(corr.trace_status)[:4] == [0, 4, 0, 4]
+    assert list(corr.trace_status)[7:] == [0, 0, 4]
     monkeypatch.setenv("XSP_JOIN_HASH", "1")
     c2, _ = engine.run_host(b)
     for k in corr.cols:
