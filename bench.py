@@ -737,7 +737,7 @@ def main():
 
     if args.c5_copies <= 0:  # quick iteration: the C3 line alone
         if rank == 0:
-            print(json.dumps({"c3": c3_line, "sort_shuffled": sort_line}))
+            print(json.dumps({"c3": c3_line, "sort_shuffled": sort_line, "validate": val_line}))
         if dist:
             dist.destroy_process_group()
         return

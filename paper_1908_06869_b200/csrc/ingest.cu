@@ -24,7 +24,10 @@
 // such stream: the caller runs the reference-exact host parser (the C++
 // drop-in's strata::ingest) for the error text or the result.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -810,6 +813,15 @@ struct IngestHost {
 void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uint32_t S, xsp_ingest_out* out,
                       cudaStream_t st) {
   static thread_local IngestHost H;  // one result per thread (pointers valid until the next call)
+  // XSP_INGEST_TRACE=1: host wall time at the phase boundaries (after syncs)
+  const bool trace = std::getenv("XSP_INGEST_TRACE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    XSP_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "ingest %-10s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+  };
   std::memset(out, 0, sizeof(*out));
   out->status = XSP_INGEST_HOST;
   out->bad_stream = 0;
@@ -822,6 +834,7 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   uint32_t* cnt = ctx->d<uint32_t>("ig.nlc", nch + 1);
   uint32_t* pos = ctx->d<uint32_t>("ig.nlp", nch + 1);
   uint32_t* tot = ctx->d<uint32_t>("ig.nlt", 1);
+  mark("h2d");
   k_nl_count<<<blocks(nch), 256, 0, st>>>(dtext, n_text, cnt);
   uint32_t* scr = ctx->d<uint32_t>("ig.scan", scan_scratch_elems(nch + 1));
   exclusive_scan<uint32_t, uint32_t>(cnt, pos, nch, scr, tot, st, &ctx->launches);
@@ -883,7 +896,9 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   lo.occ = ctx->d<double>("ig.l.oc", L);
   lo.alloc = ctx->d<int64_t>("ig.l.al", L);
   lo.tag_bits = ctx->d<uint8_t>("ig.l.tb", L);
+  mark("lines");
   if (L) k_parse_lines<<<blocks(L), 256, 0, st>>>(dtext, n_text, lstart, nl, L, lo);
+  mark("parse");
   std::vector<uint8_t> hkind(L);
   XSP_CUDA(cudaMemcpyAsync(hkind.data(), lo.kind, L, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
@@ -949,7 +964,9 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   g.dwrite = ctx->d<uint64_t>("ig.s.dw", n + 1);
   g.occ = ctx->d<double>("ig.s.oc", n + 1);
   g.alloc = ctx->d<int64_t>("ig.s.al", n + 1);
+  mark("meta");
   k_gather_spans<<<blocks(L), 256, 0, st>>>(g);
+  mark("gather");
   ctx->launches += 2;
   // ---- intern names (every span) and layer types (layer spans only)
   uint32_t* name_fid = ctx->d<uint32_t>("ig.s.nid", n + 1);
@@ -996,7 +1013,9 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   // ---- sort_timeline per trace (stage (b)), then the final columns
   uint32_t* perm = ctx->d<uint32_t>("ig.perm", n + 1);
   uint32_t sorted = 1;
+  mark("intern");
   if (n) run_sort_timeline(ctx, n, g.begin, g.flags, g.span_id, S, d_soff, perm, &sorted, st);
+  mark("sort");
   Final f;
   f.perm = sorted ? nullptr : perm;
   f.n = n;
@@ -1050,7 +1069,9 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   xsp_validate_in vin{f.o_trace_id, d_mtid, f.o_tag_bits};
   xsp_validation_out vout;
   std::memset(&vout, 0, sizeof(vout));
+  mark("columns");
   run_validate(ctx, &c, &out->traces, &vin, &vout, st);
+  mark("validate");
   if (vout.n_issues) {
     std::vector<uint32_t> toff(S + 1);
     XSP_CUDA(cudaMemcpyAsync(toff.data(), vout.trace_issue_off, (S + 1ull) * 4, cudaMemcpyDeviceToHost, st));

@@ -43,10 +43,12 @@ __device__ __forceinline__ uint64_t hash_key(uint32_t t, uint64_t sid) {
 // Table entry: trace << 32 | (row + 1); 0 = empty. Equal keys share one slot
 // (the first inserted), which keeps the minimum row.
 __global__ void k_val_insert(const uint64_t* __restrict__ sid, const uint64_t* __restrict__ off, uint32_t T,
-                             uint64_t n, unsigned long long* __restrict__ table, uint64_t mask) {
+                             uint64_t n, unsigned long long* __restrict__ table, uint64_t mask,
+                             const uint32_t* __restrict__ t_big) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t t = span_trace(off, T, i);
+  if (!t_big[t]) return;  // checked on chip (k_val_dup_local)
   const uint64_t s = sid[i];
   const unsigned long long mine = ((unsigned long long)t << 32) | (uint32_t)(i + 1);
   for (uint64_t slot = hash_key(t, s) & mask;; slot = (slot + 1) & mask) {
@@ -68,6 +70,65 @@ __device__ __forceinline__ bool is_duplicate(const uint64_t* __restrict__ sid, u
   }
 }
 
+// Traces of at most kDupCap spans find their duplicate span ids on chip: one
+// CTA per trace stages the trace's span ids in shared memory and inserts them
+// into a shared open-addressing table (slot = local row + 1, the minimum row
+// of a key kept by atomicMin), so the check never touches a global table.
+// Longer traces are flagged for the global table (k_val_insert).
+constexpr uint32_t kDupCap = 12288;
+constexpr uint32_t kDupSlots = 32768;  // power-of-two table >= 2 x the trace, at most this
+constexpr size_t kDupSmem = kDupCap * 8 + kDupSlots * 4;
+constexpr int kDupThreads = 1024;
+
+__global__ void __launch_bounds__(kDupThreads) k_val_dup_local(const uint64_t* __restrict__ sid,
+                                                               const uint64_t* __restrict__ off, uint32_t T,
+                                                               uint8_t* __restrict__ dup, uint32_t* __restrict__ t_big,
+                                                               uint32_t* __restrict__ any_big) {
+  extern __shared__ __align__(16) unsigned char dup_dyn[];
+  uint64_t* s_sid = reinterpret_cast<uint64_t*>(dup_dyn);
+  uint32_t* s_tab = reinterpret_cast<uint32_t*>(s_sid + kDupCap);
+  const uint32_t t = blockIdx.x;
+  const uint64_t lo = off[t], m = off[t + 1] - lo;
+  if (m > kDupCap) {
+    if (threadIdx.x == 0) {
+      t_big[t] = 1;
+      *any_big = 1;
+    }
+    return;
+  }
+  if (threadIdx.x == 0) t_big[t] = 0;
+  uint32_t slots = 16;
+  while (slots < 2 * m) slots <<= 1;
+  const uint32_t mask = slots - 1;
+  for (uint32_t r = threadIdx.x; r < m; r += kDupThreads) s_sid[r] = sid[lo + r];
+  for (uint32_t q = threadIdx.x; q < slots; q += kDupThreads) s_tab[q] = 0;
+  __syncthreads();
+  for (uint32_t r = threadIdx.x; r < m; r += kDupThreads) {
+    const uint64_t s = s_sid[r];
+    for (uint32_t slot = (uint32_t)hash_key(0, s) & mask;; slot = (slot + 1) & mask) {
+      const uint32_t cur = atomicCAS(s_tab + slot, 0u, r + 1);
+      if (cur == 0u) break;
+      if (s_sid[cur - 1] == s) {
+        atomicMin(s_tab + slot, r + 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t r = threadIdx.x; r < m; r += kDupThreads) {
+    const uint64_t s = s_sid[r];
+    uint8_t d = 0;
+    for (uint32_t slot = (uint32_t)hash_key(0, s) & mask;; slot = (slot + 1) & mask) {
+      const uint32_t cur = s_tab[slot];
+      if (s_sid[cur - 1] == s) {
+        d = cur != r + 1;
+        break;
+      }
+    }
+    dup[lo + r] = d;
+  }
+}
+
 struct ValArgs {
   const uint64_t* span_id;
   const uint64_t* begin;
@@ -82,6 +143,8 @@ struct ValArgs {
   uint32_t T;
   uint64_t n;
   const uint32_t* metric_base;  // [blocks] metric rows before each block
+  const uint8_t* dup;           // duplicate flags of the on-chip traces
+  const uint32_t* t_big;        // traces checked through the global table
   const unsigned long long* table;
   uint64_t mask;
   uint32_t* model_count;  // [T]
@@ -152,7 +215,8 @@ __global__ void __launch_bounds__(kValThreads) k_val_spans(ValArgs a) {
     const bool has_cid = (f & XSP_F_CID) != 0;
     if (needs_cid && !has_cid) emit_issue(a, t, local, XSP_V_CID_MISSING);
     if (!needs_cid && has_cid) emit_issue(a, t, local, XSP_V_CID_ON_SYNC);
-    if (is_duplicate(a.span_id, t, i, a.table, a.mask)) emit_issue(a, t, local, XSP_V_DUP_SPAN_ID);
+    if (a.t_big[t] ? is_duplicate(a.span_id, t, i, a.table, a.mask) : a.dup[i] != 0)
+      emit_issue(a, t, local, XSP_V_DUP_SPAN_ID);
     if (a.trace_id && a.trace_id[i] != a.meta_trace_id[t]) emit_issue(a, t, local, XSP_V_TRACE_ID);
     if (is_model_span(f)) atomicAdd(a.model_count + t, 1u);
     if (local > 0) {
@@ -213,10 +277,25 @@ void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, co
   uint32_t* counters = ctx->d<uint32_t>("v.counters", 4);
   uint32_t* model_count = ctx->d<uint32_t>("v.model_count", T + 1);
   uint32_t* trace_count = ctx->d<uint32_t>("v.trace_count", T + 1);
-  uint64_t cap = 1024;
-  while (cap < 2 * n) cap <<= 1;
+  // duplicate span ids: on chip per trace; traces beyond kDupCap spans through a
+  // global (trace, span_id) table sized for their spans only
+  uint8_t* dupf = ctx->d<uint8_t>("v.dup", n + 1);
+  uint32_t* t_big = ctx->d<uint32_t>("v.t_big", T + 1);
+  uint32_t* any_big = ctx->d<uint32_t>("v.any_big", 1);
+  XSP_CUDA(cudaMemsetAsync(any_big, 0, 4, st));
+  if (T) {
+    XSP_CUDA(cudaFuncSetAttribute(k_val_dup_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDupSmem));
+    k_val_dup_local<<<T, kDupThreads, kDupSmem, st>>>(c->span_id, tr->span_off, T, dupf, t_big, any_big);
+    ++ctx->launches;
+  }
+  uint32_t* hb = ctx->h<uint32_t>("v.any_big_h", 1);
+  xfer_small(hb, any_big, 4, st);
+  XSP_CUDA(cudaStreamSynchronize(st));
+  uint64_t cap = 16;
+  if (hb[0])
+    while (cap < 2 * n) cap <<= 1;
   auto* table = ctx->d<unsigned long long>("v.table", cap);
-  XSP_CUDA(cudaMemsetAsync(table, 0, cap * 8, st));
+  if (hb[0]) XSP_CUDA(cudaMemsetAsync(table, 0, cap * 8, st));
   ValArgs a;
   a.span_id = c->span_id;
   a.begin = c->begin_ns;
@@ -232,6 +311,8 @@ void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, co
   a.T = T;
   a.n = n;
   a.metric_base = mcount;
+  a.dup = dupf;
+  a.t_big = t_big;
   a.table = table;
   a.mask = cap - 1;
   a.model_count = model_count;
@@ -241,8 +322,11 @@ void run_validate(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, co
     k_val_mcount<<<nb, kValThreads, 0, st>>>(c->flags, n, mcount);
     uint32_t* scr = ctx->d<uint32_t>("v.scan", scan_scratch_elems(nb));
     exclusive_scan<uint32_t, uint32_t>(mcount, mcount, nb, scr, (uint32_t*)nullptr, st, &ctx->launches);
-    k_val_insert<<<ceil_div(n, 256), 256, 0, st>>>(c->span_id, tr->span_off, T, n, table, cap - 1);
-    ctx->launches += 2;
+    ctx->launches += 1;
+    if (hb[0]) {
+      k_val_insert<<<ceil_div(n, 256), 256, 0, st>>>(c->span_id, tr->span_off, T, n, table, cap - 1, t_big);
+      ++ctx->launches;
+    }
   }
   // issue keys: sized for a mostly clean batch; rerun once with the exact count on overflow
   uint32_t* h = ctx->h<uint32_t>("v.count_h", 1);
