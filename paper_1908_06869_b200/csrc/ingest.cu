@@ -844,36 +844,35 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   // newline positions + the stream ends (a stream's last line may lack '\n')
   uint64_t* nl = ctx->d<uint64_t>("ig.nl", hnl + S + 1);
   k_nl_write<<<blocks(nch), 256, 0, st>>>(dtext, n_text, pos, nl);
-  std::vector<uint64_t> hnlpos(hnl);
-  XSP_CUDA(cudaMemcpyAsync(hnlpos.data(), nl, hnl * 8ull, cudaMemcpyDeviceToHost, st));
+  // (pinned staging: these arrays cross PCIe twice)
+  uint64_t* hnlpos = ctx->h<uint64_t>("ig.hnl", hnl + 1ull);
+  XSP_CUDA(cudaMemcpyAsync(hnlpos, nl, hnl * 8ull, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
   // merge stream ends that are not already line ends; the line -> stream map
-  std::vector<uint64_t> ends, starts;
-  ends.reserve(hnl + S);
-  starts.reserve(hnl + S);
-  std::vector<uint32_t> line_stream;
-  line_stream.reserve(hnl + S);
+  uint64_t* ends = ctx->h<uint64_t>("ig.hends", hnl + S + 1ull);
+  uint64_t* starts = ctx->h<uint64_t>("ig.hstarts", hnl + S + 1ull);
+  std::vector<uint32_t> line_stream(hnl + S + 1ull);
+  uint64_t L = 0;
   {
     uint64_t k = 0;
     for (uint32_t s = 0; s < S; ++s) {
       uint64_t at = soff[s];
       while (k < hnl && hnlpos[k] < soff[s + 1]) {
-        starts.push_back(at);
-        ends.push_back(hnlpos[k]);
+        starts[L] = at;
+        ends[L] = hnlpos[k];
+        line_stream[L++] = s;
         at = hnlpos[k++] + 1;
-        line_stream.push_back(s);
       }
       if (at < soff[s + 1]) {  // unterminated last line of stream s
-        starts.push_back(at);
-        ends.push_back(soff[s + 1]);
-        line_stream.push_back(s);
+        starts[L] = at;
+        ends[L] = soff[s + 1];
+        line_stream[L++] = s;
       }
     }
   }
-  const uint64_t L = ends.size();
-  XSP_CUDA(cudaMemcpyAsync(nl, ends.data(), L * 8, cudaMemcpyHostToDevice, st));
+  XSP_CUDA(cudaMemcpyAsync(nl, ends, L * 8, cudaMemcpyHostToDevice, st));
   uint64_t* lstart = ctx->d<uint64_t>("ig.ls", L + 1);
-  XSP_CUDA(cudaMemcpyAsync(lstart, starts.data(), L * 8, cudaMemcpyHostToDevice, st));
+  XSP_CUDA(cudaMemcpyAsync(lstart, starts, L * 8, cudaMemcpyHostToDevice, st));
   // ---- parse every line
   LineOut lo;
   lo.kind = ctx->d<uint8_t>("ig.kind", L + 1);
