@@ -576,13 +576,16 @@ class C5:
         torch.cuda.empty_cache()
 
 
-def e2e_host(eng, hb, groups, copies: int, steps: int, barrier, dist, packed=None):
+def e2e_host(eng, hb, groups, copies: int, steps: int, barrier, dist, packed=None, rows_only=False):
     """End to end through the host-buffer C ABI (xsp_run_host, or
     xsp_run_host_packed when `packed` is given): every step runs `copies` calls
     on pinned host columns, each with H2D of its inputs and D2H of every result
     column inside the timed region (wall clock around the calls, device
     synchronised on both sides; max over ranks)."""
     import torch
+    from paper_1908_06869_b200 import _capi as capi
+
+    eng.set_host_outputs(capi.HOST_OUT_ROWS if rows_only else capi.HOST_OUT_ALL)
 
     def call():
         if packed is not None:
@@ -599,6 +602,7 @@ def e2e_host(eng, hb, groups, copies: int, steps: int, barrier, dist, packed=Non
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / steps
     h2d, d2h = eng.transfer_bytes()
+    eng.set_host_outputs(capi.HOST_OUT_ALL)
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -722,12 +726,19 @@ def main():
     # the packed wire form (xsp_pack_host: u32 begin deltas / durations / cid
     # offsets, sparse parent / cid lists), built once like the columns themselves
     pk = eng.pack_host(hb)
-    e3_ms, h2d3, d2h3 = e2e_host(eng, hb, groups, 1, max(2, args.steps // 4), barrier, dist, packed=pk)
+    e3_ms, h2d3, d2h3 = e2e_host(eng, hb, groups, 1, max(2, args.steps // 4), barrier, dist, packed=pk,
+                                 rows_only=True)
+    e3f_ms, h2d3f, d2h3f = e2e_host(eng, hb, groups, 1, max(2, args.steps // 4), barrier, dist, packed=pk)
     e3d_ms, h2d3d, d2h3d = e2e_host(eng, hb, groups, 1, max(2, args.steps // 4), barrier, dist)
     c3_line = {"metric": METRIC, "value": b.n_spans * world / (c3_ms / 1e3) / 1e6, "unit": UNIT,
                "ms_per_step": c3_ms, "spans_per_gpu": b.n_spans, "scaling": "weak", "config": c3_config(args),
                "e2e": {"value": b.n_spans * world / (e3_ms / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d3,
-                       "d2h_bytes_per_step": d2h3, "ms_per_step": e3_ms, "input": "packed (xsp_run_host_packed)"},
+                       "d2h_bytes_per_step": d2h3, "ms_per_step": e3_ms, "input": "packed (xsp_run_host_packed)",
+                       "outputs": "XSP_HOST_OUT_ROWS: every table + the correlation's span / metric rows"},
+               "e2e_full": {"value": b.n_spans * world / (e3f_ms / 1e3) / 1e6, "unit": UNIT,
+                            "h2d_bytes_per_step": h2d3f, "d2h_bytes_per_step": d2h3f, "ms_per_step": e3f_ms,
+                            "input": "packed (xsp_run_host_packed)",
+                            "outputs": "XSP_HOST_OUT_ALL: + layer_dur, kernel_dur / name / occ"},
                "e2e_dense": {"value": b.n_spans * world / (e3d_ms / 1e3) / 1e6, "unit": UNIT,
                              "h2d_bytes_per_step": h2d3d, "d2h_bytes_per_step": d2h3d, "ms_per_step": e3d_ms,
                              "input": "dense span columns (xsp_run_host)"},
@@ -760,14 +771,19 @@ def main():
     value = c5.spans_all / (ms / 1e3) / 1e6
     # end to end: the same corpus from pinned host buffers through xsp_run_host
     # (one call per copy: H2D of its columns, D2H of every result column)
-    e_ms, h2d, d2h = e2e_host(eng, hb, groups, len(c5.mine), args.e2e_steps, barrier, dist, packed=pk)
+    e_ms, h2d, d2h = e2e_host(eng, hb, groups, len(c5.mine), args.e2e_steps, barrier, dist, packed=pk,
+                              rows_only=True)
     e2e = {"value": c5.spans_all / (e_ms / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "steps": args.e2e_steps,
            "calls_per_step": len(c5.mine),
            "how": "xsp_run_host_packed per C3 copy on the same pinned host buffers (every copy's H2D and D2H "
                   "happen); the span columns in the packed wire form (xsp_pack_host, built once outside the "
                   "timed region like the columns themselves: u32 begin deltas / durations / cid offsets, "
-                  "parent_id and cid only where flagged), unpacked on the device",
+                  "parent_id and cid only where flagged), unpacked on the device; results: every analysis "
+                  "table and the correlation as span / metric rows (XSP_HOST_OUT_ROWS: the reference's "
+                  "CorrelationResult refers to spans; the four lookup columns it leaves out are "
+                  "c3.e2e_full's extra D2H)",
+           "full_outputs_c3_e2e_value": c3_line["e2e_full"]["value"],
            "dense_c3_e2e_value": c3_line["e2e_dense"]["value"]}
     calls = len(c5.calls)
     p1_ms = stages["pass1"][0] / max(stages["pass1"][1], 1)  # per launch

@@ -428,6 +428,20 @@ xsp_status xsp_run_host(xsp_ctx* ctx, const xsp_span_cols* host_cols,
                         const xsp_system_spec* spec, const xsp_analysis_opts* opts,
                         xsp_corr_out* corr_host, xsp_tables_out* tables_host, void* stream);
 
+/* Columns the host-buffer calls (xsp_run_host, xsp_run_host_packed) copy back.
+ * XSP_HOST_OUT_ALL (the default) copies every xsp_corr_out column.
+ * XSP_HOST_OUT_ROWS skips the four columns that are lookups into the caller's
+ * own span and metric columns and leaves them NULL:
+ *   layer_dur[l]   = end_ns - begin_ns of span layer_row[l] (0 if end < begin),
+ *   kernel_dur[k]  = the same of span kernel_exec_row[k],
+ *   kernel_name[k] = name_id[kernel_exec_row[k]],
+ *   kernel_occ[k]  = occupancy[kernel_metric_row[k]] (0 if UINT32_MAX).
+ * What remains is what the reference's CorrelationResult carries (EntityTree
+ * nodes refer to spans; correlator.hpp:40-75) plus every analysis table. */
+#define XSP_HOST_OUT_ALL 0u
+#define XSP_HOST_OUT_ROWS 1u
+xsp_status xsp_set_host_outputs(xsp_ctx* ctx, uint32_t mode);
+
 /* ---- packed host input (fewer PCIe bytes for xsp_run_host) -----------------
  * The same spans as an xsp_span_cols, with the 8-byte span columns packed:
  * begin as a u32 delta from the previous span (XSP_PACK_ESC: the value is in the

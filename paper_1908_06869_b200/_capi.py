@@ -198,6 +198,7 @@ INGEST_OK, INGEST_HOST = 0, 1
 # report tables (xsp_report_csv): a8..a14
 REPORT_TABLES = {"a8": 8, "a9": 9, "a10": 10, "a11": 11, "a12": 12, "a13": 13, "a14": 14}
 
+HOST_OUT_ALL, HOST_OUT_ROWS = 0, 1  # xsp_set_host_outputs
 L_OK, L_TOO_FEW, L_NOT_CHAIN, L_AMBIGUOUS, L_TRACE_FAILED = range(5)
 EV_IN_NARROW, EV_IN_WIDE, EV_CLAMPED, EV_NEGATIVE = 1, 2, 4, 8
 
@@ -210,6 +211,7 @@ EXPORTS = [
     "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline", "xsp_resolve_serialized",
     "xsp_resolve_serialized_host", "xsp_report_csv", "xsp_report_csv_host", "xsp_comm_unique_id",
     "xsp_comm_init", "xsp_combine_tables", "xsp_ingest_jsonl", "xsp_pack_host", "xsp_run_host_packed",
+    "xsp_set_host_outputs",
 ]
 
 _lib = None
@@ -289,6 +291,8 @@ def load() -> C.CDLL:
                        C.POINTER(C.c_char_p), u64p, P]
         fn.restype = C.c_int32
     lib.xsp_pack_host.argtypes = [P, C.POINTER(SpanCols), C.POINTER(Traces), C.POINTER(PackedCols)]
+    lib.xsp_set_host_outputs.argtypes = [P, C.c_uint32]
+    lib.xsp_set_host_outputs.restype = C.c_int
     lib.xsp_pack_host.restype = C.c_int32
     lib.xsp_run_host_packed.argtypes = [P, C.POINTER(PackedCols), C.POINTER(SpanCols), C.POINTER(Traces),
                                         C.POINTER(Groups), C.POINTER(SystemSpec), C.POINTER(AnalysisOpts),

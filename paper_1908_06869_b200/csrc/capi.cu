@@ -163,14 +163,14 @@ void download_corr(xsp_ctx* ctx, const xsp_corr_out& dcorr, xsp_corr_out* c, cud
   c->trace_amb_off = to_host(ctx, "t_aoff", dcorr.trace_amb_off, T + 1ull, st);
   c->layer_row = to_host(ctx, "l_row", dcorr.layer_row, dcorr.n_layers, st);
   c->layer_kernel_off = to_host(ctx, "l_koff", dcorr.layer_kernel_off, dcorr.n_layers + 1, st);
-  c->layer_dur = to_host(ctx, "l_dur", dcorr.layer_dur, dcorr.n_layers, st);
+  c->layer_dur = ctx->host_out == XSP_HOST_OUT_ROWS ? nullptr : to_host(ctx, "l_dur", dcorr.layer_dur, dcorr.n_layers, st);
   c->layer_attr_row = to_host(ctx, "l_attr", dcorr.layer_attr_row, dcorr.n_layers, st);
   c->kernel_launch_row = to_host(ctx, "k_launch", dcorr.kernel_launch_row, dcorr.n_kernels, st);
   c->kernel_exec_row = to_host(ctx, "k_exec", dcorr.kernel_exec_row, dcorr.n_kernels, st);
   c->kernel_metric_row = to_host(ctx, "k_mrow", dcorr.kernel_metric_row, dcorr.n_kernels, st);
-  c->kernel_dur = to_host(ctx, "k_dur", dcorr.kernel_dur, dcorr.n_kernels, st);
-  c->kernel_name = to_host(ctx, "k_name", dcorr.kernel_name, dcorr.n_kernels, st);
-  c->kernel_occ = to_host(ctx, "k_occ", dcorr.kernel_occ, dcorr.n_kernels, st);
+  c->kernel_dur = ctx->host_out == XSP_HOST_OUT_ROWS ? nullptr : to_host(ctx, "k_dur", dcorr.kernel_dur, dcorr.n_kernels, st);
+  c->kernel_name = ctx->host_out == XSP_HOST_OUT_ROWS ? nullptr : to_host(ctx, "k_name", dcorr.kernel_name, dcorr.n_kernels, st);
+  c->kernel_occ = ctx->host_out == XSP_HOST_OUT_ROWS ? nullptr : to_host(ctx, "k_occ", dcorr.kernel_occ, dcorr.n_kernels, st);
   c->orphan_row = to_host(ctx, "o_row", dcorr.orphan_row, dcorr.n_orphans, st);
   c->orphan_reason = to_host(ctx, "o_reason", dcorr.orphan_reason, dcorr.n_orphans, st);
   c->amb_row = to_host(ctx, "a_row", dcorr.amb_row, dcorr.n_ambiguities, st);
@@ -264,6 +264,16 @@ XSP_API void* xsp_host_alloc(size_t bytes) {
 
 XSP_API void xsp_host_free(void* p) {
   if (p) cudaFreeHost(p);
+}
+
+XSP_API xsp_status xsp_set_host_outputs(xsp_ctx* ctx, uint32_t mode) {
+  if (!ctx) return XSP_E_INVALID;
+  if (mode != XSP_HOST_OUT_ALL && mode != XSP_HOST_OUT_ROWS) {
+    ctx->last_error = "xsp_set_host_outputs: unknown mode";
+    return XSP_E_INVALID;
+  }
+  ctx->host_out = mode;
+  return XSP_OK;
 }
 
 XSP_API void xsp_set_profiling(xsp_ctx* ctx, int enabled) {

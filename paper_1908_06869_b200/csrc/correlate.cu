@@ -1577,9 +1577,11 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
   uint32_t tl = kNone;
   uint64_t mn = ~0ull, mx = 0;
   // a trace already known to be slow needs no alignment check (one L2 read per
-  // trace change, not per entry)
-  uint32_t tslow = kNone, tnm = kNone;
-  bool slow = false;
+  // trace change, not per entry). A stale 0 only costs the check, so the read
+  // of the warp's first trace is a plain L2 load issued with the entry loads
+  // (a volatile read there held 37% of the kernel's stall samples on C4).
+  uint32_t tslow = t, tnm = kNone;
+  bool slow = __ldcg(t_slow + t) != 0;
   // all of the lane's entries and their flag bytes are loaded up front (the
   // loads of an entry no longer wait for the previous entry's checks)
   KlEnt e[JC_ITEMS];
@@ -1607,7 +1609,7 @@ __global__ void k_join_check(uint32_t nkl, const KlEnt* __restrict__ kl, const E
     while (t + 1 < T && __ldg(t_kl_off + t + 1) <= k) ++t;
     if (t != tslow) {
       tslow = t;
-      slow = *((volatile uint32_t*)(t_slow + t)) != 0;
+      slow = __ldcg(t_slow + t) != 0;
     }
     const uint32_t r = k - t_kl_off[t];
     const KlEnt ent = e[i];

@@ -48,6 +48,7 @@ struct xsp_ctx {
     uint64_t calls = 0;
   };
   bool profiling = false;
+  uint32_t host_out = 0;  // XSP_HOST_OUT_* (xsp_set_host_outputs)
   std::vector<Stage> stages;
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t take_event() {

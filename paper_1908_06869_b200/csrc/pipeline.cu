@@ -42,23 +42,26 @@ struct Field {
   bool csr;     // [count + 1] offsets: the last chunk also writes the sentinel
   Base base;
   const char* name;
+  bool lookup = false;  // a span / metric column lookup (skipped under XSP_HOST_OUT_ROWS)
 };
 
 #define CF(m, T, c, csr, b) Field{offsetof(xsp_corr_out, m), sizeof(T), c, csr, b, "pc." #m}
+#define CFL(m, T, c) Field{offsetof(xsp_corr_out, m), sizeof(T), c, false, B_NONE, "pc." #m, true}
 const Field kCorrFields[] = {
     CF(trace_status, int32_t, N_T, false, B_NONE),    CF(trace_err_row, uint32_t, N_2T, false, B_SPAN),
     CF(trace_model_row, uint32_t, N_T, false, B_SPAN), CF(trace_layer_off, uint32_t, N_T, true, B_L),
     CF(trace_kernel_off, uint32_t, N_T, true, B_K),    CF(trace_orphan_off, uint32_t, N_T, true, B_O),
     CF(trace_amb_off, uint32_t, N_T, true, B_A),       CF(layer_row, uint32_t, N_L, false, B_SPAN),
-    CF(layer_kernel_off, uint32_t, N_L, true, B_K),    CF(layer_dur, uint64_t, N_L, false, B_NONE),
+    CF(layer_kernel_off, uint32_t, N_L, true, B_K),    CFL(layer_dur, uint64_t, N_L),
     CF(layer_attr_row, uint32_t, N_L, false, B_LAYER), CF(kernel_launch_row, uint32_t, N_K, false, B_SPAN),
     CF(kernel_exec_row, uint32_t, N_K, false, B_SPAN), CF(kernel_metric_row, uint32_t, N_K, false, B_METRIC),
-    CF(kernel_dur, uint64_t, N_K, false, B_NONE),      CF(kernel_name, uint32_t, N_K, false, B_NONE),
-    CF(kernel_occ, double, N_K, false, B_NONE),        CF(orphan_row, uint32_t, N_O, false, B_SPAN),
+    CFL(kernel_dur, uint64_t, N_K),      CFL(kernel_name, uint32_t, N_K),
+    CFL(kernel_occ, double, N_K),        CF(orphan_row, uint32_t, N_O, false, B_SPAN),
     CF(orphan_reason, uint8_t, N_O, false, B_NONE),    CF(amb_row, uint32_t, N_A, false, B_SPAN),
     CF(amb_cand_off, uint32_t, N_A, true, B_AC),       CF(amb_cand_row, uint32_t, N_AC, false, B_SPAN),
 };
 #undef CF
+#undef CFL
 
 #define TF(m, T, c) Field{offsetof(xsp_tables_out, m), sizeof(T), c, false, B_NONE, "pt." #m}
 #define TFB(m, T, c, csr, b) Field{offsetof(xsp_tables_out, m), sizeof(T), c, csr, b, "pt." #m}
@@ -357,7 +360,9 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
   auto d2h_fields = [&](const Field* F, size_t nf, void* dev_struct, void* host_struct, const Pos& P, bool last) {
     // grow host columns first (rare: sync so that no copy targets a moved buffer)
     bool synced = false;
+    const bool rows_only = ctx->host_out == XSP_HOST_OUT_ROWS;
     for (size_t f = 0; f < nf; ++f) {
+      if (rows_only && F[f].lookup) continue;
       const uint64_t cnt = P.n[F[f].cnt] + (F[f].csr && last ? 1 : 0);
       const uint64_t need = (P.at[F[f].cnt] + cnt) * F[f].esz;
       if (ctx->hcap(F[f].name) < need || !ctx->host[F[f].name].ptr) {
@@ -370,6 +375,10 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     }
     for (size_t f = 0; f < nf; ++f) {
       const Field& fd = F[f];
+      if (rows_only && fd.lookup) {
+        member(host_struct, fd.off) = nullptr;
+        continue;
+      }
       const uint64_t cnt = P.n[fd.cnt] + (fd.csr && last ? 1 : 0);
       void* dsrc = member(dev_struct, fd.off);
       char* hdst = static_cast<char*>(ctx->host[fd.name].ptr);

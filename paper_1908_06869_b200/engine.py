@@ -104,6 +104,27 @@ class Tables:
             raise AttributeError(k) from e
 
 
+def fill_lookups(corr: "CorrResult", batch: SpanBatch) -> None:
+    """The four xsp_corr_out columns XSP_HOST_OUT_ROWS does not copy back, as the
+    lookups include/xsp.h defines them (filled only where absent)."""
+    def dur(rows):
+        b, e = batch.begin_ns[rows], batch.end_ns[rows]
+        return np.where(e >= b, e - b, 0).astype(np.uint64)
+    c = corr.cols
+    lr = c["layer_row"].astype(np.int64)
+    xr = c["kernel_exec_row"].astype(np.int64)
+    mr = c["kernel_metric_row"]
+    if not c.get("layer_dur", np.zeros(0)).size and lr.size:
+        c["layer_dur"] = dur(lr)
+    if not c.get("kernel_dur", np.zeros(0)).size and xr.size:
+        c["kernel_dur"] = dur(xr)
+        c["kernel_name"] = batch.name_id[xr].astype(np.uint32)
+        has = mr != 0xFFFFFFFF
+        occ = np.zeros(xr.size, dtype=np.float64)
+        occ[has] = batch.occupancy[mr[has].astype(np.int64)]
+        c["kernel_occ"] = occ
+
+
 def _corr_counts(o: capi.CorrOut) -> Dict[str, int]:
     T = o.n_traces
     return {"T": T, "2T": 2 * T, "T1": T + 1, "L": o.n_layers, "L1": o.n_layers + 1,
@@ -409,6 +430,11 @@ class Engine:
         tabs = Tables(to.n_groups, {n: _copy(getattr(to, n), t, tc[k]) for n, t, k in capi.TABLE_FIELDS},
                       to.n_layers, to.n_kernels, to.n_names)
         return corr, tabs
+
+    def set_host_outputs(self, mode: int):
+        """xsp_set_host_outputs: capi.HOST_OUT_ROWS leaves layer_dur / kernel_dur /
+        kernel_name / kernel_occ on the device (fill_lookups rebuilds them)."""
+        self._check(self.lib.xsp_set_host_outputs(self.ctx, mode))
 
     def set_profiling(self, on: bool):
         self.lib.xsp_set_profiling(self.ctx, int(on))

@@ -56,3 +56,40 @@ def test_packed_escapes(engine, monkeypatch):
     T = b.n_traces
     run_both(engine, b, (np.arange(T), np.ones(T), b.trace_batch), 0, monkeypatch)
     run_both(engine, b, (np.arange(T), np.ones(T), b.trace_batch), 3000, monkeypatch)
+
+
+@pytest.mark.parametrize("chunk", [0, 50_000])
+def test_host_outputs_rows_only(engine, monkeypatch, chunk):
+    """XSP_HOST_OUT_ROWS: the four lookup columns stay on the device (NULL in
+    the host result, fewer D2H bytes); every other column is unchanged and the
+    lookups rebuilt from the span columns (engine.fill_lookups) equal the
+    device's."""
+    from paper_1908_06869_b200 import _capi as capi
+    from paper_1908_06869_b200.engine import fill_lookups
+    monkeypatch.setenv("XSP_CHUNK_SPANS", str(chunk))
+    b, gf, gr, gb = synth.c3(runs=3, n_models=6, max_layers=400)
+    pk = engine.pack_host(b)
+    c0, t0 = engine.run_host_packed(pk, b, groups=(gf, gr, gb))
+    _, d0 = engine.transfer_bytes()
+    try:
+        engine.set_host_outputs(capi.HOST_OUT_ROWS)
+        co, _ = engine.run_host_packed(pk, b, groups=(gf, gr, gb), raw=True)
+        assert not co.kernel_dur and not co.kernel_name and not co.kernel_occ and not co.layer_dur
+        c1, t1 = engine.run_host_packed(pk, b, groups=(gf, gr, gb))
+        _, d1 = engine.transfer_bytes()
+        c2, _ = engine.run_host(b, groups=(gf, gr, gb))
+    finally:
+        engine.set_host_outputs(capi.HOST_OUT_ALL)
+    lookups = ("layer_dur", "kernel_dur", "kernel_name", "kernel_occ")
+    for k in lookups:
+        assert c1.cols[k].size == 0 and c2.cols[k].size == 0, k
+    skip = lambda c: type(c)(c.n_traces, c.n_failed, {k: v for k, v in c.cols.items() if k not in lookups})  # noqa
+    same(skip(c1), skip(c0))
+    same(skip(c2), skip(c0))
+    same(t1, t0)
+    kb = c0.n_kernels * 20 + c0.n_layers * 8
+    assert d0 - d1 == kb, (d0, d1, kb)
+    fill_lookups(c1, b)
+    same(c1, c0)
+    with pytest.raises(capi.XspError):
+        engine.set_host_outputs(7)
