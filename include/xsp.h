@@ -452,10 +452,19 @@ xsp_status xsp_set_host_outputs(xsp_ctx* ctx, uint32_t mode);
  * ascending, with esc_val the raw value. flags / name_id are as in
  * xsp_span_cols; the metric and layer tables and span_id stay in the
  * xsp_span_cols given next to it. xsp_pack_host builds one (host arrays in
- * ctx-owned pinned memory, valid until the next xsp_pack_host). C3: 52 -> 34 B
- * per span on the wire. */
+ * ctx-owned pinned memory, valid until the next xsp_pack_host). name_id and
+ * the metric / layer tables are byte-width coded, occupancy dictionary coded
+ * (XSP_PACK_TABLES=0 leaves them raw). C3: 52 -> 24 B per span on the wire. */
 #define XSP_PACK_ESC 0xFFFFFFFFu
 #define XSP_PACK_BLOCK 256u
+/* Byte-width coded column, in blocks of XSP_PACK_BLOCK values: every value of
+ * block b is width[b] (0..8) little-endian bytes, the block's values starting
+ * at data + boff[b] (width 0: the block is all zero). */
+typedef struct xsp_bw_col {
+  const uint8_t* width;  /* [ceil(n / XSP_PACK_BLOCK)]; NULL: column not coded */
+  const uint64_t* boff;  /* [ceil(n / XSP_PACK_BLOCK) + 1] */
+  const uint8_t* data;
+} xsp_bw_col;
 typedef struct xsp_packed_cols {
   uint64_t n_spans;
   const uint8_t* flags;
@@ -473,6 +482,18 @@ typedef struct xsp_packed_cols {
   uint64_t n_esc;
   const uint64_t* esc_key;
   const uint64_t* esc_val;
+  /* name_id and the metric / layer tables, byte-width coded (alloc_bytes as
+   * its u64 two's complement); a NULL width sends that column raw (name_id
+   * above, the tables from the xsp_span_cols given next to the packed input) */
+  xsp_bw_col name_bw;                      /* n_spans values */
+  xsp_bw_col flops_bw, read_bw, write_bw;  /* n_metric_rows values */
+  xsp_bw_col alloc_bw, type_bw;            /* n_layer_rows values */
+  /* occupancy as indexes into a dictionary of its distinct values (first
+   * appearance order); occ_dict_n == 0: occupancy raw */
+  uint32_t occ_dict_n;
+  uint32_t occ_idx_bytes;  /* 1 (<= 256 values) or 2 (<= 65536) */
+  const double* occ_dict;
+  const uint8_t* occ_idx;  /* [n_metric_rows * occ_idx_bytes], little-endian */
 } xsp_packed_cols;
 xsp_status xsp_pack_host(xsp_ctx* ctx, const xsp_span_cols* host_cols, const xsp_traces* host_traces,
                          xsp_packed_cols* out);

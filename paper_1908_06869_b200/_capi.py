@@ -174,11 +174,18 @@ class StringTable(C.Structure):
     _fields_ = [("n", C.c_uint32), ("bytes", C.c_char_p), ("off", u64p)]
 
 
+class BwCol(C.Structure):
+    _fields_ = [("width", u8p), ("boff", u64p), ("data", u8p)]
+
+
 class PackedCols(C.Structure):
     _fields_ = [("n_spans", C.c_uint64), ("flags", u8p), ("name_id", u32p), ("dbegin", u32p), ("dur", u32p),
                 ("n_cid", C.c_uint64), ("dcid", u32p), ("n_parent", C.c_uint64), ("parent", u64p),
                 ("n_blocks", C.c_uint64), ("blk_cid_base", u64p), ("blk_cid0", u32p), ("blk_par0", u32p),
-                ("n_esc", C.c_uint64), ("esc_key", u64p), ("esc_val", u64p)]
+                ("n_esc", C.c_uint64), ("esc_key", u64p), ("esc_val", u64p),
+                ("name_bw", BwCol), ("flops_bw", BwCol), ("read_bw", BwCol), ("write_bw", BwCol),
+                ("alloc_bw", BwCol), ("type_bw", BwCol), ("occ_dict_n", C.c_uint32), ("occ_idx_bytes", C.c_uint32),
+                ("occ_dict", C.POINTER(C.c_double)), ("occ_idx", u8p)]
 
 
 class StringTableOut(C.Structure):  # xsp_string_table as returned by the library

@@ -12,6 +12,10 @@
 
 namespace xsp {
 void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_packed_cols* out);
+uint64_t stage_tables_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, const xsp_span_cols* hc, uint64_t s0,
+                             uint64_t s1, uint64_t m0, uint64_t m1, uint64_t l0, uint64_t l1, uint32_t* name_id,
+                             uint64_t* flops, uint64_t* rd, uint64_t* wr, double* occ, int64_t* alloc,
+                             uint32_t* type_id, const std::string& tag, cudaStream_t st, void* deferred);
 uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint64_t s1, uint8_t* flags,
                       uint32_t* name_id, uint64_t* begin, uint64_t* end, uint64_t* cid, uint64_t* parent,
                       const std::string& tag, cudaStream_t st, void* deferred = nullptr);
@@ -552,17 +556,18 @@ XSP_API xsp_status xsp_run_host_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, 
     // single shot: span_id and the tables as xsp_run_host uploads them, the
     // span columns unpacked on the device
     const uint64_t n = pk->n_spans;
+    const uint64_t nm_rows = hc->n_metric_rows, nl_rows = hc->n_layer_rows;
     xsp_span_cols dc;
     dc.n_spans = n;
     dc.span_id = to_dev(ctx, "span_id", hc->span_id, n, st);
-    dc.n_metric_rows = hc->n_metric_rows;
-    dc.flops = to_dev(ctx, "flops", hc->flops, hc->n_metric_rows, st);
-    dc.dram_read = to_dev(ctx, "read", hc->dram_read, hc->n_metric_rows, st);
-    dc.dram_write = to_dev(ctx, "write", hc->dram_write, hc->n_metric_rows, st);
-    dc.occupancy = to_dev(ctx, "occ", hc->occupancy, hc->n_metric_rows, st);
-    dc.n_layer_rows = hc->n_layer_rows;
-    dc.alloc_bytes = to_dev(ctx, "alloc", hc->alloc_bytes, hc->n_layer_rows, st);
-    dc.type_id = to_dev(ctx, "type", hc->type_id, hc->n_layer_rows, st);
+    dc.n_metric_rows = nm_rows;
+    dc.n_layer_rows = nl_rows;
+    uint64_t* d_fl = ctx->d<uint64_t>("pk1.fl", nm_rows + 1);
+    uint64_t* d_rd = ctx->d<uint64_t>("pk1.rd", nm_rows + 1);
+    uint64_t* d_wr = ctx->d<uint64_t>("pk1.wr", nm_rows + 1);
+    double* d_oc = ctx->d<double>("pk1.oc", nm_rows + 1);
+    int64_t* d_al = ctx->d<int64_t>("pk1.al", nl_rows + 1);
+    uint32_t* d_ty = ctx->d<uint32_t>("pk1.ty", nl_rows + 1);
     uint8_t* f = ctx->d<uint8_t>("pk1.f", n + 1);
     uint32_t* nm = ctx->d<uint32_t>("pk1.n", n + 1);
     uint64_t* b = ctx->d<uint64_t>("pk1.b", n + 1);
@@ -570,6 +575,14 @@ XSP_API xsp_status xsp_run_host_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, 
     uint64_t* c = ctx->d<uint64_t>("pk1.c", n + 1);
     uint64_t* p = ctx->d<uint64_t>("pk1.p", n + 1);
     ctx->h2d_bytes += xsp::stage_packed(ctx, pk, 0, n, f, nm, b, e, c, p, "pk1.", st);
+    ctx->h2d_bytes += xsp::stage_tables_packed(ctx, pk, hc, 0, n, 0, nm_rows, 0, nl_rows, nm, d_fl, d_rd, d_wr, d_oc,
+                                               d_al, d_ty, "pk1t.", st, nullptr);
+    dc.flops = d_fl;
+    dc.dram_read = d_rd;
+    dc.dram_write = d_wr;
+    dc.occupancy = d_oc;
+    dc.alloc_bytes = d_al;
+    dc.type_id = d_ty;
     dc.flags = f;
     dc.name_id = nm;
     dc.begin_ns = b;

@@ -10,8 +10,10 @@
 // or >= 2^32 deltas, durations, cid offsets) travel raw in a sorted escape
 // list.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <unordered_map>
 #include <vector>
 
 #include "ctx.h"
@@ -22,6 +24,72 @@ namespace xsp {
 constexpr uint32_t kPB = XSP_PACK_BLOCK;
 
 // ---- host packer -----------------------------------------------------------
+// Byte-width code n values (xsp_bw_col): per block the bytes of its widest value.
+template <typename T>
+void bw_encode(xsp_ctx* ctx, const std::string& tag, const T* v, uint64_t n, xsp_bw_col& out) {
+  const uint64_t nb = (n + kPB - 1) / kPB;
+  uint8_t* w = ctx->h<uint8_t>(tag + ".w", nb + 1);
+  uint64_t* off = ctx->h<uint64_t>(tag + ".o", nb + 1);
+  uint64_t total = 0;
+  for (uint64_t b = 0; b < nb; ++b) {
+    const uint64_t r0 = b * kPB, r1 = std::min(n, r0 + kPB);
+    uint64_t m = 0;
+    for (uint64_t i = r0; i < r1; ++i) m |= (uint64_t)v[i];
+    w[b] = m ? (uint8_t)((64 - __builtin_clzll(m) + 7) / 8) : 0;
+    off[b] = total;
+    total += w[b] * (r1 - r0);
+  }
+  off[nb] = total;
+  uint8_t* d = ctx->h<uint8_t>(tag + ".d", total + 8);
+  for (uint64_t b = 0; b < nb; ++b) {
+    const uint64_t r0 = b * kPB, r1 = std::min(n, r0 + kPB);
+    uint8_t* p = d + off[b];
+    const uint32_t wb = w[b];
+    for (uint64_t i = r0; i < r1; ++i, p += wb) {
+      const uint64_t x = (uint64_t)v[i];
+      std::memcpy(p, &x, wb);  // little-endian host
+    }
+  }
+  out.width = w;
+  out.boff = off;
+  out.data = d;
+}
+
+// Occupancy as u8 / u16 indexes into its distinct values (none if > 65536).
+void occ_encode(xsp_ctx* ctx, const double* v, uint64_t n, xsp_packed_cols* out) {
+  out->occ_dict_n = 0;
+  out->occ_idx_bytes = 0;
+  out->occ_dict = nullptr;
+  out->occ_idx = nullptr;
+  if (!n) return;
+  std::unordered_map<uint64_t, uint32_t> ix;
+  std::vector<double> dict;
+  uint16_t* tmp = ctx->h<uint16_t>("pk.occ.t", n);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t bits;
+    std::memcpy(&bits, v + i, 8);
+    auto it = ix.find(bits);
+    if (it == ix.end()) {
+      if (dict.size() == 65536) return;
+      it = ix.emplace(bits, (uint32_t)dict.size()).first;
+      dict.push_back(v[i]);
+    }
+    tmp[i] = (uint16_t)it->second;
+  }
+  const uint32_t ib = dict.size() <= 256 ? 1 : 2;
+  uint8_t* idx = ctx->h<uint8_t>("pk.occ.i", n * ib + 8);
+  if (ib == 1)
+    for (uint64_t i = 0; i < n; ++i) idx[i] = (uint8_t)tmp[i];
+  else
+    std::memcpy(idx, tmp, n * 2);
+  double* d = ctx->h<double>("pk.occ.d", dict.size());
+  std::memcpy(d, dict.data(), dict.size() * 8);
+  out->occ_dict_n = (uint32_t)dict.size();
+  out->occ_idx_bytes = ib;
+  out->occ_dict = d;
+  out->occ_idx = idx;
+}
+
 void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_packed_cols* out) {
   const uint64_t n = c->n_spans;
   const uint64_t nb = (n + kPB - 1) / kPB;
@@ -104,6 +172,24 @@ void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_p
   out->n_esc = ekey.size();
   out->esc_key = ek;
   out->esc_val = ev;
+  xsp_bw_col none{nullptr, nullptr, nullptr};
+  out->name_bw = out->flops_bw = out->read_bw = out->write_bw = out->alloc_bw = out->type_bw = none;
+  out->occ_dict_n = out->occ_idx_bytes = 0;
+  out->occ_dict = nullptr;
+  out->occ_idx = nullptr;
+  const char* e = std::getenv("XSP_PACK_TABLES");
+  if (e && !std::strcmp(e, "0")) return;
+  bw_encode(ctx, "pk.name", c->name_id, n, out->name_bw);
+  if (c->n_metric_rows) {
+    bw_encode(ctx, "pk.flops", c->flops, c->n_metric_rows, out->flops_bw);
+    bw_encode(ctx, "pk.read", c->dram_read, c->n_metric_rows, out->read_bw);
+    bw_encode(ctx, "pk.write", c->dram_write, c->n_metric_rows, out->write_bw);
+    occ_encode(ctx, c->occupancy, c->n_metric_rows, out);
+  }
+  if (c->n_layer_rows) {
+    bw_encode(ctx, "pk.alloc", c->alloc_bytes, c->n_layer_rows, out->alloc_bw);
+    bw_encode(ctx, "pk.type", c->type_id, c->n_layer_rows, out->type_bw);
+  }
 }
 
 // ---- device unpack -----------------------------------------------------------
@@ -263,7 +349,7 @@ uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint
   uint64_t* d_ek = ctx->d<uint64_t>(tag + "pk.ek", ne + 1);
   uint64_t* d_ev = ctx->d<uint64_t>(tag + "pk.ev", ne + 1);
   h2d(flags, pk->flags + s0, ns);
-  h2d(name_id, pk->name_id + s0, ns * 4);
+  if (!pk->name_bw.width) h2d(name_id, pk->name_id + s0, ns * 4);  // else stage_tables_packed
   h2d(d_dbeg, pk->dbegin + s0, ns * 4);
   h2d(d_dur, pk->dur + s0, ns * 4);
   h2d(d_dcid, pk->dcid + c0, (c1 - c0) * 4);
@@ -300,6 +386,135 @@ uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint
     k_unpack<<<(unsigned)nbk, kPB, 0, st>>>(a);
     ++ctx->launches;
   }
+  return bytes;
+}
+
+// ---- coded name / table columns ----------------------------------------------
+struct BwDev {
+  const uint8_t* width;  // blocks b0 ..
+  const uint64_t* boff;  // blocks b0 .. (global byte offsets)
+  const uint8_t* data;   // the staged bytes from global offset `base`
+  uint64_t base;
+  uint64_t r0, n, b0;    // global first row, rows, first block
+  void* out;
+  uint32_t osz;          // 4 or 8
+};
+constexpr int kTabCols = 6;
+struct TabUnpackArgs {
+  BwDev c[kTabCols];
+  uint32_t ncols;
+  uint32_t idx_bytes;
+  const double* dict;
+  const uint8_t* idx;
+  uint64_t n_occ;        // 0: no occupancy decode
+  double* occ;
+  uint64_t max_n;
+};
+
+// blockIdx.y < ncols: byte-width column y; == ncols: the occupancy dictionary
+__global__ void k_unpack_tables(TabUnpackArgs a) {
+  const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t y = blockIdx.y;
+  if (y < a.ncols) {
+    const BwDev& c = a.c[y];
+    if (v >= c.n) return;
+    const uint64_t row = c.r0 + v;
+    const uint64_t b = row / kPB - c.b0;
+    const uint32_t w = c.width[b];
+    const uint8_t* p = c.data + (c.boff[b] - c.base) + (row % kPB) * w;
+    uint64_t x = 0;
+    for (uint32_t k = 0; k < w; ++k) x |= (uint64_t)p[k] << (8 * k);
+    if (c.osz == 8)
+      static_cast<uint64_t*>(c.out)[v] = x;
+    else
+      static_cast<uint32_t*>(c.out)[v] = (uint32_t)x;
+  } else {
+    if (v >= a.n_occ) return;
+    const uint32_t k = a.idx_bytes == 1 ? a.idx[v] : (uint32_t)a.idx[2 * v] | (uint32_t)a.idx[2 * v + 1] << 8;
+    a.occ[v] = a.dict[k];
+  }
+}
+
+void launch_unpack_tables(xsp_ctx* ctx, const void* args, cudaStream_t st) {
+  const TabUnpackArgs& a = *static_cast<const TabUnpackArgs*>(args);
+  const uint32_t ny = a.ncols + (a.n_occ ? 1 : 0);
+  if (!ny || !a.max_n) return;
+  k_unpack_tables<<<dim3((unsigned)((a.max_n + 255) / 256), ny), 256, 0, st>>>(a);
+  ++ctx->launches;
+}
+
+size_t unpack_tables_args_bytes() { return sizeof(TabUnpackArgs); }
+
+// Stages name_id rows [s0, s1), metric rows [m0, m1) and layer rows [l0, l1)
+// into dst's device columns: coded columns as their covering blocks (decoded
+// by k_unpack_tables, deferred like k_unpack when `deferred` is given), the
+// others raw. Returns the H2D bytes issued.
+uint64_t stage_tables_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, const xsp_span_cols* hc, uint64_t s0,
+                             uint64_t s1, uint64_t m0, uint64_t m1, uint64_t l0, uint64_t l1, uint32_t* name_id,
+                             uint64_t* flops, uint64_t* rd, uint64_t* wr, double* occ, int64_t* alloc,
+                             uint32_t* type_id, const std::string& tag, cudaStream_t st, void* deferred) {
+  uint64_t bytes = 0;
+  auto h2d = [&](void* d, const void* h, uint64_t nbytes) {
+    if (!nbytes) return;
+    XSP_CUDA(cudaMemcpyAsync(d, h, nbytes, cudaMemcpyHostToDevice, st));
+    bytes += nbytes;
+  };
+  TabUnpackArgs a;
+  std::memset(&a, 0, sizeof(a));
+  auto col = [&](const char* nm, const xsp_bw_col& bw, const void* raw, uint32_t esz, uint64_t r0, uint64_t r1,
+                 void* out) {
+    const uint64_t n = r1 - r0;
+    if (!n) return;
+    if (!bw.width) {
+      h2d(out, static_cast<const char*>(raw) + r0 * esz, n * esz);
+      return;
+    }
+    const uint64_t b0 = r0 / kPB, b1 = (r1 + kPB - 1) / kPB, nbk = b1 - b0;
+    const uint64_t d0 = bw.boff[b0], d1 = bw.boff[b1];
+    uint8_t* dw = ctx->d<uint8_t>(tag + nm + ".w", nbk);
+    uint64_t* doff = ctx->d<uint64_t>(tag + nm + ".o", nbk);
+    uint8_t* dd = ctx->d<uint8_t>(tag + nm + ".d", d1 - d0 + 8);
+    h2d(dw, bw.width + b0, nbk);
+    h2d(doff, bw.boff + b0, nbk * 8);
+    h2d(dd, bw.data + d0, d1 - d0);
+    BwDev& c = a.c[a.ncols++];
+    c.width = dw;
+    c.boff = doff;
+    c.data = dd;
+    c.base = d0;
+    c.r0 = r0;
+    c.n = n;
+    c.b0 = b0;
+    c.out = out;
+    c.osz = esz;
+    a.max_n = std::max(a.max_n, n);
+  };
+  col("name", pk->name_bw, pk->name_id, 4, s0, s1, name_id);
+  col("flops", pk->flops_bw, hc->flops, 8, m0, m1, flops);
+  col("read", pk->read_bw, hc->dram_read, 8, m0, m1, rd);
+  col("write", pk->write_bw, hc->dram_write, 8, m0, m1, wr);
+  col("alloc", pk->alloc_bw, hc->alloc_bytes, 8, l0, l1, alloc);
+  col("type", pk->type_bw, hc->type_id, 4, l0, l1, type_id);
+  if (m1 > m0) {
+    if (pk->occ_dict_n) {
+      double* dd = ctx->d<double>(tag + "occ.d", pk->occ_dict_n);
+      uint8_t* di = ctx->d<uint8_t>(tag + "occ.i", (m1 - m0) * pk->occ_idx_bytes + 8);
+      h2d(dd, pk->occ_dict, pk->occ_dict_n * 8ull);
+      h2d(di, pk->occ_idx + m0 * pk->occ_idx_bytes, (m1 - m0) * pk->occ_idx_bytes);
+      a.dict = dd;
+      a.idx = di;
+      a.idx_bytes = pk->occ_idx_bytes;
+      a.n_occ = m1 - m0;
+      a.occ = occ;
+      a.max_n = std::max(a.max_n, m1 - m0);
+    } else {
+      h2d(occ, hc->occupancy + m0, (m1 - m0) * 8);
+    }
+  }
+  if (deferred)
+    std::memcpy(deferred, &a, sizeof(a));
+  else
+    launch_unpack_tables(ctx, &a, st);
   return bytes;
 }
 

@@ -163,6 +163,12 @@ uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint
                       uint32_t* name_id, uint64_t* begin, uint64_t* end, uint64_t* cid, uint64_t* parent,
                       const std::string& tag, cudaStream_t st, void* deferred);
 void launch_unpack(xsp_ctx* ctx, const void* args, cudaStream_t st);
+uint64_t stage_tables_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, const xsp_span_cols* hc, uint64_t s0,
+                             uint64_t s1, uint64_t m0, uint64_t m1, uint64_t l0, uint64_t l1, uint32_t* name_id,
+                             uint64_t* flops, uint64_t* rd, uint64_t* wr, double* occ, int64_t* alloc,
+                             uint32_t* type_id, const std::string& tag, cudaStream_t st, void* deferred);
+void launch_unpack_tables(xsp_ctx* ctx, const void* args, cudaStream_t st);
+size_t unpack_tables_args_bytes();
 size_t unpack_args_bytes();
 
 bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht, const xsp_groups* groups,
@@ -216,6 +222,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
   }
   if (ch.size() < 2) return false;
   if (unpack_args_bytes() > 256) throw std::logic_error("UnpackArgs outgrew its slot");
+  if (unpack_tables_args_bytes() > 512) throw std::logic_error("TabUnpackArgs outgrew its slot");
   uint64_t max_n = 0;
   uint32_t max_t = 0;
   for (auto& c : ch) {
@@ -248,6 +255,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     uint64_t* h_off;  // pinned staging of the re-based trace offsets
     uint64_t* sid_buf;  // device span_id column (unused while span_id is read zero-copy)
     alignas(16) unsigned char unpack[256];  // deferred k_unpack arguments (packed input)
+    alignas(16) unsigned char tab_unpack[512];  // deferred k_unpack_tables arguments
     cudaEvent_t in_ready, free;
     cudaEvent_t computed, out_done;  // this parity's ctx buffers: results ready / copied out
   } slot[2];
@@ -335,12 +343,21 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
       throw std::invalid_argument("metric/layer table shorter than the span flags imply");
     m_run = C.m1;
     l_run = C.l1;
-    h2d(const_cast<uint64_t*>(S.cols.flops), hc->flops + C.m0, mc * 8);
-    h2d(const_cast<uint64_t*>(S.cols.dram_read), hc->dram_read + C.m0, mc * 8);
-    h2d(const_cast<uint64_t*>(S.cols.dram_write), hc->dram_write + C.m0, mc * 8);
-    h2d(const_cast<double*>(S.cols.occupancy), hc->occupancy + C.m0, mc * 8);
-    h2d(const_cast<int64_t*>(S.cols.alloc_bytes), hc->alloc_bytes + C.l0, lc * 8);
-    h2d(const_cast<uint32_t*>(S.cols.type_id), hc->type_id + C.l0, lc * 4);
+    if (pk) {  // coded name_id / tables: decoded on the work stream with the span columns
+      ctx->h2d_bytes += stage_tables_packed(
+          ctx, pk, hc, s0, C.s1, C.m0, C.m1, C.l0, C.l1, const_cast<uint32_t*>(S.cols.name_id),
+          const_cast<uint64_t*>(S.cols.flops), const_cast<uint64_t*>(S.cols.dram_read),
+          const_cast<uint64_t*>(S.cols.dram_write), const_cast<double*>(S.cols.occupancy),
+          const_cast<int64_t*>(S.cols.alloc_bytes), const_cast<uint32_t*>(S.cols.type_id),
+          "plt" + std::to_string(c & 1) + ".", cs, S.tab_unpack);
+    } else {
+      h2d(const_cast<uint64_t*>(S.cols.flops), hc->flops + C.m0, mc * 8);
+      h2d(const_cast<uint64_t*>(S.cols.dram_read), hc->dram_read + C.m0, mc * 8);
+      h2d(const_cast<uint64_t*>(S.cols.dram_write), hc->dram_write + C.m0, mc * 8);
+      h2d(const_cast<double*>(S.cols.occupancy), hc->occupancy + C.m0, mc * 8);
+      h2d(const_cast<int64_t*>(S.cols.alloc_bytes), hc->alloc_bytes + C.l0, lc * 8);
+      h2d(const_cast<uint32_t*>(S.cols.type_id), hc->type_id + C.l0, lc * 4);
+    }
     const uint32_t nt = C.t1 - C.t0;
     for (uint32_t t = 0; t <= nt; ++t) S.h_off[t] = off[C.t0 + t] - s0;
     h2d(const_cast<uint64_t*>(S.tr.span_off), S.h_off, ((uint64_t)nt + 1) * 8);
@@ -408,7 +425,10 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     XSP_CUDA(cudaStreamWaitEvent(ws, S.in_ready, 0));
     // this parity's ctx buffers are free once chunk c-2's results are copied out
     if (c >= 2) XSP_CUDA(cudaStreamWaitEvent(ws, S.out_done, 0));
-    if (pk) launch_unpack(ctx, S.unpack, ws);  // packed input: rebuild the span columns first
+    if (pk) {  // packed input: rebuild the span columns and tables first
+      launch_unpack(ctx, S.unpack, ws);
+      launch_unpack_tables(ctx, S.tab_unpack, ws);
+    }
     ctx->tag = (c & 1) ? "#p1" : "#p0";
     xsp_corr_out dcorr;
     std::memset(&dcorr, 0, sizeof(dcorr));

@@ -93,3 +93,68 @@ def test_host_outputs_rows_only(engine, monkeypatch, chunk):
     same(c1, c0)
     with pytest.raises(capi.XspError):
         engine.set_host_outputs(7)
+
+
+def _bw_decode(col, n):
+    """include/xsp.h xsp_bw_col, decoded with numpy (the wire format as documented)."""
+    import ctypes as C
+    nb = (n + 255) // 256
+    w = np.ctypeslib.as_array(col.width, shape=(nb,)).copy()
+    off = np.ctypeslib.as_array(col.boff, shape=(nb + 1,)).copy()
+    data = np.frombuffer((C.c_uint8 * int(off[-1] + 8)).from_address(C.cast(col.data, C.c_void_p).value),
+                         dtype=np.uint8)
+    out = np.zeros(n, dtype=np.uint64)
+    for b in range(nb):
+        r0, r1 = b * 256, min(n, b * 256 + 256)
+        wb = int(w[b])
+        if wb:
+            raw = data[off[b]:off[b] + wb * (r1 - r0)].reshape(r1 - r0, wb).astype(np.uint64)
+            out[r0:r1] = (raw << (np.arange(wb, dtype=np.uint64) * np.uint64(8))).sum(axis=1, dtype=np.uint64)
+    return out
+
+
+def test_packed_tables_wire_format(engine, monkeypatch):
+    """The coded name / metric / layer columns decode (numpy, per the header's
+    description) to the host columns; edge values: all-zero blocks (width 0),
+    full 64-bit counters, negative alloc_bytes (two's complement), more than
+    65536 distinct occupancies (dictionary off -> raw), and the device decode
+    equals the raw upload bit for bit."""
+    b, gf, gr, gb = synth.c3(runs=3, n_models=6, max_layers=400)
+    b.flops = b.flops.copy()
+    b.flops[:300] = 0
+    b.flops[700] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    b.alloc_bytes = b.alloc_bytes.copy()
+    b.alloc_bytes[5] = -12345
+    pk = engine.pack_host(b)
+    assert np.array_equal(_bw_decode(pk.name_bw, b.n_spans), b.name_id.astype(np.uint64))
+    m, l_ = len(b.flops), len(b.alloc_bytes)
+    assert np.array_equal(_bw_decode(pk.flops_bw, m), b.flops)
+    assert np.array_equal(_bw_decode(pk.read_bw, m), b.dram_read)
+    assert np.array_equal(_bw_decode(pk.write_bw, m), b.dram_write)
+    assert np.array_equal(_bw_decode(pk.alloc_bw, l_).view(np.int64), b.alloc_bytes)
+    assert np.array_equal(_bw_decode(pk.type_bw, l_), b.type_id.astype(np.uint64))
+    assert pk.flops_bw.width[0] == 0
+    assert 0 < pk.occ_dict_n <= 256 and pk.occ_idx_bytes == 1
+    d = np.ctypeslib.as_array(pk.occ_dict, shape=(pk.occ_dict_n,))
+    ix = np.ctypeslib.as_array(pk.occ_idx, shape=(m,))
+    assert np.array_equal(d[ix].view(np.uint64), b.occupancy.view(np.uint64))
+    for chunk in (0, 40_000):
+        run_both(engine, b, (gf, gr, gb), chunk, monkeypatch)
+    # many distinct occupancies: raw fallback, still equal
+    b.occupancy = np.random.default_rng(5).random(m)
+    pk = engine.pack_host(b)
+    assert pk.occ_dict_n == (0 if m > 65536 else pk.occ_dict_n)
+    run_both(engine, b, (gf, gr, gb), 40_000, monkeypatch)
+
+
+@pytest.mark.parametrize("chunk", [0, 50_000])
+def test_packed_tables_off(engine, monkeypatch, chunk):
+    """XSP_PACK_TABLES=0: name_id and the tables travel raw; results equal, and
+    the coded form moves fewer bytes."""
+    b, gf, gr, gb = synth.c3(runs=3, n_models=6, max_layers=400)
+    h_coded = run_both(engine, b, (gf, gr, gb), chunk, monkeypatch)[1]
+    monkeypatch.setenv("XSP_PACK_TABLES", "0")
+    pk = engine.pack_host(b)
+    assert not pk.name_bw.width and not pk.flops_bw.width and pk.occ_dict_n == 0
+    h_raw = run_both(engine, b, (gf, gr, gb), chunk, monkeypatch)[1]
+    assert h_coded < h_raw, (h_coded, h_raw)
