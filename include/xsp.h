@@ -494,6 +494,10 @@ typedef struct xsp_packed_cols {
   uint32_t occ_idx_bytes;  /* 1 (<= 256 values) or 2 (<= 65536) */
   const double* occ_dict;
   const uint8_t* occ_idx;  /* [n_metric_rows * occ_idx_bytes], little-endian */
+  /* dbegin / dur / dcid + 1 (mod 2^32, so XSP_PACK_ESC codes as 0), byte-width
+   * coded; a NULL width sends the raw u32 arrays above */
+  xsp_bw_col dbegin_bw, dur_bw; /* n_spans values */
+  xsp_bw_col dcid_bw;           /* n_cid values */
 } xsp_packed_cols;
 xsp_status xsp_pack_host(xsp_ctx* ctx, const xsp_span_cols* host_cols, const xsp_traces* host_traces,
                          xsp_packed_cols* out);

@@ -185,7 +185,8 @@ class PackedCols(C.Structure):
                 ("n_esc", C.c_uint64), ("esc_key", u64p), ("esc_val", u64p),
                 ("name_bw", BwCol), ("flops_bw", BwCol), ("read_bw", BwCol), ("write_bw", BwCol),
                 ("alloc_bw", BwCol), ("type_bw", BwCol), ("occ_dict_n", C.c_uint32), ("occ_idx_bytes", C.c_uint32),
-                ("occ_dict", C.POINTER(C.c_double)), ("occ_idx", u8p)]
+                ("occ_dict", C.POINTER(C.c_double)), ("occ_idx", u8p),
+                ("dbegin_bw", BwCol), ("dur_bw", BwCol), ("dcid_bw", BwCol)]
 
 
 class StringTableOut(C.Structure):  # xsp_string_table as returned by the library

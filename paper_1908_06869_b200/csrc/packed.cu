@@ -174,12 +174,22 @@ void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_p
   out->esc_val = ev;
   xsp_bw_col none{nullptr, nullptr, nullptr};
   out->name_bw = out->flops_bw = out->read_bw = out->write_bw = out->alloc_bw = out->type_bw = none;
+  out->dbegin_bw = out->dur_bw = out->dcid_bw = none;
   out->occ_dict_n = out->occ_idx_bytes = 0;
   out->occ_dict = nullptr;
   out->occ_idx = nullptr;
   const char* e = std::getenv("XSP_PACK_TABLES");
   if (e && !std::strcmp(e, "0")) return;
   bw_encode(ctx, "pk.name", c->name_id, n, out->name_bw);
+  {  // the delta lists + 1 (XSP_PACK_ESC wraps to 0)
+    uint32_t* p1 = ctx->h<uint32_t>("pk.p1", std::max(n, ncid) + 1);
+    for (uint64_t i = 0; i < n; ++i) p1[i] = dbeg[i] + 1u;
+    bw_encode(ctx, "pk.xb", p1, n, out->dbegin_bw);
+    for (uint64_t i = 0; i < n; ++i) p1[i] = dur[i] + 1u;
+    bw_encode(ctx, "pk.xd", p1, n, out->dur_bw);
+    for (uint64_t i = 0; i < ncid; ++i) p1[i] = dcid[i] + 1u;
+    bw_encode(ctx, "pk.xc", p1, ncid, out->dcid_bw);
+  }
   if (c->n_metric_rows) {
     bw_encode(ctx, "pk.flops", c->flops, c->n_metric_rows, out->flops_bw);
     bw_encode(ctx, "pk.read", c->dram_read, c->n_metric_rows, out->read_bw);
@@ -297,8 +307,107 @@ __global__ void __launch_bounds__(kPB) k_unpack(UnpackArgs a) {
   a.parent_out[r] = (f & XSP_F_PARENT) ? a.parent[pbefore + pp] : 0;
 }
 
+
+// ---- coded name / table columns ----------------------------------------------
+struct BwDev {
+  const uint8_t* width;  // blocks b0 ..
+  const uint64_t* boff;  // blocks b0 .. (global byte offsets)
+  const uint8_t* data;   // the staged bytes from global offset `base`
+  uint64_t base;
+  uint64_t r0, n, b0;    // global first row, rows, first block
+  void* out;
+  uint32_t osz;          // 4 or 8
+  uint32_t sub1;         // decode to value - 1 (mod 2^32): the +1-coded delta lists
+};
+constexpr int kTabCols = 6;  // name_id, flops, dram_read, dram_write, alloc_bytes, type_id
+struct TabUnpackArgs {
+  BwDev c[kTabCols];
+  uint32_t ncols;
+  uint32_t idx_bytes;
+  const double* dict;
+  const uint8_t* idx;
+  uint64_t n_occ;        // 0: no occupancy decode
+  double* occ;
+  uint64_t max_n;
+};
+
+// blockIdx.y < ncols: byte-width column y; == ncols: the occupancy dictionary
+__global__ void k_unpack_tables(TabUnpackArgs a) {
+  const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t y = blockIdx.y;
+  if (y < a.ncols) {
+    const BwDev& c = a.c[y];
+    if (v >= c.n) return;
+    const uint64_t row = c.r0 + v;
+    const uint64_t b = row / kPB - c.b0;
+    const uint32_t w = c.width[b];
+    const uint8_t* p = c.data + (c.boff[b] - c.base) + (row % kPB) * w;
+    uint64_t x = 0;
+    for (uint32_t k = 0; k < w; ++k) x |= (uint64_t)p[k] << (8 * k);
+    if (c.osz == 8)
+      static_cast<uint64_t*>(c.out)[v] = x;
+    else
+      static_cast<uint32_t*>(c.out)[v] = (uint32_t)x - c.sub1;
+  } else {
+    if (v >= a.n_occ) return;
+    const uint32_t k = a.idx_bytes == 1 ? a.idx[v] : (uint32_t)a.idx[2 * v] | (uint32_t)a.idx[2 * v + 1] << 8;
+    a.occ[v] = a.dict[k];
+  }
+}
+
+void launch_unpack_tables(xsp_ctx* ctx, const void* args, cudaStream_t st) {
+  const TabUnpackArgs& a = *static_cast<const TabUnpackArgs*>(args);
+  const uint32_t ny = a.ncols + (a.n_occ ? 1 : 0);
+  if (!ny || !a.max_n) return;
+  k_unpack_tables<<<dim3((unsigned)((a.max_n + 255) / 256), ny), 256, 0, st>>>(a);
+  ++ctx->launches;
+}
+
+size_t unpack_tables_args_bytes() { return sizeof(TabUnpackArgs); }
+
+// Stage rows [r0, r1) of a coded column (its covering blocks) and append its
+// decode to `a`; a column without a width array goes raw (`raw`, esz bytes per row).
+uint64_t stage_bw(xsp_ctx* ctx, TabUnpackArgs& a, const std::string& tag, const xsp_bw_col& bw, const void* raw,
+                  uint32_t esz, uint64_t r0, uint64_t r1, void* out, cudaStream_t st, uint32_t sub1 = 0) {
+  const uint64_t n = r1 - r0;
+  if (!n) return 0;
+  uint64_t bytes = 0;
+  auto h2d = [&](void* d, const void* h, uint64_t nbytes) {
+    if (!nbytes) return;
+    XSP_CUDA(cudaMemcpyAsync(d, h, nbytes, cudaMemcpyHostToDevice, st));
+    bytes += nbytes;
+  };
+  if (!bw.width) {
+    h2d(out, static_cast<const char*>(raw) + r0 * esz, n * esz);
+    return bytes;
+  }
+  if (a.ncols == (uint32_t)kTabCols) throw std::logic_error("TabUnpackArgs: too many coded columns");
+  const uint64_t b0 = r0 / kPB, b1 = (r1 + kPB - 1) / kPB, nbk = b1 - b0;
+  const uint64_t d0 = bw.boff[b0], d1 = bw.boff[b1];
+  uint8_t* dw = ctx->d<uint8_t>(tag + ".w", nbk);
+  uint64_t* doff = ctx->d<uint64_t>(tag + ".o", nbk);
+  uint8_t* dd = ctx->d<uint8_t>(tag + ".d", d1 - d0 + 8);
+  h2d(dw, bw.width + b0, nbk);
+  h2d(doff, bw.boff + b0, nbk * 8);
+  h2d(dd, bw.data + d0, d1 - d0);
+  BwDev& c = a.c[a.ncols++];
+  c.width = dw;
+  c.boff = doff;
+  c.data = dd;
+  c.base = d0;
+  c.r0 = r0;
+  c.n = n;
+  c.b0 = b0;
+  c.out = out;
+  c.osz = esz;
+  c.sub1 = sub1;
+  a.max_n = std::max(a.max_n, n);
+  return bytes;
+}
+
 void launch_unpack(xsp_ctx* ctx, const void* args, cudaStream_t st) {
-  const UnpackArgs& a = *static_cast<const UnpackArgs*>(args);
+  launch_unpack_tables(ctx, args, st);  // the coded delta lists first
+  const UnpackArgs& a = *reinterpret_cast<const UnpackArgs*>(static_cast<const char*>(args) + sizeof(TabUnpackArgs));
   const uint64_t nbk = (a.s1 + kPB - 1) / kPB - a.b0;
   if (a.s1 > a.s0) {
     k_unpack<<<(unsigned)nbk, kPB, 0, st>>>(a);
@@ -306,7 +415,7 @@ void launch_unpack(xsp_ctx* ctx, const void* args, cudaStream_t st) {
   }
 }
 
-size_t unpack_args_bytes() { return sizeof(UnpackArgs); }
+size_t unpack_args_bytes() { return sizeof(TabUnpackArgs) + sizeof(UnpackArgs); }
 
 // Stages rows [s0, s1) of a packed batch on stream st into the device columns
 // of `dst` (begin / end / cid / parent_id rebuilt; flags and name_id copied),
@@ -350,9 +459,13 @@ uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint
   uint64_t* d_ev = ctx->d<uint64_t>(tag + "pk.ev", ne + 1);
   h2d(flags, pk->flags + s0, ns);
   if (!pk->name_bw.width) h2d(name_id, pk->name_id + s0, ns * 4);  // else stage_tables_packed
-  h2d(d_dbeg, pk->dbegin + s0, ns * 4);
-  h2d(d_dur, pk->dur + s0, ns * 4);
-  h2d(d_dcid, pk->dcid + c0, (c1 - c0) * 4);
+  // the u32 delta lists, byte-width coded (+1) or raw; decoded by k_unpack_tables
+  // into d_dbeg / d_dur / d_dcid before k_unpack reads them
+  TabUnpackArgs pre;
+  std::memset(&pre, 0, sizeof(pre));
+  bytes += stage_bw(ctx, pre, tag + "pk.xb", pk->dbegin_bw, pk->dbegin, 4, s0, s1, d_dbeg, st, 1);
+  bytes += stage_bw(ctx, pre, tag + "pk.xd", pk->dur_bw, pk->dur, 4, s0, s1, d_dur, st, 1);
+  bytes += stage_bw(ctx, pre, tag + "pk.xc", pk->dcid_bw, pk->dcid, 4, c0, c1, d_dcid, st, 1);
   h2d(d_par, pk->parent + p0, (p1 - p0) * 8);
   h2d(d_cb, pk->blk_cid_base + b0, nbk * 8);
   h2d(d_c0, pk->blk_cid0 + b0, nbk * 4);
@@ -380,70 +493,16 @@ uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint
   a.end = end;
   a.cid = cid;
   a.parent_out = parent;
-  if (deferred) {
-    std::memcpy(deferred, &a, sizeof(a));
+  if (deferred) {  // [TabUnpackArgs pre][UnpackArgs a]: launch_unpack runs both in order
+    std::memcpy(deferred, &pre, sizeof(pre));
+    std::memcpy(static_cast<char*>(deferred) + sizeof(pre), &a, sizeof(a));
   } else {
+    launch_unpack_tables(ctx, &pre, st);
     k_unpack<<<(unsigned)nbk, kPB, 0, st>>>(a);
     ++ctx->launches;
   }
   return bytes;
 }
-
-// ---- coded name / table columns ----------------------------------------------
-struct BwDev {
-  const uint8_t* width;  // blocks b0 ..
-  const uint64_t* boff;  // blocks b0 .. (global byte offsets)
-  const uint8_t* data;   // the staged bytes from global offset `base`
-  uint64_t base;
-  uint64_t r0, n, b0;    // global first row, rows, first block
-  void* out;
-  uint32_t osz;          // 4 or 8
-};
-constexpr int kTabCols = 6;
-struct TabUnpackArgs {
-  BwDev c[kTabCols];
-  uint32_t ncols;
-  uint32_t idx_bytes;
-  const double* dict;
-  const uint8_t* idx;
-  uint64_t n_occ;        // 0: no occupancy decode
-  double* occ;
-  uint64_t max_n;
-};
-
-// blockIdx.y < ncols: byte-width column y; == ncols: the occupancy dictionary
-__global__ void k_unpack_tables(TabUnpackArgs a) {
-  const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t y = blockIdx.y;
-  if (y < a.ncols) {
-    const BwDev& c = a.c[y];
-    if (v >= c.n) return;
-    const uint64_t row = c.r0 + v;
-    const uint64_t b = row / kPB - c.b0;
-    const uint32_t w = c.width[b];
-    const uint8_t* p = c.data + (c.boff[b] - c.base) + (row % kPB) * w;
-    uint64_t x = 0;
-    for (uint32_t k = 0; k < w; ++k) x |= (uint64_t)p[k] << (8 * k);
-    if (c.osz == 8)
-      static_cast<uint64_t*>(c.out)[v] = x;
-    else
-      static_cast<uint32_t*>(c.out)[v] = (uint32_t)x;
-  } else {
-    if (v >= a.n_occ) return;
-    const uint32_t k = a.idx_bytes == 1 ? a.idx[v] : (uint32_t)a.idx[2 * v] | (uint32_t)a.idx[2 * v + 1] << 8;
-    a.occ[v] = a.dict[k];
-  }
-}
-
-void launch_unpack_tables(xsp_ctx* ctx, const void* args, cudaStream_t st) {
-  const TabUnpackArgs& a = *static_cast<const TabUnpackArgs*>(args);
-  const uint32_t ny = a.ncols + (a.n_occ ? 1 : 0);
-  if (!ny || !a.max_n) return;
-  k_unpack_tables<<<dim3((unsigned)((a.max_n + 255) / 256), ny), 256, 0, st>>>(a);
-  ++ctx->launches;
-}
-
-size_t unpack_tables_args_bytes() { return sizeof(TabUnpackArgs); }
 
 // Stages name_id rows [s0, s1), metric rows [m0, m1) and layer rows [l0, l1)
 // into dst's device columns: coded columns as their covering blocks (decoded
@@ -461,40 +520,12 @@ uint64_t stage_tables_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, const xsp_
   };
   TabUnpackArgs a;
   std::memset(&a, 0, sizeof(a));
-  auto col = [&](const char* nm, const xsp_bw_col& bw, const void* raw, uint32_t esz, uint64_t r0, uint64_t r1,
-                 void* out) {
-    const uint64_t n = r1 - r0;
-    if (!n) return;
-    if (!bw.width) {
-      h2d(out, static_cast<const char*>(raw) + r0 * esz, n * esz);
-      return;
-    }
-    const uint64_t b0 = r0 / kPB, b1 = (r1 + kPB - 1) / kPB, nbk = b1 - b0;
-    const uint64_t d0 = bw.boff[b0], d1 = bw.boff[b1];
-    uint8_t* dw = ctx->d<uint8_t>(tag + nm + ".w", nbk);
-    uint64_t* doff = ctx->d<uint64_t>(tag + nm + ".o", nbk);
-    uint8_t* dd = ctx->d<uint8_t>(tag + nm + ".d", d1 - d0 + 8);
-    h2d(dw, bw.width + b0, nbk);
-    h2d(doff, bw.boff + b0, nbk * 8);
-    h2d(dd, bw.data + d0, d1 - d0);
-    BwDev& c = a.c[a.ncols++];
-    c.width = dw;
-    c.boff = doff;
-    c.data = dd;
-    c.base = d0;
-    c.r0 = r0;
-    c.n = n;
-    c.b0 = b0;
-    c.out = out;
-    c.osz = esz;
-    a.max_n = std::max(a.max_n, n);
-  };
-  col("name", pk->name_bw, pk->name_id, 4, s0, s1, name_id);
-  col("flops", pk->flops_bw, hc->flops, 8, m0, m1, flops);
-  col("read", pk->read_bw, hc->dram_read, 8, m0, m1, rd);
-  col("write", pk->write_bw, hc->dram_write, 8, m0, m1, wr);
-  col("alloc", pk->alloc_bw, hc->alloc_bytes, 8, l0, l1, alloc);
-  col("type", pk->type_bw, hc->type_id, 4, l0, l1, type_id);
+  bytes += stage_bw(ctx, a, tag + "name", pk->name_bw, pk->name_id, 4, s0, s1, name_id, st);
+  bytes += stage_bw(ctx, a, tag + "flops", pk->flops_bw, hc->flops, 8, m0, m1, flops, st);
+  bytes += stage_bw(ctx, a, tag + "read", pk->read_bw, hc->dram_read, 8, m0, m1, rd, st);
+  bytes += stage_bw(ctx, a, tag + "write", pk->write_bw, hc->dram_write, 8, m0, m1, wr, st);
+  bytes += stage_bw(ctx, a, tag + "alloc", pk->alloc_bw, hc->alloc_bytes, 8, l0, l1, alloc, st);
+  bytes += stage_bw(ctx, a, tag + "type", pk->type_bw, hc->type_id, 4, l0, l1, type_id, st);
   if (m1 > m0) {
     if (pk->occ_dict_n) {
       double* dd = ctx->d<double>(tag + "occ.d", pk->occ_dict_n);

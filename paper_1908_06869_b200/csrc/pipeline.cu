@@ -174,7 +174,7 @@ size_t unpack_args_bytes();
 bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* ht, const xsp_groups* groups,
                       const xsp_system_spec* spec, const xsp_analysis_opts* opts, xsp_corr_out* corr_host,
                       xsp_tables_out* tab_host, const xsp_packed_cols* pk) {
-  uint64_t target = 6000000;
+  uint64_t target = 12000000;
   if (const char* e = std::getenv("XSP_CHUNK_SPANS")) target = std::strtoull(e, nullptr, 10);
   const uint64_t n = hc->n_spans;
   const uint32_t T = ht->n_traces, G = groups->n_groups;
@@ -204,24 +204,32 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     c.t1 = T;
     c.g1 = G;
     // the compute + D2H of the final chunk is the only part not hidden behind
-    // the input stream: cut the last chunk ~2/3 : 1/3 at a group boundary
-    const uint64_t rem = off[T] - off[c.t0];
-    for (uint32_t g = c.g0; g + 1 < G; ++g) {
-      const uint64_t end_t = (uint64_t)groups->first_trace[g] + groups->n_runs[g];
-      if (3 * (off[end_t] - off[c.t0]) >= 2 * rem) {
-        Chunk a = c;
-        a.t1 = groups->first_trace[g + 1];
-        a.g1 = g + 1;
-        ch.push_back(a);
-        c.t0 = a.t1;
-        c.g0 = g + 1;
-        break;
+    // the input stream: cut the tail geometrically (~2/3 : 1/3 at group
+    // boundaries) until the last chunk is below min(target / 4, 2 M) spans
+    const uint64_t tail_min = std::min<uint64_t>(target / 4, 2000000);
+    for (;;) {
+      const uint64_t rem = off[T] - off[c.t0];
+      if (rem <= tail_min) break;
+      bool cut = false;
+      for (uint32_t g = c.g0; g + 1 < G; ++g) {
+        const uint64_t end_t = (uint64_t)groups->first_trace[g] + groups->n_runs[g];
+        if (3 * (off[end_t] - off[c.t0]) >= 2 * rem) {
+          Chunk a = c;
+          a.t1 = groups->first_trace[g + 1];
+          a.g1 = g + 1;
+          ch.push_back(a);
+          c.t0 = a.t1;
+          c.g0 = g + 1;
+          cut = true;
+          break;
+        }
       }
+      if (!cut) break;
     }
     ch.push_back(c);
   }
   if (ch.size() < 2) return false;
-  if (unpack_args_bytes() > 256) throw std::logic_error("UnpackArgs outgrew its slot");
+  if (unpack_args_bytes() > 1024) throw std::logic_error("UnpackArgs outgrew its slot");
   if (unpack_tables_args_bytes() > 512) throw std::logic_error("TabUnpackArgs outgrew its slot");
   uint64_t max_n = 0;
   uint32_t max_t = 0;
@@ -254,7 +262,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     xsp_traces tr;
     uint64_t* h_off;  // pinned staging of the re-based trace offsets
     uint64_t* sid_buf;  // device span_id column (unused while span_id is read zero-copy)
-    alignas(16) unsigned char unpack[256];  // deferred k_unpack arguments (packed input)
+    alignas(16) unsigned char unpack[1024];  // deferred k_unpack (+ delta-list decode) arguments
     alignas(16) unsigned char tab_unpack[512];  // deferred k_unpack_tables arguments
     cudaEvent_t in_ready, free;
     cudaEvent_t computed, out_done;  // this parity's ctx buffers: results ready / copied out

@@ -134,6 +134,11 @@ def test_packed_tables_wire_format(engine, monkeypatch):
     assert np.array_equal(_bw_decode(pk.alloc_bw, l_).view(np.int64), b.alloc_bytes)
     assert np.array_equal(_bw_decode(pk.type_bw, l_), b.type_id.astype(np.uint64))
     assert pk.flops_bw.width[0] == 0
+    # the u32 delta lists travel + 1 (the escape code wraps to 0)
+    n, nc = b.n_spans, int(pk.n_cid)
+    for bw, raw, cnt in ((pk.dbegin_bw, pk.dbegin, n), (pk.dur_bw, pk.dur, n), (pk.dcid_bw, pk.dcid, nc)):
+        dec = (_bw_decode(bw, cnt) - np.uint64(1)).astype(np.uint32)
+        assert np.array_equal(dec, np.ctypeslib.as_array(raw, shape=(cnt,))), cnt
     assert 0 < pk.occ_dict_n <= 256 and pk.occ_idx_bytes == 1
     d = np.ctypeslib.as_array(pk.occ_dict, shape=(pk.occ_dict_n,))
     ix = np.ctypeslib.as_array(pk.occ_idx, shape=(m,))
@@ -155,6 +160,6 @@ def test_packed_tables_off(engine, monkeypatch, chunk):
     h_coded = run_both(engine, b, (gf, gr, gb), chunk, monkeypatch)[1]
     monkeypatch.setenv("XSP_PACK_TABLES", "0")
     pk = engine.pack_host(b)
-    assert not pk.name_bw.width and not pk.flops_bw.width and pk.occ_dict_n == 0
+    assert not pk.name_bw.width and not pk.flops_bw.width and pk.occ_dict_n == 0 and not pk.dbegin_bw.width
     h_raw = run_both(engine, b, (gf, gr, gb), chunk, monkeypatch)[1]
     assert h_coded < h_raw, (h_coded, h_raw)

@@ -12,12 +12,14 @@ from paper_1908_06869_b200.engine import Engine  # noqa: E402
 b, gf, gr, gb = synth.c3()
 hb = b.pinned()
 eng = Engine(0)
+from paper_1908_06869_b200 import _capi as capi  # noqa: E402
+if os.environ.get("ROWS", "1") == "1":
+    eng.set_host_outputs(capi.HOST_OUT_ROWS)  # the bench's e2e outputs
 groups = (gf, gr, gb)
 pk = eng.pack_host(hb)
 for chunk in (sys.argv[1:] or ["6000000"]):
     os.environ["XSP_CHUNK_SPANS"] = chunk
-    for name, fn in (("packed", lambda: eng.run_host_packed(pk, hb, groups=groups, raw=True)),
-                     ("dense", lambda: eng.run_host(hb, groups=groups, raw=True))):
+    for name, fn in (("packed", lambda: eng.run_host_packed(pk, hb, groups=groups, raw=True)),):
         fn()
         torch.cuda.synchronize()
         t = time.perf_counter()
@@ -28,6 +30,6 @@ for chunk in (sys.argv[1:] or ["6000000"]):
         h, d = eng.transfer_bytes()
         print(f"chunk {chunk} {name}: {ms:.1f} ms  {b.n_spans / ms / 1e3:.0f} M spans/s  h2d {h / 1e9:.2f} GB "
               f"({h / ms / 1e6:.1f} GB/s)  d2h {d / 1e9:.2f} GB", flush=True)
-os.environ["XSP_CHUNK_SPANS"] = "6000000"
+os.environ["XSP_CHUNK_SPANS"] = "12000000"
 os.environ["XSP_PIPE_TRACE"] = "1"
 eng.run_host_packed(pk, hb, groups=groups, raw=True)
