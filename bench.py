@@ -391,8 +391,10 @@ def measure_leveled(eng, args, local: int):
     models, each profiled at {M}, {M,L}, {M,L,G} x 10 repetitions (synth.
     leveled_corpus, simprof's leveled-chain shape with per-level profiling
     overhead); one step = correlate every run (one call) + compute_overhead of
-    each model's LeveledRunGroup (65 xsp_leveled calls, synchronous: the chain
-    order is decided on the host). Device-resident, CUDA events."""
+    every model's LeveledRunGroup (one xsp_leveled_batch call: three host round
+    trips for all 65 groups; chain orders are decided on the host).
+    Device-resident, CUDA events. `per_group_ms` times the same step with one
+    synchronous xsp_leveled per group."""
     import torch
     from paper_1908_06869_b200 import synth
     from paper_1908_06869_b200.engine import DeviceBatch
@@ -404,23 +406,32 @@ def measure_leveled(eng, args, local: int):
     n_events = sum(1 + m.layer_ns.size + m.exec_ns.size for m in models)
     runs_per_model = 3 * args.leveled_runs
 
-    def step():
+    def step_per_group():
         co = eng.correlate_device(dev, stream=stream)
         for s, _ in ls:
             out = eng.leveled_device(dev, co, s, stream=stream)
             assert out.status == 0 and out.n_sets == 3
 
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize()
-    steps = max(2, args.steps // 4)
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record()
-    for _ in range(steps):
-        step()
-    t1.record()
-    torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1) / steps
+    def step():
+        co = eng.correlate_device(dev, stream=stream)
+        outs = eng.leveled_batch_device(dev, co, [s for s, _ in ls], stream=stream)
+        assert all(o.status == 0 and o.n_sets == 3 for o in outs)
+
+    def time_of(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        steps = max(2, args.steps // 4)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(steps):
+            fn()
+        t1.record()
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1) / steps
+
+    per_group_ms = time_of(step_per_group)
+    ms = time_of(step)
     eng.set_profiling(True)
     eng.stage_reset()
     step()
@@ -431,13 +442,14 @@ def measure_leveled(eng, args, local: int):
     byts = n_events * runs_per_model * 8 + n_events * 24
     return {"metric": "M spans/s correlated + leveled (compute_overhead), device-resident",
             "value": b.n_spans / (ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": ms, "spans": b.n_spans,
+            "per_group_ms": per_group_ms,
             "models": len(models), "runs_per_level_set": args.leveled_runs, "events": n_events,
             "workload": "C2 at scale: 65 synthetic models x level sets {M},{M,L},{M,L,G} x 10 runs, batch 1",
             "stages_ms": {k: v[0] for k, v in st.items()},
             "roofline": {"bound": "hbm", "kernels": "k_lev_*", "bytes": byts,
                          "definition": "SURVEY 8(d): 8 B per (event, run) + 24 B per event",
                          "achieved": byts / (lev_ms / 1e3) / 1e9 if lev_ms else None, "unit": "GB/s",
-                         "note": "65 tiny synchronous calls per step: launch/sync bound, not HBM bound"}}
+                         "note": "k_lev_latency gathers each (set, event) sample by trace (one row per run): latency bound at this size; the step is 3 host round trips + correlate"}}
 
 
 def measure_ingest(eng, args, local: int, with_cpu: bool):
@@ -480,6 +492,7 @@ def measure_ingest(eng, args, local: int, with_cpu: bool):
     ms = (time.perf_counter() - t0) / reps * 1e3
     line = {"metric": "M spans/s ingested from JSONL (GPU, host text to device columns)",
             "value": b.n_spans / (ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": ms, "spans": b.n_spans,
+            "per_group_ms": per_group_ms,
             "streams": len(streams), "text_bytes": len(raw), "text_GB_per_s": len(raw) / (ms / 1e3) / 1e9,
             "how": "xsp_ingest_jsonl wall time on page-locked text (synchronous call: H2D of the text + line "
                    "index + parse + intern + sort + validate)",

@@ -415,6 +415,14 @@ xsp_status xsp_analyze(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_o
 xsp_status xsp_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
                        const xsp_level_sets* sets, const xsp_analysis_opts* opts, xsp_overhead_out* out,
                        void* stream);
+/* xsp_leveled for n_groups LeveledRunGroups at once (e.g. one per model): group
+ * g's level sets are sets[g] and its result outs[g], exactly as xsp_leveled
+ * would fill them (device columns in ctx-owned buffers shared by the batch,
+ * chain pointers in ctx-owned host memory; both valid until the next call).
+ * The whole batch costs three host round trips instead of three per group. */
+xsp_status xsp_leveled_batch(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                             uint32_t n_groups, const xsp_level_sets* sets, const xsp_analysis_opts* opts,
+                             xsp_overhead_out* outs, void* stream);
 
 /* End-to-end convenience for host-resident inputs: copies the HOST columns to the
  * device, runs xsp_correlate + xsp_analyze, and copies every result column back
@@ -464,6 +472,8 @@ typedef struct xsp_bw_col {
   const uint8_t* width;  /* [ceil(n / XSP_PACK_BLOCK)]; NULL: column not coded */
   const uint64_t* boff;  /* [ceil(n / XSP_PACK_BLOCK) + 1] */
   const uint8_t* data;
+  const uint64_t* base;  /* [ceil(n / XSP_PACK_BLOCK)] frame of reference added to
+                            every value of the block (NULL: none) */
 } xsp_bw_col;
 typedef struct xsp_packed_cols {
   uint64_t n_spans;
@@ -498,6 +508,7 @@ typedef struct xsp_packed_cols {
    * coded; a NULL width sends the raw u32 arrays above */
   xsp_bw_col dbegin_bw, dur_bw; /* n_spans values */
   xsp_bw_col dcid_bw;           /* n_cid values */
+  xsp_bw_col parent_bw;         /* n_parent values, with a per-block base; NULL width: `parent` raw */
 } xsp_packed_cols;
 xsp_status xsp_pack_host(xsp_ctx* ctx, const xsp_span_cols* host_cols, const xsp_traces* host_traces,
                          xsp_packed_cols* out);

@@ -175,7 +175,7 @@ class StringTable(C.Structure):
 
 
 class BwCol(C.Structure):
-    _fields_ = [("width", u8p), ("boff", u64p), ("data", u8p)]
+    _fields_ = [("width", u8p), ("boff", u64p), ("data", u8p), ("base", u64p)]
 
 
 class PackedCols(C.Structure):
@@ -186,7 +186,7 @@ class PackedCols(C.Structure):
                 ("name_bw", BwCol), ("flops_bw", BwCol), ("read_bw", BwCol), ("write_bw", BwCol),
                 ("alloc_bw", BwCol), ("type_bw", BwCol), ("occ_dict_n", C.c_uint32), ("occ_idx_bytes", C.c_uint32),
                 ("occ_dict", C.POINTER(C.c_double)), ("occ_idx", u8p),
-                ("dbegin_bw", BwCol), ("dur_bw", BwCol), ("dcid_bw", BwCol)]
+                ("dbegin_bw", BwCol), ("dur_bw", BwCol), ("dcid_bw", BwCol), ("parent_bw", BwCol)]
 
 
 class StringTableOut(C.Structure):  # xsp_string_table as returned by the library
@@ -219,7 +219,7 @@ EXPORTS = [
     "xsp_analyze_host", "xsp_leveled_host", "xsp_validate", "xsp_validate_host", "xsp_sort_timeline", "xsp_resolve_serialized",
     "xsp_resolve_serialized_host", "xsp_report_csv", "xsp_report_csv_host", "xsp_comm_unique_id",
     "xsp_comm_init", "xsp_combine_tables", "xsp_ingest_jsonl", "xsp_pack_host", "xsp_run_host_packed",
-    "xsp_set_host_outputs",
+    "xsp_set_host_outputs", "xsp_leveled_batch",
 ]
 
 _lib = None
@@ -277,6 +277,9 @@ def load() -> C.CDLL:
     lib.xsp_leveled.argtypes = [P, C.POINTER(SpanCols), C.POINTER(CorrOut), C.POINTER(LevelSets),
                                 C.POINTER(AnalysisOpts), C.POINTER(OverheadOut), P]
     lib.xsp_leveled.restype = C.c_int32
+    lib.xsp_leveled_batch.argtypes = [P, C.POINTER(SpanCols), C.POINTER(CorrOut), C.c_uint32, C.POINTER(LevelSets),
+                                      C.POINTER(AnalysisOpts), C.POINTER(OverheadOut), P]
+    lib.xsp_leveled_batch.restype = C.c_int32
     lib.xsp_sort_timeline_host.argtypes = [P, C.c_uint64, u64p, u8p, u64p, C.c_uint32, u64p, u32p,
                                            C.POINTER(C.c_int)]
     lib.xsp_sort_timeline_host.restype = C.c_int32

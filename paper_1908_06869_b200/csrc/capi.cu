@@ -71,6 +71,9 @@ xsp_status guard(xsp_ctx* ctx, const char* what, auto&& body) {
       return XSP_E_UNSORTED;
     }
     return XSP_E_INVALID;
+  } catch (const std::exception& e) {  // no C++ exception crosses the C ABI
+    ctx->last_error = std::string(what) + ": internal error: " + e.what();
+    return XSP_E_INVALID;
   }
 }
 
@@ -358,6 +361,19 @@ XSP_API xsp_status xsp_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xs
       throw std::invalid_argument("null level-set column");
     std::memset(out, 0, sizeof(*out));
     xsp::run_leveled(ctx, cols, corr, sets, opts, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+XSP_API xsp_status xsp_leveled_batch(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
+                                     uint32_t n_groups, const xsp_level_sets* sets, const xsp_analysis_opts* opts,
+                                     xsp_overhead_out* outs, void* stream) {
+  return guard(ctx, "xsp_leveled_batch", [&] {
+    if (!cols || !corr || !opts || (n_groups && (!sets || !outs))) throw std::invalid_argument("null argument");
+    for (uint32_t g = 0; g < n_groups; ++g)
+      if (!sets[g].set_off || (sets[g].n_sets && (!sets[g].trace_idx || !sets[g].levels)))
+        throw std::invalid_argument("null level-set column");
+    if (n_groups) std::memset(outs, 0, n_groups * sizeof(*outs));
+    xsp::run_leveled_batch(ctx, cols, corr, n_groups, sets, opts, outs, static_cast<cudaStream_t>(stream));
   });
 }
 

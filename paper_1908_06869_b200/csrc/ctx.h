@@ -239,4 +239,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* co
 void run_leveled(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr,
                  const xsp_level_sets* sets, const xsp_analysis_opts* opts, xsp_overhead_out* out,
                  cudaStream_t st);
+void run_leveled_batch(xsp_ctx* ctx, const xsp_span_cols* cols, const xsp_corr_out* corr, uint32_t n_groups,
+                       const xsp_level_sets* sets, const xsp_analysis_opts* opts, xsp_overhead_out* outs,
+                       cudaStream_t st);
 }  // namespace xsp

@@ -25,16 +25,25 @@ constexpr uint32_t kPB = XSP_PACK_BLOCK;
 
 // ---- host packer -----------------------------------------------------------
 // Byte-width code n values (xsp_bw_col): per block the bytes of its widest value.
+// for_base: code value - (the block's least value), the least value in base[].
 template <typename T>
-void bw_encode(xsp_ctx* ctx, const std::string& tag, const T* v, uint64_t n, xsp_bw_col& out) {
+void bw_encode(xsp_ctx* ctx, const std::string& tag, const T* v, uint64_t n, xsp_bw_col& out,
+               bool for_base = false) {
   const uint64_t nb = (n + kPB - 1) / kPB;
   uint8_t* w = ctx->h<uint8_t>(tag + ".w", nb + 1);
   uint64_t* off = ctx->h<uint64_t>(tag + ".o", nb + 1);
+  uint64_t* fb = for_base ? ctx->h<uint64_t>(tag + ".b", nb + 1) : nullptr;
+  auto val = [&](uint64_t b, uint64_t i) { return (uint64_t)v[i] - (fb ? fb[b] : 0); };
   uint64_t total = 0;
   for (uint64_t b = 0; b < nb; ++b) {
     const uint64_t r0 = b * kPB, r1 = std::min(n, r0 + kPB);
+    if (fb) {
+      uint64_t lo = ~0ull;
+      for (uint64_t i = r0; i < r1; ++i) lo = std::min(lo, (uint64_t)v[i]);
+      fb[b] = lo;
+    }
     uint64_t m = 0;
-    for (uint64_t i = r0; i < r1; ++i) m |= (uint64_t)v[i];
+    for (uint64_t i = r0; i < r1; ++i) m |= val(b, i);
     w[b] = m ? (uint8_t)((64 - __builtin_clzll(m) + 7) / 8) : 0;
     off[b] = total;
     total += w[b] * (r1 - r0);
@@ -46,13 +55,14 @@ void bw_encode(xsp_ctx* ctx, const std::string& tag, const T* v, uint64_t n, xsp
     uint8_t* p = d + off[b];
     const uint32_t wb = w[b];
     for (uint64_t i = r0; i < r1; ++i, p += wb) {
-      const uint64_t x = (uint64_t)v[i];
+      const uint64_t x = val(b, i);
       std::memcpy(p, &x, wb);  // little-endian host
     }
   }
   out.width = w;
   out.boff = off;
   out.data = d;
+  out.base = fb;
 }
 
 // Occupancy as u8 / u16 indexes into its distinct values (none if > 65536).
@@ -172,9 +182,9 @@ void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_p
   out->n_esc = ekey.size();
   out->esc_key = ek;
   out->esc_val = ev;
-  xsp_bw_col none{nullptr, nullptr, nullptr};
+  xsp_bw_col none{nullptr, nullptr, nullptr, nullptr};
   out->name_bw = out->flops_bw = out->read_bw = out->write_bw = out->alloc_bw = out->type_bw = none;
-  out->dbegin_bw = out->dur_bw = out->dcid_bw = none;
+  out->dbegin_bw = out->dur_bw = out->dcid_bw = out->parent_bw = none;
   out->occ_dict_n = out->occ_idx_bytes = 0;
   out->occ_dict = nullptr;
   out->occ_idx = nullptr;
@@ -190,6 +200,7 @@ void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_p
     for (uint64_t i = 0; i < ncid; ++i) p1[i] = dcid[i] + 1u;
     bw_encode(ctx, "pk.xc", p1, ncid, out->dcid_bw);
   }
+  if (npar) bw_encode(ctx, "pk.xp", par, npar, out->parent_bw, true);
   if (c->n_metric_rows) {
     bw_encode(ctx, "pk.flops", c->flops, c->n_metric_rows, out->flops_bw);
     bw_encode(ctx, "pk.read", c->dram_read, c->n_metric_rows, out->read_bw);
@@ -315,11 +326,12 @@ struct BwDev {
   const uint8_t* data;   // the staged bytes from global offset `base`
   uint64_t base;
   uint64_t r0, n, b0;    // global first row, rows, first block
+  const uint64_t* fbase;  // blocks b0 .. frame of reference, or null
   void* out;
   uint32_t osz;          // 4 or 8
   uint32_t sub1;         // decode to value - 1 (mod 2^32): the +1-coded delta lists
 };
-constexpr int kTabCols = 6;  // name_id, flops, dram_read, dram_write, alloc_bytes, type_id
+constexpr int kTabCols = 6;  // name_id + the metric / layer tables, or the four delta / sparse lists
 struct TabUnpackArgs {
   BwDev c[kTabCols];
   uint32_t ncols;
@@ -342,8 +354,10 @@ __global__ void k_unpack_tables(TabUnpackArgs a) {
     const uint64_t b = row / kPB - c.b0;
     const uint32_t w = c.width[b];
     const uint8_t* p = c.data + (c.boff[b] - c.base) + (row % kPB) * w;
-    uint64_t x = 0;
-    for (uint32_t k = 0; k < w; ++k) x |= (uint64_t)p[k] << (8 * k);
+    uint64_t x = c.fbase ? c.fbase[b] : 0;
+    uint64_t y = 0;
+    for (uint32_t k = 0; k < w; ++k) y |= (uint64_t)p[k] << (8 * k);
+    x += y;
     if (c.osz == 8)
       static_cast<uint64_t*>(c.out)[v] = x;
     else
@@ -390,7 +404,13 @@ uint64_t stage_bw(xsp_ctx* ctx, TabUnpackArgs& a, const std::string& tag, const 
   h2d(dw, bw.width + b0, nbk);
   h2d(doff, bw.boff + b0, nbk * 8);
   h2d(dd, bw.data + d0, d1 - d0);
+  uint64_t* dfb = nullptr;
+  if (bw.base) {
+    dfb = ctx->d<uint64_t>(tag + ".b", nbk);
+    h2d(dfb, bw.base + b0, nbk * 8);
+  }
   BwDev& c = a.c[a.ncols++];
+  c.fbase = dfb;
   c.width = dw;
   c.boff = doff;
   c.data = dd;
@@ -466,7 +486,7 @@ uint64_t stage_packed(xsp_ctx* ctx, const xsp_packed_cols* pk, uint64_t s0, uint
   bytes += stage_bw(ctx, pre, tag + "pk.xb", pk->dbegin_bw, pk->dbegin, 4, s0, s1, d_dbeg, st, 1);
   bytes += stage_bw(ctx, pre, tag + "pk.xd", pk->dur_bw, pk->dur, 4, s0, s1, d_dur, st, 1);
   bytes += stage_bw(ctx, pre, tag + "pk.xc", pk->dcid_bw, pk->dcid, 4, c0, c1, d_dcid, st, 1);
-  h2d(d_par, pk->parent + p0, (p1 - p0) * 8);
+  bytes += stage_bw(ctx, pre, tag + "pk.xp", pk->parent_bw, pk->parent, 8, p0, p1, d_par, st);
   h2d(d_cb, pk->blk_cid_base + b0, nbk * 8);
   h2d(d_c0, pk->blk_cid0 + b0, nbk * 4);
   h2d(d_p0, pk->blk_par0 + b0, nbk * 4);

@@ -230,7 +230,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
   }
   if (ch.size() < 2) return false;
   if (unpack_args_bytes() > 1024) throw std::logic_error("UnpackArgs outgrew its slot");
-  if (unpack_tables_args_bytes() > 512) throw std::logic_error("TabUnpackArgs outgrew its slot");
+  if (unpack_tables_args_bytes() > 1024) throw std::logic_error("TabUnpackArgs outgrew its slot");
   uint64_t max_n = 0;
   uint32_t max_t = 0;
   for (auto& c : ch) {
@@ -263,7 +263,7 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     uint64_t* h_off;  // pinned staging of the re-based trace offsets
     uint64_t* sid_buf;  // device span_id column (unused while span_id is read zero-copy)
     alignas(16) unsigned char unpack[1024];  // deferred k_unpack (+ delta-list decode) arguments
-    alignas(16) unsigned char tab_unpack[512];  // deferred k_unpack_tables arguments
+    alignas(16) unsigned char tab_unpack[1024];  // deferred k_unpack_tables arguments
     cudaEvent_t in_ready, free;
     cudaEvent_t computed, out_done;  // this parity's ctx buffers: results ready / copied out
   } slot[2];

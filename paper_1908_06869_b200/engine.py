@@ -397,6 +397,21 @@ class Engine:
                                          C.byref(opts), C.byref(out), C.c_void_p(stream)))
         return out
 
+    def leveled_batch_device(self, dbatch: DeviceBatch, corr: capi.CorrOut, level_sets_list, trim=0.2,
+                             noise=0.01, stream=None):
+        """xsp_leveled_batch: compute_overhead of many LeveledRunGroups in one
+        call; level_sets_list = [make_level_sets(...)[0], ...]. Returns the
+        OverheadOut of every group (valid until the next leveled call)."""
+        cols = dbatch.cols()
+        n = len(level_sets_list)
+        arr = (capi.LevelSets * max(n, 1))(*level_sets_list)
+        outs = (capi.OverheadOut * max(n, 1))()
+        opts = self.make_opts(trim=trim, noise=noise)
+        self._check(self.lib.xsp_leveled_batch(self.ctx, C.byref(cols), C.byref(corr), n, arr, C.byref(opts),
+                                               outs, C.c_void_p(stream)))
+        self._lev_keep = (arr, level_sets_list)
+        return list(outs)[:n]
+
     def pack_host(self, batch: SpanBatch) -> capi.PackedCols:
         """xsp_pack_host: the batch's span columns in the packed wire form (ctx-owned
         pinned arrays, valid until the next pack_host on this engine)."""

@@ -134,3 +134,45 @@ def test_synthetic_leveled_corpus_per_model(engine, has_ref):
         ls, keep = engine.make_level_sets(s)
         out = engine.leveled_device(dev, co, ls)
         assert out.status == 0 and out.n_sets == 3 and out.n_events == len(rep.rows)
+
+
+def test_leveled_batch_equals_per_group(engine):
+    """xsp_leveled_batch over many LeveledRunGroups (the bench's one-call-per-
+    batch path) returns, group by group, exactly what xsp_leveled returns:
+    statuses, chains, event keys, per-set latencies, overheads, flags and
+    accurate latencies (bit for bit) — including groups that report
+    TOO_FEW / NOT_CHAIN and an empty group."""
+    from paper_1908_06869_b200 import synth
+    from paper_1908_06869_b200.engine import DeviceBatch
+    from paper_1908_06869_b200.leveled import _d2h
+    models = synth.make_models(5, seed=7, max_layers=300)
+    b, sets = synth.leveled_corpus(models, runs=4)
+    # extra groups: one set only, a non-chain pair, no sets, sets in reverse order
+    extra = [sets[0][:1], [(0b011, sets[1][1][1]), (0b101, sets[1][2][1])], [], list(reversed(sets[2]))]
+    groups = sets + extra
+    dev = DeviceBatch(b)
+    co = engine.correlate_device(dev)
+    keep = [engine.make_level_sets(s) for s in groups]
+
+    def arrays(o):
+        ne, ns = o.n_events, o.n_sets
+        cols = {"ev_level": (o.ev_level, np.uint8, ne), "ev_layer": (o.ev_layer, np.uint32, ne),
+                "ev_kernel": (o.ev_kernel, np.uint32, ne), "lat": (o.lat, np.float64, ns * ne),
+                "overhead": (o.overhead, np.float64, max(ns - 1, 0) * ne),
+                "step_flags": (o.step_flags, np.uint8, max(ns - 1, 0) * ne),
+                "accurate": (o.accurate, np.float64, ne)}
+        out = {k: _d2h(engine.lib, engine.ctx, p, t, n) for k, (p, t, n) in cols.items()}
+        out["chain"] = [o.chain[i] for i in range(ns)] if ns and o.chain else []
+        return (o.status, o.err_a, o.err_b, ns, ne), out
+
+    single = [arrays(engine.leveled_device(dev, co, ls)) for ls, _ in keep]
+    batch = engine.leveled_batch_device(dev, co, [ls for ls, _ in keep])
+    assert len(batch) == len(groups)
+    got = [arrays(o) for o in batch]
+    statuses = [g[0][0] for g in got]
+    assert statuses[:len(sets)] == [0] * len(sets) and statuses[len(sets):] == [1, 2, 1, 0], statuses
+    for (h1, a1), (h2, a2) in zip(single, got):
+        assert h1 == h2
+        for k in a1:
+            x, y = np.asarray(a1[k]), np.asarray(a2[k])
+            assert x.shape == y.shape and np.array_equal(x.view(np.uint8), y.view(np.uint8)), k

@@ -110,6 +110,9 @@ def _bw_decode(col, n):
         if wb:
             raw = data[off[b]:off[b] + wb * (r1 - r0)].reshape(r1 - r0, wb).astype(np.uint64)
             out[r0:r1] = (raw << (np.arange(wb, dtype=np.uint64) * np.uint64(8))).sum(axis=1, dtype=np.uint64)
+    if col.base:
+        base = np.ctypeslib.as_array(col.base, shape=(nb,)).copy()
+        out += np.repeat(base, 256)[:n]
     return out
 
 
@@ -139,6 +142,9 @@ def test_packed_tables_wire_format(engine, monkeypatch):
     for bw, raw, cnt in ((pk.dbegin_bw, pk.dbegin, n), (pk.dur_bw, pk.dur, n), (pk.dcid_bw, pk.dcid, nc)):
         dec = (_bw_decode(bw, cnt) - np.uint64(1)).astype(np.uint32)
         assert np.array_equal(dec, np.ctypeslib.as_array(raw, shape=(cnt,))), cnt
+    npar = int(pk.n_parent)
+    assert pk.parent_bw.base and np.array_equal(_bw_decode(pk.parent_bw, npar),
+                                                np.ctypeslib.as_array(pk.parent, shape=(npar,)))
     assert 0 < pk.occ_dict_n <= 256 and pk.occ_idx_bytes == 1
     d = np.ctypeslib.as_array(pk.occ_dict, shape=(pk.occ_dict_n,))
     ix = np.ctypeslib.as_array(pk.occ_idx, shape=(m,))
