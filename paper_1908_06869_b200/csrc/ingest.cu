@@ -476,65 +476,6 @@ __global__ void k_gather_spans(Gather g) {
   g.line_of[j] = (uint32_t)l;
 }
 
-// ---- interning: runs of equal hashes in sorted order
-__global__ void k_iota32(uint32_t* v, uint64_t n) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (uint32_t)i;
-}
-
-__global__ void k_run_heads(const uint64_t* __restrict__ h, uint64_t n, uint32_t* __restrict__ head) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) head[i] = (i == 0 || h[i] != h[i - 1]) ? 1u : 0u;
-}
-
-// uid[idx[i]] = run number; rep[run] = first member; byte-compare each member with the representative
-__global__ void k_run_assign(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ head,
-                             const uint32_t* __restrict__ runpos, uint64_t n, uint32_t* __restrict__ uid,
-                             uint32_t* __restrict__ rep) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t r = runpos[i] + head[i] - 1;
-  uid[idx[i]] = r;
-  if (head[i]) rep[r] = idx[i];
-}
-
-__global__ void k_run_verify(const char* __restrict__ t, const uint64_t* __restrict__ off,
-                             const uint32_t* __restrict__ len, const uint32_t* __restrict__ uid,
-                             const uint32_t* __restrict__ rep, const uint8_t* __restrict__ use, uint64_t n,
-                             uint32_t* __restrict__ collision) {
-  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n || (use && !use[j])) return;
-  const uint32_t r = rep[uid[j]];
-  if (r == j) return;
-  if (len[r] != len[j]) {
-    *collision = 1;
-    return;
-  }
-  const char* a = t + off[j];
-  const char* b = t + off[r];
-  for (uint32_t k = 0; k < len[j]; ++k)
-    if (a[k] != b[k]) {
-      *collision = 1;
-      return;
-    }
-}
-
-__global__ void k_rep_ranges(const uint32_t* __restrict__ rep, const uint64_t* __restrict__ off,
-                             const uint32_t* __restrict__ len, uint32_t U, uint64_t* __restrict__ ro,
-                             uint32_t* __restrict__ rl) {
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < U) {
-    ro[r] = off[rep[r]];
-    rl[r] = len[rep[r]];
-  }
-}
-
-__global__ void k_mark_used(const uint32_t* __restrict__ uid, const uint8_t* __restrict__ use, uint64_t n,
-                            uint8_t* __restrict__ used) {
-  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n && use[j]) used[uid[j]] = 1;
-}
-
 __global__ void k_is_layer(const uint8_t* __restrict__ flags, uint64_t n, uint8_t* __restrict__ out) {
   const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) out[j] = (flags[j] & 3u) == XSP_LEVEL_LAYER ? 1 : 0;
@@ -552,12 +493,6 @@ __global__ void k_tid_check(const uint64_t* __restrict__ tid, const uint64_t* __
     if (soff[mid] <= j) lo = mid; else hi = mid;
   }
   if (tid[j] != mtid[lo]) atomicMin(bad, lo);
-}
-
-__global__ void k_map_ids(const uint32_t* __restrict__ uid, const uint32_t* __restrict__ rank, uint64_t n,
-                          uint32_t* __restrict__ out) {
-  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) out[j] = rank[uid[j]];
 }
 
 // ---- final columns in timeline order (perm = file index of timeline position)
@@ -616,16 +551,131 @@ __global__ void k_final_tables(Final f, const uint32_t* __restrict__ mpos, const
   }
 }
 
-RadixScratch radix_scratch_ing(xsp_ctx* ctx, uint64_t n) {
-  RadixScratch s;
-  s.keys_alt = ctx->d<uint64_t>("ig.rs.keys_alt", n);
-  s.vals_alt = ctx->d<uint32_t>("ig.rs.vals_alt", n);
-  const uint64_t ce = radix_counts_elems(n);
-  s.counts = ctx->d<uint32_t>("ig.rs.counts", ce);
-  s.scan_tmp = ctx->d<uint32_t>("ig.rs.scan", scan_scratch_elems(ce));
-  s.and_or = ctx->d<unsigned long long>("ig.rs.andor", 2);
-  s.and_or_host = ctx->h<unsigned long long>("ig.rs.andor_h", 2);
-  return s;
+// ---- interning by hash table (one insert pass; no sort of the span keys) ----
+// Slot keys are the 64-bit string hashes of the parser (kHashEmpty = a free slot;
+// a string hashing to it goes to the host interner); each slot keeps one member
+// as its representative, every other member is byte-compared with it.
+constexpr uint64_t kHashEmpty = ~0ull;
+__global__ void k_hash_insert(const uint64_t* __restrict__ hash, const uint8_t* __restrict__ use, uint64_t n,
+                              uint64_t mask, unsigned long long* __restrict__ tkey, uint32_t* __restrict__ trep,
+                              uint32_t* __restrict__ slot_of, uint32_t* __restrict__ bad) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n || (use && !use[j])) return;
+  const uint64_t h = hash[j];
+  if (h == kHashEmpty) {
+    *bad = 1;
+    return;
+  }
+  uint64_t sl = (h ^ (h >> 29)) & mask;
+  for (uint64_t probes = 0; probes <= mask; ++probes) {
+    unsigned long long k = *reinterpret_cast<volatile unsigned long long*>(tkey + sl);
+    if (k == kHashEmpty) {
+      k = atomicCAS(tkey + sl, kHashEmpty, (unsigned long long)h);
+      if (k == kHashEmpty) {
+        trep[sl] = (uint32_t)j;
+        slot_of[j] = (uint32_t)sl;
+        return;
+      }
+    }
+    if (k == h) {
+      slot_of[j] = (uint32_t)sl;
+      return;
+    }
+    sl = (sl + 1) & mask;
+  }
+  *bad = 1;
+}
+
+// every member byte-equal to its slot's representative (else a hash collision)
+__global__ void k_hash_verify(const char* __restrict__ t, const uint64_t* __restrict__ off,
+                              const uint32_t* __restrict__ len, const uint32_t* __restrict__ slot_of,
+                              const uint32_t* __restrict__ trep, const uint8_t* __restrict__ use, uint64_t n,
+                              uint32_t* __restrict__ bad) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n || (use && !use[j])) return;
+  const uint32_t r = *reinterpret_cast<const volatile uint32_t*>(trep + slot_of[j]);
+  if (r == (uint32_t)j) return;
+  if (len[r] != len[j]) {
+    *bad = 1;
+    return;
+  }
+  const char* a = t + off[j];
+  const char* b = t + off[r];
+  for (uint32_t k = 0; k < len[j]; ++k)
+    if (a[k] != b[k]) {
+      *bad = 1;
+      return;
+    }
+}
+
+__global__ void k_slot_used(const unsigned long long* __restrict__ tkey, uint64_t cap, uint32_t* __restrict__ used) {
+  const uint64_t sl = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (sl < cap) used[sl] = tkey[sl] != kHashEmpty;
+}
+
+// dense run number of each used slot; its representative's byte range
+__global__ void k_slot_compact(const uint32_t* __restrict__ used, const uint32_t* __restrict__ pos,
+                               const uint32_t* __restrict__ trep, const uint64_t* __restrict__ off,
+                               const uint32_t* __restrict__ len, uint64_t cap, uint32_t* __restrict__ dense,
+                               uint64_t* __restrict__ ro, uint32_t* __restrict__ rl, uint32_t* __restrict__ maxlen,
+                               unsigned long long* __restrict__ total) {
+  const uint64_t sl = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (sl >= cap || !used[sl]) return;
+  const uint32_t u = pos[sl], r = trep[sl];
+  dense[sl] = u;
+  ro[u] = off[r];
+  rl[u] = len[r];
+  atomicMax(maxlen, len[r]);
+  atomicAdd(total, (unsigned long long)len[r]);
+}
+
+__global__ void k_iota_u32(uint32_t* __restrict__ v, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (uint32_t)i;
+}
+
+// big-endian word w (bytes [8w, 8w + 8), zero padded) of distinct string ord[i]
+__global__ void k_word_keys(const char* __restrict__ t, const uint64_t* __restrict__ ro,
+                            const uint32_t* __restrict__ rl, const uint32_t* __restrict__ ord, uint64_t U, uint32_t w,
+                            uint64_t* __restrict__ key) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= U) return;
+  const uint32_t u = ord[i], l = rl[u];
+  const unsigned char* a = reinterpret_cast<const unsigned char*>(t + ro[u]);
+  uint64_t k = 0;
+  for (uint32_t b = 0; b < 8; ++b) {
+    const uint32_t at = 8 * w + b;
+    k = k << 8 | (at < l ? a[at] : 0u);
+  }
+  key[i] = k;
+}
+
+// rank of each distinct string; the lengths in id order
+__global__ void k_rank_lengths(const uint32_t* __restrict__ ord, const uint32_t* __restrict__ rl, uint64_t U,
+                               uint32_t* __restrict__ rank, uint64_t* __restrict__ sl) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= U) return;
+  rank[ord[k]] = (uint32_t)k;
+  sl[k] = rl[ord[k]];
+}
+
+// string of id k to blob[so[k], so[k + 1])
+__global__ void k_gather_sorted(const char* __restrict__ t, const uint64_t* __restrict__ ro,
+                                const uint32_t* __restrict__ rl, const uint32_t* __restrict__ ord,
+                                const uint64_t* __restrict__ so, uint64_t U, char* __restrict__ blob) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= U) return;
+  const uint32_t u = ord[k];
+  const char* a = t + ro[u];
+  char* d = blob + so[k];
+  for (uint32_t b = 0; b < rl[u]; ++b) d[b] = a[b];
+}
+
+__global__ void k_map_slots(const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ dense,
+                            const uint32_t* __restrict__ rank, const uint8_t* __restrict__ use, uint64_t n,
+                            uint32_t* __restrict__ ids) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) ids[j] = (use && !use[j]) ? 0u : rank[dense[slot_of[j]]];
 }
 
 unsigned blocks(uint64_t n) { return ceil_div(n ? n : 1, 256); }
@@ -735,65 +785,96 @@ bool parse_meta(const char* s, const char* e, Meta& m) {
 // and ids[j] for the used entries
 bool intern(xsp_ctx* ctx, const std::string& tag, const char* dtext, const char* htext, uint64_t n,
             const uint64_t* hash, const uint64_t* off, const uint32_t* len, const uint8_t* use, uint32_t* ids,
-            std::vector<std::string>& table, cudaStream_t st) {
-  table.clear();
+            std::string& tblob, std::vector<uint64_t>& toff, cudaStream_t st) {
+  tblob.clear();
+  toff.assign(1, 0);
   if (n == 0) return true;
-  uint64_t* keys = ctx->d<uint64_t>(tag + ".k", n);
-  uint32_t* idx = ctx->d<uint32_t>(tag + ".i", n);
-  XSP_CUDA(cudaMemcpyAsync(keys, hash, n * 8, cudaMemcpyDeviceToDevice, st));
-  k_iota32<<<blocks(n), 256, 0, st>>>(idx, n);
-  RadixScratch rs = radix_scratch_ing(ctx, n);
-  radix_sort_pairs(keys, idx, n, 0, 64, rs, st, &ctx->launches);
-  uint32_t* head = ctx->d<uint32_t>(tag + ".h", n + 1);
-  uint32_t* runpos = ctx->d<uint32_t>(tag + ".rp", n + 1);
-  uint32_t* nrun = ctx->d<uint32_t>(tag + ".nr", 1);
-  k_run_heads<<<blocks(n), 256, 0, st>>>(keys, n, head);
-  uint32_t* scr = ctx->d<uint32_t>(tag + ".sc", scan_scratch_elems(n + 1));
-  exclusive_scan<uint32_t, uint32_t>(head, runpos, n, scr, nrun, st, &ctx->launches);
-  uint32_t* uid = ctx->d<uint32_t>(tag + ".u", n);
-  uint32_t* rep = ctx->d<uint32_t>(tag + ".r", n);
-  k_run_assign<<<blocks(n), 256, 0, st>>>(idx, head, runpos, n, uid, rep);
-  uint32_t* col = ctx->d<uint32_t>(tag + ".c", 1);
-  XSP_CUDA(cudaMemsetAsync(col, 0, 4, st));
-  k_run_verify<<<blocks(n), 256, 0, st>>>(dtext, off, len, uid, rep, use, n, col);
-  uint32_t h2[2];
-  XSP_CUDA(cudaMemcpyAsync(h2, nrun, 4, cudaMemcpyDeviceToHost, st));
-  XSP_CUDA(cudaMemcpyAsync(h2 + 1, col, 4, cudaMemcpyDeviceToHost, st));
+  uint64_t cap = 1024;
+  while (cap < 2 * n) cap <<= 1;
+  auto* tkey = ctx->d<unsigned long long>(tag + ".tk", cap);
+  uint32_t* trep = ctx->d<uint32_t>(tag + ".tr", cap);
+  uint32_t* slot_of = ctx->d<uint32_t>(tag + ".so", n);
+  uint32_t* used = ctx->d<uint32_t>(tag + ".us", cap + 1);
+  uint32_t* pos = ctx->d<uint32_t>(tag + ".ps", cap + 1);
+  uint32_t* dense = ctx->d<uint32_t>(tag + ".dn", cap);
+  // [0] distinct strings [1] collision / probe overflow [2] longest [3] (pad) [4..5] total bytes
+  uint32_t* cnt = ctx->d<uint32_t>(tag + ".cn", 6);
+  XSP_CUDA(cudaMemsetAsync(tkey, 0xFF, cap * 8, st));
+  XSP_CUDA(cudaMemsetAsync(cnt, 0, 24, st));
+  k_hash_insert<<<blocks(n), 256, 0, st>>>(hash, use, n, cap - 1, tkey, trep, slot_of, cnt + 1);
+  k_hash_verify<<<blocks(n), 256, 0, st>>>(dtext, off, len, slot_of, trep, use, n, cnt + 1);
+  k_slot_used<<<blocks(cap), 256, 0, st>>>(tkey, cap, used);
+  uint32_t* scr = ctx->d<uint32_t>(tag + ".sc", scan_scratch_elems(cap + 1));
+  exclusive_scan<uint32_t, uint32_t>(used, pos, cap, scr, cnt, st, &ctx->launches);
+  // the representatives' byte ranges (at most n of them), longest, total bytes
+  uint64_t* d_ro = ctx->d<uint64_t>(tag + ".ro", n + 1);
+  uint32_t* d_rl = ctx->d<uint32_t>(tag + ".rl", n + 1);
+  k_slot_compact<<<blocks(cap), 256, 0, st>>>(used, pos, trep, off, len, cap, dense, d_ro, d_rl, cnt + 2,
+                                               reinterpret_cast<unsigned long long*>(cnt + 4));
+  uint32_t* h2 = ctx->h<uint32_t>(tag + ".h2", 6);
+  XSP_CUDA(cudaMemcpyAsync(h2, cnt, 24, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
   if (h2[1]) return false;
-  const uint32_t U = h2[0];
-  // the representatives' byte ranges and which runs hold a used entry
-  uint64_t* d_ro = ctx->d<uint64_t>(tag + ".ro", U + 1ull);
-  uint32_t* d_rl = ctx->d<uint32_t>(tag + ".rl", U + 1ull);
-  uint8_t* d_used = ctx->d<uint8_t>(tag + ".used", U + 1ull);
-  XSP_CUDA(cudaMemsetAsync(d_used, use ? 0 : 1, U, st));
-  k_rep_ranges<<<blocks(U), 256, 0, st>>>(rep, off, len, U, d_ro, d_rl);
-  if (use) k_mark_used<<<blocks(n), 256, 0, st>>>(uid, use, n, d_used);
-  std::vector<uint64_t> roff(U);
-  std::vector<uint32_t> rlen(U);
-  std::vector<uint8_t> used_run(U);
-  XSP_CUDA(cudaMemcpyAsync(roff.data(), d_ro, U * 8ull, cudaMemcpyDeviceToHost, st));
-  XSP_CUDA(cudaMemcpyAsync(rlen.data(), d_rl, U * 4ull, cudaMemcpyDeviceToHost, st));
-  XSP_CUDA(cudaMemcpyAsync(used_run.data(), d_used, U, cudaMemcpyDeviceToHost, st));
-  XSP_CUDA(cudaStreamSynchronize(st));
-  std::vector<uint32_t> order;
-  order.reserve(U);
-  for (uint32_t r = 0; r < U; ++r)
-    if (used_run[r]) order.push_back(r);
-  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-    return std::string_view(htext + roff[a], rlen[a]) < std::string_view(htext + roff[b], rlen[b]);
-  });
-  std::vector<uint32_t> rank(U, 0);
-  table.reserve(order.size());
-  for (uint32_t k = 0; k < order.size(); ++k) {
-    rank[order[k]] = k;
-    table.emplace_back(htext + roff[order[k]], rlen[order[k]]);
+  const uint32_t U = h2[0], maxlen = h2[2];
+  uint64_t nb;
+  std::memcpy(&nb, h2 + 4, 8);
+  if (U == 0) {  // nothing used (no layer spans): every id 0
+    k_map_slots<<<blocks(n), 256, 0, st>>>(slot_of, dense, dense, use, n, ids);
+    ++ctx->launches;
+    return true;
   }
-  uint32_t* d_rank = ctx->d<uint32_t>(tag + ".rank", U + 1);
-  XSP_CUDA(cudaMemcpyAsync(d_rank, rank.data(), U * 4ull, cudaMemcpyHostToDevice, st));
-  k_map_ids<<<blocks(n), 256, 0, st>>>(uid, d_rank, n, ids);
+  // ids in lexicographic order of the strings (the reference interns sorted
+  // names): an LSD radix sort of the distinct strings over their big-endian
+  // 8-byte words on the device (zero padded: the strings hold no NUL), last
+  // word first; strings longer than kDevSortMax are sorted on the host
+  constexpr uint32_t kDevSortMax = 256;
+  uint32_t* d_ord = ctx->d<uint32_t>(tag + ".ord", U + 1ull);
+  if (maxlen <= kDevSortMax) {
+    uint64_t* d_key = ctx->d<uint64_t>(tag + ".key", U + 1ull);
+    RadixScratch rs;
+    rs.keys_alt = ctx->d<uint64_t>(tag + ".rs.ka", U + 1ull);
+    rs.vals_alt = ctx->d<uint32_t>(tag + ".rs.va", U + 1ull);
+    const uint64_t ce = radix_counts_elems(U);
+    rs.counts = ctx->d<uint32_t>(tag + ".rs.c", ce);
+    rs.scan_tmp = ctx->d<uint32_t>(tag + ".rs.s", scan_scratch_elems(ce));
+    rs.and_or = ctx->d<unsigned long long>(tag + ".rs.ao", 2);
+    rs.and_or_host = ctx->h<unsigned long long>(tag + ".rs.aoh", 2);
+    k_iota_u32<<<blocks(U), 256, 0, st>>>(d_ord, U);
+    for (int w = (int)((maxlen + 7) / 8) - 1; w >= 0; --w) {
+      k_word_keys<<<blocks(U), 256, 0, st>>>(dtext, d_ro, d_rl, d_ord, U, (uint32_t)w, d_key);
+      radix_sort_pairs(d_key, d_ord, U, 0, 64, rs, st, &ctx->launches);
+    }
+  } else {
+    uint64_t* roff = ctx->h<uint64_t>(tag + ".hro", U + 1ull);
+    uint32_t* rlen = ctx->h<uint32_t>(tag + ".hrl", U + 1ull);
+    XSP_CUDA(cudaMemcpyAsync(roff, d_ro, U * 8ull, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaMemcpyAsync(rlen, d_rl, U * 4ull, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaStreamSynchronize(st));
+    uint32_t* order = ctx->h<uint32_t>(tag + ".hord", U + 1ull);
+    for (uint32_t r = 0; r < U; ++r) order[r] = r;
+    std::sort(order, order + U, [&](uint32_t a, uint32_t b) {
+      return std::string_view(htext + roff[a], rlen[a]) < std::string_view(htext + roff[b], rlen[b]);
+    });
+    XSP_CUDA(cudaMemcpyAsync(d_ord, order, U * 4ull, cudaMemcpyHostToDevice, st));
+  }
+  // ranks, the strings in id order as one blob, the span ids
+  uint32_t* d_rank = ctx->d<uint32_t>(tag + ".rank", U + 1ull);
+  uint64_t* d_sl = ctx->d<uint64_t>(tag + ".sl", U + 1ull);
+  uint64_t* d_so = ctx->d<uint64_t>(tag + ".so64", U + 1ull);
+  uint64_t* scr64 = ctx->d<uint64_t>(tag + ".sc64", scan_scratch_elems(U + 1ull));
+  char* d_blob = ctx->d<char>(tag + ".blob", nb + 1);
+  k_rank_lengths<<<blocks(U), 256, 0, st>>>(d_ord, d_rl, U, d_rank, d_sl);
+  exclusive_scan<uint64_t, uint64_t>(d_sl, d_so, U, scr64, d_so + U, st, &ctx->launches);
+  k_gather_sorted<<<blocks(U), 256, 0, st>>>(dtext, d_ro, d_rl, d_ord, d_so, U, d_blob);
+  k_map_slots<<<blocks(n), 256, 0, st>>>(slot_of, dense, d_rank, use, n, ids);
+  char* hblob = ctx->h<char>(tag + ".hblob", nb + 1);
+  uint64_t* hso = ctx->h<uint64_t>(tag + ".hso", U + 1ull);
+  XSP_CUDA(cudaMemcpyAsync(hblob, d_blob, nb, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(hso, d_so, (U + 1ull) * 8, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
-  ctx->launches += 7;
+  tblob.assign(hblob, nb);
+  toff.assign(hso, hso + U + 1);
+  ctx->launches += 9;
   return true;
 }
 
@@ -801,8 +882,8 @@ bool intern(xsp_ctx* ctx, const std::string& tag, const char* dtext, const char*
 
 // ctx-owned host storage of one ingest result
 struct IngestHost {
-  std::vector<std::string> names, types;
-  std::string blob_names, blob_types;
+  std::string blob_names, blob_types;  // interned strings in id order
+
   std::vector<uint64_t> off_names, off_types;
   std::vector<uint64_t> span_off, trace_id;
   std::vector<uint32_t> levels, batch, run;
@@ -972,11 +1053,18 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   uint32_t* type_fid = ctx->d<uint32_t>("ig.s.tyid", n + 1);
   uint8_t* is_layer = ctx->d<uint8_t>("ig.s.isl", n + 1);
   if (n) k_is_layer<<<blocks(n), 256, 0, st>>>(g.flags, n, is_layer);
-  if (!intern(ctx, "ig.in", dtext, htext, n, g.name_hash, g.name_off, g.name_len, nullptr, name_fid, H.names, st) ||
-      !intern(ctx, "ig.it", dtext, htext, n, g.type_hash, g.type_off, g.type_len, is_layer, type_fid, H.types, st)) {
+  if (!intern(ctx, "ig.in", dtext, htext, n, g.name_hash, g.name_off, g.name_len, nullptr, name_fid, H.blob_names,
+              H.off_names, st)) {
     out->bad_stream = 0;  // a hash collision: the host interns
     return;
   }
+  mark("names");
+  if (!intern(ctx, "ig.it", dtext, htext, n, g.type_hash, g.type_off, g.type_len, is_layer, type_fid, H.blob_types,
+              H.off_types, st)) {
+    out->bad_stream = 0;
+    return;
+  }
+  mark("types");
   // ---- trace arrays (host) and the trace_id check (ingest's own fault, collector.cpp:248-255)
   H.trace_id.resize(S);
   H.levels.resize(S);
@@ -1083,18 +1171,8 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
     return;
   }
   // ---- host side of the result
-  auto blob = [](const std::vector<std::string>& v, std::string& b, std::vector<uint64_t>& off) {
-    b.clear();
-    off.assign(v.size() + 1, 0);
-    for (size_t i = 0; i < v.size(); ++i) {
-      b += v[i];
-      off[i + 1] = b.size();
-    }
-  };
-  blob(H.names, H.blob_names, H.off_names);
-  blob(H.types, H.blob_types, H.off_types);
-  out->names = {(uint32_t)H.names.size(), H.blob_names.data(), H.off_names.data()};
-  out->types = {(uint32_t)H.types.size(), H.blob_types.data(), H.off_types.data()};
+  out->names = {(uint32_t)(H.off_names.size() - 1), H.blob_names.data(), H.off_names.data()};
+  out->types = {(uint32_t)(H.off_types.size() - 1), H.blob_types.data(), H.off_types.data()};
   out->trace_id = H.trace_id.data();
   out->trace_batch = H.batch.data();
   out->trace_run = H.run.data();

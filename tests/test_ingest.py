@@ -50,14 +50,32 @@ def test_workloads_parse_with_the_reference(has_ref):
         assert b.n_traces == len(streams) and b.n_spans > 0
 
 
+def _renamed(streams, fn):
+    """The streams with every span name passed through fn (same JSON layout)."""
+    import re
+    out = []
+    for s in streams:
+        out.append(re.sub(rb'"name":"([^"]*)"', lambda m: b'"name":"' + fn(m.group(1)) + b'"', s))
+    return out
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("which", ["reference_generators", "synth_c3", "shuffled_lines"])
+@pytest.mark.parametrize("which", ["reference_generators", "synth_c3", "shuffled_lines", "long_names",
+                                   "shared_prefixes"])
 def test_gpu_ingest_matches_reference(engine, has_ref, which):
+    """long_names: names over 256 bytes (the interner's host sort); shared
+    prefixes: names equal in their first 8 / 16 / 24 bytes and names that are
+    prefixes of others (the device sort's zero-padded word order)."""
     from oracle import ref
     if which == "reference_generators":
         streams = ref_streams()
     elif which == "synth_c3":
         streams = synth_streams()
+    elif which == "long_names":
+        streams = _renamed(synth_streams(1, 2), lambda n: n + b"_" + b"x" * (250 + len(n) % 17))
+    elif which == "shared_prefixes":
+        streams = _renamed(synth_streams(1, 2),
+                           lambda n: b"common/prefix/of/length32/" + n[: (len(n) * 7) % (len(n) + 1)])
     else:  # records out of timeline order: ingest sorts them (collector.cpp:256)
         rng = np.random.default_rng(4)
         streams = []
