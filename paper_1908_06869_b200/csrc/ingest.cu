@@ -407,6 +407,96 @@ __global__ void k_nl_write(const char* __restrict__ t, uint64_t n, const uint32_
     if (t[i] == '\n') nl[k++] = i;
 }
 
+// Lines from the newline positions, on the device: stream s's lines are its
+// newlines plus, when its last byte is not '\n', one unterminated tail line
+// [last newline + 1, soff[s + 1]); a line never straddles two streams.
+__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* __restrict__ v, uint64_t n, uint64_t x) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (v[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// nbefore[s] = newlines before soff[s] (s <= S); tail[s] = stream s ends in an unterminated line
+__global__ void k_stream_lines(const uint64_t* __restrict__ nl, uint64_t hnl, const uint64_t* __restrict__ soff,
+                               uint32_t S, uint64_t* __restrict__ nbefore, uint32_t* __restrict__ tail) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > S) return;
+  nbefore[s] = lower_bound_u64(nl, hnl, soff[s]);
+  if (s == S) return;
+  const uint64_t nf = lower_bound_u64(nl, hnl, soff[s]), nla = lower_bound_u64(nl, hnl, soff[s + 1]);
+  const uint64_t at = nla > nf ? nl[nla - 1] + 1 : soff[s];
+  tail[s] = at < soff[s + 1] ? 1u : 0u;
+}
+
+// line of newline k: index k + (tail lines of earlier streams)
+__global__ void k_lines_nl(const uint64_t* __restrict__ nl, uint64_t hnl, const uint64_t* __restrict__ soff,
+                           uint32_t S, const uint32_t* __restrict__ tb, uint64_t* __restrict__ lstart,
+                           uint64_t* __restrict__ lend, uint32_t* __restrict__ lstream) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= hnl) return;
+  const uint64_t p = nl[k];
+  uint32_t lo = 0, hi = S;  // the last stream with soff[s] <= p (empty streams before it hold no byte)
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (soff[mid] <= p) lo = mid; else hi = mid;
+  }
+  const uint64_t idx = k + tb[lo];
+  lend[idx] = p;
+  lstart[idx] = (k > 0 && nl[k - 1] >= soff[lo]) ? nl[k - 1] + 1 : soff[lo];
+  lstream[idx] = lo;
+}
+
+__global__ void k_lines_tail(const uint64_t* __restrict__ nl, const uint64_t* __restrict__ nbefore,
+                             const uint64_t* __restrict__ soff, uint32_t S, const uint32_t* __restrict__ tail,
+                             const uint32_t* __restrict__ tb, uint64_t* __restrict__ lstart,
+                             uint64_t* __restrict__ lend, uint32_t* __restrict__ lstream) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S || !tail[s]) return;
+  const uint64_t nf = nbefore[s], nla = nbefore[s + 1];
+  const uint64_t idx = nla + tb[s];
+  lstart[idx] = nla > nf ? nl[nla - 1] + 1 : soff[s];
+  lend[idx] = soff[s + 1];
+  lstream[idx] = s;
+}
+
+// per stream: meta records (count, a line holding one), span lines; the first
+// line the device parser left to the host
+struct LineStats {
+  uint32_t* nmeta;            // [S]
+  uint32_t* nspan;            // [S]
+  unsigned long long* mline;  // [S]
+  unsigned long long* first_host;
+};
+__global__ void k_line_stats(const uint8_t* __restrict__ kind, const uint32_t* __restrict__ lstream, uint64_t L,
+                             LineStats o) {
+  const uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const uint8_t k = kind[l];
+  const uint32_t s = lstream[l];
+  if (k == LK_HOST) {
+    atomicMin(o.first_host, (unsigned long long)l);
+  } else if (k == LK_META) {
+    atomicAdd(o.nmeta + s, 1u);
+    o.mline[s] = l;
+  } else if (k == LK_SPAN) {
+    atomicAdd(o.nspan + s, 1u);
+  }
+}
+
+// byte range of each stream's meta line (the per-stream record of a clean batch)
+__global__ void k_meta_ranges(const unsigned long long* __restrict__ mline, const uint32_t* __restrict__ nmeta,
+                              uint32_t S, const uint64_t* __restrict__ lstart, const uint64_t* __restrict__ lend,
+                              uint64_t* __restrict__ mrange) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const bool one = nmeta[s] == 1;
+  mrange[2 * s] = one ? lstart[mline[s]] : 0;
+  mrange[2 * s + 1] = one ? lend[mline[s]] : 0;
+}
+
 // line l = [start[l], end[l]) (end: its newline, or its stream's end)
 __global__ void k_parse_lines(const char* __restrict__ t, uint64_t n, const uint64_t* __restrict__ start,
                               const uint64_t* __restrict__ nl, uint64_t nlines, LineOut o) {
@@ -922,38 +1012,29 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   uint32_t hnl = 0;
   XSP_CUDA(cudaMemcpyAsync(&hnl, tot, 4, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
-  // newline positions + the stream ends (a stream's last line may lack '\n')
-  uint64_t* nl = ctx->d<uint64_t>("ig.nl", hnl + S + 1);
+  // newline positions, then the lines (device): newlines + unterminated stream tails
+  uint64_t* nl = ctx->d<uint64_t>("ig.nl", hnl + 1ull);
   k_nl_write<<<blocks(nch), 256, 0, st>>>(dtext, n_text, pos, nl);
-  // (pinned staging: these arrays cross PCIe twice)
-  uint64_t* hnlpos = ctx->h<uint64_t>("ig.hnl", hnl + 1ull);
-  XSP_CUDA(cudaMemcpyAsync(hnlpos, nl, hnl * 8ull, cudaMemcpyDeviceToHost, st));
+  uint64_t* d_tsoff = ctx->d<uint64_t>("ig.tsoff", S + 1ull);
+  uint64_t* h_tsoff = ctx->h<uint64_t>("ig.htsoff", S + 1ull);
+  std::memcpy(h_tsoff, soff, (S + 1ull) * 8);
+  XSP_CUDA(cudaMemcpyAsync(d_tsoff, h_tsoff, (S + 1ull) * 8, cudaMemcpyHostToDevice, st));
+  uint64_t* nbefore = ctx->d<uint64_t>("ig.nbef", S + 1ull);
+  uint32_t* tail = ctx->d<uint32_t>("ig.tail", S + 1ull);
+  uint32_t* tb = ctx->d<uint32_t>("ig.tb", S + 1ull);
+  k_stream_lines<<<blocks(S + 1ull), 256, 0, st>>>(nl, hnl, d_tsoff, S, nbefore, tail);
+  uint32_t* scr_s = ctx->d<uint32_t>("ig.scs", scan_scratch_elems(S + 1ull));
+  exclusive_scan<uint32_t, uint32_t>(tail, tb, S, scr_s, tb + S, st, &ctx->launches);
+  uint32_t* h_nt = ctx->h<uint32_t>("ig.hnt", 1);
+  XSP_CUDA(cudaMemcpyAsync(h_nt, tb + S, 4, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
-  // merge stream ends that are not already line ends; the line -> stream map
-  uint64_t* ends = ctx->h<uint64_t>("ig.hends", hnl + S + 1ull);
-  uint64_t* starts = ctx->h<uint64_t>("ig.hstarts", hnl + S + 1ull);
-  std::vector<uint32_t> line_stream(hnl + S + 1ull);
-  uint64_t L = 0;
-  {
-    uint64_t k = 0;
-    for (uint32_t s = 0; s < S; ++s) {
-      uint64_t at = soff[s];
-      while (k < hnl && hnlpos[k] < soff[s + 1]) {
-        starts[L] = at;
-        ends[L] = hnlpos[k];
-        line_stream[L++] = s;
-        at = hnlpos[k++] + 1;
-      }
-      if (at < soff[s + 1]) {  // unterminated last line of stream s
-        starts[L] = at;
-        ends[L] = soff[s + 1];
-        line_stream[L++] = s;
-      }
-    }
-  }
-  XSP_CUDA(cudaMemcpyAsync(nl, ends, L * 8, cudaMemcpyHostToDevice, st));
+  const uint64_t L = hnl + (uint64_t)*h_nt;
   uint64_t* lstart = ctx->d<uint64_t>("ig.ls", L + 1);
-  XSP_CUDA(cudaMemcpyAsync(lstart, starts, L * 8, cudaMemcpyHostToDevice, st));
+  uint64_t* lend = ctx->d<uint64_t>("ig.le", L + 1);
+  uint32_t* lstream = ctx->d<uint32_t>("ig.lst", L + 1);
+  if (hnl) k_lines_nl<<<blocks(hnl), 256, 0, st>>>(nl, hnl, d_tsoff, S, tb, lstart, lend, lstream);
+  if (S) k_lines_tail<<<blocks(S), 256, 0, st>>>(nl, nbefore, d_tsoff, S, tail, tb, lstart, lend, lstream);
+  ctx->launches += 4;
   // ---- parse every line
   LineOut lo;
   lo.kind = ctx->d<uint8_t>("ig.kind", L + 1);
@@ -977,35 +1058,70 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   lo.alloc = ctx->d<int64_t>("ig.l.al", L);
   lo.tag_bits = ctx->d<uint8_t>("ig.l.tb", L);
   mark("lines");
-  if (L) k_parse_lines<<<blocks(L), 256, 0, st>>>(dtext, n_text, lstart, nl, L, lo);
+  if (L) k_parse_lines<<<blocks(L), 256, 0, st>>>(dtext, n_text, lstart, lend, L, lo);
   mark("parse");
-  std::vector<uint8_t> hkind(L);
-  XSP_CUDA(cudaMemcpyAsync(hkind.data(), lo.kind, L, cudaMemcpyDeviceToHost, st));
+  // ---- per stream: exactly one meta record (parsed on the host), no line the
+  // device parser left to the host; counted on the device, the host touches
+  // only the S meta lines (the exact line-order walk runs only for a bad batch)
+  LineStats ls;
+  ls.nmeta = ctx->d<uint32_t>("ig.nmeta", 2ull * S + 1);
+  ls.nspan = ls.nmeta + S;
+  ls.mline = ctx->d<unsigned long long>("ig.mline", S + 1ull);
+  ls.first_host = ls.mline + S;
+  uint64_t* mrange = ctx->d<uint64_t>("ig.mrange", 2ull * S + 1);
+  XSP_CUDA(cudaMemsetAsync(ls.nmeta, 0, (2ull * S + 1) * 4, st));
+  XSP_CUDA(cudaMemsetAsync(ls.first_host, 0xFF, 8, st));
+  if (L) k_line_stats<<<blocks(L), 256, 0, st>>>(lo.kind, lstream, L, ls);
+  if (S) k_meta_ranges<<<blocks(S), 256, 0, st>>>(ls.mline, ls.nmeta, S, lstart, lend, mrange);
+  uint32_t* h_cnt = ctx->h<uint32_t>("ig.hcnt", 2ull * S + 1);
+  uint64_t* h_mr = ctx->h<uint64_t>("ig.hmr", 2ull * S + 2);
+  XSP_CUDA(cudaMemcpyAsync(h_cnt, ls.nmeta, 2ull * S * 4, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(h_mr, mrange, 2ull * S * 8, cudaMemcpyDeviceToHost, st));
+  XSP_CUDA(cudaMemcpyAsync(h_mr + 2ull * S, ls.first_host, 8, cudaMemcpyDeviceToHost, st));
   XSP_CUDA(cudaStreamSynchronize(st));
-  ctx->launches += 4;
-  // ---- per stream: exactly one meta record (host), no line the fast path left to the host
+  ctx->launches += 6;
   std::vector<Meta> meta(S);
-  std::vector<int> nmeta(S, 0);
   std::vector<uint64_t> nspan(S, 0);
-  for (uint64_t l = 0; l < L; ++l) {
-    const uint32_t s = line_stream[l];
-    if (hkind[l] == LK_HOST) {
-      out->bad_stream = s;
-      return;
+  bool clean = h_mr[2ull * S] == ~0ull;
+  for (uint32_t s = 0; s < S && clean; ++s) clean = h_cnt[s] == 1;
+  if (clean) {
+    for (uint32_t s = 0; s < S; ++s) {
+      if (!parse_meta(htext + h_mr[2 * s], htext + h_mr[2 * s + 1], meta[s])) {
+        out->bad_stream = s;  // the first bad meta line in line order
+        return;
+      }
+      nspan[s] = h_cnt[S + s];
     }
-    if (hkind[l] == LK_META) {
-      if (++nmeta[s] > 1 || !parse_meta(htext + starts[l], htext + ends[l], meta[s])) {
+  } else {  // the first violation in line order, as the host ingest meets it
+    std::vector<uint8_t> hkind(L);
+    std::vector<uint32_t> hls(L);
+    std::vector<uint64_t> hst(L), hen(L);
+    XSP_CUDA(cudaMemcpyAsync(hkind.data(), lo.kind, L, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaMemcpyAsync(hls.data(), lstream, L * 4, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaMemcpyAsync(hst.data(), lstart, L * 8, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaMemcpyAsync(hen.data(), lend, L * 8, cudaMemcpyDeviceToHost, st));
+    XSP_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> nmeta(S, 0);
+    for (uint64_t l = 0; l < L; ++l) {
+      const uint32_t s = hls[l];
+      if (hkind[l] == LK_HOST) {
         out->bad_stream = s;
         return;
       }
+      if (hkind[l] == LK_META) {
+        if (++nmeta[s] > 1 || !parse_meta(htext + hst[l], htext + hen[l], meta[s])) {
+          out->bad_stream = s;
+          return;
+        }
+      }
     }
-    if (hkind[l] == LK_SPAN) ++nspan[s];
+    for (uint32_t s = 0; s < S; ++s)
+      if (nmeta[s] != 1) {
+        out->bad_stream = s;
+        return;
+      }
+    return;  // unreachable: a clean batch takes the branch above
   }
-  for (uint32_t s = 0; s < S; ++s)
-    if (nmeta[s] != 1) {
-      out->bad_stream = s;
-      return;
-    }
   uint64_t n = 0;
   H.span_off.assign(S + 1, 0);
   for (uint32_t s = 0; s < S; ++s) H.span_off[s + 1] = H.span_off[s] + nspan[s];
@@ -1021,7 +1137,7 @@ void run_ingest_jsonl(xsp_ctx* ctx, const char* htext, const uint64_t* soff, uin
   Gather g;
   g.isspan = isspan;
   g.spos = spos;
-  g.nl = nl;
+  g.nl = lend;
   g.nlines = L;
   g.lo = lo;
   g.span_id = ctx->d<uint64_t>("ig.s.sid", n + 1);
