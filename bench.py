@@ -492,7 +492,6 @@ def measure_ingest(eng, args, local: int, with_cpu: bool):
     ms = (time.perf_counter() - t0) / reps * 1e3
     line = {"metric": "M spans/s ingested from JSONL (GPU, host text to device columns)",
             "value": b.n_spans / (ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": ms, "spans": b.n_spans,
-            "per_group_ms": per_group_ms,
             "streams": len(streams), "text_bytes": len(raw), "text_GB_per_s": len(raw) / (ms / 1e3) / 1e9,
             "how": "xsp_ingest_jsonl wall time on page-locked text (synchronous call: H2D of the text + line "
                    "index + parse + intern + sort + validate)",
