@@ -509,6 +509,12 @@ typedef struct xsp_packed_cols {
   xsp_bw_col dbegin_bw, dur_bw; /* n_spans values */
   xsp_bw_col dcid_bw;           /* n_cid values */
   xsp_bw_col parent_bw;         /* n_parent values, with a per-block base; NULL width: `parent` raw */
+  /* [n_blocks + 1] metric rows / layer rows / non-layer explicit-parent spans
+   * before each block (a chunk's table rows without a pass over its flags);
+   * NULL: counted from the flags */
+  const uint32_t* blk_met0;
+  const uint32_t* blk_lay0;
+  const uint32_t* blk_cpar0;
 } xsp_packed_cols;
 xsp_status xsp_pack_host(xsp_ctx* ctx, const xsp_span_cols* host_cols, const xsp_traces* host_traces,
                          xsp_packed_cols* out);

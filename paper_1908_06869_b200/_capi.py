@@ -186,7 +186,8 @@ class PackedCols(C.Structure):
                 ("name_bw", BwCol), ("flops_bw", BwCol), ("read_bw", BwCol), ("write_bw", BwCol),
                 ("alloc_bw", BwCol), ("type_bw", BwCol), ("occ_dict_n", C.c_uint32), ("occ_idx_bytes", C.c_uint32),
                 ("occ_dict", C.POINTER(C.c_double)), ("occ_idx", u8p),
-                ("dbegin_bw", BwCol), ("dur_bw", BwCol), ("dcid_bw", BwCol), ("parent_bw", BwCol)]
+                ("dbegin_bw", BwCol), ("dur_bw", BwCol), ("dcid_bw", BwCol), ("parent_bw", BwCol),
+                ("blk_met0", u32p), ("blk_lay0", u32p), ("blk_cpar0", u32p)]
 
 
 class StringTableOut(C.Structure):  # xsp_string_table as returned by the library

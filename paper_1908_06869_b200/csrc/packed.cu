@@ -115,6 +115,27 @@ void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_p
   uint64_t* cbase = ctx->h<uint64_t>("pk.cbase", nb + 1);
   uint32_t* cid0 = ctx->h<uint32_t>("pk.cid0", nb + 1);
   uint32_t* par0 = ctx->h<uint32_t>("pk.par0", nb + 1);
+  uint32_t* met0 = ctx->h<uint32_t>("pk.met0", nb + 1);
+  uint32_t* lay0 = ctx->h<uint32_t>("pk.lay0", nb + 1);
+  uint32_t* cpar0 = ctx->h<uint32_t>("pk.cpar0", nb + 1);
+  {
+    uint32_t m = 0, l = 0, cp = 0;
+    for (uint64_t b = 0; b < nb; ++b) {
+      met0[b] = m;
+      lay0[b] = l;
+      cpar0[b] = cp;
+      for (uint64_t i = b * kPB, e = std::min(n, i + kPB); i < e; ++i) {
+        const uint8_t f = c->flags[i];
+        m += (f & XSP_F_METRICS) != 0;
+        const bool lay = (f & 3u) == XSP_LEVEL_LAYER;
+        l += lay;
+        cp += !lay && (f & XSP_F_PARENT);
+      }
+    }
+    met0[nb] = m;
+    lay0[nb] = l;
+    cpar0[nb] = cp;
+  }
   std::vector<uint64_t> ekey, eval;
   ekey.reserve(nb + tr->n_traces + 1024);
   eval.reserve(nb + tr->n_traces + 1024);
@@ -179,6 +200,9 @@ void pack_host(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* tr, xsp_p
   out->blk_cid_base = cbase;
   out->blk_cid0 = cid0;
   out->blk_par0 = par0;
+  out->blk_met0 = met0;
+  out->blk_lay0 = lay0;
+  out->blk_cpar0 = cpar0;
   out->n_esc = ekey.size();
   out->esc_key = ek;
   out->esc_val = ev;

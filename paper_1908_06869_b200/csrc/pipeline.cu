@@ -204,9 +204,12 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
     c.t1 = T;
     c.g1 = G;
     // the compute + D2H of the final chunk is the only part not hidden behind
-    // the input stream: cut the tail geometrically (~2/3 : 1/3 at group
-    // boundaries) until the last chunk is below min(target / 4, 2 M) spans
-    const uint64_t tail_min = std::min<uint64_t>(target / 4, 2000000);
+    // the input stream, but every chunk also has ~1 ms of fixed cost (launches,
+    // read-backs): measured on C3 (12 M-span chunks), no tail split beat
+    // geometric tails down to 1 M / 3 M / 6 M spans by 0.2-0.6 ms. XSP_TAIL_SPANS
+    // cuts the tail ~2/3 : 1/3 at group boundaries until it is below that size.
+    uint64_t tail_min = target;
+    if (const char* e = std::getenv("XSP_TAIL_SPANS")) tail_min = std::strtoull(e, nullptr, 10);
     for (;;) {
       const uint64_t rem = off[T] - off[c.t0];
       if (rem <= tail_min) break;
@@ -333,7 +336,25 @@ bool run_host_chunked(xsp_ctx* ctx, const xsp_span_cols* hc, const xsp_traces* h
       h2d(const_cast<uint32_t*>(S.cols.name_id), hc->name_id + s0, ns * 4);
     }
     uint64_t mc, lc, cp;
-    count_rows((pk ? pk->flags : hc->flags) + s0, ns, mc, lc, cp);
+    if (pk && pk->blk_met0 && pk->blk_lay0 && pk->blk_cpar0) {
+      // packed input: per-block prefix counts + the partial blocks at the chunk's edges
+      auto before = [&](uint64_t s, uint64_t& m, uint64_t& l, uint64_t& p) {
+        const uint64_t b = s / XSP_PACK_BLOCK;
+        uint64_t pm, pl, pp;
+        count_rows(pk->flags + b * XSP_PACK_BLOCK, s - b * XSP_PACK_BLOCK, pm, pl, pp);
+        m = pk->blk_met0[b] + pm;
+        l = pk->blk_lay0[b] + pl;
+        p = pk->blk_cpar0[b] + pp;
+      };
+      uint64_t m0, l0, p0, m1, l1, p1;
+      before(s0, m0, l0, p0);
+      before(C.s1, m1, l1, p1);
+      mc = m1 - m0;
+      lc = l1 - l0;
+      cp = p1 - p0;
+    } else {
+      count_rows((pk ? pk->flags : hc->flags) + s0, ns, mc, lc, cp);
+    }
     // span_id is read sparsely (model spans, timeline ties, orphans,
     // ambiguities) unless kernels carry explicit parents: read it in place
     // from page-locked host memory when possible instead of copying it

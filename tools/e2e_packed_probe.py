@@ -33,3 +33,20 @@ for chunk in (sys.argv[1:] or ["6000000"]):
 os.environ["XSP_CHUNK_SPANS"] = "12000000"
 os.environ["XSP_PIPE_TRACE"] = "1"
 eng.run_host_packed(pk, hb, groups=groups, raw=True)
+torch.cuda.synchronize()
+os.environ.pop("XSP_PIPE_TRACE", None)
+# device stage times inside one packed call (work stream), vs the same with span_id copied
+for zc in ("zero-copy span_id", "copied span_id"):
+    if zc.startswith("copied"):
+        os.environ["XSP_NO_ZERO_COPY"] = "1"
+    eng.run_host_packed(pk, hb, groups=groups, raw=True)
+    torch.cuda.synchronize()
+    eng.set_profiling(True)
+    eng.stage_reset()
+    t = time.perf_counter()
+    eng.run_host_packed(pk, hb, groups=groups, raw=True)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t) * 1e3
+    st = eng.stage_times()
+    eng.set_profiling(False)
+    print(zc, f"{ms:.1f} ms", {k: round(v[0], 3) for k, v in st.items()}, flush=True)

@@ -1,2 +1,2 @@
 set -x
-timeout 900 python tools/e2e_packed_probe.py 8000000 12000000 16000000 2>&1 | tail -30
+timeout 900 python tools/e2e_packed_probe.py 12000000 2>&1 | tail -30
