@@ -646,6 +646,11 @@ __global__ void k_final_tables(Final f, const uint32_t* __restrict__ mpos, const
 // a string hashing to it goes to the host interner); each slot keeps one member
 // as its representative, every other member is byte-compared with it.
 constexpr uint64_t kHashEmpty = ~0ull;
+__global__ void k_mask_hash(uint64_t* __restrict__ h, uint64_t n, uint64_t mask) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) h[i] &= mask;
+}
+
 __global__ void k_hash_insert(const uint64_t* __restrict__ hash, const uint8_t* __restrict__ use, uint64_t n,
                               uint64_t mask, unsigned long long* __restrict__ tkey, uint32_t* __restrict__ trep,
                               uint32_t* __restrict__ slot_of, uint32_t* __restrict__ bad) {
@@ -879,6 +884,11 @@ bool intern(xsp_ctx* ctx, const std::string& tag, const char* dtext, const char*
   tblob.clear();
   toff.assign(1, 0);
   if (n == 0) return true;
+  if (const char* e = std::getenv("XSP_INGEST_HASH_BITS")) {  // test hook: force hash collisions
+    const int bits = std::atoi(e);
+    if (bits > 0 && bits < 64)
+      k_mask_hash<<<blocks(n), 256, 0, st>>>(const_cast<uint64_t*>(hash), n, (1ull << bits) - 1);
+  }
   uint64_t cap = 1024;
   while (cap < 2 * n) cap <<= 1;
   auto* tkey = ctx->d<unsigned long long>(tag + ".tk", cap);

@@ -142,6 +142,13 @@ def test_packed_tables_wire_format(engine, monkeypatch):
     for bw, raw, cnt in ((pk.dbegin_bw, pk.dbegin, n), (pk.dur_bw, pk.dur, n), (pk.dcid_bw, pk.dcid, nc)):
         dec = (_bw_decode(bw, cnt) - np.uint64(1)).astype(np.uint32)
         assert np.array_equal(dec, np.ctypeslib.as_array(raw, shape=(cnt,))), cnt
+    # per-block prefix counts of metric rows, layer rows, non-layer explicit parents
+    nb = int(pk.n_blocks)
+    f = b.flags
+    lay = (f & 3) == 1
+    for arr, pred in ((pk.blk_met0, (f & 0x40) != 0), (pk.blk_lay0, lay), (pk.blk_cpar0, ~lay & ((f & 0x10) != 0))):
+        want = np.concatenate([[0], np.cumsum(pred)])[np.minimum(np.arange(nb + 1) * 256, n)]
+        assert np.array_equal(np.ctypeslib.as_array(arr, shape=(nb + 1,)), want.astype(np.uint32))
     npar = int(pk.n_parent)
     assert pk.parent_bw.base and np.array_equal(_bw_decode(pk.parent_bw, npar),
                                                 np.ctypeslib.as_array(pk.parent, shape=(npar,)))

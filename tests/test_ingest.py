@@ -131,3 +131,18 @@ def test_gpu_ingest_defers_to_host(engine, has_ref, what):
     streams[1] = _mutate(streams[1], what)
     got, bad = engine.ingest_jsonl(streams)
     assert got is None and bad == 1, what
+
+
+@pytest.mark.gpu
+def test_gpu_ingest_hash_collision_goes_to_host(engine, has_ref, monkeypatch):
+    """Distinct strings with equal hashes (forced by XSP_INGEST_HASH_BITS=3) are
+    caught by the byte comparison against each slot's representative: the call
+    reports XSP_INGEST_HOST instead of merging two names; with full hashes the
+    same streams ingest on the GPU."""
+    streams = synth_streams(1, 2)
+    monkeypatch.setenv("XSP_INGEST_HASH_BITS", "3")
+    got, bad = engine.ingest_jsonl(streams)
+    assert got is None and bad == 0
+    monkeypatch.delenv("XSP_INGEST_HASH_BITS")
+    got, bad = engine.ingest_jsonl(streams)
+    assert bad == -1
