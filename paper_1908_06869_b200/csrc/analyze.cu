@@ -388,10 +388,11 @@ __global__ void __launch_bounds__(256) k_kernels_r1(LayerArgs a, uint32_t total_
 
 // a11-a14 row of layer q (group-local index li, correlation layer gl0) from its
 // Accumulator (analysis.cpp:173-211, 458-494) and top-k
+template <typename TopIdx>
 __device__ __forceinline__ void layer_row_out(const LayerArgs& a, uint32_t q, uint32_t li, uint32_t gl0,
                                               double layer_lat, uint32_t nk, double acc_lat, double acc_occw,
                                               uint64_t acc_f, uint64_t acc_r, uint64_t acc_w,
-                                              const uint32_t* top_idx, uint32_t ntop) {
+                                              const TopIdx& top_idx, uint32_t ntop) {
   const uint32_t K = a.top_k;
   if (a.l_occw) a.l_occw[q] = acc_occw;
   const uint32_t lo_out = q;
@@ -426,6 +427,30 @@ __device__ __forceinline__ void layer_row_out(const LayerArgs& a, uint32_t q, ui
   for (uint32_t s = 0; s < K; ++s) a.l_topk[(uint64_t)lo_out * K + s] = s < ntop ? top_idx[s] : kNone;
 }
 
+// top-k (K <= 4) in registers: the same insertion as topk_push (latency desc,
+// ties in arrival order) without a dynamically indexed local array
+struct TopK4 {
+  double l0 = 0, l1 = 0, l2 = 0, l3 = 0;
+  uint32_t i0 = 0, i1 = 0, i2 = 0, i3 = 0, n = 0;
+  __device__ __forceinline__ void push(uint32_t K, double klat, uint32_t ord) {
+    if (!K) return;
+    const uint32_t pos = (n > 0 && l0 >= klat) + (n > 1 && l1 >= klat) + (n > 2 && l2 >= klat) +
+                         (n > 3 && l3 >= klat);
+    if (pos >= K) return;
+    if (pos <= 2 && K > 3) { l3 = l2; i3 = i2; }
+    if (pos <= 1 && K > 2) { l2 = l1; i2 = i1; }
+    if (pos == 0 && K > 1) { l1 = l0; i1 = i0; }
+    if (pos == 0) { l0 = klat; i0 = ord; }
+    else if (pos == 1) { l1 = klat; i1 = ord; }
+    else if (pos == 2) { l2 = klat; i2 = ord; }
+    else { l3 = klat; i3 = ord; }
+    if (n < K) ++n;
+  }
+  __device__ __forceinline__ uint32_t operator[](uint32_t s) const {
+    return s == 0 ? i0 : s == 1 ? i1 : s == 2 ? i2 : i3;
+  }
+};
+
 // top-k insertion: latency desc, ordinal asc
 __device__ __forceinline__ void topk_push(uint32_t K, double klat, uint32_t ord, uint32_t* top_idx, double* top_lat,
                                           uint32_t& ntop) {
@@ -449,7 +474,10 @@ __device__ __forceinline__ void topk_push(uint32_t K, double klat, uint32_t ord,
 // kOneRun: every group has one run (a long single trace), so the layer latency
 // is its only sample and the trimmed-mean code is not instantiated.
 template <bool kOneRun>
-__global__ void __launch_bounds__(256, kOneRun ? 4 : 3) k_layers(LayerArgs a) {
+#ifndef XSP_LAYERS_R1_MINB
+#define XSP_LAYERS_R1_MINB 4
+#endif
+__global__ void __launch_bounds__(256, kOneRun ? XSP_LAYERS_R1_MINB : 3) k_layers(LayerArgs a) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= a.total_layers) return;
   const uint32_t g = group_of(a.gl_off, a.G, q);
@@ -469,28 +497,30 @@ __global__ void __launch_bounds__(256, kOneRun ? 4 : 3) k_layers(LayerArgs a) {
   double acc_lat = 0.0, acc_occw = 0.0;
   uint64_t acc_f = 0, acc_r = 0, acc_w = 0;
   const uint32_t K = a.top_k;
-  uint32_t top_idx[8];
-  double top_lat[8];
-  uint32_t ntop = 0;
-  for (uint32_t x = kb; x < ke; ++x) {
-    double klat, kocc;
-    uint64_t f, rd, wr;
-    {
-      klat = a.k_lat[x];
-      kocc = a.k_occ[x];
-      f = a.k_flops[x];
-      rd = a.k_read[x];
-      wr = a.k_write[x];
+  auto fold = [&](auto&& push) {
+    for (uint32_t x = kb; x < ke; ++x) {
+      const double klat = a.k_lat[x], kocc = a.k_occ[x];
+      const uint64_t f = a.k_flops[x], rd = a.k_read[x], wr = a.k_write[x];
+      a.k_layer[x] = li;
+      acc_lat = __dadd_rn(acc_lat, klat);
+      acc_f += f;
+      acc_r += rd;
+      acc_w += wr;
+      acc_occw = __dadd_rn(acc_occw, __dmul_rn(kocc, klat));
+      push(klat, x - a.gk_off[g]);
     }
-    a.k_layer[x] = li;
-    acc_lat = __dadd_rn(acc_lat, klat);
-    acc_f += f;
-    acc_r += rd;
-    acc_w += wr;
-    acc_occw = __dadd_rn(acc_occw, __dmul_rn(kocc, klat));
-    topk_push(K, klat, x - a.gk_off[g], top_idx, top_lat, ntop);
+  };
+  if (K <= 4) {  // the usual top-3: registers only
+    TopK4 t;
+    fold([&](double l, uint32_t o) { t.push(K, l, o); });
+    layer_row_out(a, q, li, gl0, layer_lat, ke - kb, acc_lat, acc_occw, acc_f, acc_r, acc_w, t, t.n);
+  } else {
+    uint32_t top_idx[8];
+    double top_lat[8];
+    uint32_t ntop = 0;
+    fold([&](double l, uint32_t o) { topk_push(K, l, o, top_idx, top_lat, ntop); });
+    layer_row_out(a, q, li, gl0, layer_lat, ke - kb, acc_lat, acc_occw, acc_f, acc_r, acc_w, top_idx, ntop);
   }
-  layer_row_out(a, q, li, gl0, layer_lat, ke - kb, acc_lat, acc_occw, acc_f, acc_r, acc_w, top_idx, ntop);
 }
 
 struct ModelArgs {
