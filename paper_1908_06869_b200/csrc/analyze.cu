@@ -899,6 +899,17 @@ struct NameFastArgs {
 constexpr uint32_t kNameSmemCap = 8192;
 constexpr size_t kNameSmem = kNameSmemCap * (1 + 2 + 2);
 
+// Raw mode's per-warp accumulators (dynamic shared memory; raw launches ask for
+// just this much, so more CTAs fit an SM than with the kNameSmem scratch).
+struct RawAcc {
+  double lat[NAME_WARPS][NCAP], occw[NAME_WARPS][NCAP];
+  unsigned long long f[NAME_WARPS][NCAP], r[NAME_WARPS][NCAP], w[NAME_WARPS][NCAP];
+  uint32_t cnt[NAME_WARPS][NCAP];
+  double st_l[NAME_WARPS][32], st_o[NAME_WARPS][32];
+  unsigned long long st_f[NAME_WARPS][32], st_r[NAME_WARPS][32], st_w[NAME_WARPS][32];
+};
+constexpr size_t kNameRawSmem = sizeof(RawAcc);
+
 __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) {
   extern __shared__ __align__(16) unsigned char nm_dyn[];
   uint8_t* s_slot = nm_dyn;
@@ -939,13 +950,6 @@ __global__ void __launch_bounds__(NAME_WARPS * 32) k_names_fast(NameFastArgs a) 
     // loads. Per 32 kernels, each name's leader lane adds its peers' values in
     // lane order into the warp's table; the four warp tables are then added in
     // warp order. Deterministic, and no gathers through a name permutation.
-    struct RawAcc {
-      double lat[NAME_WARPS][NCAP], occw[NAME_WARPS][NCAP];
-      unsigned long long f[NAME_WARPS][NCAP], r[NAME_WARPS][NCAP], w[NAME_WARPS][NCAP];
-      uint32_t cnt[NAME_WARPS][NCAP];
-      double st_l[NAME_WARPS][32], st_o[NAME_WARPS][32];
-      unsigned long long st_f[NAME_WARPS][32], st_r[NAME_WARPS][32], st_w[NAME_WARPS][32];
-    };
     static_assert(sizeof(RawAcc) <= kNameSmem, "raw accumulators fit the scratch");
     RawAcc& R = *reinterpret_cast<RawAcc*>(nm_dyn);
     for (uint32_t s = lane; s < NCAP; s += 32) {
@@ -2138,7 +2142,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       tc.s_flops = ctx->d<uint64_t>("a.yc_sum", ccap);
       tc.s_read = ctx->d<uint64_t>("a.yc_r", ccap);
       tc.s_write = ctx->d<uint64_t>("a.yc_w", ccap);
-      k_names_fast<<<nlc, NAME_WARPS * 32, kNameSmem, st>>>(tc);
+      k_names_fast<<<nlc, NAME_WARPS * 32, kNameRawSmem, st>>>(tc);
       NameBigArgs yb;
       yb.G = G;
       yb.gkc_off = d_glc_rel;
@@ -2262,7 +2266,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       nc.s_flops = ctx->d<uint64_t>("a.c_f", ccap);
       nc.s_read = ctx->d<uint64_t>("a.c_r", ccap);
       nc.s_write = ctx->d<uint64_t>("a.c_w", ccap);
-      k_names_fast<<<nkc, NAME_WARPS * 32, kNameSmem, sn>>>(nc);
+      k_names_fast<<<nkc, NAME_WARPS * 32, kNameRawSmem, sn>>>(nc);
       NameBigArgs nb;
       nb.G = G;
       nb.gkc_off = d_gkc;
