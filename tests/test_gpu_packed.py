@@ -176,3 +176,13 @@ def test_packed_tables_off(engine, monkeypatch, chunk):
     assert not pk.name_bw.width and not pk.flops_bw.width and pk.occ_dict_n == 0 and not pk.dbegin_bw.width
     h_raw = run_both(engine, b, (gf, gr, gb), chunk, monkeypatch)[1]
     assert h_coded < h_raw, (h_coded, h_raw)
+
+
+@pytest.mark.parametrize("model", ["minimal", "overlap", "async-straggler"])
+def test_packed_small_reference_bundles(engine, monkeypatch, model):
+    """Tiny bundles of the reference's generator models (one block or less,
+    few or no metric rows) through both packed paths."""
+    from oracle import ref
+    b = ref.Generator().emit(model).batch()
+    T = b.n_traces
+    run_both(engine, b, (np.arange(T), np.ones(T), b.trace_batch), 0, monkeypatch)
