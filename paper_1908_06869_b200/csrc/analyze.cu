@@ -1865,20 +1865,23 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
     d_pl = d_pk_off + G + 1;
     d_pl_off = d_pl + 2ull * npl;
   }
-  // a long group's chunk tables: partial folds, then the ordered fold + ranking
+  // a long group's chunk tables: partial folds (levels of kNamePart tables while
+  // a group has more than kNamePart of them), then the ordered fold + ranking
   auto fold_big = [&](NameBigArgs nb, const uint32_t* d_rng, const uint32_t* d_poff, uint32_t np,
-                      const std::string& tag, cudaStream_t st) {
-    if (np) {
+                      const std::vector<uint32_t>& h_poff, const std::string& tag, cudaStream_t st) {
+    std::vector<uint32_t> poff = h_poff;  // group -> [first, last) table of the current level
+    for (int level = 0; np; ++level) {
+      const std::string lt = tag + (level ? std::to_string(level) : std::string());
       const uint64_t cap = (uint64_t)np * NCAP;
       NamePartOut po;
-      po.count = ctx->d<uint32_t>(tag + ".count", np);
-      po.name = ctx->d<uint32_t>(tag + ".name", cap);
-      po.cnt = ctx->d<uint64_t>(tag + ".cnt", cap);
-      po.lat = ctx->d<double>(tag + ".lat", cap);
-      po.occw = ctx->d<double>(tag + ".occw", cap);
-      po.f = ctx->d<uint64_t>(tag + ".f", cap);
-      po.r = ctx->d<uint64_t>(tag + ".r", cap);
-      po.w = ctx->d<uint64_t>(tag + ".w", cap);
+      po.count = ctx->d<uint32_t>(lt + ".count", np);
+      po.name = ctx->d<uint32_t>(lt + ".name", cap);
+      po.cnt = ctx->d<uint64_t>(lt + ".cnt", cap);
+      po.lat = ctx->d<double>(lt + ".lat", cap);
+      po.occw = ctx->d<double>(lt + ".occw", cap);
+      po.f = ctx->d<uint64_t>(lt + ".f", cap);
+      po.r = ctx->d<uint64_t>(lt + ".r", cap);
+      po.w = ctx->d<uint64_t>(lt + ".w", cap);
       k_names_partial<<<np, 32, 0, st>>>(nb, d_rng, d_rng + np, po);
       ++ctx->launches;
       nb.gkc_off = d_poff;
@@ -1890,6 +1893,29 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       nb.c_f = po.f;
       nb.c_r = po.r;
       nb.c_w = po.w;
+      // next level: kNamePart consecutive partial tables of one group each
+      uint32_t widest = 0;
+      for (uint32_t g = 0; g < G; ++g) widest = std::max(widest, poff[g + 1] - poff[g]);
+      if (widest <= kNamePart) break;
+      std::vector<uint32_t> rng, noff(G + 1, 0);
+      for (uint32_t g = 0; g < G; ++g) {
+        noff[g] = (uint32_t)(rng.size() / 2);
+        for (uint32_t q = poff[g]; q < poff[g + 1]; q += kNamePart)
+          rng.insert(rng.end(), {q, std::min(q + kNamePart, poff[g + 1])});
+      }
+      np = (uint32_t)(rng.size() / 2);
+      noff[G] = np;
+      uint32_t* h = ctx->h<uint32_t>(lt + ".lvl_h", 2ull * np + G + 1);
+      for (uint32_t q = 0; q < np; ++q) {
+        h[q] = rng[2 * q];
+        h[np + q] = rng[2 * q + 1];
+      }
+      std::memcpy(h + 2ull * np, noff.data(), (G + 1) * 4ull);
+      uint32_t* d = ctx->d<uint32_t>(lt + ".lvl", 2ull * np + G + 1);
+      xfer_small(d, h, (2ull * np + G + 1) * 4, st);
+      d_rng = d;
+      d_poff = d + 2ull * np;
+      poff.swap(noff);
     }
     k_names_big<<<G, 32, 0, st>>>(nb);
     ++ctx->launches;
@@ -2171,7 +2197,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       yb.s_ai = ty.s_ai;
       yb.s_tput = ty.s_tput;
       yb.s_bound = ty.s_bound;
-      fold_big(yb, d_pl, d_pl_off, npl, "a.yp", st);
+      fold_big(yb, d_pl, d_pl_off, npl, pl_off, "a.yp", st);
       ++ctx->launches;
     }
     exclusive_scan<uint32_t, uint32_t>(ty.g_count, out->group_type_off, G, ctx->d<uint32_t>("a.scan_y", scan_scratch_elems(G + 16)), out->group_type_off + G, st,
@@ -2295,7 +2321,7 @@ void run_analyze(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_corr_out* corr,
       nb.s_ai = nf.s_ai;
       nb.s_tput = nf.s_tput;
       nb.s_bound = nf.s_bound;
-      fold_big(nb, d_pk, d_pk_off, npk, "a.np", sn);
+      fold_big(nb, d_pk, d_pk_off, npk, pk_off, "a.np", sn);
       ++ctx->launches;
     }
     exclusive_scan<uint32_t, uint32_t>(nf.g_count, out->group_name_off, G, scan_tmp, out->group_name_off + G, sn,

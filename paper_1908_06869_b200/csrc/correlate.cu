@@ -108,21 +108,11 @@ __global__ void k_trace_prep(const uint8_t* __restrict__ flags, const uint64_t* 
                              const uint64_t* __restrict__ off, uint32_t T,
                              uint32_t* __restrict__ model_row, uint64_t* __restrict__ mb,
                              uint64_t* __restrict__ me, uint64_t* __restrict__ msid,
-                             unsigned long long* __restrict__ err_key, uint64_t n, uint32_t tile_spans,
-                             uint32_t* __restrict__ tile_lo, uint32_t* __restrict__ tile_hi) {
+                             unsigned long long* __restrict__ err_key) {
   const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
   if (t >= T) return;
   const uint64_t lo = off[t], hi = off[t + 1];
-  if (lo < hi) {
-    // pass-1 tiles whose first / last span lies in this trace (trace_of semantics:
-    // the containing non-empty trace)
-    for (uint64_t b = (lo + tile_spans - 1) / tile_spans + lane; b * tile_spans < hi; b += 32) tile_lo[b] = t;
-    for (uint64_t b = lo / tile_spans + lane; b * tile_spans < hi; b += 32) {
-      const uint64_t last = min((b + 1) * tile_spans, n) - 1;
-      if (last >= lo && last < hi) tile_hi[b] = t;
-    }
-  }
   uint64_t found = ~0ull;
   for (uint64_t base = lo; base < hi; base += 32) {
     uint64_t i = base + lane;
@@ -147,6 +137,28 @@ __global__ void k_trace_prep(const uint8_t* __restrict__ flags, const uint64_t* 
       msid[t] = 0;
     }
   }
+}
+
+// Pass-1 tiles: the (non-empty) trace holding each tile's first / last span, by
+// binary search over the trace offsets — one thread per tile, so a long trace
+// costs no serial walk over its tiles.
+__global__ void k_tile_traces(const uint64_t* __restrict__ off, uint32_t T, uint64_t n, uint32_t tile_spans,
+                              uint32_t ntiles, uint32_t* __restrict__ tile_lo, uint32_t* __restrict__ tile_hi) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= ntiles) return;
+  // the last trace t < T with off[t] <= i (empty traces share their offset with
+  // the next trace, so the last one is the non-empty trace that holds i)
+  auto trace_at = [&](uint64_t i) {
+    uint32_t lo = 0, hi = T;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(off + mid) <= i) lo = mid; else hi = mid;
+    }
+    return lo;
+  };
+  const uint64_t first = (uint64_t)b * tile_spans;
+  tile_lo[b] = trace_at(first);
+  tile_hi[b] = trace_at(min(first + tile_spans, n) - 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -259,7 +271,7 @@ struct P1Args {
   const uint64_t* mb;
   const uint64_t* me;
   const uint64_t* msid;
-  const uint32_t* tile_lo;  // trace of each tile's first span (k_trace_prep)
+  const uint32_t* tile_lo;  // trace of each tile's first span (k_tile_traces)
   const uint32_t* tile_hi;  // trace of each tile's last span
   uint32_t ntiles;
   Full* tile_agg;           // [ntiles] (k_p1_reduce)
@@ -2218,9 +2230,12 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     ctx->stage_begin("trace_prep", st);
     unsigned blocks = ceil_div((uint64_t)T * 32, 256);
     k_trace_prep<<<blocks, 256, 0, st>>>(c->flags, c->begin_ns, c->end_ns, c->span_id, off, T, model_row, mb, me,
-                                         msid, err_key, n, (uint32_t)P1_TILE, tile_lo, tile_hi);
+                                         msid, err_key);
+    if (ntiles)
+      k_tile_traces<<<ceil_div((uint64_t)ntiles, 256), 256, 0, st>>>(off, T, n, (uint32_t)P1_TILE, ntiles, tile_lo,
+                                                                     tile_hi);
     ctx->stage_end("trace_prep", st);
-    ++ctx->launches;
+    ctx->launches += 1 + (ntiles != 0);
   }
 
   // ---- pass 1
