@@ -1739,6 +1739,7 @@ struct JoinArgs {
   uint32_t* ex_slot;
   uint32_t* kl_slot;
   uint32_t* t_dup;       // bit0 exec dup, bit1 launch dup
+  uint32_t* any_dup;     // some trace has a duplicate (zeroed per call)
   const uint32_t* t_dense;  // dense direct-address traces (k_region_size)
 };
 
@@ -1781,33 +1782,42 @@ __global__ void k_join_insert(JoinArgs a) {
   const uint32_t s = (uint32_t)(base + h);
   if (is_ex) {
     a.ex_slot[it] = s;
-    if (atomicMin(a.sl_exec + s, it) != kNone) atomicOr(a.t_dup + t, 1u);
+    if (atomicMin(a.sl_exec + s, it) != kNone) {
+      atomicOr(a.t_dup + t, 1u);
+      *a.any_dup = 1;
+    }
   } else {
     uint32_t k = it - a.n_ex;
     a.kl_slot[k] = s;
-    if (atomicMin(a.sl_launch + s, k) != kNone) atomicOr(a.t_dup + t, 2u);
+    if (atomicMin(a.sl_launch + s, k) != kNone) {
+      atomicOr(a.t_dup + t, 2u);
+      *a.any_dup = 1;
+    }
   }
 }
 
 // Exact duplicate report: the first item in timeline order whose cid was seen
-// before, and that earlier (first) item (correlator.cpp:296-316).
+// before, and that earlier (first) item (correlator.cpp:296-316). Grid-stride;
+// a batch without duplicates (the common case) exits on one flag read.
 __global__ void k_join_dups(JoinArgs a, unsigned long long* __restrict__ dup_ex,
                             unsigned long long* __restrict__ dup_kl) {
-  uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
-  if (it >= a.n_ex + a.n_kl) return;
-  if (it < a.n_ex) {
-    uint32_t t = trace_of32(a.t_ex_off, a.T, it);
-    if (!(a.t_dup[t] & 1u)) return;
-    uint32_t first = a.sl_exec[a.ex_slot[it]];
-    if (first != it) atomicMin(dup_ex + t, ((unsigned long long)it << 32) | first);
-  } else {
-    uint32_t k = it - a.n_ex;
-    uint32_t t = trace_of32(a.t_kl_off, a.T, k);
-    if (!(a.t_dup[t] & 2u)) return;
-    const uint8_t f = a.flags[a.kl[k].row];
-    if (!is_kernel_launch(f) || !(f & XSP_F_CID)) return;
-    uint32_t first = a.sl_launch[a.kl_slot[k]];
-    if (first != k) atomicMin(dup_kl + t, ((unsigned long long)k << 32) | first);
+  if (!*((volatile uint32_t*)a.any_dup)) return;
+  const uint32_t n = a.n_ex + a.n_kl;
+  for (uint32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < n; it += gridDim.x * blockDim.x) {
+    if (it < a.n_ex) {
+      uint32_t t = trace_of32(a.t_ex_off, a.T, it);
+      if (!(a.t_dup[t] & 1u)) continue;
+      uint32_t first = a.sl_exec[a.ex_slot[it]];
+      if (first != it) atomicMin(dup_ex + t, ((unsigned long long)it << 32) | first);
+    } else {
+      uint32_t k = it - a.n_ex;
+      uint32_t t = trace_of32(a.t_kl_off, a.T, k);
+      if (!(a.t_dup[t] & 2u)) continue;
+      const uint8_t f = a.flags[a.kl[k].row];
+      if (!is_kernel_launch(f) || !(f & XSP_F_CID)) continue;
+      uint32_t first = a.sl_launch[a.kl_slot[k]];
+      if (first != k) atomicMin(dup_kl + t, ((unsigned long long)k << 32) | first);
+    }
   }
 }
 
@@ -2638,8 +2648,12 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     XSP_CUDA(cudaMemsetAsync(j.sl_exec, 0xFF, nslots * 4, st));
     XSP_CUDA(cudaMemsetAsync(j.sl_launch, 0xFF, nslots * 4, st));
     XSP_CUDA(cudaMemsetAsync(j.t_dup, 0, T * 4ull, st));
+    j.any_dup = ctx->d<uint32_t>("c.any_dup", 1);
+    XSP_CUDA(cudaMemsetAsync(j.any_dup, 0, 4, st));
     launch(ctx, k_join_insert, (uint64_t)nex + nkl, st, j);
-    launch(ctx, k_join_dups, (uint64_t)nex + nkl, st, j, dup_ex, dup_kl);
+    k_join_dups<<<(unsigned)std::min<uint64_t>(ceil_div((uint64_t)nex + nkl, 256), 148u * 8u), 256, 0, st>>>(
+        j, dup_ex, dup_kl);
+    ++ctx->launches;
   } else {
     j.sl_exec = j.sl_launch = nullptr;
   }
