@@ -108,11 +108,21 @@ __global__ void k_trace_prep(const uint8_t* __restrict__ flags, const uint64_t* 
                              const uint64_t* __restrict__ off, uint32_t T,
                              uint32_t* __restrict__ model_row, uint64_t* __restrict__ mb,
                              uint64_t* __restrict__ me, uint64_t* __restrict__ msid,
-                             unsigned long long* __restrict__ err_key) {
+                             unsigned long long* __restrict__ err_key, uint64_t n, uint32_t tile_spans,
+                             uint32_t* __restrict__ tile_lo, uint32_t* __restrict__ tile_hi) {
   const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
   if (t >= T) return;
   const uint64_t lo = off[t], hi = off[t + 1];
+  if (tile_lo && lo < hi) {
+    // pass-1 tiles whose first / last span lies in this trace (trace_of semantics:
+    // the containing non-empty trace); batches of long traces use k_tile_traces
+    for (uint64_t b = (lo + tile_spans - 1) / tile_spans + lane; b * tile_spans < hi; b += 32) tile_lo[b] = t;
+    for (uint64_t b = lo / tile_spans + lane; b * tile_spans < hi; b += 32) {
+      const uint64_t last = min((b + 1) * tile_spans, n) - 1;
+      if (last >= lo && last < hi) tile_hi[b] = t;
+    }
+  }
   uint64_t found = ~0ull;
   for (uint64_t base = lo; base < hi; base += 32) {
     uint64_t i = base + lane;
@@ -271,7 +281,7 @@ struct P1Args {
   const uint64_t* mb;
   const uint64_t* me;
   const uint64_t* msid;
-  const uint32_t* tile_lo;  // trace of each tile's first span (k_tile_traces)
+  const uint32_t* tile_lo;  // trace of each tile's first span (k_trace_prep / k_tile_traces)
   const uint32_t* tile_hi;  // trace of each tile's last span
   uint32_t ntiles;
   Full* tile_agg;           // [ntiles] (k_p1_reduce)
@@ -2239,13 +2249,18 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
   if (T) {
     ctx->stage_begin("trace_prep", st);
     unsigned blocks = ceil_div((uint64_t)T * 32, 256);
+    // tile -> trace: per trace by its warp when traces are short on average (one
+    // launch), per tile by binary search when they are long (a trace's warp
+    // would walk all of its tiles serially)
+    const bool per_tile = ntiles && n / T > 64ull * P1_TILE;
     k_trace_prep<<<blocks, 256, 0, st>>>(c->flags, c->begin_ns, c->end_ns, c->span_id, off, T, model_row, mb, me,
-                                         msid, err_key);
-    if (ntiles)
+                                         msid, err_key, n, (uint32_t)P1_TILE, per_tile ? nullptr : tile_lo,
+                                         tile_hi);
+    if (per_tile)
       k_tile_traces<<<ceil_div((uint64_t)ntiles, 256), 256, 0, st>>>(off, T, n, (uint32_t)P1_TILE, ntiles, tile_lo,
                                                                      tile_hi);
     ctx->stage_end("trace_prep", st);
-    ctx->launches += 1 + (ntiles != 0);
+    ctx->launches += 1 + per_tile;
   }
 
   // ---- pass 1
