@@ -1912,14 +1912,16 @@ __global__ void k_compact_kernels(uint32_t n_kl, const uint32_t* __restrict__ ke
   const uint32_t par = kl[k].parent;
   key[j] = par;
   val[j] = k;
-}
-
-// tree order == timeline order unless explicit parents broke it
-__global__ void k_check_mono(const uint32_t* __restrict__ nk, const uint64_t* __restrict__ key,
-                             uint32_t* __restrict__ nonmono) {
-  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j == 0 || j >= *nk) return;
-  if (key[j] < key[j - 1]) *nonmono = 1;
+  // tree order == list order unless a kept entry's parent is below the previous
+  // kept entry's (key[j] < key[j - 1]). Only the first kept entry after a run of
+  // dropped ones walks it (e.g. the ambiguous launches of a concurrent layer
+  // group); a run longer than 4096 sets the flag conservatively (the stable
+  // sort is then a no-op)
+  if (j > 0) {
+    uint32_t q = k - 1;
+    for (int step = 0; !kept[q] && step < 4096; ++step) --q;
+    if (!kept[q] || kl[q].parent > par) *nonmono = 1;
+  }
 }
 
 __global__ void k_gather_kernels(uint32_t nk, const uint32_t* __restrict__ val, const KlEnt* __restrict__ kl,
@@ -2719,7 +2721,6 @@ void run_correlate_once(xsp_ctx* ctx, const xsp_span_cols* c, const xsp_traces* 
     kkey = ctx->d<uint64_t>("c.kkey", nkl + 1);
     kval = ctx->d<uint32_t>("c.kval", nkl + 1);
     launch(ctx, k_compact_kernels, nkl, st, nkl, fa.kept, kpos, a.kl, kkey, kval, counters + 3);
-    launch(ctx, k_check_mono, nkl, st, nk_d, kkey, counters + 3);
     xfer_small(htot, nk_d, 4, st);
     xfer_small(htot + 1, counters + 3, 4, st);
     XSP_CUDA(cudaStreamSynchronize(st));
